@@ -1,0 +1,489 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU oracle of the MatMul-free LM
+ * block forward pass (arxiv 2406.02528).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load or call this
+ * library.  It shares no code, header, table or constant generator with the
+ * CUDA path in paper_2406_02528_b200/ and never includes or links it.
+ *
+ * Citation keys: "P:n" = /root/reference/PAPER.md line n (section named
+ * beside it); "C<k>" = a reading listed in DESIGN.md section "Readings".
+ *
+ * Conventions:
+ *   - every float operation is one IEEE binary32 operation, round to nearest
+ *     even; this file is built with -O2 -ffp-contract=off, no fast-math, so
+ *     the compiler never fuses a*b+c except where fmaf() is written;
+ *   - round() in the paper ("round then clamp") is round half away
+ *     from zero (C3) == C99 roundf();
+ *   - sums of squares / absolute values accumulate in binary64 in index order
+ *     (C4) and are rounded once to binary32;
+ *   - exp is the canonical exp_c specified in DESIGN.md (C12), written out
+ *     below from that specification;
+ *   - bf16 storage points R0..R3 round to nearest even (C13).
+ *
+ * Loops run in the order the paper's equations are written; OpenMP is used
+ * only across independent rows / (sequence, channel) pairs, each of which is
+ * reduced sequentially, so results do not depend on the thread count.
+ *
+ * Parity status per function: all functions are pinned by tests in
+ * tests/test_oracle_pins.py except the composed end-to-end block values,
+ * which the paper never prints ("parity unpinned" for orc_block values;
+ * they are pinned only through their pinned parts and invariants).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_OK 0
+#define ORC_ERR_ARG 1
+#define ORC_ERR_DEGENERATE 2
+#define ORC_ERR_OVERFLOW 5
+
+/* ------------------------------------------------------------------------ */
+/* threading                                                                 */
+/* ------------------------------------------------------------------------ */
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+int orc_get_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+/* ------------------------------------------------------------------------ */
+/* scalar primitives                                                         */
+/* ------------------------------------------------------------------------ */
+
+/* bf16 storage rounding (C13): round a binary32 to the nearest bfloat16
+ * (ties to even) and return it widened back to binary32.  NaN passes. */
+float orc_bf16(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return x;
+  uint32_t lsb = (u >> 16) & 1u;
+  u += 0x7fffu + lsb;
+  u &= 0xffff0000u;
+  memcpy(&x, &u, 4);
+  return x;
+}
+
+/* "round then clamp" of Alg. 1; round half away from zero
+ * (C3) is exactly C99 roundf. */
+static float rha(float v) { return roundf(v); }
+
+/* Canonical exp_c (C12): range reduction
+ * x = k ln2 + r with k = rint(x log2e), Cody-Waite two-constant reduction
+ * with fmaf, degree-7 Taylor polynomial in Horner form with fmaf, then
+ * scaling by 2^k.  Constants are the binary32 values listed in DESIGN.md. */
+float orc_exp(float x) {
+  if (x != x) return x;
+  if (x >= 0x1.62e430p+6f) return INFINITY;   /* >= ln(FLT_MAX) */
+  if (x < -0x1.5d589ep+6f) return 0.0f;       /* <  ln(FLT_MIN) */
+  float k = rintf(x * 0x1.715476p+0f);         /* log2(e) */
+  float r = fmaf(-k, 0x1.62e400p-1f, x);       /* ln2_hi  */
+  r = fmaf(-k, 0x1.7f7d1cp-20f, r);            /* ln2_lo  */
+  float p = 0x1.a01a02p-13f;                   /* 1/5040 */
+  p = fmaf(p, r, 0x1.6c16c2p-10f);             /* 1/720  */
+  p = fmaf(p, r, 0x1.111112p-7f);              /* 1/120  */
+  p = fmaf(p, r, 0x1.555556p-5f);              /* 1/24   */
+  p = fmaf(p, r, 0x1.555556p-3f);              /* 1/6    */
+  p = fmaf(p, r, 0.5f);
+  p = fmaf(p, r, 1.0f);
+  p = fmaf(p, r, 1.0f);
+  int ki = (int)k;
+  if (ki > 127) { p = p * 2.0f; ki -= 1; }
+  return p * ldexpf(1.0f, ki);
+}
+
+/* logistic sigmoid sigma(x) = 1/(1+e^{-x}) */
+float orc_sigmoid(float x) { return 1.0f / (1.0f + orc_exp(-x)); }
+
+/* SiLU tau(x) = x * sigma(x) ("tau is the SiLU activation") */
+float orc_silu(float x) { return x * orc_sigmoid(x); }
+
+void orc_exp_arr(const float* x, float* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = orc_exp(x[i]);
+}
+void orc_sigmoid_arr(const float* x, float* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = orc_sigmoid(x[i]);
+}
+void orc_bf16_arr(const float* x, float* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = orc_bf16(x[i]);
+}
+
+/* ------------------------------------------------------------------------ */
+/* a1: weight_quant (Alg. 1), absmean ternarization                */
+/* ------------------------------------------------------------------------ */
+
+/* m = mean(|W|) over the whole matrix (one scale per matrix, C6), summed in
+ * binary64 in index order and rounded once to binary32 (C4).
+ * Returns ORC_ERR_DEGENERATE for an all-zero or non-finite W (C7). */
+int orc_absmean(const float* W, int64_t n, float* m_out) {
+  if (n <= 0) return ORC_ERR_ARG;
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!isfinite(W[i])) return ORC_ERR_DEGENERATE;
+    s += fabs((double)W[i]);
+  }
+  float m = (float)(s / (double)n);
+  if (!(m > 0.0f) || !isfinite(m)) return ORC_ERR_DEGENERATE;
+  *m_out = m;
+  return ORC_OK;
+}
+
+/* s = 1/mean|W|;  W~ = round(s W) clamped to [-1,1]   (the listing's
+ * "sX" is read as "sW", C6).  The dequantized weight is t * m ("* 1/s"). */
+void orc_ternarize(const float* W, int64_t n, float m, int8_t* t) {
+  float s = 1.0f / m;
+  for (int64_t i = 0; i < n; ++i) {
+    float v = rha(W[i] * s);
+    if (v > 1.0f) v = 1.0f;
+    if (v < -1.0f) v = -1.0f;
+    t[i] = (int8_t)v;
+  }
+}
+
+/* Zero fraction of a ternary matrix ("unstructured sparsity"). */
+double orc_zero_fraction(const int8_t* t, int64_t n) {
+  int64_t z = 0;
+  for (int64_t i = 0; i < n; ++i) z += (t[i] == 0);
+  return n > 0 ? (double)z / (double)n : 0.0;
+}
+
+/* Decoder of the GPU packing layout, written from its specification in
+ * DESIGN.md "Packed weight layout" (not from the CUDA code):
+ *   trit k of a row lives in word k/16, byte j = k%4, bit field f = (k%16)/4
+ *   at bits [8j+2f, 8j+2f+1]; the field holds e = t + 1 in {0,1,2}.
+ * Rows of fused groups are interleaved in groups of seg_rows:
+ *   packed row of (segment s, logical row r) =
+ *     (r / seg_rows) * (n_seg * seg_rows) + s * seg_rows + r % seg_rows.
+ * Returns ORC_ERR_ARG if a field holds the unused value 3. */
+int64_t orc_packed_row(int64_t s, int64_t r, int64_t n_seg, int64_t seg_rows) {
+  return (r / seg_rows) * (n_seg * seg_rows) + s * seg_rows + (r % seg_rows);
+}
+int orc_unpack_row(const uint32_t* codes_row, int k, int8_t* t) {
+  for (int kk = 0; kk < k; ++kk) {
+    uint32_t w = codes_row[kk / 16];
+    int j = kk % 4, f = (kk % 16) / 4;
+    uint32_t e = (w >> (8 * j + 2 * f)) & 3u;
+    if (e == 3u) return ORC_ERR_ARG;
+    t[kk] = (int8_t)((int)e - 1);
+  }
+  return ORC_OK;
+}
+/* Unpack segment s (n logical rows) of a packed group into t[n][k]. */
+int orc_unpack_segment(const uint32_t* codes, int64_t ldw, int n, int k, int n_seg, int s,
+                       int seg_rows, int8_t* t) {
+  for (int r = 0; r < n; ++r) {
+    int64_t pr = orc_packed_row(s, r, n_seg, seg_rows);
+    int rc = orc_unpack_row(codes + pr * ldw, k, t + (int64_t)r * k);
+    if (rc) return rc;
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a2: RMSNorm (Eq. 1, read as the mean form C1) and               */
+/*     activation_quant (Alg. 1, per token C2)                     */
+/* ------------------------------------------------------------------------ */
+
+/* RMSNorm(x; w, eps) = x / sqrt(eps + mean(x^2)) * w   (C1).
+ * r = 1/sqrt(mean(x^2) + eps) computed in binary64, rounded to binary32;
+ * y_j = (x_j * r) * w_j  in binary32.  gain == NULL means w = 1. */
+float orc_rmsnorm(const float* x, int K, const float* gain, float eps, float* y) {
+  double ss = 0.0;
+  for (int j = 0; j < K; ++j) ss += (double)x[j] * (double)x[j];
+  double ms = ss / (double)K;
+  float r = (float)(1.0 / sqrt(ms + (double)eps));
+  for (int j = 0; j < K; ++j) {
+    float v = x[j] * r;
+    if (gain) v = v * gain[j];
+    y[j] = v;
+  }
+  return r;
+}
+
+/* activation_quant: s = 127/max|y|, q = round(s y) clamped to
+ * [-128,127]; the dequantization factor is 1/s, carried as deq = max|y|/127.
+ * An all-zero row gives q = 0 and deq = 0 (C7). Returns max|y|. */
+float orc_act_quant(const float* y, int K, int8_t* q, float* deq) {
+  float a = 0.0f;
+  for (int j = 0; j < K; ++j) {
+    float v = fabsf(y[j]);
+    if (v > a) a = v;
+  }
+  if (a == 0.0f) {
+    for (int j = 0; j < K; ++j) q[j] = 0;
+    *deq = 0.0f;
+    return a;
+  }
+  float s = 127.0f / a;
+  for (int j = 0; j < K; ++j) {
+    float v = rha(y[j] * s);
+    if (v > 127.0f) v = 127.0f;
+    if (v < -128.0f) v = -128.0f;
+    q[j] = (int8_t)v;
+  }
+  *deq = a / 127.0f;
+  return a;
+}
+
+/* Fused norm + quant of M rows of X[M][K] (Alg. 1 rms_norm_fwd, P:325-334,
+ * with the C1 reading).  Outputs q[M][K], deq[M], inv_rms[M], absmax[M]. */
+int orc_quant_rows(const float* X, int M, int K, const float* gain, float eps, int8_t* q,
+                   float* deq, float* inv_rms, float* absmax) {
+  if (M < 0 || K <= 0) return ORC_ERR_ARG;
+  int bad = 0;
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < M; ++i) {
+    float* y = (float*)malloc(sizeof(float) * (size_t)K);
+    if (!y) { bad = 1; continue; }
+    float r = orc_rmsnorm(X + (int64_t)i * K, K, gain, eps, y);
+    float a = orc_act_quant(y, K, q + (int64_t)i * K, &deq[i]);
+    if (inv_rms) inv_rms[i] = r;
+    if (absmax) absmax[i] = a;
+    free(y);
+  }
+  return bad ? ORC_ERR_ARG : ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a3/a4: ternary accumulation, literally  sum_{W=+1} x - sum_{W=-1} x  */
+/* ------------------------------------------------------------------------ */
+int64_t orc_tern_dot(const int8_t* t, const int8_t* q, int K) {
+  int64_t plus = 0, minus = 0;
+  for (int j = 0; j < K; ++j) {
+    if (t[j] == 1) plus += q[j];
+    else if (t[j] == -1) minus += q[j];
+  }
+  return plus - minus;
+}
+
+/* acc[M][N] = q[M][K] (*) t[N][K]^T  (int32; errors if a sum leaves int32) */
+int orc_tern_matmul(const int8_t* q, int M, int K, const int8_t* t, int N, int32_t* acc) {
+  int bad = 0;
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < M; ++i)
+    for (int n = 0; n < N; ++n) {
+      int64_t a = orc_tern_dot(t + (int64_t)n * K, q + (int64_t)i * K, K);
+      if (a > INT32_MAX || a < INT32_MIN) bad = 1;
+      acc[(int64_t)i * N + n] = (int32_t)a;
+    }
+  return bad ? ORC_ERR_OVERFLOW : ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* BitLinear forward (Alg. 1 forward_pass):                        */
+/*   O = Y~ (*) W~ + b, Y~ = act_quant(RMSNorm(X)), dequantized by            */
+/*   (1/s_a) * mean|W|  ("* 1/s", "* 1/s").                        */
+/*   O_n = (float)acc_n * (deq * m)  [+ b_n]; in bf16 mode O is rounded to     */
+/*   bf16 (R1).                                                               */
+/* Optional taps: q_out[M][K], acc_out[M][N], deq_out[M].                      */
+/* ------------------------------------------------------------------------ */
+int orc_bitlinear(const float* X, int M, int K, const float* gain, float eps, const int8_t* t,
+                  int N, float m_w, const float* bias, int bf16, float* O, int8_t* q_out,
+                  int32_t* acc_out, float* deq_out) {
+  if (M < 0 || K <= 0 || N <= 0) return ORC_ERR_ARG;
+  int bad = 0;
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < M; ++i) {
+    float* y = (float*)malloc(sizeof(float) * (size_t)K);
+    int8_t* q = (int8_t*)malloc((size_t)K);
+    if (!y || !q) { bad = ORC_ERR_ARG; free(y); free(q); continue; }
+    float deq;
+    orc_rmsnorm(X + (int64_t)i * K, K, gain, eps, y);
+    orc_act_quant(y, K, q, &deq);
+    float sc = deq * m_w;
+    for (int n = 0; n < N; ++n) {
+      int64_t a = orc_tern_dot(t + (int64_t)n * K, q, K);
+      if (a > INT32_MAX || a < INT32_MIN) bad = ORC_ERR_OVERFLOW;
+      float o = (float)a * sc;
+      if (bias) o = o + bias[n];
+      if (bf16) o = orc_bf16(o);
+      O[(int64_t)i * N + n] = o;
+      if (acc_out) acc_out[(int64_t)i * N + n] = (int32_t)a;
+    }
+    if (q_out) memcpy(q_out + (int64_t)i * K, q, (size_t)K);
+    if (deq_out) deq_out[i] = deq;
+    free(y);
+    free(q);
+  }
+  return bad;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a6: MLGRU elementwise part:                                    */
+/*   f_t = sigma(fhat_t), c_t = tau(chat_t), h_t = f_t h_{t-1} + (1-f_t) c_t, */
+/*   o'_t = g_t * sigma(h_t)   (gate_mode 0)                           */
+/*   o'_t = g_t * h_t          (gate_mode 1, BASELINE config 0 literal, C8)   */
+/* Sequential over t per channel; h_0 = H (0 at prefill start).         */
+/* Arrays are [B][T][d]; H is [B][d] in/out.  bf16 mode rounds o' (R2).       */
+/* ------------------------------------------------------------------------ */
+
+/* one recurrence step, h' = f*h + (1-f)*c, each product / sum one binary32 op */
+static float scan_step(float f, float h, float c) {
+  float a = f * h;
+  float om = 1.0f - f;
+  float b = om * c;
+  return a + b;
+}
+
+/* Plain sequential scan of raw gates: h_t = f_t h_{t-1} + (1-f_t) c_t */
+void orc_scan_seq(const float* f, const float* c, int T, float h0, float* h_out) {
+  float h = h0;
+  for (int t = 0; t < T; ++t) {
+    h = scan_step(f[t], h, c[t]);
+    h_out[t] = h;
+  }
+}
+
+/* Self-check only (not the definition): chunked scan composing pairs
+ * (a_t, b_t) = (f_t, (1-f_t) c_t) with (a2,b2) o (a1,b1) = (a1 a2, a2 b1 + b2)
+ * (S:197).  Within a chunk the pairs are composed left to right; chunk
+ * aggregates are then applied to the carried state. */
+void orc_scan_chunked(const float* f, const float* c, int T, int chunk, float h0, float* h_out) {
+  if (chunk <= 0) chunk = T > 0 ? T : 1;
+  float h = h0;
+  for (int s = 0; s < T; s += chunk) {
+    int e = s + chunk < T ? s + chunk : T;
+    /* local prefix of the chunk from state 0 with running products */
+    float A = 1.0f, Bv = 0.0f;
+    for (int t = s; t < e; ++t) {
+      float a = f[t];
+      float b = (1.0f - f[t]) * c[t];
+      /* (a,b) o (A,Bv) */
+      A = A * a;
+      Bv = a * Bv + b;
+      h_out[t] = A * h + Bv;
+    }
+    h = h_out[e - 1];
+  }
+}
+
+int orc_mlgru_scan(const float* fhat, const float* chat, const float* ghat, int B, int T, int d,
+                   int gate_mode, int bf16, float* H, float* oprime) {
+  if (B < 0 || T < 0 || d <= 0) return ORC_ERR_ARG;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int b = 0; b < B; ++b)
+    for (int ch = 0; ch < d; ++ch) {
+      float h = H[(int64_t)b * d + ch];
+      for (int t = 0; t < T; ++t) {
+        int64_t i = ((int64_t)b * T + t) * d + ch;
+        float f = orc_sigmoid(fhat[i]);
+        float c = orc_silu(chat[i]);
+        h = scan_step(f, h, c);
+        float o = gate_mode == 0 ? ghat[i] * orc_sigmoid(h) : ghat[i] * h;
+        if (bf16) o = orc_bf16(o);
+        oprime[i] = o;
+      }
+      H[(int64_t)b * d + ch] = h;
+    }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* MLGRU token mixer, one call = B sequences of T tokens.         */
+/* f,c,g,o BitLinears each preceded by their RMSNorm; f,c,g share the */
+/* input and gain_x (C10).  Biases optional (C11).                            */
+/* Taps (optional, [B][T][d]): fhat, chat, ghat, oprime.                      */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  const int8_t *tf, *tc, *tg, *to;   /* [d][d] each, row = output channel */
+  float mf, mc, mg, mo;              /* mean|W| per matrix */
+  const float *bf, *bc, *bg, *bo;    /* [d] or NULL */
+  const float *gain_x, *gain_o;      /* [d] or NULL (= ones) */
+} orc_mlgru_w;
+
+typedef struct {
+  const int8_t *tg, *tu, *td;        /* [l][d], [l][d], [d][l] */
+  float mg, mu, md;
+  const float *gain_x, *gain_p;      /* [d], [l] or NULL */
+} orc_glu_w;
+
+int orc_mlgru(const orc_mlgru_w* w, const float* X, int B, int T, int d, float eps,
+              int gate_mode, int bf16, float* H, float* O, float* fhat, float* chat,
+              float* ghat, float* oprime) {
+  int64_t n = (int64_t)B * T * d;
+  int M = B * T;
+  float* F = fhat ? fhat : (float*)malloc(sizeof(float) * (size_t)(n ? n : 1));
+  float* C = chat ? chat : (float*)malloc(sizeof(float) * (size_t)(n ? n : 1));
+  float* G = ghat ? ghat : (float*)malloc(sizeof(float) * (size_t)(n ? n : 1));
+  float* P = oprime ? oprime : (float*)malloc(sizeof(float) * (size_t)(n ? n : 1));
+  int rc = 0;
+  rc |= orc_bitlinear(X, M, d, w->gain_x, eps, w->tf, d, w->mf, w->bf, bf16, F, 0, 0, 0);
+  rc |= orc_bitlinear(X, M, d, w->gain_x, eps, w->tc, d, w->mc, w->bc, bf16, C, 0, 0, 0);
+  rc |= orc_bitlinear(X, M, d, w->gain_x, eps, w->tg, d, w->mg, w->bg, bf16, G, 0, 0, 0);
+  rc |= orc_mlgru_scan(F, C, G, B, T, d, gate_mode, bf16, H, P);
+  rc |= orc_bitlinear(P, M, d, w->gain_o, eps, w->to, d, w->mo, w->bo, bf16, O, 0, 0, 0);
+  if (!fhat) free(F);
+  if (!chat) free(C);
+  if (!ghat) free(G);
+  if (!oprime) free(P);
+  return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a7: GLU channel mixer: g = x(*)W_g, u = x(*)W_u,               */
+/* p = tau(g) * u, d = p (*) W_d.  No biases.  bf16 rounds p (R2). */
+/* Taps (optional): ghat, uhat [M][l], p [M][l].                               */
+/* ------------------------------------------------------------------------ */
+int orc_glu(const orc_glu_w* w, const float* X, int M, int d, int l, float eps, int bf16,
+            float* O, float* ghat, float* uhat, float* p) {
+  int64_t n = (int64_t)M * l;
+  float* G = ghat ? ghat : (float*)malloc(sizeof(float) * (size_t)(n ? n : 1));
+  float* U = uhat ? uhat : (float*)malloc(sizeof(float) * (size_t)(n ? n : 1));
+  float* Pp = p ? p : (float*)malloc(sizeof(float) * (size_t)(n ? n : 1));
+  int rc = 0;
+  rc |= orc_bitlinear(X, M, d, w->gain_x, eps, w->tg, l, w->mg, 0, bf16, G, 0, 0, 0);
+  rc |= orc_bitlinear(X, M, d, w->gain_x, eps, w->tu, l, w->mu, 0, bf16, U, 0, 0, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    float v = orc_silu(G[i]) * U[i];
+    if (bf16) v = orc_bf16(v);
+    Pp[i] = v;
+  }
+  rc |= orc_bitlinear(Pp, M, l, w->gain_p, eps, w->td, d, w->md, 0, bf16, O, 0, 0, 0);
+  if (!ghat) free(G);
+  if (!uhat) free(U);
+  if (!p) free(Pp);
+  return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a8: block = token mixer + channel mixer with residuals (C9):        */
+/*   x1 = x + MLGRU(x);  y = x1 + GLU(x1)   (bf16 mode rounds x1 and y, R3)   */
+/* X, Y: [B][T][d]; H: [B][d] in/out.  Taps: x1 [B][T][d] (optional).          */
+/* ------------------------------------------------------------------------ */
+int orc_block(const orc_mlgru_w* mw, const orc_glu_w* gw, const float* X, int B, int T, int d,
+              int l, float eps, int gate_mode, int bf16, float* H, float* Y, float* x1_tap) {
+  int64_t n = (int64_t)B * T * d;
+  int M = B * T;
+  float* O = (float*)malloc(sizeof(float) * (size_t)(n ? n : 1));
+  float* X1 = x1_tap ? x1_tap : (float*)malloc(sizeof(float) * (size_t)(n ? n : 1));
+  float* D = (float*)malloc(sizeof(float) * (size_t)(n ? n : 1));
+  int rc = orc_mlgru(mw, X, B, T, d, eps, gate_mode, bf16, H, O, 0, 0, 0, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    float v = X[i] + O[i];
+    X1[i] = bf16 ? orc_bf16(v) : v;
+  }
+  rc |= orc_glu(gw, X1, M, d, l, eps, bf16, D, 0, 0, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    float v = X1[i] + D[i];
+    Y[i] = bf16 ? orc_bf16(v) : v;
+  }
+  free(O);
+  free(D);
+  if (!x1_tap) free(X1);
+  return rc;
+}
