@@ -1,0 +1,251 @@
+/*
+ * tern.h -- C ABI of libtern.so, a B200 (sm_100a) implementation of the
+ * forward pass of the MatMul-free LM block (arxiv 2406.02528).
+ *
+ * Citation keys: P:n = /root/reference/PAPER.md line n; C<k> = a reading of
+ * the paper listed in DESIGN.md "Readings"; DESIGN.md sections are named.
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ *  - All tensor pointers are DEVICE pointers (cudaMalloc / torch CUDA memory)
+ *    unless a comment says "host".  The caller owns every buffer, including
+ *    the workspace; the library never allocates device memory.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream), performs no host synchronisation (except tern_pack,
+ *    see below) and no allocation, and is therefore CUDA-graph capturable.
+ *  - Arguments are validated before anything is launched; a call that
+ *    returns an error has had no side effect.  Checked: NULL pointers, sizes
+ *    <= 0, K and leading dimensions not multiples of 16 elements, pointers
+ *    not 16-byte aligned, workspace too small, device not sm_100.
+ *  - Errors are returned as tern_status; tern_last_error() gives a
+ *    thread-local message.  Asynchronous kernel faults surface at the next
+ *    synchronisation, as in CUDA.  Nothing aborts and nothing throws.
+ *  - Activations are row-major [rows][ld] in tern_dtype; fp32 scales;
+ *    the recurrent state h is always fp32 [B][d] (C13).
+ *  - Numerics follow DESIGN.md "Canonical numerics" exactly (round half
+ *    away from zero C3, binary64 sums of squares C4, canonical exp C12,
+ *    bf16 storage points R0-R3), so integer results (int8 activations,
+ *    int32 accumulators, ternary codes) reproduce the CPU oracle bit for bit
+ *    given the same fp32 scales.
+ *  - y must not alias x.  h is updated in place.  Concurrent calls must use
+ *    disjoint h and workspace buffers.
+ */
+#ifndef TERN_H
+#define TERN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define TERN_ABI_VERSION 1
+
+typedef struct CUstream_st* tern_stream; /* == cudaStream_t */
+
+typedef enum {
+  TERN_OK = 0,
+  TERN_ERR_INVALID_ARG = 1,  /* bad pointer / size / alignment / workspace       */
+  TERN_ERR_DEGENERATE = 2,   /* tern_pack: mean|W| == 0 or W non-finite (C7)       */
+  TERN_ERR_UNSUPPORTED = 3,  /* shape or device this build does not handle        */
+  TERN_ERR_CUDA = 4          /* a CUDA runtime error; text in tern_last_error()    */
+} tern_status;
+
+typedef enum { TERN_F32 = 0, TERN_BF16 = 1 } tern_dtype;
+
+/* MLGRU output gate (C8): o' = g * sigma(h) as written in P:452 / P:661, or
+ * o' = g * h as written in BASELINE.json configs[0]. */
+typedef enum { TERN_GATE_SIGMOID_H = 0, TERN_GATE_LINEAR_H = 1 } tern_gate_mode;
+
+int tern_abi_version(void);
+/* Thread-local text of the last error (host pointer, valid until the next call). */
+const char* tern_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * Packed ternary weights (a1).  DESIGN.md "Packed weight layout":
+ *   trit t in {-1,0,+1} is stored as the 2-bit field e = t + 1;
+ *   16 trits per uint32 word: trit k of a row is in word k/16, byte k%4,
+ *   bits [2f, 2f+1] of that byte with f = (k%16)/4;
+ *   rows are K-contiguous, ldw = Kp/16 words, Kp = roundup(k, 128);
+ *   trits in the padding k..Kp-1 are 0 (field 1).
+ * A fused group of n_seg matrices of n_out rows each (f|c|g: 3, gate|up: 2)
+ * interleaves rows in groups of seg_rows (64):
+ *   packed row of (segment s, row r) = (r/64)*(n_seg*64) + s*64 + r%64,
+ *   n_rows = roundup(n_out, 64) * n_seg (rows of a ragged last group are
+ *   padding and produce outputs that are never stored).
+ * One fp32 dequantization scale mean|W| per segment (one per matrix, C6).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  const uint32_t* codes;  /* device [n_rows][ldw]                                 */
+  const float* scales;    /* device [n_seg]: mean|W| of each source matrix         */
+  int32_t n_out;          /* logical output rows per segment                       */
+  int32_t k;              /* logical input features                                */
+  int32_t ldw;            /* words per packed row, >= roundup(k,128)/16            */
+  int32_t n_seg;          /* 1, 2 or 3                                             */
+  int32_t n_rows;         /* packed rows = roundup(n_out,64)*n_seg (n_seg>1) or n_out */
+} tern_weight;
+
+/* Number of packed rows and words per row for a group (host helper). */
+int32_t tern_packed_rows(int32_t n_out, int32_t n_seg);
+int32_t tern_packed_ldw(int32_t k);
+
+/* Fill codes[n_rows][ldw] with the zero trit (field value 1 everywhere).
+ * Call once on a fresh buffer before tern_pack. */
+tern_status tern_codes_init(uint32_t* codes, int32_t n_rows, int32_t ldw, tern_stream stream);
+
+/* Bytes of workspace tern_pack needs for an [n][k] matrix. */
+size_t tern_pack_workspace(int32_t n, int32_t k);
+
+/* a1: absmean ternarization + packing (Alg. 1 weight_quant):
+ *   m = mean|W| (binary64 sum, rounded once to fp32, C4) or *scale_in,
+ *   s = 1/m, t = clamp(round(s*W), -1, 1) with round half away from zero.
+ * W: device fp32 [n][k] row-major (the latent weight of ONE matrix).
+ * scale_in: device pointer to one float, or NULL to compute mean|W|.
+ * Writes segment seg_idx of the group into codes (see layout above) and the
+ * scale to scale_out[0] (device).  This offline call synchronises `stream`
+ * to check the scale: returns TERN_ERR_DEGENERATE if m == 0 or is not finite
+ * (S:39).  ws: device workspace of tern_pack_workspace(n,k) bytes. */
+tern_status tern_pack(const float* W, int32_t n, int32_t k, const float* scale_in, int32_t n_seg,
+                      int32_t seg_idx, uint32_t* codes, int32_t ldw, float* scale_out, void* ws,
+                      size_t ws_bytes, tern_stream stream);
+
+/* ------------------------------------------------------------------------
+ * a2: fused RMSNorm + per-token absmax int8 quantization (Alg. 1
+ * rms_norm_fwd + activation_quant, Eq. 1, readings C1,
+ * C2, C3, C4, C5, C7):
+ *   r = (float)(1/sqrt(mean_fp64(x^2) + eps)); y = (x*r)*gain;
+ *   a = max|y|; q = clamp(round(y*(127/a)), -128, 127); deq = a/127;
+ *   a == 0 gives q = 0 and deq = 0.
+ * x: [m][ldx] of xdt; gain: [k] fp32 or NULL (ones).
+ * Outputs: q int8 [m][ldq] (ldq >= roundup(k,128); columns k..ldq-1 are
+ * written as 0), deq [m], qsum [m] = sum_j q_j (int32), and optionally
+ * inv_rms [m] and absmax [m] (NULL to skip).
+ * ------------------------------------------------------------------------ */
+tern_status tern_quant(const void* x, tern_dtype xdt, int32_t m, int32_t k, int32_t ldx,
+                       const float* gain, float eps, int8_t* q, int32_t ldq, float* deq,
+                       int32_t* qsum, float* inv_rms, float* absmax, tern_stream stream);
+
+/* Optional parity taps of bitlinear_fwd; any pointer may be NULL. */
+typedef struct {
+  int8_t* q;        /* [m][ldq] quantized activations                       */
+  int32_t ldq;
+  int32_t* acc;     /* [m][ldacc] int32 ternary accumulators, packed-row order */
+  int32_t ldacc;
+  float* deq;       /* [m] absmax/127                                         */
+  float* inv_rms;   /* [m]                                                    */
+  float* absmax;    /* [m]                                                    */
+} tern_bl_taps;
+
+/* Workspace bytes for bitlinear_fwd on m rows of k features. */
+size_t tern_bitlinear_workspace(int32_t m, int32_t k);
+
+/* a2-a5: BitLinear forward (Alg. 1 forward_pass):
+ *   acc_n = sum_{t=+1} q - sum_{t=-1} q  (int32)
+ *   y_n = (float)acc_n * (deq * m_seg) [+ bias_n]
+ * rounded to bf16 when ydt == TERN_BF16 (R1).
+ * w must have n_seg == 1.  y: [m][ldy] of ydt, ldy >= w->n_out.
+ * m <= tern_get_gemv_max_m() runs the decode GEMV (norm+quant fused in its
+ * prologue); larger m runs tern_quant + the tcgen05 int8 GEMM. */
+tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, int32_t ldx,
+                          const float* gain, float eps, const tern_weight* w, const float* bias,
+                          void* y, tern_dtype ydt, int32_t ldy, const tern_bl_taps* taps, void* ws,
+                          size_t ws_bytes, tern_stream stream);
+
+/* a3/a4 on pre-quantized activations (parity entry point):
+ * acc[m][ldacc] = q (*) W~ over all packed rows (int32, exact). */
+tern_status tern_contract(const int8_t* q, int32_t m, int32_t ldq, const int32_t* qsum,
+                          const tern_weight* w, int32_t* acc, int32_t ldacc, tern_stream stream);
+
+/* ------------------------------------------------------------------------
+ * a6: MLGRU gates + recurrence + output gate:
+ *   f = sigma(fhat), c = SiLU(chat), h_t = f*h_{t-1} + (1-f)*c, h_0 = h,
+ *   o' = ghat * sigma(h_t) (gate = TERN_GATE_SIGMOID_H) or ghat * h_t.
+ * fcg: [B*T][3d] pre-activations in the fused interleaved order
+ *      (per 64-channel group: 64 f | 64 c | 64 g), dtype dt;
+ * h:   fp32 [B][d] in/out; oprime: [B*T][d] dtype dt (bf16 rounds o', R2).
+ * Exact sequential recurrence per channel (bit-identical to the oracle);
+ * the transcendental work is spread over time within each CTA. d % 64 == 0.
+ * ------------------------------------------------------------------------ */
+tern_status tern_mlgru_scan(const void* fcg, tern_dtype dt, int32_t B, int32_t T, int32_t d,
+                            tern_gate_mode gate, float* h, void* oprime, tern_stream stream);
+
+/* ------------------------------------------------------------------------
+ * Mixers and block.  Weight groups: fcg = {W_f, W_c, W_g} (n_seg 3, d->d),
+ * o = W_o (d->d), gu = {W_gate, W_up} (n_seg 2, d->l), down = W_down (l->d).
+ * Gains: NULL = ones.  Biases (C11) optional; the GLU has none.
+ * Each BitLinear normalizes its own input; f, c and g share theirs
+ * (C10), as do gate and up.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  tern_weight fcg, o;
+  const float *gain_x, *gain_o;     /* [d], [d]                */
+  const float *bias_fcg;            /* [3][d] (f, c, g) or NULL */
+  const float *bias_o;              /* [d] or NULL              */
+  tern_gate_mode gate;
+  float eps;
+} tern_mlgru;
+
+typedef struct {
+  tern_weight gu, down;
+  const float *gain_x, *gain_p;     /* [d], [l] */
+  float eps;
+} tern_glu;
+
+typedef struct {
+  tern_mlgru mix;
+  tern_glu ch;
+  int32_t d, l;
+} tern_block;
+
+/* Workspace bytes for mlgru_fwd / glu_fwd / block_* on B sequences x T tokens. */
+size_t tern_mlgru_workspace(const tern_mlgru* p, int32_t B, int32_t T, int32_t d, tern_dtype dt);
+size_t tern_glu_workspace(const tern_glu* p, int32_t m, int32_t d, int32_t l, tern_dtype dt);
+size_t tern_block_workspace(const tern_block* b, int32_t B, int32_t T, tern_dtype dt);
+
+/* Byte offsets of the block's intermediates inside its workspace, valid after
+ * block_prefill / block_decode returns on the stream (parity taps):
+ *   fcg [B*T][3d], oprime [B*T][d], x1 [B*T][d], p [B*T][l], all dtype dt. */
+typedef struct {
+  size_t fcg, oprime, x1, p;
+} tern_block_taps;
+tern_status tern_block_ws_layout(const tern_block* b, int32_t B, int32_t T, tern_dtype dt,
+                                 tern_block_taps* out /* host */);
+
+/* MLGRU token mixer: out = o_t for x [B][T][d] (no residual). */
+tern_status mlgru_fwd(const tern_mlgru* p, const void* x, void* out, tern_dtype dt, int32_t B,
+                      int32_t T, int32_t d, float* h, void* ws, size_t ws_bytes,
+                      tern_stream stream);
+
+/* GLU channel mixer: out = d_t for x [m][d] (no residual). */
+tern_status glu_fwd(const tern_glu* p, const void* x, void* out, tern_dtype dt, int32_t m,
+                    int32_t d, int32_t l, void* ws, size_t ws_bytes, tern_stream stream);
+
+/* a8: block prefill, x1 = x + MLGRU(x), y = x1 + GLU(x1) (C9), over
+ * B sequences of T tokens starting from state h (0 at a fresh prefill,
+ * P:456); h holds h_T afterwards.  bf16 rounds x1 and y (R3). */
+tern_status block_prefill(const tern_block* b, const void* x, void* y, tern_dtype dt, int32_t B,
+                          int32_t T, float* h, void* ws, size_t ws_bytes, tern_stream stream);
+
+/* a8/a9: one decode step (T = 1) continuing state h. B <= gemv_max_m runs
+ * four GEMV launches (norm+quant fused into each prologue, the MLGRU step
+ * and SwiGLU fused into epilogues); larger B runs the prefill path with T=1. */
+tern_status block_decode(const tern_block* b, const void* x, void* y, tern_dtype dt, int32_t B,
+                         float* h, void* ws, size_t ws_bytes, tern_stream stream);
+
+/* Tuning knob (host): largest m sent to the decode GEMV (default 8, max 8;
+ * 0 forces the tensor-core path everywhere).  Not thread-safe to change
+ * while calls are in flight. */
+void tern_set_gemv_max_m(int32_t m);
+int32_t tern_get_gemv_max_m(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* TERN_H */

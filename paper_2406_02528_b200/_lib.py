@@ -1,0 +1,228 @@
+"""ctypes binding of libtern.so (include/tern.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  Function names match the C ABI.  There is no fallback: if the
+shared library is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("TERN_LIB", os.path.join(_HERE, "libtern.so"))
+
+TERN_OK, TERN_ERR_INVALID_ARG, TERN_ERR_DEGENERATE, TERN_ERR_UNSUPPORTED, TERN_ERR_CUDA = range(5)
+TERN_F32, TERN_BF16 = 0, 1
+TERN_GATE_SIGMOID_H, TERN_GATE_LINEAR_H = 0, 1
+
+
+class TernError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[tern status {status}] {msg}")
+        self.status = status
+
+
+class tern_weight(C.Structure):
+    _fields_ = [("codes", C.c_void_p), ("scales", C.c_void_p), ("n_out", C.c_int32),
+                ("k", C.c_int32), ("ldw", C.c_int32), ("n_seg", C.c_int32),
+                ("n_rows", C.c_int32)]
+
+
+class tern_bl_taps(C.Structure):
+    _fields_ = [("q", C.c_void_p), ("ldq", C.c_int32), ("acc", C.c_void_p), ("ldacc", C.c_int32),
+                ("deq", C.c_void_p), ("inv_rms", C.c_void_p), ("absmax", C.c_void_p)]
+
+
+class tern_mlgru(C.Structure):
+    _fields_ = [("fcg", tern_weight), ("o", tern_weight), ("gain_x", C.c_void_p),
+                ("gain_o", C.c_void_p), ("bias_fcg", C.c_void_p), ("bias_o", C.c_void_p),
+                ("gate", C.c_int), ("eps", C.c_float)]
+
+
+class tern_glu(C.Structure):
+    _fields_ = [("gu", tern_weight), ("down", tern_weight), ("gain_x", C.c_void_p),
+                ("gain_p", C.c_void_p), ("eps", C.c_float)]
+
+
+class tern_block(C.Structure):
+    _fields_ = [("mix", tern_mlgru), ("ch", tern_glu), ("d", C.c_int32), ("l", C.c_int32)]
+
+
+class tern_block_taps(C.Structure):
+    _fields_ = [("fcg", C.c_size_t), ("oprime", C.c_size_t), ("x1", C.c_size_t),
+                ("p", C.c_size_t)]
+
+
+P = C.c_void_p
+I32 = C.c_int32
+SZ = C.c_size_t
+F = C.c_float
+_SIGS = {
+    "tern_abi_version": (C.c_int, []),
+    "tern_last_error": (C.c_char_p, []),
+    "tern_packed_rows": (I32, [I32, I32]),
+    "tern_packed_ldw": (I32, [I32]),
+    "tern_codes_init": (C.c_int, [P, I32, I32, P]),
+    "tern_pack_workspace": (SZ, [I32, I32]),
+    "tern_pack": (C.c_int, [P, I32, I32, P, I32, I32, P, I32, P, P, SZ, P]),
+    "tern_quant": (C.c_int, [P, C.c_int, I32, I32, I32, P, F, P, I32, P, P, P, P, P]),
+    "tern_bitlinear_workspace": (SZ, [I32, I32]),
+    "bitlinear_fwd": (C.c_int, [P, C.c_int, I32, I32, I32, P, F, C.POINTER(tern_weight), P, P,
+                                C.c_int, I32, C.POINTER(tern_bl_taps), P, SZ, P]),
+    "tern_contract": (C.c_int, [P, I32, I32, P, C.POINTER(tern_weight), P, I32, P]),
+    "tern_mlgru_scan": (C.c_int, [P, C.c_int, I32, I32, I32, C.c_int, P, P, P]),
+    "tern_mlgru_workspace": (SZ, [C.POINTER(tern_mlgru), I32, I32, I32, C.c_int]),
+    "tern_glu_workspace": (SZ, [C.POINTER(tern_glu), I32, I32, I32, C.c_int]),
+    "tern_block_workspace": (SZ, [C.POINTER(tern_block), I32, I32, C.c_int]),
+    "tern_block_ws_layout": (C.c_int, [C.POINTER(tern_block), I32, I32, C.c_int,
+                                       C.POINTER(tern_block_taps)]),
+    "mlgru_fwd": (C.c_int, [C.POINTER(tern_mlgru), P, P, C.c_int, I32, I32, I32, P, P, SZ, P]),
+    "glu_fwd": (C.c_int, [C.POINTER(tern_glu), P, P, C.c_int, I32, I32, I32, P, SZ, P]),
+    "block_prefill": (C.c_int, [C.POINTER(tern_block), P, P, C.c_int, I32, I32, P, P, SZ, P]),
+    "block_decode": (C.c_int, [C.POINTER(tern_block), P, P, C.c_int, I32, P, P, SZ, P]),
+    "tern_set_gemv_max_m": (None, [I32]),
+    "tern_get_gemv_max_m": (I32, []),
+}
+EXPORTS = tuple(_SIGS)
+
+_lib = None
+
+
+def load():
+    """Load libtern.so (raises OSError if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise OSError(f"libtern.so not found at {LIB_PATH}; run "
+                          f"`python -m paper_2406_02528_b200.build` (there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int, what: str):
+    if st != TERN_OK:
+        msg = load().tern_last_error()
+        raise TernError(st, f"{what}: {msg.decode() if msg else ''}")
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.float32:
+        return TERN_F32
+    if dt == torch.bfloat16:
+        return TERN_BF16
+    raise TypeError(f"unsupported activation dtype {dt}")
+
+
+def stream_handle(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+# ------------------------------------------------------------------ wrappers with C names
+def tern_packed_rows(n_out: int, n_seg: int) -> int:
+    return int(load().tern_packed_rows(n_out, n_seg))
+
+
+def tern_packed_ldw(k: int) -> int:
+    return int(load().tern_packed_ldw(k))
+
+
+def tern_codes_init(codes: torch.Tensor, stream=None):
+    n_rows, ldw = codes.shape
+    _check(load().tern_codes_init(ptr(codes), n_rows, ldw, stream_handle(stream)), "tern_codes_init")
+
+
+def tern_pack(W: torch.Tensor, codes: torch.Tensor, scale_out: torch.Tensor, n_seg=1, seg_idx=0,
+              scale_in: torch.Tensor | None = None, stream=None):
+    """Ternarize + pack fp32 W [n][k] (device) into segment seg_idx of codes."""
+    assert W.is_cuda and W.dtype == torch.float32 and W.is_contiguous()
+    n, k = W.shape
+    L = load()
+    wsb = int(L.tern_pack_workspace(n, k))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=W.device)
+    _check(L.tern_pack(ptr(W), n, k, ptr(scale_in), n_seg, seg_idx, ptr(codes), codes.shape[1],
+                       ptr(scale_out), ptr(ws), wsb, stream_handle(stream)), "tern_pack")
+
+
+def tern_quant(x: torch.Tensor, q: torch.Tensor, deq: torch.Tensor, qsum: torch.Tensor,
+               gain=None, eps=1e-6, inv_rms=None, absmax=None, stream=None):
+    m, k = x.shape
+    _check(load().tern_quant(ptr(x), dtype_code(x.dtype), m, k, x.stride(0), ptr(gain), eps,
+                             ptr(q), q.stride(0), ptr(deq), ptr(qsum), ptr(inv_rms), ptr(absmax),
+                             stream_handle(stream)), "tern_quant")
+
+
+def bitlinear_fwd(x, w: tern_weight, y, gain=None, bias=None, eps=1e-6, taps=None, ws=None,
+                  stream=None):
+    m, k = x.shape
+    L = load()
+    need = int(L.tern_bitlinear_workspace(m, k))
+    if ws is None:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
+    tp = None
+    if taps is not None:
+        tp = tern_bl_taps(ptr(taps.get("q")), taps["q"].stride(0) if taps.get("q") is not None else 0,
+                          ptr(taps.get("acc")),
+                          taps["acc"].stride(0) if taps.get("acc") is not None else 0,
+                          ptr(taps.get("deq")), ptr(taps.get("inv_rms")), ptr(taps.get("absmax")))
+    _check(L.bitlinear_fwd(ptr(x), dtype_code(x.dtype), m, k, x.stride(0), ptr(gain), eps,
+                           C.byref(w), ptr(bias), ptr(y), dtype_code(y.dtype), y.stride(0),
+                           C.byref(tp) if tp is not None else None, ptr(ws), ws.numel(),
+                           stream_handle(stream)), "bitlinear_fwd")
+
+
+def tern_contract(q, qsum, w: tern_weight, acc, stream=None):
+    m = q.shape[0]
+    _check(load().tern_contract(ptr(q), m, q.stride(0), ptr(qsum), C.byref(w), ptr(acc),
+                                acc.stride(0), stream_handle(stream)), "tern_contract")
+
+
+def tern_mlgru_scan(fcg, B, T, d, h, oprime, gate=TERN_GATE_SIGMOID_H, stream=None):
+    _check(load().tern_mlgru_scan(ptr(fcg), dtype_code(fcg.dtype), B, T, d, gate, ptr(h),
+                                  ptr(oprime), stream_handle(stream)), "tern_mlgru_scan")
+
+
+def mlgru_fwd(p: tern_mlgru, x, out, h, ws, stream=None):
+    B, T, d = x.shape
+    _check(load().mlgru_fwd(C.byref(p), ptr(x), ptr(out), dtype_code(x.dtype), B, T, d, ptr(h),
+                            ptr(ws), ws.numel(), stream_handle(stream)), "mlgru_fwd")
+
+
+def glu_fwd(p: tern_glu, x, out, l, ws, stream=None):
+    m, d = x.shape
+    _check(load().glu_fwd(C.byref(p), ptr(x), ptr(out), dtype_code(x.dtype), m, d, l, ptr(ws),
+                          ws.numel(), stream_handle(stream)), "glu_fwd")
+
+
+def block_prefill(b: tern_block, x, y, h, ws, stream=None):
+    B, T, d = x.shape
+    _check(load().block_prefill(C.byref(b), ptr(x), ptr(y), dtype_code(x.dtype), B, T, ptr(h),
+                                ptr(ws), ws.numel(), stream_handle(stream)), "block_prefill")
+
+
+def block_decode(b: tern_block, x, y, h, ws, stream=None):
+    B = x.shape[0]
+    _check(load().block_decode(C.byref(b), ptr(x), ptr(y), dtype_code(x.dtype), B, ptr(h),
+                               ptr(ws), ws.numel(), stream_handle(stream)), "block_decode")
+
+
+def tern_set_gemv_max_m(m: int):
+    load().tern_set_gemv_max_m(int(m))
+
+
+def tern_get_gemv_max_m() -> int:
+    return int(load().tern_get_gemv_max_m())

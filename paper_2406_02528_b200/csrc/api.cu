@@ -1,0 +1,461 @@
+// api.cu -- the C ABI of libtern.so (include/tern.h): argument validation,
+// workspace carve-up and the launch sequences of the block (DESIGN.md
+// "Boundary").  Every check runs before the first launch, so a failing call
+// has no side effects.  No allocation, no host sync (except tern_pack).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "internal.h"
+
+using namespace tern;
+
+namespace {
+
+thread_local std::string g_err;
+int g_gemv_max_m = 8;
+
+tern_status fail(tern_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+tern_status cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return TERN_OK;
+  return fail(TERN_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define TRY_CUDA(expr, where)                              \
+  do {                                                     \
+    tern_status _st = cuda_status((expr), (where));        \
+    if (_st != TERN_OK) return _st;                        \
+  } while (0)
+#define CHECK(cond, ...)                                   \
+  do {                                                     \
+    if (!(cond)) return fail(TERN_ERR_INVALID_ARG, __VA_ARGS__); \
+  } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+int kpad(int k) { return (k + kKAlign - 1) / kKAlign * kKAlign; }
+size_t dsize(tern_dtype dt) { return dt == TERN_BF16 ? 2 : 4; }
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+bool valid_dt(tern_dtype dt) { return dt == TERN_F32 || dt == TERN_BF16; }
+
+// device must be sm_100 (B200); cached per device
+tern_status check_device() {
+  static int cached[64];
+  static std::once_flag once;
+  std::call_once(once, [] { memset(cached, 0, sizeof(cached)); });
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(TERN_ERR_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  if (dev < 0 || dev >= 64) return fail(TERN_ERR_UNSUPPORTED, "device index %d", dev);
+  if (cached[dev] == 0) {
+    int maj = 0, mnr = 0;
+    cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&mnr, cudaDevAttrComputeCapabilityMinor, dev);
+    cached[dev] = (maj == 10 && mnr == 0) ? 1 : -1;
+  }
+  if (cached[dev] < 0) return fail(TERN_ERR_UNSUPPORTED, "libtern needs an sm_100 (B200) device");
+  return TERN_OK;
+}
+
+tern_status check_weight(const tern_weight* w, int k, int n_seg, const char* name) {
+  CHECK(w, "%s: null weight", name);
+  CHECK(w->codes && aligned16(w->codes), "%s: codes null or not 16-byte aligned", name);
+  CHECK(w->scales, "%s: null scales", name);
+  CHECK(w->k == k, "%s: weight k=%d but input has %d features", name, w->k, k);
+  CHECK(w->n_seg == n_seg, "%s: n_seg=%d, expected %d", name, w->n_seg, n_seg);
+  CHECK(w->n_out > 0, "%s: n_out must be > 0", name);
+  CHECK(w->n_rows == tern_packed_rows(w->n_out, w->n_seg), "%s: n_rows=%d inconsistent", name,
+        w->n_rows);
+  CHECK(w->ldw >= kpad(k) / 16 && w->ldw % 4 == 0, "%s: ldw=%d must be >= %d and a multiple of 4",
+        name, w->ldw, kpad(k) / 16);
+  return TERN_OK;
+}
+
+Epi make_epi(int kind, const tern_weight& w, const float* bias, void* out, int ldo) {
+  Epi e{};
+  e.kind = kind;
+  e.n_out = w.n_out;
+  e.n_seg = w.n_seg;
+  e.scales = w.scales;
+  e.bias = bias;
+  e.out = out;
+  e.ldo = ldo;
+  return e;
+}
+
+struct BlockWs {
+  size_t q, deq, qsum, fcg, oprime, x1, p, total;
+};
+BlockWs block_ws(int32_t M, int32_t d, int32_t l, int32_t fcg_rows, tern_dtype dt) {
+  BlockWs w{};
+  size_t off = 0;
+  const int kq = kpad(d > l ? d : l);
+  w.q = off; off += al256((size_t)M * kq);
+  w.deq = off; off += al256((size_t)M * 4);
+  w.qsum = off; off += al256((size_t)M * 4);
+  w.fcg = off; off += al256((size_t)M * fcg_rows * dsize(dt));
+  w.oprime = off; off += al256((size_t)M * d * dsize(dt));
+  w.x1 = off; off += al256((size_t)M * d * dsize(dt));
+  w.p = off; off += al256((size_t)M * (l > 0 ? l : 1) * dsize(dt));
+  w.total = off;
+  return w;
+}
+
+template <typename T> T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+// one BitLinear on the tensor-core path: quant (a2) then GEMM (a4+a5+functor)
+tern_status bl_tc(const void* x, tern_dtype xdt, int M, int K, int ldx, const float* gain,
+                  float eps, const tern_weight& w, tern_dtype ydt, const Epi& epi, int8_t* q,
+                  int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
+                  cudaStream_t s) {
+  TRY_CUDA(launch_quant(x, xdt, M, K, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s),
+           "quant");
+  TRY_CUDA(launch_gemm(q, M, ldq, deq, qsum, w, ydt, epi, s), "gemm");
+  return TERN_OK;
+}
+
+tern_status check_block(const tern_block* b) {
+  CHECK(b, "null block");
+  const int d = b->d, l = b->l;
+  CHECK(d > 0 && d % 64 == 0, "d=%d must be a positive multiple of 64", d);
+  CHECK(l > 0 && l % 16 == 0, "l=%d must be a positive multiple of 16", l);
+  tern_status st;
+  if ((st = check_weight(&b->mix.fcg, d, 3, "fcg")) != TERN_OK) return st;
+  if ((st = check_weight(&b->mix.o, d, 1, "o")) != TERN_OK) return st;
+  if ((st = check_weight(&b->ch.gu, d, 2, "gate|up")) != TERN_OK) return st;
+  if ((st = check_weight(&b->ch.down, l, 1, "down")) != TERN_OK) return st;
+  CHECK(b->mix.fcg.n_out == d && b->mix.o.n_out == d, "MLGRU weights must be d x d");
+  CHECK(b->ch.gu.n_out == l && b->ch.down.n_out == d, "GLU weights must be d->l, l->d");
+  CHECK(b->mix.gate == TERN_GATE_SIGMOID_H || b->mix.gate == TERN_GATE_LINEAR_H, "bad gate mode");
+  CHECK(b->mix.eps > 0 && b->ch.eps > 0, "eps must be > 0");
+  return TERN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tern_abi_version(void) { return TERN_ABI_VERSION; }
+const char* tern_last_error(void) { return g_err.c_str(); }
+void tern_set_gemv_max_m(int32_t m) { g_gemv_max_m = m < 0 ? 0 : (m > 8 ? 8 : m); }
+int32_t tern_get_gemv_max_m(void) { return g_gemv_max_m; }
+
+int32_t tern_packed_rows(int32_t n_out, int32_t n_seg) {
+  if (n_seg <= 1) return n_out;
+  return (n_out + kSegRows - 1) / kSegRows * kSegRows * n_seg;
+}
+int32_t tern_packed_ldw(int32_t k) { return kpad(k) / 16; }
+
+tern_status tern_codes_init(uint32_t* codes, int32_t n_rows, int32_t ldw, tern_stream stream) {
+  CHECK(codes && n_rows > 0 && ldw > 0, "tern_codes_init: bad arguments");
+  tern_status st = check_device();
+  if (st) return st;
+  TRY_CUDA(launch_codes_init(codes, n_rows, ldw, (cudaStream_t)stream), "codes_init");
+  return TERN_OK;
+}
+
+size_t tern_pack_workspace(int32_t n, int32_t k) {
+  (void)n; (void)k;
+  return pack_workspace_bytes() + 256;
+}
+
+tern_status tern_pack(const float* W, int32_t n, int32_t k, const float* scale_in, int32_t n_seg,
+                      int32_t seg_idx, uint32_t* codes, int32_t ldw, float* scale_out, void* ws,
+                      size_t ws_bytes, tern_stream stream) {
+  CHECK(W && codes && scale_out && ws, "tern_pack: null pointer");
+  CHECK(n > 0 && k > 0, "tern_pack: n=%d k=%d must be > 0", n, k);
+  CHECK(n_seg >= 1 && n_seg <= 3 && seg_idx >= 0 && seg_idx < n_seg, "tern_pack: bad segment");
+  CHECK(ldw >= kpad(k) / 16, "tern_pack: ldw=%d < %d", ldw, kpad(k) / 16);
+  CHECK(ws_bytes >= tern_pack_workspace(n, k), "tern_pack: workspace too small");
+  CHECK(aligned16(ws), "tern_pack: workspace not 16-byte aligned");
+  tern_status st = check_device();
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* part = static_cast<double*>(ws);
+  float* scratch = reinterpret_cast<float*>(static_cast<char*>(ws) + pack_workspace_bytes());
+  TRY_CUDA(launch_absmean(W, (int64_t)n * k, scale_in, scratch, part, s), "absmean");
+  float m = 0.0f;
+  TRY_CUDA(cudaMemcpyAsync(&m, scratch, sizeof(float), cudaMemcpyDeviceToHost, s), "scale d2h");
+  TRY_CUDA(cudaStreamSynchronize(s), "tern_pack sync");
+  if (!(m > 0.0f) || !(m < __FLT_MAX__))
+    return fail(TERN_ERR_DEGENERATE, "tern_pack: mean|W| = %g (all-zero or non-finite W)", m);
+  TRY_CUDA(cudaMemcpyAsync(scale_out, scratch, sizeof(float), cudaMemcpyDeviceToDevice, s),
+           "scale copy");
+  TRY_CUDA(launch_pack_codes(W, n, k, n_seg, seg_idx, codes, ldw, scratch, s), "pack");
+  return TERN_OK;
+}
+
+tern_status tern_quant(const void* x, tern_dtype xdt, int32_t m, int32_t k, int32_t ldx,
+                       const float* gain, float eps, int8_t* q, int32_t ldq, float* deq,
+                       int32_t* qsum, float* inv_rms, float* absmax, tern_stream stream) {
+  CHECK(x && q && deq && qsum, "tern_quant: null pointer");
+  CHECK(valid_dt(xdt), "tern_quant: bad dtype");
+  CHECK(m >= 0 && k > 0 && k % 16 == 0, "tern_quant: m=%d k=%d (k must be a multiple of 16)", m, k);
+  CHECK(k <= 32 * 128 * 4, "tern_quant: k=%d too large", k);
+  CHECK(ldx >= k && ldx % 16 == 0 && aligned16(x), "tern_quant: ldx/alignment");
+  CHECK(ldq >= kpad(k) && ldq % 16 == 0 && aligned16(q), "tern_quant: ldq must be >= %d", kpad(k));
+  CHECK(eps > 0, "tern_quant: eps must be > 0");
+  tern_status st = check_device();
+  if (st) return st;
+  TRY_CUDA(launch_quant(x, xdt, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax,
+                        (cudaStream_t)stream),
+           "quant");
+  return TERN_OK;
+}
+
+size_t tern_bitlinear_workspace(int32_t m, int32_t k) {
+  return al256((size_t)m * kpad(k)) + 2 * al256((size_t)m * 4);
+}
+
+tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, int32_t ldx,
+                          const float* gain, float eps, const tern_weight* w, const float* bias,
+                          void* y, tern_dtype ydt, int32_t ldy, const tern_bl_taps* taps, void* ws,
+                          size_t ws_bytes, tern_stream stream) {
+  CHECK(x && y, "bitlinear_fwd: null x/y");
+  CHECK(valid_dt(xdt) && valid_dt(ydt), "bitlinear_fwd: bad dtype");
+  CHECK(m >= 0 && k > 0 && k % 16 == 0, "bitlinear_fwd: m=%d k=%d", m, k);
+  CHECK(ldx >= k && ldx % 16 == 0 && aligned16(x), "bitlinear_fwd: ldx/alignment");
+  tern_status st = check_weight(w, k, 1, "bitlinear_fwd");
+  if (st) return st;
+  CHECK(ldy >= w->n_out && ldy % 16 == 0 && aligned16(y), "bitlinear_fwd: ldy/alignment");
+  CHECK(eps > 0, "bitlinear_fwd: eps must be > 0");
+  const bool gemv = m <= g_gemv_max_m;
+  if (taps) {
+    CHECK(!taps->q || taps->ldq >= kpad(k), "bitlinear_fwd: taps ldq");
+    CHECK(!taps->acc || taps->ldacc >= w->n_rows, "bitlinear_fwd: taps ldacc");
+  }
+  if (!gemv) {
+    CHECK(ws && aligned16(ws) && ws_bytes >= tern_bitlinear_workspace(m, k),
+          "bitlinear_fwd: workspace too small (%zu < %zu)", ws_bytes,
+          tern_bitlinear_workspace(m, k));
+    CHECK(k <= 16384, "bitlinear_fwd: k too large");
+  } else {
+    CHECK(k <= 7168, "bitlinear_fwd: decode path supports k <= 7168");
+  }
+  st = check_device();
+  if (st) return st;
+  if (m == 0) return TERN_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  Epi e = make_epi(EPI_STORE, *w, bias, y, ldy);
+  if (taps && taps->acc) {
+    e.acc = taps->acc;
+    e.ldacc = taps->ldacc;
+  }
+  if (gemv) {
+    QuantTaps qt{};
+    if (taps) {
+      qt.q = taps->q; qt.ldq = taps->ldq; qt.deq = taps->deq;
+      qt.inv_rms = taps->inv_rms; qt.absmax = taps->absmax;
+    }
+    TRY_CUDA(launch_gemv(x, xdt, ydt, m, k, ldx, gain, eps, *w, e, &qt, s), "gemv");
+    return TERN_OK;
+  }
+  int8_t* q = (taps && taps->q) ? taps->q : static_cast<int8_t*>(ws);
+  const int ldq = (taps && taps->q) ? taps->ldq : kpad(k);
+  float* deq = (taps && taps->deq) ? taps->deq : at<float>(ws, al256((size_t)m * kpad(k)));
+  int32_t* qsum = at<int32_t>(ws, al256((size_t)m * kpad(k)) + al256((size_t)m * 4));
+  return bl_tc(x, xdt, m, k, ldx, gain, eps, *w, ydt, e, q, ldq, deq, qsum,
+               taps ? taps->inv_rms : nullptr, taps ? taps->absmax : nullptr, s);
+}
+
+tern_status tern_contract(const int8_t* q, int32_t m, int32_t ldq, const int32_t* qsum,
+                          const tern_weight* w, int32_t* acc, int32_t ldacc, tern_stream stream) {
+  CHECK(q && qsum && acc && w, "tern_contract: null pointer");
+  CHECK(m >= 0, "tern_contract: m < 0");
+  tern_status st = check_weight(w, w ? w->k : 0, w ? w->n_seg : 1, "tern_contract");
+  if (st) return st;
+  CHECK(ldq >= kpad(w->k) && ldq % 16 == 0 && aligned16(q), "tern_contract: ldq");
+  CHECK(ldacc >= w->n_rows, "tern_contract: ldacc < n_rows");
+  st = check_device();
+  if (st) return st;
+  Epi e = make_epi(EPI_NONE, *w, nullptr, nullptr, 0);
+  e.acc = acc;
+  e.ldacc = ldacc;
+  // deq is unused by EPI_NONE; pass qsum as a harmless readable pointer
+  TRY_CUDA(launch_gemm(q, m, ldq, reinterpret_cast<const float*>(qsum), qsum, *w, TERN_F32, e,
+                       (cudaStream_t)stream),
+           "gemm");
+  return TERN_OK;
+}
+
+tern_status tern_mlgru_scan(const void* fcg, tern_dtype dt, int32_t B, int32_t T, int32_t d,
+                            tern_gate_mode gate, float* h, void* oprime, tern_stream stream) {
+  CHECK(fcg && h && oprime, "tern_mlgru_scan: null pointer");
+  CHECK(valid_dt(dt), "tern_mlgru_scan: bad dtype");
+  CHECK(B >= 0 && T >= 0 && d > 0 && d % 64 == 0, "tern_mlgru_scan: B=%d T=%d d=%d", B, T, d);
+  CHECK(gate == TERN_GATE_SIGMOID_H || gate == TERN_GATE_LINEAR_H, "tern_mlgru_scan: gate");
+  tern_status st = check_device();
+  if (st) return st;
+  TRY_CUDA(launch_scan(fcg, dt, B, T, d, gate, h, oprime, (cudaStream_t)stream), "scan");
+  return TERN_OK;
+}
+
+size_t tern_mlgru_workspace(const tern_mlgru* p, int32_t B, int32_t T, int32_t d, tern_dtype dt) {
+  const int rows = p ? p->fcg.n_rows : 3 * d;
+  return block_ws(B * T, d, 0, rows, dt).total;
+}
+size_t tern_glu_workspace(const tern_glu* p, int32_t m, int32_t d, int32_t l, tern_dtype dt) {
+  (void)p;
+  return block_ws(m, d, l, 0, dt).total;
+}
+size_t tern_block_workspace(const tern_block* b, int32_t B, int32_t T, tern_dtype dt) {
+  if (!b) return 0;
+  return block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt).total;
+}
+
+tern_status tern_block_ws_layout(const tern_block* b, int32_t B, int32_t T, tern_dtype dt,
+                                 tern_block_taps* out) {
+  CHECK(b && out, "tern_block_ws_layout: null pointer");
+  BlockWs w = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt);
+  out->fcg = w.fcg;
+  out->oprime = w.oprime;
+  out->x1 = w.x1;
+  out->p = w.p;
+  return TERN_OK;
+}
+
+namespace {
+
+// token mixer: x [M][d] -> out (o, or x1 = x + o when resid), state h
+tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid, tern_dtype dt,
+                      int B, int T, int d, float* h, void* ws, const BlockWs& L, cudaStream_t s) {
+  const int M = B * T;
+  void* op = at<char>(ws, L.oprime);
+  if (T == 1 && B <= g_gemv_max_m) {
+    Epi e1 = make_epi(EPI_MLGRU, p.fcg, p.bias_fcg, op, d);
+    e1.h = h;
+    e1.gate = p.gate;
+    TRY_CUDA(launch_gemv(x, dt, dt, B, d, d, p.gain_x, p.eps, p.fcg, e1, nullptr, s), "gemv fcg");
+    Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.o, p.bias_o, out, d);
+    e2.res = x;
+    e2.ldr = d;
+    TRY_CUDA(launch_gemv(op, dt, dt, B, d, d, p.gain_o, p.eps, p.o, e2, nullptr, s), "gemv o");
+    return TERN_OK;
+  }
+  int8_t* q = at<int8_t>(ws, L.q);
+  float* deq = at<float>(ws, L.deq);
+  int32_t* qsum = at<int32_t>(ws, L.qsum);
+  void* fcg = at<char>(ws, L.fcg);
+  const int ldq = kpad(d);
+  Epi e1 = make_epi(EPI_FCG, p.fcg, p.bias_fcg, fcg, p.fcg.n_rows);
+  tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
+                         nullptr, nullptr, s);
+  if (st) return st;
+  TRY_CUDA(launch_scan(fcg, dt, B, T, d, p.gate, h, op, s), "scan");
+  Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.o, p.bias_o, out, d);
+  e2.res = x;
+  e2.ldr = d;
+  return bl_tc(op, dt, M, d, d, p.gain_o, p.eps, p.o, dt, e2, q, ldq, deq, qsum, nullptr, nullptr,
+               s);
+}
+
+// channel mixer: x [M][d] -> out (d, or y = x + d when resid)
+tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, tern_dtype dt, int M,
+                    int d, int l, void* ws, const BlockWs& L, cudaStream_t s) {
+  void* pp = at<char>(ws, L.p);
+  Epi e1 = make_epi(EPI_SWIGLU, p.gu, nullptr, pp, l);
+  Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.down, nullptr, out, d);
+  e2.res = x;
+  e2.ldr = d;
+  if (M <= g_gemv_max_m) {
+    TRY_CUDA(launch_gemv(x, dt, dt, M, d, d, p.gain_x, p.eps, p.gu, e1, nullptr, s), "gemv gu");
+    TRY_CUDA(launch_gemv(pp, dt, dt, M, l, l, p.gain_p, p.eps, p.down, e2, nullptr, s),
+             "gemv down");
+    return TERN_OK;
+  }
+  int8_t* q = at<int8_t>(ws, L.q);
+  float* deq = at<float>(ws, L.deq);
+  int32_t* qsum = at<int32_t>(ws, L.qsum);
+  tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.gu, dt, e1, q, kpad(d), deq, qsum,
+                         nullptr, nullptr, s);
+  if (st) return st;
+  return bl_tc(pp, dt, M, l, l, p.gain_p, p.eps, p.down, dt, e2, q, kpad(l), deq, qsum, nullptr,
+               nullptr, s);
+}
+
+tern_status check_act(const void* x, const void* y, const void* ws, size_t ws_bytes, size_t need,
+                      tern_dtype dt, const char* name) {
+  CHECK(x && y, "%s: null x/y", name);
+  CHECK(aligned16(x) && aligned16(y), "%s: x/y not 16-byte aligned", name);
+  CHECK(x != y, "%s: y must not alias x", name);
+  CHECK(valid_dt(dt), "%s: bad dtype", name);
+  CHECK(ws && aligned16(ws) && ws_bytes >= need, "%s: workspace too small (%zu < %zu)", name,
+        ws_bytes, need);
+  return TERN_OK;
+}
+
+}  // namespace
+
+tern_status mlgru_fwd(const tern_mlgru* p, const void* x, void* out, tern_dtype dt, int32_t B,
+                      int32_t T, int32_t d, float* h, void* ws, size_t ws_bytes,
+                      tern_stream stream) {
+  CHECK(p && h, "mlgru_fwd: null params/state");
+  CHECK(B >= 0 && T >= 0 && d > 0 && d % 64 == 0, "mlgru_fwd: B=%d T=%d d=%d", B, T, d);
+  tern_status st;
+  if ((st = check_weight(&p->fcg, d, 3, "fcg")) != TERN_OK) return st;
+  if ((st = check_weight(&p->o, d, 1, "o")) != TERN_OK) return st;
+  CHECK(p->fcg.n_out == d && p->o.n_out == d, "mlgru_fwd: weights must be d x d");
+  CHECK(p->eps > 0, "mlgru_fwd: eps");
+  BlockWs L = block_ws(B * T, d, 0, p->fcg.n_rows, dt);
+  if ((st = check_act(x, out, ws, ws_bytes, L.total, dt, "mlgru_fwd")) != TERN_OK) return st;
+  if ((st = check_device()) != TERN_OK) return st;
+  if (B * T == 0) return TERN_OK;
+  return run_mlgru(*p, x, out, false, dt, B, T, d, h, ws, L, (cudaStream_t)stream);
+}
+
+tern_status glu_fwd(const tern_glu* p, const void* x, void* out, tern_dtype dt, int32_t m,
+                    int32_t d, int32_t l, void* ws, size_t ws_bytes, tern_stream stream) {
+  CHECK(p, "glu_fwd: null params");
+  CHECK(m >= 0 && d > 0 && d % 16 == 0 && l > 0 && l % 16 == 0, "glu_fwd: m=%d d=%d l=%d", m, d, l);
+  tern_status st;
+  if ((st = check_weight(&p->gu, d, 2, "gate|up")) != TERN_OK) return st;
+  if ((st = check_weight(&p->down, l, 1, "down")) != TERN_OK) return st;
+  CHECK(p->gu.n_out == l && p->down.n_out == d, "glu_fwd: weights must be d->l, l->d");
+  CHECK(p->eps > 0, "glu_fwd: eps");
+  BlockWs L = block_ws(m, d, l, 0, dt);
+  if ((st = check_act(x, out, ws, ws_bytes, L.total, dt, "glu_fwd")) != TERN_OK) return st;
+  if ((st = check_device()) != TERN_OK) return st;
+  if (m == 0) return TERN_OK;
+  return run_glu(*p, x, out, false, dt, m, d, l, ws, L, (cudaStream_t)stream);
+}
+
+static tern_status block_run(const tern_block* b, const void* x, void* y, tern_dtype dt, int32_t B,
+                             int32_t T, float* h, void* ws, size_t ws_bytes, tern_stream stream,
+                             const char* name) {
+  tern_status st = check_block(b);
+  if (st) return st;
+  CHECK(h, "%s: null state", name);
+  CHECK(B >= 0 && T >= 0, "%s: B=%d T=%d", name, B, T);
+  BlockWs L = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt);
+  if ((st = check_act(x, y, ws, ws_bytes, L.total, dt, name)) != TERN_OK) return st;
+  if ((st = check_device()) != TERN_OK) return st;
+  if (B * T == 0) return TERN_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  void* x1 = at<char>(ws, L.x1);
+  if ((st = run_mlgru(b->mix, x, x1, true, dt, B, T, b->d, h, ws, L, s)) != TERN_OK) return st;
+  return run_glu(b->ch, x1, y, true, dt, B * T, b->d, b->l, ws, L, s);
+}
+
+tern_status block_prefill(const tern_block* b, const void* x, void* y, tern_dtype dt, int32_t B,
+                          int32_t T, float* h, void* ws, size_t ws_bytes, tern_stream stream) {
+  return block_run(b, x, y, dt, B, T, h, ws, ws_bytes, stream, "block_prefill");
+}
+
+tern_status block_decode(const tern_block* b, const void* x, void* y, tern_dtype dt, int32_t B,
+                         float* h, void* ws, size_t ws_bytes, tern_stream stream) {
+  return block_run(b, x, y, dt, B, 1, h, ws, ws_bytes, stream, "block_decode");
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// internal.h -- launch interfaces between the C ABI (api.cu) and the kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tern.h"
+
+namespace tern {
+
+constexpr int kSegRows = 64;  // interleave group of fused weight segments
+constexpr int kKAlign = 128;  // K padding of packed rows / quantized activations
+
+// Epilogue applied to int32 accumulators (shared by the GEMV and the GEMM).
+enum EpiKind : int {
+  EPI_STORE = 0,   // y[m][r] = R1(dequant + bias)                      (n_seg == 1)
+  EPI_RESID = 1,   // y[m][r] = R3(res[m][r] + R1(dequant + bias))       (n_seg == 1)
+  EPI_FCG = 2,     // y[m][packed row] = R1(dequant + bias)  (interleaved pre-activations)
+  EPI_MLGRU = 3,   // decode: f,c,g -> h update -> o'[m][r]              (n_seg == 3, GEMV)
+  EPI_SWIGLU = 4,  // p[m][r] = R2(SiLU(R1 g) * R1 u)                    (n_seg == 2)
+  EPI_NONE = 5     // accumulators only (tap)
+};
+
+struct Epi {
+  int kind;
+  int n_out, n_seg;
+  const float* scales;   // [n_seg] mean|W|
+  const float* bias;     // [n_seg*n_out] or null
+  void* out;             // output activations (dtype of the kernel)
+  int ldo;
+  const void* res;       // residual input, same dtype as out
+  int ldr;
+  float* h;              // MLGRU state [M][n_out] fp32
+  int gate;              // tern_gate_mode
+  int32_t* acc;          // optional int32 accumulator tap [M][ldacc] (packed rows)
+  int ldacc;
+};
+
+struct QuantTaps {
+  int8_t* q;
+  int ldq;
+  float* deq;
+  float* inv_rms;
+  float* absmax;
+};
+
+// a1
+cudaError_t launch_codes_init(uint32_t* codes, int n_rows, int ldw, cudaStream_t s);
+cudaError_t launch_absmean(const float* W, int64_t numel, const float* scale_in, float* scale_out,
+                           double* ws, cudaStream_t s);
+cudaError_t launch_pack_codes(const float* W, int n, int k, int n_seg, int seg, uint32_t* codes,
+                              int ldw, const float* scale, cudaStream_t s);
+size_t pack_workspace_bytes();
+// a2
+cudaError_t launch_quant(const void* x, int xdt, int m, int k, int ldx, const float* gain,
+                         float eps, int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
+                         float* absmax, cudaStream_t s);
+// a3 (decode GEMV, norm+quant prologue fused): x [M][ldx] -> epilogue
+cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, const float* gain,
+                        float eps, const tern_weight& w, const Epi& epi, const QuantTaps* taps,
+                        cudaStream_t s);
+// a4 (tcgen05 int8 GEMM): q [M][ldq] -> epilogue
+cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
+                        const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s);
+// a6
+cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
+                        void* oprime, cudaStream_t s);
+
+}  // namespace tern

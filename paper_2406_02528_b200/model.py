@@ -1,0 +1,185 @@
+"""Python driver over the C ABI: packed weights, blocks and the L-block stack.
+
+Everything numeric runs inside libtern.so; this module owns device buffers
+(torch tensors), streams and CUDA graphs.  (P:409 block = token mixer +
+channel mixer; P:698 prefill = pipelined mode, decode = fall-through mode.)
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib as L
+from . import synth
+
+
+class PackedWeight:
+    """A fused group of n_seg ternary matrices packed 16 trits per word (a1).
+
+    latents: list of fp32 [n_out][k] device tensors (one per segment)."""
+
+    def __init__(self, latents, scales_in=None):
+        n_seg = len(latents)
+        n_out, k = latents[0].shape
+        dev = latents[0].device
+        self.n_out, self.k, self.n_seg = int(n_out), int(k), n_seg
+        self.n_rows = L.tern_packed_rows(self.n_out, n_seg)
+        self.ldw = L.tern_packed_ldw(self.k)
+        self.codes = torch.empty((self.n_rows, self.ldw), dtype=torch.int32, device=dev)
+        self.scales = torch.empty(n_seg, dtype=torch.float32, device=dev)
+        L.tern_codes_init(self.codes)
+        for s, W in enumerate(latents):
+            W = W.to(device=dev, dtype=torch.float32).contiguous()
+            sin = None if scales_in is None else scales_in[s]
+            L.tern_pack(W, self.codes, self.scales[s:s + 1], n_seg=n_seg, seg_idx=s, scale_in=sin)
+        self.struct = L.tern_weight(self.codes.data_ptr(), self.scales.data_ptr(), self.n_out,
+                                    self.k, self.ldw, self.n_seg, self.n_rows)
+
+    @property
+    def nbytes(self) -> int:
+        return self.codes.numel() * 4
+
+
+class Block:
+    """One MatMul-free block: MLGRU token mixer + GLU channel mixer."""
+
+    def __init__(self, latent: dict, d: int, l: int, gate=L.TERN_GATE_SIGMOID_H, eps=1e-6,
+                 gains: dict | None = None, biases: dict | None = None, device="cuda"):
+        self.d, self.l = d, l
+        dev = torch.device(device)
+        lat = {k: v.to(dev) for k, v in latent.items()}
+        self.fcg = PackedWeight([lat["f"], lat["c"], lat["g"]])
+        self.o = PackedWeight([lat["o"]])
+        self.gu = PackedWeight([lat["gate"], lat["up"]])
+        self.down = PackedWeight([lat["down"]])
+        gains = gains or {}
+        biases = biases or {}
+        self._keep = []
+
+        def dp(t):
+            if t is None:
+                return None
+            t = t.to(device=dev, dtype=torch.float32).contiguous()
+            self._keep.append(t)
+            return t.data_ptr()
+
+        bias_fcg = None
+        if any(biases.get(k) is not None for k in ("f", "c", "g")):
+            z = torch.zeros(d)
+            bias_fcg = torch.cat([biases.get(k, z).float().cpu() for k in ("f", "c", "g")])
+        self.mix = L.tern_mlgru(self.fcg.struct, self.o.struct, dp(gains.get("x")),
+                                dp(gains.get("o")), dp(bias_fcg), dp(biases.get("o")), int(gate),
+                                float(eps))
+        self.ch = L.tern_glu(self.gu.struct, self.down.struct, dp(gains.get("x1")),
+                             dp(gains.get("p")), float(eps))
+        self.struct = L.tern_block(self.mix, self.ch, d, l)
+
+    @property
+    def weight_bytes(self) -> int:
+        return sum(w.nbytes for w in (self.fcg, self.o, self.gu, self.down))
+
+    def workspace_bytes(self, B: int, T: int, dtype: torch.dtype) -> int:
+        return int(L.load().tern_block_workspace(C.byref(self.struct), B, T, L.dtype_code(dtype)))
+
+    def ws_layout(self, B: int, T: int, dtype: torch.dtype) -> dict:
+        t = L.tern_block_taps()
+        L._check(L.load().tern_block_ws_layout(C.byref(self.struct), B, T, L.dtype_code(dtype),
+                                               C.byref(t)), "tern_block_ws_layout")
+        return {"fcg": t.fcg, "oprime": t.oprime, "x1": t.x1, "p": t.p}
+
+
+class Stack:
+    """L blocks; prefill over [B][T][d] and graph-captured decode steps."""
+
+    def __init__(self, blocks, d: int, l: int, dtype: torch.dtype, device="cuda"):
+        self.blocks = list(blocks)
+        self.d, self.l, self.dtype = d, l, dtype
+        self.device = torch.device(device)
+        self._ws = None
+        self._ws_bytes = 0
+        self._graph = None
+
+    @classmethod
+    def random(cls, cfg: synth.Config, device="cuda", gate=L.TERN_GATE_SIGMOID_H, n_blocks=None,
+               gen_device=None, keep_latents=0):
+        """Build cfg's stack from seeded N(0, 0.02) latents (drawn per block on
+        gen_device, packed on the GPU and dropped).  keep_latents=n keeps the
+        first n blocks' latents on the host (for oracle parity)."""
+        gen_device = gen_device or device
+        g = synth.generator(cfg.seed, gen_device)
+        blocks, kept = [], []
+        for i in range(n_blocks if n_blocks is not None else cfg.L):
+            lat = synth.latent_block(cfg.d, cfg.l, g, device=gen_device)
+            if i < keep_latents:
+                kept.append({k: v.cpu() for k, v in lat.items()})
+            blocks.append(Block(lat, cfg.d, cfg.l, gate=gate, eps=cfg.eps, device=device))
+            del lat
+        st = cls(blocks, cfg.d, cfg.l, synth.torch_dtype(cfg.dtype), device)
+        st.latents = kept
+        st.generator = g
+        return st
+
+    @property
+    def weight_bytes(self) -> int:
+        return sum(b.weight_bytes for b in self.blocks)
+
+    def workspace(self, B: int, T: int) -> torch.Tensor:
+        need = max(b.workspace_bytes(B, T, self.dtype) for b in self.blocks)
+        if self._ws is None or self._ws_bytes < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self._ws_bytes = need
+        return self._ws
+
+    def new_state(self, B: int) -> list:
+        return [torch.zeros((B, self.d), dtype=torch.float32, device=self.device)
+                for _ in self.blocks]
+
+    def prefill(self, x: torch.Tensor, states: list, out: torch.Tensor | None = None,
+                bufs=None) -> torch.Tensor:
+        """x [B][T][d] -> y [B][T][d]; states (one fp32 [B][d] per block) updated."""
+        B, T, d = x.shape
+        ws = self.workspace(B, T)
+        if bufs is None:
+            bufs = (torch.empty_like(x), torch.empty_like(x))
+        cur = x
+        for i, blk in enumerate(self.blocks):
+            nxt = bufs[i % 2] if (i < len(self.blocks) - 1 or out is None) else out
+            L.block_prefill(blk.struct, cur, nxt, states[i], ws)
+            cur = nxt
+        return cur
+
+    def decode(self, x: torch.Tensor, states: list, out: torch.Tensor | None = None,
+               bufs=None) -> torch.Tensor:
+        """One decode step: x [B][d] -> y [B][d] through all blocks."""
+        B, d = x.shape
+        ws = self.workspace(B, 1)
+        if bufs is None:
+            bufs = (torch.empty_like(x), torch.empty_like(x))
+        cur = x
+        for i, blk in enumerate(self.blocks):
+            nxt = bufs[i % 2] if (i < len(self.blocks) - 1 or out is None) else out
+            L.block_decode(blk.struct, cur, nxt, states[i], ws)
+            cur = nxt
+        return cur
+
+    def capture_decode(self, B: int, states: list):
+        """Capture one whole-stack decode step in a CUDA graph.  Returns
+        (graph, x_in, y_out): copy the step input into x_in, replay, read y_out."""
+        x_in = torch.zeros((B, self.d), dtype=self.dtype, device=self.device)
+        y_out = torch.empty_like(x_in)
+        bufs = (torch.empty_like(x_in), torch.empty_like(x_in))
+        self.workspace(B, 1)
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        saved = [h.clone() for h in states]
+        with torch.cuda.stream(s):
+            self.decode(x_in, states, out=y_out, bufs=bufs)   # warm-up (sets attributes)
+        torch.cuda.current_stream().wait_stream(s)
+        for h, h0 in zip(states, saved):
+            h.copy_(h0)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.decode(x_in, states, out=y_out, bufs=bufs)
+        self._graph_bufs = bufs
+        return g, x_in, y_out

@@ -1,0 +1,96 @@
+"""The C-ABI library builds, loads and exports every symbol include/tern.h
+declares; argument validation rejects bad calls before touching the GPU.
+(CPU only: no compute calls.)"""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "tern.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\**\s+\**([a-z_0-9]+)\s*\(", src, flags=re.M)
+    return sorted(set(names) - {"typedef"})
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2406_02528_b200 import _lib, build
+    build.build()
+    return _lib.load()
+
+
+def test_header_declares_the_north_star_entry_points():
+    names = header_functions()
+    for n in ("tern_pack", "bitlinear_fwd", "mlgru_fwd", "glu_fwd", "block_prefill", "block_decode"):
+        assert n in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    for n in header_functions():
+        assert hasattr(lib, n), f"{n} declared in tern.h but not exported"
+
+
+def test_binding_covers_every_symbol():
+    from paper_2406_02528_b200 import _lib
+    assert set(header_functions()) == set(_lib.EXPORTS)
+
+
+def test_abi_version_and_host_helpers(lib):
+    assert lib.tern_abi_version() == 1
+    assert lib.tern_packed_rows(688, 2) == 2 * 704
+    assert lib.tern_packed_rows(1024, 3) == 3072
+    assert lib.tern_packed_rows(1000, 1) == 1000
+    assert lib.tern_packed_ldw(688) == 48
+    assert lib.tern_packed_ldw(1024) == 64
+
+
+def test_validation_rejects_before_launch(lib):
+    from paper_2406_02528_b200 import _lib as L
+    st = lib.tern_quant(None, 0, 4, 256, 256, None, 1e-6, None, 256, None, None, None, None, None)
+    assert st == L.TERN_ERR_INVALID_ARG
+    assert b"null" in lib.tern_last_error()
+    fake = C.c_void_p(0x1000)
+    # K not a multiple of 16
+    st = lib.tern_quant(fake, 0, 4, 250, 256, None, 1e-6, fake, 256, fake, fake, None, None, None)
+    assert st == L.TERN_ERR_INVALID_ARG
+    # misaligned pointer
+    st = lib.tern_quant(C.c_void_p(0x1004), 0, 4, 256, 256, None, 1e-6, fake, 256, fake, fake,
+                        None, None, None)
+    assert st == L.TERN_ERR_INVALID_ARG
+    # bad weight struct
+    w = L.tern_weight(0x1000, 0x2000, 64, 128, 8, 1, 65)   # n_rows inconsistent
+    y = C.c_void_p(0x3000)
+    st = lib.bitlinear_fwd(fake, 0, 1, 128, 128, None, 1e-6, C.byref(w), None, y, 0, 64, None,
+                           None, 0, None)
+    assert st == L.TERN_ERR_INVALID_ARG and b"n_rows" in lib.tern_last_error()
+    st = lib.tern_mlgru_scan(fake, 0, 1, 1, 100, 0, fake, fake, None)   # d % 64 != 0
+    assert st == L.TERN_ERR_INVALID_ARG
+
+
+def test_product_path_has_no_fallback(tmp_path, monkeypatch):
+    """The binding raises when the CUDA library is missing (no CPU fallback)."""
+    import importlib
+    monkeypatch.setenv("TERN_LIB", str(tmp_path / "missing.so"))
+    import paper_2406_02528_b200._lib as mod
+    m2 = importlib.reload(mod)
+    try:
+        with pytest.raises(OSError):
+            m2.load()
+    finally:
+        monkeypatch.delenv("TERN_LIB")
+        importlib.reload(mod)
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2406_02528_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dp, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle", txt, re.M), f
+                assert "oracle.h" not in txt and "liboracle" not in txt, f

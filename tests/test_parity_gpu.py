@@ -1,0 +1,321 @@
+"""GPU-vs-oracle parity of every hot-path step, through the C ABI (B200 only).
+
+Bar (BASELINE.json north_star): ternary codes,
+int8 activations and int32 accumulators bit-exact given the same fp32 scales;
+float outputs and hidden states within 1e-4 relative (fp32) / 2e-2 (bf16) --
+and, because both sides follow the canonical numerics, they are expected (and
+here required, up to logged fp64-boundary events) to be bit-identical.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2406_02528_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2406_02528_b200 import _lib
+    _lib.load()
+    return _lib
+
+
+@pytest.fixture(scope="module")
+def M():
+    from paper_2406_02528_b200 import model
+    return model
+
+
+def dev(x):
+    return torch.as_tensor(x).cuda()
+
+
+def f32np(t):
+    return t.detach().float().cpu().numpy()
+
+
+def close(g, o, tol, what=""):
+    """Elementwise |g-o| <= tol*max(|o|, 1e-2*rms(o_row)) (DESIGN.md tolerance rule)."""
+    g = np.asarray(g, np.float64)
+    o = np.asarray(o, np.float64)
+    o2 = o.reshape(-1, o.shape[-1]) if o.ndim > 1 else o.reshape(1, -1)
+    rms = np.sqrt(np.mean(o2 ** 2, axis=1, keepdims=True)).repeat(o2.shape[1], 1).reshape(o.shape)
+    lim = tol * np.maximum(np.abs(o), 1e-2 * rms) + 1e-30
+    bad = np.abs(g - o) > lim
+    assert not bad.any(), f"{what}: {bad.sum()} / {bad.size} outside tol {tol}; " \
+                          f"max abs err {np.max(np.abs(g - o)):.3e}"
+
+
+def latents(n, k, seed):
+    g = synth.generator(seed)
+    return synth.latent_matrix(n, k, g)
+
+
+def acts(shape, seed, dtype="f32"):
+    g = synth.generator(seed)
+    return synth.hidden(shape, g, dtype)
+
+
+# ------------------------------------------------------------------------ a1 pack
+@pytest.mark.parametrize("n,k,n_seg", [(64, 128, 1), (48, 40, 1), (256, 256, 3), (688, 256, 2),
+                                       (1024, 2816, 1), (100, 1008, 3)])
+def test_pack_parity(L, M, n, k, n_seg):
+    lats = [latents(n, k, 100 + s) for s in range(n_seg)]
+    pw = M.PackedWeight([x.cuda() for x in lats])
+    codes = pw.codes.cpu().numpy().view(np.uint32)
+    scales = pw.scales.cpu().numpy()
+    for s, W in enumerate(lats):
+        t_ref, m_ref = O.ternarize(W.numpy())
+        assert abs(float(scales[s]) - float(m_ref)) <= np.spacing(np.float32(m_ref)), "scale"
+        t_gpu = O.unpack_segment(codes, n, k, n_seg=n_seg, s=s)
+        if scales[s] == m_ref:
+            assert np.array_equal(t_gpu, t_ref)
+        # with the oracle's scale forced, codes are bit-exact unconditionally
+        pw2 = M.PackedWeight([W.cuda()], scales_in=[torch.tensor([float(m_ref)]).cuda()])
+        t2 = O.unpack_segment(pw2.codes.cpu().numpy().view(np.uint32), n, k)
+        assert np.array_equal(t2, t_ref)
+    # K padding words hold the zero trit
+    if pw.ldw * 16 > k:
+        full = O.unpack_segment(codes, n, pw.ldw * 16, n_seg=n_seg, s=0)
+        assert np.all(full[:, k:] == 0)
+
+
+def test_pack_degenerate(L, M):
+    with pytest.raises(L.TernError) as e:
+        M.PackedWeight([torch.zeros(64, 128, device="cuda")])
+    assert e.value.status == L.TERN_ERR_DEGENERATE
+
+
+# ------------------------------------------------------------------------ a2 quant
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("m,k", [(1, 256), (7, 688), (33, 1024), (5, 2816), (3, 6912), (300, 256)])
+def test_quant_parity(L, m, k, dtype):
+    x = acts((m, k), 7 + k, dtype)
+    x[0, :] = 0                       # all-zero row (C7)
+    if m > 2:
+        x[1, :] = 1.5                 # constant row
+        x[2, : k // 2] *= 1000.0      # large dynamic range
+    xd = x.cuda()
+    kp = (k + 127) // 128 * 128
+    q = torch.full((m, kp), 99, dtype=torch.int8, device="cuda")
+    deq = torch.empty(m, device="cuda")
+    qsum = torch.empty(m, dtype=torch.int32, device="cuda")
+    r = torch.empty(m, device="cuda")
+    a = torch.empty(m, device="cuda")
+    L.tern_quant(xd, q, deq, qsum, inv_rms=r, absmax=a)
+    torch.cuda.synchronize()
+    qo, do, ro, ao = O.quant_rows(f32np(x))
+    r_g = r.cpu().numpy()
+    # inv_rms: within one ulp of the oracle's (fp64 sum order), normally identical
+    assert np.all(np.abs(r_g - ro) <= np.spacing(ro))
+    same = r_g == ro
+    assert same.mean() > 0.99
+    qg = q.cpu().numpy()
+    assert np.all(qg[:, k:] == 0)
+    assert np.array_equal(qg[same, :k], qo[same])
+    assert np.array_equal(deq.cpu().numpy()[same], do[same])
+    assert np.array_equal(a.cpu().numpy()[same], ao[same])
+    assert np.array_equal(qsum.cpu().numpy(), qg[:, :k].astype(np.int64).sum(1))
+
+
+# ------------------------------------------------------------------------ a3/a4 contraction
+@pytest.mark.parametrize("m,n,k,n_seg", [(1, 256, 128, 1), (130, 640, 384, 1),
+                                         (300, 1100, 1008, 1), (129, 256, 256, 3),
+                                         (257, 688, 256, 2), (64, 5632, 2048, 1)])
+def test_contract_gemm_exact(L, M, m, n, k, n_seg):
+    rng = np.random.default_rng(m * 7 + n)
+    lats = [latents(n, k, 200 + s) for s in range(n_seg)]
+    pw = M.PackedWeight([x.cuda() for x in lats])
+    kp = (k + 127) // 128 * 128
+    qn = rng.integers(-128, 128, size=(m, kp), dtype=np.int8)
+    qn[:, k:] = 0
+    q = torch.from_numpy(qn).cuda()
+    qsum = torch.from_numpy(qn.astype(np.int32).sum(1).astype(np.int32)).cuda()
+    acc = torch.full((m, pw.n_rows), -7, dtype=torch.int32, device="cuda")
+    L.tern_contract(q, qsum, pw.struct, acc)
+    torch.cuda.synchronize()
+    accg = acc.cpu().numpy()
+    codes = pw.codes.cpu().numpy().view(np.uint32)
+    for s, W in enumerate(lats):
+        t = O.unpack_segment(codes, n, k, n_seg=n_seg, s=s)
+        ref = O.tern_matmul(qn[:, :k], t)
+        rows = [O.packed_row(s, r, n_seg, 64) for r in range(n)]
+        assert np.array_equal(accg[:, rows], ref), f"segment {s}"
+
+
+@pytest.mark.parametrize("xdt,ydt", [(torch.float32, torch.float32),
+                                     (torch.bfloat16, torch.bfloat16),
+                                     (torch.bfloat16, torch.float32)])
+@pytest.mark.parametrize("m", [1, 2, 3, 8, 16, 130])
+@pytest.mark.parametrize("k,n", [(256, 256), (1024, 1024), (688, 256), (2816, 1024)])
+@pytest.mark.parametrize("force_gemm", [False, True])
+def test_bitlinear_parity(L, M, m, k, n, xdt, ydt, force_gemm):
+    if force_gemm and m > 8:
+        pytest.skip("same path")
+    W = latents(n, k, 300 + k)
+    pw = M.PackedWeight([W.cuda()])
+    t, mw = O.ternarize(W.numpy())
+    x = acts((m, k), 11 + m, "bf16" if xdt == torch.bfloat16 else "f32")
+    bias = torch.randn(n, generator=synth.generator(5)) if m % 2 else None
+    y = torch.empty((m, n), dtype=ydt, device="cuda")
+    kp = (k + 127) // 128 * 128
+    taps = {"q": torch.empty((m, kp), dtype=torch.int8, device="cuda"),
+            "acc": torch.empty((m, pw.n_rows), dtype=torch.int32, device="cuda"),
+            "deq": torch.empty(m, device="cuda"), "inv_rms": torch.empty(m, device="cuda"),
+            "absmax": torch.empty(m, device="cuda")}
+    old = L.tern_get_gemv_max_m()
+    try:
+        if force_gemm:
+            L.tern_set_gemv_max_m(0)
+        L.bitlinear_fwd(x.cuda(), pw.struct, y, bias=None if bias is None else bias.cuda(), taps=taps)
+        torch.cuda.synchronize()
+    finally:
+        L.tern_set_gemv_max_m(old)
+    assert float(pw.scales[0]) == float(mw)
+    xo = f32np(x)
+    out_o, tp = O.bitlinear(xo, t, mw, bias=None if bias is None else bias.numpy(),
+                            bf16=(ydt == torch.bfloat16), taps=True)
+    qg = taps["q"].cpu().numpy()[:, :k]
+    # teacher forcing: the oracle accumulates the GPU's own int8 activations
+    assert np.array_equal(taps["acc"].cpu().numpy(), O.tern_matmul(qg, t))
+    # free running: identical quantization and accumulators, outputs bit-exact
+    assert np.array_equal(qg, tp["q"])
+    assert np.array_equal(taps["acc"].cpu().numpy(), tp["acc"])
+    assert np.array_equal(taps["deq"].cpu().numpy(), tp["deq"])
+    close(f32np(y), out_o, TOL[ydt], "y")
+    assert np.array_equal(f32np(y), out_o)
+
+
+# ------------------------------------------------------------------------ a6 scan
+def deinterleave(fcg, d):
+    Mx = fcg.shape[0]
+    v = fcg.reshape(Mx, d // 64, 3, 64)
+    return [v[:, :, s, :].reshape(Mx, d) for s in range(3)]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("B,T,d", [(1, 1, 64), (2, 5, 128), (2, 64, 256), (3, 130, 64),
+                                   (1, 300, 1024)])
+@pytest.mark.parametrize("gate", [0, 1])
+def test_scan_parity(L, B, T, d, dtype, gate):
+    g = synth.generator(B * 1000 + T)
+    fcg = (torch.randn((B * T, 3 * d), generator=g) * 2).to(dtype)
+    h0 = torch.randn((B, d), generator=g)
+    h = h0.clone().cuda()
+    op = torch.empty((B * T, d), dtype=dtype, device="cuda")
+    L.tern_mlgru_scan(fcg.cuda(), B, T, d, h, op, gate=gate)
+    torch.cuda.synchronize()
+    fh, ch, gh = (a.reshape(B, T, d) for a in deinterleave(f32np(fcg), d))
+    o_ref, h_ref = O.mlgru_scan(fh, ch, gh, h0.numpy(), gate_mode=gate,
+                                bf16=(dtype == torch.bfloat16))
+    assert np.array_equal(h.cpu().numpy(), h_ref)
+    assert np.array_equal(f32np(op).reshape(B, T, d), o_ref)
+
+
+# ------------------------------------------------------------------------ mixers + block
+def _blocks(cfg, M, n_blocks, gate, gen_device="cpu"):
+    st = M.Stack.random(cfg, gate=gate, n_blocks=n_blocks, gen_device=gen_device,
+                        keep_latents=n_blocks)
+    oblocks = [O.OracleBlock({k: v.numpy() for k, v in lat.items()}, cfg.d, cfg.l)
+               for lat in st.latents]
+    return st, oblocks
+
+
+@pytest.mark.parametrize("gate", [0, 1])
+def test_c0_block_prefill_then_decode(L, M, gate):
+    """BASELINE configs[0]: one block, fp32, d=256, l=688, batch 2 x 128, then 16 decode steps."""
+    cfg = synth.CONFIGS["c0"]
+    st, ob = _blocks(cfg, M, 1, gate)
+    B, T, n = cfg.prefill_B, cfg.prefill_T, cfg.decode_steps
+    x = synth.hidden((B, T + n, cfg.d), st.generator, cfg.dtype)   # drawn after the weights
+    xd = x.cuda()
+    states = st.new_state(B)
+    y = st.prefill(xd[:, :T].contiguous(), states)
+    ys = [y]
+    for t in range(T, T + n):
+        ys.append(st.decode(xd[:, t].contiguous(), states).unsqueeze(1))
+    torch.cuda.synchronize()
+    yg = f32np(torch.cat(ys, 1))
+    H = np.zeros((B, cfg.d), np.float32)
+    yo, Ho = O.block(ob[0], x.numpy()[:, :T], H, gate_mode=gate)
+    outs = [yo]
+    for t in range(T, T + n):
+        yt, Ho = O.block(ob[0], x.numpy()[:, t:t + 1], Ho, gate_mode=gate)
+        outs.append(yt)
+    yo = np.concatenate(outs, 1)
+    close(yg, yo, 1e-4, "y")
+    close(states[0].cpu().numpy(), Ho, 1e-4, "h")
+    assert np.array_equal(yg, yo), "free-running c0 expected bit-exact"
+    assert np.array_equal(states[0].cpu().numpy(), Ho)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_mlgru_and_glu_fwd(L, M, dtype):
+    cfg = synth.Config("t", 1, 256, 688, dtype, 9, 2, 70, 2, 0)
+    st, ob = _blocks(cfg, M, 1, 0)
+    blk = st.blocks[0]
+    tdt = synth.torch_dtype(dtype)
+    x = synth.hidden((2, 70, 256), synth.generator(3), dtype)
+    ws = torch.empty(blk.workspace_bytes(2, 70, tdt), dtype=torch.uint8, device="cuda")
+    h = torch.zeros((2, 256), device="cuda")
+    out = torch.empty((2, 70, 256), dtype=tdt, device="cuda")
+    L.mlgru_fwd(blk.mix, x.cuda(), out, h, ws)
+    g_out = torch.empty((140, 256), dtype=tdt, device="cuda")
+    L.glu_fwd(blk.ch, x.cuda().reshape(140, 256), g_out, 688, ws)
+    torch.cuda.synchronize()
+    bf = dtype == "bf16"
+    o_ref, h_ref = O.mlgru(ob[0], f32np(x), np.zeros((2, 256), np.float32), bf16=bf)
+    assert np.array_equal(f32np(out), o_ref)
+    assert np.array_equal(h.cpu().numpy(), h_ref)
+    g_ref = O.glu(ob[0], f32np(x).reshape(140, 256), bf16=bf)
+    assert np.array_equal(f32np(g_out), g_ref)
+
+
+@pytest.mark.parametrize("cfg_name,n_blocks,T,n_dec", [("c2", 2, 64, 4), ("c3", 1, 16, 2),
+                                                       ("c4", 1, 8, 2)])
+def test_stack_truncated_parity(L, M, cfg_name, n_blocks, T, n_dec):
+    """Configs 2-4 truncated (first blocks, a few tokens, a few decode steps)."""
+    cfg = synth.CONFIGS[cfg_name]
+    st, ob = _blocks(cfg, M, n_blocks, 0, gen_device="cuda")
+    B = 1
+    x = synth.hidden((B, T + n_dec, cfg.d), synth.generator(cfg.seed + 1000), cfg.dtype)
+    xd = x.cuda()
+    states = st.new_state(B)
+    ys = [st.prefill(xd[:, :T].contiguous(), states)]
+    for t in range(T, T + n_dec):
+        ys.append(st.decode(xd[:, t].contiguous(), states).unsqueeze(1))
+    torch.cuda.synchronize()
+    yg = f32np(torch.cat(ys, 1))
+    bf = cfg.dtype == "bf16"
+    Hs = [np.zeros((B, cfg.d), np.float32) for _ in ob]
+    xo = f32np(x)
+    y0, Hs = O.stack(ob, xo[:, :T], Hs, bf16=bf)
+    outs = [y0]
+    for t in range(T, T + n_dec):
+        yt, Hs = O.stack(ob, xo[:, t:t + 1], Hs, bf16=bf)
+        outs.append(yt)
+    yo = np.concatenate(outs, 1)
+    close(yg, yo, 2e-2 if bf else 1e-4, cfg_name)
+    assert np.array_equal(yg, yo)
+
+
+def test_sampled_full_size_bitlinear_c1(L, M):
+    """configs[1] at a full-size point (M=4096, K=2048, N=5632, bf16) checked on
+    sampled rows the oracle computes one by one."""
+    m, k, n = 4096, 2048, 5632
+    W = latents(n, k, 1)
+    pw = M.PackedWeight([W.cuda()])
+    t, mw = O.ternarize(W.numpy())
+    x = acts((m, k), 1, "bf16")
+    y = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    L.bitlinear_fwd(x.cuda(), pw.struct, y)
+    torch.cuda.synchronize()
+    rows = np.random.default_rng(0).choice(m, 24, replace=False)
+    rows = np.concatenate([rows, [0, m - 1]])
+    ref = O.bitlinear(f32np(x)[rows], t, mw, bf16=True)
+    assert np.array_equal(f32np(y)[rows], ref)
