@@ -236,6 +236,28 @@ tern_status block_prefill(const tern_block* b, const void* x, void* y, tern_dtyp
 tern_status block_decode(const tern_block* b, const void* x, void* y, tern_dtype dt, int32_t B,
                          float* h, void* ws, size_t ws_bytes, tern_stream stream);
 
+/* ------------------------------------------------------------------------
+ * Measurement hooks (bench.py roofline): while enabled, every kernel launch
+ * made by this library on a non-capturing stream is bracketed by two CUDA
+ * events recorded on that same stream, with its shape.  tern_profile_collect
+ * synchronises those events, copies up to `max` records into `out` (host
+ * array; NULL just counts) and returns the number of records; records are
+ * kept until the next tern_profile_enable(1).  Not for use in production.
+ * ------------------------------------------------------------------------ */
+typedef enum { TERN_K_QUANT = 0, TERN_K_GEMV = 1, TERN_K_GEMM = 2, TERN_K_SCAN = 3 } tern_kernel_id;
+typedef struct {
+  int32_t kernel;   /* tern_kernel_id                                        */
+  int32_t epi;      /* epilogue kind (GEMV/GEMM) or gate mode (scan)         */
+  int32_t m;        /* rows (tokens); scan: B*T                              */
+  int32_t n;        /* GEMV/GEMM: packed weight rows; scan: d; quant: 0      */
+  int32_t k;        /* input features                                        */
+  int32_t n_seg;    /* weight segments                                       */
+  int32_t dtype;    /* activation dtype (tern_dtype)                         */
+  float ms;         /* elapsed device time between the two events            */
+} tern_prof_rec;
+void tern_profile_enable(int32_t on);
+int32_t tern_profile_collect(tern_prof_rec* out, int32_t max);
+
 /* Tuning knob (host): largest m sent to the decode GEMV (default 8, max 8;
  * 0 forces the tensor-core path everywhere).  Not thread-safe to change
  * while calls are in flight. */

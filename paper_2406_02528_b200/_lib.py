@@ -56,6 +56,13 @@ class tern_block_taps(C.Structure):
                 ("p", C.c_size_t)]
 
 
+class tern_prof_rec(C.Structure):
+    _fields_ = [("kernel", C.c_int32), ("epi", C.c_int32), ("m", C.c_int32), ("n", C.c_int32),
+                ("k", C.c_int32), ("n_seg", C.c_int32), ("dtype", C.c_int32), ("ms", C.c_float)]
+
+
+KERNEL_NAMES = {0: "quant", 1: "gemv", 2: "gemm_tc", 3: "scan"}
+
 P = C.c_void_p
 I32 = C.c_int32
 SZ = C.c_size_t
@@ -83,6 +90,8 @@ _SIGS = {
     "glu_fwd": (C.c_int, [C.POINTER(tern_glu), P, P, C.c_int, I32, I32, I32, P, SZ, P]),
     "block_prefill": (C.c_int, [C.POINTER(tern_block), P, P, C.c_int, I32, I32, P, P, SZ, P]),
     "block_decode": (C.c_int, [C.POINTER(tern_block), P, P, C.c_int, I32, P, P, SZ, P]),
+    "tern_profile_enable": (None, [I32]),
+    "tern_profile_collect": (I32, [C.POINTER(tern_prof_rec), I32]),
     "tern_set_gemv_max_m": (None, [I32]),
     "tern_get_gemv_max_m": (I32, []),
 }
@@ -226,3 +235,20 @@ def tern_set_gemv_max_m(m: int):
 
 def tern_get_gemv_max_m() -> int:
     return int(load().tern_get_gemv_max_m())
+
+
+def tern_profile_enable(on: bool):
+    load().tern_profile_enable(1 if on else 0)
+
+
+def tern_profile_collect() -> list:
+    """Per-launch records [(kernel name, dict(meta), ms)] of the library's kernels."""
+    Lb = load()
+    n = int(Lb.tern_profile_collect(None, 0))
+    arr = (tern_prof_rec * max(n, 1))()
+    n = int(Lb.tern_profile_collect(arr, n))
+    out = []
+    for r in arr[:n]:
+        out.append({"kernel": KERNEL_NAMES.get(r.kernel, str(r.kernel)), "epi": r.epi, "m": r.m,
+                    "n": r.n, "k": r.k, "n_seg": r.n_seg, "dtype": r.dtype, "ms": float(r.ms)})
+    return out

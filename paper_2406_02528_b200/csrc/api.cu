@@ -7,6 +7,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "internal.h"
 
@@ -81,6 +82,50 @@ tern_status check_weight(const tern_weight* w, int k, int n_seg, const char* nam
   return TERN_OK;
 }
 
+// ----------------------------------------------------------------- profiling hooks
+struct ProfRec {
+  cudaEvent_t a, b;
+  tern_prof_rec meta;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_ev_pool;
+
+cudaEvent_t prof_event() {
+  if (!g_ev_pool.empty()) {
+    cudaEvent_t e = g_ev_pool.back();
+    g_ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII: records an event before and after the launches in its scope.
+struct Prof {
+  bool on = false;
+  ProfRec r{};
+  cudaStream_t s;
+  Prof(int kernel, int epi, int m, int n, int k, int n_seg, int dtype, cudaStream_t st) : s(st) {
+    if (!g_prof_on) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    r.a = prof_event();
+    r.b = prof_event();
+    r.meta = tern_prof_rec{kernel, epi, m, n, k, n_seg, dtype, 0.0f};
+    on = r.a && r.b && cudaEventRecord(r.a, st) == cudaSuccess;
+  }
+  ~Prof() {
+    if (!on) return;
+    cudaEventRecord(r.b, s);
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof.push_back(r);
+  }
+};
+
 Epi make_epi(int kind, const tern_weight& w, const float* bias, void* out, int ldo) {
   Epi e{};
   e.kind = kind;
@@ -120,8 +165,12 @@ tern_status bl_tc(const void* x, tern_dtype xdt, int M, int K, int ldx, const fl
                   float eps, const tern_weight& w, tern_dtype ydt, const Epi& epi, int8_t* q,
                   int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
                   cudaStream_t s) {
-  TRY_CUDA(launch_quant(x, xdt, M, K, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s),
-           "quant");
+  {
+    Prof p(TERN_K_QUANT, 0, M, 0, K, 0, xdt, s);
+    TRY_CUDA(launch_quant(x, xdt, M, K, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s),
+             "quant");
+  }
+  Prof p(TERN_K_GEMM, epi.kind, M, w.n_rows, w.k, w.n_seg, ydt, s);
   TRY_CUDA(launch_gemm(q, M, ldq, deq, qsum, w, ydt, epi, s), "gemm");
   return TERN_OK;
 }
@@ -148,6 +197,34 @@ tern_status check_block(const tern_block* b) {
 extern "C" {
 
 int tern_abi_version(void) { return TERN_ABI_VERSION; }
+
+void tern_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (on) {
+    for (auto& r : g_prof) {
+      g_ev_pool.push_back(r.a);
+      g_ev_pool.push_back(r.b);
+    }
+    g_prof.clear();
+  }
+  g_prof_on = on != 0;
+}
+
+int32_t tern_profile_collect(tern_prof_rec* out, int32_t max) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  int32_t n = 0;
+  for (auto& r : g_prof) {
+    if (out && n < max) {
+      cudaEventSynchronize(r.b);
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, r.a, r.b);
+      out[n] = r.meta;
+      out[n].ms = ms;
+    }
+    ++n;
+  }
+  return out ? (n < max ? n : max) : n;
+}
 const char* tern_last_error(void) { return g_err.c_str(); }
 void tern_set_gemv_max_m(int32_t m) { g_gemv_max_m = m < 0 ? 0 : (m > 8 ? 8 : m); }
 int32_t tern_get_gemv_max_m(void) { return g_gemv_max_m; }
@@ -259,6 +336,7 @@ tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, i
       qt.q = taps->q; qt.ldq = taps->ldq; qt.deq = taps->deq;
       qt.inv_rms = taps->inv_rms; qt.absmax = taps->absmax;
     }
+    Prof pr(TERN_K_GEMV, e.kind, m, w->n_rows, k, 1, xdt, s);
     TRY_CUDA(launch_gemv(x, xdt, ydt, m, k, ldx, gain, eps, *w, e, &qt, s), "gemv");
     return TERN_OK;
   }
@@ -298,6 +376,7 @@ tern_status tern_mlgru_scan(const void* fcg, tern_dtype dt, int32_t B, int32_t T
   CHECK(gate == TERN_GATE_SIGMOID_H || gate == TERN_GATE_LINEAR_H, "tern_mlgru_scan: gate");
   tern_status st = check_device();
   if (st) return st;
+  Prof pr(TERN_K_SCAN, gate, B * T, d, d, 3, dt, (cudaStream_t)stream);
   TRY_CUDA(launch_scan(fcg, dt, B, T, d, gate, h, oprime, (cudaStream_t)stream), "scan");
   return TERN_OK;
 }
@@ -337,10 +416,14 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
     Epi e1 = make_epi(EPI_MLGRU, p.fcg, p.bias_fcg, op, d);
     e1.h = h;
     e1.gate = p.gate;
-    TRY_CUDA(launch_gemv(x, dt, dt, B, d, d, p.gain_x, p.eps, p.fcg, e1, nullptr, s), "gemv fcg");
+    {
+      Prof pr(TERN_K_GEMV, e1.kind, B, p.fcg.n_rows, d, 3, dt, s);
+      TRY_CUDA(launch_gemv(x, dt, dt, B, d, d, p.gain_x, p.eps, p.fcg, e1, nullptr, s), "gemv fcg");
+    }
     Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.o, p.bias_o, out, d);
     e2.res = x;
     e2.ldr = d;
+    Prof pr(TERN_K_GEMV, e2.kind, B, p.o.n_rows, d, 1, dt, s);
     TRY_CUDA(launch_gemv(op, dt, dt, B, d, d, p.gain_o, p.eps, p.o, e2, nullptr, s), "gemv o");
     return TERN_OK;
   }
@@ -353,7 +436,10 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
                          nullptr, nullptr, s);
   if (st) return st;
-  TRY_CUDA(launch_scan(fcg, dt, B, T, d, p.gate, h, op, s), "scan");
+  {
+    Prof pr(TERN_K_SCAN, p.gate, B * T, d, d, 3, dt, s);
+    TRY_CUDA(launch_scan(fcg, dt, B, T, d, p.gate, h, op, s), "scan");
+  }
   Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.o, p.bias_o, out, d);
   e2.res = x;
   e2.ldr = d;
@@ -370,7 +456,11 @@ tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, ter
   e2.res = x;
   e2.ldr = d;
   if (M <= g_gemv_max_m) {
-    TRY_CUDA(launch_gemv(x, dt, dt, M, d, d, p.gain_x, p.eps, p.gu, e1, nullptr, s), "gemv gu");
+    {
+      Prof pr(TERN_K_GEMV, e1.kind, M, p.gu.n_rows, d, 2, dt, s);
+      TRY_CUDA(launch_gemv(x, dt, dt, M, d, d, p.gain_x, p.eps, p.gu, e1, nullptr, s), "gemv gu");
+    }
+    Prof pr(TERN_K_GEMV, e2.kind, M, p.down.n_rows, l, 1, dt, s);
     TRY_CUDA(launch_gemv(pp, dt, dt, M, l, l, p.gain_p, p.eps, p.down, e2, nullptr, s),
              "gemv down");
     return TERN_OK;

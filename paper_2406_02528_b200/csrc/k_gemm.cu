@@ -20,46 +20,164 @@ namespace tern {
 constexpr int kBM = 128;
 constexpr int kBK = 128;  // int8 elements = bytes = one 128B swizzle row
 
+// Warp roles (448 threads):
+//   warp 0       TMA producer            warp 1      TMEM alloc + MMA issuer
+//   warps 2-5    B unpack (128 thr)      warps 6-13  epilogue (256 thr, 2 per TMEM quadrant)
+// Persistent: grid = min(#tiles, #SMs), static round-robin over tiles (m-major
+// so CTAs running together share A rows in L2).  Two TMEM accumulators of BN
+// columns let the epilogue of tile i overlap the main loop of tile i+1.
+constexpr int kGemmThreads = 448;
+constexpr int kEpiWarp0 = 6;
+constexpr int kEpiWarps = 8;
+constexpr int kStageLd = 33;  // epilogue staging row stride (floats): conflict-free
+
 template <int BN> struct GemmCfg {
   static constexpr int S = BN == 256 ? 3 : 4;
   static constexpr int A_BYTES = kBM * kBK;       // 16 KB
   static constexpr int BU_BYTES = BN * kBK;       // unpacked B
   static constexpr int BP_BYTES = BN * (kBK / 4); // packed B: BN rows x 8 words
   static constexpr int STAGE = A_BYTES + BU_BYTES + BP_BYTES;
-  static constexpr int SMEM = S * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_BYTES = kEpiWarps * 32 * kStageLd * 4;
+  static constexpr int SMEM = S * STAGE + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = 2 * BN;
 };
 
 struct GemmArgs {
-  int M, n_rows, num_kb;
+  int M, n_rows, num_kb, n_tiles, m_tiles;
   const float* deq;
   const int32_t* qsum;
   Epi epi;
 };
 
+// Epilogue of one 32-column chunk held by this thread (one row): computes the
+// stored values (phase A, thread = row) into the warp's staging tile, then
+// writes it with row-contiguous coalesced stores (phase B, lane = column).
+template <typename TY>
+__device__ __forceinline__ void epi_chunk(const Epi& e, const GemmArgs& a, float* stg, int lane,
+                                          int row0, int row, float deq, int qsum, int col0,
+                                          const uint32_t (&v)[32], const uint32_t* vu) {
+  const bool rv = row < a.M;
+  const int nseg = e.n_seg;
+  int out_col0;     // first output column of the chunk
+  bool active = col0 < a.n_rows;
+  if (e.kind == EPI_SWIGLU) {
+    const int grp = col0 / 128, half = (col0 % 128) / 32;
+    out_col0 = grp * 64 + half * 32;
+    active = active && out_col0 < e.n_out;
+  } else if (e.kind == EPI_FCG || e.kind == EPI_NONE) {
+    out_col0 = col0;
+  } else {
+    out_col0 = (col0 / (kSegRows * nseg)) * kSegRows + (col0 % kSegRows);  // n_seg == 1: col0
+  }
+  if (!active) return;
+  const int seg = (col0 / kSegRows) % nseg;
+  const int rr0 = (col0 / (kSegRows * nseg)) * kSegRows + (col0 % kSegRows);
+  // ---- optional int32 accumulator tap (parity), staged the same way
+  if (e.acc) {
+    int* si = reinterpret_cast<int*>(stg);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) si[lane * kStageLd + j] = (int)v[j] - qsum;
+    if (vu) {
+      __syncwarp();
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r)
+        if (row0 + r < a.M && col0 + lane < a.n_rows)
+          e.acc[(int64_t)(row0 + r) * e.ldacc + col0 + lane] = si[r * kStageLd + lane];
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) si[lane * kStageLd + j] = (int)vu[j] - qsum;
+      __syncwarp();
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r)
+        if (row0 + r < a.M && col0 + 64 + lane < a.n_rows)
+          e.acc[(int64_t)(row0 + r) * e.ldacc + col0 + 64 + lane] = si[r * kStageLd + lane];
+    } else {
+      __syncwarp();
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r)
+        if (row0 + r < a.M && col0 + lane < a.n_rows)
+          e.acc[(int64_t)(row0 + r) * e.ldacc + col0 + lane] = si[r * kStageLd + lane];
+    }
+    __syncwarp();
+    if (e.kind == EPI_NONE) return;
+  }
+  // ---- phase A: thread = row
+  if (rv) {
+    const float sc = __fmul_rn(deq, __ldg(e.scales + seg));
+    if (e.kind == EPI_SWIGLU) {
+      const float scu = __fmul_rn(deq, __ldg(e.scales + 1));
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float g = storage_round<TY>(__fmul_rn((float)((int)v[j] - qsum), sc));
+        const float u = storage_round<TY>(__fmul_rn((float)((int)vu[j] - qsum), scu));
+        stg[lane * kStageLd + j] = swiglu(g, u);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float o = __fmul_rn((float)((int)v[j] - qsum), sc);
+        if (e.bias) o = __fadd_rn(o, __ldg(e.bias + seg * e.n_out + rr0 + j));
+        stg[lane * kStageLd + j] = storage_round<TY>(o);
+      }
+    }
+  }
+  __syncwarp();
+  // ---- phase B: lane = column, one coalesced row segment per store
+  TY* out = static_cast<TY*>(e.out);
+  const int oc = out_col0 + lane;
+  const bool cv = (e.kind == EPI_SWIGLU) ? (oc < e.n_out) : (col0 + lane < a.n_rows);
+  if (e.kind == EPI_RESID) {
+    // all residual loads of the chunk first (they cannot be reordered past the
+    // stores by the compiler), then the adds and stores
+    const TY* res = static_cast<const TY*>(e.res);
+    float xr[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const int rw = row0 + r;
+      xr[r] = (rw < a.M && cv) ? ld_act<TY>(res + (int64_t)rw * e.ldr + oc) : 0.0f;
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const int rw = row0 + r;
+      if (rw < a.M && cv)
+        st_act<TY>(out + (int64_t)rw * e.ldo + oc, __fadd_rn(xr[r], stg[r * kStageLd + lane]));
+    }
+  } else {
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+      const int rw = row0 + r;
+      if (rw < a.M && cv) st_act<TY>(out + (int64_t)rw * e.ldo + oc, stg[r * kStageLd + lane]);
+    }
+  }
+  __syncwarp();
+}
+
 template <int BN, typename TY>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const GemmArgs a) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::S;
   extern __shared__ uint8_t gsm_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) &
+                                           ~uintptr_t(1023));
   uint8_t* sA = sm;                                   // [S][A_BYTES]
   uint8_t* sBu = sm + S * Cfg::A_BYTES;               // [S][BU_BYTES]
   uint8_t* sBp = sBu + S * Cfg::BU_BYTES;             // [S][BP_BYTES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sBp + S * Cfg::BP_BYTES);
+  float* sEpi = reinterpret_cast<float*>(sBp + S * Cfg::BP_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + Cfg::EPI_BYTES);
   uint64_t* full = bars;            // TMA landed
   uint64_t* unpacked = bars + S;    // B unpacked
   uint64_t* empty = bars + 2 * S;   // MMA finished reading the stage
-  uint64_t* accfull = bars + 3 * S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 1);
+  uint64_t* tfull = bars + 3 * S;   // [2] accumulator ready
+  uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN;
-  const int m0 = blockIdx.y * kBM;
   const int nk = a.num_kb;
+  const int total = a.n_tiles * a.m_tiles;
 
-  if (warp == 4 && lane == 0) {
+  if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < S; ++s) {
@@ -67,136 +185,134 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&unpacked[s], 128);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiWarps);
+    }
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc<BN>(tmem_slot);
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % S;
-        if (kb >= S) mbar_wait(&empty[s], ((kb / S) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::BP_BYTES);
-        tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kBK, m0);
-        tma_load_2d(sBp + s * Cfg::BP_BYTES, &tmB, &full[s], kb * (kBK / 16), n0);
+      uint32_t g = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int m0 = (t / a.n_tiles) * kBM, n0 = (t % a.n_tiles) * BN;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % S;
+          if (g >= (uint32_t)S) mbar_wait(&empty[s], ((g / S) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::BP_BYTES);
+          tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kBK, m0);
+          tma_load_2d(sBp + s * Cfg::BP_BYTES, &tmB, &full[s], kb * (kBK / 16), n0);
+        }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 1) {
     // ---------------- MMA issuer
     if (lane == 0) {
       // kind::i8 instruction descriptor: D s32, A s8, B u8, both K-major, M=128, N=BN
       const uint32_t idesc = (2u << 4) | (1u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(kBM >> 4) << 24);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % S;
-        mbar_wait(&unpacked[s], (kb / S) & 1);
+      uint32_t g = 0, it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        const uint32_t acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t a_addr = smem_u32(sA + s * Cfg::A_BYTES);
-        const uint32_t b_addr = smem_u32(sBu + s * Cfg::BU_BYTES);
+        const uint32_t d_addr = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % S;
+          mbar_wait(&unpacked[s], (g / S) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + s * Cfg::A_BYTES);
+          const uint32_t b_addr = smem_u32(sBu + s * Cfg::BU_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < kBK / 32; ++kk) {
-          mma_i8(tmem_base, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
-                 idesc, (kb | kk) != 0);
+          for (int kk = 0; kk < kBK / 32; ++kk)
+            mma_i8(d_addr, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                   idesc, (kb | kk) != 0);
+          mma_commit(&empty[s]);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&tfull[acc]);
       }
-      mma_commit(accfull);
+    }
+  } else if (warp < kEpiWarp0) {
+    // ---------------- unpack (warps 2-5): 2-bit fields -> u8 e, SW128 K-major
+    const int tid = threadIdx.x - 64;
+    uint32_t g = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % S;
+        mbar_wait(&full[s], (g / S) & 1);
+        const uint32_t* bp = reinterpret_cast<const uint32_t*>(sBp + s * Cfg::BP_BYTES);
+        uint8_t* bu = sBu + s * Cfg::BU_BYTES;
+#pragma unroll 4
+        for (int i = tid; i < BN * 8; i += 128) {
+          const int row = i >> 3, w = i & 7;
+          const uint32_t word = bp[i];
+          uint4 v;
+          v.x = word & 0x03030303u;
+          v.y = (word >> 2) & 0x03030303u;
+          v.z = (word >> 4) & 0x03030303u;
+          v.w = (word >> 6) & 0x03030303u;
+          *reinterpret_cast<uint4*>(bu + row * 128 + ((w ^ (row & 7)) << 4)) = v;
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&unpacked[s]);
+      }
     }
   } else {
-    // ---------------- unpack (warps 0-3)
-    const int tid = threadIdx.x;  // 0..127
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % S;
-      mbar_wait(&full[s], (kb / S) & 1);
-      const uint32_t* bp = reinterpret_cast<const uint32_t*>(sBp + s * Cfg::BP_BYTES);
-      uint8_t* bu = sBu + s * Cfg::BU_BYTES;
-#pragma unroll 4
-      for (int it = tid; it < BN * 8; it += 128) {
-        const int row = it >> 3, w = it & 7;
-        const uint32_t word = bp[it];
-        uint4 v;
-        v.x = word & 0x03030303u;
-        v.y = (word >> 2) & 0x03030303u;
-        v.z = (word >> 4) & 0x03030303u;
-        v.w = (word >> 6) & 0x03030303u;
-        *reinterpret_cast<uint4*>(bu + row * 128 + ((w ^ (row & 7)) << 4)) = v;
-      }
-      fence_proxy_async_smem();
-      mbar_arrive(&unpacked[s]);
-    }
-
-    // ---------------- epilogue: TMEM -> registers -> dequant -> functor -> global
-    mbar_wait(accfull, 0);
-    tc_fence_after();
-    const int row = m0 + warp * 32 + lane;
-    const bool rv = row < a.M;
-    const float deq = rv ? __ldg(a.deq + row) : 0.0f;
-    const int qsum = rv ? __ldg(a.qsum + row) : 0;
-    const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16);
+    // ---------------- epilogue (warps 6-13): two warps per TMEM lane quadrant
+    const int ew = warp - kEpiWarp0;
+    const int quad = warp & 3;          // TMEM lanes [32*quad, 32*quad+32)
+    const int half = ew >> 2;           // which half of the chunks this warp takes
+    float* stg = sEpi + ew * 32 * kStageLd;
     const Epi& e = a.epi;
-    const int nseg = e.n_seg;
-    if (e.kind == EPI_SWIGLU) {
-      // each 128-column group holds [64 gate | 64 up] of the same 64 channels
-      for (int g = 0; g < BN / 128; ++g) {
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      const uint32_t acc = it & 1;
+      const int m0 = (t / a.n_tiles) * kBM, n0 = (t % a.n_tiles) * BN;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row0 = m0 + quad * 32;
+      const int row = row0 + lane;
+      const bool rv = row < a.M;
+      const float deq = rv ? __ldg(a.deq + row) : 0.0f;
+      const int qsum = rv ? __ldg(a.qsum + row) : 0;
+      const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
+      if (e.kind == EPI_SWIGLU) {
+        // pair p = (128-col group, 32-col half): gate at +0, up at +64
 #pragma unroll 1
-        for (int half = 0; half < 2; ++half) {
-          uint32_t rg[32], ru[32];
-          tmem_ld32(trow + g * 128 + half * 32, rg);
-          tmem_ld32(trow + g * 128 + 64 + half * 32, ru);
+        for (int p = half; p < BN / 64; p += 2) {
+          const int cb = (p >> 1) * 128 + (p & 1) * 32;
+          uint32_t vg[32], vu[32];
+          tmem_ld32(trow + cb, vg);
+          tmem_ld32(trow + cb + 64, vu);
           tmem_ld_wait();
-          const int pcol = n0 + g * 128 + half * 32;  // packed row of the gate column
-          const int grp = pcol / 128;
-          const int r0 = grp * 64 + half * 32;        // logical channel of lane 0 column
-          if (rv) {
-            TY* out = static_cast<TY*>(e.out) + (int64_t)row * e.ldo;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int rr = r0 + j;
-              const int ag = (int)rg[j] - qsum, au = (int)ru[j] - qsum;
-              if (e.acc && pcol < a.n_rows) {
-                e.acc[(int64_t)row * e.ldacc + pcol + j] = ag;
-                e.acc[(int64_t)row * e.ldacc + pcol + 64 + j] = au;
-              }
-              if (rr < e.n_out) {
-                const float gh = bl_out<TY>(e, ag, deq, 0, rr);
-                const float uh = bl_out<TY>(e, au, deq, 1, rr);
-                st_act<TY>(out + rr, swiglu(gh, uh));
-              }
-            }
-          }
+          epi_chunk<TY>(e, a, stg, lane, row0, row, deq, qsum, n0 + cb, vg, vu);
         }
-      }
-    } else {
+      } else {
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t rv32[32];
-        tmem_ld32(trow + c * 32, rv32);
-        tmem_ld_wait();
-        const int col0 = n0 + c * 32;
-        if (rv && col0 < a.n_rows) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = col0 + j;
-            const int seg = (col / kSegRows) % nseg;
-            const int rr = (col / (kSegRows * nseg)) * kSegRows + (col % kSegRows);
-            if (col < a.n_rows && rr < e.n_out)
-              epi_single<TY>(e, row, col, seg, rr, (int)rv32[j] - qsum, deq);
-          }
+        for (int c = half; c < BN / 32; c += 2) {
+          uint32_t v[32];
+          tmem_ld32(trow + c * 32, v);
+          tmem_ld_wait();
+          epi_chunk<TY>(e, a, stg, lane, row0, row, deq, qsum, n0 + c * 32, v, nullptr);
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<BN>(tmem_base);
+    tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -245,8 +361,15 @@ static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, con
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid((a.n_rows + BN - 1) / BN, (a.M + kBM - 1) / kBM);
-  kern<<<grid, 192, GemmCfg<BN>::SMEM, s>>>(ta, tb, a);
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int total = a.n_tiles * a.m_tiles;
+  const int grid = total < num_sms ? total : num_sms;
+  kern<<<grid, kGemmThreads, GemmCfg<BN>::SMEM, s>>>(ta, tb, a);
   return cudaGetLastError();
 }
 
@@ -268,6 +391,8 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   a.M = M;
   a.n_rows = w.n_rows;
   a.num_kb = kp / kBK;
+  a.n_tiles = (w.n_rows + BN - 1) / BN;
+  a.m_tiles = (M + kBM - 1) / kBM;
   a.deq = deq;
   a.qsum = qsum;
   a.epi = epi;

@@ -1,6 +1,9 @@
 // k_gemv.cu -- a3: decode-time ternary GEMV (M <= 8 tokens), HBM-bound on the
 // packed weights.
 //
+//  * before griddepcontrol.wait (PDL) one thread starts bulk async copies of
+//    the CTA's packed weight rows into shared memory, so the weight fetch
+//    overlaps the previous kernel's tail (weights do not depend on it);
 //  * prologue: every CTA re-computes the fused RMSNorm + absmax int8 quantization
 //    of the M input rows (a2) into shared memory, in a fixed
 //    reduction order, so no extra launch or grid sync is needed;
@@ -41,16 +44,38 @@ __device__ __forceinline__ uint32_t ldg_stream(const uint32_t* p) {
 
 template <int MM, typename TX, typename TY>
 __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
-  extern __shared__ __align__(16) uint8_t g_smem[];
+  extern __shared__ __align__(128) uint8_t g_smem[];
   const int R = a.n_seg * a.ch;
-  int8_t* qs = reinterpret_cast<int8_t*>(g_smem);            // [MM][Kp]
-  int* accs = reinterpret_cast<int*>(g_smem + MM * a.Kp);    // [MM][R]
+  const int row_bytes = a.Kp / 4;                             // packed bytes of one row
+  uint32_t* sW = reinterpret_cast<uint32_t*>(g_smem);         // [R][Kp/16] words
+  int8_t* qs = reinterpret_cast<int8_t*>(g_smem + R * row_bytes);   // [MM][Kp]
+  int* accs = reinterpret_cast<int*>(qs + MM * a.Kp);               // [MM][R]
+  __shared__ __align__(8) uint64_t wbar;
   __shared__ float s_deq[MM];
   __shared__ int s_qsum[MM];
   __shared__ double red_d[kGWarps];
   __shared__ float red_f[kGWarps];
   __shared__ int red_i[kGWarps];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int unit = blockIdx.x;
+
+  // ---------------- weight prefetch (independent of the previous kernel)
+  if (tid == 0) {
+    mbar_init(&wbar, 1);
+    fence_barrier_init();
+    fence_proxy_async_smem();
+    int nvalid = 0;
+    for (int j = 0; j < R; ++j) nvalid += (unit * a.ch + j % a.ch) < a.n_out;
+    mbar_arrive_expect_tx(&wbar, (uint32_t)(nvalid * row_bytes));
+    for (int j = 0; j < R; ++j) {
+      const int seg = j / a.ch, rr = unit * a.ch + j % a.ch;
+      if (rr < a.n_out)
+        bulk_load(reinterpret_cast<uint8_t*>(sW) + j * row_bytes,
+                  a.codes + (int64_t)packed_row(seg, rr, a.n_seg) * a.ldw, row_bytes, &wbar);
+    }
+  }
+  pdl_launch_dependents();
+  pdl_wait();
 
   for (int i = tid; i < MM * R; i += kGThreads) accs[i] = 0;
 
@@ -131,7 +156,7 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
   }
 
   // ---------------- main loop: (row quad, K slice) items per warp
-  const int unit = blockIdx.x;
+  mbar_wait(&wbar, 0);
   const int nwords = a.Kp >> 4;
   const int nquads = (R + 3) >> 2;
   const int items = nquads * a.ksplit;
@@ -148,7 +173,8 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
       const int seg = j / a.ch, i = j % a.ch;
       const int rr = unit * a.ch + i;
       valid[qd] = (j < R) && (rr < a.n_out);
-      wrow[qd] = a.codes + (int64_t)packed_row(seg, valid[qd] ? rr : 0, a.n_seg) * a.ldw;
+      wrow[qd] = sW + (valid[qd] ? j : 0) * (row_bytes / 4);
+      (void)seg;
     }
     int acc[4][MM];
 #pragma unroll
@@ -158,7 +184,7 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
     for (int w = w0 + lane; w < w1; w += 32) {
       uint32_t wd[4];
 #pragma unroll
-      for (int qd = 0; qd < 4; ++qd) wd[qd] = valid[qd] ? ldg_stream(wrow[qd] + w) : 0x55555555u;
+      for (int qd = 0; qd < 4; ++qd) wd[qd] = valid[qd] ? wrow[qd][w] : 0x55555555u;
 #pragma unroll
       for (int m = 0; m < MM; ++m) {
         const uint4 qv = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
@@ -220,14 +246,26 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
 
 template <int MM, typename TX, typename TY>
 static cudaError_t gemv_launch(const GemvArgs& a, int units, cudaStream_t s) {
-  const size_t smem = (size_t)MM * a.Kp + (size_t)MM * a.n_seg * a.ch * sizeof(int);
+  const int R = a.n_seg * a.ch;
+  const size_t smem = (size_t)R * (a.Kp / 4) + (size_t)MM * a.Kp + (size_t)MM * R * sizeof(int);
   auto kern = k_gemv<MM, TX, TY>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static size_t smem_set = 48 * 1024;
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
+    smem_set = 200 * 1024;
   }
-  kern<<<units, kGThreads, smem, s>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(units);
+  cfg.blockDim = dim3(kGThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <typename TX, typename TY>

@@ -138,6 +138,80 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
   }
 }
 
+// Warp-per-row variant for K <= 32*4*NV: no block-level barriers at all; 8 rows
+// per 256-thread CTA.  Same arithmetic, reductions in a fixed shuffle order.
+template <typename TX, int NV>
+__global__ void __launch_bounds__(256) k_quant_warp(const TX* __restrict__ x, int M, int K,
+                                                    int ldx, const float* __restrict__ gain,
+                                                    float eps, int8_t* __restrict__ q, int ldq,
+                                                    float* __restrict__ deq,
+                                                    int32_t* __restrict__ qsum,
+                                                    float* __restrict__ inv_rms,
+                                                    float* __restrict__ absmax) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= M) return;
+  const TX* xr = x + (int64_t)row * ldx;
+  const int nc = K >> 2;
+  float v[NV][4];
+  double ss = 0.0;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < nc) {
+      Vec4<TX>::load(xr + 4 * c, v[i]);
+    } else {
+      v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ss += (double)v[i][j] * (double)v[i][j];
+  }
+  ss = warp_sum_f64(ss);
+  const float r = (float)(1.0 / sqrt(ss / (double)K + (double)eps));
+  float a = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float y = __fmul_rn(v[i][j], r);
+      if (gain && c < nc) y = __fmul_rn(y, __ldg(gain + 4 * c + j));
+      v[i][j] = y;
+      a = fmaxf(a, fabsf(y));
+    }
+  }
+  a = warp_max_f32(a);
+  const float s = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
+  int8_t* qr = q + (int64_t)row * ldq;
+  const int ncp = ((K + kKAlign - 1) / kKAlign * kKAlign) >> 2;
+  int qs = 0;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < ncp) {
+      uint32_t packed = 0;
+      if (c < nc && a > 0.0f) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float t = round_half_away(__fmul_rn(v[i][j], s));
+          t = fminf(fmaxf(t, -128.0f), 127.0f);
+          const int qi = (int)t;
+          qs += qi;
+          packed |= ((uint32_t)qi & 0xffu) << (8 * j);
+        }
+      }
+      reinterpret_cast<uint32_t*>(qr)[c] = packed;
+    }
+  }
+  qs = warp_sum_i32(qs);
+  if (lane == 0) {
+    deq[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 0.0f;
+    qsum[row] = qs;
+    if (inv_rms) inv_rms[row] = r;
+    if (absmax) absmax[row] = a;
+  }
+}
+
 template <typename TX>
 static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const float* gain, float eps,
                                   int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
@@ -145,6 +219,15 @@ static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const floa
   const int kp = (k + kKAlign - 1) / kKAlign * kKAlign;
   const int chunks = kp / 4;
   const int nch = (chunks + kQThreads - 1) / kQThreads;
+  const int nv = (chunks + 31) / 32;
+  const int g8 = (m + 7) / 8;
+#define TERN_QW(N)                                                                            \
+  k_quant_warp<TX, N><<<g8, 256, 0, s>>>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, \
+                                         absmax)
+  if (nv <= 8) { TERN_QW(8); return cudaGetLastError(); }
+  if (nv <= 16) { TERN_QW(16); return cudaGetLastError(); }
+  if (nv <= 24) { TERN_QW(24); return cudaGetLastError(); }
+#undef TERN_QW
 #define TERN_Q(N)                                                                              \
   k_quant<TX, N><<<m, kQThreads, 0, s>>>(x, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, \
                                          absmax)

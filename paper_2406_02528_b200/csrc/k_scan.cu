@@ -72,9 +72,17 @@ __global__ void __launch_bounds__(kSWarps * 32) k_scan(const T* __restrict__ fcg
     // phase 2: the sequential carry (exact definition order: (f*h) + ((1-f)*c))
     if (warp == 0) {
       const int steps = min(kSTile, T_ - t0);
-      for (int t = 0; t < steps; ++t) {
-        hc = __fadd_rn(__fmul_rn(sF[t][lane], hc), sB[t][lane]);
-        sF[t][lane] = hc;
+      if (steps == kSTile) {
+#pragma unroll 8
+        for (int t = 0; t < kSTile; ++t) {
+          hc = __fadd_rn(__fmul_rn(sF[t][lane], hc), sB[t][lane]);
+          sF[t][lane] = hc;
+        }
+      } else {
+        for (int t = 0; t < steps; ++t) {
+          hc = __fadd_rn(__fmul_rn(sF[t][lane], hc), sB[t][lane]);
+          sF[t][lane] = hc;
+        }
       }
     }
     __syncthreads();
