@@ -68,10 +68,13 @@ const char* tern_last_error(void);
 /* ------------------------------------------------------------------------
  * Packed ternary weights (a1).  DESIGN.md "Packed weight layout":
  *   trit t in {-1,0,+1} is stored as the 2-bit field e = t + 1;
- *   16 trits per uint32 word: trit k of a row is in word k/16, byte k%4,
+ *   16 trits per uint32 word: trit k is in word k/16 of its row, byte k%4,
  *   bits [2f, 2f+1] of that byte with f = (k%16)/4;
- *   rows are K-contiguous, ldw = Kp/16 words, Kp = roundup(k, 128);
- *   trits in the padding k..Kp-1 are 0 (field 1).
+ *   K-block-major storage: codes[Kp/128][n_rows][8] -- word j of packed row
+ *   r in K-block b (trits 128b+16j .. 128b+16j+15) is at ((b*n_rows)+r)*8+j,
+ *   so one K-block of any run of rows is contiguous (one bulk copy per tile);
+ *   Kp = roundup(k, 128), ldw = Kp/16 words per row; trits in the padding
+ *   k..Kp-1 are 0 (field 1).
  * A fused group of n_seg matrices of n_out rows each (f|c|g: 3, gate|up: 2)
  * interleaves rows in groups of seg_rows (64):
  *   packed row of (segment s, row r) = (r/64)*(n_seg*64) + s*64 + r%64,
@@ -80,20 +83,24 @@ const char* tern_last_error(void);
  * One fp32 dequantization scale mean|W| per segment (one per matrix, C6).
  * ------------------------------------------------------------------------ */
 typedef struct {
-  const uint32_t* codes;  /* device [n_rows][ldw]                                 */
+  const uint32_t* codes;  /* device [Kp/128][n_rows][8] (K-block-major, see above) */
   const float* scales;    /* device [n_seg]: mean|W| of each source matrix         */
   int32_t n_out;          /* logical output rows per segment                       */
   int32_t k;              /* logical input features                                */
-  int32_t ldw;            /* words per packed row, >= roundup(k,128)/16            */
+  int32_t ldw;            /* words per packed row, == roundup(k,128)/16            */
   int32_t n_seg;          /* 1, 2 or 3                                             */
   int32_t n_rows;         /* packed rows = roundup(n_out,64)*n_seg (n_seg>1) or n_out */
+  const uint8_t* e8;      /* optional device [n_rows][Kp] u8 copy of the fields e=t+1
+                             (tern_expand); when set, the prefill GEMM loads it with TMA
+                             instead of unpacking the 2-bit codes in shared memory; NULL
+                             = unpack in shared memory (4x less memory)             */
 } tern_weight;
 
 /* Number of packed rows and words per row for a group (host helper). */
 int32_t tern_packed_rows(int32_t n_out, int32_t n_seg);
 int32_t tern_packed_ldw(int32_t k);
 
-/* Fill codes[n_rows][ldw] with the zero trit (field value 1 everywhere).
+/* Fill the n_rows*ldw words of codes with the zero trit (field value 1).
  * Call once on a fresh buffer before tern_pack. */
 tern_status tern_codes_init(uint32_t* codes, int32_t n_rows, int32_t ldw, tern_stream stream);
 
@@ -105,13 +112,18 @@ size_t tern_pack_workspace(int32_t n, int32_t k);
  *   s = 1/m, t = clamp(round(s*W), -1, 1) with round half away from zero.
  * W: device fp32 [n][k] row-major (the latent weight of ONE matrix).
  * scale_in: device pointer to one float, or NULL to compute mean|W|.
- * Writes segment seg_idx of the group into codes (see layout above) and the
+ * Writes segment seg_idx of the group into codes (see layout above; n_rows =
+ * tern_packed_rows(n, n_seg) rows of the whole group) and the
  * scale to scale_out[0] (device).  This offline call synchronises `stream`
  * to check the scale: returns TERN_ERR_DEGENERATE if m == 0 or is not finite
  * (S:39).  ws: device workspace of tern_pack_workspace(n,k) bytes. */
 tern_status tern_pack(const float* W, int32_t n, int32_t k, const float* scale_in, int32_t n_seg,
-                      int32_t seg_idx, uint32_t* codes, int32_t ldw, float* scale_out, void* ws,
+                      int32_t seg_idx, uint32_t* codes, int32_t n_rows, float* scale_out, void* ws,
                       size_t ws_bytes, tern_stream stream);
+
+/* Expand the 2-bit codes of w into the u8 copy e8[n_rows][Kp] (field values
+ * e = t+1) used by the prefill GEMM's TMA path; e8 must hold n_rows*Kp bytes. */
+tern_status tern_expand(const tern_weight* w, uint8_t* e8, tern_stream stream);
 
 /* ------------------------------------------------------------------------
  * a2: fused RMSNorm + per-token absmax int8 quantization (Alg. 1
@@ -257,6 +269,14 @@ typedef struct {
 } tern_prof_rec;
 void tern_profile_enable(int32_t on);
 int32_t tern_profile_collect(tern_prof_rec* out, int32_t max);
+
+/* Device self-check of the numerics shortcuts the kernels take (test use):
+ * which = 0: the FMA-corrected reciprocal used by sigmoid equals IEEE 1/d for
+ * every mantissa at exponents {0,1,2,5,10,20,40,60,80,100,119};
+ * which = 1: sigmoid equals 1/(1+exp_c(-x)) with IEEE division at 2^24
+ * points in [-96, 96).  Synchronous; writes the mismatch count to *mismatches
+ * (host).  ws: device scratch of >= 64 bytes. */
+tern_status tern_selftest(int32_t which, void* ws, uint64_t* mismatches);
 
 /* Tuning knob (host): largest m sent to the decode GEMV (default 8, max 8;
  * 0 forces the tensor-core path everywhere).  Not thread-safe to change

@@ -181,8 +181,13 @@ def packed_row(s, r, n_seg, seg_rows) -> int:
 
 
 def unpack_segment(codes, n, k, n_seg=1, s=0, seg_rows=64):
-    """Decode segment ``s`` (n rows of k trits) of a packed uint32 [rows][ldw] array."""
+    """Decode segment ``s`` (n rows of k trits) of a packed uint32 array in the
+    K-block-major layout [Kp/128][n_rows][8]."""
     codes = np.ascontiguousarray(codes, dtype=np.uint32)
+    if codes.ndim == 2:                    # a single K-block [n_rows][8]
+        codes = codes.reshape(1, *codes.shape)
+    if codes.shape[-1] != 8 or codes.shape[0] * 128 < k:
+        raise OracleError("unpack: codes must be [Kp/128][n_rows][8] covering k")
     t = np.empty((n, k), dtype=np.int8)
     _check(lib().orc_unpack_segment(codes.reshape(-1), codes.shape[1], n, k, n_seg, s, seg_rows,
                                     t.reshape(-1)), "unpack")

@@ -164,8 +164,10 @@ double orc_zero_fraction(const int8_t* t, int64_t n) {
 
 /* Decoder of the GPU packing layout, written from its specification in
  * DESIGN.md "Packed weight layout" (not from the CUDA code):
- *   trit k of a row lives in word k/16, byte j = k%4, bit field f = (k%16)/4
- *   at bits [8j+2f, 8j+2f+1]; the field holds e = t + 1 in {0,1,2}.
+ *   trit k of a row lives in word k/16 of that row, byte j = k%4, bit field
+ *   f = (k%16)/4 at bits [8j+2f, 8j+2f+1]; the field holds e = t + 1 in
+ *   {0,1,2}; storage is K-block-major: word w of packed row r is at index
+ *   ((w/8) * n_rows + r) * 8 + w%8 (8 words = one K-block of 128 trits).
  * Rows of fused groups are interleaved in groups of seg_rows:
  *   packed row of (segment s, logical row r) =
  *     (r / seg_rows) * (n_seg * seg_rows) + s * seg_rows + r % seg_rows.
@@ -173,9 +175,10 @@ double orc_zero_fraction(const int8_t* t, int64_t n) {
 int64_t orc_packed_row(int64_t s, int64_t r, int64_t n_seg, int64_t seg_rows) {
   return (r / seg_rows) * (n_seg * seg_rows) + s * seg_rows + (r % seg_rows);
 }
-int orc_unpack_row(const uint32_t* codes_row, int k, int8_t* t) {
+int orc_unpack_row(const uint32_t* codes, int64_t n_rows, int64_t r, int k, int8_t* t) {
   for (int kk = 0; kk < k; ++kk) {
-    uint32_t w = codes_row[kk / 16];
+    int64_t widx = kk / 16;
+    uint32_t w = codes[((widx / 8) * n_rows + r) * 8 + widx % 8];
     int j = kk % 4, f = (kk % 16) / 4;
     uint32_t e = (w >> (8 * j + 2 * f)) & 3u;
     if (e == 3u) return ORC_ERR_ARG;
@@ -184,11 +187,11 @@ int orc_unpack_row(const uint32_t* codes_row, int k, int8_t* t) {
   return ORC_OK;
 }
 /* Unpack segment s (n logical rows) of a packed group into t[n][k]. */
-int orc_unpack_segment(const uint32_t* codes, int64_t ldw, int n, int k, int n_seg, int s,
+int orc_unpack_segment(const uint32_t* codes, int64_t n_rows, int n, int k, int n_seg, int s,
                        int seg_rows, int8_t* t) {
   for (int r = 0; r < n; ++r) {
     int64_t pr = orc_packed_row(s, r, n_seg, seg_rows);
-    int rc = orc_unpack_row(codes + pr * ldw, k, t + (int64_t)r * k);
+    int rc = orc_unpack_row(codes, n_rows, pr, k, t + (int64_t)r * k);
     if (rc) return rc;
   }
   return ORC_OK;

@@ -28,7 +28,7 @@ class TernError(RuntimeError):
 class tern_weight(C.Structure):
     _fields_ = [("codes", C.c_void_p), ("scales", C.c_void_p), ("n_out", C.c_int32),
                 ("k", C.c_int32), ("ldw", C.c_int32), ("n_seg", C.c_int32),
-                ("n_rows", C.c_int32)]
+                ("n_rows", C.c_int32), ("e8", C.c_void_p)]
 
 
 class tern_bl_taps(C.Structure):
@@ -75,6 +75,7 @@ _SIGS = {
     "tern_codes_init": (C.c_int, [P, I32, I32, P]),
     "tern_pack_workspace": (SZ, [I32, I32]),
     "tern_pack": (C.c_int, [P, I32, I32, P, I32, I32, P, I32, P, P, SZ, P]),
+    "tern_expand": (C.c_int, [C.POINTER(tern_weight), P, P]),
     "tern_quant": (C.c_int, [P, C.c_int, I32, I32, I32, P, F, P, I32, P, P, P, P, P]),
     "tern_bitlinear_workspace": (SZ, [I32, I32]),
     "bitlinear_fwd": (C.c_int, [P, C.c_int, I32, I32, I32, P, F, C.POINTER(tern_weight), P, P,
@@ -92,6 +93,7 @@ _SIGS = {
     "block_decode": (C.c_int, [C.POINTER(tern_block), P, P, C.c_int, I32, P, P, SZ, P]),
     "tern_profile_enable": (None, [I32]),
     "tern_profile_collect": (I32, [C.POINTER(tern_prof_rec), I32]),
+    "tern_selftest": (C.c_int, [I32, P, C.POINTER(C.c_uint64)]),
     "tern_set_gemv_max_m": (None, [I32]),
     "tern_get_gemv_max_m": (I32, []),
 }
@@ -151,8 +153,10 @@ def tern_packed_ldw(k: int) -> int:
 
 
 def tern_codes_init(codes: torch.Tensor, stream=None):
-    n_rows, ldw = codes.shape
-    _check(load().tern_codes_init(ptr(codes), n_rows, ldw, stream_handle(stream)), "tern_codes_init")
+    """codes: int32 [Kp/128][n_rows][8] (K-block-major packed layout)."""
+    nkb, n_rows, _ = codes.shape
+    _check(load().tern_codes_init(ptr(codes), n_rows, nkb * 8, stream_handle(stream)),
+           "tern_codes_init")
 
 
 def tern_pack(W: torch.Tensor, codes: torch.Tensor, scale_out: torch.Tensor, n_seg=1, seg_idx=0,
@@ -165,6 +169,10 @@ def tern_pack(W: torch.Tensor, codes: torch.Tensor, scale_out: torch.Tensor, n_s
     ws = torch.empty(wsb, dtype=torch.uint8, device=W.device)
     _check(L.tern_pack(ptr(W), n, k, ptr(scale_in), n_seg, seg_idx, ptr(codes), codes.shape[1],
                        ptr(scale_out), ptr(ws), wsb, stream_handle(stream)), "tern_pack")
+
+
+def tern_expand(w: tern_weight, e8: torch.Tensor, stream=None):
+    _check(load().tern_expand(C.byref(w), ptr(e8), stream_handle(stream)), "tern_expand")
 
 
 def tern_quant(x: torch.Tensor, q: torch.Tensor, deq: torch.Tensor, qsum: torch.Tensor,
@@ -252,3 +260,10 @@ def tern_profile_collect() -> list:
         out.append({"kernel": KERNEL_NAMES.get(r.kernel, str(r.kernel)), "epi": r.epi, "m": r.m,
                     "n": r.n, "k": r.k, "n_seg": r.n_seg, "dtype": r.dtype, "ms": float(r.ms)})
     return out
+
+
+def tern_selftest(which: int) -> int:
+    ws = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    out = C.c_uint64(0)
+    _check(load().tern_selftest(int(which), ptr(ws), C.byref(out)), "tern_selftest")
+    return int(out.value)

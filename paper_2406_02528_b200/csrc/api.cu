@@ -77,8 +77,8 @@ tern_status check_weight(const tern_weight* w, int k, int n_seg, const char* nam
   CHECK(w->n_out > 0, "%s: n_out must be > 0", name);
   CHECK(w->n_rows == tern_packed_rows(w->n_out, w->n_seg), "%s: n_rows=%d inconsistent", name,
         w->n_rows);
-  CHECK(w->ldw >= kpad(k) / 16 && w->ldw % 4 == 0, "%s: ldw=%d must be >= %d and a multiple of 4",
-        name, w->ldw, kpad(k) / 16);
+  CHECK(w->ldw == kpad(k) / 16, "%s: ldw=%d must be %d", name, w->ldw, kpad(k) / 16);
+  CHECK(w->e8 == nullptr || aligned16(w->e8), "%s: e8 not 16-byte aligned", name);
   return TERN_OK;
 }
 
@@ -198,6 +198,22 @@ extern "C" {
 
 int tern_abi_version(void) { return TERN_ABI_VERSION; }
 
+tern_status tern_selftest(int32_t which, void* ws, uint64_t* mismatches) {
+  CHECK(ws && mismatches && aligned16(ws) && (which == 0 || which == 1), "tern_selftest: args");
+  tern_status st = check_device();
+  if (st) return st;
+  static const int exps[11] = {0, 1, 2, 5, 10, 20, 40, 60, 80, 100, 119};
+  unsigned long long* bad = static_cast<unsigned long long*>(ws);
+  int* dexp = reinterpret_cast<int*>(static_cast<char*>(ws) + 16);
+  TRY_CUDA(cudaMemset(bad, 0, 8), "selftest memset");
+  TRY_CUDA(cudaMemcpy(dexp, exps, sizeof(exps), cudaMemcpyHostToDevice), "selftest h2d");
+  TRY_CUDA(launch_selftest(which, bad, dexp, 11, 0), "selftest");
+  unsigned long long h = 0;
+  TRY_CUDA(cudaMemcpy(&h, bad, 8, cudaMemcpyDeviceToHost), "selftest d2h");
+  *mismatches = h;
+  return TERN_OK;
+}
+
 void tern_profile_enable(int32_t on) {
   std::lock_guard<std::mutex> g(g_prof_mu);
   if (on) {
@@ -243,18 +259,28 @@ tern_status tern_codes_init(uint32_t* codes, int32_t n_rows, int32_t ldw, tern_s
   return TERN_OK;
 }
 
+tern_status tern_expand(const tern_weight* w, uint8_t* e8, tern_stream stream) {
+  CHECK(w && e8 && aligned16(e8), "tern_expand: null/misaligned pointer");
+  tern_status st = check_weight(w, w->k, w->n_seg, "tern_expand");
+  if (st) return st;
+  if ((st = check_device()) != TERN_OK) return st;
+  TRY_CUDA(launch_expand(*w, e8, (cudaStream_t)stream), "expand");
+  return TERN_OK;
+}
+
 size_t tern_pack_workspace(int32_t n, int32_t k) {
   (void)n; (void)k;
   return pack_workspace_bytes() + 256;
 }
 
 tern_status tern_pack(const float* W, int32_t n, int32_t k, const float* scale_in, int32_t n_seg,
-                      int32_t seg_idx, uint32_t* codes, int32_t ldw, float* scale_out, void* ws,
+                      int32_t seg_idx, uint32_t* codes, int32_t n_rows, float* scale_out, void* ws,
                       size_t ws_bytes, tern_stream stream) {
   CHECK(W && codes && scale_out && ws, "tern_pack: null pointer");
   CHECK(n > 0 && k > 0, "tern_pack: n=%d k=%d must be > 0", n, k);
   CHECK(n_seg >= 1 && n_seg <= 3 && seg_idx >= 0 && seg_idx < n_seg, "tern_pack: bad segment");
-  CHECK(ldw >= kpad(k) / 16, "tern_pack: ldw=%d < %d", ldw, kpad(k) / 16);
+  CHECK(n_rows == tern_packed_rows(n, n_seg), "tern_pack: n_rows=%d, expected %d", n_rows,
+        tern_packed_rows(n, n_seg));
   CHECK(ws_bytes >= tern_pack_workspace(n, k), "tern_pack: workspace too small");
   CHECK(aligned16(ws), "tern_pack: workspace not 16-byte aligned");
   tern_status st = check_device();
@@ -270,7 +296,7 @@ tern_status tern_pack(const float* W, int32_t n, int32_t k, const float* scale_i
     return fail(TERN_ERR_DEGENERATE, "tern_pack: mean|W| = %g (all-zero or non-finite W)", m);
   TRY_CUDA(cudaMemcpyAsync(scale_out, scratch, sizeof(float), cudaMemcpyDeviceToDevice, s),
            "scale copy");
-  TRY_CUDA(launch_pack_codes(W, n, k, n_seg, seg_idx, codes, ldw, scratch, s), "pack");
+  TRY_CUDA(launch_pack_codes(W, n, k, n_seg, seg_idx, codes, n_rows, scratch, s), "pack");
   return TERN_OK;
 }
 

@@ -44,9 +44,22 @@ __device__ __forceinline__ float exp_c(float x) {
   return __fmul_rn(p, __int_as_float((ki + 127) << 23));
 }
 
-// sigma(x) = 1/(1+exp(-x)), IEEE division.
+// Correctly rounded 1/d for d >= 1 (== IEEE __fdiv_rn(1, d)) without the
+// division's special-case scaffolding: MUFU reciprocal estimate + one Newton
+// correction with an exact FMA residual.  d >= 2^120 (results near the
+// subnormal range) and NaN take the IEEE path.  Equality with __fdiv_rn is
+// checked exhaustively over all mantissas by tern_selftest (GPU test).
+__device__ __forceinline__ float rcp_ge1(float d) {
+  if (!(d < 0x1p120f)) return __fdiv_rn(1.0f, d);
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+  const float e = __fmaf_rn(-d, r, 1.0f);
+  return __fmaf_rn(r, e, r);
+}
+
+// sigma(x) = 1/(1+exp(-x)); the reciprocal is the correctly rounded one.
 __device__ __forceinline__ float sigmoid_c(float x) {
-  return __fdiv_rn(1.0f, __fadd_rn(1.0f, exp_c(-x)));
+  return rcp_ge1(__fadd_rn(1.0f, exp_c(-x)));
 }
 // SiLU tau(x) = x sigma(x).
 __device__ __forceinline__ float silu_c(float x) { return __fmul_rn(x, sigmoid_c(x)); }

@@ -49,7 +49,7 @@ cudaError_t launch_codes_init(uint32_t* codes, int n_rows, int ldw, cudaStream_t
 cudaError_t launch_absmean(const float* W, int64_t numel, const float* scale_in, float* scale_out,
                            double* ws, cudaStream_t s);
 cudaError_t launch_pack_codes(const float* W, int n, int k, int n_seg, int seg, uint32_t* codes,
-                              int ldw, const float* scale, cudaStream_t s);
+                              int n_rows, const float* scale, cudaStream_t s);
 size_t pack_workspace_bytes();
 // a2
 cudaError_t launch_quant(const void* x, int xdt, int m, int k, int ldx, const float* gain,
@@ -62,6 +62,9 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
 // a4 (tcgen05 int8 GEMM): q [M][ldq] -> epilogue
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s);
+cudaError_t launch_selftest(int which, unsigned long long* bad, int* exps, int n_exp,
+                            cudaStream_t s);
+cudaError_t launch_expand(const tern_weight& w, uint8_t* e8, cudaStream_t s);
 // a6
 cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
                         void* oprime, cudaStream_t s);

@@ -4,191 +4,202 @@
 //   D[m][n] = sum_k q[m][k] * e[n][k]     (q int8 activations, e = t+1 in {0,1,2})
 //   acc     = D - qsum[m]                 (= sum_{t=+1} q - sum_{t=-1} q)
 //
-// Per CTA: one 128 x BN output tile, K walked in 128-element blocks through an
-// S-stage ring:
-//   warp 4      TMA producer: A tile (int8, 128B-swizzled) + packed B tile
-//               (BN rows x 8 words) -> smem, mbarrier complete_tx
-//   warps 0-3   unpack: 2-bit fields -> uint8 e in the UMMA K-major SW128
-//               layout (one AND per 4 values), fence.proxy.async, arrive;
-//               afterwards the epilogue (tcgen05.ld -> dequant -> functor -> st)
-//   warp 5      TMEM allocation + single-thread tcgen05.mma issue, commit to
-//               the stage's empty barrier and finally to the accumulator barrier
+// Persistent, warp-specialised, one 128 x BN output tile per step:
+//   warp 0      TMA producer: A tile (int8, SW128) and the B tile, either the
+//               pre-expanded u8 copy (kPre: TMA SW128, no unpack) or the 2-bit
+//               packed span (one bulk copy, K-block-major layout)
+//   warp 1      TMEM allocation + single-thread tcgen05.mma issue
+//   warps 2-5   (packed B only) unpack 2-bit fields -> u8 e in the SW128 layout
+//   warps 6-13  epilogue, two per TMEM lane quadrant: tcgen05.ld -> dequant ->
+//               functor -> swizzled smem tile -> TMA bulk-tensor store
+// Two TMEM accumulators let the epilogue of tile i overlap the main loop of
+// tile i+1.  Shared-memory (MIO) traffic is the binding resource on this chip
+// for 1-CTA tiles, which is what the pre-expanded B and the TMA-store epilogue
+// minimise (measured with the TERN_GEMM_PROF counters).
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
 #include "epilogue.cuh"
 
 namespace tern {
 
 constexpr int kBM = 128;
 constexpr int kBK = 128;  // int8 elements = bytes = one 128B swizzle row
-
-// Warp roles (448 threads):
-//   warp 0       TMA producer            warp 1      TMEM alloc + MMA issuer
-//   warps 2-5    B unpack (128 thr)      warps 6-13  epilogue (256 thr, 2 per TMEM quadrant)
-// Persistent: grid = min(#tiles, #SMs), static round-robin over tiles (m-major
-// so CTAs running together share A rows in L2).  Two TMEM accumulators of BN
-// columns let the epilogue of tile i overlap the main loop of tile i+1.
 constexpr int kGemmThreads = 448;
 constexpr int kEpiWarp0 = 6;
 constexpr int kEpiWarps = 8;
-constexpr int kStageLd = 33;  // epilogue staging row stride (floats): conflict-free
+constexpr int kEpiBuf = 4096;  // bytes of one 32x32 staging tile (fp32)
 
-template <int BN> struct GemmCfg {
-  static constexpr int S = BN == 256 ? 3 : 4;
-  static constexpr int A_BYTES = kBM * kBK;       // 16 KB
-  static constexpr int BU_BYTES = BN * kBK;       // unpacked B
-  static constexpr int BP_BYTES = BN * (kBK / 4); // packed B: BN rows x 8 words
-  static constexpr int STAGE = A_BYTES + BU_BYTES + BP_BYTES;
-  static constexpr int EPI_BYTES = kEpiWarps * 32 * kStageLd * 4;
-  static constexpr int SMEM = S * STAGE + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+template <int BN, bool kPre> struct GemmCfg {
+  static constexpr int A_BYTES = kBM * kBK;        // 16 KB
+  static constexpr int B_BYTES = BN * kBK;         // u8 B tile
+  static constexpr int BP_BYTES = BN * (kBK / 4);  // packed B: BN rows x 8 words
+  // TMA ring depth S, unpacked ring depth U (packed path only)
+  static constexpr int S = kPre ? (BN == 256 ? 3 : 4) : (BN == 256 ? 4 : 5);
+  static constexpr int U = kPre ? 0 : 2;
+  static constexpr int RING = kPre ? S * (A_BYTES + B_BYTES) : S * (A_BYTES + BP_BYTES) + U * B_BYTES;
+  static constexpr int EPI_BYTES = kEpiWarps * 2 * kEpiBuf;
+  static constexpr int SMEM = RING + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
 struct GemmArgs {
   int M, n_rows, num_kb, n_tiles, m_tiles;
+  const uint32_t* codes;     // K-block-major packed weights [num_kb][n_rows][8]
   const float* deq;
   const int32_t* qsum;
   Epi epi;
+  unsigned long long* prof;  // debug (TERN_GEMM_PROF): [grid][8] wait cycles per site
 };
 
-// Epilogue of one 32-column chunk held by this thread (one row): computes the
-// stored values (phase A, thread = row) into the warp's staging tile, then
-// writes it with row-contiguous coalesced stores (phase B, lane = column).
-template <typename TY>
-__device__ __forceinline__ void epi_chunk(const Epi& e, const GemmArgs& a, float* stg, int lane,
-                                          int row0, int row, float deq, int qsum, int col0,
-                                          const uint32_t (&v)[32], const uint32_t* vu) {
-  const bool rv = row < a.M;
-  const int nseg = e.n_seg;
-  int out_col0;     // first output column of the chunk
-  bool active = col0 < a.n_rows;
-  if (e.kind == EPI_SWIGLU) {
-    const int grp = col0 / 128, half = (col0 % 128) / 32;
-    out_col0 = grp * 64 + half * 32;
-    active = active && out_col0 < e.n_out;
-  } else if (e.kind == EPI_FCG || e.kind == EPI_NONE) {
-    out_col0 = col0;
-  } else {
-    out_col0 = (col0 / (kSegRows * nseg)) * kSegRows + (col0 % kSegRows);  // n_seg == 1: col0
+// mbar_wait that (in the TERN_GEMM_PROF debug mode) adds the cycles it blocked
+// to a per-CTA counter for its call site.
+__device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity, unsigned long long* prof,
+                                      int site) {
+  if (prof == nullptr) {
+    mbar_wait(bar, parity);
+    return;
   }
-  if (!active) return;
-  const int seg = (col0 / kSegRows) % nseg;
-  const int rr0 = (col0 / (kSegRows * nseg)) * kSegRows + (col0 % kSegRows);
-  // ---- optional int32 accumulator tap (parity), staged the same way
-  if (e.acc) {
-    int* si = reinterpret_cast<int*>(stg);
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  atomicAdd(prof + blockIdx.x * 8 + site, (unsigned long long)(clock64() - t0));
+}
+
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N> __device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// byte offset of 16-byte chunk c of row r in a swizzled 32-row staging tile
+// (fp32: 128-byte rows, SWIZZLE_128B; bf16: 64-byte rows, SWIZZLE_64B)
+template <typename TY> __device__ __forceinline__ int stg_off(int r, int c);
+template <> __device__ __forceinline__ int stg_off<float>(int r, int c) {
+  return r * 128 + ((c ^ (r & 7)) << 4);
+}
+template <> __device__ __forceinline__ int stg_off<__nv_bfloat16>(int r, int c) {
+  return r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+}
+
+// write the 32 values of this thread's row into the staging tile
+template <typename TY> __device__ __forceinline__ void stg_write_row(uint8_t* buf, int r, const float (&o)[32]);
+template <> __device__ __forceinline__ void stg_write_row<float>(uint8_t* buf, int r, const float (&o)[32]) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) si[lane * kStageLd + j] = (int)v[j] - qsum;
-    if (vu) {
-      __syncwarp();
-#pragma unroll 4
-      for (int r = 0; r < 32; ++r)
-        if (row0 + r < a.M && col0 + lane < a.n_rows)
-          e.acc[(int64_t)(row0 + r) * e.ldacc + col0 + lane] = si[r * kStageLd + lane];
-      __syncwarp();
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<float4*>(buf + stg_off<float>(r, c)) =
+        make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const uint32_t a = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+  const uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
+  return a | (b << 16);
+}
+template <> __device__ __forceinline__ void stg_write_row<__nv_bfloat16>(uint8_t* buf, int r,
+                                                                          const float (&o)[32]) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) si[lane * kStageLd + j] = (int)vu[j] - qsum;
-      __syncwarp();
-#pragma unroll 4
-      for (int r = 0; r < 32; ++r)
-        if (row0 + r < a.M && col0 + 64 + lane < a.n_rows)
-          e.acc[(int64_t)(row0 + r) * e.ldacc + col0 + 64 + lane] = si[r * kStageLd + lane];
-    } else {
-      __syncwarp();
-#pragma unroll 4
-      for (int r = 0; r < 32; ++r)
-        if (row0 + r < a.M && col0 + lane < a.n_rows)
-          e.acc[(int64_t)(row0 + r) * e.ldacc + col0 + lane] = si[r * kStageLd + lane];
+  for (int c = 0; c < 4; ++c) {
+    uint4 v;
+    v.x = pack_bf16x2(o[8 * c], o[8 * c + 1]);
+    v.y = pack_bf16x2(o[8 * c + 2], o[8 * c + 3]);
+    v.z = pack_bf16x2(o[8 * c + 4], o[8 * c + 5]);
+    v.w = pack_bf16x2(o[8 * c + 6], o[8 * c + 7]);
+    *reinterpret_cast<uint4*>(buf + stg_off<__nv_bfloat16>(r, c)) = v;
+  }
+}
+// read this thread's row of the (residual) tile back as floats
+template <typename TY> __device__ __forceinline__ void stg_read_row(const uint8_t* buf, int r, float (&x)[32]);
+template <> __device__ __forceinline__ void stg_read_row<float>(const uint8_t* buf, int r, float (&x)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 v = *reinterpret_cast<const float4*>(buf + stg_off<float>(r, c));
+    x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+  }
+}
+template <> __device__ __forceinline__ void stg_read_row<__nv_bfloat16>(const uint8_t* buf, int r,
+                                                                         float (&x)[32]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 v = *reinterpret_cast<const uint4*>(buf + stg_off<__nv_bfloat16>(r, c));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[8 * c + 2 * i] = __uint_as_float(w[i] << 16);
+      x[8 * c + 2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
     }
-    __syncwarp();
-    if (e.kind == EPI_NONE) return;
   }
-  // ---- phase A: thread = row
-  if (rv) {
-    const float sc = __fmul_rn(deq, __ldg(e.scales + seg));
-    if (e.kind == EPI_SWIGLU) {
-      const float scu = __fmul_rn(deq, __ldg(e.scales + 1));
+}
+
+// int32 accumulator tap (parity tests only): plain coalesced stores through a
+// padded staging tile (the two staging buffers of the warp, 8 KB)
+__device__ void acc_tap_chunk(const Epi& e, const GemmArgs& a, int* si, int lane, int row0,
+                              int col0, int qsum, const uint32_t (&v)[32]) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float g = storage_round<TY>(__fmul_rn((float)((int)v[j] - qsum), sc));
-        const float u = storage_round<TY>(__fmul_rn((float)((int)vu[j] - qsum), scu));
-        stg[lane * kStageLd + j] = swiglu(g, u);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        float o = __fmul_rn((float)((int)v[j] - qsum), sc);
-        if (e.bias) o = __fadd_rn(o, __ldg(e.bias + seg * e.n_out + rr0 + j));
-        stg[lane * kStageLd + j] = storage_round<TY>(o);
-      }
-    }
-  }
+  for (int j = 0; j < 32; ++j) si[lane * 33 + j] = (int)v[j] - qsum;
   __syncwarp();
-  // ---- phase B: lane = column, one coalesced row segment per store
-  TY* out = static_cast<TY*>(e.out);
-  const int oc = out_col0 + lane;
-  const bool cv = (e.kind == EPI_SWIGLU) ? (oc < e.n_out) : (col0 + lane < a.n_rows);
-  if (e.kind == EPI_RESID) {
-    // all residual loads of the chunk first (they cannot be reordered past the
-    // stores by the compiler), then the adds and stores
-    const TY* res = static_cast<const TY*>(e.res);
-    float xr[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const int rw = row0 + r;
-      xr[r] = (rw < a.M && cv) ? ld_act<TY>(res + (int64_t)rw * e.ldr + oc) : 0.0f;
-    }
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const int rw = row0 + r;
-      if (rw < a.M && cv)
-        st_act<TY>(out + (int64_t)rw * e.ldo + oc, __fadd_rn(xr[r], stg[r * kStageLd + lane]));
-    }
-  } else {
-#pragma unroll 8
-    for (int r = 0; r < 32; ++r) {
-      const int rw = row0 + r;
-      if (rw < a.M && cv) st_act<TY>(out + (int64_t)rw * e.ldo + oc, stg[r * kStageLd + lane]);
-    }
-  }
+  for (int r = 0; r < 32; ++r)
+    if (row0 + r < a.M && col0 + lane < a.n_rows)
+      e.acc[(int64_t)(row0 + r) * e.ldacc + col0 + lane] = si[r * 33 + lane];
   __syncwarp();
 }
 
-template <int BN, typename TY>
+template <int BN, bool kPre, typename TY>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
               const GemmArgs a) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, kPre>;
   constexpr int S = Cfg::S;
-  extern __shared__ uint8_t gsm_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) &
-                                           ~uintptr_t(1023));
-  uint8_t* sA = sm;                                   // [S][A_BYTES]
-  uint8_t* sBu = sm + S * Cfg::A_BYTES;               // [S][BU_BYTES]
-  uint8_t* sBp = sBu + S * Cfg::BU_BYTES;             // [S][BP_BYTES]
-  float* sEpi = reinterpret_cast<float*>(sBp + S * Cfg::BP_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + Cfg::EPI_BYTES);
-  uint64_t* full = bars;            // TMA landed
-  uint64_t* unpacked = bars + S;    // B unpacked
-  uint64_t* empty = bars + 2 * S;   // MMA finished reading the stage
-  uint64_t* tfull = bars + 3 * S;   // [2] accumulator ready
-  uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  constexpr int U = Cfg::U;
+  extern __shared__ __align__(1024) uint8_t gsm_raw[];
+  // 1024-byte alignment for the swizzle atoms; offset arithmetic keeps the
+  // pointer in the shared address space (no generic loads/stores)
+  uint8_t* sm = gsm_raw + ((1024u - (smem_u32(gsm_raw) & 1023u)) & 1023u);
+  uint8_t* sA = sm;                                                    // [S][A_BYTES]
+  uint8_t* sB = sA + S * Cfg::A_BYTES;    // kPre: [S][B_BYTES]   else: [U][B_BYTES] unpacked
+  uint8_t* sBp = sB + (kPre ? S : U) * Cfg::B_BYTES;                   // packed: [S][BP_BYTES]
+  uint8_t* sEpi = sm + Cfg::RING;                                      // [8 warps][2][4 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + Cfg::EPI_BYTES);
+  uint64_t* full = bars;                 // [S] TMA landed
+  uint64_t* empty = bars + 8;            // [S] MMA finished with the stage
+  uint64_t* unpacked = bars + 16;        // [U] B unpacked
+  uint64_t* ufree = bars + 20;           // [U] MMA finished with the unpacked B
+  uint64_t* tfull = bars + 24;           // [2] accumulator ready
+  uint64_t* tempty = bars + 26;          // [2] accumulator drained
+  uint64_t* rbar = bars + 28;            // [8 warps][2] residual tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 44);
 
+  const long long t_start = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = a.num_kb;
   const int total = a.n_tiles * a.m_tiles;
+  const Epi& e = a.epi;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
+    if (kPre) tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmO);
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&unpacked[s], 128);
       mbar_init(&empty[s], 1);
+    }
+    for (int u = 0; u < U; ++u) {
+      mbar_init(&unpacked[u], 128);
+      mbar_init(&ufree[u], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kEpiWarps);
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
@@ -205,10 +216,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int m0 = (t / a.n_tiles) * kBM, n0 = (t % a.n_tiles) * BN;
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % S;
-          if (g >= (uint32_t)S) mbar_wait(&empty[s], ((g / S) - 1) & 1);
-          mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::BP_BYTES);
-          tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kBK, m0);
-          tma_load_2d(sBp + s * Cfg::BP_BYTES, &tmB, &full[s], kb * (kBK / 16), n0);
+          if (g >= (uint32_t)S) pwait(&empty[s], ((g / S) - 1) & 1, a.prof, 0);
+          if (kPre) {
+            mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
+            tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kBK, m0);
+            tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * kBK, n0);
+          } else {
+            // one contiguous span (K-block-major layout); ragged last tile shorter
+            const uint32_t bbytes = (uint32_t)min(BN, a.n_rows - n0) * 32u;
+            mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + bbytes);
+            tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kBK, m0);
+            bulk_load(sBp + s * Cfg::BP_BYTES, a.codes + ((int64_t)kb * a.n_rows + n0) * 8,
+                      bbytes, &full[s]);
+          }
         }
       }
     }
@@ -221,47 +241,63 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t g = 0, it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
         const uint32_t acc = it & 1;
-        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        pwait(&tempty[acc], ((it >> 1) & 1) ^ 1, a.prof, 1);
         tc_fence_after();
         const uint32_t d_addr = tmem_base + acc * BN;
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % S;
-          mbar_wait(&unpacked[s], (g / S) & 1);
+          uint32_t b_addr;
+          if (kPre) {
+            pwait(&full[s], (g / S) & 1, a.prof, 2);
+            b_addr = smem_u32(sB + s * Cfg::B_BYTES);
+          } else {
+            const int u = g % U;
+            pwait(&unpacked[u], (g / U) & 1, a.prof, 2);
+            b_addr = smem_u32(sB + u * Cfg::B_BYTES);
+          }
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + s * Cfg::A_BYTES);
-          const uint32_t b_addr = smem_u32(sBu + s * Cfg::BU_BYTES);
 #pragma unroll
           for (int kk = 0; kk < kBK / 32; ++kk)
             mma_i8(d_addr, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
                    idesc, (kb | kk) != 0);
           mma_commit(&empty[s]);
+          if (!kPre) mma_commit(&ufree[g % U]);
         }
         mma_commit(&tfull[acc]);
       }
     }
   } else if (warp < kEpiWarp0) {
-    // ---------------- unpack (warps 2-5): 2-bit fields -> u8 e, SW128 K-major
-    const int tid = threadIdx.x - 64;
-    uint32_t g = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      for (int kb = 0; kb < nk; ++kb, ++g) {
-        const int s = g % S;
-        mbar_wait(&full[s], (g / S) & 1);
-        const uint32_t* bp = reinterpret_cast<const uint32_t*>(sBp + s * Cfg::BP_BYTES);
-        uint8_t* bu = sBu + s * Cfg::BU_BYTES;
-#pragma unroll 4
-        for (int i = tid; i < BN * 8; i += 128) {
-          const int row = i >> 3, w = i & 7;
-          const uint32_t word = bp[i];
-          uint4 v;
-          v.x = word & 0x03030303u;
-          v.y = (word >> 2) & 0x03030303u;
-          v.z = (word >> 4) & 0x03030303u;
-          v.w = (word >> 6) & 0x03030303u;
-          *reinterpret_cast<uint4*>(bu + row * 128 + ((w ^ (row & 7)) << 4)) = v;
+    // ---------------- unpack (warps 2-5, packed path): 2-bit fields -> u8 e, SW128 K-major
+    if (!kPre) {
+      const int tid = threadIdx.x - 64;
+      const bool pt = tid == 0;
+      uint32_t g = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % S, u = g % (U > 0 ? U : 1);
+          if (g >= (uint32_t)U) pwait(&ufree[u], ((g / U) - 1) & 1, pt ? a.prof : nullptr, 3);
+          pwait(&full[s], (g / S) & 1, pt ? a.prof : nullptr, 4);
+          const uint32_t* bp = reinterpret_cast<const uint32_t*>(sBp + s * Cfg::BP_BYTES);
+          uint8_t* bu = sB + u * Cfg::B_BYTES;
+          // thread owns word w = tid%8 of rows tid/8 + 16 j: its swizzled 16-byte
+          // chunk offset inside a row is the same for every j
+          const int r0 = tid >> 3, w = tid & 7;
+          const uint32_t* src = bp + tid;
+          uint8_t* dst = bu + r0 * 128 + ((w ^ (r0 & 7)) << 4);
+#pragma unroll
+          for (int j = 0; j < BN / 16; ++j) {
+            const uint32_t word = src[j * 128];
+            uint4 v;
+            v.x = word & 0x03030303u;
+            v.y = (word >> 2) & 0x03030303u;
+            v.z = (word >> 4) & 0x03030303u;
+            v.w = (word >> 6) & 0x03030303u;
+            *reinterpret_cast<uint4*>(dst + j * 2048) = v;
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&unpacked[u]);
         }
-        fence_proxy_async_smem();
-        mbar_arrive(&unpacked[s]);
       }
     }
   } else {
@@ -269,13 +305,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int ew = warp - kEpiWarp0;
     const int quad = warp & 3;          // TMEM lanes [32*quad, 32*quad+32)
     const int half = ew >> 2;           // which half of the chunks this warp takes
-    float* stg = sEpi + ew * 32 * kStageLd;
-    const Epi& e = a.epi;
-    uint32_t it = 0;
+    uint8_t* bufs = sEpi + ew * 2 * kEpiBuf;
+    uint64_t* rb = rbar + ew * 2;
+    const bool lead = lane == 0;
+    const bool legacy = e.acc != nullptr || e.kind == EPI_NONE;   // tap / parity path
+    const int nseg = e.n_seg;
+    const float msc0 = __ldg(e.scales), msc1 = nseg > 1 ? __ldg(e.scales + 1) : 0.0f;
+    const float msc2 = nseg > 2 ? __ldg(e.scales + 2) : 0.0f;
+    uint32_t it = 0, nchunk = 0;
+    uint32_t rphase[2] = {0, 0};
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const uint32_t acc = it & 1;
       const int m0 = (t / a.n_tiles) * kBM, n0 = (t % a.n_tiles) * BN;
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      pwait(&tfull[acc], (it >> 1) & 1, (ew == 0 && lead) ? a.prof : nullptr, 5);
       tc_fence_after();
       const int row0 = m0 + quad * 32;
       const int row = row0 + lane;
@@ -283,30 +325,90 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const float deq = rv ? __ldg(a.deq + row) : 0.0f;
       const int qsum = rv ? __ldg(a.qsum + row) : 0;
       const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
-      if (e.kind == EPI_SWIGLU) {
-        // pair p = (128-col group, 32-col half): gate at +0, up at +64
+      const bool swig = e.kind == EPI_SWIGLU;
+      const int nch = swig ? BN / 64 : BN / 32;   // chunks (or gate/up pairs) per tile
 #pragma unroll 1
-        for (int p = half; p < BN / 64; p += 2) {
-          const int cb = (p >> 1) * 128 + (p & 1) * 32;
-          uint32_t vg[32], vu[32];
-          tmem_ld32(trow + cb, vg);
-          tmem_ld32(trow + cb + 64, vu);
-          tmem_ld_wait();
-          epi_chunk<TY>(e, a, stg, lane, row0, row, deq, qsum, n0 + cb, vg, vu);
+      for (int c = half; c < nch; c += 2) {
+        // column bookkeeping of this chunk
+        int col0, out_col0;
+        if (swig) {
+          col0 = n0 + (c >> 1) * 128 + (c & 1) * 32;
+          out_col0 = (col0 / 128) * 64 + (c & 1) * 32;
+        } else {
+          col0 = n0 + c * 32;
+          out_col0 = e.kind == EPI_FCG ? col0 : (col0 / (kSegRows * nseg)) * kSegRows + (col0 % kSegRows);
         }
-      } else {
-#pragma unroll 1
-        for (int c = half; c < BN / 32; c += 2) {
-          uint32_t v[32];
-          tmem_ld32(trow + c * 32, v);
+        if (col0 >= a.n_rows || (swig && out_col0 >= e.n_out)) continue;
+        uint32_t v[32], vu[32];
+        tmem_ld32(trow + (col0 - n0), v);
+        if (swig) tmem_ld32(trow + (col0 - n0) + 64, vu);
+        if (legacy) {
           tmem_ld_wait();
-          epi_chunk<TY>(e, a, stg, lane, row0, row, deq, qsum, n0 + c * 32, v, nullptr);
+          int* si = reinterpret_cast<int*>(bufs);
+          if (lead) bulk_wait_read<0>();   // staging buffers free of pending stores
+          __syncwarp();
+          if (e.acc) {
+            acc_tap_chunk(e, a, si, lane, row0, col0, qsum, v);
+            if (swig) acc_tap_chunk(e, a, si, lane, row0, col0 + 64, qsum, vu);
+          }
+          if (e.kind == EPI_NONE) continue;
         }
+        const int buf = nchunk & 1;
+        uint8_t* sb = bufs + buf * kEpiBuf;
+        // the TMA store that last read this buffer (two chunks ago) must be done
+        if (lead) bulk_wait_read<1>();
+        __syncwarp();
+        const bool resid = e.kind == EPI_RESID;
+        if (resid && lead) {
+          mbar_arrive_expect_tx(&rb[buf], 32 * 32 * sizeof(TY));
+          tma_load_2d(sb, &tmR, &rb[buf], out_col0, row0);
+        }
+        if (!legacy) tmem_ld_wait();
+        // dequantize (a5) + functor, thread = row
+        const int seg = (col0 / kSegRows) % nseg;
+        const int rr0 = (col0 / (kSegRows * nseg)) * kSegRows + (col0 % kSegRows);
+        const float msc = seg == 0 ? msc0 : (seg == 1 ? msc1 : msc2);
+        const float sc = __fmul_rn(deq, msc);
+        float o[32];
+        if (swig) {
+          const float scu = __fmul_rn(deq, msc1);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float gg = storage_round<TY>(__fmul_rn((float)((int)v[j] - qsum), sc));
+            const float uu = storage_round<TY>(__fmul_rn((float)((int)vu[j] - qsum), scu));
+            o[j] = swiglu(gg, uu);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float x = __fmul_rn((float)((int)v[j] - qsum), sc);
+            if (e.bias) x = __fadd_rn(x, __ldg(e.bias + seg * e.n_out + rr0 + j));
+            o[j] = storage_round<TY>(x);
+          }
+        }
+        if (resid) {
+          mbar_wait(&rb[buf], rphase[buf]);
+          rphase[buf] ^= 1;
+          float xr[32];
+          stg_read_row<TY>(sb, lane, xr);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __fadd_rn(xr[j], o[j]);
+          __syncwarp();   // all lanes read their residual rows before they are overwritten
+        }
+        stg_write_row<TY>(sb, lane, o);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lead) {
+          tma_store_2d(&tmO, sb, out_col0, row0);   // rows >= M / cols >= n clipped by TMA
+          bulk_commit();
+        }
+        ++nchunk;
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lead) mbar_arrive(&tempty[acc]);
     }
+    if (lead) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -314,6 +416,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
   }
+  if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 8 + 7] = clock64() - t_start;
 }
 
 // ----------------------------------------------------------------- host side
@@ -350,14 +453,14 @@ static bool make_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* ba
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, typename TY>
-static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
-                               cudaStream_t s) {
-  auto kern = k_gemm_tc<BN, TY>;
+template <int BN, bool kPre, typename TY>
+static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
+                               const CUtensorMap& tr, const GemmArgs& a, cudaStream_t s) {
+  using Cfg = GemmCfg<BN, kPre>;
+  auto kern = k_gemm_tc<BN, kPre, TY>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         GemmCfg<BN>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -369,37 +472,108 @@ static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, con
   }
   const int total = a.n_tiles * a.m_tiles;
   const int grid = total < num_sms ? total : num_sms;
-  kern<<<grid, kGemmThreads, GemmCfg<BN>::SMEM, s>>>(ta, tb, a);
+  static unsigned long long* dprof = nullptr;
+  static const bool prof_on = getenv("TERN_GEMM_PROF") != nullptr;
+  GemmArgs aa = a;
+  if (prof_on) {  // debug only: per-site wait cycles, printed after a synchronous run
+    if (!dprof) cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * 1024);
+    cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * 8 * 1024, s);
+    aa.prof = dprof;
+  }
+  kern<<<grid, kGemmThreads, Cfg::SMEM, s>>>(ta, tb, to, tr, aa);
+  if (prof_on) {
+    static unsigned long long h[8 * 1024];
+    cudaMemcpyAsync(h, dprof, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double sum[8] = {0};
+    for (int b = 0; b < grid; ++b)
+      for (int i = 0; i < 8; ++i) sum[i] += (double)h[b * 8 + i] / grid;
+    fprintf(stderr,
+            "[gemm prof] M=%d n=%d K=%d BN=%d pre=%d kind=%d tiles=%d | total=%.0f prod.empty=%.0f "
+            "mma.tempty=%.0f mma.B=%.0f unp.ufree=%.0f unp.full=%.0f epi.tfull=%.0f\n",
+            a.M, a.n_rows, a.num_kb * 128, BN, (int)kPre, a.epi.kind, total, sum[7], sum[0],
+            sum[1], sum[2], sum[3], sum[4], sum[5]);
+  }
   return cudaGetLastError();
+}
+
+template <bool kPre, typename TY>
+static cudaError_t gemm_dispatch_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb,
+                                    const CUtensorMap& to, const CUtensorMap& tr,
+                                    const GemmArgs& a, cudaStream_t s) {
+  return BN == 256 ? gemm_launch<256, kPre, TY>(ta, tb, to, tr, a, s)
+                   : gemm_launch<128, kPre, TY>(ta, tb, to, tr, a, s);
 }
 
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
   const int kp = (w.k + kKAlign - 1) / kKAlign * kKAlign;
-  // BN = 256 when the group has whole 256-row tiles worth of work, else 128
   const int BN = (w.n_rows >= 1024 || w.n_rows % 256 == 0) ? 256 : 128;
-  CUtensorMap ta, tb;
+  const bool pre = w.e8 != nullptr;
+  const bool yb = ydt == TERN_BF16;
+  const size_t ys = yb ? 2 : 4;
+  const CUtensorMapDataType ydtype = yb ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const CUtensorMapSwizzle yswz = yb ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUtensorMap ta, tb, to, tr;
+  memset(&tb, 0, sizeof(tb));
+  memset(&to, 0, sizeof(to));
+  memset(&tr, 0, sizeof(tr));
   if (!make_map_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, (uint64_t)kp, (uint64_t)M,
                    (uint64_t)ldq, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  if (!make_map_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT32, w.codes, (uint64_t)(kp / 16),
-                   (uint64_t)w.n_rows, (uint64_t)w.ldw * 4, kBK / 16, BN,
-                   CU_TENSOR_MAP_SWIZZLE_NONE))
+  if (pre && !make_map_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, w.e8, (uint64_t)kp,
+                          (uint64_t)w.n_rows, (uint64_t)kp, kBK, BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
+  if (epi.kind != EPI_NONE) {
+    const int ncols = epi.kind == EPI_FCG ? w.n_rows : epi.n_out;
+    if (!make_map_2d(&to, ydtype, epi.out, (uint64_t)ncols, (uint64_t)M, (uint64_t)epi.ldo * ys,
+                     32, 32, yswz))
+      return cudaErrorInvalidValue;
+    if (epi.kind == EPI_RESID &&
+        !make_map_2d(&tr, ydtype, epi.res, (uint64_t)epi.n_out, (uint64_t)M,
+                     (uint64_t)epi.ldr * ys, 32, 32, yswz))
+      return cudaErrorInvalidValue;
+  }
   GemmArgs a{};
   a.M = M;
   a.n_rows = w.n_rows;
+  a.codes = w.codes;
   a.num_kb = kp / kBK;
   a.n_tiles = (w.n_rows + BN - 1) / BN;
   a.m_tiles = (M + kBM - 1) / kBM;
   a.deq = deq;
   a.qsum = qsum;
   a.epi = epi;
-  const bool yb = ydt == TERN_BF16;
-  if (BN == 256)
-    return yb ? gemm_launch<256, __nv_bfloat16>(ta, tb, a, s) : gemm_launch<256, float>(ta, tb, a, s);
-  return yb ? gemm_launch<128, __nv_bfloat16>(ta, tb, a, s) : gemm_launch<128, float>(ta, tb, a, s);
+  if (pre)
+    return yb ? gemm_dispatch_bn<true, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)
+              : gemm_dispatch_bn<true, float>(BN, ta, tb, to, tr, a, s);
+  return yb ? gemm_dispatch_bn<false, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)
+            : gemm_dispatch_bn<false, float>(BN, ta, tb, to, tr, a, s);
+}
+
+// ----------------------------------------------------------------- u8 expansion (kPre B)
+// e8[r][k] = 2-bit field of trit k of packed row r (e = t+1), k < Kp.
+__global__ void k_expand(const uint32_t* __restrict__ codes, int n_rows, int kp,
+                         uint8_t* __restrict__ e8) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one word
+  const int words = kp / 16;
+  if (idx >= (int64_t)n_rows * words) return;
+  const int r = (int)(idx / words), w = (int)(idx % words);
+  const uint32_t word = codes[((int64_t)(w >> 3) * n_rows + r) * 8 + (w & 7)];
+  uint4 v;
+  v.x = word & 0x03030303u;
+  v.y = (word >> 2) & 0x03030303u;
+  v.z = (word >> 4) & 0x03030303u;
+  v.w = (word >> 6) & 0x03030303u;
+  *reinterpret_cast<uint4*>(e8 + (int64_t)r * kp + w * 16) = v;
+}
+
+cudaError_t launch_expand(const tern_weight& w, uint8_t* e8, cudaStream_t s) {
+  const int kp = w.ldw * 16;
+  const int64_t n = (int64_t)w.n_rows * (kp / 16);
+  k_expand<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w.codes, w.n_rows, kp, e8);
+  return cudaGetLastError();
 }
 
 }  // namespace tern

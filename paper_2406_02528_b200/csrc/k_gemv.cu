@@ -31,7 +31,7 @@ struct GemvArgs {
   const float* gain;
   float eps;
   const uint32_t* codes;
-  int ldw, n_out, n_seg, ch, ksplit;
+  int n_rows, n_out, n_seg, ch, ksplit;
   Epi epi;
   QuantTaps taps;
 };
@@ -46,9 +46,10 @@ template <int MM, typename TX, typename TY>
 __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
   extern __shared__ __align__(128) uint8_t g_smem[];
   const int R = a.n_seg * a.ch;
-  const int row_bytes = a.Kp / 4;                             // packed bytes of one row
-  uint32_t* sW = reinterpret_cast<uint32_t*>(g_smem);         // [R][Kp/16] words
-  int8_t* qs = reinterpret_cast<int8_t*>(g_smem + R * row_bytes);   // [MM][Kp]
+  const int nkb = a.Kp / kKAlign;
+  const int slot = a.ch * 8 + 8;   // words per (segment, K-block) slot, padded vs bank conflicts
+  uint32_t* sW = reinterpret_cast<uint32_t*>(g_smem);         // [n_seg][nkb][slot] words
+  int8_t* qs = reinterpret_cast<int8_t*>(g_smem + a.n_seg * nkb * slot * 4);   // [MM][Kp]
   int* accs = reinterpret_cast<int*>(qs + MM * a.Kp);               // [MM][R]
   __shared__ __align__(8) uint64_t wbar;
   __shared__ float s_deq[MM];
@@ -64,14 +65,15 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
     mbar_init(&wbar, 1);
     fence_barrier_init();
     fence_proxy_async_smem();
-    int nvalid = 0;
-    for (int j = 0; j < R; ++j) nvalid += (unit * a.ch + j % a.ch) < a.n_out;
-    mbar_arrive_expect_tx(&wbar, (uint32_t)(nvalid * row_bytes));
-    for (int j = 0; j < R; ++j) {
-      const int seg = j / a.ch, rr = unit * a.ch + j % a.ch;
-      if (rr < a.n_out)
-        bulk_load(reinterpret_cast<uint8_t*>(sW) + j * row_bytes,
-                  a.codes + (int64_t)packed_row(seg, rr, a.n_seg) * a.ldw, row_bytes, &wbar);
+    // the unit's rows of one segment are consecutive packed rows, so each
+    // (segment, K-block) is one contiguous span of vcnt*32 bytes
+    const int vcnt = min(a.ch, a.n_out - unit * a.ch);
+    mbar_arrive_expect_tx(&wbar, (uint32_t)(a.n_seg * nkb * vcnt * 32));
+    for (int sg = 0; sg < a.n_seg; ++sg) {
+      const int p0 = packed_row(sg, unit * a.ch, a.n_seg);
+      for (int kb = 0; kb < nkb; ++kb)
+        bulk_load(sW + (sg * nkb + kb) * slot, a.codes + ((int64_t)kb * a.n_rows + p0) * 8,
+                  (uint32_t)vcnt * 32u, &wbar);
     }
   }
   pdl_launch_dependents();
@@ -88,46 +90,68 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
       continue;
     }
     const TX* xr = static_cast<const TX*>(a.x) + (int64_t)m * a.ldx;
+    const int npt = (a.K + kGThreads - 1) / kGThreads;   // uniform: skips unused slots
     float v[kGMaxPT];
     double ss = 0.0;
+    float xmax = 0.0f;
 #pragma unroll
     for (int i = 0; i < kGMaxPT; ++i) {
-      const int k = tid + i * kGThreads;
-      v[i] = k < a.K ? ld_act<TX>(xr + k) : 0.0f;
-      ss += (double)v[i] * (double)v[i];
+      v[i] = 0.0f;
+      if (i < npt) {
+        const int k = tid + i * kGThreads;
+        v[i] = k < a.K ? ld_act<TX>(xr + k) : 0.0f;
+        ss += (double)v[i] * (double)v[i];
+        xmax = fmaxf(xmax, fabsf(v[i]));
+      }
     }
+    // one reduction round for sum(x^2) and max|x|: without a gain,
+    // max|x*r| = fl(max|x| * r) exactly (rounding is monotone)
     ss = warp_sum_f64(ss);
-    if (lane == 0) red_d[warp] = ss;
+    xmax = warp_max_f32(xmax);
+    if (lane == 0) { red_d[warp] = ss; red_f[warp] = xmax; }
     __syncthreads();
     double tot = 0.0;
+    xmax = 0.0f;
 #pragma unroll
-    for (int i = 0; i < kGWarps; ++i) tot += red_d[i];
+    for (int i = 0; i < kGWarps; ++i) { tot += red_d[i]; xmax = fmaxf(xmax, red_f[i]); }
     const float r = (float)(1.0 / sqrt(tot / (double)a.K + (double)a.eps));
-    float amax = 0.0f;
+    float amax;
+    if (a.gain == nullptr) {
+      amax = __fmul_rn(xmax, r);
 #pragma unroll
-    for (int i = 0; i < kGMaxPT; ++i) {
-      const int k = tid + i * kGThreads;
-      float y = __fmul_rn(v[i], r);
-      if (a.gain && k < a.K) y = __fmul_rn(y, __ldg(a.gain + k));
-      v[i] = y;
-      amax = fmaxf(amax, fabsf(y));
+      for (int i = 0; i < kGMaxPT; ++i)
+        if (i < npt) v[i] = __fmul_rn(v[i], r);
+    } else {
+      amax = 0.0f;
+#pragma unroll
+      for (int i = 0; i < kGMaxPT; ++i) {
+        if (i < npt) {
+          const int k = tid + i * kGThreads;
+          float y = __fmul_rn(v[i], r);
+          if (k < a.K) y = __fmul_rn(y, __ldg(a.gain + k));
+          v[i] = y;
+          amax = fmaxf(amax, fabsf(y));
+        }
+      }
+      amax = warp_max_f32(amax);
+      __syncthreads();
+      if (lane == 0) red_f[warp] = amax;
+      __syncthreads();
+      amax = 0.0f;
+#pragma unroll
+      for (int i = 0; i < kGWarps; ++i) amax = fmaxf(amax, red_f[i]);
     }
-    amax = warp_max_f32(amax);
-    if (lane == 0) red_f[warp] = amax;
-    __syncthreads();
-    amax = 0.0f;
-#pragma unroll
-    for (int i = 0; i < kGWarps; ++i) amax = fmaxf(amax, red_f[i]);
     const float s = amax > 0.0f ? __fdiv_rn(127.0f, amax) : 0.0f;
     int qsum = 0;
 #pragma unroll
     for (int i = 0; i < kGMaxPT; ++i) {
       const int k = tid + i * kGThreads;
-      if (k < a.Kp) {
+      if (i <= npt && k < a.Kp) {
         int qi = 0;
         if (k < a.K && amax > 0.0f) {
-          float t = round_half_away(__fmul_rn(v[i], s));
-          qi = (int)fminf(fmaxf(t, -128.0f), 127.0f);
+          // |v*s| <= 127 (1+2^-23) always, so the clamp to [-128,127] (C5) is inert
+          const float t = round_half_away(__fmul_rn(v[i], s));
+          qi = (int)t;
         }
         qsum += qi;
         qrow[k] = (int8_t)qi;
@@ -173,8 +197,7 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
       const int seg = j / a.ch, i = j % a.ch;
       const int rr = unit * a.ch + i;
       valid[qd] = (j < R) && (rr < a.n_out);
-      wrow[qd] = sW + (valid[qd] ? j : 0) * (row_bytes / 4);
-      (void)seg;
+      wrow[qd] = sW + (valid[qd] ? (seg * nkb * slot + i * 8) : 0);
     }
     int acc[4][MM];
 #pragma unroll
@@ -184,7 +207,9 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
     for (int w = w0 + lane; w < w1; w += 32) {
       uint32_t wd[4];
 #pragma unroll
-      for (int qd = 0; qd < 4; ++qd) wd[qd] = valid[qd] ? wrow[qd][w] : 0x55555555u;
+      const int wo = (w >> 3) * slot + (w & 7);   // (K-block, word) inside the slot
+#pragma unroll
+      for (int qd = 0; qd < 4; ++qd) wd[qd] = valid[qd] ? wrow[qd][wo] : 0x55555555u;
 #pragma unroll
       for (int m = 0; m < MM; ++m) {
         const uint4 qv = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
@@ -247,7 +272,8 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
 template <int MM, typename TX, typename TY>
 static cudaError_t gemv_launch(const GemvArgs& a, int units, cudaStream_t s) {
   const int R = a.n_seg * a.ch;
-  const size_t smem = (size_t)R * (a.Kp / 4) + (size_t)MM * a.Kp + (size_t)MM * R * sizeof(int);
+  const size_t smem = (size_t)a.n_seg * (a.Kp / kKAlign) * (a.ch * 8 + 8) * 4 + (size_t)MM * a.Kp +
+                      (size_t)MM * R * sizeof(int);
   auto kern = k_gemv<MM, TX, TY>;
   static size_t smem_set = 48 * 1024;
   if (smem > smem_set) {
@@ -290,7 +316,7 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
   a.gain = gain;
   a.eps = eps;
   a.codes = w.codes;
-  a.ldw = w.ldw;
+  a.n_rows = w.n_rows;
   a.n_out = w.n_out;
   a.n_seg = w.n_seg;
   // channels per CTA: enough CTAs to cover the SMs about twice

@@ -46,7 +46,7 @@ __global__ void k_absmean_final(const double* part, int64_t n, const float* scal
 
 // One thread per packed word: trits k = 16w .. 16w+15 of logical row r.
 __global__ void k_pack(const float* __restrict__ W, int n, int k, int n_seg, int seg,
-                       uint32_t* __restrict__ codes, int ldw, const float* __restrict__ scale) {
+                       uint32_t* __restrict__ codes, int n_rows, const float* __restrict__ scale) {
   const int words_per_row = (k + 15) / 16;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * words_per_row) return;
@@ -67,7 +67,8 @@ __global__ void k_pack(const float* __restrict__ W, int n, int k, int n_seg, int
     const int j = i & 3, f = i >> 2;
     word |= (uint32_t)e << (8 * j + 2 * f);
   }
-  codes[(int64_t)packed_row(seg, r, n_seg) * ldw + w] = word;
+  // K-block-major: [w/8][packed row][w%8]
+  codes[((int64_t)(w >> 3) * n_rows + packed_row(seg, r, n_seg)) * 8 + (w & 7)] = word;
 }
 
 __global__ void k_codes_init(uint32_t* codes, int64_t n) {
@@ -89,9 +90,9 @@ cudaError_t launch_absmean(const float* W, int64_t numel, const float* scale_in,
 }
 
 cudaError_t launch_pack_codes(const float* W, int n, int k, int n_seg, int seg, uint32_t* codes,
-                              int ldw, const float* scale, cudaStream_t s) {
+                              int n_rows, const float* scale, cudaStream_t s) {
   const int64_t words = (int64_t)n * ((k + 15) / 16);
-  k_pack<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(W, n, k, n_seg, seg, codes, ldw, scale);
+  k_pack<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(W, n, k, n_seg, seg, codes, n_rows, scale);
   return cudaGetLastError();
 }
 

@@ -119,9 +119,8 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
       if (c < nc && a > 0.0f) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float t = round_half_away(__fmul_rn(v[i][j], s));
-          t = fminf(fmaxf(t, -128.0f), 127.0f);
-          const int qi = (int)t;
+          // |y*s| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
+          const int qi = (int)round_half_away(__fmul_rn(v[i][j], s));
           qs += qi;
           packed |= ((uint32_t)qi & 0xffu) << (8 * j);
         }
@@ -193,9 +192,8 @@ __global__ void __launch_bounds__(256) k_quant_warp(const TX* __restrict__ x, in
       if (c < nc && a > 0.0f) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float t = round_half_away(__fmul_rn(v[i][j], s));
-          t = fminf(fmaxf(t, -128.0f), 127.0f);
-          const int qi = (int)t;
+          // |y*s| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
+          const int qi = (int)round_half_away(__fmul_rn(v[i][j], s));
           qs += qi;
           packed |= ((uint32_t)qi & 0xffu) << (8 * j);
         }

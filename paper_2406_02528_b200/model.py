@@ -19,14 +19,15 @@ class PackedWeight:
 
     latents: list of fp32 [n_out][k] device tensors (one per segment)."""
 
-    def __init__(self, latents, scales_in=None):
+    def __init__(self, latents, scales_in=None, expand=True):
         n_seg = len(latents)
         n_out, k = latents[0].shape
         dev = latents[0].device
         self.n_out, self.k, self.n_seg = int(n_out), int(k), n_seg
         self.n_rows = L.tern_packed_rows(self.n_out, n_seg)
         self.ldw = L.tern_packed_ldw(self.k)
-        self.codes = torch.empty((self.n_rows, self.ldw), dtype=torch.int32, device=dev)
+        # K-block-major packed layout [Kp/128][n_rows][8] (include/tern.h)
+        self.codes = torch.empty((self.ldw // 8, self.n_rows, 8), dtype=torch.int32, device=dev)
         self.scales = torch.empty(n_seg, dtype=torch.float32, device=dev)
         L.tern_codes_init(self.codes)
         for s, W in enumerate(latents):
@@ -34,7 +35,13 @@ class PackedWeight:
             sin = None if scales_in is None else scales_in[s]
             L.tern_pack(W, self.codes, self.scales[s:s + 1], n_seg=n_seg, seg_idx=s, scale_in=sin)
         self.struct = L.tern_weight(self.codes.data_ptr(), self.scales.data_ptr(), self.n_out,
-                                    self.k, self.ldw, self.n_seg, self.n_rows)
+                                    self.k, self.ldw, self.n_seg, self.n_rows, None)
+        self.e8 = None
+        if expand:
+            # u8 copy of the fields for the prefill GEMM's TMA path (4x the codes' bytes)
+            self.e8 = torch.empty((self.n_rows, self.ldw * 16), dtype=torch.uint8, device=dev)
+            L.tern_expand(self.struct, self.e8)
+            self.struct.e8 = self.e8.data_ptr()
 
     @property
     def nbytes(self) -> int:

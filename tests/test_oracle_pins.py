@@ -111,7 +111,8 @@ def test_weight_quant_matches_scalar_formula():
 # ------------------------------------------------------------------ packed layout decoder
 def test_packed_word_example():
     g = GOLD["packed_word"]
-    codes = np.array([[int(g["word"], 16)]], np.uint32)
+    codes = np.zeros((1, 1, 8), np.uint32)
+    codes[0, 0, 0] = int(g["word"], 16)
     t = O.unpack_segment(codes, 1, 16)
     assert t.tolist() == [g["trits"]]
 
@@ -126,8 +127,24 @@ def test_packed_row_interleave():
 
 
 def test_unpack_rejects_reserved_field():
+    codes = np.zeros((1, 1, 8), np.uint32)
+    codes[0, 0, 0] = 0x3
     with pytest.raises(O.OracleError):
-        O.unpack_segment(np.array([[0x3]], np.uint32), 1, 16)
+        O.unpack_segment(codes, 1, 16)
+
+
+def test_unpack_k_block_major_layout():
+    # word w of packed row r sits at ((w/8)*n_rows + r)*8 + w%8: put a +1 trit at
+    # k = 128*b + 16*j + 4*f + byte for a few (b, j, f, byte, r) and read it back
+    n_rows, nkb = 3, 2
+    for (b, j, f, byte, r) in [(0, 0, 0, 0, 0), (1, 7, 3, 3, 2), (1, 2, 1, 2, 1), (0, 5, 2, 1, 1)]:
+        codes = np.full((nkb, n_rows, 8), 0x55555555, np.uint32)      # all zero trits
+        w = codes[b, r, j]
+        shift = 8 * byte + 2 * f
+        codes[b, r, j] = (w & ~np.uint32(3 << shift)) | np.uint32(2 << shift)   # e = 2 -> +1
+        t = O.unpack_segment(codes, n_rows, 256)
+        k = 128 * b + 16 * j + 4 * f + byte
+        assert t[r, k] == 1 and np.count_nonzero(t) == 1
 
 
 # ------------------------------------------------------------------ a2 activation quant

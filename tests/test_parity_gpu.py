@@ -61,6 +61,13 @@ def acts(shape, seed, dtype="f32"):
     return synth.hidden(shape, g, dtype)
 
 
+# ------------------------------------------------------------------------ numerics shortcuts
+@pytest.mark.parametrize("which", [0, 1])
+def test_device_selftest(L, which):
+    """The FMA-corrected reciprocal inside sigmoid equals IEEE division everywhere tested."""
+    assert L.tern_selftest(which) == 0
+
+
 # ------------------------------------------------------------------------ a1 pack
 @pytest.mark.parametrize("n,k,n_seg", [(64, 128, 1), (48, 40, 1), (256, 256, 3), (688, 256, 2),
                                        (1024, 2816, 1), (100, 1008, 3)])
