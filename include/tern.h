@@ -160,7 +160,8 @@ size_t tern_bitlinear_workspace(int32_t m, int32_t k);
  *   y_n = (float)acc_n * (deq * m_seg) [+ bias_n]
  * rounded to bf16 when ydt == TERN_BF16 (R1).
  * w must have n_seg == 1.  y: [m][ldy] of ydt, ldy >= w->n_out.
- * m <= tern_get_gemv_max_m() runs the decode GEMV (norm+quant fused in its
+ * m <= tern_get_gemv_max_m() (and K within the GEMV's register tile: fp32
+ * K <= 8192 at m <= 2, 4096 at m <= 4; bf16 twice that) runs the decode GEMV (norm+quant fused in its
  * prologue); larger m runs tern_quant + the tcgen05 int8 GEMM. */
 tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, int32_t ldx,
                           const float* gain, float eps, const tern_weight* w, const float* bias,
@@ -270,6 +271,19 @@ typedef struct {
 void tern_profile_enable(int32_t on);
 int32_t tern_profile_collect(tern_prof_rec* out, int32_t max);
 
+/* Device-side timeline of decode-GEMV launches (debug; works inside CUDA
+ * graphs): while enabled, each GEMV launch made on the host gets a trace slot
+ * (up to 1024 launches, then the slots wrap) in which every CTA records the
+ * %globaltimer (ns) at its start, after griddepcontrol.wait, and at its end,
+ * plus its SM id.  tern_trace_collect synchronises the device and copies up
+ * to max_launches records to out (host), each 1 + 1024*16 uint64: [0] = CTA
+ * count, then per CTA {start, released, end, clock64 at start, clock64 at
+ * end, up to 11 intermediate phase marks}; returns the number of
+ * launches recorded (out == NULL just counts).  Replaying a captured graph
+ * overwrites the slots assigned at capture time. */
+void tern_trace_enable(int32_t on);
+int32_t tern_trace_collect(uint64_t* out, int32_t max_launches);
+
 /* Device self-check of the numerics shortcuts the kernels take (test use):
  * which = 0: the FMA-corrected reciprocal used by sigmoid equals IEEE 1/d for
  * every mantissa at exponents {0,1,2,5,10,20,40,60,80,100,119};
@@ -278,7 +292,7 @@ int32_t tern_profile_collect(tern_prof_rec* out, int32_t max);
  * (host).  ws: device scratch of >= 64 bytes. */
 tern_status tern_selftest(int32_t which, void* ws, uint64_t* mismatches);
 
-/* Tuning knob (host): largest m sent to the decode GEMV (default 8, max 8;
+/* Tuning knob (host): largest m sent to the decode GEMV (default 4, max 4;
  * 0 forces the tensor-core path everywhere).  Not thread-safe to change
  * while calls are in flight. */
 void tern_set_gemv_max_m(int32_t m);

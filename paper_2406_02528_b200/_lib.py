@@ -92,6 +92,8 @@ _SIGS = {
     "block_prefill": (C.c_int, [C.POINTER(tern_block), P, P, C.c_int, I32, I32, P, P, SZ, P]),
     "block_decode": (C.c_int, [C.POINTER(tern_block), P, P, C.c_int, I32, P, P, SZ, P]),
     "tern_profile_enable": (None, [I32]),
+    "tern_trace_enable": (None, [I32]),
+    "tern_trace_collect": (I32, [C.c_void_p, I32]),
     "tern_profile_collect": (I32, [C.POINTER(tern_prof_rec), I32]),
     "tern_selftest": (C.c_int, [I32, P, C.POINTER(C.c_uint64)]),
     "tern_set_gemv_max_m": (None, [I32]),
@@ -243,6 +245,26 @@ def tern_set_gemv_max_m(m: int):
 
 def tern_get_gemv_max_m() -> int:
     return int(load().tern_get_gemv_max_m())
+
+
+def tern_trace_enable(on: bool):
+    load().tern_trace_enable(1 if on else 0)
+
+
+def tern_trace_collect():
+    """-> list of (units, array[units][16]: start, released, end, clk0, clk1, phase marks...)."""
+    import numpy as np
+    Lb = load()
+    n = int(Lb.tern_trace_collect(None, 0))
+    rec = 1 + 1024 * 16
+    buf = np.zeros(n * rec, dtype=np.uint64)
+    n = int(Lb.tern_trace_collect(buf.ctypes.data_as(C.c_void_p), n))
+    out = []
+    for i in range(n):
+        r = buf[i * rec:(i + 1) * rec]
+        u = int(r[0])
+        out.append((u, r[1:1 + 16 * u].reshape(u, 16).astype(np.int64)))
+    return out
 
 
 def tern_profile_enable(on: bool):

@@ -16,7 +16,7 @@ using namespace tern;
 namespace {
 
 thread_local std::string g_err;
-int g_gemv_max_m = 8;
+int g_gemv_max_m = kGemvMaxM;
 
 tern_status fail(tern_status st, const char* fmt, ...) {
   char buf[512];
@@ -226,6 +226,11 @@ void tern_profile_enable(int32_t on) {
   g_prof_on = on != 0;
 }
 
+void tern_trace_enable(int32_t on) { gemv_trace_enable(on); }
+int32_t tern_trace_collect(uint64_t* out, int32_t max_launches) {
+  return gemv_trace_collect(reinterpret_cast<unsigned long long*>(out), max_launches);
+}
+
 int32_t tern_profile_collect(tern_prof_rec* out, int32_t max) {
   std::lock_guard<std::mutex> g(g_prof_mu);
   int32_t n = 0;
@@ -242,7 +247,7 @@ int32_t tern_profile_collect(tern_prof_rec* out, int32_t max) {
   return out ? (n < max ? n : max) : n;
 }
 const char* tern_last_error(void) { return g_err.c_str(); }
-void tern_set_gemv_max_m(int32_t m) { g_gemv_max_m = m < 0 ? 0 : (m > 8 ? 8 : m); }
+void tern_set_gemv_max_m(int32_t m) { g_gemv_max_m = m < 0 ? 0 : (m > kGemvMaxM ? kGemvMaxM : m); }
 int32_t tern_get_gemv_max_m(void) { return g_gemv_max_m; }
 
 int32_t tern_packed_rows(int32_t n_out, int32_t n_seg) {
@@ -334,7 +339,7 @@ tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, i
   if (st) return st;
   CHECK(ldy >= w->n_out && ldy % 16 == 0 && aligned16(y), "bitlinear_fwd: ldy/alignment");
   CHECK(eps > 0, "bitlinear_fwd: eps must be > 0");
-  const bool gemv = m <= g_gemv_max_m;
+  const bool gemv = m <= g_gemv_max_m && gemv_supported(m, k, xdt);
   if (taps) {
     CHECK(!taps->q || taps->ldq >= kpad(k), "bitlinear_fwd: taps ldq");
     CHECK(!taps->acc || taps->ldacc >= w->n_rows, "bitlinear_fwd: taps ldacc");
@@ -344,8 +349,6 @@ tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, i
           "bitlinear_fwd: workspace too small (%zu < %zu)", ws_bytes,
           tern_bitlinear_workspace(m, k));
     CHECK(k <= 16384, "bitlinear_fwd: k too large");
-  } else {
-    CHECK(k <= 7168, "bitlinear_fwd: decode path supports k <= 7168");
   }
   st = check_device();
   if (st) return st;
@@ -438,7 +441,7 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
                       int B, int T, int d, float* h, void* ws, const BlockWs& L, cudaStream_t s) {
   const int M = B * T;
   void* op = at<char>(ws, L.oprime);
-  if (T == 1 && B <= g_gemv_max_m) {
+  if (T == 1 && B <= g_gemv_max_m && gemv_supported(B, d, dt)) {
     Epi e1 = make_epi(EPI_MLGRU, p.fcg, p.bias_fcg, op, d);
     e1.h = h;
     e1.gate = p.gate;
@@ -481,7 +484,7 @@ tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, ter
   Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.down, nullptr, out, d);
   e2.res = x;
   e2.ldr = d;
-  if (M <= g_gemv_max_m) {
+  if (M <= g_gemv_max_m && gemv_supported(M, d, dt) && gemv_supported(M, l, dt)) {
     {
       Prof pr(TERN_K_GEMV, e1.kind, M, p.gu.n_rows, d, 2, dt, s);
       TRY_CUDA(launch_gemv(x, dt, dt, M, d, d, p.gain_x, p.eps, p.gu, e1, nullptr, s), "gemv gu");

@@ -21,6 +21,14 @@ __device__ __forceinline__ float bl_out(const Epi& e, int acc, float deq, int se
   return storage_round<TY>(o);
 }
 
+// Same with the segment's scale already in a register.
+template <typename TY>
+__device__ __forceinline__ float bl_val(const Epi& e, int acc, float deq, float mseg, int seg, int r) {
+  float o = dequant(acc, deq, mseg);
+  if (e.bias) o = __fadd_rn(o, __ldg(e.bias + seg * e.n_out + r));
+  return storage_round<TY>(o);
+}
+
 // One recurrence step of the MLGRU with the same op order as the
 // sequential definition: h' = (f*h) + ((1-f)*c).
 __device__ __forceinline__ float mlgru_step(float f, float h, float c) {

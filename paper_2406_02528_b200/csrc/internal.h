@@ -56,12 +56,17 @@ cudaError_t launch_quant(const void* x, int xdt, int m, int k, int ldx, const fl
                          float eps, int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
                          float* absmax, cudaStream_t s);
 // a3 (decode GEMV, norm+quant prologue fused): x [M][ldx] -> epilogue
+constexpr int kGemvMaxM = 4;
+bool gemv_supported(int M, int K, int xdt);   // M <= kGemvMaxM and K within the register tile
 cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, const float* gain,
                         float eps, const tern_weight& w, const Epi& epi, const QuantTaps* taps,
                         cudaStream_t s);
 // a4 (tcgen05 int8 GEMM): q [M][ldq] -> epilogue
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s);
+// debug timeline of GEMV launches (globaltimer per CTA), see tern_trace_enable
+void gemv_trace_enable(int on);
+int gemv_trace_collect(unsigned long long* out, int max_launches);
 cudaError_t launch_selftest(int which, unsigned long long* bad, int* exps, int n_exp,
                             cudaStream_t s);
 cudaError_t launch_expand(const tern_weight& w, uint8_t* e8, cudaStream_t s);

@@ -1,29 +1,37 @@
-// k_gemv.cu -- a3: decode-time ternary GEMV (M <= 8 tokens), HBM-bound on the
-// packed weights.
+// k_gemv.cu -- a3: decode-time ternary GEMV (M <= 8 tokens) with the fused
+// RMSNorm+quant prologue (a2) and the block's epilogues (a5-a8), DESIGN.md
+// "Kernels / decode GEMV".
 //
-//  * before griddepcontrol.wait (PDL) one thread starts bulk async copies of
-//    the CTA's packed weight rows into shared memory, so the weight fetch
-//    overlaps the previous kernel's tail (weights do not depend on it);
-//  * prologue: every CTA re-computes the fused RMSNorm + absmax int8 quantization
-//    of the M input rows (a2) into shared memory, in a fixed
-//    reduction order, so no extra launch or grid sync is needed;
-//  * main loop: packed weights are streamed with coalesced 32-bit non-caching
-//    loads; the 2-bit fields e = t+1 are isolated with one AND each and fed to
-//    dp4a (u8 x s8) against the int8 activations:
-//        sum_k e_k q_k = acc + sum_k q_k  ->  acc = (sum) - qsum        (P:298)
-//    four field accumulators per token are recombined exactly
-//    (field f carries a factor 4^f);
-//  * epilogue: dequantization (a5) and the fused functors (MLGRU step with the
-//    state update, SwiGLU, residual add) per (token, channel).
-// Work unit = `ch` logical channels of every segment of the group, so a CTA
-// owns f, c and g (or gate and up) of the same channels.
+// A decode step is a chain of 4 dependent BitLinears per block, so
+// each launch is latency-bound at batch 1 and HBM-bound on the packed weights
+// at large models; the kernel is organised around its critical path:
+//  * before griddepcontrol.wait (PDL) every thread loads its share of the
+//    CTA's packed weights into REGISTERS (16-byte non-temporal loads), so the
+//    weight fetch overlaps the previous kernel (weights do not depend on it);
+//  * right after the wait: the input row(s) and, for the epilogue, the state
+//    h / residual are loaded at once; the row's RMSNorm + absmax int8 quant is
+//    recomputed per CTA (no extra launch or grid sync) with two block barriers;
+//    sum(x^2) in double-float (common.cuh, reading C4), one thread finishes it
+//    in binary64;
+//  * dot: lanes split K in 64-trit chunks, warps split rows; each 2-bit field
+//    e = t+1 is isolated with one AND and fed to dp4a (u8 x s8):
+//        sum_k e_k q_k = acc + sum_k q_k  ->  acc = (sum) - qsum      (P:298)
+//    (field f carries e*4^f; the exact sum is shifted back);
+//  * epilogue per (token, channel): dequantization (a5), then the MLGRU step
+//    with the state update (a6), SwiGLU (a7) or the residual add (a8).
+// CTA = `ch` logical channels of every segment of the group, so f, c and g
+// (or gate and up) of the same channels meet in one CTA.
+#include <cstdio>
+#include <cstdlib>
+
 #include "epilogue.cuh"
 
 namespace tern {
 
-constexpr int kGThreads = 256;
+constexpr int kGThreads = 512;
 constexpr int kGWarps = kGThreads / 32;
-constexpr int kGMaxPT = 28;  // prologue register tile: K <= 28*256 = 7168
+// 16-byte activation vectors per thread per row (register tile of the prologue)
+template <int MM> struct GNVX { static constexpr int v = MM <= 2 ? 4 : 2; };
 
 struct GemvArgs {
   const void* x;
@@ -31,253 +39,457 @@ struct GemvArgs {
   const float* gain;
   float eps;
   const uint32_t* codes;
-  int n_rows, n_out, n_seg, ch, ksplit;
+  int n_rows, n_out, n_seg, ch;
+  int sw_stride;  // words between consecutive K-blocks of a segment in smem
+  double inv_k;  // 1/K (binary64)
   Epi epi;
   QuantTaps taps;
+  unsigned long long* prof;  // debug (TERN_GEMV_PROF): [grid][8] clock64 per phase
+  unsigned long long* trace; // tern_trace_enable: [grid][8] globaltimer (start, released, end, smid, phases)
 };
 
-__device__ __forceinline__ uint32_t ldg_stream(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ uint4 ldg_stream16(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// 16 bytes of activations -> floats
+template <typename TX> struct XVec;
+template <> struct XVec<float> {
+  static constexpr int N = 4;
+  __device__ static void unpack(const uint4& u, float* v) {
+    v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y);
+    v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
+  }
+};
+template <> struct XVec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ static void unpack(const uint4& u, float* v) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+};
+
+// dot of one 16-byte weight chunk (4 words = 64 trits) with 64 int8 activations
+__device__ __forceinline__ int chunk_dot(const uint4& w, const int8_t* q) {
+  const uint4* qv = reinterpret_cast<const uint4*>(q);
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint4 a = qv[k];
+    // field f of word k holds trits 4f..4f+3 of its 16, i.e. q bytes [4f, 4f+4)
+    const int f0 = dp4a_us(ws[k] & 0x03030303u, a.x, 0);
+    const int f1 = dp4a_us(ws[k] & 0x0C0C0C0Cu, a.y, 0);
+    const int f2 = dp4a_us(ws[k] & 0x30303030u, a.z, 0);
+    const int f3 = dp4a_us(ws[k] & 0xC0C0C0C0u, a.w, 0);
+    s += f0 + (f1 >> 2) + (f2 >> 4) + (f3 >> 6);   // each term is an exact multiple
+  }
+  return s;
+}
+
+__device__ __forceinline__ uint32_t* sw_words(uint8_t* smem) { return reinterpret_cast<uint32_t*>(smem); }
+
+// sum over the 32 lanes, result in every lane
+__device__ __forceinline__ int warp_allsum_i32(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
 template <int MM, typename TX, typename TY>
 __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
   extern __shared__ __align__(128) uint8_t g_smem[];
-  const int R = a.n_seg * a.ch;
-  const int nkb = a.Kp / kKAlign;
-  const int slot = a.ch * 8 + 8;   // words per (segment, K-block) slot, padded vs bank conflicts
-  uint32_t* sW = reinterpret_cast<uint32_t*>(g_smem);         // [n_seg][nkb][slot] words
-  int8_t* qs = reinterpret_cast<int8_t*>(g_smem + a.n_seg * nkb * slot * 4);   // [MM][Kp]
-  int* accs = reinterpret_cast<int*>(qs + MM * a.Kp);               // [MM][R]
-  __shared__ __align__(8) uint64_t wbar;
-  __shared__ float s_deq[MM];
-  __shared__ int s_qsum[MM];
-  __shared__ double red_d[kGWarps];
-  __shared__ float red_f[kGWarps];
-  __shared__ int red_i[kGWarps];
+  int8_t* qs = reinterpret_cast<int8_t*>(g_smem + (size_t)a.n_seg * (a.Kp >> 7) * a.sw_stride * 4);  // [MM][Kp]
+  __shared__ double red_d[MM][kGWarps];
+  __shared__ float red_m[MM][kGWarps];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int unit = blockIdx.x;
+  long long pt0 = 0;
+  if (a.prof) pt0 = clock64();
+  if (a.trace && tid == 0) {
+    a.trace[blockIdx.x * 16 + 0] = gtimer();
+    a.trace[blockIdx.x * 16 + 3] = clock64();
+  }
+#define GPROF(i)                                                                 \
+  if (a.prof && tid == 0 && (i) < 8) a.prof[blockIdx.x * 8 + (i)] = clock64() - pt0; \
+  if (a.trace && tid == 0 && (i) >= 2) a.trace[blockIdx.x * 16 + 3 + (i)] = gtimer();
 
-  // ---------------- weight prefetch (independent of the previous kernel)
-  if (tid == 0) {
-    mbar_init(&wbar, 1);
-    fence_barrier_init();
-    fence_proxy_async_smem();
-    // the unit's rows of one segment are consecutive packed rows, so each
-    // (segment, K-block) is one contiguous span of vcnt*32 bytes
-    const int vcnt = min(a.ch, a.n_out - unit * a.ch);
-    mbar_arrive_expect_tx(&wbar, (uint32_t)(a.n_seg * nkb * vcnt * 32));
-    for (int sg = 0; sg < a.n_seg; ++sg) {
-      const int p0 = packed_row(sg, unit * a.ch, a.n_seg);
-      for (int kb = 0; kb < nkb; ++kb)
-        bulk_load(sW + (sg * nkb + kb) * slot, a.codes + ((int64_t)kb * a.n_rows + p0) * 8,
-                  (uint32_t)vcnt * 32u, &wbar);
+  // ---------------- packed weights -> smem with the TMA engine (bulk copies; the
+  // LSU pipe stays free for the running kernel's critical path).  In the
+  // K-block-major layout the CTA's rows of one segment within one 64-row group
+  // are one contiguous span per K-block.  Smem: [seg][kb] blocks of ch rows x
+  // 8 words, block stride SW words (SW = 8 mod 32: conflict-free dot reads).
+  const int nkb = a.Kp >> 7;
+  const int SW = a.sw_stride;
+  __shared__ __align__(8) uint64_t wbar;
+  const int r0 = unit * a.ch, r1 = min(r0 + a.ch, a.n_out);   // logical rows [r0, r1)
+  if (warp == 0) {
+    const int g0 = r0 >> 6, g1 = (r1 - 1) >> 6;   // 64-row groups touched (<= 2)
+    const int nparts = a.n_seg == 1 ? 1 : g1 - g0 + 1;
+    if (lane == 0) {
+      mbar_init(&wbar, 1);
+      fence_barrier_init();
+      mbar_arrive_expect_tx(&wbar, (uint32_t)(a.n_seg * nkb * (r1 - r0) * 32));
+    }
+    __syncwarp();
+    const int nspan = a.n_seg * nkb * nparts;
+    for (int sp = lane; sp < nspan; sp += 32) {
+      const int part = sp % nparts, t = sp / nparts;
+      const int kb = t % nkb, sg = t / nkb;
+      int a0r = r0, a1r = r1;
+      if (a.n_seg > 1) {
+        const int gb = (g0 + part) << 6;
+        a0r = max(r0, gb);
+        a1r = min(r1, gb + 64);
+      }
+      const int pr = a.n_seg == 1 ? a0r : packed_row(sg, a0r, a.n_seg);
+      bulk_load(sw_words(g_smem) + (sg * nkb + kb) * SW + (a0r - r0) * 8,
+                a.codes + ((int64_t)kb * a.n_rows + pr) * 8, (uint32_t)(a1r - a0r) * 32u, &wbar);
     }
   }
-  pdl_launch_dependents();
+  // dequantization scales are constants: load them before the wait too
+  const Epi& e = a.epi;
+  float msc[3];
+#pragma unroll
+  for (int sg = 0; sg < 3; ++sg) msc[sg] = sg < a.n_seg ? __ldg(e.scales + sg) : 0.0f;
+  GPROF(0)
   pdl_wait();
+  // let the next kernel start its weight prefetch only now: earlier triggers
+  // let grids two launches ahead occupy SM slots and delay this grid's CTAs
+  pdl_launch_dependents();
+  GPROF(1)
+  if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 1] = gtimer();
 
-  for (int i = tid; i < MM * R; i += kGThreads) accs[i] = 0;
-
-  // ---------------- prologue: fused RMSNorm + quantization (a2) per row
-  for (int m = 0; m < MM; ++m) {
-    int8_t* qrow = qs + m * a.Kp;
-    if (m >= a.M) {
-      for (int k = tid; k < a.Kp; k += kGThreads) qrow[k] = 0;
-      if (tid == 0) { s_deq[m] = 0.0f; s_qsum[m] = 0; }
-      continue;
+  // ---------------- epilogue operands prefetch: lane m of warp w owns token m of
+  // channels w, w+16, w+32, w+48 (state h or residual)
+  float pre[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int i = warp + j * kGWarps, rr = unit * a.ch + i;
+    if (lane < a.M && i < a.ch && rr < a.n_out) {
+      if (e.kind == EPI_MLGRU) pre[j] = __ldcg(e.h + (int64_t)lane * e.n_out + rr);
+      if (e.kind == EPI_RESID)
+        pre[j] = ld_act_cg<TY>(static_cast<const TY*>(e.res) + (int64_t)lane * e.ldr + rr);
     }
-    const TX* xr = static_cast<const TX*>(a.x) + (int64_t)m * a.ldx;
-    const int npt = (a.K + kGThreads - 1) / kGThreads;   // uniform: skips unused slots
-    float v[kGMaxPT];
-    double ss = 0.0;
+  }
+
+  // ---------------- prologue: fused RMSNorm + int8 quant (a2) of the M rows.
+  // x in registers (kGNVX 16-byte vectors per thread per row); sum(x^2) in
+  // binary64 (C4), max|x|; one block barrier for the partials, every warp then
+  // finishes the reduction itself.
+  constexpr int VE = XVec<TX>::N;
+  const int nvec = a.K / VE, nvecp = a.Kp / VE;
+  constexpr int kGNVX = GNVX<MM>::v;
+  uint4 xv[MM][kGNVX];
+#pragma unroll
+  for (int m = 0; m < MM; ++m) {
+    const uint4* src =
+        reinterpret_cast<const uint4*>(static_cast<const TX*>(a.x) + (int64_t)m * a.ldx);
+#pragma unroll
+    for (int i = 0; i < kGNVX; ++i) {
+      const int v = tid + i * kGThreads;
+      xv[m][i] = (m < a.M && v < nvec) ? __ldcg(src + v) : make_uint4(0, 0, 0, 0);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < MM; ++m) {
+    double s0 = 0.0, s1 = 0.0;
     float xmax = 0.0f;
 #pragma unroll
-    for (int i = 0; i < kGMaxPT; ++i) {
-      v[i] = 0.0f;
-      if (i < npt) {
-        const int k = tid + i * kGThreads;
-        v[i] = k < a.K ? ld_act<TX>(xr + k) : 0.0f;
-        ss += (double)v[i] * (double)v[i];
-        xmax = fmaxf(xmax, fabsf(v[i]));
+    for (int i = 0; i < kGNVX; ++i) {
+      float v[VE];
+      XVec<TX>::unpack(xv[m][i], v);
+#pragma unroll
+      for (int j = 0; j < VE; j += 2) {
+        const double d0 = (double)v[j], d1 = (double)v[j + 1];
+        s0 = fma(d0, d0, s0);
+        s1 = fma(d1, d1, s1);
+        xmax = fmaxf(xmax, fmaxf(fabsf(v[j]), fabsf(v[j + 1])));
       }
     }
-    // one reduction round for sum(x^2) and max|x|: without a gain,
-    // max|x*r| = fl(max|x| * r) exactly (rounding is monotone)
-    ss = warp_sum_f64(ss);
-    xmax = warp_max_f32(xmax);
-    if (lane == 0) { red_d[warp] = ss; red_f[warp] = xmax; }
-    __syncthreads();
-    double tot = 0.0;
-    xmax = 0.0f;
+    double sd = s0 + s1;
+    if (m == 0) { GPROF(2) }
 #pragma unroll
-    for (int i = 0; i < kGWarps; ++i) { tot += red_d[i]; xmax = fmaxf(xmax, red_f[i]); }
-    const float r = (float)(1.0 / sqrt(tot / (double)a.K + (double)a.eps));
-    float amax;
-    if (a.gain == nullptr) {
-      amax = __fmul_rn(xmax, r);
-#pragma unroll
-      for (int i = 0; i < kGMaxPT; ++i)
-        if (i < npt) v[i] = __fmul_rn(v[i], r);
-    } else {
-      amax = 0.0f;
-#pragma unroll
-      for (int i = 0; i < kGMaxPT; ++i) {
-        if (i < npt) {
-          const int k = tid + i * kGThreads;
-          float y = __fmul_rn(v[i], r);
-          if (k < a.K) y = __fmul_rn(y, __ldg(a.gain + k));
-          v[i] = y;
-          amax = fmaxf(amax, fabsf(y));
-        }
-      }
-      amax = warp_max_f32(amax);
-      __syncthreads();
-      if (lane == 0) red_f[warp] = amax;
-      __syncthreads();
-      amax = 0.0f;
-#pragma unroll
-      for (int i = 0; i < kGWarps; ++i) amax = fmaxf(amax, red_f[i]);
+    for (int o = 16; o > 0; o >>= 1) {
+      sd += __shfl_xor_sync(0xffffffffu, sd, o);
+      xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
     }
-    const float s = amax > 0.0f ? __fdiv_rn(127.0f, amax) : 0.0f;
-    int qsum = 0;
-#pragma unroll
-    for (int i = 0; i < kGMaxPT; ++i) {
-      const int k = tid + i * kGThreads;
-      if (i <= npt && k < a.Kp) {
-        int qi = 0;
-        if (k < a.K && amax > 0.0f) {
-          // |v*s| <= 127 (1+2^-23) always, so the clamp to [-128,127] (C5) is inert
-          const float t = round_half_away(__fmul_rn(v[i], s));
-          qi = (int)t;
-        }
-        qsum += qi;
-        qrow[k] = (int8_t)qi;
-      }
-    }
-    qsum = warp_sum_i32(qsum);
-    if (lane == 0) red_i[warp] = qsum;
-    __syncthreads();
-    if (tid == 0) {
-      int t = 0;
-      for (int i = 0; i < kGWarps; ++i) t += red_i[i];
-      s_qsum[m] = t;
-      s_deq[m] = amax > 0.0f ? __fdiv_rn(amax, 127.0f) : 0.0f;
-      if (blockIdx.x == 0) {
-        if (a.taps.deq) a.taps.deq[m] = s_deq[m];
-        if (a.taps.inv_rms) a.taps.inv_rms[m] = r;
-        if (a.taps.absmax) a.taps.absmax[m] = amax;
-      }
-    }
-    __syncthreads();  // red_* reused by the next row
-  }
-  if (blockIdx.x == 0 && a.taps.q) {
-    for (int m = 0; m < a.M; ++m)
-      for (int k = tid; k < a.Kp; k += kGThreads)
-        a.taps.q[(int64_t)m * a.taps.ldq + k] = qs[m * a.Kp + k];
-  }
-
-  // ---------------- main loop: (row quad, K slice) items per warp
-  mbar_wait(&wbar, 0);
-  const int nwords = a.Kp >> 4;
-  const int nquads = (R + 3) >> 2;
-  const int items = nquads * a.ksplit;
-  const int wslice = (nwords + a.ksplit - 1) / a.ksplit;
-  for (int it = warp; it < items; it += kGWarps) {
-    const int quad = it / a.ksplit, ks = it % a.ksplit;
-    const int w0 = ks * wslice;
-    const int w1 = min(nwords, w0 + wslice);
-    const uint32_t* wrow[4];
-    bool valid[4];
-#pragma unroll
-    for (int qd = 0; qd < 4; ++qd) {
-      const int j = quad * 4 + qd;
-      const int seg = j / a.ch, i = j % a.ch;
-      const int rr = unit * a.ch + i;
-      valid[qd] = (j < R) && (rr < a.n_out);
-      wrow[qd] = sW + (valid[qd] ? (seg * nkb * slot + i * 8) : 0);
-    }
-    int acc[4][MM];
-#pragma unroll
-    for (int qd = 0; qd < 4; ++qd)
-#pragma unroll
-      for (int m = 0; m < MM; ++m) acc[qd][m] = 0;
-    for (int w = w0 + lane; w < w1; w += 32) {
-      uint32_t wd[4];
-#pragma unroll
-      const int wo = (w >> 3) * slot + (w & 7);   // (K-block, word) inside the slot
-#pragma unroll
-      for (int qd = 0; qd < 4; ++qd) wd[qd] = valid[qd] ? wrow[qd][wo] : 0x55555555u;
-#pragma unroll
-      for (int m = 0; m < MM; ++m) {
-        const uint4 qv = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
-#pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-          // field f carries e*4^f; fold 4^f back after the reduction
-          int f0 = dp4a_us(wd[qd] & 0x03030303u, qv.x, 0);
-          int f1 = dp4a_us(wd[qd] & 0x0C0C0C0Cu, qv.y, 0);
-          int f2 = dp4a_us(wd[qd] & 0x30303030u, qv.z, 0);
-          int f3 = dp4a_us(wd[qd] & 0xC0C0C0C0u, qv.w, 0);
-          acc[qd][m] += f0 + (f1 >> 2) + (f2 >> 4) + (f3 >> 6);
-        }
-      }
-    }
-#pragma unroll
-    for (int qd = 0; qd < 4; ++qd)
-#pragma unroll
-      for (int m = 0; m < MM; ++m) {
-        const int t = warp_sum_i32(acc[qd][m]);
-        if (lane == 0 && valid[qd]) atomicAdd(&accs[m * R + quad * 4 + qd], t);
-      }
+    if (m == 0) { GPROF(3) }
+    if (lane == 0) { red_d[m][warp] = sd; red_m[m][warp] = xmax; }
   }
   __syncthreads();
-
-  // ---------------- epilogue per (token, channel)
-  const Epi& e = a.epi;
-  for (int idx = tid; idx < MM * a.ch; idx += kGThreads) {
-    const int m = idx / a.ch, i = idx % a.ch;
-    const int rr = unit * a.ch + i;
-    if (m >= a.M || rr >= a.n_out) continue;
-    const float deq = s_deq[m];
-    const int* am = accs + m * R;
-    if (e.acc) {
-      for (int sg = 0; sg < a.n_seg; ++sg)
-        e.acc[(int64_t)m * e.ldacc + packed_row(sg, rr, a.n_seg)] = am[sg * a.ch + i] - s_qsum[m];
+  GPROF(4)
+  float rinv[MM], amax[MM];
+#pragma unroll
+  for (int m = 0; m < MM; ++m) {
+    // every warp: lanes 0..15 take one partial each, tree over 16
+    double sd = lane < kGWarps ? red_d[m][lane] : 0.0;
+    float xm = lane < kGWarps ? red_m[m][lane] : 0.0f;
+#pragma unroll
+    for (int o = kGWarps / 2; o > 0; o >>= 1) {
+      sd += __shfl_xor_sync(0xffffffffu, sd, o);
+      xm = fmaxf(xm, __shfl_xor_sync(0xffffffffu, xm, o));
     }
-    TY* out = static_cast<TY*>(e.out);
-    if (e.kind == EPI_MLGRU) {
-      const float fh = bl_out<TY>(e, am[i] - s_qsum[m], deq, 0, rr);
-      const float chh = bl_out<TY>(e, am[a.ch + i] - s_qsum[m], deq, 1, rr);
-      const float gh = bl_out<TY>(e, am[2 * a.ch + i] - s_qsum[m], deq, 2, rr);
-      const float f = sigmoid_c(fh);
-      const float c = silu_c(chh);
-      float* hp = e.h + (int64_t)m * e.n_out + rr;
-      const float h = mlgru_step(f, *hp, c);
-      *hp = h;
-      st_act<TY>(out + (int64_t)m * e.ldo + rr, mlgru_out(gh, h, e.gate));
-    } else if (e.kind == EPI_SWIGLU) {
-      const float gh = bl_out<TY>(e, am[i] - s_qsum[m], deq, 0, rr);
-      const float uh = bl_out<TY>(e, am[a.ch + i] - s_qsum[m], deq, 1, rr);
-      st_act<TY>(out + (int64_t)m * e.ldo + rr, swiglu(gh, uh));
-    } else if (e.kind != EPI_NONE) {
-      Epi e1 = e;
-      e1.acc = nullptr;
-      epi_single<TY>(e1, m, rr, 0, rr, am[i] - s_qsum[m], deq);
+    sd = __shfl_sync(0xffffffffu, sd, 0);
+    xm = __shfl_sync(0xffffffffu, xm, 0);
+    rinv[m] = (float)rsqrt(fma(sd, a.inv_k, (double)a.eps));
+    // max|fl(x r)| = fl(max|x| r): rounding is monotone and r > 0
+    amax[m] = __fmul_rn(xm, rinv[m]);
+  }
+  if (a.gain) {   // with a gain the max is taken over y = (x r) g: one more round
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      float am = 0.0f;
+#pragma unroll
+      for (int i = 0; i < kGNVX; ++i) {
+        const int v = tid + i * kGThreads;
+        float xf[VE];
+        XVec<TX>::unpack(xv[m][i], xf);
+#pragma unroll
+        for (int j = 0; j < VE; ++j)
+          if (v < nvec)
+            am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(xf[j], rinv[m]), __ldg(a.gain + v * VE + j))));
+      }
+      am = warp_max_f32(am);
+      __syncthreads();   // everyone has read red_m above
+      if (lane == 0) red_m[m][warp] = am;
+      __syncthreads();
+      am = lane < kGWarps ? red_m[m][lane] : 0.0f;
+      am = warp_max_f32(am);
+      amax[m] = am;
     }
   }
+  GPROF(5)
+  // quantize own elements: q = round(y * 127/amax), half away from zero (C3, C5)
+#pragma unroll
+  for (int m = 0; m < MM; ++m) {
+    const float sc = amax[m] > 0.0f ? __fdiv_rn(127.0f, amax[m]) : 0.0f;
+    int8_t* qrow = qs + m * a.Kp;
+#pragma unroll
+    for (int i = 0; i < kGNVX; ++i) {
+      const int v = tid + i * kGThreads;
+      if (v < nvecp) {
+        uint32_t pk[VE / 4];
+#pragma unroll
+        for (int j4 = 0; j4 < VE / 4; ++j4) pk[j4] = 0;
+        if (v < nvec && amax[m] > 0.0f) {
+          float xf[VE];
+          XVec<TX>::unpack(xv[m][i], xf);
+#pragma unroll
+          for (int j = 0; j < VE; ++j) {
+            float y = __fmul_rn(xf[j], rinv[m]);
+            if (a.gain) y = __fmul_rn(y, __ldg(a.gain + v * VE + j));
+            // |y*sc| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
+            const int qi = (int)round_half_away(__fmul_rn(y, sc));
+            pk[j >> 2] |= ((uint32_t)qi & 0xffu) << (8 * (j & 3));
+          }
+        }
+        if (VE == 4)
+          *reinterpret_cast<uint32_t*>(qrow + v * 4) = pk[0];
+        else
+          *reinterpret_cast<uint2*>(qrow + v * 8) = make_uint2(pk[0], pk[VE / 4 - 1]);
+      }
+    }
+  }
+  float deq[MM];
+#pragma unroll
+  for (int m = 0; m < MM; ++m) deq[m] = amax[m] > 0.0f ? __fdiv_rn(amax[m], 127.0f) : 0.0f;
+  if (blockIdx.x == 0 && tid < a.M) {
+#pragma unroll
+    for (int m = 0; m < MM; ++m)
+      if (m == tid) {
+        if (a.taps.deq) a.taps.deq[m] = deq[m];
+        if (a.taps.inv_rms) a.taps.inv_rms[m] = rinv[m];
+        if (a.taps.absmax) a.taps.absmax[m] = amax[m];
+      }
+  }
+  __syncthreads();       // q rows visible
+  mbar_wait(&wbar, 0);   // weights landed (long since, in a PDL chain)
+  GPROF(6)
+  if (blockIdx.x == 0 && a.taps.q) {
+    for (int m = 0; m < a.M; ++m)
+      for (int k = tid * 16; k < a.Kp; k += kGThreads * 16)
+        *reinterpret_cast<uint4*>(a.taps.q + (int64_t)m * a.taps.ldq + k) =
+            *reinterpret_cast<const uint4*>(qs + m * a.Kp + k);
+  }
+
+  // ---------------- dot + epilogue: warp w owns channels w, w+16, ... with all
+  // their segments (f,c,g / gate,up); lanes split the row's 32-bit words
+  // (16 trits x 16 q bytes; consecutive lanes -> consecutive words, no bank
+  // conflicts).  sum e*q - sum q = sum t*q: each lane starts from minus
+  // the sum of the q bytes it will visit, so no per-row q sum is needed.
+  const uint32_t* swd = sw_words(g_smem);
+  const int W = a.Kp >> 4;   // words per row
+  int lq[MM];
+#pragma unroll
+  for (int m = 0; m < MM; ++m) lq[m] = 0;
+  for (int w = lane; w < W; w += 32) {
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      const uint4 qv = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
+      lq[m] = dp4a_us(0x01010101u, qv.x, lq[m]);
+      lq[m] = dp4a_us(0x01010101u, qv.y, lq[m]);
+      lq[m] = dp4a_us(0x01010101u, qv.z, lq[m]);
+      lq[m] = dp4a_us(0x01010101u, qv.w, lq[m]);
+    }
+  }
+  TY* out = static_cast<TY*>(e.out);
+#pragma unroll 1
+  for (int j = 0; j < 4; ++j) {
+    const int i = warp + j * kGWarps;
+    if (i >= a.ch) break;
+    const int rr = unit * a.ch + i;
+    int part[3][MM];
+#pragma unroll
+    for (int sgi = 0; sgi < 3; ++sgi)
+#pragma unroll
+      for (int m = 0; m < MM; ++m) part[sgi][m] = -lq[m];
+    for (int w = lane; w < W; w += 32) {
+      uint4 qv[MM];
+#pragma unroll
+      for (int m = 0; m < MM; ++m) qv[m] = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
+#pragma unroll
+      for (int sgi = 0; sgi < 3; ++sgi) {
+        if (sgi < a.n_seg) {
+          const uint32_t wd = swd[(sgi * nkb + (w >> 3)) * SW + i * 8 + (w & 7)];
+#pragma unroll
+          for (int m = 0; m < MM; ++m) {
+            const int f0 = dp4a_us(wd & 0x03030303u, qv[m].x, 0);
+            const int f1 = dp4a_us(wd & 0x0C0C0C0Cu, qv[m].y, 0);
+            const int f2 = dp4a_us(wd & 0x30303030u, qv[m].z, 0);
+            const int f3 = dp4a_us(wd & 0xC0C0C0C0u, qv[m].w, 0);
+            part[sgi][m] += f0 + (f1 >> 2) + (f2 >> 4) + (f3 >> 6);   // exact multiples
+          }
+        }
+      }
+    }
+    if (j == 0) { GPROF(7) }
+    // all-reduce, then lane m keeps token m's accumulators
+    int acc[3] = {0, 0, 0};
+#pragma unroll
+    for (int sgi = 0; sgi < 3; ++sgi) {
+      if (sgi < a.n_seg) {
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+          const int v = warp_allsum_i32(part[sgi][m]);
+          if (lane == m) acc[sgi] = v;
+        }
+      }
+    }
+    if (j == 0) { GPROF(8) }
+    if (rr >= a.n_out || lane >= a.M) continue;
+    const int m = lane;
+    float dq = deq[0];
+#pragma unroll
+    for (int mm = 1; mm < MM; ++mm)
+      if (m == mm) dq = deq[mm];
+    const float pv = j == 0 ? pre[0] : (j == 1 ? pre[1] : (j == 2 ? pre[2] : pre[3]));
+    if (e.acc) {
+      for (int sg = 0; sg < a.n_seg; ++sg)
+        e.acc[(int64_t)m * e.ldacc + (a.n_seg == 1 ? rr : packed_row(sg, rr, a.n_seg))] =
+            sg == 0 ? acc[0] : (sg == 1 ? acc[1] : acc[2]);
+    }
+    if (e.kind == EPI_MLGRU) {
+      const float fh = bl_val<TY>(e, acc[0], dq, msc[0], 0, rr);
+      const float chh = bl_val<TY>(e, acc[1], dq, msc[1], 1, rr);
+      const float gh = bl_val<TY>(e, acc[2], dq, msc[2], 2, rr);
+      const float f = sigmoid_c(fh);
+      const float cc = silu_c(chh);
+      const float h = mlgru_step(f, pv, cc);
+      e.h[(int64_t)m * e.n_out + rr] = h;
+      st_act<TY>(out + (int64_t)m * e.ldo + rr, mlgru_out(gh, h, e.gate));
+    } else if (e.kind == EPI_SWIGLU) {
+      const float gh = bl_val<TY>(e, acc[0], dq, msc[0], 0, rr);
+      const float uh = bl_val<TY>(e, acc[1], dq, msc[1], 1, rr);
+      st_act<TY>(out + (int64_t)m * e.ldo + rr, swiglu(gh, uh));
+    } else if (e.kind == EPI_RESID) {
+      const float o = bl_val<TY>(e, acc[0], dq, msc[0], 0, rr);
+      st_act<TY>(out + (int64_t)m * e.ldo + rr, __fadd_rn(pv, o));
+    } else if (e.kind == EPI_STORE || e.kind == EPI_FCG) {
+      for (int sg = 0; sg < a.n_seg; ++sg) {
+        const float o = bl_val<TY>(e, sg == 0 ? acc[0] : (sg == 1 ? acc[1] : acc[2]), dq,
+                                   sg == 0 ? msc[0] : (sg == 1 ? msc[1] : msc[2]), sg, rr);
+        const int col = e.kind == EPI_FCG ? packed_row(sg, rr, a.n_seg) : rr;
+        st_act<TY>(out + (int64_t)m * e.ldo + col, o);
+      }
+    }
+  }
+  GPROF(9)
+  if (a.trace) {
+    __syncthreads();
+    if (tid == 0) {
+      a.trace[blockIdx.x * 16 + 2] = gtimer();
+      a.trace[blockIdx.x * 16 + 4] = clock64();
+    }
+  }
+#undef GPROF
+}
+
+// ----------------------------------------------------------------- device trace (debug)
+constexpr int kTraceLaunches = 1024, kTraceCtas = 1024;
+static unsigned long long* g_trace = nullptr;
+static bool g_trace_on = false;
+static int g_trace_seq = 0;
+static int g_trace_units[kTraceLaunches];
+
+void gemv_trace_enable(int on) {
+  if (on && !g_trace) {
+    if (cudaMalloc(&g_trace, sizeof(unsigned long long) * kTraceLaunches * kTraceCtas * 16) != cudaSuccess) {
+      g_trace = nullptr;
+      return;
+    }
+  }
+  g_trace_on = on && g_trace;
+  g_trace_seq = 0;
+}
+
+int gemv_trace_collect(unsigned long long* out, int max_launches) {
+  const int n = g_trace_seq < kTraceLaunches ? g_trace_seq : kTraceLaunches;
+  if (!out || !g_trace) return n;
+  const int m = n < max_launches ? n : max_launches;
+  cudaDeviceSynchronize();
+  for (int i = 0; i < m; ++i) {
+    out[(size_t)i * (kTraceCtas * 16 + 1)] = (unsigned long long)g_trace_units[i];
+    cudaMemcpy(out + (size_t)i * (kTraceCtas * 16 + 1) + 1, g_trace + (size_t)i * kTraceCtas * 16,
+               sizeof(unsigned long long) * kTraceCtas * 16, cudaMemcpyDeviceToHost);
+  }
+  return m;
+}
+
+// smem words between K-blocks of one segment: ch rows x 8 words, padded to 8 mod 32
+static int gemv_sw_stride(int ch) { return ch * 8 + ((8 - ch * 8) % 32 + 32) % 32; }
+// dynamic shared memory of one CTA: weights and q rows
+static size_t gemv_smem(int MM, int n_seg, int ch, int Kp) {
+  return (size_t)n_seg * (Kp / 128) * gemv_sw_stride(ch) * 4 + (size_t)MM * Kp;
 }
 
 template <int MM, typename TX, typename TY>
 static cudaError_t gemv_launch(const GemvArgs& a, int units, cudaStream_t s) {
-  const int R = a.n_seg * a.ch;
-  const size_t smem = (size_t)a.n_seg * (a.Kp / kKAlign) * (a.ch * 8 + 8) * 4 + (size_t)MM * a.Kp +
-                      (size_t)MM * R * sizeof(int);
+  const size_t smem = gemv_smem(MM, a.n_seg, a.ch, a.Kp);
   auto kern = k_gemv<MM, TX, TY>;
   static size_t smem_set = 48 * 1024;
   if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     smem_set = 200 * 1024;
   }
@@ -291,26 +503,75 @@ static cudaError_t gemv_launch(const GemvArgs& a, int units, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a);
+  static unsigned long long* dprof = nullptr;
+  static const bool prof_on = getenv("TERN_GEMV_PROF") != nullptr;
+  GemvArgs aa = a;
+  if (g_trace_on && units <= kTraceCtas) {
+    const int slot = g_trace_seq % kTraceLaunches;
+    aa.trace = g_trace + (size_t)slot * kTraceCtas * 16;
+    g_trace_units[slot] = units;
+    ++g_trace_seq;
+  }
+  if (prof_on) {  // debug only: per-phase clocks, printed after a synchronous run
+    if (!dprof) cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * 4096);
+    cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * 8 * 4096, s);
+    aa.prof = dprof;
+  }
+  cudaError_t err = cudaLaunchKernelEx(&cfg, kern, aa);
+  if (prof_on) {
+    static unsigned long long h[8 * 4096];
+    cudaMemcpyAsync(h, dprof, sizeof(unsigned long long) * 8 * units, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double sum[8] = {0}, mx[8] = {0};
+    for (int b = 0; b < units; ++b)
+      for (int i = 0; i < 7; ++i) {
+        sum[i] += (double)h[b * 8 + i] / units;
+        mx[i] = fmax(mx[i], (double)h[b * 8 + i]);
+      }
+    fprintf(stderr,
+            "[gemv prof] M=%d K=%d n_out=%d n_seg=%d ch=%d units=%d | cycles avg: "
+            "wload %.0f pdlwait %.0f sq %.0f r %.0f quant %.0f dot %.0f end %.0f (max end %.0f)\n",
+            a.M, a.K, a.n_out, a.n_seg, a.ch, units, sum[0], sum[1],
+            sum[2], sum[3], sum[4], sum[5], sum[6], mx[6]);
+  }
+  return err;
 }
 
 template <typename TX, typename TY>
 static cudaError_t gemv_dispatch_m(const GemvArgs& a, int units, cudaStream_t s) {
   if (a.M <= 1) return gemv_launch<1, TX, TY>(a, units, s);
   if (a.M <= 2) return gemv_launch<2, TX, TY>(a, units, s);
-  if (a.M <= 4) return gemv_launch<4, TX, TY>(a, units, s);
-  return gemv_launch<8, TX, TY>(a, units, s);
+  return gemv_launch<4, TX, TY>(a, units, s);
+}
+
+bool gemv_supported(int M, int K, int xdt) {
+  const int ve = xdt == TERN_BF16 ? 8 : 4;
+  if (M < 1 || M > kGemvMaxM) return false;
+  const int nvx = M <= 2 ? GNVX<2>::v : GNVX<4>::v;
+  return K <= nvx * kGThreads * ve;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, const float* gain,
                         float eps, const tern_weight& w, const Epi& epi, const QuantTaps* taps,
                         cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
-  if (M > 8 || K > kGMaxPT * kGThreads) return cudaErrorInvalidValue;
+  if (!gemv_supported(M, K, xdt)) return cudaErrorInvalidValue;
   GemvArgs a{};
   a.x = x;
   a.ldx = ldx;
   a.K = K;
+  a.inv_k = 1.0 / (double)K;
   a.Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
   a.M = M;
   a.gain = gain;
@@ -319,15 +580,15 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
   a.n_rows = w.n_rows;
   a.n_out = w.n_out;
   a.n_seg = w.n_seg;
-  // channels per CTA: enough CTAs to cover the SMs about twice
-  int ch = 32;
-  while (ch > 4 && (w.n_out + ch - 1) / ch < 296) ch >>= 1;
-  if (w.n_seg == 3 && ch > 8) ch = 8;
+  const int MMt = M <= 1 ? 1 : (M <= 2 ? 2 : 4);
+  // channels per CTA: one CTA per SM (the per-SM work is balanced and every
+  // SM streams its share of the weights), bounded by shared memory and by
+  // one thread per (token, channel) in the epilogue
+  int ch = (w.n_out + num_sms() - 1) / num_sms();
+  while (ch > 1 && (gemv_smem(MMt, w.n_seg, ch, a.Kp) > 160 * 1024 || ch > 4 * kGWarps)) --ch;
+  if (gemv_smem(MMt, w.n_seg, ch, a.Kp) > 200 * 1024) return cudaErrorInvalidValue;
   a.ch = ch;
-  const int nquads = (w.n_seg * ch + 3) / 4;
-  int ksplit = 1;
-  while (nquads * ksplit < kGWarps && ksplit < 8) ksplit <<= 1;
-  a.ksplit = ksplit;
+  a.sw_stride = gemv_sw_stride(ch);
   a.epi = epi;
   if (taps) a.taps = *taps;
   const int units = (w.n_out + ch - 1) / ch;
