@@ -25,9 +25,7 @@ namespace tern {
 // Cody-Waite reduction, degree-7 Taylor polynomial in Horner form with fma,
 // then multiply by 2^k.  Constants are the binary32 values in DESIGN.md.
 __device__ __forceinline__ float exp_c(float x) {
-  if (x != x) return x;
-  if (x >= 0x1.62e430p+6f) return __int_as_float(0x7f800000);
-  if (x < -0x1.5d589ep+6f) return 0.0f;
+  // branch-free (selects only), so unrolled element loops keep their ILP
   const float k = rintf(__fmul_rn(x, 0x1.715476p+0f));
   float r = __fmaf_rn(-k, 0x1.62e400p-1f, x);
   r = __fmaf_rn(-k, 0x1.7f7d1cp-20f, r);
@@ -40,8 +38,14 @@ __device__ __forceinline__ float exp_c(float x) {
   p = __fmaf_rn(p, r, 1.0f);
   p = __fmaf_rn(p, r, 1.0f);
   int ki = (int)k;
-  if (ki > 127) { p = __fmul_rn(p, 2.0f); ki -= 1; }
-  return __fmul_rn(p, __int_as_float((ki + 127) << 23));
+  const bool big = ki > 127;
+  p = big ? __fmul_rn(p, 2.0f) : p;
+  ki = big ? ki - 1 : ki;
+  ki = max(min(ki, 127), -126);   // in-range x never needs the clamp
+  float res = __fmul_rn(p, __int_as_float((ki + 127) << 23));
+  res = x >= 0x1.62e430p+6f ? __int_as_float(0x7f800000) : res;
+  res = x < -0x1.5d589ep+6f ? 0.0f : res;
+  return x != x ? x : res;
 }
 
 // Correctly rounded 1/d for d >= 1 (== IEEE __fdiv_rn(1, d)) without the
@@ -63,6 +67,18 @@ __device__ __forceinline__ float sigmoid_c(float x) {
 }
 // SiLU tau(x) = x sigma(x).
 __device__ __forceinline__ float silu_c(float x) { return __fmul_rn(x, sigmoid_c(x)); }
+
+// Fast sigmoid for vectorised loops: the reciprocal's fast path only (exact
+// for 1+e^-x < 2^120, i.e. x > -83.17); `slow` is set when an element needs
+// the exact path, and the caller recomputes that chunk with sigmoid_c.
+__device__ __forceinline__ float sigmoid_fast(float x, bool& slow) {
+  const float d = __fadd_rn(1.0f, exp_c(-x));
+  slow |= !(d < 0x1p120f);
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+  const float e = __fmaf_rn(-d, r, 1.0f);
+  return __fmaf_rn(r, e, r);
+}
 
 // round half away from zero (reading C3), exact for any finite float.
 __device__ __forceinline__ float round_half_away(float v) {

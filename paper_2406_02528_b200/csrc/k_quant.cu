@@ -1,213 +1,202 @@
 // k_quant.cu -- a2: fused RMSNorm + per-token absmax int8 quantization
 // (Alg. 1 rms_norm_fwd + activation_quant; Eq. 1 P:501-505;
-// readings C1-C5, C7).  One CTA per row, the row held in registers, so the
-// activation is read from HBM exactly once (the point of the fused design,
-// P:391).  HBM-bound: reads K*sizeof(x), writes roundup(K,128) bytes + 12 B.
+// readings C1-C5, C7).  The row is held in registers, so the activation is read
+// from HBM exactly once (the point of the fused design).  HBM-bound:
+// reads K*sizeof(x), writes roundup(K,128) bytes + 12 B per row.
+//
+// TPR threads per row (32..256) so that every thread holds at most NV 16-byte
+// vectors: small register tiles keep occupancy (and bytes in flight) high.
+// Element loops are branch-free (out-of-row vectors are predicated to zero,
+// which also produces the zero padding up to Kp); sum(x^2) accumulates in
+// binary64 with explicit fma (C4), partials combined in a fixed order.
 #include "common.cuh"
 #include "internal.h"
 
 namespace tern {
 
-constexpr int kQThreads = 128;
+constexpr int kQThreads = 256;
 
-template <typename TX> struct Vec4;
-template <> struct Vec4<float> {
-  __device__ static void load(const float* p, float (&v)[4]) {
-    float4 t = __ldg(reinterpret_cast<const float4*>(p));
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+template <typename TX> struct QVec;
+template <> struct QVec<float> {
+  static constexpr int N = 4;
+  __device__ static void unpack(const uint4& u, float* v) {
+    v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y);
+    v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
   }
 };
-template <> struct Vec4<__nv_bfloat16> {
-  __device__ static void load(const __nv_bfloat16* p, float (&v)[4]) {
-    uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
-    v[0] = __uint_as_float(t.x << 16);
-    v[1] = __uint_as_float(t.x & 0xffff0000u);
-    v[2] = __uint_as_float(t.y << 16);
-    v[3] = __uint_as_float(t.y & 0xffff0000u);
+template <> struct QVec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ static void unpack(const uint4& u, float* v) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
   }
 };
 
-// Deterministic block reductions: fixed shuffle tree, then warp partials summed
-// in warp order by every thread.
-template <int NW>
-__device__ __forceinline__ double block_sum_f64(double v, double* red) {
-  v = warp_sum_f64(v);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double t = 0.0;
-#pragma unroll
-  for (int i = 0; i < NW; ++i) t += red[i];
-  return t;
-}
-template <int NW>
-__device__ __forceinline__ float block_max_f32(float v, float* red) {
-  v = warp_max_f32(v);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  float t = 0.0f;
-#pragma unroll
-  for (int i = 0; i < NW; ++i) t = fmaxf(t, red[i]);
-  return t;
-}
-template <int NW>
-__device__ __forceinline__ int block_sum_i32(int v, int* red) {
-  v = warp_sum_i32(v);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  int t = 0;
-#pragma unroll
-  for (int i = 0; i < NW; ++i) t += red[i];
-  return t;
+__device__ __forceinline__ uint4 ldg_stream_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
 }
 
-// NCH = max number of 4-element chunks per thread (compile-time register tile).
-template <typename TX, int NCH>
-__global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, int K, int ldx,
+// TPR threads per row, NV vectors per thread; CTA = kQThreads/TPR rows.
+template <typename TX, int TPR, int NV, bool GAIN>
+__global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, int M, int K, int ldx,
                                                      const float* __restrict__ gain, float eps,
-                                                     int8_t* __restrict__ q, int ldq,
+                                                     double inv_k, int8_t* __restrict__ q, int ldq,
                                                      float* __restrict__ deq,
                                                      int32_t* __restrict__ qsum,
                                                      float* __restrict__ inv_rms,
                                                      float* __restrict__ absmax) {
-  constexpr int NW = kQThreads / 32;
-  __shared__ double red_d[NW];
-  __shared__ float red_f[NW];
-  __shared__ int red_i[NW];
-  const int row = blockIdx.x;
-  const TX* xr = x + (int64_t)row * ldx;
-  const int nc = K >> 2;  // K % 16 == 0
-  float v[NCH][4];
-  double ss = 0.0;
-#pragma unroll
-  for (int i = 0; i < NCH; ++i) {
-    const int c = threadIdx.x + i * kQThreads;
-    if (c < nc) {
-      Vec4<TX>::load(xr + 4 * c, v[i]);
-    } else {
-      v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.0f;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) ss += (double)v[i][j] * (double)v[i][j];
-  }
-  ss = block_sum_f64<NW>(ss, red_d);
-  const float r = (float)(1.0 / sqrt(ss / (double)K + (double)eps));
-  float a = 0.0f;
-#pragma unroll
-  for (int i = 0; i < NCH; ++i) {
-    const int c = threadIdx.x + i * kQThreads;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float y = __fmul_rn(v[i][j], r);
-      if (gain && c < nc) y = __fmul_rn(y, __ldg(gain + 4 * c + j));
-      v[i][j] = y;
-      a = fmaxf(a, fabsf(y));
-    }
-  }
-  a = block_max_f32<NW>(a, red_f);
-  const float s = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
-  int8_t* qr = q + (int64_t)row * ldq;
-  const int ncp = ((K + kKAlign - 1) / kKAlign * kKAlign) >> 2;
-  int qs = 0;
-#pragma unroll
-  for (int i = 0; i < NCH; ++i) {
-    const int c = threadIdx.x + i * kQThreads;
-    if (c < ncp) {
-      uint32_t packed = 0;
-      if (c < nc && a > 0.0f) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          // |y*s| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
-          const int qi = (int)round_half_away(__fmul_rn(v[i][j], s));
-          qs += qi;
-          packed |= ((uint32_t)qi & 0xffu) << (8 * j);
-        }
-      }
-      reinterpret_cast<uint32_t*>(qr)[c] = packed;
-    }
-  }
-  qs = block_sum_i32<NW>(qs, red_i);
-  if (threadIdx.x == 0) {
-    deq[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 0.0f;
-    qsum[row] = qs;
-    if (inv_rms) inv_rms[row] = r;
-    if (absmax) absmax[row] = a;
-  }
-}
-
-// Warp-per-row variant for K <= 32*4*NV: no block-level barriers at all; 8 rows
-// per 256-thread CTA.  Same arithmetic, reductions in a fixed shuffle order.
-template <typename TX, int NV>
-__global__ void __launch_bounds__(256) k_quant_warp(const TX* __restrict__ x, int M, int K,
-                                                    int ldx, const float* __restrict__ gain,
-                                                    float eps, int8_t* __restrict__ q, int ldq,
-                                                    float* __restrict__ deq,
-                                                    int32_t* __restrict__ qsum,
-                                                    float* __restrict__ inv_rms,
-                                                    float* __restrict__ absmax) {
+  constexpr int VE = QVec<TX>::N;
+  constexpr int WPR = TPR / 32;                 // warps per row
+  constexpr int RPC = kQThreads / TPR;          // rows per CTA
+  __shared__ double red_d[RPC][WPR];
+  __shared__ float red_f[RPC][WPR];
+  __shared__ int red_i[RPC][WPR];
   const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= M) return;
-  const TX* xr = x + (int64_t)row * ldx;
-  const int nc = K >> 2;
-  float v[NV][4];
-  double ss = 0.0;
+  const int rloc = threadIdx.x / TPR, t = threadIdx.x % TPR, wr = t >> 5;
+  const int row = blockIdx.x * RPC + rloc;
+  const bool rv = row < M;
+  const int nvec = K / VE, nvecp = ((K + kKAlign - 1) / kKAlign * kKAlign) / VE;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)(rv ? row : 0) * ldx);
+
+  uint4 xv[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    const int c = lane + i * 32;
-    if (c < nc) {
-      Vec4<TX>::load(xr + 4 * c, v[i]);
-    } else {
-      v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.0f;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) ss += (double)v[i][j] * (double)v[i][j];
+    const int v = t + i * TPR;
+    xv[i] = (rv && v < nvec) ? ldg_stream_v4(xr + v) : make_uint4(0, 0, 0, 0);
   }
-  ss = warp_sum_f64(ss);
-  const float r = (float)(1.0 / sqrt(ss / (double)K + (double)eps));
-  float a = 0.0f;
+  double s0 = 0.0, s1 = 0.0;
+  float xm = 0.0f;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    const int c = lane + i * 32;
+    float v[VE];
+    QVec<TX>::unpack(xv[i], v);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float y = __fmul_rn(v[i][j], r);
-      if (gain && c < nc) y = __fmul_rn(y, __ldg(gain + 4 * c + j));
-      v[i][j] = y;
-      a = fmaxf(a, fabsf(y));
+    for (int j = 0; j < VE; j += 2) {
+      const double d0 = (double)v[j], d1 = (double)v[j + 1];
+      s0 = fma(d0, d0, s0);
+      s1 = fma(d1, d1, s1);
+      xm = fmaxf(xm, fmaxf(fabsf(v[j]), fabsf(v[j + 1])));
     }
   }
-  a = warp_max_f32(a);
-  const float s = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
-  int8_t* qr = q + (int64_t)row * ldq;
-  const int ncp = ((K + kKAlign - 1) / kKAlign * kKAlign) >> 2;
+  double ss = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    xm = fmaxf(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+  }
+  if (WPR > 1) {
+    if (lane == 0) { red_d[rloc][wr] = ss; red_f[rloc][wr] = xm; }
+    __syncthreads();
+    ss = red_d[rloc][0];
+    xm = red_f[rloc][0];
+#pragma unroll
+    for (int i = 1; i < WPR; ++i) { ss += red_d[rloc][i]; xm = fmaxf(xm, red_f[rloc][i]); }
+  }
+  const float r = (float)rsqrt(fma(ss, inv_k, (double)eps));
+  float amax;
+  if (!GAIN) {
+    // max|fl(x r)| = fl(max|x| r): rounding is monotone and r > 0
+    amax = __fmul_rn(xm, r);
+  } else {
+    float am = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int v = t + i * TPR;
+      float xf[VE];
+      QVec<TX>::unpack(xv[i], xf);
+      const float4* g4 = reinterpret_cast<const float4*>(gain + (v < nvec ? v : 0) * VE);
+#pragma unroll
+      for (int j = 0; j < VE; j += 4) {
+        const float4 g = __ldg(g4 + j / 4);
+        am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(xf[j], r), g.x)));
+        am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(xf[j + 1], r), g.y)));
+        am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(xf[j + 2], r), g.z)));
+        am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(xf[j + 3], r), g.w)));
+      }
+    }
+    am = warp_max_f32(am);
+    if (WPR > 1) {
+      __syncthreads();   // red_f of the first round has been read
+      if (lane == 0) red_f[rloc][wr] = am;
+      __syncthreads();
+      am = red_f[rloc][0];
+#pragma unroll
+      for (int i = 1; i < WPR; ++i) am = fmaxf(am, red_f[rloc][i]);
+    }
+    amax = am;
+  }
+  const float sc = amax > 0.0f ? __fdiv_rn(127.0f, amax) : 0.0f;
+  int8_t* qr = q + (int64_t)(rv ? row : 0) * ldq;
   int qs = 0;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    const int c = lane + i * 32;
-    if (c < ncp) {
-      uint32_t packed = 0;
-      if (c < nc && a > 0.0f) {
+    const int v = t + i * TPR;
+    float xf[VE];
+    QVec<TX>::unpack(xv[i], xf);   // zeros outside the row -> q = 0 (the padding)
+    uint32_t pk[VE / 4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          // |y*s| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
-          const int qi = (int)round_half_away(__fmul_rn(v[i][j], s));
-          qs += qi;
-          packed |= ((uint32_t)qi & 0xffu) << (8 * j);
-        }
+    for (int j4 = 0; j4 < VE / 4; ++j4) {
+      float g[4] = {1.0f, 1.0f, 1.0f, 1.0f};
+      if (GAIN) {
+        const float4 gg = __ldg(reinterpret_cast<const float4*>(gain + (v < nvec ? v : 0) * VE) + j4);
+        g[0] = gg.x; g[1] = gg.y; g[2] = gg.z; g[3] = gg.w;
       }
-      reinterpret_cast<uint32_t*>(qr)[c] = packed;
+      uint32_t w = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float y = __fmul_rn(xf[4 * j4 + j], r);
+        if (GAIN) y = __fmul_rn(y, g[j]);
+        // |y*sc| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
+        const int qi = __float2int_rz(round_half_away(__fmul_rn(y, sc)));
+        qs += qi;
+        w |= ((uint32_t)qi & 0xffu) << (8 * j);
+      }
+      pk[j4] = w;
+    }
+    if (rv && v < nvecp) {
+      if (VE == 4)
+        reinterpret_cast<uint32_t*>(qr)[v] = pk[0];
+      else
+        reinterpret_cast<uint2*>(qr)[v] = make_uint2(pk[0], pk[VE / 4 - 1]);
     }
   }
   qs = warp_sum_i32(qs);
-  if (lane == 0) {
-    deq[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 0.0f;
+  if (WPR > 1) {
+    if (lane == 0) red_i[rloc][wr] = qs;
+    __syncthreads();
+    qs = red_i[rloc][0];
+#pragma unroll
+    for (int i = 1; i < WPR; ++i) qs += red_i[rloc][i];
+  }
+  if (t == 0 && rv) {
+    deq[row] = amax > 0.0f ? __fdiv_rn(amax, 127.0f) : 0.0f;
     qsum[row] = qs;
     if (inv_rms) inv_rms[row] = r;
-    if (absmax) absmax[row] = a;
+    if (absmax) absmax[row] = amax;
   }
+}
+
+template <typename TX, int TPR, int NV>
+static void quant_go(const TX* x, int m, int k, int ldx, const float* gain, float eps, int8_t* q,
+                     int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
+                     cudaStream_t s) {
+  constexpr int RPC = kQThreads / TPR;
+  const int grid = (m + RPC - 1) / RPC;
+  const double inv_k = 1.0 / (double)k;
+  if (gain)
+    k_quant<TX, TPR, NV, true><<<grid, kQThreads, 0, s>>>(x, m, k, ldx, gain, eps, inv_k, q, ldq,
+                                                          deq, qsum, inv_rms, absmax);
+  else
+    k_quant<TX, TPR, NV, false><<<grid, kQThreads, 0, s>>>(x, m, k, ldx, gain, eps, inv_k, q, ldq,
+                                                           deq, qsum, inv_rms, absmax);
 }
 
 template <typename TX>
@@ -215,27 +204,18 @@ static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const floa
                                   int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
                                   float* absmax, cudaStream_t s) {
   const int kp = (k + kKAlign - 1) / kKAlign * kKAlign;
-  const int chunks = kp / 4;
-  const int nch = (chunks + kQThreads - 1) / kQThreads;
-  const int nv = (chunks + 31) / 32;
-  const int g8 = (m + 7) / 8;
-#define TERN_QW(N)                                                                            \
-  k_quant_warp<TX, N><<<g8, 256, 0, s>>>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, \
-                                         absmax)
-  if (nv <= 8) { TERN_QW(8); return cudaGetLastError(); }
-  if (nv <= 16) { TERN_QW(16); return cudaGetLastError(); }
-  if (nv <= 24) { TERN_QW(24); return cudaGetLastError(); }
-#undef TERN_QW
-#define TERN_Q(N)                                                                              \
-  k_quant<TX, N><<<m, kQThreads, 0, s>>>(x, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, \
-                                         absmax)
-  if (nch <= 2) TERN_Q(2);
-  else if (nch <= 4) TERN_Q(4);
-  else if (nch <= 8) TERN_Q(8);
-  else if (nch <= 14) TERN_Q(14);
-  else if (nch <= 32) TERN_Q(32);
-  else return cudaErrorInvalidValue;
-#undef TERN_Q
+  const int nvp = kp / QVec<TX>::N;   // vectors per (padded) row
+  // smallest threads-per-row with <= 8 vectors per thread
+  if (nvp <= 32 * 8)
+    quant_go<TX, 32, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+  else if (nvp <= 64 * 8)
+    quant_go<TX, 64, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+  else if (nvp <= 128 * 8)
+    quant_go<TX, 128, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+  else if (nvp <= 256 * 8)
+    quant_go<TX, 256, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+  else
+    return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
