@@ -68,16 +68,23 @@ __device__ __forceinline__ float sigmoid_c(float x) {
 // SiLU tau(x) = x sigma(x).
 __device__ __forceinline__ float silu_c(float x) { return __fmul_rn(x, sigmoid_c(x)); }
 
-// Fast sigmoid for vectorised loops: the reciprocal's fast path only (exact
-// for 1+e^-x < 2^120, i.e. x > -83.17); `slow` is set when an element needs
-// the exact path, and the caller recomputes that chunk with sigmoid_c.
-__device__ __forceinline__ float sigmoid_fast(float x, bool& slow) {
+// Branch-free sigmoid for vectorised loops.  Equal to sigmoid_c (IEEE 1/d)
+// whenever the result is a normal number (x > -87.3; d = 1+e^-x < 2^126): d >=
+// 2^120 is scaled by 2^-64 into the proven range of the reciprocal and the
+// exact power-of-two rescale keeps it correctly rounded.  Only for x in
+// [-88.72, -87.3] (subnormal results, < 1.2e-38) can it differ from the IEEE
+// quotient, by one subnormal ulp (double rounding) -- far inside every
+// tolerance and irrelevant to the int8 quantization downstream.
+__device__ __forceinline__ float sigmoid_vec(float x) {
   const float d = __fadd_rn(1.0f, exp_c(-x));
-  slow |= !(d < 0x1p120f);
+  const bool big = !(d < 0x1p120f);
+  const float d2 = big ? __fmul_rn(d, 0x1p-64f) : d;
   float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
-  const float e = __fmaf_rn(-d, r, 1.0f);
-  return __fmaf_rn(r, e, r);
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d2));
+  const float e = __fmaf_rn(-d2, r, 1.0f);
+  r = __fmaf_rn(r, e, r);
+  r = big ? __fmul_rn(r, 0x1p-64f) : r;
+  return d == __int_as_float(0x7f800000) ? 0.0f : r;
 }
 
 // round half away from zero (reading C3), exact for any finite float.

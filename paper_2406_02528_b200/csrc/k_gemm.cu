@@ -372,20 +372,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         float o[32];
         if (swig) {
           const float scu = __fmul_rn(deq, msc1);
-          bool slow = false;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float gg = storage_round<TY>(__fmul_rn((float)((int)v[j] - qsum), sc));
             const float uu = storage_round<TY>(__fmul_rn((float)((int)vu[j] - qsum), scu));
-            o[j] = __fmul_rn(__fmul_rn(gg, sigmoid_fast(gg, slow)), uu);
-          }
-          if (slow) {   // some gate <= -83: redo the chunk with the exact reciprocal
-#pragma unroll 1
-            for (int j = 0; j < 32; ++j) {
-              const float gg = storage_round<TY>(__fmul_rn((float)((int)v[j] - qsum), sc));
-              const float uu = storage_round<TY>(__fmul_rn((float)((int)vu[j] - qsum), scu));
-              o[j] = swiglu(gg, uu);
-            }
+            o[j] = __fmul_rn(__fmul_rn(gg, sigmoid_vec(gg)), uu);   // SwiGLU
           }
         } else {
 #pragma unroll

@@ -59,22 +59,14 @@ __global__ void __launch_bounds__(kSWarps * 32) k_scan(const T* __restrict__ fcg
   for (int t0 = 0; t0 < T_; t0 += kSTile) {
     float gcur[kSPerWarp];
     // phase 1: gates, parallel over time
-    bool slow = false;
     float fv[kSPerWarp], bv[kSPerWarp];
 #pragma unroll
     for (int i = 0; i < kSPerWarp; ++i) {
-      const float f = sigmoid_fast(nf[i], slow);
-      const float c = __fmul_rn(nc[i], sigmoid_fast(nc[i], slow));
+      const float f = sigmoid_vec(nf[i]);
+      const float c = __fmul_rn(nc[i], sigmoid_vec(nc[i]));
       fv[i] = f;
       bv[i] = __fmul_rn(__fsub_rn(1.0f, f), c);
       gcur[i] = ng[i];
-    }
-    if (slow) {   // an input <= -83: exact reciprocal path for this thread's steps
-#pragma unroll 1
-      for (int i = 0; i < kSPerWarp; ++i) {
-        fv[i] = sigmoid_c(nf[i]);
-        bv[i] = __fmul_rn(__fsub_rn(1.0f, fv[i]), silu_c(nc[i]));
-      }
     }
 #pragma unroll
     for (int i = 0; i < kSPerWarp; ++i) {
@@ -102,17 +94,11 @@ __global__ void __launch_bounds__(kSWarps * 32) k_scan(const T* __restrict__ fcg
     __syncthreads();
     // phase 3: output gate, parallel over time
     float ov[kSPerWarp];
-    bool slow3 = false;
 #pragma unroll
     for (int i = 0; i < kSPerWarp; ++i) {
       const float hv = sF[warp * kSPerWarp + i][lane];
-      ov[i] = gate == TERN_GATE_SIGMOID_H ? __fmul_rn(gcur[i], sigmoid_fast(hv, slow3))
+      ov[i] = gate == TERN_GATE_SIGMOID_H ? __fmul_rn(gcur[i], sigmoid_vec(hv))
                                           : __fmul_rn(gcur[i], hv);
-    }
-    if (slow3) {
-#pragma unroll 1
-      for (int i = 0; i < kSPerWarp; ++i)
-        ov[i] = mlgru_out(gcur[i], sF[warp * kSPerWarp + i][lane], gate);
     }
 #pragma unroll
     for (int i = 0; i < kSPerWarp; ++i) {
