@@ -44,6 +44,11 @@ struct QuantTaps {
   float* absmax;
 };
 
+// host: 2-D TMA descriptor (inner = contiguous dim), 128-B L2 promotion (k_gemm.cu)
+bool make_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                 uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                 CUtensorMapSwizzle swz);
+
 // a1
 cudaError_t launch_codes_init(uint32_t* codes, int n_rows, int ldw, cudaStream_t s);
 cudaError_t launch_absmean(const float* W, int64_t numel, const float* scale_in, float* scale_out,

@@ -2,126 +2,181 @@
 // ("linearized ... enabling a parallel scan").
 //
 // The recurrence h_t = f_t h_{t-1} + (1-f_t) c_t is evaluated exactly in the
-// sequential order of its definition (so h and o' are bit-identical to the
-// oracle), but only the two dependent operations per step stay sequential.
-// Per CTA (32 channels of one sequence, 8 warps) and time tile of 64 steps:
-//   phase 1 (all warps, parallel over time): f = sigma(fhat), c = SiLU(chat),
-//           b = (1-f) c  -> smem;  the next tile's loads are issued here
-//   phase 2 (one warp): h = f*h + b for 64 steps (FMUL + FADD per step)
-//   phase 3 (all warps, parallel over time): o' = ghat * sigma(h) -> global
-// This is the "chunked parallel scan" of the transcendental work with a
-// sequential carry: it keeps parity exact while spreading ~95% of the
-// arithmetic over time.
+// sequential order of its definition (h and o' bit-identical to the oracle);
+// only its two dependent operations per step stay sequential, everything
+// transcendental runs parallel over time.  One CTA = 32 channels of one
+// sequence, warp-specialised and pipelined over time tiles of kTS steps:
+//   warp 0 lane 0   TMA producer: 3 boxes [kTS steps x 32 ch] (f^, c^, g^ of the
+//                   fused interleaved pre-activations) per tile into a kS-deep ring
+//   warps 2..9      gates, phase 1 of tile i: f = sigma(f^), b = (1-f) SiLU(c^)
+//                   (parallel over time, lane = channel); then phase 3 of tile
+//                   i-1: o' = g^ sigma(h) (or g^ h) -> global
+//   warp 1          the carry: h = f h + b over the tile's steps, in order
+// so the serial carry of tile i overlaps the gate work of tiles i+1 and i-1,
+// and loads run kS tiles ahead.
 #include "epilogue.cuh"
 
 namespace tern {
 
-constexpr int kSCh = 32;         // channels per CTA (one per lane)
-constexpr int kSWarps = 8;
-constexpr int kSTile = 64;       // time steps per tile
-constexpr int kSPerWarp = kSTile / kSWarps;
+constexpr int kSCh = 32;                    // channels per CTA (one per lane)
+constexpr int kTS = 32;                     // time steps per tile
+constexpr int kS = 4;                       // ring stages
+constexpr int kGateWarps = 8;
+constexpr int kScanThreads = (2 + kGateWarps) * 32;
+constexpr int kStepsPerGateWarp = kTS / kGateWarps;
 
 template <typename T>
-__global__ void __launch_bounds__(kSWarps * 32) k_scan(const T* __restrict__ fcg, int B, int T_,
-                                                       int d, int gate, float* __restrict__ h,
-                                                       T* __restrict__ oprime) {
-  __shared__ float sF[kSTile][kSCh];   // f, then h after phase 2
-  __shared__ float sB[kSTile][kSCh];
+struct ScanSmem {
+  T in[kS][3][kTS][kSCh];       // TMA destination: f^, c^, g^
+  float fh[kS][kTS][kSCh];      // f, then h after the carry
+  float bv[kS][kTS][kSCh];      // (1-f) c
+  uint64_t full[kS], gated[kS], scanned[kS], empty[kS];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ CUtensorMap tmX, int B,
+                                                       int T_, int d, int gate,
+                                                       float* __restrict__ h, T* __restrict__ oprime) {
+  extern __shared__ __align__(128) uint8_t scan_smem[];
+  ScanSmem<T>& sm = *reinterpret_cast<ScanSmem<T>*>(scan_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cpb = d / kSCh;                       // channel blocks per sequence
   const int b = blockIdx.x / cpb;
   const int c0 = (blockIdx.x % cpb) * kSCh;
-  const int ch = c0 + lane;
   // interleaved fused layout: per 64-channel group [64 f | 64 c | 64 g]
-  const int colf = (c0 / kSegRows) * (3 * kSegRows) + (c0 % kSegRows) + lane;
-  const int64_t ld = 3 * (int64_t)d;
-  const T* base = fcg + (int64_t)b * T_ * ld;
-  T* obase = oprime + (int64_t)b * T_ * d;
+  const int colf = (c0 / kSegRows) * (3 * kSegRows) + (c0 % kSegRows);
+  const int nt = (T_ + kTS - 1) / kTS;
 
-  float nf[kSPerWarp], nc[kSPerWarp], ng[kSPerWarp];
-  auto load_tile = [&](int t0) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kS; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.gated[s], kGateWarps);
+      mbar_init(&sm.scanned[s], 1);
+      mbar_init(&sm.empty[s], kGateWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tmX);
+      const uint32_t bytes = 3u * kTS * kSCh * sizeof(T);
+      for (int i = 0; i < nt; ++i) {
+        const int s = i % kS;
+        if (i >= kS) mbar_wait(&sm.empty[s], ((i / kS) - 1) & 1);
+        mbar_arrive_expect_tx(&sm.full[s], bytes);
+        const int row = b * T_ + i * kTS;
 #pragma unroll
-    for (int i = 0; i < kSPerWarp; ++i) {
-      const int t = t0 + warp * kSPerWarp + i;
-      if (t < T_) {
-        const T* p = base + (int64_t)t * ld + colf;
-        nf[i] = ld_act<T>(p);
-        nc[i] = ld_act<T>(p + kSegRows);
-        ng[i] = ld_act<T>(p + 2 * kSegRows);
-      } else {
-        nf[i] = 0.0f; nc[i] = 0.0f; ng[i] = 0.0f;
+        for (int g = 0; g < 3; ++g)
+          tma_load_2d(&sm.in[s][g][0][0], &tmX, &sm.full[s], colf + g * kSegRows, row);
       }
     }
-  };
-
-  float hc = (warp == 0) ? h[(int64_t)b * d + ch] : 0.0f;
-  load_tile(0);
-  for (int t0 = 0; t0 < T_; t0 += kSTile) {
-    float gcur[kSPerWarp];
-    // phase 1: gates, parallel over time
-    float fv[kSPerWarp], bv[kSPerWarp];
-#pragma unroll
-    for (int i = 0; i < kSPerWarp; ++i) {
-      const float f = sigmoid_vec(nf[i]);
-      const float c = __fmul_rn(nc[i], sigmoid_vec(nc[i]));
-      fv[i] = f;
-      bv[i] = __fmul_rn(__fsub_rn(1.0f, f), c);
-      gcur[i] = ng[i];
-    }
-#pragma unroll
-    for (int i = 0; i < kSPerWarp; ++i) {
-      sF[warp * kSPerWarp + i][lane] = fv[i];
-      sB[warp * kSPerWarp + i][lane] = bv[i];
-    }
-    if (t0 + kSTile < T_) load_tile(t0 + kSTile);  // prefetch the next tile
-    __syncthreads();
-    // phase 2: the sequential carry (exact definition order: (f*h) + ((1-f)*c))
-    if (warp == 0) {
-      const int steps = min(kSTile, T_ - t0);
-      if (steps == kSTile) {
+  } else if (warp == 1) {
+    // ---------------- the carry (exact definition order: (f*h) + ((1-f)*c))
+    float hc = h[(int64_t)b * d + c0 + lane];
+    for (int i = 0; i < nt; ++i) {
+      const int s = i % kS;
+      mbar_wait(&sm.gated[s], (i / kS) & 1);
+      const int steps = min(kTS, T_ - i * kTS);
+      if (steps == kTS) {
 #pragma unroll 8
-        for (int t = 0; t < kSTile; ++t) {
-          hc = __fadd_rn(__fmul_rn(sF[t][lane], hc), sB[t][lane]);
-          sF[t][lane] = hc;
+        for (int t = 0; t < kTS; ++t) {
+          hc = __fadd_rn(__fmul_rn(sm.fh[s][t][lane], hc), sm.bv[s][t][lane]);
+          sm.fh[s][t][lane] = hc;
         }
       } else {
         for (int t = 0; t < steps; ++t) {
-          hc = __fadd_rn(__fmul_rn(sF[t][lane], hc), sB[t][lane]);
-          sF[t][lane] = hc;
+          hc = __fadd_rn(__fmul_rn(sm.fh[s][t][lane], hc), sm.bv[s][t][lane]);
+          sm.fh[s][t][lane] = hc;
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.scanned[s]);
     }
-    __syncthreads();
-    // phase 3: output gate, parallel over time
-    float ov[kSPerWarp];
+    h[(int64_t)b * d + c0 + lane] = hc;
+  } else {
+    // ---------------- gate warps
+    const int gw = warp - 2;
+    T* obase = oprime + (int64_t)b * T_ * d + c0 + lane;
+    auto phase1 = [&](int i) {
+      const int s = i % kS;
+      mbar_wait(&sm.full[s], (i / kS) & 1);
+      float fv[kStepsPerGateWarp], bvv[kStepsPerGateWarp];
 #pragma unroll
-    for (int i = 0; i < kSPerWarp; ++i) {
-      const float hv = sF[warp * kSPerWarp + i][lane];
-      ov[i] = gate == TERN_GATE_SIGMOID_H ? __fmul_rn(gcur[i], sigmoid_vec(hv))
-                                          : __fmul_rn(gcur[i], hv);
-    }
+      for (int j = 0; j < kStepsPerGateWarp; ++j) {
+        const int t = gw * kStepsPerGateWarp + j;
+        const float fx = ld_act<T>(&sm.in[s][0][t][lane]);
+        const float cx = ld_act<T>(&sm.in[s][1][t][lane]);
+        const float f = sigmoid_vec(fx);
+        fv[j] = f;
+        bvv[j] = __fmul_rn(__fsub_rn(1.0f, f), __fmul_rn(cx, sigmoid_vec(cx)));   // (1-f) SiLU(c)
+      }
 #pragma unroll
-    for (int i = 0; i < kSPerWarp; ++i) {
-      const int t = t0 + warp * kSPerWarp + i;
-      if (t < T_) st_act<T>(obase + (int64_t)t * d + ch, ov[i]);
+      for (int j = 0; j < kStepsPerGateWarp; ++j) {
+        const int t = gw * kStepsPerGateWarp + j;
+        sm.fh[s][t][lane] = fv[j];
+        sm.bv[s][t][lane] = bvv[j];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.gated[s]);
+    };
+    auto phase3 = [&](int i) {
+      const int s = i % kS;
+      mbar_wait(&sm.scanned[s], (i / kS) & 1);
+      float ov[kStepsPerGateWarp];
+#pragma unroll
+      for (int j = 0; j < kStepsPerGateWarp; ++j) {
+        const int t = gw * kStepsPerGateWarp + j;
+        const float gx = ld_act<T>(&sm.in[s][2][t][lane]);
+        const float hv = sm.fh[s][t][lane];
+        ov[j] = gate == TERN_GATE_SIGMOID_H ? __fmul_rn(gx, sigmoid_vec(hv)) : __fmul_rn(gx, hv);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);   // stage free once read
+#pragma unroll
+      for (int j = 0; j < kStepsPerGateWarp; ++j) {
+        const int t = i * kTS + gw * kStepsPerGateWarp + j;
+        if (t < T_) st_act<T>(obase + (int64_t)t * d, ov[j]);
+      }
+    };
+    for (int i = 0; i < nt; ++i) {
+      phase1(i);
+      if (i > 0) phase3(i - 1);
     }
-    __syncthreads();
+    phase3(nt - 1);
   }
-  if (warp == 0) h[(int64_t)b * d + ch] = hc;
+}
+
+template <typename TE>
+static cudaError_t scan_go(const CUtensorMap& tm, int grid, int B, int T, int d, int gate,
+                           float* h, void* oprime, cudaStream_t s) {
+  static bool attr = false;
+  const size_t smem = sizeof(ScanSmem<TE>);
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan<TE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_scan<TE><<<grid, kScanThreads, smem, s>>>(tm, B, T, d, gate, h, static_cast<TE*>(oprime));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
                         void* oprime, cudaStream_t s) {
   if (B == 0 || T == 0) return cudaSuccess;
   const int grid = B * (d / kSCh);
-  if (dt == TERN_BF16)
-    k_scan<__nv_bfloat16><<<grid, kSWarps * 32, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(fcg), B, T, d, gate, h,
-        static_cast<__nv_bfloat16*>(oprime));
-  else
-    k_scan<float><<<grid, kSWarps * 32, 0, s>>>(static_cast<const float*>(fcg), B, T, d, gate, h,
-                                                static_cast<float*>(oprime));
-  return cudaGetLastError();
+  const bool bf = dt == TERN_BF16;
+  const size_t es = bf ? 2 : 4;
+  CUtensorMap tm;
+  if (!make_map_2d(&tm, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, fcg,
+                   (uint64_t)3 * d, (uint64_t)B * T, (uint64_t)3 * d * es, kSCh, kTS,
+                   CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  return bf ? scan_go<__nv_bfloat16>(tm, grid, B, T, d, gate, h, oprime, s)
+            : scan_go<float>(tm, grid, B, T, d, gate, h, oprime, s);
 }
 
 }  // namespace tern
