@@ -43,10 +43,15 @@ def parse():
 
 def peaks():
     try:
-        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
-                "_fallback": True}
+        pk = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+              "_fallback": True}
+    try:   # dense INT8 peak measured on this pool by tools/int8_peak.py (cuBLASLt IMMA)
+        pk["int8"] = json.load(open(os.path.join(ROOT, "profiles", "int8_peak.json")))
+    except Exception:
+        pass
+    return pk
 
 
 # ------------------------------------------------------------------ clocks
@@ -133,7 +138,8 @@ def roofline(records, elem, pk, traffic_db):
         s = e["ms"] / 1e3
         if e["unit"] == "flop":
             ach = e["work"] / s / 1e12
-            peak = 2.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+            peak = pk["int8"]["int8_tops_sustained"] if "int8" in pk else \
+                2.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
             kernels[name] = {"bound": "tensor", "achieved": round(ach, 1), "peak": round(peak, 1),
                              "unit": "TFLOP/s", "frac": round(ach / peak, 4)}
         else:
@@ -169,8 +175,10 @@ def roofline(records, elem, pk, traffic_db):
         tr = traffic_db.get(dom)
         rl = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
               "unit": d["unit"], "frac": d["frac"], "traffic": tr,
-              "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained x 2 (int8:bf16 nominal "
-                              "ratio)" if d["bound"] == "tensor" else "MEASURED_PEAKS.json hbm_gbs")
+              "peak_source": (("profiles/int8_peak.json int8_tops_sustained (cuBLASLt s8 GEMM "
+                               "8192^3 measured on this pool, back to back)" if "int8" in pk else
+                               "MEASURED_PEAKS.json bf16_tflops_sustained x 2 (int8:bf16 nominal "
+                               "ratio)") if d["bound"] == "tensor" else "MEASURED_PEAKS.json hbm_gbs")
               + (" [fallback]" if pk.get("_fallback") else "")}
     return rl, kernels
 

@@ -285,11 +285,14 @@ void tern_trace_enable(int32_t on);
 int32_t tern_trace_collect(uint64_t* out, int32_t max_launches);
 
 /* Device self-check of the numerics shortcuts the kernels take (test use):
- * which = 0: the FMA-corrected reciprocal used by sigmoid equals IEEE 1/d for
- * every mantissa at exponents {0,1,2,5,10,20,40,60,80,100,119};
+ * which = 0: the FMA-corrected reciprocals used by the sigmoids equal IEEE
+ * 1/d for every mantissa of every exponent 0..125 (d in [1, 2^126));
  * which = 1: sigmoid equals 1/(1+exp_c(-x)) with IEEE division at 2^24
- * points in [-96, 96).  Synchronous; writes the mismatch count to *mismatches
- * (host).  ws: device scratch of >= 64 bytes. */
+ * points in [-96, 96);
+ * which = 2: the paired vector sigmoid of the scan / SwiGLU epilogue equals
+ * the same except that results below 2^-126 may be 0.
+ * Synchronous; writes the mismatch count to *mismatches (host).  ws: device
+ * scratch of >= 64 bytes. */
 tern_status tern_selftest(int32_t which, void* ws, uint64_t* mismatches);
 
 /* Tuning knob (host): largest m sent to the decode GEMV (default 4, max 4;

@@ -68,23 +68,59 @@ __device__ __forceinline__ float sigmoid_c(float x) {
 // SiLU tau(x) = x sigma(x).
 __device__ __forceinline__ float silu_c(float x) { return __fmul_rn(x, sigmoid_c(x)); }
 
-// Branch-free sigmoid for vectorised loops.  Equal to sigmoid_c (IEEE 1/d)
-// whenever the result is a normal number (x > -87.3; d = 1+e^-x < 2^126): d >=
-// 2^120 is scaled by 2^-64 into the proven range of the reciprocal and the
-// exact power-of-two rescale keeps it correctly rounded.  Only for x in
-// [-88.72, -87.3] (subnormal results, < 1.2e-38) can it differ from the IEEE
-// quotient, by one subnormal ulp (double rounding) -- far inside every
-// tolerance and irrelevant to the int8 quantization downstream.
-__device__ __forceinline__ float sigmoid_vec(float x) {
-  const float d = __fadd_rn(1.0f, exp_c(-x));
-  const bool big = !(d < 0x1p120f);
-  const float d2 = big ? __fmul_rn(d, 0x1p-64f) : d;
+// Fast reciprocal of d >= 1: MUFU estimate + one Newton step with an exact
+// FMA residual; equal to IEEE 1/d for 1 <= d < 2^126 (tern_selftest 0 checks
+// every mantissa of every exponent), 0 for d >= 2^126 (flush-to-zero).
+__device__ __forceinline__ float rcp_fast(float d) {
   float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d2));
-  const float e = __fmaf_rn(-d2, r, 1.0f);
-  r = __fmaf_rn(r, e, r);
-  r = big ? __fmul_rn(r, 0x1p-64f) : r;
-  return d == __int_as_float(0x7f800000) ? 0.0f : r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+  const float e = __fmaf_rn(-d, r, 1.0f);
+  return __fmaf_rn(r, e, r);
+}
+
+// a = a*b + c on two lanes at once (FFMA2, sm_100); FMA only -- an explicit
+// f32x2 mul+add pair could be contracted by ptxas, so none is written.
+__device__ __forceinline__ void fma2(float& a0, float& a1, float b0, float b1, float c0, float c1) {
+  unsigned long long A, B, Cc, D;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(Cc) : "f"(c0), "f"(c1));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(D) : "l"(A), "l"(B), "l"(Cc));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(D));
+}
+
+// Two sigmoids for vectorised loops (scan, SwiGLU epilogue): exp_c's exact
+// operation sequence with the FMAs paired on FFMA2, no branches and no range
+// selects.  Equal bit for bit to sigmoid_c (IEEE 1/(1+exp_c(-x))) whenever
+// that result is a normal number (>= 2^-126, i.e. x > -87.3); below it returns
+// 0 instead of a subnormal (< 1.2e-38): far inside every tolerance and
+// quantizing identically downstream.  Checked over 2^24 points by
+// tern_selftest 2.
+__device__ __forceinline__ void sigmoid2(float x0, float x1, float& s0, float& s1) {
+  const float y0 = -x0, y1 = -x1;
+  const float k0 = rintf(__fmul_rn(y0, 0x1.715476p+0f));
+  const float k1 = rintf(__fmul_rn(y1, 0x1.715476p+0f));
+  float r0 = -k0, r1 = -k1;
+  fma2(r0, r1, 0x1.62e400p-1f, 0x1.62e400p-1f, y0, y1);       // y - k ln2_hi
+  float t0 = -k0, t1 = -k1;
+  fma2(t0, t1, 0x1.7f7d1cp-20f, 0x1.7f7d1cp-20f, r0, r1);     // - k ln2_lo
+  r0 = t0; r1 = t1;
+  float p0 = 0x1.a01a02p-13f, p1 = 0x1.a01a02p-13f;
+  fma2(p0, p1, r0, r1, 0x1.6c16c2p-10f, 0x1.6c16c2p-10f);
+  fma2(p0, p1, r0, r1, 0x1.111112p-7f, 0x1.111112p-7f);
+  fma2(p0, p1, r0, r1, 0x1.555556p-5f, 0x1.555556p-5f);
+  fma2(p0, p1, r0, r1, 0x1.555556p-3f, 0x1.555556p-3f);
+  fma2(p0, p1, r0, r1, 0.5f, 0.5f);
+  fma2(p0, p1, r0, r1, 1.0f, 1.0f);
+  fma2(p0, p1, r0, r1, 1.0f, 1.0f);
+  // p * 2^k with k clamped to the normal exponents: k >= 128 (exp overflows)
+  // then gives d ~ 2^127 whose reciprocal flushes to 0 = 1/inf; k <= -127
+  // gives d == 1 exactly, as the true tiny exp would.
+  const int i0 = max(min((int)k0, 127), -126), i1 = max(min((int)k1, 127), -126);
+  const float e0 = __fmul_rn(p0, __int_as_float((i0 + 127) << 23));
+  const float e1 = __fmul_rn(p1, __int_as_float((i1 + 127) << 23));
+  s0 = rcp_fast(__fadd_rn(1.0f, e0));
+  s1 = rcp_fast(__fadd_rn(1.0f, e1));
 }
 
 // round half away from zero (reading C3), exact for any finite float.

@@ -373,10 +373,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (swig) {
           const float scu = __fmul_rn(deq, msc1);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float gg = storage_round<TY>(__fmul_rn((float)((int)v[j] - qsum), sc));
-            const float uu = storage_round<TY>(__fmul_rn((float)((int)vu[j] - qsum), scu));
-            o[j] = __fmul_rn(__fmul_rn(gg, sigmoid_vec(gg)), uu);   // SwiGLU
+          for (int j = 0; j < 32; j += 2) {
+            const float g0 = storage_round<TY>(__fmul_rn((float)((int)v[j] - qsum), sc));
+            const float g1 = storage_round<TY>(__fmul_rn((float)((int)v[j + 1] - qsum), sc));
+            const float u0 = storage_round<TY>(__fmul_rn((float)((int)vu[j] - qsum), scu));
+            const float u1 = storage_round<TY>(__fmul_rn((float)((int)vu[j + 1] - qsum), scu));
+            float s0, s1;
+            sigmoid2(g0, g1, s0, s1);
+            o[j] = __fmul_rn(__fmul_rn(g0, s0), u0);   // SwiGLU p = SiLU(g) u
+            o[j + 1] = __fmul_rn(__fmul_rn(g1, s1), u1);
           }
         } else {
 #pragma unroll

@@ -109,9 +109,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
         const int t = gw * kStepsPerGateWarp + j;
         const float fx = ld_act<T>(&sm.in[s][0][t][lane]);
         const float cx = ld_act<T>(&sm.in[s][1][t][lane]);
-        const float f = sigmoid_vec(fx);
+        float f, sc;
+        sigmoid2(fx, cx, f, sc);
         fv[j] = f;
-        bvv[j] = __fmul_rn(__fsub_rn(1.0f, f), __fmul_rn(cx, sigmoid_vec(cx)));   // (1-f) SiLU(c)
+        bvv[j] = __fmul_rn(__fsub_rn(1.0f, f), __fmul_rn(cx, sc));   // (1-f) SiLU(c)
       }
 #pragma unroll
       for (int j = 0; j < kStepsPerGateWarp; ++j) {
@@ -127,11 +128,19 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
       mbar_wait(&sm.scanned[s], (i / kS) & 1);
       float ov[kStepsPerGateWarp];
 #pragma unroll
-      for (int j = 0; j < kStepsPerGateWarp; ++j) {
+      for (int j = 0; j < kStepsPerGateWarp; j += 2) {
         const int t = gw * kStepsPerGateWarp + j;
-        const float gx = ld_act<T>(&sm.in[s][2][t][lane]);
-        const float hv = sm.fh[s][t][lane];
-        ov[j] = gate == TERN_GATE_SIGMOID_H ? __fmul_rn(gx, sigmoid_vec(hv)) : __fmul_rn(gx, hv);
+        const float g0 = ld_act<T>(&sm.in[s][2][t][lane]), g1 = ld_act<T>(&sm.in[s][2][t + 1][lane]);
+        const float h0 = sm.fh[s][t][lane], h1 = sm.fh[s][t + 1][lane];
+        if (gate == TERN_GATE_SIGMOID_H) {
+          float s0, s1;
+          sigmoid2(h0, h1, s0, s1);
+          ov[j] = __fmul_rn(g0, s0);
+          ov[j + 1] = __fmul_rn(g1, s1);
+        } else {
+          ov[j] = __fmul_rn(g0, h0);
+          ov[j + 1] = __fmul_rn(g1, h1);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);   // stage free once read

@@ -62,9 +62,11 @@ def acts(shape, seed, dtype="f32"):
 
 
 # ------------------------------------------------------------------------ numerics shortcuts
-@pytest.mark.parametrize("which", [0, 1])
+@pytest.mark.parametrize("which", [0, 1, 2])
 def test_device_selftest(L, which):
-    """The FMA-corrected reciprocal inside sigmoid equals IEEE division everywhere tested."""
+    """The FMA-corrected reciprocals equal IEEE division on [1, 2^126); the scalar sigmoid
+    equals 1/(1+exp_c(-x)); the paired vector sigmoid equals it wherever the result is a
+    normal number."""
     assert L.tern_selftest(which) == 0
 
 
