@@ -183,6 +183,25 @@ def roofline(records, elem, pk, traffic_db):
     return rl, kernels
 
 
+# ------------------------------------------------------------------ multi-rank timing
+def max_over_ranks(ms: float, world: int, device=None) -> float:
+    """The job's time is the slowest rank's (B200_PROFILING.md): all-reduce MAX."""
+    if world <= 1:
+        return float(ms)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def split_sequences(B_global: int, world: int, rank: int) -> tuple[int, int]:
+    """Data-parallel split of a global batch of sequences: (first, count) of rank."""
+    base, extra = divmod(B_global, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
 # ------------------------------------------------------------------ oracle (cpu) arm
 def oracle_blocks(latents, cfg):
     import oracle as O
@@ -334,10 +353,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     recs = L.tern_profile_collect()
     ck = clocks.stop()
     ms = sum(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ms, world, dev)
     tokens = B * T * args.steps * world
     value = tokens / (ms_max / 1e3)
     rl, kernels = roofline(recs, elem, pk, traffic_db)
@@ -363,10 +379,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     e1.record()
     torch.cuda.synchronize()
     barrier()
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e = {"value": round(tokens / (float(t.item()) / 1e3), 1), "unit": "tokens/s",
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world, dev)
+    e2e = {"value": round(tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
            "h2d_bytes_per_step": xh.numel() * xh.element_size(),
            "d2h_bytes_per_step": yh.numel() * yh.element_size(),
            "path": "Stack.prefill via block_prefill (C ABI), pinned host buffers"}
@@ -396,10 +410,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     d1.record()
     torch.cuda.synchronize()
     barrier()
-    t = torch.tensor([d0.elapsed_time(d1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dms = float(t.item())
+    dms = max_over_ranks(d0.elapsed_time(d1), world, dev)
     wbytes = st.weight_bytes
     dec = {"tokens_per_s": round(nd * Bd * world / (dms / 1e3), 1), "batch_per_gpu": Bd,
            "steps": nd, "ms_per_token_step": round(dms / nd, 4),

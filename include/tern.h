@@ -208,10 +208,33 @@ typedef struct {
   float eps;
 } tern_glu;
 
+/* Output-feature sharding of a block over `world` ranks (BASELINE.json
+ * configs[3,4]).  Rank r holds the rows of every
+ * BitLinear for its channel slice: f, c, g, o and down rows [r*ds, (r+1)*ds)
+ * with ds = d/world, gate and up rows [r*ls, (r+1)*ls) with ls = l/world, each
+ * packed with the FULL matrix's mean|W| scale (tern_pack's scale_in).  Its
+ * state h is [B][ds].  Before every BitLinear the input row is gathered whole
+ * (the row norm and the contraction need all K), so each block calls `ag`
+ * four times on `stream`: o', x1, p and y.  ag(ctx, send, recv,
+ * bytes_per_rank, stream) must place the world equal chunks, in rank order,
+ * at recv (a torch.distributed / NCCL all-gather into a tensor) and return 0;
+ * it is called from inside block_prefill / block_decode (also during CUDA
+ * graph capture).  Outputs are bit-identical to world = 1: gathers move
+ * values unchanged, int32 sums are exact and every norm sees the full row.
+ * Requires ds % 64 == 0 and ls % 16 == 0.  world <= 1: no sharding. */
+typedef int (*tern_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes_per_rank,
+                                 tern_stream stream);
+typedef struct {
+  int32_t rank, world;
+  tern_allgather_fn ag;
+  void* ctx;
+} tern_shard;
+
 typedef struct {
   tern_mlgru mix;
   tern_glu ch;
-  int32_t d, l;
+  int32_t d, l;       /* full widths (also when sharded) */
+  tern_shard shard;   /* zero-initialise for an unsharded block */
 } tern_block;
 
 /* Workspace bytes for mlgru_fwd / glu_fwd / block_* on B sequences x T tokens. */
@@ -221,7 +244,8 @@ size_t tern_block_workspace(const tern_block* b, int32_t B, int32_t T, tern_dtyp
 
 /* Byte offsets of the block's intermediates inside its workspace, valid after
  * block_prefill / block_decode returns on the stream (parity taps):
- *   fcg [B*T][3d], oprime [B*T][d], x1 [B*T][d], p [B*T][l], all dtype dt. */
+ *   fcg [B*T][3d], oprime [B*T][d], x1 [B*T][d], p [B*T][l], all dtype dt
+ *   (sharded blocks: fcg of the rank's channels; oprime, x1, p gathered whole). */
 typedef struct {
   size_t fcg, oprime, x1, p;
 } tern_block_taps;

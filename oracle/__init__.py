@@ -100,6 +100,7 @@ def lib():
             L.orc_block.argtypes = [C.POINTER(MlgruW), C.POINTER(GluW), f32p, C.c_int, C.c_int,
                                     C.c_int, C.c_int, C.c_float, C.c_int, C.c_int, f32p, f32p,
                                     C.c_void_p]
+            L.orc_swiglu_arr.argtypes = [f32p, f32p, C.c_int64, C.c_int, f32p]
             L.orc_set_threads.argtypes = [C.c_int]
             L.orc_get_threads.restype = C.c_int
             _lib = L
@@ -285,6 +286,14 @@ def mlgru_scan(fhat, chat, ghat, H, gate_mode=0, bf16=False):
     _check(lib().orc_mlgru_scan(fhat, chat, ghat, B, T, d, int(gate_mode), int(bf16), H, o),
            "mlgru_scan")
     return o, H
+
+
+def silu_mul(g, u, bf16=False):
+    """GLU gating p = SiLU(g) * u, elementwise."""
+    g, u = _f32(g), _f32(u)
+    p = np.empty_like(g)
+    lib().orc_swiglu_arr(g.ravel(), u.ravel(), g.size, int(bf16), p.ravel())
+    return p
 
 
 # ---------------------------------------------------------------- weights

@@ -442,6 +442,14 @@ int orc_mlgru(const orc_mlgru_w* w, const float* X, int B, int T, int d, float e
 /* p = tau(g) * u, d = p (*) W_d.  No biases.  bf16 rounds p (R2). */
 /* Taps (optional): ghat, uhat [M][l], p [M][l].                               */
 /* ------------------------------------------------------------------------ */
+/* GLU gating p = tau(g) * u elementwise; bf16 mode rounds p (R2). */
+void orc_swiglu_arr(const float* g, const float* u, int64_t n, int bf16, float* p) {
+  for (int64_t i = 0; i < n; ++i) {
+    float v = orc_silu(g[i]) * u[i];
+    p[i] = bf16 ? orc_bf16(v) : v;
+  }
+}
+
 int orc_glu(const orc_glu_w* w, const float* X, int M, int d, int l, float eps, int bf16,
             float* O, float* ghat, float* uhat, float* p) {
   int64_t n = (int64_t)M * l;
@@ -451,11 +459,7 @@ int orc_glu(const orc_glu_w* w, const float* X, int M, int d, int l, float eps, 
   int rc = 0;
   rc |= orc_bitlinear(X, M, d, w->gain_x, eps, w->tg, l, w->mg, 0, bf16, G, 0, 0, 0);
   rc |= orc_bitlinear(X, M, d, w->gain_x, eps, w->tu, l, w->mu, 0, bf16, U, 0, 0, 0);
-  for (int64_t i = 0; i < n; ++i) {
-    float v = orc_silu(G[i]) * U[i];
-    if (bf16) v = orc_bf16(v);
-    Pp[i] = v;
-  }
+  orc_swiglu_arr(G, U, n, bf16, Pp);
   rc |= orc_bitlinear(Pp, M, l, w->gain_p, eps, w->td, d, w->md, 0, bf16, O, 0, 0, 0);
   if (!ghat) free(G);
   if (!uhat) free(U);

@@ -47,8 +47,18 @@ class tern_glu(C.Structure):
                 ("gain_p", C.c_void_p), ("eps", C.c_float)]
 
 
+# int ag(void* ctx, const void* send, void* recv, size_t bytes_per_rank, cudaStream_t stream)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class tern_shard(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("ag", ALLGATHER_FN),
+                ("ctx", C.c_void_p)]
+
+
 class tern_block(C.Structure):
-    _fields_ = [("mix", tern_mlgru), ("ch", tern_glu), ("d", C.c_int32), ("l", C.c_int32)]
+    _fields_ = [("mix", tern_mlgru), ("ch", tern_glu), ("d", C.c_int32), ("l", C.c_int32),
+                ("shard", tern_shard)]
 
 
 class tern_block_taps(C.Structure):

@@ -139,9 +139,12 @@ Epi make_epi(int kind, const tern_weight& w, const float* bias, void* out, int l
 }
 
 struct BlockWs {
-  size_t q, deq, qsum, fcg, oprime, x1, p, total;
+  size_t q, deq, qsum, fcg, oprime, x1, p, sout, gbuf, total;
 };
-BlockWs block_ws(int32_t M, int32_t d, int32_t l, int32_t fcg_rows, tern_dtype dt) {
+// world > 1 adds the rank's local outputs [M][max(ds,ls)] and the gather
+// target [world][M][max(ds,ls)] (M > 1 gathers are then unshuffled to [M][width])
+BlockWs block_ws(int32_t M, int32_t d, int32_t l, int32_t fcg_rows, tern_dtype dt,
+                 int32_t world = 1) {
   BlockWs w{};
   size_t off = 0;
   const int kq = kpad(d > l ? d : l);
@@ -152,6 +155,12 @@ BlockWs block_ws(int32_t M, int32_t d, int32_t l, int32_t fcg_rows, tern_dtype d
   w.oprime = off; off += al256((size_t)M * d * dsize(dt));
   w.x1 = off; off += al256((size_t)M * d * dsize(dt));
   w.p = off; off += al256((size_t)M * (l > 0 ? l : 1) * dsize(dt));
+  w.sout = w.gbuf = off;
+  if (world > 1) {
+    const size_t cs = (size_t)((d > l ? d : l) / world);
+    w.sout = off; off += al256((size_t)M * cs * dsize(dt));
+    w.gbuf = off; off += al256((size_t)world * M * cs * dsize(dt));
+  }
   w.total = off;
   return w;
 }
@@ -175,18 +184,29 @@ tern_status bl_tc(const void* x, tern_dtype xdt, int M, int K, int ldx, const fl
   return TERN_OK;
 }
 
+int block_world(const tern_block* b) { return b->shard.world > 1 ? b->shard.world : 1; }
+
 tern_status check_block(const tern_block* b) {
   CHECK(b, "null block");
   const int d = b->d, l = b->l;
   CHECK(d > 0 && d % 64 == 0, "d=%d must be a positive multiple of 64", d);
   CHECK(l > 0 && l % 16 == 0, "l=%d must be a positive multiple of 16", l);
+  const int world = block_world(b);
+  if (world > 1) {
+    CHECK(b->shard.ag, "sharded block: null all-gather callback");
+    CHECK(b->shard.rank >= 0 && b->shard.rank < world, "shard rank %d of %d", b->shard.rank, world);
+    CHECK(d % (64 * world) == 0 && l % (16 * world) == 0,
+          "sharded block: d/world=%d must be a multiple of 64 and l/world=%d of 16", d / world,
+          l / world);
+  }
+  const int ds = d / world, ls = l / world;
   tern_status st;
   if ((st = check_weight(&b->mix.fcg, d, 3, "fcg")) != TERN_OK) return st;
   if ((st = check_weight(&b->mix.o, d, 1, "o")) != TERN_OK) return st;
   if ((st = check_weight(&b->ch.gu, d, 2, "gate|up")) != TERN_OK) return st;
   if ((st = check_weight(&b->ch.down, l, 1, "down")) != TERN_OK) return st;
-  CHECK(b->mix.fcg.n_out == d && b->mix.o.n_out == d, "MLGRU weights must be d x d");
-  CHECK(b->ch.gu.n_out == l && b->ch.down.n_out == d, "GLU weights must be d->l, l->d");
+  CHECK(b->mix.fcg.n_out == ds && b->mix.o.n_out == ds, "MLGRU weights must be d x d/world");
+  CHECK(b->ch.gu.n_out == ls && b->ch.down.n_out == ds, "GLU weights must be d->l/world, l->d/world");
   CHECK(b->mix.gate == TERN_GATE_SIGMOID_H || b->mix.gate == TERN_GATE_LINEAR_H, "bad gate mode");
   CHECK(b->mix.eps > 0 && b->ch.eps > 0, "eps must be > 0");
   return TERN_OK;
@@ -420,13 +440,13 @@ size_t tern_glu_workspace(const tern_glu* p, int32_t m, int32_t d, int32_t l, te
 }
 size_t tern_block_workspace(const tern_block* b, int32_t B, int32_t T, tern_dtype dt) {
   if (!b) return 0;
-  return block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt).total;
+  return block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt, block_world(b)).total;
 }
 
 tern_status tern_block_ws_layout(const tern_block* b, int32_t B, int32_t T, tern_dtype dt,
                                  tern_block_taps* out) {
   CHECK(b && out, "tern_block_ws_layout: null pointer");
-  BlockWs w = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt);
+  BlockWs w = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt, block_world(b));
   out->fcg = w.fcg;
   out->oprime = w.oprime;
   out->x1 = w.x1;
@@ -504,6 +524,76 @@ tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, ter
                nullptr, s);
 }
 
+// one BitLinear on either path (decode GEMV with its fused prologue, or quant + GEMM)
+tern_status bitlinear_any(bool gemv, const void* x, tern_dtype dt, int M, int K, const float* gain,
+                          float eps, const tern_weight& w, const Epi& e, void* ws, const BlockWs& L,
+                          cudaStream_t s) {
+  if (gemv) {
+    Prof pr(TERN_K_GEMV, e.kind, M, w.n_rows, K, w.n_seg, dt, s);
+    TRY_CUDA(launch_gemv(x, dt, dt, M, K, K, gain, eps, w, e, nullptr, s), "gemv");
+    return TERN_OK;
+  }
+  return bl_tc(x, dt, M, K, K, gain, eps, w, dt, e, at<int8_t>(ws, L.q), kpad(K),
+               at<float>(ws, L.deq), at<int32_t>(ws, L.qsum), nullptr, nullptr, s);
+}
+
+// gather the ranks' [M][cs] slices into full [M][world*cs] rows
+tern_status shard_gather(const tern_shard& sh, const void* send, void* full, int M, int cs,
+                         tern_dtype dt, void* ws, const BlockWs& L, cudaStream_t s) {
+  const size_t bytes = (size_t)M * cs * dsize(dt);
+  void* dst = M == 1 ? full : at<char>(ws, L.gbuf);
+  const int rc = sh.ag(sh.ctx, send, dst, bytes, (tern_stream)s);
+  if (rc != 0) return fail(TERN_ERR_CUDA, "all-gather callback failed (%d)", rc);
+  if (M > 1) TRY_CUDA(launch_unshard(dst, dt, sh.world, M, cs, full, s), "unshard");
+  return TERN_OK;
+}
+
+// a8 with output-feature sharding (tern.h tern_shard): 4 gathers per block
+tern_status run_block_sharded(const tern_block& b, const void* x, void* y, tern_dtype dt, int B,
+                              int T, float* h, void* ws, const BlockWs& L, cudaStream_t s) {
+  const tern_shard& sh = b.shard;
+  const int M = B * T, d = b.d, l = b.l, ds = d / sh.world, ls = l / sh.world;
+  const size_t es = dsize(dt);
+  const tern_mlgru& mx = b.mix;
+  const tern_glu& gl = b.ch;
+  const bool gv = T == 1 && B <= g_gemv_max_m && gemv_supported(B, d, dt) &&
+                  gemv_supported(B, l, dt);
+  void* sout = at<char>(ws, L.sout);
+  void* op = at<char>(ws, L.oprime);
+  void* x1 = at<char>(ws, L.x1);
+  void* pf = at<char>(ws, L.p);
+  tern_status st;
+  // token mixer on this rank's channels: f, c, g -> (scan) -> o'_r
+  if (gv) {
+    Epi e1 = make_epi(EPI_MLGRU, mx.fcg, mx.bias_fcg, sout, ds);
+    e1.h = h;
+    e1.gate = mx.gate;
+    if ((st = bitlinear_any(true, x, dt, M, d, mx.gain_x, mx.eps, mx.fcg, e1, ws, L, s))) return st;
+  } else {
+    void* fcg = at<char>(ws, L.fcg);
+    Epi e1 = make_epi(EPI_FCG, mx.fcg, mx.bias_fcg, fcg, mx.fcg.n_rows);
+    if ((st = bitlinear_any(false, x, dt, M, d, mx.gain_x, mx.eps, mx.fcg, e1, ws, L, s))) return st;
+    Prof pr(TERN_K_SCAN, mx.gate, M, ds, ds, 3, dt, s);
+    TRY_CUDA(launch_scan(fcg, dt, B, T, ds, mx.gate, h, sout, s), "scan");
+  }
+  if ((st = shard_gather(sh, sout, op, M, ds, dt, ws, L, s))) return st;
+  // o: x1_r = x[:, r] + o'(*)W_o[r]
+  Epi e2 = make_epi(EPI_RESID, mx.o, mx.bias_o, sout, ds);
+  e2.res = static_cast<const char*>(x) + (size_t)sh.rank * ds * es;
+  e2.ldr = d;
+  if ((st = bitlinear_any(gv, op, dt, M, d, mx.gain_o, mx.eps, mx.o, e2, ws, L, s))) return st;
+  if ((st = shard_gather(sh, sout, x1, M, ds, dt, ws, L, s))) return st;
+  // channel mixer: p_r = SiLU(g_r) u_r, then y_r = x1[:, r] + p(*)W_d[r]
+  Epi e3 = make_epi(EPI_SWIGLU, gl.gu, nullptr, sout, ls);
+  if ((st = bitlinear_any(gv, x1, dt, M, d, gl.gain_x, gl.eps, gl.gu, e3, ws, L, s))) return st;
+  if ((st = shard_gather(sh, sout, pf, M, ls, dt, ws, L, s))) return st;
+  Epi e4 = make_epi(EPI_RESID, gl.down, nullptr, sout, ds);
+  e4.res = static_cast<const char*>(x1) + (size_t)sh.rank * ds * es;
+  e4.ldr = d;
+  if ((st = bitlinear_any(gv, pf, dt, M, l, gl.gain_p, gl.eps, gl.down, e4, ws, L, s))) return st;
+  return shard_gather(sh, sout, y, M, ds, dt, ws, L, s);
+}
+
 tern_status check_act(const void* x, const void* y, const void* ws, size_t ws_bytes, size_t need,
                       tern_dtype dt, const char* name) {
   CHECK(x && y, "%s: null x/y", name);
@@ -557,11 +647,12 @@ static tern_status block_run(const tern_block* b, const void* x, void* y, tern_d
   if (st) return st;
   CHECK(h, "%s: null state", name);
   CHECK(B >= 0 && T >= 0, "%s: B=%d T=%d", name, B, T);
-  BlockWs L = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt);
+  BlockWs L = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt, block_world(b));
   if ((st = check_act(x, y, ws, ws_bytes, L.total, dt, name)) != TERN_OK) return st;
   if ((st = check_device()) != TERN_OK) return st;
   if (B * T == 0) return TERN_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (block_world(b) > 1) return run_block_sharded(*b, x, y, dt, B, T, h, ws, L, s);
   void* x1 = at<char>(ws, L.x1);
   if ((st = run_mlgru(b->mix, x, x1, true, dt, B, T, b->d, h, ws, L, s)) != TERN_OK) return st;
   return run_glu(b->ch, x1, y, true, dt, B * T, b->d, b->l, ws, L, s);

@@ -75,6 +75,9 @@ int gemv_trace_collect(unsigned long long* out, int max_launches);
 cudaError_t launch_selftest(int which, unsigned long long* bad, int* exps, int n_exp,
                             cudaStream_t s);
 cudaError_t launch_expand(const tern_weight& w, uint8_t* e8, cudaStream_t s);
+// sharding: full[m][r*cs + j] = gathered[r][m][j]
+cudaError_t launch_unshard(const void* gathered, int dt, int world, int M, int cs, void* full,
+                           cudaStream_t s);
 // a6
 cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
                         void* oprime, cudaStream_t s);

@@ -52,14 +52,25 @@ class Block:
     """One MatMul-free block: MLGRU token mixer + GLU channel mixer."""
 
     def __init__(self, latent: dict, d: int, l: int, gate=L.TERN_GATE_SIGMOID_H, eps=1e-6,
-                 gains: dict | None = None, biases: dict | None = None, device="cuda"):
+                 gains: dict | None = None, biases: dict | None = None, device="cuda",
+                 shard=None):
+        """shard = (rank, AllGather) for an output-feature-sharded block (shard.py);
+        latent holds the FULL matrices, gains/biases this rank's slices."""
         self.d, self.l = d, l
         dev = torch.device(device)
         lat = {k: v.to(dev) for k, v in latent.items()}
-        self.fcg = PackedWeight([lat["f"], lat["c"], lat["g"]])
-        self.o = PackedWeight([lat["o"]])
-        self.gu = PackedWeight([lat["gate"], lat["up"]])
-        self.down = PackedWeight([lat["down"]])
+        sc = {k: None for k in lat}
+        if shard is not None:
+            from . import shard as S
+            rank, gather = shard
+            sc = S.full_scales(lat, dev)
+            lat = S.shard_latents(lat, d, l, gather.world, rank)
+        self.fcg = PackedWeight([lat["f"], lat["c"], lat["g"]],
+                                None if sc["f"] is None else [sc["f"], sc["c"], sc["g"]])
+        self.o = PackedWeight([lat["o"]], None if sc["o"] is None else [sc["o"]])
+        self.gu = PackedWeight([lat["gate"], lat["up"]],
+                               None if sc["gate"] is None else [sc["gate"], sc["up"]])
+        self.down = PackedWeight([lat["down"]], None if sc["down"] is None else [sc["down"]])
         gains = gains or {}
         biases = biases or {}
         self._keep = []
@@ -73,7 +84,7 @@ class Block:
 
         bias_fcg = None
         if any(biases.get(k) is not None for k in ("f", "c", "g")):
-            z = torch.zeros(d)
+            z = torch.zeros(self.fcg.n_out)
             bias_fcg = torch.cat([biases.get(k, z).float().cpu() for k in ("f", "c", "g")])
         self.mix = L.tern_mlgru(self.fcg.struct, self.o.struct, dp(gains.get("x")),
                                 dp(gains.get("o")), dp(bias_fcg), dp(biases.get("o")), int(gate),
@@ -81,6 +92,9 @@ class Block:
         self.ch = L.tern_glu(self.gu.struct, self.down.struct, dp(gains.get("x1")),
                              dp(gains.get("p")), float(eps))
         self.struct = L.tern_block(self.mix, self.ch, d, l)
+        if shard is not None:
+            from . import shard as S
+            self.struct.shard = S.make_shard(shard[1], shard[0])
 
     @property
     def weight_bytes(self) -> int:
@@ -106,10 +120,15 @@ class Stack:
         self._ws = None
         self._ws_bytes = 0
         self._graph = None
+        self.gather = None   # shard.AllGather of a sharded stack
+
+    def _reg(self, *ts):
+        if self.gather is not None:
+            self.gather.register(*[t for t in ts if t is not None])
 
     @classmethod
     def random(cls, cfg: synth.Config, device="cuda", gate=L.TERN_GATE_SIGMOID_H, n_blocks=None,
-               gen_device=None, keep_latents=0):
+               gen_device=None, keep_latents=0, shard=None):
         """Build cfg's stack from seeded N(0, 0.02) latents (drawn per block on
         gen_device, packed on the GPU and dropped).  keep_latents=n keeps the
         first n blocks' latents on the host (for oracle parity)."""
@@ -120,9 +139,11 @@ class Stack:
             lat = synth.latent_block(cfg.d, cfg.l, g, device=gen_device)
             if i < keep_latents:
                 kept.append({k: v.cpu() for k, v in lat.items()})
-            blocks.append(Block(lat, cfg.d, cfg.l, gate=gate, eps=cfg.eps, device=device))
+            blocks.append(Block(lat, cfg.d, cfg.l, gate=gate, eps=cfg.eps, device=device,
+                                shard=shard))
             del lat
         st = cls(blocks, cfg.d, cfg.l, synth.torch_dtype(cfg.dtype), device)
+        st.gather = None if shard is None else shard[1]
         st.latents = kept
         st.generator = g
         return st
@@ -136,10 +157,13 @@ class Stack:
         if self._ws is None or self._ws_bytes < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
             self._ws_bytes = need
+            self._reg(self._ws)
         return self._ws
 
     def new_state(self, B: int) -> list:
-        return [torch.zeros((B, self.d), dtype=torch.float32, device=self.device)
+        """One fp32 state per block: [B][d], or [B][d/world] for a sharded stack."""
+        w = self.gather.world if self.gather is not None else 1
+        return [torch.zeros((B, self.d // w), dtype=torch.float32, device=self.device)
                 for _ in self.blocks]
 
     def prefill(self, x: torch.Tensor, states: list, out: torch.Tensor | None = None,
@@ -149,6 +173,7 @@ class Stack:
         ws = self.workspace(B, T)
         if bufs is None:
             bufs = (torch.empty_like(x), torch.empty_like(x))
+        self._reg(x, out, *bufs)
         cur = x
         for i, blk in enumerate(self.blocks):
             nxt = bufs[i % 2] if (i < len(self.blocks) - 1 or out is None) else out
@@ -163,6 +188,7 @@ class Stack:
         ws = self.workspace(B, 1)
         if bufs is None:
             bufs = (torch.empty_like(x), torch.empty_like(x))
+        self._reg(x, out, *bufs)
         cur = x
         for i, blk in enumerate(self.blocks):
             nxt = bufs[i % 2] if (i < len(self.blocks) - 1 or out is None) else out

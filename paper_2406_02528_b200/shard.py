@@ -1,0 +1,146 @@
+"""Output-feature sharding of the MatMul-free block over ranks (tern.h
+`tern_shard`; BASELINE.json configs[3,4]).
+
+Rank r owns channels [r*ds, (r+1)*ds) of f, c, g, o and down (ds = d/world)
+and [r*ls, (r+1)*ls) of gate and up (ls = l/world).  Its weight rows are packed
+with the FULL matrix's absmean scale (one scale per matrix), so every
+output element is computed exactly as without sharding; the library gathers
+the 4 per-block activations (o', x1, p, y) through the callback of an
+`AllGather` object.  Two back-ends:
+  * `NcclAllGather`: torch.distributed all_gather_into_tensor (NCCL over
+    NVLink / NVSwitch, one process per GPU) on the library's stream;
+  * `ThreadAllGather`: `world` virtual ranks as host threads on one GPU, each
+    with its own stream, ordered by CUDA events (no kernel waits on another) --
+    the single-GPU emulation used by the tests.
+`plan()` is the pure host-side partition (tested on CPU with gloo against the
+oracle in tests/test_shard_cpu.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import torch
+
+from . import _lib as L
+
+
+def plan(d: int, l: int, world: int, rank: int) -> dict:
+    """Channel ranges of `rank` (pure host logic)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} of world {world}")
+    if d % world or l % world:
+        raise ValueError(f"d={d} and l={l} must divide by world={world}")
+    ds, ls = d // world, l // world
+    if world > 1 and (ds % 64 or ls % 16):
+        raise ValueError(f"d/world={ds} must be a multiple of 64 and l/world={ls} of 16")
+    return {"ds": ds, "ls": ls, "ch": (rank * ds, (rank + 1) * ds),
+            "gl": (rank * ls, (rank + 1) * ls)}
+
+
+def shard_latents(latent: dict, d: int, l: int, world: int, rank: int) -> dict:
+    """Row slices of one block's latent matrices for `rank` (see plan())."""
+    p = plan(d, l, world, rank)
+    c0, c1 = p["ch"]
+    g0, g1 = p["gl"]
+    out = {k: latent[k][c0:c1] for k in ("f", "c", "g", "o", "down")}
+    out.update({k: latent[k][g0:g1] for k in ("gate", "up")})
+    return out
+
+
+def full_scales(latent: dict, device) -> dict:
+    """mean|W| of each full latent matrix, computed by tern_pack (binary64 sum, C4)."""
+    from .model import PackedWeight
+    return {k: PackedWeight([latent[k].to(device)], expand=False).scales[0:1].clone()
+            for k in ("f", "c", "g", "o", "gate", "up", "down")}
+
+
+class AllGather:
+    """Base: owns the ctypes callback and resolves raw device pointers back to
+    byte views of registered torch tensors (workspaces, activations)."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self._tensors = []
+        self.cb = L.ALLGATHER_FN(self._call)
+        self.error = None
+
+    def register(self, *tensors):
+        have = {(t.data_ptr(), t.numel() * t.element_size()) for t in self._tensors}
+        for t in tensors:
+            if (t.data_ptr(), t.numel() * t.element_size()) not in have:
+                self._tensors.append(t)
+
+    def view(self, p: int, nbytes: int) -> torch.Tensor:
+        for t in self._tensors:
+            base = t.data_ptr()
+            size = t.numel() * t.element_size()
+            if base <= p and p + nbytes <= base + size:
+                flat = t.view(torch.uint8).reshape(-1) if t.dtype != torch.uint8 else t.reshape(-1)
+                return flat[p - base:p - base + nbytes]
+        raise KeyError(f"pointer {p:#x} (+{nbytes}) is in no registered tensor")
+
+    def _call(self, ctx, send, recv, nbytes, stream):
+        try:
+            self.gather(int(ctx or 0), int(send), int(recv), int(nbytes), int(stream or 0))
+            return 0
+        except Exception as e:  # surfaces as TERN_ERR_CUDA in the C call
+            self.error = e
+            return 1
+
+    def gather(self, rank, send, recv, nbytes, stream):
+        raise NotImplementedError
+
+
+class NcclAllGather(AllGather):
+    """torch.distributed all-gather (NCCL) on the library's stream."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        super().__init__(dist.get_world_size(group))
+
+    def gather(self, rank, send, recv, nbytes, stream):
+        s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.dist.all_gather_into_tensor(self.view(recv, nbytes * self.world),
+                                             self.view(send, nbytes), group=self.group)
+
+
+class ThreadAllGather(AllGather):
+    """`world` virtual ranks as host threads on one GPU (one stream each).  At a
+    gather every rank records an event, meets the others at a host barrier,
+    then copies all ranks' chunks on its own stream after their events; a
+    second round of events keeps a rank from overwriting its send buffer before
+    every peer has copied it."""
+
+    def __init__(self, world: int):
+        super().__init__(world)
+        self.barrier = threading.Barrier(world)
+        self.sends = [None] * world
+        self.ev = [None] * world
+        self.ev2 = [None] * world
+        self.streams = {}
+
+    def gather(self, rank, send, recv, nbytes, stream):
+        s = torch.cuda.ExternalStream(stream)
+        e = torch.cuda.Event()
+        e.record(s)
+        self.sends[rank], self.ev[rank] = send, e
+        self.barrier.wait()
+        with torch.cuda.stream(s):
+            for r in range(self.world):
+                s.wait_event(self.ev[r])
+                self.view(recv + r * nbytes, nbytes).copy_(self.view(self.sends[r], nbytes))
+        e2 = torch.cuda.Event()
+        e2.record(s)
+        self.ev2[rank] = e2
+        self.barrier.wait()
+        for r in range(self.world):
+            s.wait_event(self.ev2[r])
+        self.barrier.wait()   # all waits enqueued before the slots are reused
+
+
+def make_shard(gather: AllGather, rank: int) -> "L.tern_shard":
+    return L.tern_shard(rank, gather.world, gather.cb, C.c_void_p(rank))

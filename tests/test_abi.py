@@ -13,8 +13,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_functions():
     src = open(os.path.join(ROOT, "include", "tern.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\**\s+\**([a-z_0-9]+)\s*\(", src, flags=re.M)
-    return sorted(set(names) - {"typedef"})
+    names = re.findall(r"^\s*(?!typedef)(?:const\s+)?[a-z_0-9]+\s*\**\s+\**([a-z_0-9]+)\s*\(", src,
+                       flags=re.M)
+    return sorted(set(names))
 
 
 @pytest.fixture(scope="module")

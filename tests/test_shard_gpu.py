@@ -1,0 +1,72 @@
+"""Output-feature sharding through the C ABI on one GPU (tern.h tern_shard):
+`world` virtual ranks run as host threads, each on its own stream with its own
+shard of every weight, exchanging o', x1, p and y through the library's
+all-gather callback (shard.ThreadAllGather: CUDA events + copies, no kernel
+waits on another).  Every rank's output must be bit-identical to the unsharded
+library path (and that one to the oracle, tests/test_parity_gpu.py): gathers
+move values unchanged, int32 sums are exact and every norm sees the full row.
+"""
+import threading
+
+import pytest
+import torch
+
+from paper_2406_02528_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(world, cfg, T, n_dec, B):
+    from paper_2406_02528_b200 import _lib as L
+    from paper_2406_02528_b200 import model, shard
+    L.load()
+    ref = model.Stack.random(cfg, device="cuda", gen_device="cpu")
+    x = synth.hidden((B, T + n_dec, cfg.d), synth.generator(3), cfg.dtype).cuda()
+    hs = ref.new_state(B)
+    ys = [ref.prefill(x[:, :T].contiguous(), hs)]
+    for t in range(T, T + n_dec):
+        ys.append(ref.decode(x[:, t].contiguous(), hs).unsqueeze(1))
+    torch.cuda.synchronize()
+    yref = torch.cat(ys, 1)
+
+    gather = shard.ThreadAllGather(world)
+    stacks = [model.Stack.random(cfg, device="cuda", gen_device="cpu", shard=(r, gather))
+              for r in range(world)]
+    outs, errs = [None] * world, []
+
+    def worker(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                st = stacks[r]
+                h = st.new_state(B)
+                xr = x.clone()
+                gather.register(xr)
+                o = [st.prefill(xr[:, :T].contiguous(), h)]
+                for t in range(T, T + n_dec):
+                    o.append(st.decode(xr[:, t].contiguous(), h).unsqueeze(1))
+                s.synchronize()
+                outs[r] = torch.cat(o, 1)
+        except Exception as e:   # re-raised in the main thread
+            errs.append(e)
+            gather.barrier.abort()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    for r in range(world):
+        assert torch.equal(outs[r], yref), f"rank {r} differs from the unsharded path"
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_block_prefill_decode_bit_identical(world):
+    cfg = synth.Config("shard", 2, 512, 1024, "f32", 21, 2, 40, 2, 3)
+    _run(world, cfg, T=40, n_dec=3, B=2)
+
+
+def test_sharded_bf16_batch1_decode():
+    cfg = synth.Config("shard_bf16", 1, 256, 512, "bf16", 22, 1, 33, 1, 4)
+    _run(2, cfg, T=33, n_dec=4, B=1)
