@@ -113,7 +113,7 @@ def algo_work(rec: dict, elem: int) -> tuple[str, float]:
     """(unit, amount) of algorithmic work of one launch."""
     k, m, n = rec["k"], rec["m"], rec["n"]
     kp = (k + 127) // 128 * 128
-    if rec["kernel"] == "gemm_tc":
+    if rec["kernel"] in ("gemm_tc", "fcgscan"):
         return "flop", 2.0 * m * n * k                       # dense-equivalent int8 ops
     if rec["kernel"] == "quant":
         return "byte", m * k * elem + m * kp + 12.0 * m      # read x, write q + stats
@@ -153,7 +153,7 @@ def roofline(records, elem, pk, traffic_db):
     epi_names = {0: "store", 1: "resid", 2: "fcg", 3: "mlgru", 4: "swiglu", 5: "acc"}
     sub = {}
     for r in records:
-        if r["kernel"] not in ("gemm_tc", "gemv"):
+        if r["kernel"] not in ("gemm_tc", "gemv", "fcgscan"):
             continue
         key = f'{r["kernel"]}:{epi_names.get(r["epi"], r["epi"])}:n{r["n"]}k{r["k"]}'
         u, w = algo_work(r, elem)

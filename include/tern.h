@@ -281,7 +281,8 @@ tern_status block_decode(const tern_block* b, const void* x, void* y, tern_dtype
  * array; NULL just counts) and returns the number of records; records are
  * kept until the next tern_profile_enable(1).  Not for use in production.
  * ------------------------------------------------------------------------ */
-typedef enum { TERN_K_QUANT = 0, TERN_K_GEMV = 1, TERN_K_GEMM = 2, TERN_K_SCAN = 3 } tern_kernel_id;
+typedef enum { TERN_K_QUANT = 0, TERN_K_GEMV = 1, TERN_K_GEMM = 2, TERN_K_SCAN = 3,
+               TERN_K_FCGSCAN = 4 } tern_kernel_id;
 typedef struct {
   int32_t kernel;   /* tern_kernel_id                                        */
   int32_t epi;      /* epilogue kind (GEMV/GEMM) or gate mode (scan)         */
@@ -323,6 +324,12 @@ tern_status tern_selftest(int32_t which, void* ws, uint64_t* mismatches);
  * 0 forces the tensor-core path everywhere).  Not thread-safe to change
  * while calls are in flight. */
 void tern_set_gemv_max_m(int32_t m);
+/* Tuning knob (host): 1 (default) runs the prefill f|c|g BitLinear and the
+ * MLGRU scan as one fused kernel (k_fcgscan; needs the e8 weight copy and
+ * d % 64 == 0), 0 runs GEMM + tern_mlgru_scan (then the f^c^g^ tap of
+ * tern_block_ws_layout is written).  Results are identical. */
+void tern_set_fused_scan(int32_t on);
+int32_t tern_get_fused_scan(void);
 int32_t tern_get_gemv_max_m(void);
 
 #if defined(__GNUC__)

@@ -71,7 +71,7 @@ class tern_prof_rec(C.Structure):
                 ("k", C.c_int32), ("n_seg", C.c_int32), ("dtype", C.c_int32), ("ms", C.c_float)]
 
 
-KERNEL_NAMES = {0: "quant", 1: "gemv", 2: "gemm_tc", 3: "scan"}
+KERNEL_NAMES = {0: "quant", 1: "gemv", 2: "gemm_tc", 3: "scan", 4: "fcgscan"}
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -108,6 +108,8 @@ _SIGS = {
     "tern_selftest": (C.c_int, [I32, P, C.POINTER(C.c_uint64)]),
     "tern_set_gemv_max_m": (None, [I32]),
     "tern_get_gemv_max_m": (I32, []),
+    "tern_set_fused_scan": (None, [I32]),
+    "tern_get_fused_scan": (I32, []),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -251,6 +253,14 @@ def block_decode(b: tern_block, x, y, h, ws, stream=None):
 
 def tern_set_gemv_max_m(m: int):
     load().tern_set_gemv_max_m(int(m))
+
+
+def tern_set_fused_scan(on: bool):
+    load().tern_set_fused_scan(1 if on else 0)
+
+
+def tern_get_fused_scan() -> bool:
+    return bool(load().tern_get_fused_scan())
 
 
 def tern_get_gemv_max_m() -> int:

@@ -17,6 +17,7 @@ namespace {
 
 thread_local std::string g_err;
 int g_gemv_max_m = kGemvMaxM;
+int g_fused_scan = 1;
 
 tern_status fail(tern_status st, const char* fmt, ...) {
   char buf[512];
@@ -267,6 +268,8 @@ int32_t tern_profile_collect(tern_prof_rec* out, int32_t max) {
   return out ? (n < max ? n : max) : n;
 }
 const char* tern_last_error(void) { return g_err.c_str(); }
+void tern_set_fused_scan(int32_t on) { g_fused_scan = on != 0; }
+int32_t tern_get_fused_scan(void) { return g_fused_scan; }
 void tern_set_gemv_max_m(int32_t m) { g_gemv_max_m = m < 0 ? 0 : (m > kGemvMaxM ? kGemvMaxM : m); }
 int32_t tern_get_gemv_max_m(void) { return g_gemv_max_m; }
 
@@ -481,11 +484,21 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   int32_t* qsum = at<int32_t>(ws, L.qsum);
   void* fcg = at<char>(ws, L.fcg);
   const int ldq = kpad(d);
-  Epi e1 = make_epi(EPI_FCG, p.fcg, p.bias_fcg, fcg, p.fcg.n_rows);
-  tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
-                         nullptr, nullptr, s);
-  if (st) return st;
-  {
+  if (g_fused_scan && fcgscan_supported(p.fcg, d)) {
+    // a4 + a6 fused: f^c^g^ stay on chip (k_fcgscan.cu)
+    {
+      Prof pr(TERN_K_QUANT, 0, M, 0, d, 0, dt, s);
+      TRY_CUDA(launch_quant(x, dt, M, d, d, p.gain_x, p.eps, q, ldq, deq, qsum, nullptr, nullptr, s),
+               "quant");
+    }
+    Prof pr(TERN_K_FCGSCAN, p.gate, M, p.fcg.n_rows, d, 3, dt, s);
+    TRY_CUDA(launch_fcgscan(q, ldq, deq, qsum, p.fcg, p.bias_fcg, dt, B, T, d, p.gate, h, op, s),
+             "fcgscan");
+  } else {
+    Epi e1 = make_epi(EPI_FCG, p.fcg, p.bias_fcg, fcg, p.fcg.n_rows);
+    tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
+                           nullptr, nullptr, s);
+    if (st) return st;
     Prof pr(TERN_K_SCAN, p.gate, B * T, d, d, 3, dt, s);
     TRY_CUDA(launch_scan(fcg, dt, B, T, d, p.gate, h, op, s), "scan");
   }

@@ -78,6 +78,11 @@ cudaError_t launch_expand(const tern_weight& w, uint8_t* e8, cudaStream_t s);
 // sharding: full[m][r*cs + j] = gathered[r][m][j]
 cudaError_t launch_unshard(const void* gathered, int dt, int world, int M, int cs, void* full,
                            cudaStream_t s);
+// a4 + a6 fused (prefill): f|c|g GEMM with the MLGRU scan in its epilogue
+bool fcgscan_supported(const tern_weight& w, int d);
+cudaError_t launch_fcgscan(const int8_t* q, int ldq, const float* deq, const int32_t* qsum,
+                           const tern_weight& w, const float* bias, int dt, int B, int T, int d,
+                           int gate, float* h, void* oprime, cudaStream_t s);
 // a6
 cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
                         void* oprime, cudaStream_t s);

@@ -1,0 +1,313 @@
+// k_fcgscan.cu -- a4 + a6 fused for prefill: the f|c|g BitLinear GEMM
+// (tcgen05.mma kind::i8, accumulators in TMEM) with the MLGRU gates, the exact
+// sequential recurrence and the output gate in its epilogue (
+// PAPER.md P:446-456).  The f^c^g^ pre-activations never touch HBM.
+//
+// Work unit = a chain: one sequence b x one 64-channel group (packed rows
+// [192 g, 192 g + 192) = 64 f | 64 c | 64 g).
+// A CTA walks its chain's 128-token M-tiles in time order, carrying h in the
+// registers of the carry threads:
+//   warp 0      TMA producer: A (int8 q rows of the tile) + B (u8 fields of the
+//               group's 192 rows) per 128-wide K-block, 3-stage ring
+//   warp 1      TMEM alloc + single-thread tcgen05.mma (M=128, N=192), two
+//               accumulators so tile i+1's MMAs overlap tile i's epilogue
+//   warps 2-9   epilogue: (A) thread = token row: tcgen05.ld f^,c^,g^ ->
+//               dequant (a5) -> f = sigma(f^), b = (1-f) SiLU(c^) -> smem, TMEM
+//               released; (B) 64 threads = channels: h = f h + b over the
+//               tile's steps in order (bit-identical to the definition); (C)
+//               lane = channel: o' = g^ sigma(h) (or g^ h) -> global, coalesced.
+#include <cstring>
+
+#include "epilogue.cuh"
+
+namespace tern {
+
+constexpr int kFBM = 128;                 // tokens per M-tile
+constexpr int kFBK = 128;                 // K-block (bytes)
+constexpr int kFCW = 64;                  // channels per chain
+constexpr int kFBN = 3 * kFCW;            // packed rows per chain (f|c|g)
+constexpr int kFS = 3;                    // ring stages
+constexpr int kFThreads = 320;            // 10 warps
+constexpr int kFEpiWarps = 8;
+constexpr int kFPad = kFCW + 1;           // smem row stride (floats): conflict-free both ways
+
+struct FcgScanArgs {
+  int B, T, d, M, num_kb, n_rows;
+  const float* deq;
+  const int32_t* qsum;
+  const float* scales;   // [3] f, c, g
+  const float* bias;     // [3][d] or null
+  float* h;              // [B][d]
+  void* oprime;          // [B*T][d]
+  int gate;
+};
+
+struct FcgScanSmem {
+  uint8_t a[kFS][kFBM * kFBK];       // 16 KB per stage (SW128)
+  uint8_t b[kFS][kFBN * kFBK];       // 24 KB per stage (SW128)
+  float F[kFBM][kFPad];              // f, then h
+  float Bv[kFBM][kFPad];             // (1-f) SiLU(c)
+  float G[kFBM][kFPad];              // g^
+  uint64_t full[kFS], empty[kFS], tfull[2], tempty[2];
+  uint32_t tmem_slot;
+};
+
+__device__ __forceinline__ void epi_bar() {   // named barrier over the 8 epilogue warps
+  asm volatile("bar.sync 1, %0;" ::"n"(kFEpiWarps * 32) : "memory");
+}
+
+template <typename TY>
+__global__ void __launch_bounds__(kFThreads, 1)
+    k_fcgscan(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const FcgScanArgs a) {
+  extern __shared__ __align__(1024) uint8_t fs_raw[];
+  FcgScanSmem& sm =
+      *reinterpret_cast<FcgScanSmem*>(fs_raw + ((1024u - (smem_u32(fs_raw) & 1023u)) & 1023u));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int groups = a.d / kFCW;
+  const int chains = a.B * groups;
+  const int nt = (a.T + kFBM - 1) / kFBM;   // M-tiles per chain
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kFS; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.tfull[i], 1);
+      mbar_init(&sm.tempty[i], kFEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&sm.tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = sm.tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int ch = blockIdx.x; ch < chains; ch += gridDim.x) {
+        const int b = ch / groups, grp = ch % groups;
+        for (int i = 0; i < nt; ++i) {
+          const int m0 = b * a.T + i * kFBM;
+          for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+            const int s = g % kFS;
+            if (g >= (uint32_t)kFS) mbar_wait(&sm.empty[s], ((g / kFS) - 1) & 1);
+            mbar_arrive_expect_tx(&sm.full[s], kFBM * kFBK + kFBN * kFBK);
+            tma_load_2d(sm.a[s], &tmA, &sm.full[s], kb * kFBK, m0);
+            tma_load_2d(sm.b[s], &tmB, &sm.full[s], kb * kFBK, grp * kFBN);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      // kind::i8: D s32, A s8, B u8, both K-major, M=128, N=192
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (0u << 10) | ((uint32_t)(kFBN >> 3) << 17) |
+                             ((uint32_t)(kFBM >> 4) << 24);
+      uint32_t g = 0, it = 0;
+      for (int ch = blockIdx.x; ch < chains; ch += gridDim.x) {
+        for (int i = 0; i < nt; ++i, ++it) {
+          const uint32_t acc = it & 1;
+          mbar_wait(&sm.tempty[acc], ((it >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d_addr = tmem_base + acc * 256;
+          for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+            const int s = g % kFS;
+            mbar_wait(&sm.full[s], (g / kFS) & 1);
+            tc_fence_after();
+            const uint32_t a_addr = smem_u32(sm.a[s]), b_addr = smem_u32(sm.b[s]);
+#pragma unroll
+            for (int kk = 0; kk < kFBK / 32; ++kk)
+              mma_i8(d_addr, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                     idesc, (kb | kk) != 0);
+            mma_commit(&sm.empty[s]);
+          }
+          mma_commit(&sm.tfull[acc]);
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: gates, carry, output gate
+    const int ew = warp - 2;
+    const int quad = warp & 3;           // TMEM lanes [32 quad, 32 quad + 32)
+    const int half = ew >> 2;            // channels [32 half, 32 half + 32)
+    const int r = quad * 32 + lane;      // token row of the tile (phase A)
+    const float msf = __ldg(a.scales), msc = __ldg(a.scales + 1), msg = __ldg(a.scales + 2);
+    float hc = 0.0f;                     // carry (threads ew < 2: channel ew*32 + lane)
+    uint32_t it = 0;
+    for (int ch = blockIdx.x; ch < chains; ch += gridDim.x) {
+      const int b = ch / groups, grp = ch % groups;
+      const int c0 = grp * kFCW;         // first channel of the chain
+      if (ew < 2) hc = a.h[(int64_t)b * a.d + c0 + ew * 32 + lane];
+      for (int i = 0; i < nt; ++i, ++it) {
+        const uint32_t acc = it & 1;
+        const int t0 = i * kFBM;
+        const int steps = min(kFBM, a.T - t0);
+        // (A) thread = token row
+        mbar_wait(&sm.tfull[acc], (it >> 1) & 1);
+        tc_fence_after();
+        uint32_t vf[32], vc[32], vg[32];
+        const uint32_t trow = tmem_base + acc * 256 + ((uint32_t)(quad * 32) << 16);
+        tmem_ld32(trow + half * 32, vf);
+        tmem_ld32(trow + kFCW + half * 32, vc);
+        tmem_ld32(trow + 2 * kFCW + half * 32, vg);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.tempty[acc]);   // accumulator free for tile it+2
+        const int row = b * a.T + t0 + r;
+        const bool rv = r < steps;
+        const float deq = rv ? __ldg(a.deq + row) : 0.0f;
+        const int qs = rv ? __ldg(a.qsum + row) : 0;
+        const float sf = __fmul_rn(deq, msf), sc = __fmul_rn(deq, msc), sg = __fmul_rn(deq, msg);
+        const int cb = c0 + half * 32;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          float fh0 = __fmul_rn((float)((int)vf[j] - qs), sf);
+          float fh1 = __fmul_rn((float)((int)vf[j + 1] - qs), sf);
+          float ch0 = __fmul_rn((float)((int)vc[j] - qs), sc);
+          float ch1 = __fmul_rn((float)((int)vc[j + 1] - qs), sc);
+          float gh0 = __fmul_rn((float)((int)vg[j] - qs), sg);
+          float gh1 = __fmul_rn((float)((int)vg[j + 1] - qs), sg);
+          if (a.bias) {
+            fh0 = __fadd_rn(fh0, __ldg(a.bias + cb + j));
+            fh1 = __fadd_rn(fh1, __ldg(a.bias + cb + j + 1));
+            ch0 = __fadd_rn(ch0, __ldg(a.bias + a.d + cb + j));
+            ch1 = __fadd_rn(ch1, __ldg(a.bias + a.d + cb + j + 1));
+            gh0 = __fadd_rn(gh0, __ldg(a.bias + 2 * a.d + cb + j));
+            gh1 = __fadd_rn(gh1, __ldg(a.bias + 2 * a.d + cb + j + 1));
+          }
+          // R1: the unfused path stores these BitLinear outputs in the activation dtype
+          fh0 = storage_round<TY>(fh0); fh1 = storage_round<TY>(fh1);
+          ch0 = storage_round<TY>(ch0); ch1 = storage_round<TY>(ch1);
+          gh0 = storage_round<TY>(gh0); gh1 = storage_round<TY>(gh1);
+          float f0, f1, s0, s1;
+          sigmoid2(fh0, fh1, f0, f1);
+          sigmoid2(ch0, ch1, s0, s1);
+          const int cc = half * 32 + j;
+          sm.F[r][cc] = f0;
+          sm.F[r][cc + 1] = f1;
+          sm.Bv[r][cc] = __fmul_rn(__fsub_rn(1.0f, f0), __fmul_rn(ch0, s0));   // (1-f) SiLU(c)
+          sm.Bv[r][cc + 1] = __fmul_rn(__fsub_rn(1.0f, f1), __fmul_rn(ch1, s1));
+          sm.G[r][cc] = gh0;
+          sm.G[r][cc + 1] = gh1;
+        }
+        epi_bar();
+        // (B) the carry, in the definition's order: h = (f*h) + ((1-f)*c)
+        if (ew < 2) {
+          const int cc = ew * 32 + lane;
+          if (steps == kFBM) {
+#pragma unroll 8
+            for (int t = 0; t < kFBM; ++t) {
+              hc = __fadd_rn(__fmul_rn(sm.F[t][cc], hc), sm.Bv[t][cc]);
+              sm.F[t][cc] = hc;
+            }
+          } else {
+            for (int t = 0; t < steps; ++t) {
+              hc = __fadd_rn(__fmul_rn(sm.F[t][cc], hc), sm.Bv[t][cc]);
+              sm.F[t][cc] = hc;
+            }
+          }
+        }
+        epi_bar();
+        // (C) lane = channel, warp = 16 token rows: o' = g^ sigma(h) -> global
+        TY* obase = static_cast<TY*>(a.oprime) + (int64_t)(b * a.T + t0) * a.d + c0;
+#pragma unroll 4
+        for (int rr = 0; rr < kFBM / kFEpiWarps; ++rr) {
+          const int t = ew * (kFBM / kFEpiWarps) + rr;
+          if (t < steps) {
+            const float h0 = sm.F[t][lane], h1 = sm.F[t][lane + 32];
+            const float g0 = sm.G[t][lane], g1 = sm.G[t][lane + 32];
+            float o0, o1;
+            if (a.gate == TERN_GATE_SIGMOID_H) {
+              float q0, q1;
+              sigmoid2(h0, h1, q0, q1);
+              o0 = __fmul_rn(g0, q0);
+              o1 = __fmul_rn(g1, q1);
+            } else {
+              o0 = __fmul_rn(g0, h0);
+              o1 = __fmul_rn(g1, h1);
+            }
+            st_act<TY>(obase + (int64_t)t * a.d + lane, o0);
+            st_act<TY>(obase + (int64_t)t * a.d + lane + 32, o1);
+          }
+        }
+        epi_bar();   // F/Bv/G are rewritten by the next tile's phase A
+      }
+      if (ew < 2) a.h[(int64_t)b * a.d + c0 + ew * 32 + lane] = hc;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+template <typename TY>
+static cudaError_t fcgscan_go(const CUtensorMap& ta, const CUtensorMap& tb, const FcgScanArgs& a,
+                              cudaStream_t s) {
+  auto kern = k_fcgscan<TY>;
+  const size_t smem = sizeof(FcgScanSmem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int chains = a.B * (a.d / kFCW);
+  kern<<<chains < num_sms ? chains : num_sms, kFThreads, smem, s>>>(ta, tb, a);
+  return cudaGetLastError();
+}
+
+bool fcgscan_supported(const tern_weight& w, int d) {
+  return w.e8 != nullptr && w.n_seg == 3 && w.n_out == d && d % kFCW == 0 &&
+         sizeof(FcgScanSmem) + 1024 <= 227 * 1024;
+}
+
+cudaError_t launch_fcgscan(const int8_t* q, int ldq, const float* deq, const int32_t* qsum,
+                           const tern_weight& w, const float* bias, int dt, int B, int T, int d,
+                           int gate, float* h, void* oprime, cudaStream_t s) {
+  if (B == 0 || T == 0) return cudaSuccess;
+  if (!fcgscan_supported(w, d)) return cudaErrorInvalidValue;
+  const int kp = (w.k + kKAlign - 1) / kKAlign * kKAlign;
+  const int M = B * T;
+  CUtensorMap ta, tb;
+  if (!make_map_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, (uint64_t)kp, (uint64_t)M, (uint64_t)ldq,
+                   kFBK, kFBM, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  if (!make_map_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, w.e8, (uint64_t)kp, (uint64_t)w.n_rows,
+                   (uint64_t)kp, kFBK, kFBN, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  FcgScanArgs a{};
+  a.B = B;
+  a.T = T;
+  a.d = d;
+  a.M = M;
+  a.num_kb = kp / kFBK;
+  a.n_rows = w.n_rows;
+  a.deq = deq;
+  a.qsum = qsum;
+  a.scales = w.scales;
+  a.bias = bias;
+  a.h = h;
+  a.oprime = oprime;
+  a.gate = gate;
+  return dt == TERN_BF16 ? fcgscan_go<__nv_bfloat16>(ta, tb, a, s) : fcgscan_go<float>(ta, tb, a, s);
+}
+
+}  // namespace tern

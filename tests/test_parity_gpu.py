@@ -328,3 +328,27 @@ def test_sampled_full_size_bitlinear_c1(L, M):
     rows = np.concatenate([rows, [0, m - 1]])
     ref = O.bitlinear(f32np(x)[rows], t, mw, bf16=True)
     assert np.array_equal(f32np(y)[rows], ref)
+
+
+# ------------------------------------------------------------------------ fused a4 + a6
+@pytest.mark.parametrize("dtype,B,T,d,gate", [("f32", 2, 128, 256, 0), ("f32", 3, 200, 128, 1),
+                                              ("bf16", 2, 300, 192, 0), ("bf16", 1, 77, 64, 1)])
+def test_fused_fcg_scan_equals_unfused(L, M, dtype, B, T, d, gate):
+    """k_fcgscan (f|c|g GEMM with the scan in its epilogue) reproduces GEMM + scan bit for bit,
+    including ragged sequence lengths (T not a multiple of the 128-token tile) and both gates;
+    the unfused path is itself oracle-checked above."""
+    cfg = synth.Config("fz", 1, d, 128, dtype, 17, B, T, 1, 0)
+    st = M.Stack.random(cfg, gate=gate, gen_device="cpu")
+    x = synth.hidden((B, T, d), synth.generator(4), dtype).cuda()
+    outs = []
+    for fused in (True, False):
+        L.tern_set_fused_scan(fused)
+        try:
+            h = st.new_state(B)
+            y = st.prefill(x, h)
+            torch.cuda.synchronize()
+            outs.append((y.clone(), h[0].clone()))
+        finally:
+            L.tern_set_fused_scan(True)
+    assert torch.equal(outs[0][0], outs[1][0]), "y differs"
+    assert torch.equal(outs[0][1], outs[1][1]), "h differs"
