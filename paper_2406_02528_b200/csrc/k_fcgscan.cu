@@ -11,11 +11,18 @@
 //               group's 192 rows) per 128-wide K-block, 3-stage ring
 //   warp 1      TMEM alloc + single-thread tcgen05.mma (M=128, N=192), two
 //               accumulators so tile i+1's MMAs overlap tile i's epilogue
-//   warps 2-9   epilogue: (A) thread = token row: tcgen05.ld f^,c^,g^ ->
-//               dequant (a5) -> f = sigma(f^), b = (1-f) SiLU(c^) -> smem, TMEM
-//               released; (B) 64 threads = channels: h = f h + b over the
-//               tile's steps in order (bit-identical to the definition); (C)
-//               lane = channel: o' = g^ sigma(h) (or g^ h) -> global, coalesced.
+//   warps 2-9   gate warps, one per (TMEM lane quadrant q, channel half):
+//               (A) thread = token row: tcgen05.ld f^,c^,g^ -> dequant (a5) ->
+//               f = sigma(f^), b = (1-f) SiLU(c^), g^ -> smem, TMEM released;
+//               (C) once the carry passed its 32 rows, lane = channel:
+//               o' = g^ sigma(h) (or g^ h) -> global, coalesced
+//   warps 10-11 carry warps (channel halves): h = f h + b over the tile's
+//               rows in order, quad by quad as the gate warps deliver them
+//               (bit-identical to the definition)
+// mbarriers per (quad, half) pipeline the three phases across quads and
+// tiles, so the serial carry overlaps the transcendental work.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "epilogue.cuh"
@@ -27,7 +34,7 @@ constexpr int kFBK = 128;                 // K-block (bytes)
 constexpr int kFCW = 64;                  // channels per chain
 constexpr int kFBN = 3 * kFCW;            // packed rows per chain (f|c|g)
 constexpr int kFS = 3;                    // ring stages
-constexpr int kFThreads = 320;            // 10 warps
+constexpr int kFThreads = 384;            // 12 warps: producer, MMA, 8 gate, 2 carry
 constexpr int kFEpiWarps = 8;
 constexpr int kFPad = kFCW + 1;           // smem row stride (floats): conflict-free both ways
 
@@ -40,7 +47,13 @@ struct FcgScanArgs {
   float* h;              // [B][d]
   void* oprime;          // [B*T][d]
   int gate;
+  unsigned long long* prof;  // debug (TERN_FS_PROF): [grid][8] cycles per wait site / phase
 };
+
+// debug: add the cycles since t0 to counter `site` of this CTA
+__device__ __forceinline__ void fs_acc(const FcgScanArgs& a, int site, long long t0) {
+  if (a.prof) atomicAdd(a.prof + blockIdx.x * 8 + site, (unsigned long long)(clock64() - t0));
+}
 
 struct FcgScanSmem {
   uint8_t a[kFS][kFBM * kFBK];       // 16 KB per stage (SW128)
@@ -49,6 +62,8 @@ struct FcgScanSmem {
   float Bv[kFBM][kFPad];             // (1-f) SiLU(c)
   float G[kFBM][kFPad];              // g^
   uint64_t full[kFS], empty[kFS], tfull[2], tempty[2];
+  uint64_t ready[4][2];              // gate warp (quad, half) wrote f, b, g^ of its block
+  uint64_t hdone[4][2];              // carry warp (half) finished the quad's rows
   uint32_t tmem_slot;
 };
 
@@ -79,6 +94,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
       mbar_init(&sm.tfull[i], 1);
       mbar_init(&sm.tempty[i], kFEpiWarps);
     }
+    for (int q = 0; q < 4; ++q)
+      for (int h = 0; h < 2; ++h) {
+        mbar_init(&sm.ready[q][h], 1);
+        mbar_init(&sm.hdone[q][h], 1);
+      }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(&sm.tmem_slot);
@@ -97,7 +117,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
           const int m0 = b * a.T + i * kFBM;
           for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
             const int s = g % kFS;
+            const long long w0 = clock64();
             if (g >= (uint32_t)kFS) mbar_wait(&sm.empty[s], ((g / kFS) - 1) & 1);
+            fs_acc(a, 0, w0);
             mbar_arrive_expect_tx(&sm.full[s], kFBM * kFBK + kFBN * kFBK);
             tma_load_2d(sm.a[s], &tmA, &sm.full[s], kb * kFBK, m0);
             tma_load_2d(sm.b[s], &tmB, &sm.full[s], kb * kFBK, grp * kFBN);
@@ -115,12 +137,16 @@ __global__ void __launch_bounds__(kFThreads, 1)
       for (int ch = blockIdx.x; ch < chains; ch += gridDim.x) {
         for (int i = 0; i < nt; ++i, ++it) {
           const uint32_t acc = it & 1;
+          const long long w1 = clock64();
           mbar_wait(&sm.tempty[acc], ((it >> 1) & 1) ^ 1);
+          fs_acc(a, 1, w1);
           tc_fence_after();
           const uint32_t d_addr = tmem_base + acc * 256;
           for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
             const int s = g % kFS;
+            const long long w2 = clock64();
             mbar_wait(&sm.full[s], (g / kFS) & 1);
+            fs_acc(a, 2, w2);
             tc_fence_after();
             const uint32_t a_addr = smem_u32(sm.a[s]), b_addr = smem_u32(sm.b[s]);
 #pragma unroll
@@ -133,25 +159,26 @@ __global__ void __launch_bounds__(kFThreads, 1)
         }
       }
     }
-  } else {
-    // ---------------- epilogue: gates, carry, output gate
+  } else if (warp < 2 + kFEpiWarps) {
+    // ---------------- gate warps (quad q, channel half h): a 32-token x 32-channel block
     const int ew = warp - 2;
     const int quad = warp & 3;           // TMEM lanes [32 quad, 32 quad + 32)
     const int half = ew >> 2;            // channels [32 half, 32 half + 32)
     const int r = quad * 32 + lane;      // token row of the tile (phase A)
     const float msf = __ldg(a.scales), msc = __ldg(a.scales + 1), msg = __ldg(a.scales + 2);
-    float hc = 0.0f;                     // carry (threads ew < 2: channel ew*32 + lane)
     uint32_t it = 0;
     for (int ch = blockIdx.x; ch < chains; ch += gridDim.x) {
       const int b = ch / groups, grp = ch % groups;
       const int c0 = grp * kFCW;         // first channel of the chain
-      if (ew < 2) hc = a.h[(int64_t)b * a.d + c0 + ew * 32 + lane];
       for (int i = 0; i < nt; ++i, ++it) {
         const uint32_t acc = it & 1;
         const int t0 = i * kFBM;
         const int steps = min(kFBM, a.T - t0);
-        // (A) thread = token row
+        // (A) thread = token row: dequant, gates -> smem
+        const long long w3 = clock64();
         mbar_wait(&sm.tfull[acc], (it >> 1) & 1);
+        if (ew == 0 && lane == 0) fs_acc(a, 3, w3);
+        const long long w4 = clock64();
         tc_fence_after();
         uint32_t vf[32], vc[32], vg[32];
         const uint32_t trow = tmem_base + acc * 256 + ((uint32_t)(quad * 32) << 16);
@@ -199,49 +226,79 @@ __global__ void __launch_bounds__(kFThreads, 1)
           sm.G[r][cc] = gh0;
           sm.G[r][cc + 1] = gh1;
         }
-        epi_bar();
-        // (B) the carry, in the definition's order: h = (f*h) + ((1-f)*c)
-        if (ew < 2) {
-          const int cc = ew * 32 + lane;
-          if (steps == kFBM) {
-#pragma unroll 8
-            for (int t = 0; t < kFBM; ++t) {
-              hc = __fadd_rn(__fmul_rn(sm.F[t][cc], hc), sm.Bv[t][cc]);
-              sm.F[t][cc] = hc;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.ready[quad][half]);   // carry may run these rows
+        if (ew == 0 && lane == 0) fs_acc(a, 4, w4);
+        // (C) lane = channel: o' = g^ sigma(h) for this block's rows, after the carry
+        const long long w5 = clock64();
+        mbar_wait(&sm.hdone[quad][half], it & 1);
+        if (ew == 0 && lane == 0) fs_acc(a, 5, w5);
+        const long long w6 = clock64();
+        TY* obase = static_cast<TY*>(a.oprime) + (int64_t)(b * a.T + t0) * a.d + c0 + half * 32 + lane;
+        const int cc = half * 32 + lane;
+#pragma unroll 4
+        for (int rr = 0; rr < 32; rr += 2) {
+          const int t = quad * 32 + rr;
+          const float h0 = sm.F[t][cc], h1 = sm.F[t + 1][cc];
+          const float g0 = sm.G[t][cc], g1 = sm.G[t + 1][cc];
+          float o0, o1;
+          if (a.gate == TERN_GATE_SIGMOID_H) {
+            float q0, q1;
+            sigmoid2(h0, h1, q0, q1);
+            o0 = __fmul_rn(g0, q0);
+            o1 = __fmul_rn(g1, q1);
+          } else {
+            o0 = __fmul_rn(g0, h0);
+            o1 = __fmul_rn(g1, h1);
+          }
+          if (t < steps) st_act<TY>(obase + (int64_t)t * a.d, o0);
+          if (t + 1 < steps) st_act<TY>(obase + (int64_t)(t + 1) * a.d, o1);
+        }
+        if (ew == 0 && lane == 0) fs_acc(a, 6, w6);
+        // this block's smem rows are rewritten only by this warp's next phase A,
+        // after the carry has finished with them (hdone above)
+      }
+    }
+  } else {
+    // ---------------- carry warps (channel half h): h = (f*h) + ((1-f)*c), in order
+    const int half = warp - 2 - kFEpiWarps;
+    const int cc = half * 32 + lane;
+    uint32_t it = 0;
+    for (int ch = blockIdx.x; ch < chains; ch += gridDim.x) {
+      const int b = ch / groups, grp = ch % groups;
+      const int c0 = grp * kFCW;
+      float hc = a.h[(int64_t)b * a.d + c0 + cc];
+      for (int i = 0; i < nt; ++i, ++it) {
+        const int steps = min(kFBM, a.T - i * kFBM);
+        for (int q = 0; q < 4; ++q) {
+          mbar_wait(&sm.ready[q][half], it & 1);
+          const int tb = q * 32, te = min(tb + 32, steps);
+          if (te - tb == 32) {
+#pragma unroll
+            for (int t8 = 0; t8 < 32; t8 += 8) {
+              float fv[8], bv[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                fv[j] = sm.F[tb + t8 + j][cc];
+                bv[j] = sm.Bv[tb + t8 + j][cc];
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                hc = __fadd_rn(__fmul_rn(fv[j], hc), bv[j]);
+                sm.F[tb + t8 + j][cc] = hc;
+              }
             }
           } else {
-            for (int t = 0; t < steps; ++t) {
+            for (int t = tb; t < te; ++t) {
               hc = __fadd_rn(__fmul_rn(sm.F[t][cc], hc), sm.Bv[t][cc]);
               sm.F[t][cc] = hc;
             }
           }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.hdone[q][half]);
         }
-        epi_bar();
-        // (C) lane = channel, warp = 16 token rows: o' = g^ sigma(h) -> global
-        TY* obase = static_cast<TY*>(a.oprime) + (int64_t)(b * a.T + t0) * a.d + c0;
-#pragma unroll 4
-        for (int rr = 0; rr < kFBM / kFEpiWarps; ++rr) {
-          const int t = ew * (kFBM / kFEpiWarps) + rr;
-          if (t < steps) {
-            const float h0 = sm.F[t][lane], h1 = sm.F[t][lane + 32];
-            const float g0 = sm.G[t][lane], g1 = sm.G[t][lane + 32];
-            float o0, o1;
-            if (a.gate == TERN_GATE_SIGMOID_H) {
-              float q0, q1;
-              sigmoid2(h0, h1, q0, q1);
-              o0 = __fmul_rn(g0, q0);
-              o1 = __fmul_rn(g1, q1);
-            } else {
-              o0 = __fmul_rn(g0, h0);
-              o1 = __fmul_rn(g1, h1);
-            }
-            st_act<TY>(obase + (int64_t)t * a.d + lane, o0);
-            st_act<TY>(obase + (int64_t)t * a.d + lane + 32, o1);
-          }
-        }
-        epi_bar();   // F/Bv/G are rewritten by the next tile's phase A
       }
-      if (ew < 2) a.h[(int64_t)b * a.d + c0 + ew * 32 + lane] = hc;
+      a.h[(int64_t)b * a.d + c0 + cc] = hc;
     }
   }
   tc_fence_before();
@@ -270,7 +327,30 @@ static cudaError_t fcgscan_go(const CUtensorMap& ta, const CUtensorMap& tb, cons
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int chains = a.B * (a.d / kFCW);
-  kern<<<chains < num_sms ? chains : num_sms, kFThreads, smem, s>>>(ta, tb, a);
+  const int grid = chains < num_sms ? chains : num_sms;
+  static unsigned long long* dprof = nullptr;
+  static const bool prof_on = getenv("TERN_FS_PROF") != nullptr;
+  FcgScanArgs aa = a;
+  if (prof_on) {   // debug only: printed after a synchronous run
+    if (!dprof) cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * 1024);
+    cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * 8 * 1024, s);
+    aa.prof = dprof;
+  }
+  const long long t0 = 0;
+  (void)t0;
+  kern<<<grid, kFThreads, smem, s>>>(ta, tb, aa);
+  if (prof_on) {
+    static unsigned long long h[8 * 1024];
+    cudaMemcpyAsync(h, dprof, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double sum[8] = {0};
+    for (int b = 0; b < grid; ++b)
+      for (int i = 0; i < 8; ++i) sum[i] += (double)h[b * 8 + i] / grid;
+    fprintf(stderr,
+            "[fcgscan prof] B=%d T=%d d=%d chains=%d | per CTA cycles: prod.empty=%.0f "
+            "mma.tempty=%.0f mma.full=%.0f epi.tfull=%.0f phaseA=%.0f waitcarry=%.0f phaseC=%.0f\n",
+            a.B, a.T, a.d, chains, sum[0], sum[1], sum[2], sum[3], sum[4], sum[5], sum[6]);
+  }
   return cudaGetLastError();
 }
 
