@@ -173,6 +173,7 @@ def roofline(records, elem, pk, traffic_db):
     if dom:
         d = kernels[dom]
         tr = traffic_db.get(dom)
+        tr = tr.get("bytes_per_launch") if isinstance(tr, dict) else tr
         rl = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
               "unit": d["unit"], "frac": d["frac"], "traffic": tr,
               "peak_source": (("profiles/int8_peak.json int8_tops_sustained (cuBLASLt s8 GEMM "
