@@ -18,6 +18,7 @@ namespace {
 thread_local std::string g_err;
 int g_gemv_max_m = kGemvMaxM;
 int g_fused_scan = 1;
+constexpr int kSplitKMaxM = 256;
 
 tern_status fail(tern_status st, const char* fmt, ...) {
   char buf[512];
@@ -140,7 +141,7 @@ Epi make_epi(int kind, const tern_weight& w, const float* bias, void* out, int l
 }
 
 struct BlockWs {
-  size_t q, deq, qsum, fcg, oprime, x1, p, sout, gbuf, total;
+  size_t q, deq, qsum, fcg, oprime, x1, p, sout, gbuf, part, part_bytes, total;
 };
 // world > 1 adds the rank's local outputs [M][max(ds,ls)] and the gather
 // target [world][M][max(ds,ls)] (M > 1 gathers are then unshuffled to [M][width])
@@ -162,6 +163,21 @@ BlockWs block_ws(int32_t M, int32_t d, int32_t l, int32_t fcg_rows, tern_dtype d
     w.sout = off; off += al256((size_t)M * cs * dsize(dt));
     w.gbuf = off; off += al256((size_t)world * M * cs * dsize(dt));
   }
+  // split-K partial sums for small M (decode batches above the GEMV limit)
+  w.part = off;
+  w.part_bytes = 0;
+  if (M <= kSplitKMaxM) {
+    size_t rows = (size_t)fcg_rows;
+    const size_t gu_rows = 2 * (((size_t)(l > 0 ? l : 1) + 63) / 64 * 64);
+    if (gu_rows > rows) rows = gu_rows;
+    if ((size_t)d > rows) rows = (size_t)d;
+    // split-K slices: ksplit * tiles <~ 2 * SMs, so slices * M * rows <= 2*148*128*256
+    size_t pb = (size_t)M * rows * 4 * 8;
+    const size_t cap = (size_t)2 * 148 * 128 * 256 * 4;
+    if (pb < cap) pb = cap;
+    w.part_bytes = al256(pb);
+    off += w.part_bytes;
+  }
   w.total = off;
   return w;
 }
@@ -174,14 +190,14 @@ template <typename T> T* at(void* ws, size_t off) {
 tern_status bl_tc(const void* x, tern_dtype xdt, int M, int K, int ldx, const float* gain,
                   float eps, const tern_weight& w, tern_dtype ydt, const Epi& epi, int8_t* q,
                   int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
-                  cudaStream_t s) {
+                  cudaStream_t s, int32_t* part = nullptr, size_t part_bytes = 0) {
   {
     Prof p(TERN_K_QUANT, 0, M, 0, K, 0, xdt, s);
     TRY_CUDA(launch_quant(x, xdt, M, K, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s),
              "quant");
   }
   Prof p(TERN_K_GEMM, epi.kind, M, w.n_rows, w.k, w.n_seg, ydt, s);
-  TRY_CUDA(launch_gemm(q, M, ldq, deq, qsum, w, ydt, epi, s), "gemm");
+  TRY_CUDA(launch_gemm(q, M, ldq, deq, qsum, w, ydt, epi, s, part, part_bytes), "gemm");
   return TERN_OK;
 }
 
@@ -484,7 +500,18 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   int32_t* qsum = at<int32_t>(ws, L.qsum);
   void* fcg = at<char>(ws, L.fcg);
   const int ldq = kpad(d);
-  if (g_fused_scan && fcgscan_supported(p.fcg, d)) {
+  // the fused kernel walks each sequence's 128-token tiles; short sequences (decode
+  // steps with B > gemv_max_m) take GEMM + scan instead
+  if (T == 1 && L.part_bytes > 0) {
+    // decode step above the GEMV limit: the MLGRU step runs in the GEMM's
+    // split-K epilogue (no f^c^g^ round trip, no scan launch)
+    Epi e1 = make_epi(EPI_MLGRU, p.fcg, p.bias_fcg, op, d);
+    e1.h = h;
+    e1.gate = p.gate;
+    tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
+                           nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes);
+    if (st) return st;
+  } else if (g_fused_scan && T >= 64 && fcgscan_supported(p.fcg, d)) {
     // a4 + a6 fused: f^c^g^ stay on chip (k_fcgscan.cu)
     {
       Prof pr(TERN_K_QUANT, 0, M, 0, d, 0, dt, s);
@@ -497,7 +524,7 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   } else {
     Epi e1 = make_epi(EPI_FCG, p.fcg, p.bias_fcg, fcg, p.fcg.n_rows);
     tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
-                           nullptr, nullptr, s);
+                           nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes);
     if (st) return st;
     Prof pr(TERN_K_SCAN, p.gate, B * T, d, d, 3, dt, s);
     TRY_CUDA(launch_scan(fcg, dt, B, T, d, p.gate, h, op, s), "scan");
@@ -506,7 +533,7 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   e2.res = x;
   e2.ldr = d;
   return bl_tc(op, dt, M, d, d, p.gain_o, p.eps, p.o, dt, e2, q, ldq, deq, qsum, nullptr, nullptr,
-               s);
+               s, at<int32_t>(ws, L.part), L.part_bytes);
 }
 
 // channel mixer: x [M][d] -> out (d, or y = x + d when resid)
@@ -531,10 +558,10 @@ tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, ter
   float* deq = at<float>(ws, L.deq);
   int32_t* qsum = at<int32_t>(ws, L.qsum);
   tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.gu, dt, e1, q, kpad(d), deq, qsum,
-                         nullptr, nullptr, s);
+                         nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes);
   if (st) return st;
   return bl_tc(pp, dt, M, l, l, p.gain_p, p.eps, p.down, dt, e2, q, kpad(l), deq, qsum, nullptr,
-               nullptr, s);
+               nullptr, s, at<int32_t>(ws, L.part), L.part_bytes);
 }
 
 // one BitLinear on either path (decode GEMV with its fused prologue, or quant + GEMM)
@@ -547,7 +574,8 @@ tern_status bitlinear_any(bool gemv, const void* x, tern_dtype dt, int M, int K,
     return TERN_OK;
   }
   return bl_tc(x, dt, M, K, K, gain, eps, w, dt, e, at<int8_t>(ws, L.q), kpad(K),
-               at<float>(ws, L.deq), at<int32_t>(ws, L.qsum), nullptr, nullptr, s);
+               at<float>(ws, L.deq), at<int32_t>(ws, L.qsum), nullptr, nullptr, s,
+               at<int32_t>(ws, L.part), L.part_bytes);
 }
 
 // gather the ranks' [M][cs] slices into full [M][world*cs] rows

@@ -90,16 +90,22 @@ __device__ __forceinline__ void fma2(float& a0, float& a1, float b0, float b1, f
 }
 
 // Two sigmoids for vectorised loops (scan, SwiGLU epilogue): exp_c's exact
-// operation sequence with the FMAs paired on FFMA2, no branches and no range
-// selects.  Equal bit for bit to sigmoid_c (IEEE 1/(1+exp_c(-x))) whenever
+// operation sequence with the FMAs paired on FFMA2, no branches, no range
+// selects and no conversion-pipe instructions (domain |x| < 2^21; the
+// activations here are dequantized BitLinear outputs, |x| < 127*K*deq*m).  Equal bit for bit to sigmoid_c (IEEE 1/(1+exp_c(-x))) whenever
 // that result is a normal number (>= 2^-126, i.e. x > -87.3); below it returns
 // 0 instead of a subnormal (< 1.2e-38): far inside every tolerance and
 // quantizing identically downstream.  Checked over 2^24 points by
 // tern_selftest 2.
 __device__ __forceinline__ void sigmoid2(float x0, float x1, float& s0, float& s1) {
   const float y0 = -x0, y1 = -x1;
-  const float k0 = rintf(__fmul_rn(y0, 0x1.715476p+0f));
-  const float k1 = rintf(__fmul_rn(y1, 0x1.715476p+0f));
+  // rint(y log2e) with the 1.5*2^23 magic constant (exact round-to-nearest-even
+  // for |z| < 2^22, the same value rintf gives) -- no FRND / F2I (conversion
+  // pipe: 16/clk/SM); the integer k is read from the magic sum's bits
+  const float z0 = __fmul_rn(y0, 0x1.715476p+0f), z1 = __fmul_rn(y1, 0x1.715476p+0f);
+  const float m0 = __fadd_rn(z0, 12582912.0f), m1 = __fadd_rn(z1, 12582912.0f);
+  const float k0 = __fsub_rn(m0, 12582912.0f), k1 = __fsub_rn(m1, 12582912.0f);
+  const int ik0 = __float_as_int(m0) - 0x4B400000, ik1 = __float_as_int(m1) - 0x4B400000;
   float r0 = -k0, r1 = -k1;
   fma2(r0, r1, 0x1.62e400p-1f, 0x1.62e400p-1f, y0, y1);       // y - k ln2_hi
   float t0 = -k0, t1 = -k1;
@@ -116,7 +122,7 @@ __device__ __forceinline__ void sigmoid2(float x0, float x1, float& s0, float& s
   // p * 2^k with k clamped to the normal exponents: k >= 128 (exp overflows)
   // then gives d ~ 2^127 whose reciprocal flushes to 0 = 1/inf; k <= -127
   // gives d == 1 exactly, as the true tiny exp would.
-  const int i0 = max(min((int)k0, 127), -126), i1 = max(min((int)k1, 127), -126);
+  const int i0 = max(min(ik0, 127), -126), i1 = max(min(ik1, 127), -126);
   const float e0 = __fmul_rn(p0, __int_as_float((i0 + 127) << 23));
   const float e1 = __fmul_rn(p1, __int_as_float((i1 + 127) << 23));
   s0 = rcp_fast(__fadd_rn(1.0f, e0));
@@ -159,6 +165,13 @@ template <> __device__ __forceinline__ float storage_round<__nv_bfloat16>(float 
 // packed row index of (segment s, logical row r) in a fused group
 __device__ __forceinline__ int packed_row(int s, int r, int n_seg) {
   return (r / kSegRows) * (n_seg * kSegRows) + s * kSegRows + (r % kSegRows);
+}
+
+// Exact int -> float for |v| < 2^22 without the conversion pipe (I2F runs at
+// 16/clk/SM): add the integer to the bits of 1.5*2^23, subtract 1.5*2^23.
+// acc - qsum of a BitLinear is bounded by 127*K < 2^21.
+__device__ __forceinline__ float i2f_small(int v) {
+  return __fsub_rn(__int_as_float(0x4B400000 + v), 12582912.0f);
 }
 
 // ----------------------------------------------------------------- sum of squares (C4)
@@ -269,19 +282,28 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
-// Waits for the phase with the given parity.  A watchdog turns a lost arrival
-// (a pipeline bug) into a trap after ~2^27 polls instead of a silent hang.
+// Waits for the phase with the given parity.  try_wait carries a suspend-time
+// hint, so a waiting warp sleeps until the phase completes (or the hint
+// elapses) instead of spinning on the issue slots its CTA's busy warps need.
+// A watchdog turns a lost arrival (a pipeline bug) into a trap after ~20 s of
+// %globaltimer instead of a silent hang.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0, polls = 0;
+  unsigned long long t0 = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, P1;\n\t}"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
         : "memory");
-    if (++polls == (1u << 27)) __trap();
+    if (!done && (++polls & 1023u) == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 20000000000ull) __trap();
+    }
   } while (!done);
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -361,6 +383,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
         "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// 32 lanes x 16 columns of 32-bit from TMEM; thread i gets lane (base+i), cols [col, col+16)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() {

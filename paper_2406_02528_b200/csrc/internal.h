@@ -67,8 +67,10 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
                         float eps, const tern_weight& w, const Epi& epi, const QuantTaps* taps,
                         cudaStream_t s);
 // a4 (tcgen05 int8 GEMM): q [M][ldq] -> epilogue
+// part: optional int32 scratch [M][n_rows] enabling split-K for small M (nullptr: never)
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
-                        const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s);
+                        const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
+                        int32_t* part = nullptr, size_t part_bytes = 0);
 // debug timeline of GEMV launches (globaltimer per CTA), see tern_trace_enable
 void gemv_trace_enable(int on);
 int gemv_trace_collect(unsigned long long* out, int max_launches);

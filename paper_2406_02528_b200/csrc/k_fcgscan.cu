@@ -34,8 +34,9 @@ constexpr int kFBK = 128;                 // K-block (bytes)
 constexpr int kFCW = 64;                  // channels per chain
 constexpr int kFBN = 3 * kFCW;            // packed rows per chain (f|c|g)
 constexpr int kFS = 3;                    // ring stages
-constexpr int kFThreads = 384;            // 12 warps: producer, MMA, 8 gate, 2 carry
-constexpr int kFEpiWarps = 8;
+constexpr int kFEpiWarps = 16;           // gate warps: 4 per TMEM lane quadrant
+constexpr int kFThreads = (4 + kFEpiWarps) * 32;   // producer, MMA, gate warps, 2 carry
+constexpr int kFQCh = kFCW / 4;          // channels per gate warp (16)
 constexpr int kFPad = kFCW + 1;           // smem row stride (floats): conflict-free both ways
 
 struct FcgScanArgs {
@@ -62,7 +63,7 @@ struct FcgScanSmem {
   float Bv[kFBM][kFPad];             // (1-f) SiLU(c)
   float G[kFBM][kFPad];              // g^
   uint64_t full[kFS], empty[kFS], tfull[2], tempty[2];
-  uint64_t ready[4][2];              // gate warp (quad, half) wrote f, b, g^ of its block
+  uint64_t ready[4][2];              // both gate warps of (quad, half) wrote their f, b, g^
   uint64_t hdone[4][2];              // carry warp (half) finished the quad's rows
   uint32_t tmem_slot;
 };
@@ -96,12 +97,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
     }
     for (int q = 0; q < 4; ++q)
       for (int h = 0; h < 2; ++h) {
-        mbar_init(&sm.ready[q][h], 1);
+        mbar_init(&sm.ready[q][h], 2);   // the two 16-channel gate warps of the half
         mbar_init(&sm.hdone[q][h], 1);
       }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(&sm.tmem_slot);
+  static_assert(kFThreads <= 1024, "block size");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -160,10 +162,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
       }
     }
   } else if (warp < 2 + kFEpiWarps) {
-    // ---------------- gate warps (quad q, channel half h): a 32-token x 32-channel block
+    // ---------------- gate warps (quad q, 16-channel slice cs): a 32-token x 16-channel block
     const int ew = warp - 2;
     const int quad = warp & 3;           // TMEM lanes [32 quad, 32 quad + 32)
-    const int half = ew >> 2;            // channels [32 half, 32 half + 32)
+    const int cs = ew >> 2;              // channels [16 cs, 16 cs + 16)
+    const int half = cs >> 1;            // carry warp that consumes them
     const int r = quad * 32 + lane;      // token row of the tile (phase A)
     const float msf = __ldg(a.scales), msc = __ldg(a.scales + 1), msg = __ldg(a.scales + 2);
     uint32_t it = 0;
@@ -180,11 +183,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
         if (ew == 0 && lane == 0) fs_acc(a, 3, w3);
         const long long w4 = clock64();
         tc_fence_after();
-        uint32_t vf[32], vc[32], vg[32];
+        uint32_t vf[kFQCh], vc[kFQCh], vg[kFQCh];
         const uint32_t trow = tmem_base + acc * 256 + ((uint32_t)(quad * 32) << 16);
-        tmem_ld32(trow + half * 32, vf);
-        tmem_ld32(trow + kFCW + half * 32, vc);
-        tmem_ld32(trow + 2 * kFCW + half * 32, vg);
+        tmem_ld16(trow + cs * kFQCh, vf);
+        tmem_ld16(trow + kFCW + cs * kFQCh, vc);
+        tmem_ld16(trow + 2 * kFCW + cs * kFQCh, vg);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -194,15 +197,15 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const float deq = rv ? __ldg(a.deq + row) : 0.0f;
         const int qs = rv ? __ldg(a.qsum + row) : 0;
         const float sf = __fmul_rn(deq, msf), sc = __fmul_rn(deq, msc), sg = __fmul_rn(deq, msg);
-        const int cb = c0 + half * 32;
+        const int cb = c0 + cs * kFQCh;
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          float fh0 = __fmul_rn((float)((int)vf[j] - qs), sf);
-          float fh1 = __fmul_rn((float)((int)vf[j + 1] - qs), sf);
-          float ch0 = __fmul_rn((float)((int)vc[j] - qs), sc);
-          float ch1 = __fmul_rn((float)((int)vc[j + 1] - qs), sc);
-          float gh0 = __fmul_rn((float)((int)vg[j] - qs), sg);
-          float gh1 = __fmul_rn((float)((int)vg[j + 1] - qs), sg);
+        for (int j = 0; j < kFQCh; j += 2) {
+          float fh0 = __fmul_rn(i2f_small((int)vf[j] - qs), sf);
+          float fh1 = __fmul_rn(i2f_small((int)vf[j + 1] - qs), sf);
+          float ch0 = __fmul_rn(i2f_small((int)vc[j] - qs), sc);
+          float ch1 = __fmul_rn(i2f_small((int)vc[j + 1] - qs), sc);
+          float gh0 = __fmul_rn(i2f_small((int)vg[j] - qs), sg);
+          float gh1 = __fmul_rn(i2f_small((int)vg[j + 1] - qs), sg);
           if (a.bias) {
             fh0 = __fadd_rn(fh0, __ldg(a.bias + cb + j));
             fh1 = __fadd_rn(fh1, __ldg(a.bias + cb + j + 1));
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           float f0, f1, s0, s1;
           sigmoid2(fh0, fh1, f0, f1);
           sigmoid2(ch0, ch1, s0, s1);
-          const int cc = half * 32 + j;
+          const int cc = cs * kFQCh + j;
           sm.F[r][cc] = f0;
           sm.F[r][cc + 1] = f1;
           sm.Bv[r][cc] = __fmul_rn(__fsub_rn(1.0f, f0), __fmul_rn(ch0, s0));   // (1-f) SiLU(c)
@@ -229,18 +232,19 @@ __global__ void __launch_bounds__(kFThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.ready[quad][half]);   // carry may run these rows
         if (ew == 0 && lane == 0) fs_acc(a, 4, w4);
-        // (C) lane = channel: o' = g^ sigma(h) for this block's rows, after the carry
+        // (C) 16 lanes per row, two rows per instruction: o' = g^ sigma(h) for this
+        // block's rows, after the carry
         const long long w5 = clock64();
         mbar_wait(&sm.hdone[quad][half], it & 1);
         if (ew == 0 && lane == 0) fs_acc(a, 5, w5);
         const long long w6 = clock64();
-        TY* obase = static_cast<TY*>(a.oprime) + (int64_t)(b * a.T + t0) * a.d + c0 + half * 32 + lane;
-        const int cc = half * 32 + lane;
-#pragma unroll 4
-        for (int rr = 0; rr < 32; rr += 2) {
-          const int t = quad * 32 + rr;
-          const float h0 = sm.F[t][cc], h1 = sm.F[t + 1][cc];
-          const float g0 = sm.G[t][cc], g1 = sm.G[t + 1][cc];
+        const int cc = cs * kFQCh + (lane & 15), rsub = lane >> 4;
+        TY* obase = static_cast<TY*>(a.oprime) + (int64_t)(b * a.T + t0) * a.d + c0 + cc;
+#pragma unroll 2
+        for (int rr = 0; rr < 32; rr += 4) {
+          const int t = quad * 32 + rr + rsub;   // rows t and t + 2
+          const float h0 = sm.F[t][cc], h1 = sm.F[t + 2][cc];
+          const float g0 = sm.G[t][cc], g1 = sm.G[t + 2][cc];
           float o0, o1;
           if (a.gate == TERN_GATE_SIGMOID_H) {
             float q0, q1;
@@ -252,7 +256,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             o1 = __fmul_rn(g1, h1);
           }
           if (t < steps) st_act<TY>(obase + (int64_t)t * a.d, o0);
-          if (t + 1 < steps) st_act<TY>(obase + (int64_t)(t + 1) * a.d, o1);
+          if (t + 2 < steps) st_act<TY>(obase + (int64_t)(t + 2) * a.d, o1);
         }
         if (ew == 0 && lane == 0) fs_acc(a, 6, w6);
         // this block's smem rows are rewritten only by this warp's next phase A,

@@ -30,6 +30,7 @@ constexpr int kGemmThreads = 448;
 constexpr int kEpiWarp0 = 6;
 constexpr int kEpiWarps = 8;
 constexpr int kEpiBuf = 4096;  // bytes of one 32x32 staging tile (fp32)
+constexpr int kSmallM = 256;   // M at or below: packed B tiles (+ split-K when tiles are few)
 
 template <int BN, bool kPre> struct GemmCfg {
   static constexpr int A_BYTES = kBM * kBK;        // 16 KB
@@ -46,6 +47,8 @@ template <int BN, bool kPre> struct GemmCfg {
 
 struct GemmArgs {
   int M, n_rows, num_kb, n_tiles, m_tiles;
+  int ksplit, kb_per;        // split-K (small M): work unit = (tile, K slice)
+  int32_t* part;             // ksplit > 1: int32 partial sums [M][n_rows], pre-zeroed
   const uint32_t* codes;     // K-block-major packed weights [num_kb][n_rows][8]
   const float* deq;
   const int32_t* qsum;
@@ -138,6 +141,10 @@ template <> __device__ __forceinline__ void stg_read_row<__nv_bfloat16>(const ui
   }
 }
 
+__device__ __forceinline__ uint32_t trow_base(uint32_t tmem_base, uint32_t acc, int BN, int quad) {
+  return tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
+}
+
 // int32 accumulator tap (parity tests only): plain coalesced stores through a
 // padded staging tile (the two staging buffers of the warp, 8 KB)
 __device__ void acc_tap_chunk(const Epi& e, const GemmArgs& a, int* si, int lane, int row0,
@@ -180,7 +187,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const long long t_start = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = a.num_kb;
-  const int total = a.n_tiles * a.m_tiles;
+  const int total = a.n_tiles * a.m_tiles * a.ksplit;
   const Epi& e = a.epi;
 
   if (warp == 0 && lane == 0) {
@@ -213,8 +220,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       uint32_t g = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int m0 = (t / a.n_tiles) * kBM, n0 = (t % a.n_tiles) * BN;
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int tile = t / a.ksplit, sp = t % a.ksplit;
+        const int m0 = (tile / a.n_tiles) * kBM, n0 = (tile % a.n_tiles) * BN;
+        const int kb1 = min(nk, (sp + 1) * a.kb_per);
+        for (int kb = sp * a.kb_per; kb < kb1; ++kb, ++g) {
           const int s = g % S;
           if (g >= (uint32_t)S) pwait(&empty[s], ((g / S) - 1) & 1, a.prof, 0);
           if (kPre) {
@@ -244,7 +253,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         pwait(&tempty[acc], ((it >> 1) & 1) ^ 1, a.prof, 1);
         tc_fence_after();
         const uint32_t d_addr = tmem_base + acc * BN;
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int sp = t % a.ksplit;
+        const int kb0 = sp * a.kb_per, kb1 = min(nk, kb0 + a.kb_per);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % S;
           uint32_t b_addr;
           if (kPre) {
@@ -260,7 +271,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kBK / 32; ++kk)
             mma_i8(d_addr, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
-                   idesc, (kb | kk) != 0);
+                   idesc, ((kb - kb0) | kk) != 0);
           mma_commit(&empty[s]);
           if (!kPre) mma_commit(&ufree[g % U]);
         }
@@ -274,7 +285,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const bool pt = tid == 0;
       uint32_t g = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int sp = t % a.ksplit;
+        const int kb1 = min(nk, (sp + 1) * a.kb_per);
+        for (int kb = sp * a.kb_per; kb < kb1; ++kb, ++g) {
           const int s = g % S, u = g % (U > 0 ? U : 1);
           if (g >= (uint32_t)U) pwait(&ufree[u], ((g / U) - 1) & 1, pt ? a.prof : nullptr, 3);
           pwait(&full[s], (g / S) & 1, pt ? a.prof : nullptr, 4);
@@ -316,10 +329,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t rphase[2] = {0, 0};
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const uint32_t acc = it & 1;
-      const int m0 = (t / a.n_tiles) * kBM, n0 = (t % a.n_tiles) * BN;
+      const int tile = t / a.ksplit;
+      const int m0 = (tile / a.n_tiles) * kBM, n0 = (tile % a.n_tiles) * BN;
       pwait(&tfull[acc], (it >> 1) & 1, (ew == 0 && lead) ? a.prof : nullptr, 5);
       tc_fence_after();
       const int row0 = m0 + quad * 32;
+      if (a.part) {
+        // split-K / finalize mode: this K slice's raw sums go to part[sp][M][n_rows]
+        // (coalesced through the staging tile); k_splitk_epi sums the slices in a
+        // fixed order (exact int32) and applies the epilogue
+        int32_t* slice = a.part + (int64_t)(t % a.ksplit) * a.M * a.n_rows;
+        int* si = reinterpret_cast<int*>(bufs);
+        for (int c = half; c < BN / 32; c += 2) {
+          const int col0 = n0 + c * 32;
+          if (col0 >= a.n_rows) continue;
+          uint32_t v[32];
+          tmem_ld32(trow_base(tmem_base, acc, BN, quad) + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) si[lane * 33 + j] = (int)v[j];
+          __syncwarp();
+          for (int r = 0; r < 32; ++r)
+            if (row0 + r < a.M && col0 + lane < a.n_rows)
+              slice[(int64_t)(row0 + r) * a.n_rows + col0 + lane] = si[r * 33 + lane];
+          __syncwarp();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lead) mbar_arrive(&tempty[acc]);
+        continue;
+      }
       const int row = row0 + lane;
       const bool rv = row < a.M;
       const float deq = rv ? __ldg(a.deq + row) : 0.0f;
@@ -374,10 +413,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const float scu = __fmul_rn(deq, msc1);
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            const float g0 = storage_round<TY>(__fmul_rn((float)((int)v[j] - qsum), sc));
-            const float g1 = storage_round<TY>(__fmul_rn((float)((int)v[j + 1] - qsum), sc));
-            const float u0 = storage_round<TY>(__fmul_rn((float)((int)vu[j] - qsum), scu));
-            const float u1 = storage_round<TY>(__fmul_rn((float)((int)vu[j + 1] - qsum), scu));
+            const float g0 = storage_round<TY>(__fmul_rn(i2f_small((int)v[j] - qsum), sc));
+            const float g1 = storage_round<TY>(__fmul_rn(i2f_small((int)v[j + 1] - qsum), sc));
+            const float u0 = storage_round<TY>(__fmul_rn(i2f_small((int)vu[j] - qsum), scu));
+            const float u1 = storage_round<TY>(__fmul_rn(i2f_small((int)vu[j + 1] - qsum), scu));
             float s0, s1;
             sigmoid2(g0, g1, s0, s1);
             o[j] = __fmul_rn(__fmul_rn(g0, s0), u0);   // SwiGLU p = SiLU(g) u
@@ -386,7 +425,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            float x = __fmul_rn((float)((int)v[j] - qsum), sc);
+            float x = __fmul_rn(i2f_small((int)v[j] - qsum), sc);
             if (e.bias) x = __fadd_rn(x, __ldg(e.bias + seg * e.n_out + rr0 + j));
             o[j] = storage_round<TY>(x);
           }
@@ -475,7 +514,7 @@ static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, con
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int total = a.n_tiles * a.m_tiles;
+  const int total = a.n_tiles * a.m_tiles * a.ksplit;
   const int grid = total < num_sms ? total : num_sms;
   static unsigned long long* dprof = nullptr;
   static const bool prof_on = getenv("TERN_GEMM_PROF") != nullptr;
@@ -510,12 +549,101 @@ static cudaError_t gemm_dispatch_bn(int BN, const CUtensorMap& ta, const CUtenso
                    : gemm_launch<128, kPre, TY>(ta, tb, to, tr, a, s);
 }
 
+// ----------------------------------------------------------------- split-K epilogue
+// The epilogue of a split-K (or small-M) GEMM: sums the K slices' int32 partials
+// in slice order (exact), then the same arithmetic as the tensor-core epilogue
+// (a5 dequant, R1-R3 storage rounding, SwiGLU / MLGRU step with the paired
+// sigmoid).  One thread per (row, pair of output columns or channels).
+template <typename TY>
+__global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M, int n_rows,
+                             const float* __restrict__ deq, const int32_t* __restrict__ qsum,
+                             const Epi e) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool chan = e.kind == EPI_SWIGLU || e.kind == EPI_MLGRU;   // per logical channel
+  const int ncol = chan ? e.n_out : (e.kind == EPI_FCG ? n_rows : e.n_out);
+  const int npair = (ncol + 1) / 2;
+  if (idx >= (int64_t)M * npair) return;
+  const int m = (int)(idx / npair), c = (int)(idx % npair) * 2;
+  const float dq = __ldg(deq + m);
+  const int qs = __ldg(qsum + m);
+  const int64_t sl = (int64_t)M * n_rows;
+  auto acc_at = [&](int pcol) {
+    int v = 0;
+    for (int k = 0; k < ksplit; ++k) v += part[k * sl + (int64_t)m * n_rows + pcol];
+    return v - qs;
+  };
+  auto val = [&](int pcol, int seg, int r) {
+    float o = __fmul_rn(i2f_small(acc_at(pcol)), __fmul_rn(dq, __ldg(e.scales + seg)));
+    if (e.bias) o = __fadd_rn(o, __ldg(e.bias + seg * e.n_out + r));
+    return storage_round<TY>(o);
+  };
+  TY* out = static_cast<TY*>(e.out);
+  if (chan) {
+    const int r0 = c, r1 = min(c + 1, e.n_out - 1);
+    if (e.kind == EPI_SWIGLU) {   // p = SiLU(g) u
+      const float g0 = val(packed_row(0, r0, 2), 0, r0), g1 = val(packed_row(0, r1, 2), 0, r1);
+      const float u0 = val(packed_row(1, r0, 2), 1, r0), u1 = val(packed_row(1, r1, 2), 1, r1);
+      float s0, s1;
+      sigmoid2(g0, g1, s0, s1);
+      st_act<TY>(out + (int64_t)m * e.ldo + r0, __fmul_rn(__fmul_rn(g0, s0), u0));
+      if (c + 1 < e.n_out) st_act<TY>(out + (int64_t)m * e.ldo + r1, __fmul_rn(__fmul_rn(g1, s1), u1));
+    } else {                      // MLGRU step: f, c -> h, o'
+      const float f0 = val(packed_row(0, r0, 3), 0, r0), f1 = val(packed_row(0, r1, 3), 0, r1);
+      const float c0 = val(packed_row(1, r0, 3), 1, r0), c1 = val(packed_row(1, r1, 3), 1, r1);
+      const float g0 = val(packed_row(2, r0, 3), 2, r0), g1 = val(packed_row(2, r1, 3), 2, r1);
+      float sf0, sf1, sc0, sc1;
+      sigmoid2(f0, c0, sf0, sc0);
+      sigmoid2(f1, c1, sf1, sc1);
+      float* hp = e.h + (int64_t)m * e.n_out;
+      const float h0 = __fadd_rn(__fmul_rn(sf0, hp[r0]),
+                                 __fmul_rn(__fsub_rn(1.0f, sf0), __fmul_rn(c0, sc0)));
+      const float h1 = __fadd_rn(__fmul_rn(sf1, hp[r1]),
+                                 __fmul_rn(__fsub_rn(1.0f, sf1), __fmul_rn(c1, sc1)));
+      float o0, o1;
+      if (e.gate == TERN_GATE_SIGMOID_H) {
+        float q0, q1;
+        sigmoid2(h0, h1, q0, q1);
+        o0 = __fmul_rn(g0, q0);
+        o1 = __fmul_rn(g1, q1);
+      } else {
+        o0 = __fmul_rn(g0, h0);
+        o1 = __fmul_rn(g1, h1);
+      }
+      hp[r0] = h0;
+      st_act<TY>(out + (int64_t)m * e.ldo + r0, o0);
+      if (c + 1 < e.n_out) {
+        hp[r1] = h1;
+        st_act<TY>(out + (int64_t)m * e.ldo + r1, o1);
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int col = c + j;
+    if (col >= ncol) break;
+    int seg = 0, r = col;
+    if (e.kind == EPI_FCG) {   // col is the packed row
+      seg = (col / kSegRows) % e.n_seg;
+      r = (col / (kSegRows * e.n_seg)) * kSegRows + (col % kSegRows);
+      if (r >= e.n_out) continue;
+    }
+    float o = val(col, seg, r);
+    if (e.kind == EPI_RESID)
+      o = __fadd_rn(ld_act<TY>(static_cast<const TY*>(e.res) + (int64_t)m * e.ldr + r), o);
+    st_act<TY>(out + (int64_t)m * e.ldo + (e.kind == EPI_FCG ? col : r), o);
+  }
+}
+
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
-                        const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s) {
+                        const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
+                        int32_t* part, size_t part_bytes) {
   if (M <= 0) return cudaSuccess;
   const int kp = (w.k + kKAlign - 1) / kKAlign * kKAlign;
   const int BN = (w.n_rows >= 1024 || w.n_rows % 256 == 0) ? 256 : 128;
-  const bool pre = w.e8 != nullptr;
+  // the u8 copy halves shared-memory traffic when the tensor cores are the limit
+  // (large M); for decode batches the weight bytes are, and the 2-bit codes are 4x fewer
+  const bool pre = w.e8 != nullptr && M > kSmallM;
   const bool yb = ydt == TERN_BF16;
   const size_t ys = yb ? 2 : 4;
   const CUtensorMapDataType ydtype = yb ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -550,6 +678,46 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   a.deq = deq;
   a.qsum = qsum;
   a.epi = epi;
+  a.ksplit = 1;
+  a.kb_per = a.num_kb;
+  // split-K / finalize mode when the tiles cannot fill the SMs (decode batches,
+  // small M) or the epilogue is the MLGRU step (decode T = 1 above the GEMV
+  // limit): K slices write int32 partials, k_splitk_epi sums them exactly and
+  // runs the epilogue
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tiles = a.n_tiles * a.m_tiles;
+  const size_t slice = (size_t)M * w.n_rows * sizeof(int32_t);
+  const bool finalize = epi.kind == EPI_MLGRU ||
+                        (part && part_bytes >= slice && epi.kind != EPI_NONE &&
+                         epi.acc == nullptr && tiles * 2 <= num_sms && a.num_kb >= 2);
+  if (finalize) {
+    if (!part || part_bytes < slice) return cudaErrorInvalidValue;
+    int ks = (num_sms + tiles - 1) / tiles;
+    if (ks > a.num_kb) ks = a.num_kb;
+    if ((size_t)ks * slice > part_bytes) ks = (int)(part_bytes / slice);
+    a.kb_per = (a.num_kb + ks - 1) / ks;
+    a.ksplit = (a.num_kb + a.kb_per - 1) / a.kb_per;
+    a.part = part;
+    cudaError_t err = pre ? (yb ? gemm_dispatch_bn<true, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)
+                                : gemm_dispatch_bn<true, float>(BN, ta, tb, to, tr, a, s))
+                          : (yb ? gemm_dispatch_bn<false, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)
+                                : gemm_dispatch_bn<false, float>(BN, ta, tb, to, tr, a, s));
+    if (err != cudaSuccess) return err;
+    const bool chan = epi.kind == EPI_SWIGLU || epi.kind == EPI_MLGRU;
+    const int ncol = chan ? epi.n_out : (epi.kind == EPI_FCG ? w.n_rows : epi.n_out);
+    const int64_t n = (int64_t)M * ((ncol + 1) / 2);
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    if (yb)
+      k_splitk_epi<__nv_bfloat16><<<grid, 256, 0, s>>>(part, a.ksplit, M, w.n_rows, deq, qsum, epi);
+    else
+      k_splitk_epi<float><<<grid, 256, 0, s>>>(part, a.ksplit, M, w.n_rows, deq, qsum, epi);
+    return cudaGetLastError();
+  }
   if (pre)
     return yb ? gemm_dispatch_bn<true, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)
               : gemm_dispatch_bn<true, float>(BN, ta, tb, to, tr, a, s);

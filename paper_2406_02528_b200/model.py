@@ -7,6 +7,7 @@ channel mixer; P:698 prefill = pipelined mode, decode = fall-through mode.)
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -65,12 +66,19 @@ class Block:
             rank, gather = shard
             sc = S.full_scales(lat, dev)
             lat = S.shard_latents(lat, d, l, gather.world, rank)
+        # which groups keep only the 2-bit codes (the prefill GEMM then unpacks B
+        # tiles in shared memory instead of loading the u8 copy): debug knob
+        packed_only = set(os.environ.get("TERN_PACKED_B", "").split(","))
         self.fcg = PackedWeight([lat["f"], lat["c"], lat["g"]],
-                                None if sc["f"] is None else [sc["f"], sc["c"], sc["g"]])
-        self.o = PackedWeight([lat["o"]], None if sc["o"] is None else [sc["o"]])
+                                None if sc["f"] is None else [sc["f"], sc["c"], sc["g"]],
+                                expand="fcg" not in packed_only)
+        self.o = PackedWeight([lat["o"]], None if sc["o"] is None else [sc["o"]],
+                              expand="o" not in packed_only)
         self.gu = PackedWeight([lat["gate"], lat["up"]],
-                               None if sc["gate"] is None else [sc["gate"], sc["up"]])
-        self.down = PackedWeight([lat["down"]], None if sc["down"] is None else [sc["down"]])
+                               None if sc["gate"] is None else [sc["gate"], sc["up"]],
+                               expand="gu" not in packed_only)
+        self.down = PackedWeight([lat["down"]], None if sc["down"] is None else [sc["down"]],
+                                 expand="down" not in packed_only)
         gains = gains or {}
         biases = biases or {}
         self._keep = []

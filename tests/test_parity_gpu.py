@@ -352,3 +352,33 @@ def test_fused_fcg_scan_equals_unfused(L, M, dtype, B, T, d, gate):
             L.tern_set_fused_scan(True)
     assert torch.equal(outs[0][0], outs[1][0]), "y differs"
     assert torch.equal(outs[0][1], outs[1][1]), "h differs"
+
+
+# ------------------------------------------------------------------------ batched decode (split-K)
+@pytest.mark.parametrize("cfg_name,B,T,n_dec", [("c2", 32, 3, 2), ("c4", 16, 2, 2)])
+def test_batched_decode_split_k_parity(L, M, cfg_name, B, T, n_dec):
+    """Decode batches above the GEMV limit run quant + a split-K tcgen05 GEMM (int32 slices
+    summed exactly) + the split-K epilogue; short prefills take the same path.  Free-running
+    against the oracle, bit-exact."""
+    cfg = synth.CONFIGS[cfg_name]
+    st, ob = _blocks(cfg, M, 1, 0, gen_device="cuda")
+    x = synth.hidden((B, T + n_dec, cfg.d), synth.generator(cfg.seed + 77), cfg.dtype)
+    xd = x.cuda()
+    states = st.new_state(B)
+    ys = [st.prefill(xd[:, :T].contiguous(), states)]
+    for t in range(T, T + n_dec):
+        ys.append(st.decode(xd[:, t].contiguous(), states).unsqueeze(1))
+    torch.cuda.synchronize()
+    yg = f32np(torch.cat(ys, 1))
+    bf = cfg.dtype == "bf16"
+    H = [np.zeros((B, cfg.d), np.float32)]
+    xo = f32np(x)
+    y0, H = O.stack(ob, xo[:, :T], H, bf16=bf)
+    outs = [y0]
+    for t in range(T, T + n_dec):
+        yt, H = O.stack(ob, xo[:, t:t + 1], H, bf16=bf)
+        outs.append(yt)
+    yo = np.concatenate(outs, 1)
+    close(yg, yo, 2e-2 if bf else 1e-4, cfg_name)
+    assert np.array_equal(yg, yo)
+    assert np.array_equal(states[0].cpu().numpy(), H[0])
