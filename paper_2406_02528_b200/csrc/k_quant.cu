@@ -199,6 +199,23 @@ static void quant_go(const TX* x, int m, int k, int ldx, const float* gain, floa
                                                            deq, qsum, inv_rms, absmax);
 }
 
+template <typename TX, int TPR>
+static void quant_nv(int nv, const TX* x, int m, int k, int ldx, const float* gain, float eps,
+                     int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
+                     cudaStream_t s) {
+  // exactly as many register vectors as the row needs: predicated-off slots of
+  // the fully unrolled loops still cost issue slots, and this kernel is issue-bound
+  switch (nv) {
+    case 1: case 2: quant_go<TX, TPR, 2>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
+    case 3: quant_go<TX, TPR, 3>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
+    case 4: quant_go<TX, TPR, 4>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
+    case 5: quant_go<TX, TPR, 5>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
+    case 6: quant_go<TX, TPR, 6>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
+    case 7: quant_go<TX, TPR, 7>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
+    default: quant_go<TX, TPR, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
+  }
+}
+
 template <typename TX>
 static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const float* gain, float eps,
                                   int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
@@ -207,13 +224,13 @@ static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const floa
   const int nvp = kp / QVec<TX>::N;   // vectors per (padded) row
   // smallest threads-per-row with <= 8 vectors per thread
   if (nvp <= 32 * 8)
-    quant_go<TX, 32, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+    quant_nv<TX, 32>((nvp + 31) / 32, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
   else if (nvp <= 64 * 8)
-    quant_go<TX, 64, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+    quant_nv<TX, 64>((nvp + 63) / 64, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
   else if (nvp <= 128 * 8)
-    quant_go<TX, 128, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+    quant_nv<TX, 128>((nvp + 127) / 128, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
   else if (nvp <= 256 * 8)
-    quant_go<TX, 256, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+    quant_nv<TX, 256>((nvp + 255) / 256, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();
