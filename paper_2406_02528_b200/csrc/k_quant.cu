@@ -45,7 +45,7 @@ __device__ __forceinline__ uint4 ldg_stream_v4(const uint4* p) {
 }
 
 // TPR threads per row, NV vectors per thread; CTA = kQThreads/TPR rows.
-template <typename TX, int TPR, int NV, bool GAIN>
+template <typename TX, int TPR, int NV, bool GAIN, bool FULL>
 __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, int M, int K, int ldx,
                                                      const float* __restrict__ gain, float eps,
                                                      double inv_k, int8_t* __restrict__ q, int ldq,
@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int v = t + i * TPR;
-    xv[i] = (rv && v < nvec) ? ldg_stream_v4(xr + v) : make_uint4(0, 0, 0, 0);
+    // FULL: the row is exactly TPR*NV vectors (no bounds checks at all)
+    xv[i] = (FULL ? rv : (rv && v < nvec)) ? ldg_stream_v4(xr + v) : make_uint4(0, 0, 0, 0);
   }
   double s0 = 0.0, s1 = 0.0;
   float xm = 0.0f;
@@ -149,19 +150,20 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
         const float4 gg = __ldg(reinterpret_cast<const float4*>(gain + (v < nvec ? v : 0) * VE) + j4);
         g[0] = gg.x; g[1] = gg.y; g[2] = gg.z; g[3] = gg.w;
       }
-      uint32_t w = 0;
+      int qi[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float y = __fmul_rn(xf[4 * j4 + j], r);
         if (GAIN) y = __fmul_rn(y, g[j]);
         // |y*sc| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
-        const int qi = __float2int_rz(round_half_away(__fmul_rn(y, sc)));
-        qs += qi;
-        w |= ((uint32_t)qi & 0xffu) << (8 * j);
+        qi[j] = __float2int_rz(round_half_away(__fmul_rn(y, sc)));
+        qs += qi[j];
       }
-      pk[j4] = w;
+      // low bytes of the four ints -> one word (two byte permutes)
+      pk[j4] = __byte_perm(__byte_perm(qi[0], qi[1], 0x0040), __byte_perm(qi[2], qi[3], 0x0040),
+                           0x5410);
     }
-    if (rv && v < nvecp) {
+    if (FULL ? rv : (rv && v < nvecp)) {
       if (VE == 4)
         reinterpret_cast<uint32_t*>(qr)[v] = pk[0];
       else
@@ -191,12 +193,16 @@ static void quant_go(const TX* x, int m, int k, int ldx, const float* gain, floa
   constexpr int RPC = kQThreads / TPR;
   const int grid = (m + RPC - 1) / RPC;
   const double inv_k = 1.0 / (double)k;
+  const bool full = k == TPR * NV * QVec<TX>::N;   // then also k == Kp
   if (gain)
-    k_quant<TX, TPR, NV, true><<<grid, kQThreads, 0, s>>>(x, m, k, ldx, gain, eps, inv_k, q, ldq,
-                                                          deq, qsum, inv_rms, absmax);
+    k_quant<TX, TPR, NV, true, false><<<grid, kQThreads, 0, s>>>(x, m, k, ldx, gain, eps, inv_k, q,
+                                                                 ldq, deq, qsum, inv_rms, absmax);
+  else if (full)
+    k_quant<TX, TPR, NV, false, true><<<grid, kQThreads, 0, s>>>(x, m, k, ldx, gain, eps, inv_k, q,
+                                                                 ldq, deq, qsum, inv_rms, absmax);
   else
-    k_quant<TX, TPR, NV, false><<<grid, kQThreads, 0, s>>>(x, m, k, ldx, gain, eps, inv_k, q, ldq,
-                                                           deq, qsum, inv_rms, absmax);
+    k_quant<TX, TPR, NV, false, false><<<grid, kQThreads, 0, s>>>(x, m, k, ldx, gain, eps, inv_k,
+                                                                  q, ldq, deq, qsum, inv_rms, absmax);
 }
 
 template <typename TX, int TPR>
