@@ -640,7 +640,9 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
                         int32_t* part, size_t part_bytes) {
   if (M <= 0) return cudaSuccess;
   const int kp = (w.k + kKAlign - 1) / kKAlign * kKAlign;
-  const int BN = (w.n_rows >= 1024 || w.n_rows % 256 == 0) ? 256 : 128;
+  static const int bn_force = getenv("TERN_GEMM_BN") ? atoi(getenv("TERN_GEMM_BN")) : 0;   // debug
+  int BN = (w.n_rows >= 1024 || w.n_rows % 256 == 0) ? 256 : 128;
+  if (bn_force == 128 || bn_force == 256) BN = bn_force;
   // the u8 copy halves shared-memory traffic when the tensor cores are the limit
   // (large M); for decode batches the weight bytes are, and the 2-bit codes are 4x fewer
   const bool pre = w.e8 != nullptr && M > kSmallM;
