@@ -235,6 +235,12 @@ typedef struct {
   tern_glu ch;
   int32_t d, l;       /* full widths (also when sharded) */
   tern_shard shard;   /* zero-initialise for an unsharded block */
+  /* optional (may be NULL): the tern_block decoded right after this one.  The
+   * decode GEMVs then prefetch its f|c|g and o weights into L2 while this
+   * block's channel mixer runs (each GEMV also prefetches the weights two
+   * launches ahead inside the block), so HBM-resident stacks stream weights
+   * ahead of the dependency chain.  A hint only: results do not change. */
+  const void* next_block;
 } tern_block;
 
 /* Workspace bytes for mlgru_fwd / glu_fwd / block_* on B sequences x T tokens. */

@@ -58,7 +58,7 @@ class tern_shard(C.Structure):
 
 class tern_block(C.Structure):
     _fields_ = [("mix", tern_mlgru), ("ch", tern_glu), ("d", C.c_int32), ("l", C.c_int32),
-                ("shard", tern_shard)]
+                ("shard", tern_shard), ("next_block", C.c_void_p)]
 
 
 class tern_block_taps(C.Structure):

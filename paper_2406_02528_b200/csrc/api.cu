@@ -128,6 +128,8 @@ struct Prof {
   }
 };
 
+size_t codes_bytes(const tern_weight& w) { return (size_t)w.n_rows * w.ldw * 4; }
+
 Epi make_epi(int kind, const tern_weight& w, const float* bias, void* out, int ldo) {
   Epi e{};
   e.kind = kind;
@@ -476,8 +478,15 @@ tern_status tern_block_ws_layout(const tern_block* b, int32_t B, int32_t T, tern
 namespace {
 
 // token mixer: x [M][d] -> out (o, or x1 = x + o when resid), state h
+// L2 prefetch hints for the two GEMVs of a mixer (decode): weights of later launches
+struct PfPlan {
+  const void* p[2] = {nullptr, nullptr};
+  size_t n[2] = {0, 0};
+};
+
 tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid, tern_dtype dt,
-                      int B, int T, int d, float* h, void* ws, const BlockWs& L, cudaStream_t s) {
+                      int B, int T, int d, float* h, void* ws, const BlockWs& L, cudaStream_t s,
+                      const PfPlan& pf = PfPlan()) {
   const int M = B * T;
   void* op = at<char>(ws, L.oprime);
   if (T == 1 && B <= g_gemv_max_m && gemv_supported(B, d, dt)) {
@@ -486,13 +495,16 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
     e1.gate = p.gate;
     {
       Prof pr(TERN_K_GEMV, e1.kind, B, p.fcg.n_rows, d, 3, dt, s);
-      TRY_CUDA(launch_gemv(x, dt, dt, B, d, d, p.gain_x, p.eps, p.fcg, e1, nullptr, s), "gemv fcg");
+      TRY_CUDA(launch_gemv(x, dt, dt, B, d, d, p.gain_x, p.eps, p.fcg, e1, nullptr, s, pf.p[0],
+                           pf.n[0]),
+               "gemv fcg");
     }
     Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.o, p.bias_o, out, d);
     e2.res = x;
     e2.ldr = d;
     Prof pr(TERN_K_GEMV, e2.kind, B, p.o.n_rows, d, 1, dt, s);
-    TRY_CUDA(launch_gemv(op, dt, dt, B, d, d, p.gain_o, p.eps, p.o, e2, nullptr, s), "gemv o");
+    TRY_CUDA(launch_gemv(op, dt, dt, B, d, d, p.gain_o, p.eps, p.o, e2, nullptr, s, pf.p[1], pf.n[1]),
+             "gemv o");
     return TERN_OK;
   }
   int8_t* q = at<int8_t>(ws, L.q);
@@ -538,7 +550,8 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
 
 // channel mixer: x [M][d] -> out (d, or y = x + d when resid)
 tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, tern_dtype dt, int M,
-                    int d, int l, void* ws, const BlockWs& L, cudaStream_t s) {
+                    int d, int l, void* ws, const BlockWs& L, cudaStream_t s,
+                    const PfPlan& pf = PfPlan()) {
   void* pp = at<char>(ws, L.p);
   Epi e1 = make_epi(EPI_SWIGLU, p.gu, nullptr, pp, l);
   Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.down, nullptr, out, d);
@@ -547,10 +560,13 @@ tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, ter
   if (M <= g_gemv_max_m && gemv_supported(M, d, dt) && gemv_supported(M, l, dt)) {
     {
       Prof pr(TERN_K_GEMV, e1.kind, M, p.gu.n_rows, d, 2, dt, s);
-      TRY_CUDA(launch_gemv(x, dt, dt, M, d, d, p.gain_x, p.eps, p.gu, e1, nullptr, s), "gemv gu");
+      TRY_CUDA(launch_gemv(x, dt, dt, M, d, d, p.gain_x, p.eps, p.gu, e1, nullptr, s, pf.p[0],
+                           pf.n[0]),
+               "gemv gu");
     }
     Prof pr(TERN_K_GEMV, e2.kind, M, p.down.n_rows, l, 1, dt, s);
-    TRY_CUDA(launch_gemv(pp, dt, dt, M, l, l, p.gain_p, p.eps, p.down, e2, nullptr, s),
+    TRY_CUDA(launch_gemv(pp, dt, dt, M, l, l, p.gain_p, p.eps, p.down, e2, nullptr, s, pf.p[1],
+                         pf.n[1]),
              "gemv down");
     return TERN_OK;
   }
@@ -695,8 +711,24 @@ static tern_status block_run(const tern_block* b, const void* x, void* y, tern_d
   cudaStream_t s = (cudaStream_t)stream;
   if (block_world(b) > 1) return run_block_sharded(*b, x, y, dt, B, T, h, ws, L, s);
   void* x1 = at<char>(ws, L.x1);
-  if ((st = run_mlgru(b->mix, x, x1, true, dt, B, T, b->d, h, ws, L, s)) != TERN_OK) return st;
-  return run_glu(b->ch, x1, y, true, dt, B * T, b->d, b->l, ws, L, s);
+  // weight-stream prefetch (decode GEMVs): the token mixer pulls this block's
+  // channel-mixer weights into L2, the channel mixer the next block's token mixer
+  PfPlan pm, pg;
+  if (T == 1) {
+    pm.p[0] = b->ch.gu.codes;
+    pm.n[0] = codes_bytes(b->ch.gu);
+    pm.p[1] = b->ch.down.codes;
+    pm.n[1] = codes_bytes(b->ch.down);
+    if (b->next_block) {
+      const tern_block* nb = static_cast<const tern_block*>(b->next_block);
+      pg.p[0] = nb->mix.fcg.codes;
+      pg.n[0] = codes_bytes(nb->mix.fcg);
+      pg.p[1] = nb->mix.o.codes;
+      pg.n[1] = codes_bytes(nb->mix.o);
+    }
+  }
+  if ((st = run_mlgru(b->mix, x, x1, true, dt, B, T, b->d, h, ws, L, s, pm)) != TERN_OK) return st;
+  return run_glu(b->ch, x1, y, true, dt, B * T, b->d, b->l, ws, L, s, pg);
 }
 
 tern_status block_prefill(const tern_block* b, const void* x, void* y, tern_dtype dt, int32_t B,

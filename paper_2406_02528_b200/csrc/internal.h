@@ -63,9 +63,10 @@ cudaError_t launch_quant(const void* x, int xdt, int m, int k, int ldx, const fl
 // a3 (decode GEMV, norm+quant prologue fused): x [M][ldx] -> epilogue
 constexpr int kGemvMaxM = 4;
 bool gemv_supported(int M, int K, int xdt);   // M <= kGemvMaxM and K within the register tile
+// pf / pf_bytes: optional L2 prefetch of a later launch's packed weights
 cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, const float* gain,
                         float eps, const tern_weight& w, const Epi& epi, const QuantTaps* taps,
-                        cudaStream_t s);
+                        cudaStream_t s, const void* pf = nullptr, size_t pf_bytes = 0);
 // a4 (tcgen05 int8 GEMM): q [M][ldq] -> epilogue
 // part: optional int32 scratch [M][n_rows] enabling split-K for small M (nullptr: never)
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,

@@ -44,6 +44,8 @@ struct GemvArgs {
   double inv_k;  // 1/K (binary64)
   Epi epi;
   QuantTaps taps;
+  const uint8_t* pf;         // L2 prefetch hint: a later launch's packed weights
+  size_t pf_bytes;
   unsigned long long* prof;  // debug (TERN_GEMV_PROF): [grid][8] clock64 per phase
   unsigned long long* trace; // tern_trace_enable: [grid][8] globaltimer (start, released, end, smid, phases)
 };
@@ -164,6 +166,17 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
       const int pr = a.n_seg == 1 ? a0r : packed_row(sg, a0r, a.n_seg);
       bulk_load(sw_words(g_smem) + (sg * nkb + kb) * SW + (a0r - r0) * 8,
                 a.codes + ((int64_t)kb * a.n_rows + pr) * 8, (uint32_t)(a1r - a0r) * 32u, &wbar);
+    }
+  }
+  // L2 prefetch of this CTA's share of a later launch's weights (HBM-resident
+  // stacks: the weight stream runs ahead of the dependency chain)
+  if (a.pf && tid == 32) {
+    const size_t chunk = ((a.pf_bytes + gridDim.x - 1) / gridDim.x + 15) & ~size_t(15);
+    const size_t off = chunk * blockIdx.x;
+    if (off < a.pf_bytes) {
+      const size_t n = a.pf_bytes - off < chunk ? a.pf_bytes - off : chunk;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf + off), "r"((uint32_t)n)
+                   : "memory");
     }
   }
   // dequantization scales are constants: load them before the wait too
@@ -580,7 +593,7 @@ static int num_sms() {
 
 cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, const float* gain,
                         float eps, const tern_weight& w, const Epi& epi, const QuantTaps* taps,
-                        cudaStream_t s) {
+                        cudaStream_t s, const void* pf, size_t pf_bytes) {
   if (M <= 0) return cudaSuccess;
   if (!gemv_supported(M, K, xdt)) return cudaErrorInvalidValue;
   GemvArgs a{};
@@ -607,6 +620,9 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
   a.sw_stride = gemv_sw_stride(ch);
   a.epi = epi;
   if (taps) a.taps = *taps;
+  a.pf = static_cast<const uint8_t*>(pf);
+  a.pf_bytes = pf ? (pf_bytes & ~size_t(15)) : 0;
+  if (a.pf_bytes == 0) a.pf = nullptr;
   const int units = (w.n_out + ch - 1) / ch;
   const bool xb = xdt == TERN_BF16, yb = ydt == TERN_BF16;
   if (xb && yb) return gemv_dispatch_m<__nv_bfloat16, __nv_bfloat16>(a, units, s);

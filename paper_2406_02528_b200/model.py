@@ -130,6 +130,11 @@ class Stack:
         self._graph = None
         self.gather = None   # shard.AllGather of a sharded stack
 
+    def link_blocks(self):
+        """Point each block's next_block hint at its successor (decode L2 prefetch)."""
+        for a, b in zip(self.blocks, self.blocks[1:]):
+            a.struct.next_block = C.addressof(b.struct)
+
     def _reg(self, *ts):
         if self.gather is not None:
             self.gather.register(*[t for t in ts if t is not None])
@@ -152,6 +157,7 @@ class Stack:
             del lat
         st = cls(blocks, cfg.d, cfg.l, synth.torch_dtype(cfg.dtype), device)
         st.gather = None if shard is None else shard[1]
+        st.link_blocks()
         st.latents = kept
         st.generator = g
         return st
