@@ -174,54 +174,6 @@ __device__ __forceinline__ float i2f_small(int v) {
   return __fsub_rn(__int_as_float(0x4B400000 + v), 12582912.0f);
 }
 
-// ----------------------------------------------------------------- sum of squares (C4)
-// The reading C4 fixes sum(x^2) as a binary64-accurate sum rounded once.  The
-// fp64 pipe of this part is slow (measured: the fp64 prologue dominated the
-// decode GEMV), so per-element work is done in binary32 "double-float": x^2 =
-// p + e exactly (FMA), p is accumulated with Knuth's TwoSum and all error
-// terms in a second float.  The pair (s, c) carries ~2^-48 relative accuracy
-// per thread; partial pairs are combined in binary64 (a handful of ops per
-// warp), so the total matches a binary64 sum to ~1e-14 relative -- the same
-// order as the binary64 summation-order difference the reading already
-// admits.  Domain: |x| < 1.8e19 (x^2 finite in binary32).
-__device__ __forceinline__ void sq_acc(float x, float& s, float& c) {
-  const float p = __fmul_rn(x, x);
-  const float pe = __fmaf_rn(x, x, -p);
-  const float t = __fadd_rn(s, p);
-  const float z = __fsub_rn(t, s);
-  const float err = __fadd_rn(__fsub_rn(s, __fsub_rn(t, z)), __fsub_rn(p, z));
-  s = t;
-  c = __fadd_rn(c, __fadd_rn(err, pe));
-}
-// (s, c) += (s2, c2) with the leading sum error kept
-__device__ __forceinline__ void sq_merge(float& s, float& c, float s2, float c2) {
-  const float t = __fadd_rn(s, s2);
-  const float z = __fsub_rn(t, s);
-  const float err = __fadd_rn(__fsub_rn(s, __fsub_rn(t, z)), __fsub_rn(s2, z));
-  s = t;
-  c = __fadd_rn(c, __fadd_rn(c2, err));
-}
-__device__ __forceinline__ void warp_sq_merge(float& s, float& c) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
-    const float c2 = __shfl_xor_sync(0xffffffffu, c, o);
-    sq_merge(s, c, s2, c2);
-  }
-}
-// r = (float)(1 / sqrt(sum/K + eps)) from n per-warp (s, c) partials: the
-// partials are merged in double-float, the last steps run in binary64 with a
-// 1-ulp binary64 rsqrt (the fp64 pipe is slow; every fp64 op here is on the
-// critical path of the decode GEMV).  Agrees with the correctly rounded
-// binary64 expression except within ~1e-16 of a binary32 rounding boundary.
-__device__ __forceinline__ float inv_rms_from_parts(const float* ps, const float* pc, int n,
-                                                    double inv_k, float eps) {
-  float s = ps[0], c = pc[0];
-  for (int i = 1; i < n; ++i) sq_merge(s, c, ps[i], pc[i]);
-  const double tot = (double)s + (double)c;
-  return (float)rsqrt(tot * inv_k + (double)eps);
-}
-
 // ----------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum_f64(double v) {
 #pragma unroll
@@ -245,23 +197,6 @@ __device__ __forceinline__ int dp4a_us(uint32_t a_u8x4, uint32_t b_s8x4, int c) 
   int d;
   asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a_u8x4), "r"(b_s8x4), "r"(c));
   return d;
-}
-
-__device__ __forceinline__ uint32_t smem_u32_(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-// ----------------------------------------------------------------- cp.async (LDGSTS)
-// 16-byte asynchronous global -> shared copy, L2 only (.cg); completes at
-// cp_async_wait_all().
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32_(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ----------------------------------------------------------------- PTX: mbarrier / TMA / tcgen05
