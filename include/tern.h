@@ -14,7 +14,8 @@
  *    default stream), performs no host synchronisation (except tern_pack,
  *    see below) and no allocation, and is therefore CUDA-graph capturable.
  *  - Arguments are validated before anything is launched; a call that
- *    returns an error has had no side effect.  Checked: NULL pointers, sizes
+ *    returns an error has had no side effect.  A call with no tokens (B*T or
+ *    m == 0) is a no-op returning TERN_OK; its buffers may then be NULL.  Checked: NULL pointers, sizes
  *    <= 0, K and leading dimensions not multiples of 16 elements, pointers
  *    not 16-byte aligned, workspace too small, device not sm_100.
  *  - Errors are returned as tern_status; tern_last_error() gives a

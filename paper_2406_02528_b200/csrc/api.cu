@@ -372,9 +372,10 @@ tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, i
                           const float* gain, float eps, const tern_weight* w, const float* bias,
                           void* y, tern_dtype ydt, int32_t ldy, const tern_bl_taps* taps, void* ws,
                           size_t ws_bytes, tern_stream stream) {
-  CHECK(x && y, "bitlinear_fwd: null x/y");
   CHECK(valid_dt(xdt) && valid_dt(ydt), "bitlinear_fwd: bad dtype");
   CHECK(m >= 0 && k > 0 && k % 16 == 0, "bitlinear_fwd: m=%d k=%d", m, k);
+  if (m == 0) return TERN_OK;   // no tokens: a no-op
+  CHECK(x && y, "bitlinear_fwd: null x/y");
   CHECK(ldx >= k && ldx % 16 == 0 && aligned16(x), "bitlinear_fwd: ldx/alignment");
   tern_status st = check_weight(w, k, 1, "bitlinear_fwd");
   if (st) return st;
@@ -667,8 +668,10 @@ tern_status check_act(const void* x, const void* y, const void* ws, size_t ws_by
 tern_status mlgru_fwd(const tern_mlgru* p, const void* x, void* out, tern_dtype dt, int32_t B,
                       int32_t T, int32_t d, float* h, void* ws, size_t ws_bytes,
                       tern_stream stream) {
-  CHECK(p && h, "mlgru_fwd: null params/state");
+  CHECK(p, "mlgru_fwd: null params");
   CHECK(B >= 0 && T >= 0 && d > 0 && d % 64 == 0, "mlgru_fwd: B=%d T=%d d=%d", B, T, d);
+  if (B * T == 0) return TERN_OK;   // no tokens: a no-op
+  CHECK(h, "mlgru_fwd: null state");
   tern_status st;
   if ((st = check_weight(&p->fcg, d, 3, "fcg")) != TERN_OK) return st;
   if ((st = check_weight(&p->o, d, 1, "o")) != TERN_OK) return st;
@@ -685,6 +688,7 @@ tern_status glu_fwd(const tern_glu* p, const void* x, void* out, tern_dtype dt, 
                     int32_t d, int32_t l, void* ws, size_t ws_bytes, tern_stream stream) {
   CHECK(p, "glu_fwd: null params");
   CHECK(m >= 0 && d > 0 && d % 16 == 0 && l > 0 && l % 16 == 0, "glu_fwd: m=%d d=%d l=%d", m, d, l);
+  if (m == 0) return TERN_OK;   // no tokens: a no-op
   tern_status st;
   if ((st = check_weight(&p->gu, d, 2, "gate|up")) != TERN_OK) return st;
   if ((st = check_weight(&p->down, l, 1, "down")) != TERN_OK) return st;
@@ -702,8 +706,10 @@ static tern_status block_run(const tern_block* b, const void* x, void* y, tern_d
                              const char* name) {
   tern_status st = check_block(b);
   if (st) return st;
-  CHECK(h, "%s: null state", name);
   CHECK(B >= 0 && T >= 0, "%s: B=%d T=%d", name, B, T);
+  CHECK(valid_dt(dt), "%s: bad dtype", name);
+  if (B * T == 0) return TERN_OK;   // no tokens: a no-op (buffers may be empty / NULL)
+  CHECK(h, "%s: null state", name);
   BlockWs L = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt, block_world(b));
   if ((st = check_act(x, y, ws, ws_bytes, L.total, dt, name)) != TERN_OK) return st;
   if ((st = check_device()) != TERN_OK) return st;

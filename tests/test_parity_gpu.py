@@ -382,3 +382,61 @@ def test_batched_decode_split_k_parity(L, M, cfg_name, B, T, n_dec):
     close(yg, yo, 2e-2 if bf else 1e-4, cfg_name)
     assert np.array_equal(yg, yo)
     assert np.array_equal(states[0].cpu().numpy(), H[0])
+
+
+# ------------------------------------------------------------------------ full size, bench launch config
+@pytest.mark.parametrize("cfg_name,n_tok", [("c2", 24), ("c4", 8)])
+def test_full_size_prefill_sampled_prefixes(L, M, cfg_name, n_tok):
+    """The bench workload at full size and in bench.py's launch configuration (all blocks,
+    B x T prefill, fused f|c|g+scan, tcgen05 GEMMs): the MLGRU is causal, so the first
+    n_tok outputs of a sequence depend only on its first n_tok inputs -- the oracle computes
+    those prefixes through the whole stack and they must match bit for bit (sampled
+    sequences: first, a middle one, last)."""
+    cfg = synth.CONFIGS[cfg_name]
+    st = M.Stack.random(cfg, device="cuda", gen_device="cuda", keep_latents=cfg.L)
+    B, T = cfg.prefill_B, cfg.prefill_T
+    x = synth.hidden((B, T, cfg.d), synth.generator(cfg.seed + 7919), cfg.dtype).cuda()
+    states = st.new_state(B)
+    y = st.prefill(x, states)
+    torch.cuda.synchronize()
+    ob = [O.OracleBlock({k: v.numpy() for k, v in lat.items()}, cfg.d, cfg.l) for lat in st.latents]
+    bf = cfg.dtype == "bf16"
+    for b in (0, B // 2, B - 1):
+        xo = f32np(x[b:b + 1, :n_tok])
+        Hs = [np.zeros((1, cfg.d), np.float32) for _ in ob]
+        yo, _ = O.stack(ob, xo, Hs, bf16=bf)
+        yg = f32np(y[b:b + 1, :n_tok])
+        close(yg, yo, 2e-2 if bf else 1e-4, f"{cfg_name} seq {b}")
+        assert np.array_equal(yg, yo), f"{cfg_name} sequence {b}"
+
+
+# ------------------------------------------------------------------------ edge cases
+def test_zero_rows_and_empty_calls(L, M):
+    """Degenerate inputs (C7): an all-zero activation row quantizes to q = 0 and yields the
+    bias exactly on both contraction paths; empty batches are no-ops."""
+    n, k = 256, 512
+    W = latents(n, k, 71)
+    pw = M.PackedWeight([W.cuda()])
+    bias = torch.randn(n, generator=synth.generator(72))
+    for m, force_gemm in ((3, False), (40, True)):
+        x = acts((m, k), 73)
+        x[1] = 0.0
+        y = torch.empty((m, n), device="cuda")
+        old = L.tern_get_gemv_max_m()
+        try:
+            if force_gemm:
+                L.tern_set_gemv_max_m(0)
+            L.bitlinear_fwd(x.cuda(), pw.struct, y, bias=bias.cuda())
+            torch.cuda.synchronize()
+        finally:
+            L.tern_set_gemv_max_m(old)
+        assert torch.equal(y[1].cpu(), bias), "zero row must give the bias"
+        t, mw = O.ternarize(W.numpy())
+        assert np.array_equal(f32np(y), O.bitlinear(f32np(x), t, mw, bias=bias.numpy()))
+    # empty batches: nothing launched, nothing written, OK status
+    cfg = synth.Config("e", 1, 128, 256, "f32", 74, 1, 4, 1, 0)
+    st = M.Stack.random(cfg, gen_device="cpu")
+    x0 = torch.empty((0, 4, 128), device="cuda")
+    h0 = st.new_state(0)
+    y0 = st.prefill(x0, h0)
+    assert y0.shape == (0, 4, 128)
