@@ -36,11 +36,14 @@ template <int BN, bool kPre> struct GemmCfg {
   static constexpr int A_BYTES = kBM * kBK;        // 16 KB
   static constexpr int B_BYTES = BN * kBK;         // u8 B tile
   static constexpr int BP_BYTES = BN * (kBK / 4);  // packed B: BN rows x 8 words
-  // TMA ring depth S, unpacked ring depth U (packed path only)
-  static constexpr int S = kPre ? (BN == 256 ? 3 : 4) : (BN == 256 ? 4 : 5);
+  // TMA ring depth S, unpacked ring depth U (packed path only), epilogue
+  // staging tiles per warp NB: the u8 256-wide ring takes a 4th stage (deeper
+  // load pipeline) at the price of single-buffered epilogue stores
+  static constexpr int S = kPre ? 4 : (BN == 256 ? 4 : 5);
   static constexpr int U = kPre ? 0 : 2;
+  static constexpr int NB = (kPre && BN == 256) ? 1 : 2;
   static constexpr int RING = kPre ? S * (A_BYTES + B_BYTES) : S * (A_BYTES + BP_BYTES) + U * B_BYTES;
-  static constexpr int EPI_BYTES = kEpiWarps * 2 * kEpiBuf;
+  static constexpr int EPI_BYTES = kEpiWarps * NB * kEpiBuf;
   static constexpr int SMEM = RING + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int TMEM_COLS = 2 * BN;
 };
@@ -150,11 +153,11 @@ __device__ __forceinline__ uint32_t trow_base(uint32_t tmem_base, uint32_t acc, 
 __device__ void acc_tap_chunk(const Epi& e, const GemmArgs& a, int* si, int lane, int row0,
                               int col0, int qsum, const uint32_t (&v)[32]) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) si[lane * 33 + j] = (int)v[j] - qsum;
+  for (int j = 0; j < 32; ++j) si[lane * 32 + (j ^ lane)] = (int)v[j] - qsum;   // XOR swizzle
   __syncwarp();
   for (int r = 0; r < 32; ++r)
     if (row0 + r < a.M && col0 + lane < a.n_rows)
-      e.acc[(int64_t)(row0 + r) * e.ldacc + col0 + lane] = si[r * 33 + lane];
+      e.acc[(int64_t)(row0 + r) * e.ldacc + col0 + lane] = si[r * 32 + (lane ^ r)];
   __syncwarp();
 }
 
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int ew = warp - kEpiWarp0;
     const int quad = warp & 3;          // TMEM lanes [32*quad, 32*quad+32)
     const int half = ew >> 2;           // which half of the chunks this warp takes
-    uint8_t* bufs = sEpi + ew * 2 * kEpiBuf;
+    uint8_t* bufs = sEpi + ew * Cfg::NB * kEpiBuf;
     uint64_t* rb = rbar + ew * 2;
     const bool lead = lane == 0;
     const bool legacy = e.acc != nullptr || e.kind == EPI_NONE;   // tap / parity path
@@ -346,12 +349,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint32_t v[32];
           tmem_ld32(trow_base(tmem_base, acc, BN, quad) + c * 32, v);
           tmem_ld_wait();
+          if (lead) bulk_wait_read<0>();   // staging tile free of pending stores
+          __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) si[lane * 33 + j] = (int)v[j];
+          for (int j = 0; j < 32; ++j) si[lane * 32 + (j ^ lane)] = (int)v[j];   // XOR swizzle
           __syncwarp();
           for (int r = 0; r < 32; ++r)
             if (row0 + r < a.M && col0 + lane < a.n_rows)
-              slice[(int64_t)(row0 + r) * a.n_rows + col0 + lane] = si[r * 33 + lane];
+              slice[(int64_t)(row0 + r) * a.n_rows + col0 + lane] = si[r * 32 + (lane ^ r)];
           __syncwarp();
         }
         tc_fence_before();
@@ -392,10 +397,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (e.kind == EPI_NONE) continue;
         }
-        const int buf = nchunk & 1;
+        const int buf = Cfg::NB == 2 ? (nchunk & 1) : 0;
         uint8_t* sb = bufs + buf * kEpiBuf;
-        // the TMA store that last read this buffer (two chunks ago) must be done
-        if (lead) bulk_wait_read<1>();
+        // the TMA store that last read this buffer (NB chunks ago) must be done
+        if (lead) {
+          if (Cfg::NB == 2) bulk_wait_read<1>();
+          else bulk_wait_read<0>();
+        }
         __syncwarp();
         const bool resid = e.kind == EPI_RESID;
         if (resid && lead) {
