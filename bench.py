@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c0", "c2", "c3", "c4"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--decode-steps", type=int, default=None)
+    ap.add_argument("--decode-batch", type=int, default=None,
+                    help="decode batch per GPU (default: the config's, e.g. c4 also runs 128)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=None, help="oracle sample tokens")
     return ap.parse_args()
@@ -388,7 +390,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     # ---------------- decode (GEMV path): graph-replayed steps continuing from h = 0
     nd = args.decode_steps if args.decode_steps is not None else min(cfg.decode_steps, 500)
-    Bd = cfg.decode_B
+    Bd = args.decode_batch or cfg.decode_B
     dstates = st.new_state(Bd)
     g, xin_d, yout_d = st.capture_decode(Bd, dstates)
     for h in dstates:
