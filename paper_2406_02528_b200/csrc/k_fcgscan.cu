@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = sm.tmem_slot;
+  pdl_wait();                 // q, deq, qsum and h come from earlier kernels
+  pdl_launch_dependents();
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -342,7 +344,8 @@ static cudaError_t fcgscan_go(const CUtensorMap& ta, const CUtensorMap& tb, cons
   }
   const long long t0 = 0;
   (void)t0;
-  kern<<<grid, kFThreads, smem, s>>>(ta, tb, aa);
+  cudaError_t lerr = launch_pdl(kern, dim3(grid), dim3(kFThreads), smem, s, ta, tb, aa);
+  if (lerr != cudaSuccess) return lerr;
   if (prof_on) {
     static unsigned long long h[8 * 1024];
     cudaMemcpyAsync(h, dprof, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost, s);

@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();                 // A, deq, qsum, residual come from earlier kernels
+  pdl_launch_dependents();
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -532,7 +534,8 @@ static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, con
     cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * 8 * 1024, s);
     aa.prof = dprof;
   }
-  kern<<<grid, kGemmThreads, Cfg::SMEM, s>>>(ta, tb, to, tr, aa);
+  cudaError_t lerr = launch_pdl(kern, dim3(grid), dim3(kGemmThreads), Cfg::SMEM, s, ta, tb, to, tr, aa);
+  if (lerr != cudaSuccess) return lerr;
   if (prof_on) {
     static unsigned long long h[8 * 1024];
     cudaMemcpyAsync(h, dprof, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost, s);
@@ -566,6 +569,8 @@ template <typename TY>
 __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M, int n_rows,
                              const float* __restrict__ deq, const int32_t* __restrict__ qsum,
                              const Epi e) {
+  pdl_wait();                 // the GEMM's partial sums
+  pdl_launch_dependents();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool chan = e.kind == EPI_SWIGLU || e.kind == EPI_MLGRU;   // per logical channel
   const int ncol = chan ? e.n_out : (e.kind == EPI_FCG ? n_rows : e.n_out);
@@ -650,6 +655,8 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   const int kp = (w.k + kKAlign - 1) / kKAlign * kKAlign;
   static const int bn_force = getenv("TERN_GEMM_BN") ? atoi(getenv("TERN_GEMM_BN")) : 0;   // debug
   int BN = (w.n_rows >= 1024 || w.n_rows % 256 == 0) ? 256 : 128;
+  // small M (decode batches): narrower tiles so the weight rows spread over more SMs
+  if (M <= kSmallM) BN = 128;
   if (bn_force == 128 || bn_force == 256) BN = bn_force;
   // the u8 copy halves shared-memory traffic when the tensor cores are the limit
   // (large M); for decode batches the weight bytes are, and the 2-bit codes are 4x fewer
@@ -708,6 +715,7 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   if (finalize) {
     if (!part || part_bytes < slice) return cudaErrorInvalidValue;
     int ks = (num_sms + tiles - 1) / tiles;
+    if (ks > 4) ks = 4;   // the slices' int32 partials cost L2 traffic: few, long K slices
     if (ks > a.num_kb) ks = a.num_kb;
     if ((size_t)ks * slice > part_bytes) ks = (int)(part_bytes / slice);
     a.kb_per = (a.num_kb + ks - 1) / ks;
@@ -722,11 +730,12 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
     const int ncol = chan ? epi.n_out : (epi.kind == EPI_FCG ? w.n_rows : epi.n_out);
     const int64_t n = (int64_t)M * ((ncol + 1) / 2);
     const unsigned grid = (unsigned)((n + 255) / 256);
+    const int32_t* pc = part;
     if (yb)
-      k_splitk_epi<__nv_bfloat16><<<grid, 256, 0, s>>>(part, a.ksplit, M, w.n_rows, deq, qsum, epi);
-    else
-      k_splitk_epi<float><<<grid, 256, 0, s>>>(part, a.ksplit, M, w.n_rows, deq, qsum, epi);
-    return cudaGetLastError();
+      return launch_pdl(k_splitk_epi<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, pc, a.ksplit, M,
+                        w.n_rows, deq, qsum, epi);
+    return launch_pdl(k_splitk_epi<float>, dim3(grid), dim3(256), 0, s, pc, a.ksplit, M, w.n_rows,
+                      deq, qsum, epi);
   }
   if (pre)
     return yb ? gemm_dispatch_bn<true, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)

@@ -65,6 +65,8 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
   const bool rv = row < M;
   const int nvec = K / VE, nvecp = ((K + kKAlign - 1) / kKAlign * kKAlign) / VE;
   const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)(rv ? row : 0) * ldx);
+  pdl_wait();                 // x is the previous kernel's output
+  pdl_launch_dependents();
 
   uint4 xv[NV];
 #pragma unroll
@@ -194,15 +196,10 @@ static void quant_go(const TX* x, int m, int k, int ldx, const float* gain, floa
   const int grid = (m + RPC - 1) / RPC;
   const double inv_k = 1.0 / (double)k;
   const bool full = k == TPR * NV * QVec<TX>::N;   // then also k == Kp
-  if (gain)
-    k_quant<TX, TPR, NV, true, false><<<grid, kQThreads, 0, s>>>(x, m, k, ldx, gain, eps, inv_k, q,
-                                                                 ldq, deq, qsum, inv_rms, absmax);
-  else if (full)
-    k_quant<TX, TPR, NV, false, true><<<grid, kQThreads, 0, s>>>(x, m, k, ldx, gain, eps, inv_k, q,
-                                                                 ldq, deq, qsum, inv_rms, absmax);
-  else
-    k_quant<TX, TPR, NV, false, false><<<grid, kQThreads, 0, s>>>(x, m, k, ldx, gain, eps, inv_k,
-                                                                  q, ldq, deq, qsum, inv_rms, absmax);
+  auto kern = gain ? k_quant<TX, TPR, NV, true, false>
+                   : (full ? k_quant<TX, TPR, NV, false, true> : k_quant<TX, TPR, NV, false, false>);
+  launch_pdl(kern, dim3(grid), dim3(kQThreads), 0, s, x, m, k, ldx, gain, eps, inv_k, q, ldq, deq,
+             qsum, inv_rms, absmax);
 }
 
 template <typename TX, int TPR>

@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();                 // f^c^g^ and h come from earlier kernels
+  pdl_launch_dependents();
 
   if (warp == 0) {
     // ---------------- producer
@@ -169,8 +171,8 @@ static cudaError_t scan_go(const CUtensorMap& tm, int grid, int B, int T, int d,
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_scan<TE><<<grid, kScanThreads, smem, s>>>(tm, B, T, d, gate, h, static_cast<TE*>(oprime));
-  return cudaGetLastError();
+  return launch_pdl(k_scan<TE>, dim3(grid), dim3(kScanThreads), smem, s, tm, B, T, d, gate, h,
+                    static_cast<TE*>(oprime));
 }
 
 cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
