@@ -366,64 +366,48 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
     }
   }
   TY* out = static_cast<TY*>(e.out);
-  // all of this warp's channels (<= 4) and segments in one pass over the words:
-  // independent accumulators give the loads and dp4a chains ILP
-  int part[4][3][MM];
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
+#pragma unroll 1
+  for (int j = 0; j < 4; ++j) {
+    const int i = warp + j * kGWarps;
+    if (i >= a.ch) break;
+    const int rr = unit * a.ch + i;
+    int part[3][MM];
 #pragma unroll
     for (int sgi = 0; sgi < 3; ++sgi)
 #pragma unroll
-      for (int m = 0; m < MM; ++m) part[j][sgi][m] = -lq[m];
-  const int nj = min(4, (a.ch - warp + kGWarps - 1) / kGWarps);   // channels of this warp
-  for (int w = lane; w < W; w += 32) {
-    uint4 qv[MM];
+      for (int m = 0; m < MM; ++m) part[sgi][m] = -lq[m];
+    for (int w = lane; w < W; w += 32) {
+      uint4 qv[MM];
 #pragma unroll
-    for (int m = 0; m < MM; ++m) qv[m] = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
-    const uint32_t* wbase = swd + (w >> 3) * SW + (w & 7);
+      for (int m = 0; m < MM; ++m) qv[m] = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (j < nj) {
-        const int i = warp + j * kGWarps;
+      for (int sgi = 0; sgi < 3; ++sgi) {
+        if (sgi < a.n_seg) {
+          const uint32_t wd = swd[(sgi * nkb + (w >> 3)) * SW + i * 8 + (w & 7)];
 #pragma unroll
-        for (int sgi = 0; sgi < 3; ++sgi) {
-          if (sgi < a.n_seg) {
-            const uint32_t wd = wbase[sgi * nkb * SW + i * 8];
-#pragma unroll
-            for (int m = 0; m < MM; ++m) {
-              const int f0 = dp4a_us(wd & 0x03030303u, qv[m].x, 0);
-              const int f1 = dp4a_us(wd & 0x0C0C0C0Cu, qv[m].y, 0);
-              const int f2 = dp4a_us(wd & 0x30303030u, qv[m].z, 0);
-              const int f3 = dp4a_us(wd & 0xC0C0C0C0u, qv[m].w, 0);
-              part[j][sgi][m] += f0 + (f1 >> 2) + (f2 >> 4) + (f3 >> 6);   // exact multiples
-            }
+          for (int m = 0; m < MM; ++m) {
+            const int f0 = dp4a_us(wd & 0x03030303u, qv[m].x, 0);
+            const int f1 = dp4a_us(wd & 0x0C0C0C0Cu, qv[m].y, 0);
+            const int f2 = dp4a_us(wd & 0x30303030u, qv[m].z, 0);
+            const int f3 = dp4a_us(wd & 0xC0C0C0C0u, qv[m].w, 0);
+            part[sgi][m] += f0 + (f1 >> 2) + (f2 >> 4) + (f3 >> 6);   // exact multiples
           }
         }
       }
     }
-  }
-  GPROF(7)
-  // all-reduce, then lane m keeps token m's accumulators
-  int accs_[4][3];
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
+    if (j == 0) { GPROF(7) }
+    // all-reduce, then lane m keeps token m's accumulators
+    int acc[3] = {0, 0, 0};
 #pragma unroll
     for (int sgi = 0; sgi < 3; ++sgi) {
-      accs_[j][sgi] = 0;
-      if (j < nj && sgi < a.n_seg) {
+      if (sgi < a.n_seg) {
 #pragma unroll
         for (int m = 0; m < MM; ++m) {
-          const int v = warp_allsum_i32(part[j][sgi][m]);
-          if (lane == m) accs_[j][sgi] = v;
+          const int v = warp_allsum_i32(part[sgi][m]);
+          if (lane == m) acc[sgi] = v;
         }
       }
     }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (j >= nj) break;
-    const int i = warp + j * kGWarps;
-    const int rr = unit * a.ch + i;
-    const int acc[3] = {accs_[j][0], accs_[j][1], accs_[j][2]};
     if (j == 0) { GPROF(8) }
     if (rr >= a.n_out || lane >= a.M) continue;
     const int m = lane;
