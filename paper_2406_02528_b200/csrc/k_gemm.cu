@@ -714,7 +714,8 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
                          epi.acc == nullptr && tiles * 2 <= num_sms && a.num_kb >= 2);
   if (finalize) {
     if (!part || part_bytes < slice) return cudaErrorInvalidValue;
-    int ks = (num_sms + tiles - 1) / tiles;
+    int ks = num_sms / tiles;   // one round of work units over the SMs
+    if (ks < 1) ks = 1;
     if (ks > 4) ks = 4;   // the slices' int32 partials cost L2 traffic: few, long K slices
     if (ks > a.num_kb) ks = a.num_kb;
     if ((size_t)ks * slice > part_bytes) ks = (int)(part_bytes / slice);
