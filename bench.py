@@ -388,40 +388,60 @@ def run_ours(args, cfg, rank, world, local_rank):
            "d2h_bytes_per_step": yh.numel() * yh.element_size(),
            "path": "Stack.prefill via block_prefill (C ABI), pinned host buffers"}
 
-    # ---------------- decode (GEMV path): graph-replayed steps continuing from h = 0
+    # ---------------- decode: graph-replayed steps continuing from h = 0
     nd = args.decode_steps if args.decode_steps is not None else min(cfg.decode_steps, 500)
     Bd = args.decode_batch or cfg.decode_B
-    dstates = st.new_state(Bd)
-    g, xin_d, yout_d = st.capture_decode(Bd, dstates)
-    for h in dstates:
-        h.zero_()
     xs = synth.hidden((nd, Bd, d), synth.generator(cfg.seed + 31, dev), cfg.dtype, device=dev)
-    for t_ in range(3):
-        xin_d.copy_(xs[t_])
-        g.replay()
-    for h in dstates:
-        h.zero_()
-    torch.cuda.synchronize()
-    flush.fill_(1.0)
-    torch.cuda.synchronize()
-    barrier()
-    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    d0.record()
-    for t_ in range(nd):
-        xin_d.copy_(xs[t_])
-        g.replay()
-    d1.record()
-    torch.cuda.synchronize()
-    barrier()
-    dms = max_over_ranks(d0.elapsed_time(d1), world, dev)
+
+    def time_decode(persistent: bool):
+        st.persistent_decode = persistent
+        dstates = st.new_state(Bd)
+        g, xin_d, yout_d = st.capture_decode(Bd, dstates)
+        path = st.last_decode_path
+        for h in dstates:
+            h.zero_()
+        for t_ in range(3):
+            xin_d.copy_(xs[t_])
+            g.replay()
+        for h in dstates:
+            h.zero_()
+        torch.cuda.synchronize()
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        barrier()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record()
+        for t_ in range(nd):
+            xin_d.copy_(xs[t_])
+            g.replay()
+        d1.record()
+        torch.cuda.synchronize()
+        barrier()
+        del g
+        return max_over_ranks(d0.elapsed_time(d1), world, dev), path
+
+    dms, dpath = time_decode(False)
     wbytes = st.weight_bytes
+    persistent = dpath == "persistent"
     dec = {"tokens_per_s": round(nd * Bd * world / (dms / 1e3), 1), "batch_per_gpu": Bd,
            "steps": nd, "ms_per_token_step": round(dms / nd, 4),
            "weight_bytes_per_step": wbytes,
            "hbm_frac_of_weights_stream": round(wbytes / (dms / nd / 1e3) / 1e9 / pk["hbm_gbs"], 4),
-           "launches_per_step": 4 * cfg.L, "graph": True,
-           "note": "B<=8 decode = 4 GEMV launches per block (norm+quant prologue, MLGRU/SwiGLU/"
-                   "residual epilogues), weights L2-resident when they fit (126 MB L2)"}
+           "path": dpath,
+           "launches_per_step": ((cfg.L + 31) // 32) if persistent else 4 * cfg.L,
+           "graph": True,
+           "note": ("whole step = one persistent cooperative kernel per 32 blocks (stack_decode): "
+                    "4 BitLinear phases per block separated by grid barriers, next phase's "
+                    "weight slice TMA-copied to smem during the current one"
+                    if persistent else
+                    "4 launches per block (decode GEMV for B<=4: norm+quant prologue, "
+                    "MLGRU/SwiGLU/residual epilogues; quant + split-K tcgen05 GEMM above)")}
+    pms, ppath = time_decode(True)
+    if ppath == "persistent":   # the one-launch alternative (stack_decode), for comparison
+        dec["persistent_kernel"] = {"tokens_per_s": round(nd * Bd * world / (pms / 1e3), 1),
+                                    "ms_per_token_step": round(pms / nd, 4),
+                                    "launches_per_step": (cfg.L + 31) // 32}
+    st.persistent_decode = False
 
     out = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup,

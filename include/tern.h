@@ -280,6 +280,27 @@ tern_status block_prefill(const tern_block* b, const void* x, void* y, tern_dtyp
 tern_status block_decode(const tern_block* b, const void* x, void* y, tern_dtype dt, int32_t B,
                          float* h, void* ws, size_t ws_bytes, tern_stream stream);
 
+/* a9 + SURVEY 8(f) f2: one decode step (T = 1) through a whole stack of L
+ * blocks in ONE persistent launch: x [B][d] -> y [B][d], states h[i] ([B][d]
+ * fp32, device) of block i continued in place ("fall-through
+ * mode").  Same arithmetic as L block_decode calls chained through their
+ * outputs, bit for bit; the 4L dependent BitLinear phases are separated by
+ * grid-wide barriers in one cooperative kernel (one CTA per SM) instead of
+ * kernel launches, and each phase's weight slice is copied into shared memory
+ * while the previous phase runs.
+ *   blocks: host array of L unsharded blocks with equal d and l (next_block is
+ *           ignored); h: host array of L device pointers; x, y device, y != x.
+ *   ws: tern_stack_decode_workspace bytes (device, 16-byte aligned), owned by
+ *       the caller; concurrent calls need disjoint ws.
+ * Returns TERN_ERR_UNSUPPORTED (no side effects) when B > 4, a block is
+ * sharded, d or l exceed the decode GEMV register tile, or a phase's weight
+ * slice does not fit shared memory: use block_decode then.  B == 0 is a no-op.
+ * CUDA-graph capturable (a 4-byte memset + one kernel per 32 blocks). */
+size_t tern_stack_decode_workspace(const tern_block* blocks, int32_t L, int32_t B, tern_dtype dt);
+tern_status stack_decode(const tern_block* blocks, int32_t L, const void* x, void* y,
+                         tern_dtype dt, int32_t B, float* const* h, void* ws, size_t ws_bytes,
+                         tern_stream stream);
+
 /* ------------------------------------------------------------------------
  * Measurement hooks (bench.py roofline): while enabled, every kernel launch
  * made by this library on a non-capturing stream is bracketed by two CUDA
@@ -289,12 +310,13 @@ tern_status block_decode(const tern_block* b, const void* x, void* y, tern_dtype
  * kept until the next tern_profile_enable(1).  Not for use in production.
  * ------------------------------------------------------------------------ */
 typedef enum { TERN_K_QUANT = 0, TERN_K_GEMV = 1, TERN_K_GEMM = 2, TERN_K_SCAN = 3,
-               TERN_K_FCGSCAN = 4 } tern_kernel_id;
+               TERN_K_FCGSCAN = 4, TERN_K_STACK = 5, TERN_K_FIN = 6 } tern_kernel_id;
 typedef struct {
   int32_t kernel;   /* tern_kernel_id                                        */
   int32_t epi;      /* epilogue kind (GEMV/GEMM) or gate mode (scan)         */
   int32_t m;        /* rows (tokens); scan: B*T                              */
-  int32_t n;        /* GEMV/GEMM: packed weight rows; scan: d; quant: 0      */
+  int32_t n;        /* GEMV/GEMM: packed weight rows; scan: d; quant: 0;
+                       stack: blocks                                          */
   int32_t k;        /* input features                                        */
   int32_t n_seg;    /* weight segments                                       */
   int32_t dtype;    /* activation dtype (tern_dtype)                         */
@@ -338,6 +360,13 @@ void tern_set_gemv_max_m(int32_t m);
 void tern_set_fused_scan(int32_t on);
 int32_t tern_get_fused_scan(void);
 int32_t tern_get_gemv_max_m(void);
+/* Tuning knob (host): 1 runs decode steps with gemv_max_m < B <= 256 as, per
+ * BitLinear, a split-K GEMM writing int32 partials plus one row-wise finalize
+ * that applies the epilogue and quantizes the row for the next BitLinear
+ * (9 launches per block); 0 (default, measured faster on c3) runs quant +
+ * GEMM + epilogue per BitLinear.  Results are identical. */
+void tern_set_batched_fin(int32_t on);
+int32_t tern_get_batched_fin(void);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

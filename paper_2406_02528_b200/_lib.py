@@ -71,7 +71,7 @@ class tern_prof_rec(C.Structure):
                 ("k", C.c_int32), ("n_seg", C.c_int32), ("dtype", C.c_int32), ("ms", C.c_float)]
 
 
-KERNEL_NAMES = {0: "quant", 1: "gemv", 2: "gemm_tc", 3: "scan", 4: "fcgscan"}
+KERNEL_NAMES = {0: "quant", 1: "gemv", 2: "gemm_tc", 3: "scan", 4: "fcgscan", 5: "stack", 6: "fin"}
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -101,6 +101,9 @@ _SIGS = {
     "glu_fwd": (C.c_int, [C.POINTER(tern_glu), P, P, C.c_int, I32, I32, I32, P, SZ, P]),
     "block_prefill": (C.c_int, [C.POINTER(tern_block), P, P, C.c_int, I32, I32, P, P, SZ, P]),
     "block_decode": (C.c_int, [C.POINTER(tern_block), P, P, C.c_int, I32, P, P, SZ, P]),
+    "tern_stack_decode_workspace": (SZ, [C.POINTER(tern_block), I32, I32, C.c_int]),
+    "stack_decode": (C.c_int, [C.POINTER(tern_block), I32, P, P, C.c_int, I32,
+                               C.POINTER(C.c_void_p), P, SZ, P]),
     "tern_profile_enable": (None, [I32]),
     "tern_trace_enable": (None, [I32]),
     "tern_trace_collect": (I32, [C.c_void_p, I32]),
@@ -110,6 +113,8 @@ _SIGS = {
     "tern_get_gemv_max_m": (I32, []),
     "tern_set_fused_scan": (None, [I32]),
     "tern_get_fused_scan": (I32, []),
+    "tern_set_batched_fin": (None, [I32]),
+    "tern_get_batched_fin": (I32, []),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -251,12 +256,40 @@ def block_decode(b: tern_block, x, y, h, ws, stream=None):
                                ptr(ws), ws.numel(), stream_handle(stream)), "block_decode")
 
 
+def tern_stack_decode_workspace(blocks, B: int, dt: torch.dtype) -> int:
+    """blocks: ctypes array of tern_block."""
+    return int(load().tern_stack_decode_workspace(blocks, len(blocks), B, dtype_code(dt)))
+
+
+def stack_decode(blocks, x, y, hs, ws, stream=None, allow_unsupported=False) -> int:
+    """One decode step through the whole stack in one launch (tern.h stack_decode).
+    blocks: ctypes array of tern_block; hs: list of per-block fp32 states.
+    With allow_unsupported, TERN_ERR_UNSUPPORTED is returned instead of raised."""
+    B = x.shape[0]
+    harr = (C.c_void_p * len(hs))(*[h.data_ptr() for h in hs])
+    st = load().stack_decode(blocks, len(blocks), ptr(x), ptr(y), dtype_code(x.dtype), B, harr,
+                             ptr(ws), ws.numel(), stream_handle(stream))
+    if st == TERN_ERR_UNSUPPORTED and allow_unsupported:
+        load().tern_last_error()
+        return st
+    _check(st, "stack_decode")
+    return st
+
+
 def tern_set_gemv_max_m(m: int):
     load().tern_set_gemv_max_m(int(m))
 
 
 def tern_set_fused_scan(on: bool):
     load().tern_set_fused_scan(1 if on else 0)
+
+
+def tern_set_batched_fin(on: bool):
+    load().tern_set_batched_fin(1 if on else 0)
+
+
+def tern_get_batched_fin() -> bool:
+    return bool(load().tern_get_batched_fin())
 
 
 def tern_get_fused_scan() -> bool:

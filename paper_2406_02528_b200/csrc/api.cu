@@ -4,6 +4,7 @@
 // has no side effects.  No allocation, no host sync (except tern_pack).
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -18,6 +19,7 @@ namespace {
 thread_local std::string g_err;
 int g_gemv_max_m = kGemvMaxM;
 int g_fused_scan = 1;
+int g_batched_fin = 0;   // tern_set_batched_fin
 constexpr int kSplitKMaxM = 256;
 
 tern_status fail(tern_status st, const char* fmt, ...) {
@@ -290,6 +292,8 @@ void tern_set_fused_scan(int32_t on) { g_fused_scan = on != 0; }
 int32_t tern_get_fused_scan(void) { return g_fused_scan; }
 void tern_set_gemv_max_m(int32_t m) { g_gemv_max_m = m < 0 ? 0 : (m > kGemvMaxM ? kGemvMaxM : m); }
 int32_t tern_get_gemv_max_m(void) { return g_gemv_max_m; }
+void tern_set_batched_fin(int32_t on) { g_batched_fin = on ? 1 : 0; }
+int32_t tern_get_batched_fin(void) { return g_batched_fin; }
 
 int32_t tern_packed_rows(int32_t n_out, int32_t n_seg) {
   if (n_seg <= 1) return n_out;
@@ -652,6 +656,66 @@ tern_status run_block_sharded(const tern_block& b, const void* x, void* y, tern_
   return shard_gather(sh, sout, y, M, ds, dt, ws, L, s);
 }
 
+// a8 decode step for gemv_max_m < B <= kSplitKMaxM: per BitLinear one split-K
+// tcgen05 GEMM writing int32 partials and one row-wise finalize (k_fin.cu) that
+// applies the epilogue and quantizes its output row for the next BitLinear, so
+// only the block input needs a quant launch (9 launches per block)
+bool batched_decode_ok(const tern_block& b, int B, int T, const BlockWs& L) {
+  return T == 1 && B > g_gemv_max_m && B <= kSplitKMaxM && L.part_bytes > 0 &&
+         fin_supported(b.d) && fin_supported(b.l) && g_batched_fin;
+}
+
+tern_status run_block_decode_batched(const tern_block& b, const void* x, void* y, tern_dtype dt,
+                                     int B, float* h, void* ws, const BlockWs& L, cudaStream_t s) {
+  const int d = b.d, l = b.l;
+  const tern_mlgru& mx = b.mix;
+  const tern_glu& gl = b.ch;
+  int8_t* q = at<int8_t>(ws, L.q);
+  float* deq = at<float>(ws, L.deq);
+  int32_t* qsum = at<int32_t>(ws, L.qsum);
+  int32_t* part = at<int32_t>(ws, L.part);
+  void* op = at<char>(ws, L.oprime);
+  void* x1 = at<char>(ws, L.x1);
+  void* pp = at<char>(ws, L.p);
+  {
+    Prof pr(TERN_K_QUANT, 0, B, 0, d, 0, dt, s);
+    TRY_CUDA(launch_quant(x, dt, B, d, d, mx.gain_x, mx.eps, q, kpad(d), deq, qsum, nullptr,
+                          nullptr, s),
+             "quant");
+  }
+  // one phase: GEMM partials, then finalize (+ the next BitLinear's quant)
+  auto phase = [&](const tern_weight& w, int K, const Epi& e, const float* ngain, float neps,
+                   bool nquant) -> tern_status {
+    int ks = 1;
+    {
+      Prof pr(TERN_K_GEMM, EPI_NONE, B, w.n_rows, K, w.n_seg, dt, s);
+      Epi ge = make_epi(EPI_NONE, w, nullptr, nullptr, 0);
+      TRY_CUDA(launch_gemm(q, B, kpad(K), deq, qsum, w, dt, ge, s, part, L.part_bytes, &ks),
+               "gemm (partials)");
+    }
+    Prof pr(TERN_K_FIN, e.kind, B, w.n_rows, K, w.n_seg, dt, s);
+    TRY_CUDA(launch_fin(part, ks, B, w.n_rows, deq, qsum, e, dt, ngain, neps,
+                        nquant ? q : nullptr, kpad(e.n_out), deq, qsum, s),
+             "finalize");
+    return TERN_OK;
+  };
+  tern_status st;
+  Epi e1 = make_epi(EPI_MLGRU, mx.fcg, mx.bias_fcg, op, d);
+  e1.h = h;
+  e1.gate = mx.gate;
+  if ((st = phase(mx.fcg, d, e1, mx.gain_o, mx.eps, true))) return st;
+  Epi e2 = make_epi(EPI_RESID, mx.o, mx.bias_o, x1, d);
+  e2.res = x;
+  e2.ldr = d;
+  if ((st = phase(mx.o, d, e2, gl.gain_x, gl.eps, true))) return st;
+  Epi e3 = make_epi(EPI_SWIGLU, gl.gu, nullptr, pp, l);
+  if ((st = phase(gl.gu, d, e3, gl.gain_p, gl.eps, true))) return st;
+  Epi e4 = make_epi(EPI_RESID, gl.down, nullptr, y, d);
+  e4.res = x1;
+  e4.ldr = d;
+  return phase(gl.down, l, e4, nullptr, 0.0f, false);
+}
+
 tern_status check_act(const void* x, const void* y, const void* ws, size_t ws_bytes, size_t need,
                       tern_dtype dt, const char* name) {
   CHECK(x && y, "%s: null x/y", name);
@@ -716,6 +780,7 @@ static tern_status block_run(const tern_block* b, const void* x, void* y, tern_d
   if (B * T == 0) return TERN_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (block_world(b) > 1) return run_block_sharded(*b, x, y, dt, B, T, h, ws, L, s);
+  if (batched_decode_ok(*b, B, T, L)) return run_block_decode_batched(*b, x, y, dt, B, h, ws, L, s);
   void* x1 = at<char>(ws, L.x1);
   // weight-stream prefetch (decode GEMVs): the token mixer pulls this block's
   // channel-mixer weights into L2, the channel mixer the next block's token mixer
@@ -745,6 +810,99 @@ tern_status block_prefill(const tern_block* b, const void* x, void* y, tern_dtyp
 tern_status block_decode(const tern_block* b, const void* x, void* y, tern_dtype dt, int32_t B,
                          float* h, void* ws, size_t ws_bytes, tern_stream stream) {
   return block_run(b, x, y, dt, B, 1, h, ws, ws_bytes, stream, "block_decode");
+}
+
+// ----------------------------------------------------------------- f2: stack decode
+namespace {
+struct StackWs {
+  size_t bar, a, x1, p, xb, total;
+};
+StackWs stack_ws(int B, int d, int l, tern_dtype dt) {
+  StackWs w{};
+  size_t off = 0;
+  w.bar = off; off += al256((64 + 1024) * 4);   // grid barrier counter + per-CTA flags
+  w.a = off; off += al256((size_t)B * d * dsize(dt));    // o'
+  w.x1 = off; off += al256((size_t)B * d * dsize(dt));   // x1 = x + o
+  w.p = off; off += al256((size_t)B * l * dsize(dt));    // p = SiLU(g) u
+  w.xb = off; off += al256((size_t)B * d * dsize(dt));   // block outputs between blocks
+  w.total = off;
+  return w;
+}
+
+// the 4 phases of every block; buffers: a block's input is x (block 0) or xb,
+// its output xb (y for the last); xb can be both because the down phase that
+// overwrites it runs two grid barriers after its last reader (the o phase)
+std::vector<StackPhaseDesc> stack_phases(const tern_block* blocks, int L, const void* x, void* y,
+                                         float* const* h, void* ws, const StackWs& W) {
+  std::vector<StackPhaseDesc> ph;
+  ph.reserve((size_t)4 * L);
+  void* a = at<char>(ws, W.a);
+  void* x1 = at<char>(ws, W.x1);
+  void* p = at<char>(ws, W.p);
+  void* xb = at<char>(ws, W.xb);
+  for (int i = 0; i < L; ++i) {
+    const tern_block& b = blocks[i];
+    const void* xin = i == 0 ? x : xb;
+    void* xout = i == L - 1 ? y : xb;
+    StackPhaseDesc f{xin, nullptr, a, h[i], b.mix.fcg, b.mix.gain_x, b.mix.bias_fcg, b.mix.eps,
+                     EPI_MLGRU, (int)b.mix.gate, b.d};
+    StackPhaseDesc o{a, xin, x1, nullptr, b.mix.o, b.mix.gain_o, b.mix.bias_o, b.mix.eps,
+                     EPI_RESID, 0, b.d};
+    StackPhaseDesc g{x1, nullptr, p, nullptr, b.ch.gu, b.ch.gain_x, nullptr, b.ch.eps,
+                     EPI_SWIGLU, 0, b.d};
+    StackPhaseDesc dn{p, x1, xout, nullptr, b.ch.down, b.ch.gain_p, nullptr, b.ch.eps,
+                      EPI_RESID, 0, b.l};
+    ph.push_back(f);
+    ph.push_back(o);
+    ph.push_back(g);
+    ph.push_back(dn);
+  }
+  return ph;
+}
+
+tern_status check_stack(const tern_block* blocks, int32_t L, int32_t B, tern_dtype dt,
+                        const char* name) {
+  CHECK(blocks && L > 0, "%s: null blocks or L=%d", name, L);
+  CHECK(B >= 0, "%s: B=%d", name, B);
+  CHECK(valid_dt(dt), "%s: bad dtype", name);
+  tern_status st;
+  for (int i = 0; i < L; ++i) {
+    if ((st = check_block(&blocks[i])) != TERN_OK) return st;
+    CHECK(blocks[i].d == blocks[0].d && blocks[i].l == blocks[0].l, "%s: block %d widths differ",
+          name, i);
+  }
+  return TERN_OK;
+}
+}  // namespace
+
+size_t tern_stack_decode_workspace(const tern_block* blocks, int32_t L, int32_t B, tern_dtype dt) {
+  if (!blocks || L <= 0 || B < 0) return 0;
+  return stack_ws(B, blocks[0].d, blocks[0].l, dt).total;
+}
+
+tern_status stack_decode(const tern_block* blocks, int32_t L, const void* x, void* y,
+                         tern_dtype dt, int32_t B, float* const* h, void* ws, size_t ws_bytes,
+                         tern_stream stream) {
+  tern_status st = check_stack(blocks, L, B, dt, "stack_decode");
+  if (st) return st;
+  if (B == 0) return TERN_OK;   // no tokens: a no-op
+  CHECK(h, "stack_decode: null state array");
+  for (int i = 0; i < L; ++i) CHECK(h[i], "stack_decode: null state of block %d", i);
+  const StackWs W = stack_ws(B, blocks[0].d, blocks[0].l, dt);
+  if ((st = check_act(x, y, ws, ws_bytes, W.total, dt, "stack_decode")) != TERN_OK) return st;
+  for (int i = 0; i < L; ++i)
+    if (block_world(&blocks[i]) > 1)
+      return fail(TERN_ERR_UNSUPPORTED, "stack_decode: block %d is sharded", i);
+  if ((st = check_device()) != TERN_OK) return st;
+  std::vector<StackPhaseDesc> ph = stack_phases(blocks, L, x, y, h, ws, W);
+  if (!stack_decode_plan(ph.data(), (int)ph.size(), B, dt, nullptr))
+    return fail(TERN_ERR_UNSUPPORTED, "stack_decode: B=%d d=%d l=%d outside the persistent plan", B,
+                blocks[0].d, blocks[0].l);
+  Prof pr(TERN_K_STACK, 0, B, L, blocks[0].d, 0, dt, (cudaStream_t)stream);
+  TRY_CUDA(launch_stack_decode(ph.data(), (int)ph.size(), B, dt, at<unsigned>(ws, W.bar),
+                               (cudaStream_t)stream),
+           "stack_decode");
+  return TERN_OK;
 }
 
 }  // extern "C"

@@ -219,6 +219,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// Adds to the expected transaction bytes of the current phase without arriving.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
 // Waits for the phase with the given parity.  try_wait carries a suspend-time
 // hint, so a waiting warp sleeps until the phase completes (or the hint
 // elapses) instead of spinning on the issue slots its CTA's busy warps need.

@@ -69,9 +69,38 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
                         cudaStream_t s, const void* pf = nullptr, size_t pf_bytes = 0);
 // a4 (tcgen05 int8 GEMM): q [M][ldq] -> epilogue
 // part: optional int32 scratch [M][n_rows] enabling split-K for small M (nullptr: never)
+// ks_out: partials only (part required): the K-slice count is returned and no
+// epilogue runs (launch_fin finalizes)
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
-                        int32_t* part = nullptr, size_t part_bytes = 0);
+                        int32_t* part = nullptr, size_t part_bytes = 0, int* ks_out = nullptr);
+// batched decode: one CTA per row sums the ks partial slices [ks][M][n_rows],
+// applies e (MLGRU / SWIGLU / RESID / STORE) and, when nq is set, the next
+// BitLinear's RMSNorm + int8 quant of the stored output row (gain ngain, eps
+// neps) into nq [M][nldq], ndeq, nqsum (which may alias deq / qsum)
+bool fin_supported(int n_out);
+cudaError_t launch_fin(const int32_t* part, int ks, int M, int n_rows, const float* deq,
+                       const int32_t* qsum, const Epi& e, int ydt, const float* ngain, float neps,
+                       int8_t* nq, int nldq, float* ndeq, int32_t* nqsum, cudaStream_t s);
+// f2: whole-stack decode step in one persistent cooperative launch.  A phase
+// is one decode BitLinear with its epilogue (MLGRU / SWIGLU / RESID / STORE),
+// contiguous rows (ld = K for x, n_out for out/res/h).
+struct StackPhaseDesc {
+  const void* x;
+  const void* res;
+  void* out;
+  float* h;
+  tern_weight w;
+  const float* gain;
+  const float* bias;
+  float eps;
+  int kind, gate, K;
+};
+bool stack_decode_plan(const StackPhaseDesc* ph, int n, int M, int xdt, size_t* smem);
+// bar: one zeroed-per-launch u32 grid-barrier counter (device); returns
+// cudaErrorNotSupported when the plan does not fit (stack_decode_plan false)
+cudaError_t launch_stack_decode(const StackPhaseDesc* ph, int n, int M, int xdt, unsigned* bar,
+                                cudaStream_t s);
 // debug timeline of GEMV launches (globaltimer per CTA), see tern_trace_enable
 void gemv_trace_enable(int on);
 int gemv_trace_collect(unsigned long long* out, int max_launches);

@@ -217,12 +217,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();                 // A, deq, qsum, residual come from earlier kernels
+  // A, deq, qsum, residual come from earlier kernels: every warp but the
+  // producer waits here; the producer first starts the weight (B) loads of its
+  // first stages, which do not depend on them (PDL overlap with the previous
+  // kernel's tail; for decode batches the weight fetch is the long pole)
+  if (warp != 0) pdl_wait();
   pdl_launch_dependents();
 
   if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
+      auto load_b = [&](int s, int kb, int n0) {
+        if (kPre) {
+          tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * kBK, n0);
+        } else {
+          // one contiguous span (K-block-major layout); ragged last tile shorter
+          const uint32_t bbytes = (uint32_t)min(BN, a.n_rows - n0) * 32u;
+          bulk_load(sBp + s * Cfg::BP_BYTES, a.codes + ((int64_t)kb * a.n_rows + n0) * 8, bbytes,
+                    &full[s]);
+        }
+      };
+      auto b_bytes = [&](int n0) -> uint32_t {
+        return kPre ? (uint32_t)Cfg::B_BYTES : (uint32_t)min(BN, a.n_rows - n0) * 32u;
+      };
+      // weights of the first unit's first S k-blocks before the dependency wait
+      uint32_t npre = 0;
+      if ((int)blockIdx.x < total) {
+        const int t = blockIdx.x, tile = t / a.ksplit, sp = t % a.ksplit;
+        const int n0 = (tile % a.n_tiles) * BN;
+        const int kb0 = sp * a.kb_per, kb1 = min(nk, kb0 + a.kb_per);
+        for (int kb = kb0; kb < kb1 && npre < (uint32_t)S; ++kb, ++npre) {
+          mbar_expect_tx(&full[npre], b_bytes(n0));
+          load_b((int)npre, kb, n0);
+        }
+      }
+      pdl_wait();
       uint32_t g = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int tile = t / a.ksplit, sp = t % a.ksplit;
@@ -231,17 +260,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = sp * a.kb_per; kb < kb1; ++kb, ++g) {
           const int s = g % S;
           if (g >= (uint32_t)S) pwait(&empty[s], ((g / S) - 1) & 1, a.prof, 0);
-          if (kPre) {
-            mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
+          if (g < npre) {   // B already in flight
+            mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES);
             tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kBK, m0);
-            tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * kBK, n0);
           } else {
-            // one contiguous span (K-block-major layout); ragged last tile shorter
-            const uint32_t bbytes = (uint32_t)min(BN, a.n_rows - n0) * 32u;
-            mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + bbytes);
+            mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + b_bytes(n0));
             tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kBK, m0);
-            bulk_load(sBp + s * Cfg::BP_BYTES, a.codes + ((int64_t)kb * a.n_rows + n0) * 8,
-                      bbytes, &full[s]);
+            load_b(s, kb, n0);
           }
         }
       }
@@ -650,7 +675,7 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
 
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
-                        int32_t* part, size_t part_bytes) {
+                        int32_t* part, size_t part_bytes, int* ks_out) {
   if (M <= 0) return cudaSuccess;
   const int kp = (w.k + kKAlign - 1) / kKAlign * kKAlign;
   static const int bn_force = getenv("TERN_GEMM_BN") ? atoi(getenv("TERN_GEMM_BN")) : 0;   // debug
@@ -660,7 +685,10 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   if (bn_force == 128 || bn_force == 256) BN = bn_force;
   // the u8 copy halves shared-memory traffic when the tensor cores are the limit
   // (large M); for decode batches the weight bytes are, and the 2-bit codes are 4x fewer
-  const bool pre = w.e8 != nullptr && M > kSmallM;
+  // small M: the u8 copy too (TMA only, no smem unpack on the critical path:
+  // measured faster for decode batches than the 4x smaller 2-bit codes)
+  static const int small_pre = getenv("TERN_SMALLM_PRE") ? atoi(getenv("TERN_SMALLM_PRE")) : 1;   // debug
+  const bool pre = w.e8 != nullptr && (M > kSmallM || small_pre);
   const bool yb = ydt == TERN_BF16;
   const size_t ys = yb ? 2 : 4;
   const CUtensorMapDataType ydtype = yb ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -709,7 +737,7 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   }
   const int tiles = a.n_tiles * a.m_tiles;
   const size_t slice = (size_t)M * w.n_rows * sizeof(int32_t);
-  const bool finalize = epi.kind == EPI_MLGRU ||
+  const bool finalize = ks_out != nullptr || epi.kind == EPI_MLGRU ||
                         (part && part_bytes >= slice && epi.kind != EPI_NONE &&
                          epi.acc == nullptr && tiles * 2 <= num_sms && a.num_kb >= 2);
   if (finalize) {
@@ -727,6 +755,10 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
                           : (yb ? gemm_dispatch_bn<false, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)
                                 : gemm_dispatch_bn<false, float>(BN, ta, tb, to, tr, a, s));
     if (err != cudaSuccess) return err;
+    if (ks_out) {   // partials only: the caller finalizes (k_fin.cu)
+      *ks_out = a.ksplit;
+      return cudaSuccess;
+    }
     const bool chan = epi.kind == EPI_SWIGLU || epi.kind == EPI_MLGRU;
     const int ncol = chan ? epi.n_out : (epi.kind == EPI_FCG ? w.n_rows : epi.n_out);
     const int64_t n = (int64_t)M * ((ncol + 1) / 2);

@@ -117,86 +117,54 @@ __device__ __forceinline__ int warp_allsum_i32(int v) {
   return v;
 }
 
-template <int MM, typename TX, typename TY>
-__global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
-  extern __shared__ __align__(128) uint8_t g_smem[];
-  int8_t* qs = reinterpret_cast<int8_t*>(g_smem + (size_t)a.n_seg * (a.Kp >> 7) * a.sw_stride * 4);  // [MM][Kp]
-  __shared__ double red_d[MM][kGWarps];
-  __shared__ float red_m[MM][kGWarps];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int unit = blockIdx.x;
-  long long pt0 = 0;
-  if (a.prof) pt0 = clock64();
-  if (a.trace && tid == 0) {
-    a.trace[blockIdx.x * 16 + 0] = gtimer();
-    a.trace[blockIdx.x * 16 + 3] = clock64();
-  }
-#define GPROF(i)                                                                 \
-  if (a.prof && tid == 0 && (i) < 8) a.prof[blockIdx.x * 8 + (i)] = clock64() - pt0; \
-  if (a.trace && tid == 0 && (i) >= 2) a.trace[blockIdx.x * 16 + 3 + (i)] = gtimer();
+// ---------------------------------------------------------------- phase pieces
+// (shared by the one-BitLinear kernel k_gemv and the whole-stack persistent
+// kernel k_stack_decode)
 
-  // ---------------- packed weights -> smem with the TMA engine (bulk copies; the
-  // LSU pipe stays free for the running kernel's critical path).  In the
-  // K-block-major layout the CTA's rows of one segment within one 64-row group
-  // are one contiguous span per K-block.  Smem: [seg][kb] blocks of ch rows x
-  // 8 words, block stride SW words (SW = 8 mod 32: conflict-free dot reads).
-  const int nkb = a.Kp >> 7;
-  const int SW = a.sw_stride;
-  __shared__ __align__(8) uint64_t wbar;
+// Warp 0: bulk-copy unit's packed weights into dst (completing on bar), or with
+// l2_only just pull them into L2.  In the K-block-major layout the unit's rows
+// of one segment within one 64-row group are one contiguous span per K-block.
+// Smem: [seg][kb] blocks of ch rows x 8 words, block stride SW words (SW = 8 mod
+// 32: conflict-free dot reads).  A unit without rows arrives with 0 bytes.
+__device__ __forceinline__ void gemv_issue(const GemvArgs& a, int unit, uint32_t* dst,
+                                           uint64_t* bar, int lane, bool l2_only) {
+  const int nkb = a.Kp >> 7, SW = a.sw_stride;
   const int r0 = unit * a.ch, r1 = min(r0 + a.ch, a.n_out);   // logical rows [r0, r1)
-  if (warp == 0) {
-    const int g0 = r0 >> 6, g1 = (r1 - 1) >> 6;   // 64-row groups touched (<= 2)
-    const int nparts = a.n_seg == 1 ? 1 : g1 - g0 + 1;
-    if (lane == 0) {
-      mbar_init(&wbar, 1);
-      fence_barrier_init();
-      mbar_arrive_expect_tx(&wbar, (uint32_t)(a.n_seg * nkb * (r1 - r0) * 32));
+  if (!l2_only && lane == 0)
+    mbar_arrive_expect_tx(bar, r1 > r0 ? (uint32_t)(a.n_seg * nkb * (r1 - r0) * 32) : 0u);
+  if (r1 <= r0) return;
+  __syncwarp();
+  const int g0 = r0 >> 6, g1 = (r1 - 1) >> 6;   // 64-row groups touched (<= 2)
+  const int nparts = a.n_seg == 1 ? 1 : g1 - g0 + 1;
+  const int nspan = a.n_seg * nkb * nparts;
+  for (int sp = lane; sp < nspan; sp += 32) {
+    const int part = sp % nparts, t = sp / nparts;
+    const int kb = t % nkb, sg = t / nkb;
+    int a0r = r0, a1r = r1;
+    if (a.n_seg > 1) {
+      const int gb = (g0 + part) << 6;
+      a0r = max(r0, gb);
+      a1r = min(r1, gb + 64);
     }
-    __syncwarp();
-    const int nspan = a.n_seg * nkb * nparts;
-    for (int sp = lane; sp < nspan; sp += 32) {
-      const int part = sp % nparts, t = sp / nparts;
-      const int kb = t % nkb, sg = t / nkb;
-      int a0r = r0, a1r = r1;
-      if (a.n_seg > 1) {
-        const int gb = (g0 + part) << 6;
-        a0r = max(r0, gb);
-        a1r = min(r1, gb + 64);
-      }
-      const int pr = a.n_seg == 1 ? a0r : packed_row(sg, a0r, a.n_seg);
-      bulk_load(sw_words(g_smem) + (sg * nkb + kb) * SW + (a0r - r0) * 8,
-                a.codes + ((int64_t)kb * a.n_rows + pr) * 8, (uint32_t)(a1r - a0r) * 32u, &wbar);
-    }
+    const int pr = a.n_seg == 1 ? a0r : packed_row(sg, a0r, a.n_seg);
+    const uint32_t* src = a.codes + ((int64_t)kb * a.n_rows + pr) * 8;
+    const uint32_t bytes = (uint32_t)(a1r - a0r) * 32u;
+    if (l2_only)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+    else
+      bulk_load(dst + (sg * nkb + kb) * SW + (a0r - r0) * 8, src, bytes, bar);
   }
-  // L2 prefetch of this CTA's share of a later launch's weights (HBM-resident
-  // stacks: the weight stream runs ahead of the dependency chain)
-  if (a.pf && tid == 32) {
-    const size_t chunk = ((a.pf_bytes + gridDim.x - 1) / gridDim.x + 15) & ~size_t(15);
-    const size_t off = chunk * blockIdx.x;
-    if (off < a.pf_bytes) {
-      const size_t n = a.pf_bytes - off < chunk ? a.pf_bytes - off : chunk;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf + off), "r"((uint32_t)n)
-                   : "memory");
-    }
-  }
-  // dequantization scales are constants: load them before the wait too
-  const Epi& e = a.epi;
-  float msc[3];
-#pragma unroll
-  for (int sg = 0; sg < 3; ++sg) msc[sg] = sg < a.n_seg ? __ldg(e.scales + sg) : 0.0f;
-  GPROF(0)
-  pdl_wait();
-  // let the next kernel start its weight prefetch only now: earlier triggers
-  // let grids two launches ahead occupy SM slots and delay this grid's CTAs
-  pdl_launch_dependents();
-  GPROF(1)
-  if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 1] = gtimer();
+}
 
-  // ---------------- epilogue operands prefetch: lane m of warp w owns token m of
-  // channels w, w+16, w+32, w+48 (state h or residual)
-  float pre[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+// Epilogue operands: lane m of warp w owns token m of channels w, w+16, w+32,
+// w+48 (state h or residual).
+template <typename TY>
+__device__ __forceinline__ void gemv_pre(const GemvArgs& a, int unit, int warp, int lane,
+                                         float (&pre)[4]) {
+  const Epi& e = a.epi;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
+    pre[j] = 0.0f;
     const int i = warp + j * kGWarps, rr = unit * a.ch + i;
     if (lane < a.M && i < a.ch && rr < a.n_out) {
       if (e.kind == EPI_MLGRU) pre[j] = __ldcg(e.h + (int64_t)lane * e.n_out + rr);
@@ -204,7 +172,24 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
         pre[j] = ld_act_cg<TY>(static_cast<const TY*>(e.res) + (int64_t)lane * e.ldr + rr);
     }
   }
+}
 
+#define GPROF(i)                                                                   \
+  if (a.prof && tid == 0 && (i) < 8) a.prof[blockIdx.x * 8 + (i)] = clock64() - pt0; \
+  if (a.trace && tid == 0 && (i) >= 2) a.trace[blockIdx.x * 16 + 3 + (i)] = gtimer();
+
+// From the input rows to the stored outputs: fused RMSNorm + int8 quant of the
+// M rows (a2), wait for the weights (bar, parity), dot (a3) and epilogue.
+template <int MM, typename TX, typename TY>
+__device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint32_t* swd,
+                                         int8_t* qs, uint64_t* wbar, uint32_t parity,
+                                         const float (&msc)[3], const float (&pre)[4],
+                                         double (*red_d)[kGWarps], float (*red_m)[kGWarps],
+                                         long long pt0) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Epi& e = a.epi;
+  const int nkb = a.Kp >> 7;
+  const int SW = a.sw_stride;
   // ---------------- prologue: fused RMSNorm + int8 quant (a2) of the M rows.
   // x in registers (kGNVX 16-byte vectors per thread per row); sum(x^2) in
   // binary64 (C4), max|x|; one block barrier for the partials, every warp then
@@ -326,7 +311,7 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
   float deq[MM];
 #pragma unroll
   for (int m = 0; m < MM; ++m) deq[m] = amax[m] > 0.0f ? __fdiv_rn(amax[m], 127.0f) : 0.0f;
-  if (blockIdx.x == 0 && tid < a.M) {
+  if (unit == 0 && tid < a.M) {
 #pragma unroll
     for (int m = 0; m < MM; ++m)
       if (m == tid) {
@@ -335,10 +320,10 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
         if (a.taps.absmax) a.taps.absmax[m] = amax[m];
       }
   }
-  __syncthreads();       // q rows visible
-  mbar_wait(&wbar, 0);   // weights landed (long since, in a PDL chain)
+  __syncthreads();            // q rows visible
+  mbar_wait(wbar, parity);    // weights landed (long since, in a PDL chain)
   GPROF(6)
-  if (blockIdx.x == 0 && a.taps.q) {
+  if (unit == 0 && a.taps.q) {
     for (int m = 0; m < a.M; ++m)
       for (int k = tid * 16; k < a.Kp; k += kGThreads * 16)
         *reinterpret_cast<uint4*>(a.taps.q + (int64_t)m * a.taps.ldq + k) =
@@ -350,7 +335,6 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
   // (16 trits x 16 q bytes; consecutive lanes -> consecutive words, no bank
   // conflicts).  sum e*q - sum q = sum t*q: each lane starts from minus
   // the sum of the q bytes it will visit, so no per-row q sum is needed.
-  const uint32_t* swd = sw_words(g_smem);
   const int W = a.Kp >> 4;   // words per row
   int lq[MM];
 #pragma unroll
@@ -447,6 +431,59 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
     }
   }
   GPROF(9)
+}
+
+// One BitLinear per launch (PDL chain of launches).
+template <int MM, typename TX, typename TY>
+__global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
+  extern __shared__ __align__(128) uint8_t g_smem[];
+  int8_t* qs = reinterpret_cast<int8_t*>(g_smem + (size_t)a.n_seg * (a.Kp >> 7) * a.sw_stride * 4);  // [MM][Kp]
+  __shared__ double red_d[MM][kGWarps];
+  __shared__ float red_m[MM][kGWarps];
+  __shared__ __align__(8) uint64_t wbar;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int unit = blockIdx.x;
+  long long pt0 = 0;
+  if (a.prof) pt0 = clock64();
+  if (a.trace && tid == 0) {
+    a.trace[blockIdx.x * 16 + 0] = gtimer();
+    a.trace[blockIdx.x * 16 + 3] = clock64();
+  }
+  // packed weights -> smem with the TMA engine (bulk copies; the LSU pipe stays
+  // free for the running kernel's critical path)
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(&wbar, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    gemv_issue(a, unit, sw_words(g_smem), &wbar, lane, false);
+  }
+  // L2 prefetch of this CTA's share of a later launch's weights (HBM-resident
+  // stacks: the weight stream runs ahead of the dependency chain)
+  if (a.pf && tid == 32) {
+    const size_t chunk = ((a.pf_bytes + gridDim.x - 1) / gridDim.x + 15) & ~size_t(15);
+    const size_t off = chunk * blockIdx.x;
+    if (off < a.pf_bytes) {
+      const size_t n = a.pf_bytes - off < chunk ? a.pf_bytes - off : chunk;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf + off), "r"((uint32_t)n)
+                   : "memory");
+    }
+  }
+  // dequantization scales are constants: load them before the wait too
+  float msc[3];
+#pragma unroll
+  for (int sg = 0; sg < 3; ++sg) msc[sg] = sg < a.n_seg ? __ldg(a.epi.scales + sg) : 0.0f;
+  GPROF(0)
+  pdl_wait();
+  // let the next kernel start its weight prefetch only now: earlier triggers
+  // let grids two launches ahead occupy SM slots and delay this grid's CTAs
+  pdl_launch_dependents();
+  GPROF(1)
+  if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 1] = gtimer();
+  float pre[4];
+  gemv_pre<TY>(a, unit, warp, lane, pre);
+  gemv_run<MM, TX, TY>(a, unit, sw_words(g_smem), qs, &wbar, 0, msc, pre, red_d, red_m, pt0);
   if (a.trace) {
     __syncthreads();
     if (tid == 0) {
@@ -454,7 +491,183 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
       a.trace[blockIdx.x * 16 + 4] = clock64();
     }
   }
+}
 #undef GPROF
+
+// ---------------------------------------------------------------- f2: whole stack
+// One decode step through every block in ONE persistent launch:
+// one CTA per SM, all co-resident (cooperative launch); the 4 dependent
+// BitLinear phases of each block are separated by grid-wide barriers instead
+// of kernel boundaries.  While phase p runs, the TMA engine already copies
+// phase p+1's weight slice into the other shared-memory buffer and phase p+2's
+// slice is prefetched into L2, so the weight stream runs ahead of the chain.
+// The arithmetic of a phase is gemv_run's, bit for bit.
+struct StackPhase {
+  const void* x;          // input rows [M][K]
+  const void* res;        // residual [M][n_out] (RESID)
+  void* out;              // output [M][n_out]
+  float* h;               // MLGRU state [M][n_out]
+  const uint32_t* codes;  // packed weight group
+  const float* scales;    // [n_seg]
+  const float* gain;      // [K] or null
+  const float* bias;      // [n_seg*n_out] or null
+  int K, n_rows, n_out, ch, sw_stride, kind, n_seg, gate;
+  float eps;
+  int pad_;
+};
+constexpr int kStackMaxPhases = 128;   // 32 blocks per launch (kernel parameter space)
+constexpr size_t kStackTraceStride = 1024 * 16;   // = one k_gemv trace slot (kTraceCtas * 16)
+struct StackArgs {
+  int n_phase, M, buf_words, pad_;
+  unsigned* bar;   // grid barrier: [0] counter (zero at launch), [64 + cta] flags
+  int bar_mode;    // grid_wait
+  unsigned epoch;  // flags (mode 2): phase p of this launch is complete at epoch + p + 1
+  unsigned long long* trace;   // tern_trace_enable: one k_gemv-layout slot per phase
+  StackPhase ph[kStackMaxPhases];
+};
+
+__device__ __forceinline__ GemvArgs stack_args(const StackPhase& s, int M) {
+  GemvArgs a{};
+  a.x = s.x;
+  a.ldx = s.K;
+  a.K = s.K;
+  a.Kp = (s.K + kKAlign - 1) / kKAlign * kKAlign;
+  a.M = M;
+  a.gain = s.gain;
+  a.eps = s.eps;
+  a.codes = s.codes;
+  a.n_rows = s.n_rows;
+  a.n_out = s.n_out;
+  a.n_seg = s.n_seg;
+  a.ch = s.ch;
+  a.sw_stride = s.sw_stride;
+  a.inv_k = 1.0 / (double)s.K;
+  a.epi.kind = s.kind;
+  a.epi.n_out = s.n_out;
+  a.epi.n_seg = s.n_seg;
+  a.epi.scales = s.scales;
+  a.epi.bias = s.bias;
+  a.epi.out = s.out;
+  a.epi.ldo = s.n_out;
+  a.epi.res = s.res;
+  a.epi.ldr = s.n_out;
+  a.epi.h = s.h;
+  a.epi.gate = s.gate;
+  return a;
+}
+
+// Grid barrier between phases.  bar_mode (debug knob TERN_STACK_BAR):
+//  0: one counter, red.release add / ld.acquire polling by thread 0
+//  1: one counter, red.release add / relaxed polling + one acquire fence
+//  2: one flag word per CTA (st.release of the phase number), warp 0 polls all
+//     flags with relaxed loads, then one acquire fence
+__device__ __forceinline__ void grid_arrive(unsigned* bar, int mode, unsigned phase_done) {
+  if (mode == 2) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 64 + blockIdx.x), "r"(phase_done)
+                 : "memory");
+  } else {
+    if (mode == 0) __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+  }
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void watchdog(uint32_t& polls, unsigned long long& t0) {
+  if ((++polls & 1023u) == 0) {   // a lost arrival traps instead of hanging the GPU
+    const unsigned long long t = gtimer();
+    if (t0 == 0) t0 = t;
+    else if (t - t0 > 20000000000ull) __trap();
+  }
+}
+// mode 0/1: called by thread 0; mode 2: called by warp 0
+__device__ __forceinline__ void grid_wait(const unsigned* bar, int mode, unsigned target_count,
+                                          unsigned phase, int lane) {
+  uint32_t polls = 0;
+  unsigned long long t0 = 0;
+  if (mode == 0) {
+    unsigned v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if ((int)(v - target_count) >= 0) break;
+      watchdog(polls, t0);
+    }
+  } else if (mode == 1) {
+    while ((int)(ld_relaxed(bar) - target_count) < 0) watchdog(polls, t0);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  } else {
+    const unsigned G = gridDim.x;
+    while (true) {
+      bool ok = true;
+      for (unsigned i = lane; i < G; i += 32) ok &= (int)(ld_relaxed(bar + 64 + i) - phase) >= 0;
+      if (__all_sync(0xffffffffu, ok)) break;
+      watchdog(polls, t0);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+}
+
+template <int MM, typename TX, typename TY>
+__global__ void __launch_bounds__(kGThreads, 1) k_stack_decode(const __grid_constant__ StackArgs sa) {
+  extern __shared__ __align__(128) uint8_t g_smem[];
+  uint32_t* const wb0 = sw_words(g_smem);   // weight buffers: wb0 + (p & 1) * buf_words
+  int8_t* qs = reinterpret_cast<int8_t*>(g_smem + (size_t)sa.buf_words * 8);
+  __shared__ double red_d[MM][kGWarps];
+  __shared__ float red_m[MM][kGWarps];
+  __shared__ __align__(8) uint64_t wbar[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int unit = blockIdx.x;
+  const unsigned G = gridDim.x;
+  if (tid == 0) {
+    mbar_init(&wbar[0], 1);
+    mbar_init(&wbar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == 0) gemv_issue(stack_args(sa.ph[0], sa.M), unit, wb0, &wbar[0], lane, false);
+#pragma unroll 1
+  for (int p = 0; p < sa.n_phase; ++p) {
+    GemvArgs a = stack_args(sa.ph[p], sa.M);
+    if (sa.trace) {
+      a.trace = sa.trace + (size_t)p * kStackTraceStride;
+      if (tid == 0) {
+        a.trace[blockIdx.x * 16 + 0] = gtimer();
+        a.trace[blockIdx.x * 16 + 3] = clock64();
+      }
+    }
+    // weights run ahead: p+1 into the other buffer (free: phase p-1 ended with a
+    // block barrier), p+2 into L2
+    if (p + 1 < sa.n_phase && warp == 0) {
+      fence_proxy_async_smem();
+      gemv_issue(stack_args(sa.ph[p + 1], sa.M), unit, wb0 + ((p + 1) & 1) * sa.buf_words,
+                 &wbar[(p + 1) & 1], lane, false);
+    }
+    if (p + 2 < sa.n_phase && warp == 1)
+      gemv_issue(stack_args(sa.ph[p + 2], sa.M), unit, nullptr, nullptr, lane, true);
+    float msc[3];
+#pragma unroll
+    for (int sg = 0; sg < 3; ++sg) msc[sg] = sg < a.n_seg ? __ldg(a.epi.scales + sg) : 0.0f;
+    // h and the residual were written at least two phases ago: safe before the barrier
+    float pre[4];
+    gemv_pre<TY>(a, unit, warp, lane, pre);
+    if (p > 0) {
+      if (sa.bar_mode == 2 ? warp == 0 : tid == 0)
+        grid_wait(sa.bar, sa.bar_mode, (unsigned)p * G, sa.epoch + (unsigned)p, lane);
+      __syncthreads();
+    }
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 1] = gtimer();
+    if (unit * a.ch < a.n_out)
+      gemv_run<MM, TX, TY>(a, unit, wb0 + (p & 1) * sa.buf_words, qs, &wbar[p & 1],
+                           (uint32_t)(p >> 1) & 1u, msc, pre, red_d, red_m, 0);
+    __syncthreads();
+    if (a.trace && tid == 0) {
+      a.trace[blockIdx.x * 16 + 2] = gtimer();
+      a.trace[blockIdx.x * 16 + 4] = clock64();
+    }
+    if (p + 1 < sa.n_phase && tid == 0) grid_arrive(sa.bar, sa.bar_mode, sa.epoch + (unsigned)p + 1);
+  }
 }
 
 // ----------------------------------------------------------------- device trace (debug)
@@ -613,6 +826,120 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
   if (xb) return gemv_dispatch_m<__nv_bfloat16, float>(a, units, s);
   if (yb) return gemv_dispatch_m<float, __nv_bfloat16>(a, units, s);
   return gemv_dispatch_m<float, float>(a, units, s);
+}
+
+// ---------------------------------------------------------------- f2 host side
+template <int MM, typename T>
+static cudaError_t stack_launch(const StackArgs& sa, int grid, size_t smem, cudaStream_t s) {
+  auto kern = k_stack_decode<MM, T, T>;
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorNotSupported;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (grid barriers)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, sa);
+}
+
+bool stack_decode_plan(const StackPhaseDesc* ph, int n, int M, int xdt, size_t* smem_out) {
+  if (n <= 0 || M < 1 || M > kGemvMaxM) return false;
+  const int G = num_sms();
+  const int MMt = M <= 1 ? 1 : (M <= 2 ? 2 : 4);
+  size_t buf = 0;
+  int kp_max = 0;
+  for (int i = 0; i < n; ++i) {
+    const tern_weight& w = ph[i].w;
+    if (!gemv_supported(M, ph[i].K, xdt)) return false;
+    const int ch = (w.n_out + G - 1) / G;
+    if (ch > 4 * kGWarps) return false;   // epilogue: <= 4 channels per warp
+    const int Kp = (ph[i].K + kKAlign - 1) / kKAlign * kKAlign;
+    kp_max = Kp > kp_max ? Kp : kp_max;
+    const size_t b = (size_t)w.n_seg * (Kp / 128) * gemv_sw_stride(ch) * 4;
+    buf = b > buf ? b : buf;
+  }
+  const size_t smem = 2 * buf + (size_t)MMt * kp_max;
+  if (smem > 200 * 1024) return false;
+  if (smem_out) *smem_out = smem;
+  return true;
+}
+
+cudaError_t launch_stack_decode(const StackPhaseDesc* ph, int n, int M, int xdt, unsigned* bar,
+                                cudaStream_t s) {
+  size_t smem = 0;
+  if (!stack_decode_plan(ph, n, M, xdt, &smem)) return cudaErrorNotSupported;
+  const int G = num_sms();
+  for (int c0 = 0; c0 < n; c0 += kStackMaxPhases) {
+    const int cn = n - c0 < kStackMaxPhases ? n - c0 : kStackMaxPhases;
+    thread_local StackArgs sa;   // large: keep it off the host stack
+    sa = StackArgs{};
+    sa.n_phase = cn;
+    sa.M = M;
+    sa.bar = bar;
+    sa.trace = nullptr;
+    if (g_trace_on && G <= kTraceCtas && cn <= kTraceLaunches) {
+      if (g_trace_seq % kTraceLaunches + cn > kTraceLaunches) g_trace_seq += kTraceLaunches - g_trace_seq % kTraceLaunches;
+      const int slot = g_trace_seq % kTraceLaunches;
+      sa.trace = g_trace + (size_t)slot * kTraceCtas * 16;
+      for (int i = 0; i < cn; ++i) g_trace_units[slot + i] = G;
+      g_trace_seq += cn;
+    }
+    size_t buf = 0;
+    int kp_max = 0;
+    for (int i = 0; i < cn; ++i) {
+      const StackPhaseDesc& d = ph[c0 + i];
+      StackPhase& q = sa.ph[i];
+      q.x = d.x;
+      q.res = d.res;
+      q.out = d.out;
+      q.h = d.h;
+      q.codes = d.w.codes;
+      q.scales = d.w.scales;
+      q.gain = d.gain;
+      q.bias = d.bias;
+      q.K = d.K;
+      q.n_rows = d.w.n_rows;
+      q.n_out = d.w.n_out;
+      q.n_seg = d.w.n_seg;
+      q.ch = (d.w.n_out + G - 1) / G;
+      q.sw_stride = gemv_sw_stride(q.ch);
+      q.kind = d.kind;
+      q.gate = d.gate;
+      q.eps = d.eps;
+      const int Kp = (d.K + kKAlign - 1) / kKAlign * kKAlign;
+      kp_max = Kp > kp_max ? Kp : kp_max;
+      const size_t b = (size_t)q.n_seg * (Kp / 128) * q.sw_stride * 4;
+      buf = b > buf ? b : buf;
+    }
+    sa.buf_words = (int)(buf / 4);
+    const int MMt = M <= 1 ? 1 : (M <= 2 ? 2 : 4);
+    const size_t sm = 2 * buf + (size_t)MMt * kp_max;
+    static const int bar_mode = getenv("TERN_STACK_BAR") ? atoi(getenv("TERN_STACK_BAR")) : 1;
+    sa.bar_mode = bar_mode;
+    // flags: zeroed with the counter, so every launch counts phases from 0
+    sa.epoch = 0;
+    cudaError_t e = cudaMemsetAsync(bar, 0, (64 + (size_t)G) * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    const bool b16 = xdt == TERN_BF16;
+    if (MMt == 1) e = b16 ? stack_launch<1, __nv_bfloat16>(sa, G, sm, s) : stack_launch<1, float>(sa, G, sm, s);
+    else if (MMt == 2) e = b16 ? stack_launch<2, __nv_bfloat16>(sa, G, sm, s) : stack_launch<2, float>(sa, G, sm, s);
+    else e = b16 ? stack_launch<4, __nv_bfloat16>(sa, G, sm, s) : stack_launch<4, float>(sa, G, sm, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace tern

@@ -195,10 +195,34 @@ class Stack:
             cur = nxt
         return cur
 
+    def _stack_struct(self):
+        if getattr(self, "_blk_arr", None) is None:
+            self._blk_arr = (L.tern_block * len(self.blocks))(*[b.struct for b in self.blocks])
+        return self._blk_arr
+
     def decode(self, x: torch.Tensor, states: list, out: torch.Tensor | None = None,
-               bufs=None) -> torch.Tensor:
-        """One decode step: x [B][d] -> y [B][d] through all blocks."""
+               bufs=None, persistent: bool | None = None) -> torch.Tensor:
+        """One decode step: x [B][d] -> y [B][d] through all blocks.
+
+        persistent (default: self.persistent_decode, False): the whole step in
+        one persistent launch (tern.h stack_decode) when the library supports
+        the shape; otherwise (or False) one block_decode call per block.  The
+        results are identical.  The per-block PDL launch chain is the default
+        because it measured faster on B200."""
         B, d = x.shape
+        if persistent is None:
+            persistent = getattr(self, "persistent_decode", False)
+        if persistent and self.gather is None and B > 0:
+            arr = self._stack_struct()
+            need = L.tern_stack_decode_workspace(arr, B, self.dtype)
+            if getattr(self, "_sws", None) is None or self._sws.numel() < need:
+                self._sws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            y = out if out is not None else torch.empty_like(x)
+            st = L.stack_decode(arr, x, y, states, self._sws, allow_unsupported=True)
+            if st == L.TERN_OK:
+                self.last_decode_path = "persistent"
+                return y
+        self.last_decode_path = "per_block"
         ws = self.workspace(B, 1)
         if bufs is None:
             bufs = (torch.empty_like(x), torch.empty_like(x))

@@ -356,20 +356,28 @@ def test_fused_fcg_scan_equals_unfused(L, M, dtype, B, T, d, gate):
 
 
 # ------------------------------------------------------------------------ batched decode (split-K)
-@pytest.mark.parametrize("cfg_name,B,T,n_dec", [("c2", 32, 3, 2), ("c4", 16, 2, 2)])
-def test_batched_decode_split_k_parity(L, M, cfg_name, B, T, n_dec):
-    """Decode batches above the GEMV limit run quant + a split-K tcgen05 GEMM (int32 slices
-    summed exactly) + the split-K epilogue; short prefills take the same path.  Free-running
-    against the oracle, bit-exact."""
+@pytest.mark.parametrize("cfg_name,B,T,n_dec", [("c2", 32, 3, 2), ("c4", 16, 2, 2), ("c3", 64, 1, 2),
+                                               ("c4", 128, 1, 2)])
+@pytest.mark.parametrize("fin", [False, True])
+def test_batched_decode_split_k_parity(L, M, cfg_name, B, T, n_dec, fin):
+    """Decode batches above the GEMV limit: per BitLinear a split-K tcgen05 GEMM (int32
+    slices) and a row-wise finalize that applies the epilogue and quantizes the row for the
+    next BitLinear (k_fin.cu); short prefills take quant + GEMM + split-K epilogue.
+    Free-running against the oracle, bit-exact."""
     cfg = synth.CONFIGS[cfg_name]
     st, ob = _blocks(cfg, M, 1, 0, gen_device="cuda")
     x = synth.hidden((B, T + n_dec, cfg.d), synth.generator(cfg.seed + 77), cfg.dtype)
     xd = x.cuda()
     states = st.new_state(B)
-    ys = [st.prefill(xd[:, :T].contiguous(), states)]
-    for t in range(T, T + n_dec):
-        ys.append(st.decode(xd[:, t].contiguous(), states).unsqueeze(1))
-    torch.cuda.synchronize()
+    old = L.tern_get_batched_fin()
+    try:
+        L.tern_set_batched_fin(fin)
+        ys = [st.prefill(xd[:, :T].contiguous(), states)]
+        for t in range(T, T + n_dec):
+            ys.append(st.decode(xd[:, t].contiguous(), states).unsqueeze(1))
+        torch.cuda.synchronize()
+    finally:
+        L.tern_set_batched_fin(old)
     yg = f32np(torch.cat(ys, 1))
     bf = cfg.dtype == "bf16"
     H = [np.zeros((B, cfg.d), np.float32)]

@@ -16,10 +16,13 @@ from paper_2406_02528_b200 import model, synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--blocks", type=int, default=4)
+ap.add_argument("--per-block", action="store_true",
+                help="trace the per-block launch chain instead of the persistent kernel")
 args = ap.parse_args()
 L.load()
 cfg = synth.CONFIGS[args.config]
 st = model.Stack.random(cfg, device="cuda", gen_device="cuda", n_blocks=args.blocks)
+st.persistent_decode = not args.per_block
 states = st.new_state(cfg.decode_B)
 L.tern_trace_enable(True)
 g, xin, yout = st.capture_decode(cfg.decode_B, states)
@@ -33,6 +36,7 @@ for _ in range(20):
     g.replay()
 e1.record()
 torch.cuda.synchronize()
+print(f"path: {st.last_decode_path}")
 print(f"graph replay: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us per step, "
       f"{4 * args.blocks} launches -> {e0.elapsed_time(e1) / 20 * 1e3 / (4 * args.blocks):.2f} us/launch")
 recs = L.tern_trace_collect()
