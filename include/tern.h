@@ -325,16 +325,20 @@ typedef struct {
 void tern_profile_enable(int32_t on);
 int32_t tern_profile_collect(tern_prof_rec* out, int32_t max);
 
-/* Device-side timeline of decode-GEMV launches (debug; works inside CUDA
- * graphs): while enabled, each GEMV launch made on the host gets a trace slot
- * (up to 1024 launches, then the slots wrap) in which every CTA records the
- * %globaltimer (ns) at its start, after griddepcontrol.wait, and at its end,
- * plus its SM id.  tern_trace_collect synchronises the device and copies up
- * to max_launches records to out (host), each 1 + 1024*16 uint64: [0] = CTA
- * count, then per CTA {start, released, end, clock64 at start, clock64 at
- * end, up to 11 intermediate phase marks}; returns the number of
- * launches recorded (out == NULL just counts).  Replaying a captured graph
- * overwrites the slots assigned at capture time. */
+/* Device-side timeline of kernel launches (debug; works inside CUDA graphs):
+ * while enabled, each launch made on the host gets a trace slot (up to 1024
+ * launches, then the slots wrap) in which thread 0 of every CTA (the first
+ * 1024) records the %globaltimer (ns) at its start, when its dependency wait
+ * (griddepcontrol.wait / grid barrier) released, and at its end; decode GEMV
+ * CTAs add their SM id, clocks and intermediate phase marks.
+ * tern_trace_collect synchronises the device and copies up to max_launches
+ * records to out (host), each 1 + 1024*16 uint64: [0] = CTA count | (kernel
+ * << 20) (tern_kernel_id; the split-K epilogue is TERN_K_GEMM + 16), then per
+ * CTA {start, released, end, ...}; returns the number of launches recorded
+ * (out == NULL just counts).  Replaying a captured graph overwrites the slots
+ * assigned at capture time.  Only the decode GEMV records in the default
+ * build; the other kernels' marks are compiled into the debug variant
+ * libtern_trace.so (build.py --trace). */
 void tern_trace_enable(int32_t on);
 int32_t tern_trace_collect(uint64_t* out, int32_t max_launches);
 

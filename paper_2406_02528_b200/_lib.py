@@ -304,8 +304,9 @@ def tern_trace_enable(on: bool):
     load().tern_trace_enable(1 if on else 0)
 
 
-def tern_trace_collect():
-    """-> list of (units, array[units][16]: start, released, end, clk0, clk1, phase marks...)."""
+def tern_trace_collect(with_kind=False):
+    """-> list of (ctas, array[ctas][16]: start, released, end, ...), or with_kind
+    (kind, ctas, array) with kind a tern_kernel_id (+16: split-K epilogue)."""
     import numpy as np
     Lb = load()
     n = int(Lb.tern_trace_collect(None, 0))
@@ -315,8 +316,9 @@ def tern_trace_collect():
     out = []
     for i in range(n):
         r = buf[i * rec:(i + 1) * rec]
-        u = int(r[0])
-        out.append((u, r[1:1 + 16 * u].reshape(u, 16).astype(np.int64)))
+        u, kind = int(r[0]) & 0xFFFFF, int(r[0]) >> 20
+        arr = r[1:1 + 16 * u].reshape(u, 16).astype(np.int64)
+        out.append((kind, u, arr) if with_kind else (u, arr))
     return out
 
 

@@ -26,13 +26,13 @@ def _mtime(p):
     return os.path.getmtime(p) if os.path.exists(p) else 0.0
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+def _compile(src: str, verbose: bool, obj_dir: str = OBJ, extra=()) -> str:
+    obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
     dep = max([_mtime(os.path.join(CSRC, src))] + [_mtime(os.path.join(CSRC, h)) for h in HEADERS]
               + [_mtime(os.path.join(ROOT, "include", "tern.h"))])
     if _mtime(obj) >= dep:
         return obj
-    cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -43,25 +43,30 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace: the debug variant libtern_trace.so with the device timeline marks
+    of every kernel compiled in (-DTERN_TRACE; tools/timeline.py)."""
+    obj_dir = OBJ + "_trace" if trace else OBJ
+    lib = LIB.replace("libtern.so", "libtern_trace.so") if trace else LIB
+    extra = ("-DTERN_TRACE",) if trace else ()
+    os.makedirs(obj_dir, exist_ok=True)
     if force:
         for s in SOURCES:
-            o = os.path.join(OBJ, s.replace(".cu", ".o"))
+            o = os.path.join(obj_dir, s.replace(".cu", ".o"))
             if os.path.exists(o):
                 os.remove(o)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    if force or _mtime(LIB) < max(_mtime(o) for o in objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+        objs = list(ex.map(lambda s: _compile(s, verbose, obj_dir, extra), SOURCES))
+    if force or _mtime(lib) < max(_mtime(o) for o in objs):
+        tmp = lib + f".tmp{os.getpid()}"
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
                "-lcuda"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv))

@@ -219,28 +219,73 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  // "memory": keeps the read in program order with barriers and memory ops
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory");
+  return t;
+}
+// Device timeline (tern_trace_enable): thread 0 of CTA b < 1024 records the
+// %globaltimer at mark 0 (start), 1 (dependency wait released), 2 (end).
+// Compiled in only with -DTERN_TRACE (python -m paper_2406_02528_b200.build
+// --trace): the marks cost ~2% of a prefill step even when disabled.
+#ifdef TERN_TRACE
+#define TERN_TRACE_ON 1
+__device__ __forceinline__ void trace_mark(unsigned long long* tr, int mark) {
+  if (tr != nullptr && threadIdx.x == 0 && blockIdx.x < 1024) tr[blockIdx.x * 16 + mark] = gtimer();
+}
+#else
+#define TERN_TRACE_ON 0
+__device__ __forceinline__ void trace_mark(unsigned long long*, int) {}
+#endif
 // Adds to the expected transaction bytes of the current phase without arriving.
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
 }
+// Polling wait without a suspend-time hint (short waits on the critical path).
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
 // Waits for the phase with the given parity.  try_wait carries a suspend-time
 // hint, so a waiting warp sleeps until the phase completes (or the hint
 // elapses) instead of spinning on the issue slots its CTA's busy warps need.
 // A watchdog turns a lost arrival (a pipeline bug) into a trap after ~20 s of
 // %globaltimer instead of a silent hang.
+#ifndef TERN_MBAR_HINT
+#define TERN_MBAR_HINT 0x989680   // suspend-time hint (ns); 0: plain try_wait polling
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0, polls = 0;
   unsigned long long t0 = 0;
   do {
+#if TERN_MBAR_HINT
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, P1;\n\t}"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "r"(smem_u32(bar)), "r"(parity), "r"((uint32_t)TERN_MBAR_HINT)
         : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+#endif
     if (!done && (++polls & 1023u) == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -101,6 +101,9 @@ bool stack_decode_plan(const StackPhaseDesc* ph, int n, int M, int xdt, size_t* 
 // cudaErrorNotSupported when the plan does not fit (stack_decode_plan false)
 cudaError_t launch_stack_decode(const StackPhaseDesc* ph, int n, int M, int xdt, unsigned* bar,
                                 cudaStream_t s);
+// debug timeline (globaltimer per CTA, tern_trace_enable): a slot for one launch
+// of `ctas` CTAs of kernel `kind` (tern_kernel_id), or nullptr when tracing is off
+unsigned long long* trace_slot(int kind, int ctas);
 // debug timeline of GEMV launches (globaltimer per CTA), see tern_trace_enable
 void gemv_trace_enable(int on);
 int gemv_trace_collect(unsigned long long* out, int max_launches);

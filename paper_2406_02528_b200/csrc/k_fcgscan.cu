@@ -49,6 +49,7 @@ struct FcgScanArgs {
   void* oprime;          // [B*T][d]
   int gate;
   unsigned long long* prof;  // debug (TERN_FS_PROF): [grid][8] cycles per wait site / phase
+  unsigned long long* trace;   // tern_trace_enable timeline
 };
 
 // debug: add the cycles since t0 to counter `site` of this CTA
@@ -65,6 +66,7 @@ struct FcgScanSmem {
   uint64_t full[kFS], empty[kFS], tfull[2], tempty[2];
   uint64_t ready[4][2];              // both gate warps of (quad, half) wrote their f, b, g^
   uint64_t hdone[4][2];              // carry warp (half) finished the quad's rows
+  uint64_t tmem_free;                // every gate warp is done with TMEM
   uint32_t tmem_slot;
 };
 
@@ -83,6 +85,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
   const int groups = a.d / kFCW;
   const int chains = a.B * groups;
   const int nt = (a.T + kFBM - 1) / kFBM;   // M-tiles per chain
+  trace_mark(a.trace, 0);
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
@@ -100,8 +103,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
         mbar_init(&sm.ready[q][h], 2);   // the two 16-channel gate warps of the half
         mbar_init(&sm.hdone[q][h], 1);
       }
+    mbar_init(&sm.tmem_free, kFEpiWarps);
     fence_barrier_init();
   }
+  __syncwarp();
   if (warp == 1) tmem_alloc<512>(&sm.tmem_slot);
   static_assert(kFThreads <= 1024, "block size");
   tc_fence_before();
@@ -110,6 +115,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
   const uint32_t tmem_base = sm.tmem_slot;
   pdl_wait();                 // q, deq, qsum and h come from earlier kernels
   pdl_launch_dependents();
+  trace_mark(a.trace, 1);
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -307,11 +313,19 @@ __global__ void __launch_bounds__(kFThreads, 1)
       a.h[(int64_t)b * a.d + c0 + cc] = hc;
     }
   }
-  tc_fence_before();
-  __syncthreads();
+  // TMEM release after the gate warps' last loads: an mbarrier, not a CTA-wide
+  // bar.sync after the divergent producer / MMA roles (see k_gemm.cu)
+  if (warp >= 2 && warp < 2 + kFEpiWarps) {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.tmem_free);
+  }
   if (warp == 1) {
+    __syncwarp();
+    mbar_wait(&sm.tmem_free, 0);
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);
+    if (TERN_TRACE_ON && a.trace && lane == 0 && blockIdx.x < 1024) a.trace[blockIdx.x * 16 + 2] = gtimer();
   }
 }
 
@@ -337,6 +351,7 @@ static cudaError_t fcgscan_go(const CUtensorMap& ta, const CUtensorMap& tb, cons
   static unsigned long long* dprof = nullptr;
   static const bool prof_on = getenv("TERN_FS_PROF") != nullptr;
   FcgScanArgs aa = a;
+  aa.trace = trace_slot(TERN_K_FCGSCAN, grid);
   if (prof_on) {   // debug only: printed after a synchronous run
     if (!dprof) cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * 1024);
     cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * 8 * 1024, s);

@@ -32,6 +32,7 @@ struct FinArgs {
   int nldq, nkp;
   float* ndeq;
   int32_t* nqsum;
+  unsigned long long* trace;
 };
 
 // NP channel pairs per thread (pair p = tid + j*512 holds channels 2p, 2p+1)
@@ -47,8 +48,10 @@ __global__ void __launch_bounds__(kFinThreads, 1) k_fin(const FinArgs a) {
   // constants before the dependency wait
   const float sc0 = __ldg(e.scales), sc1 = nseg > 1 ? __ldg(e.scales + 1) : 0.0f;
   const float sc2 = nseg > 2 ? __ldg(e.scales + 2) : 0.0f;
+  trace_mark(a.trace, 0);
   pdl_wait();   // the GEMM's partials
   pdl_launch_dependents();
+  trace_mark(a.trace, 1);
   const float dq = __ldg(a.deq + m);
   const int qs = __ldg(a.qsum + m);
   const float s0 = __fmul_rn(dq, sc0), s1 = __fmul_rn(dq, sc1), s2 = __fmul_rn(dq, sc2);
@@ -153,7 +156,10 @@ __global__ void __launch_bounds__(kFinThreads, 1) k_fin(const FinArgs a) {
     ss1 = fma(d1, d1, ss1);
     ym = fmaxf(ym, fmaxf(fabsf(o0), fabsf(o1)));
   }
-  if (a.nq == nullptr) return;
+  if (a.nq == nullptr) {
+    trace_mark(a.trace, 2);
+    return;
+  }
   // ---------------- the next BitLinear's RMSNorm + absmax int8 quant of this row
   double ss = ss0 + ss1;
 #pragma unroll
@@ -224,6 +230,7 @@ __global__ void __launch_bounds__(kFinThreads, 1) k_fin(const FinArgs a) {
     a.nqsum[m] = t;
     a.ndeq[m] = amax > 0.0f ? __fdiv_rn(amax, 127.0f) : 0.0f;
   }
+  trace_mark(a.trace, 2);
 }
 
 template <typename TY>
@@ -260,6 +267,7 @@ cudaError_t launch_fin(const int32_t* part, int ks, int M, int n_rows, const flo
   a.nkp = (e.n_out + kKAlign - 1) / kKAlign * kKAlign;
   a.ndeq = ndeq;
   a.nqsum = nqsum;
+  a.trace = trace_slot(TERN_K_FIN, M);
   return ydt == TERN_BF16 ? fin_go<__nv_bfloat16>(a, s) : fin_go<float>(a, s);
 }
 

@@ -57,6 +57,9 @@ struct GemmArgs {
   const int32_t* qsum;
   Epi epi;
   unsigned long long* prof;  // debug (TERN_GEMM_PROF): [grid][8] wait cycles per site
+#ifdef TERN_TRACE
+  unsigned long long* trace; // tern_trace_enable timeline (trace build only)
+#endif
 };
 
 // mbar_wait that (in the TERN_GEMM_PROF debug mode) adds the cycles it blocked
@@ -188,6 +191,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 44);
 
   const long long t_start = clock64();
+#ifdef TERN_TRACE
+  trace_mark(a.trace, 0);
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = a.num_kb;
   const int total = a.n_tiles * a.m_tiles * a.ksplit;
@@ -252,6 +258,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       pdl_wait();
+#ifdef TERN_TRACE
+      trace_mark(a.trace, 1);
+#endif
       uint32_t g = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int tile = t / a.ksplit, sp = t % a.ksplit;
@@ -494,6 +503,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+#ifdef TERN_TRACE
+    if (lane == 0 && a.trace && blockIdx.x < 1024) a.trace[blockIdx.x * 16 + 2] = gtimer();
+#endif
   }
   if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 8 + 7] = clock64() - t_start;
 }
@@ -554,6 +566,9 @@ static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, con
   static unsigned long long* dprof = nullptr;
   static const bool prof_on = getenv("TERN_GEMM_PROF") != nullptr;
   GemmArgs aa = a;
+#ifdef TERN_TRACE
+  aa.trace = trace_slot(TERN_K_GEMM, grid);
+#endif
   if (prof_on) {  // debug only: per-site wait cycles, printed after a synchronous run
     if (!dprof) cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * 1024);
     cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * 8 * 1024, s);
@@ -593,9 +608,11 @@ static cudaError_t gemm_dispatch_bn(int BN, const CUtensorMap& ta, const CUtenso
 template <typename TY>
 __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M, int n_rows,
                              const float* __restrict__ deq, const int32_t* __restrict__ qsum,
-                             const Epi e) {
+                             const Epi e, unsigned long long* trace) {
+  trace_mark(trace, 0);
   pdl_wait();                 // the GEMM's partial sums
   pdl_launch_dependents();
+  trace_mark(trace, 1);
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool chan = e.kind == EPI_SWIGLU || e.kind == EPI_MLGRU;   // per logical channel
   const int ncol = chan ? e.n_out : (e.kind == EPI_FCG ? n_rows : e.n_out);
@@ -764,11 +781,12 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
     const int64_t n = (int64_t)M * ((ncol + 1) / 2);
     const unsigned grid = (unsigned)((n + 255) / 256);
     const int32_t* pc = part;
+    unsigned long long* tr = trace_slot(TERN_K_GEMM + 16, (int)grid);
     if (yb)
       return launch_pdl(k_splitk_epi<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, pc, a.ksplit, M,
-                        w.n_rows, deq, qsum, epi);
+                        w.n_rows, deq, qsum, epi, tr);
     return launch_pdl(k_splitk_epi<float>, dim3(grid), dim3(256), 0, s, pc, a.ksplit, M, w.n_rows,
-                      deq, qsum, epi);
+                      deq, qsum, epi, tr);
   }
   if (pre)
     return yb ? gemm_dispatch_bn<true, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)

@@ -50,11 +50,6 @@ struct GemvArgs {
   unsigned long long* trace; // tern_trace_enable: [grid][8] globaltimer (start, released, end, smid, phases)
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 __device__ __forceinline__ unsigned smid() {
   unsigned r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -688,6 +683,14 @@ void gemv_trace_enable(int on) {
   g_trace_seq = 0;
 }
 
+unsigned long long* trace_slot(int kind, int ctas) {
+  if (!g_trace_on) return nullptr;
+  const int slot = g_trace_seq % kTraceLaunches;
+  g_trace_units[slot] = (ctas < kTraceCtas ? ctas : kTraceCtas) | (kind << 20);
+  ++g_trace_seq;
+  return g_trace + (size_t)slot * kTraceCtas * 16;
+}
+
 int gemv_trace_collect(unsigned long long* out, int max_launches) {
   const int n = g_trace_seq < kTraceLaunches ? g_trace_seq : kTraceLaunches;
   if (!out || !g_trace) return n;
@@ -735,7 +738,7 @@ static cudaError_t gemv_launch(const GemvArgs& a, int units, cudaStream_t s) {
   if (g_trace_on && units <= kTraceCtas) {
     const int slot = g_trace_seq % kTraceLaunches;
     aa.trace = g_trace + (size_t)slot * kTraceCtas * 16;
-    g_trace_units[slot] = units;
+    g_trace_units[slot] = units | (TERN_K_GEMV << 20);
     ++g_trace_seq;
   }
   if (prof_on) {  // debug only: per-phase clocks, printed after a synchronous run
@@ -894,7 +897,7 @@ cudaError_t launch_stack_decode(const StackPhaseDesc* ph, int n, int M, int xdt,
       if (g_trace_seq % kTraceLaunches + cn > kTraceLaunches) g_trace_seq += kTraceLaunches - g_trace_seq % kTraceLaunches;
       const int slot = g_trace_seq % kTraceLaunches;
       sa.trace = g_trace + (size_t)slot * kTraceCtas * 16;
-      for (int i = 0; i < cn; ++i) g_trace_units[slot + i] = G;
+      for (int i = 0; i < cn; ++i) g_trace_units[slot + i] = G | (TERN_K_STACK << 20);
       g_trace_seq += cn;
     }
     size_t buf = 0;

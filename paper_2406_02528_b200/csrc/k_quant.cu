@@ -52,7 +52,9 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
                                                      float* __restrict__ deq,
                                                      int32_t* __restrict__ qsum,
                                                      float* __restrict__ inv_rms,
-                                                     float* __restrict__ absmax) {
+                                                     float* __restrict__ absmax,
+                                                     unsigned long long* trace) {
+  trace_mark(trace, 0);
   constexpr int VE = QVec<TX>::N;
   constexpr int WPR = TPR / 32;                 // warps per row
   constexpr int RPC = kQThreads / TPR;          // rows per CTA
@@ -67,6 +69,7 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
   const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)(rv ? row : 0) * ldx);
   pdl_wait();                 // x is the previous kernel's output
   pdl_launch_dependents();
+  trace_mark(trace, 1);
 
   uint4 xv[NV];
 #pragma unroll
@@ -186,6 +189,7 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
     if (inv_rms) inv_rms[row] = r;
     if (absmax) absmax[row] = amax;
   }
+  trace_mark(trace, 2);
 }
 
 template <typename TX, int TPR, int NV>
@@ -199,7 +203,7 @@ static void quant_go(const TX* x, int m, int k, int ldx, const float* gain, floa
   auto kern = gain ? k_quant<TX, TPR, NV, true, false>
                    : (full ? k_quant<TX, TPR, NV, false, true> : k_quant<TX, TPR, NV, false, false>);
   launch_pdl(kern, dim3(grid), dim3(kQThreads), 0, s, x, m, k, ldx, gain, eps, inv_k, q, ldq, deq,
-             qsum, inv_rms, absmax);
+             qsum, inv_rms, absmax, trace_slot(TERN_K_QUANT, grid));
 }
 
 template <typename TX, int TPR>

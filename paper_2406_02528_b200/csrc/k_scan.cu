@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
     }
     fence_barrier_init();
   }
+  __syncwarp();
   __syncthreads();
   pdl_wait();                 // f^c^g^ and h come from earlier kernels
   pdl_launch_dependents();

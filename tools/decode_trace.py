@@ -48,6 +48,7 @@ t0 = min(int(r[:, 0].min()) for _, r in recs)
 print(f"{'launch':>8} {'ctas':>5} {'start_min':>9} {'start_max':>9} {'rel_min':>8} {'rel_max':>8} "
       f"{'end_max':>8} {'post_wait':>9} {'gap_after_prev':>14} | mean ns after release: x warpred bar r quant dot0 red0 end")
 for i, (u, r) in enumerate(recs):
+    u &= 0xFFFFF
     s0, s1 = int(r[:, 0].min()) - t0, int(r[:, 0].max()) - t0
     w0, w1 = int(r[:, 1].min()) - t0, int(r[:, 1].max()) - t0
     e = int(r[:, 2].max()) - t0
