@@ -76,6 +76,9 @@ def lib():
             L.orc_packed_row.argtypes = [C.c_int64] * 4
             L.orc_unpack_segment.argtypes = [u32p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
                                              C.c_int, i8p]
+            L.orc_set_norm_mode.argtypes = [C.c_int]
+            L.orc_set_norm_mode.restype = None
+            L.orc_get_norm_mode.restype = C.c_int
             L.orc_rmsnorm.restype = C.c_float
             L.orc_rmsnorm.argtypes = [f32p, C.c_int, C.c_void_p, C.c_float, f32p]
             L.orc_act_quant.restype = C.c_float
@@ -196,6 +199,23 @@ def unpack_segment(codes, n, k, n_seg=1, s=0, seg_rows=64):
 
 
 # ---------------------------------------------------------------- a2
+class norm_mode:
+    """Context manager: the oracle's norm variant, 0 = RMSNorm (C1), 1 = the
+    centred form of Alg. 1 (reading C22)."""
+
+    def __init__(self, mode: int):
+        self.mode = int(mode)
+
+    def __enter__(self):
+        self.old = lib().orc_get_norm_mode()
+        lib().orc_set_norm_mode(self.mode)
+        return self
+
+    def __exit__(self, *exc):
+        lib().orc_set_norm_mode(self.old)
+        return False
+
+
 def rmsnorm(x, gain=None, eps=1e-6):
     x = _f32(x)
     y = np.empty_like(x)

@@ -202,10 +202,42 @@ int orc_unpack_segment(const uint32_t* codes, int64_t n_rows, int n, int k, int 
 /*     activation_quant (Alg. 1, per token C2)                     */
 /* ------------------------------------------------------------------------ */
 
+/* Norm variant: 0 = RMSNorm as read in C1 (default);
+ * 1 = the centred form of Alg. 1 rms_norm_fwd, reading C22.
+ * Process-wide setting of the oracle (test infrastructure). */
+static int g_norm_mode = 0;
+void orc_set_norm_mode(int mode) { g_norm_mode = mode; }
+int orc_get_norm_mode(void) { return g_norm_mode; }
+
 /* RMSNorm(x; w, eps) = x / sqrt(eps + mean(x^2)) * w   (C1).
  * r = 1/sqrt(mean(x^2) + eps) computed in binary64, rounded to binary32;
- * y_j = (x_j * r) * w_j  in binary32.  gain == NULL means w = 1. */
+ * y_j = (x_j * r) * w_j  in binary32.  gain == NULL means w = 1.
+ *
+ * Centred form (Alg. 1: mu, sigma^2 = mean(X), variance(X);
+ * r = 1/sqrt(sigma^2 + eps); Y = r (X - mu)), reading C22:
+ *   mu      = (float)( sum_j x_j / K )              sum in binary64, index order
+ *   sigma^2 = sum_j (x_j - mu)^2 / K                binary64 (x_j - mu is exact there)
+ *   r       = (float)( 1 / sqrt(sigma^2 + eps) )    binary64, rounded once
+ *   y_j     = ((x_j - mu) * r) * w_j                every step binary32 */
 float orc_rmsnorm(const float* x, int K, const float* gain, float eps, float* y) {
+  if (g_norm_mode == 1) {
+    double sx = 0.0;
+    for (int j = 0; j < K; ++j) sx += (double)x[j];
+    const float mu = (float)(sx / (double)K);
+    double sv = 0.0;
+    for (int j = 0; j < K; ++j) {
+      const double dj = (double)x[j] - (double)mu;
+      sv += dj * dj;
+    }
+    const double var = sv / (double)K;
+    float r = (float)(1.0 / sqrt(var + (double)eps));
+    for (int j = 0; j < K; ++j) {
+      float v = (x[j] - mu) * r;
+      if (gain) v = v * gain[j];
+      y[j] = v;
+    }
+    return r;
+  }
   double ss = 0.0;
   for (int j = 0; j < K; ++j) ss += (double)x[j] * (double)x[j];
   double ms = ss / (double)K;

@@ -210,6 +210,70 @@ def test_double_rmsnorm_identity():
         assert np.allclose(zc, zc2, rtol=1e-12)
 
 
+# ------------------------------------------------------------------ centred norm (Alg. 1, f4(i), C22)
+def test_centred_norm_worked_example():
+    """Alg. 1 rms_norm_fwd on x = [1, 2, 3, 4]: mu = 2.5 and
+    sigma^2 = 1.25 exactly, Y = r (X - mu) = r [-1.5, -0.5, 0.5, 1.5]; the
+    absmax quantizer then gives 127/1.5 * [-1.5, -0.5, 0.5, 1.5]
+    = [-127, -42.33, 42.33, 127] -> [-127, -42, 42, 127]."""
+    x = f32([1, 2, 3, 4])
+    with O.norm_mode(1):
+        y, r = O.rmsnorm(x, eps=1e-6)
+        q, deq, rr, a = O.quant_rows(x[None])
+    assert float(r) == float(np.float32(1 / math.sqrt(1.25 + 1e-6)))
+    assert np.array_equal(y, f32([-1.5, -0.5, 0.5, 1.5]) * np.float32(r))
+    assert q[0].tolist() == [-127, -42, 42, 127]
+    assert a[0] == np.float32(np.float32(1.5) * np.float32(r))
+    # the uncentred reading gives different codes on the same row
+    assert O.quant_rows(x[None])[0][0].tolist() == [32, 64, 95, 127]
+
+
+def test_centred_norm_shift_invariance_exact():
+    """Adding a power of two c to integer rows shifts mu by exactly c, so every
+    x_j - mu (and hence y, q, deq, r) is bit-identical: pins the subtraction
+    of the mean (dropped or wrong-signed mu fails)."""
+    for K in (8, 64, 1024):
+        x = rng.integers(-50, 50, K).astype(np.float32)
+        with O.norm_mode(1):
+            q0, d0, r0, a0 = O.quant_rows(x[None])
+            q1, d1, r1, a1 = O.quant_rows((x + np.float32(64))[None])
+        assert np.array_equal(q0, q1) and d0[0] == d1[0] and r0[0] == r1[0] and a0[0] == a1[0]
+
+
+def test_centred_norm_zero_mean_row_equals_rmsnorm():
+    """A row of +-pairs has sum exactly 0, so mu = 0 and the variance equals
+    the mean square: the centred and uncentred forms agree bit for bit."""
+    h = rng.standard_normal(256).astype(np.float32)
+    x = np.concatenate([h, -h])
+    rng.shuffle(x)
+    with O.norm_mode(1):
+        yc, rc = O.rmsnorm(x, eps=1e-6)
+    yu, ru = O.rmsnorm(x, eps=1e-6)
+    assert rc == ru and np.array_equal(yc, yu)
+
+
+def test_centred_norm_moments_closed_form():
+    """mean(y) ~ 0 and mean(y^2) (sigma^2 + eps) / sigma^2 = 1 (unit gain)."""
+    for K in (7, 256, 1000):
+        x = (rng.standard_normal(K) * 2 + 5).astype(np.float32)
+        with O.norm_mode(1):
+            y, r = O.rmsnorm(x, eps=1e-6)
+        x64 = x.astype(np.float64)
+        var = np.var(x64)
+        y64 = y.astype(np.float64)
+        assert abs(np.mean(y64)) < 1e-5
+        assert abs(np.mean(y64 ** 2) * (var + 1e-6) / var - 1) < 1e-5
+        assert abs(float(r) - 1 / math.sqrt(var + 1e-6)) <= 2e-7 / math.sqrt(var)
+
+
+def test_centred_norm_constant_row_is_degenerate():
+    """A constant row has X - mu = 0: q = 0 and deq = 0 (C7)."""
+    x = np.full((1, 64), 3.25, np.float32)
+    with O.norm_mode(1):
+        q, deq, r, a = O.quant_rows(x)
+    assert np.all(q == 0) and deq[0] == 0 and a[0] == 0
+
+
 def test_quant_rows_per_token():
     X = rng.standard_normal((5, 40)).astype(np.float32)
     X[2] = 0
