@@ -61,6 +61,11 @@ typedef enum { TERN_F32 = 0, TERN_BF16 = 1 } tern_dtype;
 /* MLGRU output gate (C8): o' = g * sigma(h) as written in P:452 / P:661, or
  * o' = g * h as written in BASELINE.json configs[0]. */
 typedef enum { TERN_GATE_SIGMOID_H = 0, TERN_GATE_LINEAR_H = 1 } tern_gate_mode;
+/* The norm in front of every BitLinear:
+ *   TERN_NORM_RMS      = 0: y = x r w, r = 1/sqrt(mean(x^2) + eps)   (Eq. 1, reading C1; default)
+ *   TERN_NORM_CENTERED = 1: y = (x - mu) r w, r = 1/sqrt(var(x) + eps)  (Alg. 1, C22)
+ * with mu = (float)(sum x / K) and var = sum (x - mu)^2 / K in binary64. */
+typedef enum { TERN_NORM_RMS = 0, TERN_NORM_CENTERED = 1 } tern_norm_mode;
 
 int tern_abi_version(void);
 /* Thread-local text of the last error (host pointer, valid until the next call). */
@@ -201,12 +206,14 @@ typedef struct {
   const float *bias_o;              /* [d] or NULL              */
   tern_gate_mode gate;
   float eps;
+  tern_norm_mode norm;              /* of both BitLinears' inputs (0: RMSNorm) */
 } tern_mlgru;
 
 typedef struct {
   tern_weight gu, down;
   const float *gain_x, *gain_p;     /* [d], [l] */
   float eps;
+  tern_norm_mode norm;              /* of both BitLinears' inputs (0: RMSNorm) */
 } tern_glu;
 
 /* Output-feature sharding of a block over `world` ranks (BASELINE.json
@@ -352,6 +359,12 @@ int32_t tern_trace_collect(uint64_t* out, int32_t max_launches);
  * Synchronous; writes the mismatch count to *mismatches (host).  ws: device
  * scratch of >= 64 bytes. */
 tern_status tern_selftest(int32_t which, void* ws, uint64_t* mismatches);
+
+/* Norm variant used by tern_quant and bitlinear_fwd (process-wide, host;
+ * default TERN_NORM_RMS).  Mixers and blocks take theirs from tern_mlgru.norm
+ * and tern_glu.norm.  Not thread-safe to change while calls are in flight. */
+void tern_set_norm_mode(tern_norm_mode mode);
+tern_norm_mode tern_get_norm_mode(void);
 
 /* Tuning knob (host): largest m sent to the decode GEMV (default 4, max 4;
  * 0 forces the tensor-core path everywhere).  Not thread-safe to change

@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("TERN_LIB", os.path.join(_HERE, "libtern.so"))
 TERN_OK, TERN_ERR_INVALID_ARG, TERN_ERR_DEGENERATE, TERN_ERR_UNSUPPORTED, TERN_ERR_CUDA = range(5)
 TERN_F32, TERN_BF16 = 0, 1
 TERN_GATE_SIGMOID_H, TERN_GATE_LINEAR_H = 0, 1
+TERN_NORM_RMS, TERN_NORM_CENTERED = 0, 1
 
 
 class TernError(RuntimeError):
@@ -39,12 +40,12 @@ class tern_bl_taps(C.Structure):
 class tern_mlgru(C.Structure):
     _fields_ = [("fcg", tern_weight), ("o", tern_weight), ("gain_x", C.c_void_p),
                 ("gain_o", C.c_void_p), ("bias_fcg", C.c_void_p), ("bias_o", C.c_void_p),
-                ("gate", C.c_int), ("eps", C.c_float)]
+                ("gate", C.c_int), ("eps", C.c_float), ("norm", C.c_int)]
 
 
 class tern_glu(C.Structure):
     _fields_ = [("gu", tern_weight), ("down", tern_weight), ("gain_x", C.c_void_p),
-                ("gain_p", C.c_void_p), ("eps", C.c_float)]
+                ("gain_p", C.c_void_p), ("eps", C.c_float), ("norm", C.c_int)]
 
 
 # int ag(void* ctx, const void* send, void* recv, size_t bytes_per_rank, cudaStream_t stream)
@@ -114,6 +115,8 @@ _SIGS = {
     "tern_set_fused_scan": (None, [I32]),
     "tern_get_fused_scan": (I32, []),
     "tern_set_batched_fin": (None, [I32]),
+    "tern_set_norm_mode": (None, [C.c_int]),
+    "tern_get_norm_mode": (C.c_int, []),
     "tern_get_batched_fin": (I32, []),
 }
 EXPORTS = tuple(_SIGS)
@@ -282,6 +285,15 @@ def tern_set_gemv_max_m(m: int):
 
 def tern_set_fused_scan(on: bool):
     load().tern_set_fused_scan(1 if on else 0)
+
+
+def tern_set_norm_mode(mode: int):
+    """Norm variant of tern_quant / bitlinear_fwd (0 RMSNorm, 1 centred, Alg. 1)."""
+    load().tern_set_norm_mode(int(mode))
+
+
+def tern_get_norm_mode() -> int:
+    return int(load().tern_get_norm_mode())
 
 
 def tern_set_batched_fin(on: bool):

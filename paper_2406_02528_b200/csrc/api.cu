@@ -20,6 +20,7 @@ thread_local std::string g_err;
 int g_gemv_max_m = kGemvMaxM;
 int g_fused_scan = 1;
 int g_batched_fin = 0;   // tern_set_batched_fin
+int g_norm_mode = TERN_NORM_RMS;   // tern_set_norm_mode (tern_quant, bitlinear_fwd)
 constexpr int kSplitKMaxM = 256;
 
 tern_status fail(tern_status st, const char* fmt, ...) {
@@ -194,10 +195,11 @@ template <typename T> T* at(void* ws, size_t off) {
 tern_status bl_tc(const void* x, tern_dtype xdt, int M, int K, int ldx, const float* gain,
                   float eps, const tern_weight& w, tern_dtype ydt, const Epi& epi, int8_t* q,
                   int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
-                  cudaStream_t s, int32_t* part = nullptr, size_t part_bytes = 0) {
+                  cudaStream_t s, int32_t* part = nullptr, size_t part_bytes = 0,
+                  int norm = TERN_NORM_RMS) {
   {
     Prof p(TERN_K_QUANT, 0, M, 0, K, 0, xdt, s);
-    TRY_CUDA(launch_quant(x, xdt, M, K, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s),
+    TRY_CUDA(launch_quant(x, xdt, M, K, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm),
              "quant");
   }
   Prof p(TERN_K_GEMM, epi.kind, M, w.n_rows, w.k, w.n_seg, ydt, s);
@@ -230,6 +232,9 @@ tern_status check_block(const tern_block* b) {
   CHECK(b->ch.gu.n_out == ls && b->ch.down.n_out == ds, "GLU weights must be d->l/world, l->d/world");
   CHECK(b->mix.gate == TERN_GATE_SIGMOID_H || b->mix.gate == TERN_GATE_LINEAR_H, "bad gate mode");
   CHECK(b->mix.eps > 0 && b->ch.eps > 0, "eps must be > 0");
+  CHECK((b->mix.norm == TERN_NORM_RMS || b->mix.norm == TERN_NORM_CENTERED) &&
+            (b->ch.norm == TERN_NORM_RMS || b->ch.norm == TERN_NORM_CENTERED),
+        "bad norm mode");
   return TERN_OK;
 }
 
@@ -293,6 +298,10 @@ int32_t tern_get_fused_scan(void) { return g_fused_scan; }
 void tern_set_gemv_max_m(int32_t m) { g_gemv_max_m = m < 0 ? 0 : (m > kGemvMaxM ? kGemvMaxM : m); }
 int32_t tern_get_gemv_max_m(void) { return g_gemv_max_m; }
 void tern_set_batched_fin(int32_t on) { g_batched_fin = on ? 1 : 0; }
+void tern_set_norm_mode(tern_norm_mode mode) {
+  g_norm_mode = mode == TERN_NORM_CENTERED ? TERN_NORM_CENTERED : TERN_NORM_RMS;
+}
+tern_norm_mode tern_get_norm_mode(void) { return (tern_norm_mode)g_norm_mode; }
 int32_t tern_get_batched_fin(void) { return g_batched_fin; }
 
 int32_t tern_packed_rows(int32_t n_out, int32_t n_seg) {
@@ -363,7 +372,7 @@ tern_status tern_quant(const void* x, tern_dtype xdt, int32_t m, int32_t k, int3
   tern_status st = check_device();
   if (st) return st;
   TRY_CUDA(launch_quant(x, xdt, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax,
-                        (cudaStream_t)stream),
+                        (cudaStream_t)stream, g_norm_mode),
            "quant");
   return TERN_OK;
 }
@@ -412,7 +421,8 @@ tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, i
       qt.inv_rms = taps->inv_rms; qt.absmax = taps->absmax;
     }
     Prof pr(TERN_K_GEMV, e.kind, m, w->n_rows, k, 1, xdt, s);
-    TRY_CUDA(launch_gemv(x, xdt, ydt, m, k, ldx, gain, eps, *w, e, &qt, s), "gemv");
+    TRY_CUDA(launch_gemv(x, xdt, ydt, m, k, ldx, gain, eps, *w, e, &qt, s, nullptr, 0, g_norm_mode),
+             "gemv");
     return TERN_OK;
   }
   int8_t* q = (taps && taps->q) ? taps->q : static_cast<int8_t*>(ws);
@@ -420,7 +430,8 @@ tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, i
   float* deq = (taps && taps->deq) ? taps->deq : at<float>(ws, al256((size_t)m * kpad(k)));
   int32_t* qsum = at<int32_t>(ws, al256((size_t)m * kpad(k)) + al256((size_t)m * 4));
   return bl_tc(x, xdt, m, k, ldx, gain, eps, *w, ydt, e, q, ldq, deq, qsum,
-               taps ? taps->inv_rms : nullptr, taps ? taps->absmax : nullptr, s);
+               taps ? taps->inv_rms : nullptr, taps ? taps->absmax : nullptr, s, nullptr, 0,
+               g_norm_mode);
 }
 
 tern_status tern_contract(const int8_t* q, int32_t m, int32_t ldq, const int32_t* qsum,
@@ -501,14 +512,15 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
     {
       Prof pr(TERN_K_GEMV, e1.kind, B, p.fcg.n_rows, d, 3, dt, s);
       TRY_CUDA(launch_gemv(x, dt, dt, B, d, d, p.gain_x, p.eps, p.fcg, e1, nullptr, s, pf.p[0],
-                           pf.n[0]),
+                           pf.n[0], p.norm),
                "gemv fcg");
     }
     Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.o, p.bias_o, out, d);
     e2.res = x;
     e2.ldr = d;
     Prof pr(TERN_K_GEMV, e2.kind, B, p.o.n_rows, d, 1, dt, s);
-    TRY_CUDA(launch_gemv(op, dt, dt, B, d, d, p.gain_o, p.eps, p.o, e2, nullptr, s, pf.p[1], pf.n[1]),
+    TRY_CUDA(launch_gemv(op, dt, dt, B, d, d, p.gain_o, p.eps, p.o, e2, nullptr, s, pf.p[1], pf.n[1],
+                         p.norm),
              "gemv o");
     return TERN_OK;
   }
@@ -526,13 +538,14 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
     e1.h = h;
     e1.gate = p.gate;
     tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
-                           nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes);
+                           nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
     if (st) return st;
   } else if (g_fused_scan && T >= 64 && fcgscan_supported(p.fcg, d)) {
     // a4 + a6 fused: f^c^g^ stay on chip (k_fcgscan.cu)
     {
       Prof pr(TERN_K_QUANT, 0, M, 0, d, 0, dt, s);
-      TRY_CUDA(launch_quant(x, dt, M, d, d, p.gain_x, p.eps, q, ldq, deq, qsum, nullptr, nullptr, s),
+      TRY_CUDA(launch_quant(x, dt, M, d, d, p.gain_x, p.eps, q, ldq, deq, qsum, nullptr, nullptr, s,
+                            p.norm),
                "quant");
     }
     Prof pr(TERN_K_FCGSCAN, p.gate, M, p.fcg.n_rows, d, 3, dt, s);
@@ -541,7 +554,7 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   } else {
     Epi e1 = make_epi(EPI_FCG, p.fcg, p.bias_fcg, fcg, p.fcg.n_rows);
     tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
-                           nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes);
+                           nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
     if (st) return st;
     Prof pr(TERN_K_SCAN, p.gate, B * T, d, d, 3, dt, s);
     TRY_CUDA(launch_scan(fcg, dt, B, T, d, p.gate, h, op, s), "scan");
@@ -550,7 +563,7 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   e2.res = x;
   e2.ldr = d;
   return bl_tc(op, dt, M, d, d, p.gain_o, p.eps, p.o, dt, e2, q, ldq, deq, qsum, nullptr, nullptr,
-               s, at<int32_t>(ws, L.part), L.part_bytes);
+               s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
 }
 
 // channel mixer: x [M][d] -> out (d, or y = x + d when resid)
@@ -566,12 +579,12 @@ tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, ter
     {
       Prof pr(TERN_K_GEMV, e1.kind, M, p.gu.n_rows, d, 2, dt, s);
       TRY_CUDA(launch_gemv(x, dt, dt, M, d, d, p.gain_x, p.eps, p.gu, e1, nullptr, s, pf.p[0],
-                           pf.n[0]),
+                           pf.n[0], p.norm),
                "gemv gu");
     }
     Prof pr(TERN_K_GEMV, e2.kind, M, p.down.n_rows, l, 1, dt, s);
     TRY_CUDA(launch_gemv(pp, dt, dt, M, l, l, p.gain_p, p.eps, p.down, e2, nullptr, s, pf.p[1],
-                         pf.n[1]),
+                         pf.n[1], p.norm),
              "gemv down");
     return TERN_OK;
   }
@@ -579,24 +592,24 @@ tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, ter
   float* deq = at<float>(ws, L.deq);
   int32_t* qsum = at<int32_t>(ws, L.qsum);
   tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.gu, dt, e1, q, kpad(d), deq, qsum,
-                         nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes);
+                         nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
   if (st) return st;
   return bl_tc(pp, dt, M, l, l, p.gain_p, p.eps, p.down, dt, e2, q, kpad(l), deq, qsum, nullptr,
-               nullptr, s, at<int32_t>(ws, L.part), L.part_bytes);
+               nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
 }
 
 // one BitLinear on either path (decode GEMV with its fused prologue, or quant + GEMM)
 tern_status bitlinear_any(bool gemv, const void* x, tern_dtype dt, int M, int K, const float* gain,
                           float eps, const tern_weight& w, const Epi& e, void* ws, const BlockWs& L,
-                          cudaStream_t s) {
+                          cudaStream_t s, int norm) {
   if (gemv) {
     Prof pr(TERN_K_GEMV, e.kind, M, w.n_rows, K, w.n_seg, dt, s);
-    TRY_CUDA(launch_gemv(x, dt, dt, M, K, K, gain, eps, w, e, nullptr, s), "gemv");
+    TRY_CUDA(launch_gemv(x, dt, dt, M, K, K, gain, eps, w, e, nullptr, s, nullptr, 0, norm), "gemv");
     return TERN_OK;
   }
   return bl_tc(x, dt, M, K, K, gain, eps, w, dt, e, at<int8_t>(ws, L.q), kpad(K),
                at<float>(ws, L.deq), at<int32_t>(ws, L.qsum), nullptr, nullptr, s,
-               at<int32_t>(ws, L.part), L.part_bytes);
+               at<int32_t>(ws, L.part), L.part_bytes, norm);
 }
 
 // gather the ranks' [M][cs] slices into full [M][world*cs] rows
@@ -630,11 +643,11 @@ tern_status run_block_sharded(const tern_block& b, const void* x, void* y, tern_
     Epi e1 = make_epi(EPI_MLGRU, mx.fcg, mx.bias_fcg, sout, ds);
     e1.h = h;
     e1.gate = mx.gate;
-    if ((st = bitlinear_any(true, x, dt, M, d, mx.gain_x, mx.eps, mx.fcg, e1, ws, L, s))) return st;
+    if ((st = bitlinear_any(true, x, dt, M, d, mx.gain_x, mx.eps, mx.fcg, e1, ws, L, s, mx.norm))) return st;
   } else {
     void* fcg = at<char>(ws, L.fcg);
     Epi e1 = make_epi(EPI_FCG, mx.fcg, mx.bias_fcg, fcg, mx.fcg.n_rows);
-    if ((st = bitlinear_any(false, x, dt, M, d, mx.gain_x, mx.eps, mx.fcg, e1, ws, L, s))) return st;
+    if ((st = bitlinear_any(false, x, dt, M, d, mx.gain_x, mx.eps, mx.fcg, e1, ws, L, s, mx.norm))) return st;
     Prof pr(TERN_K_SCAN, mx.gate, M, ds, ds, 3, dt, s);
     TRY_CUDA(launch_scan(fcg, dt, B, T, ds, mx.gate, h, sout, s), "scan");
   }
@@ -643,16 +656,16 @@ tern_status run_block_sharded(const tern_block& b, const void* x, void* y, tern_
   Epi e2 = make_epi(EPI_RESID, mx.o, mx.bias_o, sout, ds);
   e2.res = static_cast<const char*>(x) + (size_t)sh.rank * ds * es;
   e2.ldr = d;
-  if ((st = bitlinear_any(gv, op, dt, M, d, mx.gain_o, mx.eps, mx.o, e2, ws, L, s))) return st;
+  if ((st = bitlinear_any(gv, op, dt, M, d, mx.gain_o, mx.eps, mx.o, e2, ws, L, s, mx.norm))) return st;
   if ((st = shard_gather(sh, sout, x1, M, ds, dt, ws, L, s))) return st;
   // channel mixer: p_r = SiLU(g_r) u_r, then y_r = x1[:, r] + p(*)W_d[r]
   Epi e3 = make_epi(EPI_SWIGLU, gl.gu, nullptr, sout, ls);
-  if ((st = bitlinear_any(gv, x1, dt, M, d, gl.gain_x, gl.eps, gl.gu, e3, ws, L, s))) return st;
+  if ((st = bitlinear_any(gv, x1, dt, M, d, gl.gain_x, gl.eps, gl.gu, e3, ws, L, s, gl.norm))) return st;
   if ((st = shard_gather(sh, sout, pf, M, ls, dt, ws, L, s))) return st;
   Epi e4 = make_epi(EPI_RESID, gl.down, nullptr, sout, ds);
   e4.res = static_cast<const char*>(x1) + (size_t)sh.rank * ds * es;
   e4.ldr = d;
-  if ((st = bitlinear_any(gv, pf, dt, M, l, gl.gain_p, gl.eps, gl.down, e4, ws, L, s))) return st;
+  if ((st = bitlinear_any(gv, pf, dt, M, l, gl.gain_p, gl.eps, gl.down, e4, ws, L, s, gl.norm))) return st;
   return shard_gather(sh, sout, y, M, ds, dt, ws, L, s);
 }
 
@@ -680,12 +693,12 @@ tern_status run_block_decode_batched(const tern_block& b, const void* x, void* y
   {
     Prof pr(TERN_K_QUANT, 0, B, 0, d, 0, dt, s);
     TRY_CUDA(launch_quant(x, dt, B, d, d, mx.gain_x, mx.eps, q, kpad(d), deq, qsum, nullptr,
-                          nullptr, s),
+                          nullptr, s, mx.norm),
              "quant");
   }
   // one phase: GEMM partials, then finalize (+ the next BitLinear's quant)
   auto phase = [&](const tern_weight& w, int K, const Epi& e, const float* ngain, float neps,
-                   bool nquant) -> tern_status {
+                   bool nquant, int nnorm) -> tern_status {
     int ks = 1;
     {
       Prof pr(TERN_K_GEMM, EPI_NONE, B, w.n_rows, K, w.n_seg, dt, s);
@@ -695,7 +708,7 @@ tern_status run_block_decode_batched(const tern_block& b, const void* x, void* y
     }
     Prof pr(TERN_K_FIN, e.kind, B, w.n_rows, K, w.n_seg, dt, s);
     TRY_CUDA(launch_fin(part, ks, B, w.n_rows, deq, qsum, e, dt, ngain, neps,
-                        nquant ? q : nullptr, kpad(e.n_out), deq, qsum, s),
+                        nquant ? q : nullptr, kpad(e.n_out), deq, qsum, s, nnorm),
              "finalize");
     return TERN_OK;
   };
@@ -703,17 +716,17 @@ tern_status run_block_decode_batched(const tern_block& b, const void* x, void* y
   Epi e1 = make_epi(EPI_MLGRU, mx.fcg, mx.bias_fcg, op, d);
   e1.h = h;
   e1.gate = mx.gate;
-  if ((st = phase(mx.fcg, d, e1, mx.gain_o, mx.eps, true))) return st;
+  if ((st = phase(mx.fcg, d, e1, mx.gain_o, mx.eps, true, mx.norm))) return st;
   Epi e2 = make_epi(EPI_RESID, mx.o, mx.bias_o, x1, d);
   e2.res = x;
   e2.ldr = d;
-  if ((st = phase(mx.o, d, e2, gl.gain_x, gl.eps, true))) return st;
+  if ((st = phase(mx.o, d, e2, gl.gain_x, gl.eps, true, gl.norm))) return st;
   Epi e3 = make_epi(EPI_SWIGLU, gl.gu, nullptr, pp, l);
-  if ((st = phase(gl.gu, d, e3, gl.gain_p, gl.eps, true))) return st;
+  if ((st = phase(gl.gu, d, e3, gl.gain_p, gl.eps, true, gl.norm))) return st;
   Epi e4 = make_epi(EPI_RESID, gl.down, nullptr, y, d);
   e4.res = x1;
   e4.ldr = d;
-  return phase(gl.down, l, e4, nullptr, 0.0f, false);
+  return phase(gl.down, l, e4, nullptr, 0.0f, false, TERN_NORM_RMS);
 }
 
 tern_status check_act(const void* x, const void* y, const void* ws, size_t ws_bytes, size_t need,
@@ -741,6 +754,7 @@ tern_status mlgru_fwd(const tern_mlgru* p, const void* x, void* out, tern_dtype 
   if ((st = check_weight(&p->o, d, 1, "o")) != TERN_OK) return st;
   CHECK(p->fcg.n_out == d && p->o.n_out == d, "mlgru_fwd: weights must be d x d");
   CHECK(p->eps > 0, "mlgru_fwd: eps");
+  CHECK(p->norm == TERN_NORM_RMS || p->norm == TERN_NORM_CENTERED, "mlgru_fwd: bad norm mode");
   BlockWs L = block_ws(B * T, d, 0, p->fcg.n_rows, dt);
   if ((st = check_act(x, out, ws, ws_bytes, L.total, dt, "mlgru_fwd")) != TERN_OK) return st;
   if ((st = check_device()) != TERN_OK) return st;
@@ -758,6 +772,7 @@ tern_status glu_fwd(const tern_glu* p, const void* x, void* out, tern_dtype dt, 
   if ((st = check_weight(&p->down, l, 1, "down")) != TERN_OK) return st;
   CHECK(p->gu.n_out == l && p->down.n_out == d, "glu_fwd: weights must be d->l, l->d");
   CHECK(p->eps > 0, "glu_fwd: eps");
+  CHECK(p->norm == TERN_NORM_RMS || p->norm == TERN_NORM_CENTERED, "glu_fwd: bad norm mode");
   BlockWs L = block_ws(m, d, l, 0, dt);
   if ((st = check_act(x, out, ws, ws_bytes, L.total, dt, "glu_fwd")) != TERN_OK) return st;
   if ((st = check_device()) != TERN_OK) return st;
@@ -845,13 +860,13 @@ std::vector<StackPhaseDesc> stack_phases(const tern_block* blocks, int L, const 
     const void* xin = i == 0 ? x : xb;
     void* xout = i == L - 1 ? y : xb;
     StackPhaseDesc f{xin, nullptr, a, h[i], b.mix.fcg, b.mix.gain_x, b.mix.bias_fcg, b.mix.eps,
-                     EPI_MLGRU, (int)b.mix.gate, b.d};
+                     EPI_MLGRU, (int)b.mix.gate, b.d, (int)b.mix.norm};
     StackPhaseDesc o{a, xin, x1, nullptr, b.mix.o, b.mix.gain_o, b.mix.bias_o, b.mix.eps,
-                     EPI_RESID, 0, b.d};
+                     EPI_RESID, 0, b.d, (int)b.mix.norm};
     StackPhaseDesc g{x1, nullptr, p, nullptr, b.ch.gu, b.ch.gain_x, nullptr, b.ch.eps,
-                     EPI_SWIGLU, 0, b.d};
+                     EPI_SWIGLU, 0, b.d, (int)b.ch.norm};
     StackPhaseDesc dn{p, x1, xout, nullptr, b.ch.down, b.ch.gain_p, nullptr, b.ch.eps,
-                      EPI_RESID, 0, b.l};
+                      EPI_RESID, 0, b.l, (int)b.ch.norm};
     ph.push_back(f);
     ph.push_back(o);
     ph.push_back(g);

@@ -59,14 +59,15 @@ size_t pack_workspace_bytes();
 // a2
 cudaError_t launch_quant(const void* x, int xdt, int m, int k, int ldx, const float* gain,
                          float eps, int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
-                         float* absmax, cudaStream_t s);
+                         float* absmax, cudaStream_t s, int norm = TERN_NORM_RMS);
 // a3 (decode GEMV, norm+quant prologue fused): x [M][ldx] -> epilogue
 constexpr int kGemvMaxM = 4;
 bool gemv_supported(int M, int K, int xdt);   // M <= kGemvMaxM and K within the register tile
 // pf / pf_bytes: optional L2 prefetch of a later launch's packed weights
 cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, const float* gain,
                         float eps, const tern_weight& w, const Epi& epi, const QuantTaps* taps,
-                        cudaStream_t s, const void* pf = nullptr, size_t pf_bytes = 0);
+                        cudaStream_t s, const void* pf = nullptr, size_t pf_bytes = 0,
+                        int norm = TERN_NORM_RMS);
 // a4 (tcgen05 int8 GEMM): q [M][ldq] -> epilogue
 // part: optional int32 scratch [M][n_rows] enabling split-K for small M (nullptr: never)
 // ks_out: partials only (part required): the K-slice count is returned and no
@@ -81,7 +82,8 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
 bool fin_supported(int n_out);
 cudaError_t launch_fin(const int32_t* part, int ks, int M, int n_rows, const float* deq,
                        const int32_t* qsum, const Epi& e, int ydt, const float* ngain, float neps,
-                       int8_t* nq, int nldq, float* ndeq, int32_t* nqsum, cudaStream_t s);
+                       int8_t* nq, int nldq, float* ndeq, int32_t* nqsum, cudaStream_t s,
+                       int nnorm = TERN_NORM_RMS);
 // f2: whole-stack decode step in one persistent cooperative launch.  A phase
 // is one decode BitLinear with its epilogue (MLGRU / SWIGLU / RESID / STORE),
 // contiguous rows (ld = K for x, n_out for out/res/h).
@@ -94,7 +96,7 @@ struct StackPhaseDesc {
   const float* gain;
   const float* bias;
   float eps;
-  int kind, gate, K;
+  int kind, gate, K, norm;
 };
 bool stack_decode_plan(const StackPhaseDesc* ph, int n, int M, int xdt, size_t* smem);
 // bar: one zeroed-per-launch u32 grid-barrier counter (device); returns

@@ -32,6 +32,7 @@ struct FinArgs {
   int nldq, nkp;
   float* ndeq;
   int32_t* nqsum;
+  int nnorm;             // tern_norm_mode of the next BitLinear
   unsigned long long* trace;
 };
 
@@ -161,6 +162,33 @@ __global__ void __launch_bounds__(kFinThreads, 1) k_fin(const FinArgs a) {
     return;
   }
   // ---------------- the next BitLinear's RMSNorm + absmax int8 quant of this row
+  const bool cent = a.nnorm == TERN_NORM_CENTERED;
+  float mu = 0.0f;   // centred norm (Alg. 1, reading C22): moments of y - mu
+  if (cent) {
+    double sx = 0.0;
+#pragma unroll
+    for (int j = 0; j < 2 * NP; ++j) sx += (double)y[j];   // zeros outside the row
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    if (lane == 0) red_d[warp] = sx;
+    __syncthreads();
+    sx = red_d[0];
+#pragma unroll
+    for (int i = 1; i < kFinWarps; ++i) sx += red_d[i];
+    mu = (float)(sx / (double)n);
+    __syncthreads();   // red_d is reused below
+    ss0 = ss1 = 0.0;
+    ym = 0.0f;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      if (tid + j * kFinThreads < npair) {
+        const double d0 = (double)y[2 * j] - (double)mu, d1 = (double)y[2 * j + 1] - (double)mu;
+        ss0 = fma(d0, d0, ss0);
+        ss1 = fma(d1, d1, ss1);
+        ym = fmaxf(ym, fmaxf(fabsf(__fsub_rn(y[2 * j], mu)), fabsf(__fsub_rn(y[2 * j + 1], mu))));
+      }
+    }
+  }
   double ss = ss0 + ss1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -173,7 +201,8 @@ __global__ void __launch_bounds__(kFinThreads, 1) k_fin(const FinArgs a) {
   ym = red_f[0];
 #pragma unroll
   for (int i = 1; i < kFinWarps; ++i) { ss += red_d[i]; ym = fmaxf(ym, red_f[i]); }
-  const float r = (float)rsqrt(fma(ss, a.ninv_k, (double)a.neps));
+  const float r = cent ? (float)(1.0 / sqrt(ss / (double)n + (double)a.neps))
+                       : (float)rsqrt(fma(ss, a.ninv_k, (double)a.neps));
   float amax;
   if (a.ngain == nullptr) {
     amax = __fmul_rn(ym, r);   // rounding is monotone and r > 0
@@ -184,8 +213,8 @@ __global__ void __launch_bounds__(kFinThreads, 1) k_fin(const FinArgs a) {
       const int p = tid + j * kFinThreads;
       if (p < npair) {
         const float2 g = __ldg(reinterpret_cast<const float2*>(a.ngain) + p);
-        am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(y[2 * j], r), g.x)));
-        am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(y[2 * j + 1], r), g.y)));
+        am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(__fsub_rn(y[2 * j], mu), r), g.x)));
+        am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(__fsub_rn(y[2 * j + 1], mu), r), g.y)));
       }
     }
     am = warp_max_f32(am);
@@ -204,7 +233,7 @@ __global__ void __launch_bounds__(kFinThreads, 1) k_fin(const FinArgs a) {
   for (int j = 0; j < NP; ++j) {
     const int p = tid + j * kFinThreads;
     if (p < npair) {
-      float v0 = __fmul_rn(y[2 * j], r), v1 = __fmul_rn(y[2 * j + 1], r);
+      float v0 = __fmul_rn(__fsub_rn(y[2 * j], mu), r), v1 = __fmul_rn(__fsub_rn(y[2 * j + 1], mu), r);
       if (a.ngain) {
         const float2 g = __ldg(reinterpret_cast<const float2*>(a.ngain) + p);
         v0 = __fmul_rn(v0, g.x);
@@ -246,7 +275,8 @@ bool fin_supported(int n_out) { return n_out % 2 == 0 && n_out / 2 <= 8 * kFinTh
 
 cudaError_t launch_fin(const int32_t* part, int ks, int M, int n_rows, const float* deq,
                        const int32_t* qsum, const Epi& e, int ydt, const float* ngain, float neps,
-                       int8_t* nq, int nldq, float* ndeq, int32_t* nqsum, cudaStream_t s) {
+                       int8_t* nq, int nldq, float* ndeq, int32_t* nqsum, cudaStream_t s,
+                       int nnorm) {
   if (M <= 0) return cudaSuccess;
   if (!fin_supported(e.n_out)) return cudaErrorInvalidValue;
   if (e.kind != EPI_MLGRU && e.kind != EPI_SWIGLU && e.kind != EPI_RESID && e.kind != EPI_STORE)
@@ -267,6 +297,7 @@ cudaError_t launch_fin(const int32_t* part, int ks, int M, int n_rows, const flo
   a.nkp = (e.n_out + kKAlign - 1) / kKAlign * kKAlign;
   a.ndeq = ndeq;
   a.nqsum = nqsum;
+  a.nnorm = nnorm;
   a.trace = trace_slot(TERN_K_FIN, M);
   return ydt == TERN_BF16 ? fin_go<__nv_bfloat16>(a, s) : fin_go<float>(a, s);
 }

@@ -42,6 +42,7 @@ struct GemvArgs {
   int n_rows, n_out, n_seg, ch;
   int sw_stride;  // words between consecutive K-blocks of a segment in smem
   double inv_k;  // 1/K (binary64)
+  int norm;      // tern_norm_mode of the input row
   Epi epi;
   QuantTaps taps;
   const uint8_t* pf;         // L2 prefetch hint: a later launch's packed weights
@@ -203,6 +204,37 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
       xv[m][i] = (m < a.M && v < nvec) ? __ldcg(src + v) : make_uint4(0, 0, 0, 0);
     }
   }
+  // centred norm (Alg. 1, reading C22): the row mean first, then the moments
+  // are taken of x - mu (exact in binary64); mu = 0 leaves the RMSNorm path
+  float mu[MM];
+#pragma unroll
+  for (int m = 0; m < MM; ++m) mu[m] = 0.0f;
+  const bool cent = a.norm == TERN_NORM_CENTERED;
+  if (cent) {
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      double sx = 0.0;
+#pragma unroll
+      for (int i = 0; i < kGNVX; ++i) {
+        float v[VE];
+        XVec<TX>::unpack(xv[m][i], v);   // zeros outside the row
+#pragma unroll
+        for (int j = 0; j < VE; ++j) sx += (double)v[j];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+      if (lane == 0) red_d[m][warp] = sx;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      double sx = lane < kGWarps ? red_d[m][lane] : 0.0;
+#pragma unroll
+      for (int o = kGWarps / 2; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+      mu[m] = (float)(__shfl_sync(0xffffffffu, sx, 0) / (double)a.K);
+    }
+    __syncthreads();   // red_d is reused below
+  }
 #pragma unroll
   for (int m = 0; m < MM; ++m) {
     double s0 = 0.0, s1 = 0.0;
@@ -211,6 +243,19 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
     for (int i = 0; i < kGNVX; ++i) {
       float v[VE];
       XVec<TX>::unpack(xv[m][i], v);
+      if (cent) {
+        const bool in = tid + i * kGThreads < nvec;   // padding takes no part in the moments
+#pragma unroll
+        for (int j = 0; j < VE; j += 2) {
+          const double d0 = in ? (double)v[j] - (double)mu[m] : 0.0;
+          const double d1 = in ? (double)v[j + 1] - (double)mu[m] : 0.0;
+          s0 = fma(d0, d0, s0);
+          s1 = fma(d1, d1, s1);
+          if (in)
+            xmax = fmaxf(xmax, fmaxf(fabsf(__fsub_rn(v[j], mu[m])), fabsf(__fsub_rn(v[j + 1], mu[m]))));
+        }
+        continue;
+      }
 #pragma unroll
       for (int j = 0; j < VE; j += 2) {
         const double d0 = (double)v[j], d1 = (double)v[j + 1];
@@ -244,7 +289,8 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
     }
     sd = __shfl_sync(0xffffffffu, sd, 0);
     xm = __shfl_sync(0xffffffffu, xm, 0);
-    rinv[m] = (float)rsqrt(fma(sd, a.inv_k, (double)a.eps));
+    rinv[m] = cent ? (float)(1.0 / sqrt(sd / (double)a.K + (double)a.eps))
+                   : (float)rsqrt(fma(sd, a.inv_k, (double)a.eps));
     // max|fl(x r)| = fl(max|x| r): rounding is monotone and r > 0
     amax[m] = __fmul_rn(xm, rinv[m]);
   }
@@ -260,7 +306,8 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
 #pragma unroll
         for (int j = 0; j < VE; ++j)
           if (v < nvec)
-            am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(xf[j], rinv[m]), __ldg(a.gain + v * VE + j))));
+            am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(__fsub_rn(xf[j], mu[m]), rinv[m]),
+                                           __ldg(a.gain + v * VE + j))));
       }
       am = warp_max_f32(am);
       __syncthreads();   // everyone has read red_m above
@@ -289,7 +336,7 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
           XVec<TX>::unpack(xv[m][i], xf);
 #pragma unroll
           for (int j = 0; j < VE; ++j) {
-            float y = __fmul_rn(xf[j], rinv[m]);
+            float y = __fmul_rn(__fsub_rn(xf[j], mu[m]), rinv[m]);   // mu = 0: RMSNorm
             if (a.gain) y = __fmul_rn(y, __ldg(a.gain + v * VE + j));
             // |y*sc| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
             const int qi = (int)round_half_away(__fmul_rn(y, sc));
@@ -508,7 +555,7 @@ struct StackPhase {
   const float* bias;      // [n_seg*n_out] or null
   int K, n_rows, n_out, ch, sw_stride, kind, n_seg, gate;
   float eps;
-  int pad_;
+  int norm;
 };
 constexpr int kStackMaxPhases = 128;   // 32 blocks per launch (kernel parameter space)
 constexpr size_t kStackTraceStride = 1024 * 16;   // = one k_gemv trace slot (kTraceCtas * 16)
@@ -537,6 +584,7 @@ __device__ __forceinline__ GemvArgs stack_args(const StackPhase& s, int M) {
   a.ch = s.ch;
   a.sw_stride = s.sw_stride;
   a.inv_k = 1.0 / (double)s.K;
+  a.norm = s.norm;
   a.epi.kind = s.kind;
   a.epi.n_out = s.n_out;
   a.epi.n_seg = s.n_seg;
@@ -793,7 +841,7 @@ static int num_sms() {
 
 cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, const float* gain,
                         float eps, const tern_weight& w, const Epi& epi, const QuantTaps* taps,
-                        cudaStream_t s, const void* pf, size_t pf_bytes) {
+                        cudaStream_t s, const void* pf, size_t pf_bytes, int norm) {
   if (M <= 0) return cudaSuccess;
   if (!gemv_supported(M, K, xdt)) return cudaErrorInvalidValue;
   GemvArgs a{};
@@ -801,6 +849,7 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
   a.ldx = ldx;
   a.K = K;
   a.inv_k = 1.0 / (double)K;
+  a.norm = norm;
   a.Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
   a.M = M;
   a.gain = gain;
@@ -922,6 +971,7 @@ cudaError_t launch_stack_decode(const StackPhaseDesc* ph, int n, int M, int xdt,
       q.kind = d.kind;
       q.gate = d.gate;
       q.eps = d.eps;
+      q.norm = d.norm;
       const int Kp = (d.K + kKAlign - 1) / kKAlign * kKAlign;
       kp_max = Kp > kp_max ? Kp : kp_max;
       const size_t b = (size_t)q.n_seg * (Kp / 128) * q.sw_stride * 4;

@@ -44,8 +44,150 @@ __device__ __forceinline__ uint4 ldg_stream_v4(const uint4* p) {
   return v;
 }
 
+// sum over the WPR warps of one row (every thread of the row gets the total)
+template <int RPC, int WPR>
+__device__ __forceinline__ double row_sum_d(double v, double (*red)[WPR], int rloc, int wr, int lane) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (WPR > 1) {
+    __syncthreads();
+    if (lane == 0) red[rloc][wr] = v;
+    __syncthreads();
+    v = red[rloc][0];
+#pragma unroll
+    for (int i = 1; i < WPR; ++i) v += red[rloc][i];
+  }
+  return v;
+}
+template <int RPC, int WPR>
+__device__ __forceinline__ float row_max_f(float v, float (*red)[WPR], int rloc, int wr, int lane) {
+  v = warp_max_f32(v);
+  if (WPR > 1) {
+    __syncthreads();
+    if (lane == 0) red[rloc][wr] = v;
+    __syncthreads();
+    v = red[rloc][0];
+#pragma unroll
+    for (int i = 1; i < WPR; ++i) v = fmaxf(v, red[rloc][i]);
+  }
+  return v;
+}
+
+// Centred norm + quant of the thread's share of one row (reading C22):
+//   mu = (float)(sum x / K), var = sum (x - mu)^2 / K (binary64; x - mu exact),
+//   r = (float)(1 / sqrt(var + eps)), y = ((x - mu) r) w, then absmax quant.
+// Padding elements (v >= nvec) take no part in the moments and quantize to 0.
+template <typename TX, int TPR, int NV>
+__device__ __forceinline__ void centred_row(const uint4 (&xv)[NV], bool rv, int row, int t, int lane,
+                                            int wr, int rloc, int nvec, int nvecp, int K,
+                                            const float* __restrict__ gain, float eps,
+                                            int8_t* __restrict__ q, int ldq, float* __restrict__ deq,
+                                            int32_t* __restrict__ qsum, float* __restrict__ inv_rms,
+                                            float* __restrict__ absmax,
+                                            double (*red_d)[TPR / 32], float (*red_f)[TPR / 32],
+                                            int (*red_i)[TPR / 32]) {
+  constexpr int VE = QVec<TX>::N;
+  constexpr int WPR = TPR / 32;
+  constexpr int RPC = kQThreads / TPR;
+  double sx = 0.0;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float v[VE];
+    QVec<TX>::unpack(xv[i], v);   // zeros outside the row
+#pragma unroll
+    for (int j = 0; j < VE; ++j) sx += (double)v[j];
+  }
+  sx = row_sum_d<RPC, WPR>(sx, red_d, rloc, wr, lane);
+  const float mu = (float)(sx / (double)K);
+  double sv = 0.0;
+  float dm = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int v = t + i * TPR;
+    float xf[VE];
+    QVec<TX>::unpack(xv[i], xf);
+    if (v < nvec) {
+#pragma unroll
+      for (int j = 0; j < VE; ++j) {
+        const double dd = (double)xf[j] - (double)mu;
+        sv = fma(dd, dd, sv);
+        dm = fmaxf(dm, fabsf(__fsub_rn(xf[j], mu)));
+      }
+    }
+  }
+  sv = row_sum_d<RPC, WPR>(sv, red_d, rloc, wr, lane);
+  const float r = (float)(1.0 / sqrt(sv / (double)K + (double)eps));
+  float amax;
+  if (gain == nullptr) {
+    amax = __fmul_rn(row_max_f<RPC, WPR>(dm, red_f, rloc, wr, lane), r);   // monotone, r > 0
+  } else {
+    float am = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int v = t + i * TPR;
+      float xf[VE];
+      QVec<TX>::unpack(xv[i], xf);
+      if (v < nvec) {
+#pragma unroll
+        for (int j = 0; j < VE; ++j)
+          am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(__fsub_rn(xf[j], mu), r), __ldg(gain + v * VE + j))));
+      }
+    }
+    amax = row_max_f<RPC, WPR>(am, red_f, rloc, wr, lane);
+  }
+  const float sc = amax > 0.0f ? __fdiv_rn(127.0f, amax) : 0.0f;
+  int8_t* qr = q + (int64_t)(rv ? row : 0) * ldq;
+  int qs = 0;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int v = t + i * TPR;
+    float xf[VE];
+    QVec<TX>::unpack(xv[i], xf);
+    uint32_t pk[VE / 4];
+#pragma unroll
+    for (int j4 = 0; j4 < VE / 4; ++j4) {
+      int qi[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        qi[j] = 0;
+        if (v < nvec) {
+          float y = __fmul_rn(__fsub_rn(xf[4 * j4 + j], mu), r);
+          if (gain) y = __fmul_rn(y, __ldg(gain + v * VE + 4 * j4 + j));
+          qi[j] = __float2int_rz(round_half_away(__fmul_rn(y, sc)));
+        }
+        qs += qi[j];
+      }
+      pk[j4] = __byte_perm(__byte_perm(qi[0], qi[1], 0x0040), __byte_perm(qi[2], qi[3], 0x0040),
+                           0x5410);
+    }
+    if (rv && v < nvecp) {
+      if (VE == 4)
+        reinterpret_cast<uint32_t*>(qr)[v] = pk[0];
+      else
+        reinterpret_cast<uint2*>(qr)[v] = make_uint2(pk[0], pk[VE / 4 - 1]);
+    }
+  }
+  qs = warp_sum_i32(qs);
+  if (WPR > 1) {
+    __syncthreads();
+    if (lane == 0) red_i[rloc][wr] = qs;
+    __syncthreads();
+    qs = red_i[rloc][0];
+#pragma unroll
+    for (int i = 1; i < WPR; ++i) qs += red_i[rloc][i];
+  }
+  if (t == 0 && rv) {
+    deq[row] = amax > 0.0f ? __fdiv_rn(amax, 127.0f) : 0.0f;
+    qsum[row] = qs;
+    if (inv_rms) inv_rms[row] = r;
+    if (absmax) absmax[row] = amax;
+  }
+}
+
 // TPR threads per row, NV vectors per thread; CTA = kQThreads/TPR rows.
-template <typename TX, int TPR, int NV, bool GAIN, bool FULL>
+// CENT: the centred norm of Alg. 1 (reading C22; gain checked at
+// run time, row bounds always checked).
+template <typename TX, int TPR, int NV, bool GAIN, bool FULL, bool CENT = false>
 __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, int M, int K, int ldx,
                                                      const float* __restrict__ gain, float eps,
                                                      double inv_k, int8_t* __restrict__ q, int ldq,
@@ -77,6 +219,12 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
     const int v = t + i * TPR;
     // FULL: the row is exactly TPR*NV vectors (no bounds checks at all)
     xv[i] = (FULL ? rv : (rv && v < nvec)) ? ldg_stream_v4(xr + v) : make_uint4(0, 0, 0, 0);
+  }
+  if (CENT) {
+    centred_row<TX, TPR, NV>(xv, rv, row, t, lane, wr, rloc, nvec, nvecp, K, gain, eps, q, ldq, deq,
+                             qsum, inv_rms, absmax, red_d, red_f, red_i);
+    trace_mark(trace, 2);
+    return;
   }
   double s0 = 0.0, s1 = 0.0;
   float xm = 0.0f;
@@ -195,13 +343,15 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
 template <typename TX, int TPR, int NV>
 static void quant_go(const TX* x, int m, int k, int ldx, const float* gain, float eps, int8_t* q,
                      int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
-                     cudaStream_t s) {
+                     cudaStream_t s, int norm) {
   constexpr int RPC = kQThreads / TPR;
   const int grid = (m + RPC - 1) / RPC;
   const double inv_k = 1.0 / (double)k;
   const bool full = k == TPR * NV * QVec<TX>::N;   // then also k == Kp
-  auto kern = gain ? k_quant<TX, TPR, NV, true, false>
-                   : (full ? k_quant<TX, TPR, NV, false, true> : k_quant<TX, TPR, NV, false, false>);
+  auto kern = norm == TERN_NORM_CENTERED
+                  ? k_quant<TX, TPR, NV, false, false, true>
+                  : (gain ? k_quant<TX, TPR, NV, true, false>
+                          : (full ? k_quant<TX, TPR, NV, false, true> : k_quant<TX, TPR, NV, false, false>));
   launch_pdl(kern, dim3(grid), dim3(kQThreads), 0, s, x, m, k, ldx, gain, eps, inv_k, q, ldq, deq,
              qsum, inv_rms, absmax, trace_slot(TERN_K_QUANT, grid));
 }
@@ -209,35 +359,35 @@ static void quant_go(const TX* x, int m, int k, int ldx, const float* gain, floa
 template <typename TX, int TPR>
 static void quant_nv(int nv, const TX* x, int m, int k, int ldx, const float* gain, float eps,
                      int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
-                     cudaStream_t s) {
+                     cudaStream_t s, int norm) {
   // exactly as many register vectors as the row needs: predicated-off slots of
   // the fully unrolled loops still cost issue slots, and this kernel is issue-bound
   switch (nv) {
-    case 1: case 2: quant_go<TX, TPR, 2>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
-    case 3: quant_go<TX, TPR, 3>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
-    case 4: quant_go<TX, TPR, 4>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
-    case 5: quant_go<TX, TPR, 5>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
-    case 6: quant_go<TX, TPR, 6>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
-    case 7: quant_go<TX, TPR, 7>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
-    default: quant_go<TX, TPR, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s); break;
+    case 1: case 2: quant_go<TX, TPR, 2>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    case 3: quant_go<TX, TPR, 3>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    case 4: quant_go<TX, TPR, 4>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    case 5: quant_go<TX, TPR, 5>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    case 6: quant_go<TX, TPR, 6>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    case 7: quant_go<TX, TPR, 7>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    default: quant_go<TX, TPR, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
   }
 }
 
 template <typename TX>
 static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const float* gain, float eps,
                                   int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
-                                  float* absmax, cudaStream_t s) {
+                                  float* absmax, cudaStream_t s, int norm) {
   const int kp = (k + kKAlign - 1) / kKAlign * kKAlign;
   const int nvp = kp / QVec<TX>::N;   // vectors per (padded) row
   // smallest threads-per-row with <= 8 vectors per thread
   if (nvp <= 32 * 8)
-    quant_nv<TX, 32>((nvp + 31) / 32, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+    quant_nv<TX, 32>((nvp + 31) / 32, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
   else if (nvp <= 64 * 8)
-    quant_nv<TX, 64>((nvp + 63) / 64, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+    quant_nv<TX, 64>((nvp + 63) / 64, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
   else if (nvp <= 128 * 8)
-    quant_nv<TX, 128>((nvp + 127) / 128, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+    quant_nv<TX, 128>((nvp + 127) / 128, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
   else if (nvp <= 256 * 8)
-    quant_nv<TX, 256>((nvp + 255) / 256, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s);
+    quant_nv<TX, 256>((nvp + 255) / 256, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();
@@ -245,13 +395,13 @@ static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const floa
 
 cudaError_t launch_quant(const void* x, int xdt, int m, int k, int ldx, const float* gain,
                          float eps, int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
-                         float* absmax, cudaStream_t s) {
+                         float* absmax, cudaStream_t s, int norm) {
   if (m == 0) return cudaSuccess;
   if (xdt == TERN_BF16)
     return quant_dispatch(static_cast<const __nv_bfloat16*>(x), m, k, ldx, gain, eps, q, ldq, deq,
-                          qsum, inv_rms, absmax, s);
+                          qsum, inv_rms, absmax, s, norm);
   return quant_dispatch(static_cast<const float*>(x), m, k, ldx, gain, eps, q, ldq, deq, qsum,
-                        inv_rms, absmax, s);
+                        inv_rms, absmax, s, norm);
 }
 
 }  // namespace tern

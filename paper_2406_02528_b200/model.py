@@ -54,9 +54,11 @@ class Block:
 
     def __init__(self, latent: dict, d: int, l: int, gate=L.TERN_GATE_SIGMOID_H, eps=1e-6,
                  gains: dict | None = None, biases: dict | None = None, device="cuda",
-                 shard=None):
+                 shard=None, norm=L.TERN_NORM_RMS):
         """shard = (rank, AllGather) for an output-feature-sharded block (shard.py);
-        latent holds the FULL matrices, gains/biases this rank's slices."""
+        latent holds the FULL matrices, gains/biases this rank's slices.  norm: the
+        norm in front of every BitLinear (TERN_NORM_RMS, or TERN_NORM_CENTERED =
+        Alg. 1's centred form)."""
         self.d, self.l = d, l
         dev = torch.device(device)
         lat = {k: v.to(dev) for k, v in latent.items()}
@@ -96,9 +98,9 @@ class Block:
             bias_fcg = torch.cat([biases.get(k, z).float().cpu() for k in ("f", "c", "g")])
         self.mix = L.tern_mlgru(self.fcg.struct, self.o.struct, dp(gains.get("x")),
                                 dp(gains.get("o")), dp(bias_fcg), dp(biases.get("o")), int(gate),
-                                float(eps))
+                                float(eps), int(norm))
         self.ch = L.tern_glu(self.gu.struct, self.down.struct, dp(gains.get("x1")),
-                             dp(gains.get("p")), float(eps))
+                             dp(gains.get("p")), float(eps), int(norm))
         self.struct = L.tern_block(self.mix, self.ch, d, l)
         if shard is not None:
             from . import shard as S
@@ -141,7 +143,7 @@ class Stack:
 
     @classmethod
     def random(cls, cfg: synth.Config, device="cuda", gate=L.TERN_GATE_SIGMOID_H, n_blocks=None,
-               gen_device=None, keep_latents=0, shard=None):
+               gen_device=None, keep_latents=0, shard=None, norm=L.TERN_NORM_RMS):
         """Build cfg's stack from seeded N(0, 0.02) latents (drawn per block on
         gen_device, packed on the GPU and dropped).  keep_latents=n keeps the
         first n blocks' latents on the host (for oracle parity)."""
@@ -153,7 +155,7 @@ class Stack:
             if i < keep_latents:
                 kept.append({k: v.cpu() for k, v in lat.items()})
             blocks.append(Block(lat, cfg.d, cfg.l, gate=gate, eps=cfg.eps, device=device,
-                                shard=shard))
+                                shard=shard, norm=norm))
             del lat
         st = cls(blocks, cfg.d, cfg.l, synth.torch_dtype(cfg.dtype), device)
         st.gather = None if shard is None else shard[1]
