@@ -29,9 +29,15 @@
 namespace tern {
 
 constexpr int kGThreads = 512;
+// Per-dot-lane q sums folded into the quant step (fp32 rows) or recomputed by
+// every warp from the q row (bf16 rows): measured c2 (fp32) decode 2391 -> 2451
+// tok/s with the fold, c4 (bf16) 1005 -> 888 -- kept per activation type.
+template <typename TX> struct LqFold { static constexpr bool on = sizeof(TX) == 4; };
 constexpr int kGWarps = kGThreads / 32;
 // 16-byte activation vectors per thread per row (register tile of the prologue)
-template <int MM> struct GNVX { static constexpr int v = MM <= 2 ? 4 : 2; };
+// (2 vectors cover every config row: fp32 K <= 4096, bf16 K <= 8192; a deeper
+// tile only adds predicated-off registers -- 4 made the bf16 kernel spill)
+template <int MM> struct GNVX { static constexpr int v = 2; };
 
 struct GemvArgs {
   const void* x;
@@ -176,16 +182,24 @@ __device__ __forceinline__ void gemv_pre(const GemvArgs& a, int unit, int warp, 
 
 // From the input rows to the stored outputs: fused RMSNorm + int8 quant of the
 // M rows (a2), wait for the weights (bar, parity), dot (a3) and epilogue.
-template <int MM, typename TX, typename TY>
+// CENT: Alg. 1's centred norm (reading C22) instead of RMSNorm (compile-time,
+// so the default path carries none of its code).
+template <int MM, typename TX, typename TY, bool CENT>
 __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint32_t* swd,
                                          int8_t* qs, uint64_t* wbar, uint32_t parity,
                                          const float (&msc)[3], const float (&pre)[4],
                                          double (*red_d)[kGWarps], float (*red_m)[kGWarps],
-                                         long long pt0) {
+                                         int (*lq_s)[kGWarps][32], long long pt0) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const Epi& e = a.epi;
   const int nkb = a.Kp >> 7;
   const int SW = a.sw_stride;
+  // per-lane sums of the q bytes each dot lane will visit (filled by the quant
+  // step below; every block barrier before the first use orders the zeroing)
+  if (LqFold<TX>::on) {
+#pragma unroll
+    for (int m = 0; m < MM; ++m) lq_s[m][warp][lane] = 0;
+  }
   // ---------------- prologue: fused RMSNorm + int8 quant (a2) of the M rows.
   // x in registers (kGNVX 16-byte vectors per thread per row); sum(x^2) in
   // binary64 (C4), max|x|; one block barrier for the partials, every warp then
@@ -209,7 +223,7 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
   float mu[MM];
 #pragma unroll
   for (int m = 0; m < MM; ++m) mu[m] = 0.0f;
-  const bool cent = a.norm == TERN_NORM_CENTERED;
+  constexpr bool cent = CENT;
   if (cent) {
 #pragma unroll
     for (int m = 0; m < MM; ++m) {
@@ -306,7 +320,7 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
 #pragma unroll
         for (int j = 0; j < VE; ++j)
           if (v < nvec)
-            am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(__fsub_rn(xf[j], mu[m]), rinv[m]),
+            am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(CENT ? __fsub_rn(xf[j], mu[m]) : xf[j], rinv[m]),
                                            __ldg(a.gain + v * VE + j))));
       }
       am = warp_max_f32(am);
@@ -324,6 +338,7 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
   for (int m = 0; m < MM; ++m) {
     const float sc = amax[m] > 0.0f ? __fdiv_rn(127.0f, amax[m]) : 0.0f;
     int8_t* qrow = qs + m * a.Kp;
+    int tq = 0;   // this thread's q bytes, all in the 16-byte word range of one dot lane
 #pragma unroll
     for (int i = 0; i < kGNVX; ++i) {
       const int v = tid + i * kGThreads;
@@ -336,10 +351,11 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
           XVec<TX>::unpack(xv[m][i], xf);
 #pragma unroll
           for (int j = 0; j < VE; ++j) {
-            float y = __fmul_rn(__fsub_rn(xf[j], mu[m]), rinv[m]);   // mu = 0: RMSNorm
+            float y = __fmul_rn(CENT ? __fsub_rn(xf[j], mu[m]) : xf[j], rinv[m]);
             if (a.gain) y = __fmul_rn(y, __ldg(a.gain + v * VE + j));
             // |y*sc| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
             const int qi = (int)round_half_away(__fmul_rn(y, sc));
+            tq += qi;
             pk[j >> 2] |= ((uint32_t)qi & 0xffu) << (8 * (j & 3));
           }
         }
@@ -348,6 +364,15 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
         else
           *reinterpret_cast<uint2*>(qrow + v * 8) = make_uint2(pk[0], pk[VE / 4 - 1]);
       }
+    }
+    // vector v holds q bytes [v*VE, v*VE+VE) of word v*VE/16, read by dot lane
+    // (v*VE/16) % 32 -- the same lane for all of this thread's vectors; the
+    // 16/VE threads sharing a lane within the warp are adjacent
+    constexpr int G = 16 / VE;   // threads per dot lane in a warp (4 fp32, 2 bf16)
+    if (LqFold<TX>::on) {
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) tq += __shfl_xor_sync(0xffffffffu, tq, o);
+      if ((lane & (G - 1)) == 0) lq_s[m][warp][(tid / G) & 31] = tq;   // one writer per entry
     }
   }
   float deq[MM];
@@ -381,14 +406,21 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
   int lq[MM];
 #pragma unroll
   for (int m = 0; m < MM; ++m) lq[m] = 0;
-  for (int w = lane; w < W; w += 32) {
+  if (LqFold<TX>::on) {
 #pragma unroll
-    for (int m = 0; m < MM; ++m) {
-      const uint4 qv = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
-      lq[m] = dp4a_us(0x01010101u, qv.x, lq[m]);
-      lq[m] = dp4a_us(0x01010101u, qv.y, lq[m]);
-      lq[m] = dp4a_us(0x01010101u, qv.z, lq[m]);
-      lq[m] = dp4a_us(0x01010101u, qv.w, lq[m]);
+    for (int m = 0; m < MM; ++m)
+#pragma unroll
+      for (int w = 0; w < kGWarps; ++w) lq[m] += lq_s[m][w][lane];
+  } else {
+    for (int w = lane; w < W; w += 32) {
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        const uint4 qv = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
+        lq[m] = dp4a_us(0x01010101u, qv.x, lq[m]);
+        lq[m] = dp4a_us(0x01010101u, qv.y, lq[m]);
+        lq[m] = dp4a_us(0x01010101u, qv.z, lq[m]);
+        lq[m] = dp4a_us(0x01010101u, qv.w, lq[m]);
+      }
     }
   }
   TY* out = static_cast<TY*>(e.out);
@@ -476,12 +508,13 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
 }
 
 // One BitLinear per launch (PDL chain of launches).
-template <int MM, typename TX, typename TY>
+template <int MM, typename TX, typename TY, bool CENT>
 __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
   extern __shared__ __align__(128) uint8_t g_smem[];
   int8_t* qs = reinterpret_cast<int8_t*>(g_smem + (size_t)a.n_seg * (a.Kp >> 7) * a.sw_stride * 4);  // [MM][Kp]
   __shared__ double red_d[MM][kGWarps];
   __shared__ float red_m[MM][kGWarps];
+  __shared__ int lq_s[MM][kGWarps][32];
   __shared__ __align__(8) uint64_t wbar;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int unit = blockIdx.x;
@@ -525,7 +558,8 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
   if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 1] = gtimer();
   float pre[4];
   gemv_pre<TY>(a, unit, warp, lane, pre);
-  gemv_run<MM, TX, TY>(a, unit, sw_words(g_smem), qs, &wbar, 0, msc, pre, red_d, red_m, pt0);
+  gemv_run<MM, TX, TY, CENT>(a, unit, sw_words(g_smem), qs, &wbar, 0, msc, pre, red_d, red_m, lq_s,
+                             pt0);
   if (a.trace) {
     __syncthreads();
     if (tid == 0) {
@@ -659,6 +693,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_stack_decode(const __grid_cons
   int8_t* qs = reinterpret_cast<int8_t*>(g_smem + (size_t)sa.buf_words * 8);
   __shared__ double red_d[MM][kGWarps];
   __shared__ float red_m[MM][kGWarps];
+  __shared__ int lq_s[MM][kGWarps][32];
   __shared__ __align__(8) uint64_t wbar[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int unit = blockIdx.x;
@@ -701,9 +736,14 @@ __global__ void __launch_bounds__(kGThreads, 1) k_stack_decode(const __grid_cons
       __syncthreads();
     }
     if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 1] = gtimer();
-    if (unit * a.ch < a.n_out)
-      gemv_run<MM, TX, TY>(a, unit, wb0 + (p & 1) * sa.buf_words, qs, &wbar[p & 1],
-                           (uint32_t)(p >> 1) & 1u, msc, pre, red_d, red_m, 0);
+    if (unit * a.ch < a.n_out) {
+      if (a.norm == TERN_NORM_CENTERED)
+        gemv_run<MM, TX, TY, true>(a, unit, wb0 + (p & 1) * sa.buf_words, qs, &wbar[p & 1],
+                                   (uint32_t)(p >> 1) & 1u, msc, pre, red_d, red_m, lq_s, 0);
+      else
+        gemv_run<MM, TX, TY, false>(a, unit, wb0 + (p & 1) * sa.buf_words, qs, &wbar[p & 1],
+                                    (uint32_t)(p >> 1) & 1u, msc, pre, red_d, red_m, lq_s, 0);
+    }
     __syncthreads();
     if (a.trace && tid == 0) {
       a.trace[blockIdx.x * 16 + 2] = gtimer();
@@ -762,13 +802,14 @@ static size_t gemv_smem(int MM, int n_seg, int ch, int Kp) {
 template <int MM, typename TX, typename TY>
 static cudaError_t gemv_launch(const GemvArgs& a, int units, cudaStream_t s) {
   const size_t smem = gemv_smem(MM, a.n_seg, a.ch, a.Kp);
-  auto kern = k_gemv<MM, TX, TY>;
-  static size_t smem_set = 48 * 1024;
-  if (smem > smem_set) {
+  const bool cent = a.norm == TERN_NORM_CENTERED;
+  auto kern = cent ? k_gemv<MM, TX, TY, true> : k_gemv<MM, TX, TY, false>;
+  static size_t smem_set[2] = {48 * 1024, 48 * 1024};
+  if (smem > smem_set[cent]) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
-    smem_set = 200 * 1024;
+    smem_set[cent] = 200 * 1024;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(units);
