@@ -236,6 +236,16 @@ typedef struct {
   int32_t rank, world;
   tern_allgather_fn ag;
   void* ctx;
+  /* 1 = on the tensor-core path (B*T > gemv_max_m) the o',
+   * x1 and p gathers move int8 codes instead of activations: each rank sends
+   * binary64 partials of the row moments (one small gather per round: 1 for
+   * RMSNorm, 2 centred, +1 with a gain), every rank combines them in rank
+   * order, quantizes its own slice and the codes (+ int32 partial q-sums) are
+   * gathered -- 2x (bf16) / 4x (fp32) fewer bytes.  The summation order of the
+   * moments differs from world = 1, so results equal the oracle (and world = 1)
+   * except in the rare fp64-boundary cases of reading C4.  The block output y
+   * is still gathered whole.  0 (default): gather activations. */
+  int32_t gather_q;
 } tern_shard;
 
 typedef struct {

@@ -54,7 +54,7 @@ ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size
 
 class tern_shard(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("ag", ALLGATHER_FN),
-                ("ctx", C.c_void_p)]
+                ("ctx", C.c_void_p), ("gather_q", C.c_int32)]
 
 
 class tern_block(C.Structure):

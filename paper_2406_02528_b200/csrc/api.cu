@@ -146,7 +146,8 @@ Epi make_epi(int kind, const tern_weight& w, const float* bias, void* out, int l
 }
 
 struct BlockWs {
-  size_t q, deq, qsum, fcg, oprime, x1, p, sout, gbuf, part, part_bytes, total;
+  size_t q, deq, qsum, fcg, oprime, x1, p, sout, gbuf, stl, stg, qsend, qgath, part, part_bytes,
+      total;
 };
 // world > 1 adds the rank's local outputs [M][max(ds,ls)] and the gather
 // target [world][M][max(ds,ls)] (M > 1 gathers are then unshuffled to [M][width])
@@ -162,11 +163,16 @@ BlockWs block_ws(int32_t M, int32_t d, int32_t l, int32_t fcg_rows, tern_dtype d
   w.oprime = off; off += al256((size_t)M * d * dsize(dt));
   w.x1 = off; off += al256((size_t)M * d * dsize(dt));
   w.p = off; off += al256((size_t)M * (l > 0 ? l : 1) * dsize(dt));
-  w.sout = w.gbuf = off;
+  w.sout = w.gbuf = w.stl = w.stg = w.qsend = w.qgath = off;
   if (world > 1) {
     const size_t cs = (size_t)((d > l ? d : l) / world);
     w.sout = off; off += al256((size_t)M * cs * dsize(dt));
     w.gbuf = off; off += al256((size_t)world * M * cs * dsize(dt));
+    // int8-code gathers (tern_shard.gather_q): moment partials and code slices
+    w.stl = off; off += al256((size_t)M * 16);
+    w.stg = off; off += 3 * al256((size_t)world * M * 16);
+    w.qsend = off; off += al256((size_t)M * cs + 4 * (size_t)M);
+    w.qgath = off; off += al256((size_t)world * ((size_t)M * cs + 4 * (size_t)M));
   }
   // split-K partial sums for small M (decode batches above the GEMV limit)
   w.part = off;
@@ -623,6 +629,47 @@ tern_status shard_gather(const tern_shard& sh, const void* send, void* full, int
   return TERN_OK;
 }
 
+// f1(i): gather the next BitLinear's input as int8 codes (tern_shard.gather_q):
+// x_r [M][cs] this rank's slice (activations) -> q [M][kpad(K)], deq, qsum
+tern_status shard_gather_q(const tern_shard& sh, const void* x_r, int M, int cs, const float* gain,
+                           float eps, int norm, tern_dtype dt, void* ws, const BlockWs& L,
+                           cudaStream_t s) {
+  const int world = sh.world, K = cs * world;
+  double* stl = at<double>(ws, L.stl);
+  const double* st[3] = {nullptr, nullptr, nullptr};
+  const int rounds = slice_rounds(norm, gain != nullptr);
+  for (int rnd = 0; rnd < rounds; ++rnd) {
+    TRY_CUDA(launch_slice_stats(x_r, cs, M, cs, world, sh.rank, dt, gain, eps, norm, st, rnd, stl,
+                                s),
+             "slice stats");
+    double* g = at<double>(ws, L.stg + (size_t)rnd * al256((size_t)world * M * 16));
+    const int rc = sh.ag(sh.ctx, stl, g, (size_t)M * 16, (tern_stream)s);
+    if (rc != 0) return fail(TERN_ERR_CUDA, "all-gather callback failed (%d)", rc);
+    st[rnd] = g;
+  }
+  int8_t* send = at<int8_t>(ws, L.qsend);
+  TRY_CUDA(launch_slice_quant(x_r, cs, M, cs, world, sh.rank, dt, gain, eps, norm, st, send,
+                              at<float>(ws, L.deq), s),
+           "slice quant");
+  const size_t per = (size_t)M * cs + 4 * (size_t)M;
+  const int rc = sh.ag(sh.ctx, send, at<int8_t>(ws, L.qgath), per, (tern_stream)s);
+  if (rc != 0) return fail(TERN_ERR_CUDA, "all-gather callback failed (%d)", rc);
+  TRY_CUDA(launch_unshard_q(at<int8_t>(ws, L.qgath), world, M, cs, at<int8_t>(ws, L.q), kpad(K),
+                            at<int32_t>(ws, L.qsum), s),
+           "unshard q");
+  return TERN_OK;
+}
+
+// GEMM on the gathered codes (the quant already happened per slice)
+tern_status gemm_q(int M, int K, const tern_weight& w, tern_dtype dt, const Epi& e, void* ws,
+                   const BlockWs& L, cudaStream_t s) {
+  Prof pr(TERN_K_GEMM, e.kind, M, w.n_rows, K, w.n_seg, dt, s);
+  TRY_CUDA(launch_gemm(at<int8_t>(ws, L.q), M, kpad(K), at<float>(ws, L.deq),
+                       at<int32_t>(ws, L.qsum), w, dt, e, s, at<int32_t>(ws, L.part), L.part_bytes),
+           "gemm");
+  return TERN_OK;
+}
+
 // a8 with output-feature sharding (tern.h tern_shard): 4 gathers per block
 tern_status run_block_sharded(const tern_block& b, const void* x, void* y, tern_dtype dt, int B,
                               int T, float* h, void* ws, const BlockWs& L, cudaStream_t s) {
@@ -650,6 +697,24 @@ tern_status run_block_sharded(const tern_block& b, const void* x, void* y, tern_
     if ((st = bitlinear_any(false, x, dt, M, d, mx.gain_x, mx.eps, mx.fcg, e1, ws, L, s, mx.norm))) return st;
     Prof pr(TERN_K_SCAN, mx.gate, M, ds, ds, 3, dt, s);
     TRY_CUDA(launch_scan(fcg, dt, B, T, ds, mx.gate, h, sout, s), "scan");
+  }
+  if (sh.gather_q && !gv) {
+    // f1(i): o', x1 and p cross the ranks as int8 codes; x1 stays a local slice
+    void* x1r = x1;   // [M][ds]
+    if ((st = shard_gather_q(sh, sout, M, ds, mx.gain_o, mx.eps, mx.norm, dt, ws, L, s))) return st;
+    Epi e2 = make_epi(EPI_RESID, mx.o, mx.bias_o, x1r, ds);
+    e2.res = static_cast<const char*>(x) + (size_t)sh.rank * ds * es;
+    e2.ldr = d;
+    if ((st = gemm_q(M, d, mx.o, dt, e2, ws, L, s))) return st;
+    if ((st = shard_gather_q(sh, x1r, M, ds, gl.gain_x, gl.eps, gl.norm, dt, ws, L, s))) return st;
+    Epi e3 = make_epi(EPI_SWIGLU, gl.gu, nullptr, sout, ls);
+    if ((st = gemm_q(M, d, gl.gu, dt, e3, ws, L, s))) return st;
+    if ((st = shard_gather_q(sh, sout, M, ls, gl.gain_p, gl.eps, gl.norm, dt, ws, L, s))) return st;
+    Epi e4 = make_epi(EPI_RESID, gl.down, nullptr, sout, ds);
+    e4.res = x1r;
+    e4.ldr = ds;
+    if ((st = gemm_q(M, l, gl.down, dt, e4, ws, L, s))) return st;
+    return shard_gather(sh, sout, y, M, ds, dt, ws, L, s);
   }
   if ((st = shard_gather(sh, sout, op, M, ds, dt, ws, L, s))) return st;
   // o: x1_r = x[:, r] + o'(*)W_o[r]

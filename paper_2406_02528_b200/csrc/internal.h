@@ -115,6 +115,17 @@ cudaError_t launch_expand(const tern_weight& w, uint8_t* e8, cudaStream_t s);
 // sharding: full[m][r*cs + j] = gathered[r][m][j]
 cudaError_t launch_unshard(const void* gathered, int dt, int world, int M, int cs, void* full,
                            cudaStream_t s);
+// f1(i): sharded BitLinear input gathered as int8 codes (k_shard.cu).  st: the
+// gathered stat rounds so far ([world][M][2] doubles each, null if absent)
+int slice_rounds(int norm, bool gain);
+cudaError_t launch_slice_stats(const void* x, int ldx, int M, int cs, int world, int rank, int dt,
+                               const float* gain, float eps, int norm, const double* const* st,
+                               int rnd, double* out, cudaStream_t s);
+cudaError_t launch_slice_quant(const void* x, int ldx, int M, int cs, int world, int rank, int dt,
+                               const float* gain, float eps, int norm, const double* const* st,
+                               int8_t* send, float* deq, cudaStream_t s);
+cudaError_t launch_unshard_q(const int8_t* gathered, int world, int M, int cs, int8_t* q, int ldq,
+                             int32_t* qsum, cudaStream_t s);
 // a4 + a6 fused (prefill): f|c|g GEMM with the MLGRU scan in its epilogue
 bool fcgscan_supported(const tern_weight& w, int d);
 cudaError_t launch_fcgscan(const int8_t* q, int ldq, const float* deq, const int32_t* qsum,

@@ -142,5 +142,7 @@ class ThreadAllGather(AllGather):
         self.barrier.wait()   # all waits enqueued before the slots are reused
 
 
-def make_shard(gather: AllGather, rank: int) -> "L.tern_shard":
-    return L.tern_shard(rank, gather.world, gather.cb, C.c_void_p(rank))
+def make_shard(gather: AllGather, rank: int, gather_q: bool = False) -> "L.tern_shard":
+    """gather_q: move o', x1 and p between ranks as int8 codes + row-moment
+    partials instead of activations (tern.h tern_shard.gather_q)."""
+    return L.tern_shard(rank, gather.world, gather.cb, C.c_void_p(rank), int(bool(gather_q)))

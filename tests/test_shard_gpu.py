@@ -16,11 +16,11 @@ from paper_2406_02528_b200 import synth
 pytestmark = pytest.mark.gpu
 
 
-def _run(world, cfg, T, n_dec, B):
+def _run(world, cfg, T, n_dec, B, gather_q=False, norm=0):
     from paper_2406_02528_b200 import _lib as L
     from paper_2406_02528_b200 import model, shard
     L.load()
-    ref = model.Stack.random(cfg, device="cuda", gen_device="cpu")
+    ref = model.Stack.random(cfg, device="cuda", gen_device="cpu", norm=norm)
     x = synth.hidden((B, T + n_dec, cfg.d), synth.generator(3), cfg.dtype).cuda()
     hs = ref.new_state(B)
     ys = [ref.prefill(x[:, :T].contiguous(), hs)]
@@ -30,7 +30,8 @@ def _run(world, cfg, T, n_dec, B):
     yref = torch.cat(ys, 1)
 
     gather = shard.ThreadAllGather(world)
-    stacks = [model.Stack.random(cfg, device="cuda", gen_device="cpu", shard=(r, gather))
+    stacks = [model.Stack.random(cfg, device="cuda", gen_device="cpu", shard=(r, gather, gather_q),
+                                 norm=norm)
               for r in range(world)]
     outs, errs = [None] * world, []
 
@@ -70,3 +71,14 @@ def test_sharded_block_prefill_decode_bit_identical(world):
 def test_sharded_bf16_batch1_decode():
     cfg = synth.Config("shard_bf16", 1, 256, 512, "bf16", 22, 1, 33, 1, 4)
     _run(2, cfg, T=33, n_dec=4, B=1)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("dtype,norm", [("f32", 0), ("bf16", 1)])
+def test_sharded_int8_code_gathers(world, dtype, norm):
+    """tern_shard.gather_q: o', x1 and p cross the ranks as int8
+    codes after a binary64 moment exchange; prefill (M = 80) and decode with B = 8
+    run the tensor-core path that uses it.  Equal to the unsharded path (the moment
+    sums differ only in order: reading C4)."""
+    cfg = synth.Config("shard_q", 2, 512, 1024, dtype, 23, 8, 10, 8, 2)
+    _run(world, cfg, T=10, n_dec=2, B=8, gather_q=True, norm=norm)

@@ -1,5 +1,2 @@
-timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_stack_decode_gpu.py tests/test_norm_centered_gpu.py -x -q -k "bitlinear or decode or c0 or stack or persistent or centered" > gpurun_out/pytest_b.log 2>&1; echo tests=$?
-tail -2 gpurun_out/pytest_b.log
-for c in c2 c4; do
-timeout 600 python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --decode-steps 200 > /tmp/bb.log 2>&1; echo "$c: $(tail -1 /tmp/bb.log | python -c "import json,sys; D=json.loads(sys.stdin.read()); d=D['decode']; print(d['tokens_per_s'], d['ms_per_token_step'])")"
-done
+timeout 900 python -m pytest tests/test_shard_gpu.py -x -q > gpurun_out/pytest_s.log 2>&1; echo tests=$?
+tail -15 gpurun_out/pytest_s.log
