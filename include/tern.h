@@ -158,7 +158,10 @@ typedef struct {
   float* absmax;    /* [m]                                                    */
 } tern_bl_taps;
 
-/* Workspace bytes for bitlinear_fwd on m rows of k features. */
+/* Workspace bytes for bitlinear_fwd on m rows of k features.  For
+ * 4 < m <= 256 it includes room for split-K int32 partials (38.8 MB), which
+ * lets the GEMM spread few output tiles over all SMs; a smaller workspace
+ * (>= the m*Kp + 512-byte base) is accepted and runs without split-K. */
 size_t tern_bitlinear_workspace(int32_t m, int32_t k);
 
 /* a2-a5: BitLinear forward (Alg. 1 forward_pass):
@@ -167,7 +170,7 @@ size_t tern_bitlinear_workspace(int32_t m, int32_t k);
  * rounded to bf16 when ydt == TERN_BF16 (R1).
  * w must have n_seg == 1.  y: [m][ldy] of ydt, ldy >= w->n_out.
  * m <= tern_get_gemv_max_m() (and K within the GEMV's register tile: fp32
- * K <= 8192 at m <= 2, 4096 at m <= 4; bf16 twice that) runs the decode GEMV (norm+quant fused in its
+ * K <= 4096, bf16 K <= 8192) runs the decode GEMV (norm+quant fused in its
  * prologue); larger m runs tern_quant + the tcgen05 int8 GEMM. */
 tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, int32_t ldx,
                           const float* gain, float eps, const tern_weight* w, const float* bias,

@@ -383,8 +383,13 @@ tern_status tern_quant(const void* x, tern_dtype xdt, int32_t m, int32_t k, int3
   return TERN_OK;
 }
 
-size_t tern_bitlinear_workspace(int32_t m, int32_t k) {
+size_t bitlinear_ws_base(int32_t m, int32_t k) {
   return al256((size_t)m * kpad(k)) + 2 * al256((size_t)m * 4);
+}
+constexpr size_t kBlPartBytes = (size_t)2 * 148 * 128 * 256 * 4;   // split-K partials
+size_t tern_bitlinear_workspace(int32_t m, int32_t k) {
+  const bool splitk = m > kGemvMaxM && m <= kSplitKMaxM;
+  return bitlinear_ws_base(m, k) + (splitk ? kBlPartBytes : 0);
 }
 
 tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, int32_t ldx,
@@ -406,9 +411,8 @@ tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, i
     CHECK(!taps->acc || taps->ldacc >= w->n_rows, "bitlinear_fwd: taps ldacc");
   }
   if (!gemv) {
-    CHECK(ws && aligned16(ws) && ws_bytes >= tern_bitlinear_workspace(m, k),
-          "bitlinear_fwd: workspace too small (%zu < %zu)", ws_bytes,
-          tern_bitlinear_workspace(m, k));
+    CHECK(ws && aligned16(ws) && ws_bytes >= bitlinear_ws_base(m, k),
+          "bitlinear_fwd: workspace too small (%zu < %zu)", ws_bytes, bitlinear_ws_base(m, k));
     CHECK(k <= 16384, "bitlinear_fwd: k too large");
   }
   st = check_device();
@@ -435,8 +439,16 @@ tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, i
   const int ldq = (taps && taps->q) ? taps->ldq : kpad(k);
   float* deq = (taps && taps->deq) ? taps->deq : at<float>(ws, al256((size_t)m * kpad(k)));
   int32_t* qsum = at<int32_t>(ws, al256((size_t)m * kpad(k)) + al256((size_t)m * 4));
+  // split-K partials behind the base workspace when the caller provided them
+  const size_t base = bitlinear_ws_base(m, k);
+  int32_t* part = nullptr;
+  size_t part_bytes = 0;
+  if (m <= kSplitKMaxM && ws_bytes >= base + kBlPartBytes && !(taps && taps->acc)) {
+    part = at<int32_t>(ws, base);
+    part_bytes = ws_bytes - base;
+  }
   return bl_tc(x, xdt, m, k, ldx, gain, eps, *w, ydt, e, q, ldq, deq, qsum,
-               taps ? taps->inv_rms : nullptr, taps ? taps->absmax : nullptr, s, nullptr, 0,
+               taps ? taps->inv_rms : nullptr, taps ? taps->absmax : nullptr, s, part, part_bytes,
                g_norm_mode);
 }
 

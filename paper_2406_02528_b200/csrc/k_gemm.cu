@@ -761,7 +761,10 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
     if (!part || part_bytes < slice) return cudaErrorInvalidValue;
     int ks = num_sms / tiles;   // one round of work units over the SMs
     if (ks < 1) ks = 1;
-    if (ks > 4) ks = 4;   // the slices' int32 partials cost L2 traffic: few, long K slices
+    // the slices' int32 partials cost L2 traffic (ks * M * n * 4 bytes): few, long K
+    // slices -- except for very small M, where that traffic is negligible
+    const int ks_cap = M <= 64 ? 16 : 4;
+    if (ks > ks_cap) ks = ks_cap;
     if (ks > a.num_kb) ks = a.num_kb;
     if ((size_t)ks * slice > part_bytes) ks = (int)(part_bytes / slice);
     a.kb_per = (a.num_kb + ks - 1) / ks;
