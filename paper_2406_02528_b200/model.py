@@ -202,6 +202,52 @@ class Stack:
             self._blk_arr = (L.tern_block * len(self.blocks))(*[b.struct for b in self.blocks])
         return self._blk_arr
 
+    def prefill_host(self, xs_host: list, ys_host: list, before_step=None) -> None:
+        """Serve a sequence of independent prefill requests host to host: each
+        pinned [B][T][d] input in xs_host is copied to the device, run through
+        the stack from h = 0, and its output copied into the pinned ys_host
+        entry.  Copies run on their own streams, double-buffered, so request
+        i+1's upload and request i-1's download overlap request i's compute.
+        before_step(i), if given, is called before request i's compute is
+        enqueued (bench.py flushes L2 there).  Returns when every output has
+        landed on the host."""
+        if not xs_host:
+            return
+        B, T, d = xs_host[0].shape
+        main = torch.cuda.current_stream(self.device)
+        up, down = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
+        xin = [torch.empty((B, T, d), dtype=self.dtype, device=self.device) for _ in range(2)]
+        yout = [torch.empty_like(xin[0]) for _ in range(2)]
+        bufs = (torch.empty_like(xin[0]), torch.empty_like(xin[0]))
+        states = self.new_state(B)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_free = [torch.cuda.Event() for _ in range(2)]    # xin[k] consumed
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_drained = [torch.cuda.Event() for _ in range(2)]  # yout[k] copied out
+        for k in range(2):
+            ev_free[k].record(main)
+            ev_drained[k].record(main)
+        for i, (xh, yh) in enumerate(zip(xs_host, ys_host)):
+            k = i % 2
+            with torch.cuda.stream(up):
+                up.wait_event(ev_free[k])
+                xin[k].copy_(xh, non_blocking=True)
+                ev_in[k].record(up)
+            main.wait_event(ev_in[k])
+            main.wait_event(ev_drained[k])
+            for h in states:
+                h.zero_()
+            if before_step is not None:
+                before_step(i)
+            self.prefill(xin[k], states, out=yout[k], bufs=bufs)
+            ev_free[k].record(main)
+            ev_out[k].record(main)
+            with torch.cuda.stream(down):
+                down.wait_event(ev_out[k])
+                yh.copy_(yout[k], non_blocking=True)
+                ev_drained[k].record(down)
+        main.wait_stream(down)
+
     def decode(self, x: torch.Tensor, states: list, out: torch.Tensor | None = None,
                bufs=None, persistent: bool | None = None) -> torch.Tensor:
         """One decode step: x [B][d] -> y [B][d] through all blocks.
