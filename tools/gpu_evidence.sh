@@ -11,3 +11,4 @@ CMD="python bench.py --steps 2 --warmup 3 --decode-steps 4 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 2500 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu.log 2>&1; echo ncul=$?
 CMD2="python tools/prof_block.py --reps 2"
 $CMD2 > gpurun_out/pf_plain.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_gemm_tc|k_quant|k_fcgscan" -s 8 -c 8 -o gpurun_out/prof_block $CMD2 > gpurun_out/ncu_pf.log 2>&1; echo ncuf=$?
+timeout 900 python tools/c1_sweep.py --out gpurun_out/c1_sweep.json > gpurun_out/c1.log 2>&1; echo c1=$?
