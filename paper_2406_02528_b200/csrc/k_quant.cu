@@ -379,6 +379,12 @@ static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const floa
                                   float* absmax, cudaStream_t s, int norm) {
   const int kp = (k + kKAlign - 1) / kKAlign * kKAlign;
   const int nvp = kp / QVec<TX>::N;   // vectors per (padded) row
+  // few rows (decode batches): latency-bound, so spread each row over 256
+  // threads (<= 4 vectors each) instead of maximising per-thread work
+  if (m <= 256 && nvp > 64 && nvp <= 256 * 4) {
+    quant_nv<TX, 256>((nvp + 255) / 256, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
+    return cudaGetLastError();
+  }
   // smallest threads-per-row with <= 8 vectors per thread
   if (nvp <= 32 * 8)
     quant_nv<TX, 32>((nvp + 31) / 32, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);

@@ -1,3 +1,4 @@
-timeout 600 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline --decode-steps 50 > gpurun_out/bb.log 2>&1; echo rc=$?
-tail -1 gpurun_out/bb.log | python -c "import json,sys; D=json.loads(sys.stdin.read()); print(D['value'], D['e2e'])"
-tail -3 gpurun_out/bb.log | head -2
+timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_norm_centered_gpu.py -x -q -k "quant or batched" > gpurun_out/pb.log 2>&1; echo tests=$?; tail -1 gpurun_out/pb.log
+for c in "c3" "c4 --decode-batch 128"; do
+timeout 600 python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --decode-steps 100 > /tmp/bb.log 2>&1; echo "$c: $(tail -1 /tmp/bb.log | python -c "import json,sys; D=json.loads(sys.stdin.read()); d=D['decode']; print(d['tokens_per_s'], d['ms_per_token_step'])")"
+done
