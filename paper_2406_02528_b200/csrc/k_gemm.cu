@@ -622,37 +622,53 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
   const float dq = __ldg(deq + m);
   const int qs = __ldg(qsum + m);
   const int64_t sl = (int64_t)M * n_rows;
-  auto acc_at = [&](int pcol) {
-    int v = 0;
-    for (int k = 0; k < ksplit; ++k) v += part[k * sl + (int64_t)m * n_rows + pcol];
-    return v - qs;
-  };
-  auto val = [&](int pcol, int seg, int r) {
-    float o = __fmul_rn(i2f_small(acc_at(pcol)), __fmul_rn(dq, __ldg(e.scales + seg)));
+  // int32 sums over the K slices of packed columns (col, col+1) of row m, minus
+  // qsum: one 8-byte load per slice (n_rows and col are even)
+  const int* prow = part + (int64_t)m * n_rows;
+  auto dqv = [&](int acc, int seg, int r) {
+    float o = __fmul_rn(i2f_small(acc), __fmul_rn(dq, __ldg(e.scales + seg)));
     if (e.bias) o = __fadd_rn(o, __ldg(e.bias + seg * e.n_out + r));
     return storage_round<TY>(o);
   };
   TY* out = static_cast<TY*>(e.out);
-  if (chan) {
-    const int r0 = c, r1 = min(c + 1, e.n_out - 1);
+  if (chan) {   // n_out even: channels c, c+1 share a 64-row group (c even)
+    const int nseg = e.kind == EPI_SWIGLU ? 2 : 3;
+    int2 a[3] = {make_int2(0, 0), make_int2(0, 0), make_int2(0, 0)};
+    for (int k = 0; k < ksplit; ++k) {
+#pragma unroll
+      for (int sg = 0; sg < 3; ++sg) {
+        if (sg < nseg) {
+          const int2 v = __ldg(reinterpret_cast<const int2*>(prow + k * sl + packed_row(sg, c, nseg)));
+          a[sg].x += v.x;
+          a[sg].y += v.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int sg = 0; sg < 3; ++sg) {
+      a[sg].x -= qs;
+      a[sg].y -= qs;
+    }
+    const int r0 = c, r1 = c + 1;
     if (e.kind == EPI_SWIGLU) {   // p = SiLU(g) u
-      const float g0 = val(packed_row(0, r0, 2), 0, r0), g1 = val(packed_row(0, r1, 2), 0, r1);
-      const float u0 = val(packed_row(1, r0, 2), 1, r0), u1 = val(packed_row(1, r1, 2), 1, r1);
+      const float g0 = dqv(a[0].x, 0, r0), g1 = dqv(a[0].y, 0, r1);
+      const float u0 = dqv(a[1].x, 1, r0), u1 = dqv(a[1].y, 1, r1);
       float s0, s1;
       sigmoid2(g0, g1, s0, s1);
       st_act<TY>(out + (int64_t)m * e.ldo + r0, __fmul_rn(__fmul_rn(g0, s0), u0));
-      if (c + 1 < e.n_out) st_act<TY>(out + (int64_t)m * e.ldo + r1, __fmul_rn(__fmul_rn(g1, s1), u1));
+      st_act<TY>(out + (int64_t)m * e.ldo + r1, __fmul_rn(__fmul_rn(g1, s1), u1));
     } else {                      // MLGRU step: f, c -> h, o'
-      const float f0 = val(packed_row(0, r0, 3), 0, r0), f1 = val(packed_row(0, r1, 3), 0, r1);
-      const float c0 = val(packed_row(1, r0, 3), 1, r0), c1 = val(packed_row(1, r1, 3), 1, r1);
-      const float g0 = val(packed_row(2, r0, 3), 2, r0), g1 = val(packed_row(2, r1, 3), 2, r1);
+      float* hp = e.h + (int64_t)m * e.n_out;
+      const float2 hv = *reinterpret_cast<const float2*>(hp + r0);
+      const float f0 = dqv(a[0].x, 0, r0), f1 = dqv(a[0].y, 0, r1);
+      const float c0 = dqv(a[1].x, 1, r0), c1 = dqv(a[1].y, 1, r1);
+      const float g0 = dqv(a[2].x, 2, r0), g1 = dqv(a[2].y, 2, r1);
       float sf0, sf1, sc0, sc1;
       sigmoid2(f0, c0, sf0, sc0);
       sigmoid2(f1, c1, sf1, sc1);
-      float* hp = e.h + (int64_t)m * e.n_out;
-      const float h0 = __fadd_rn(__fmul_rn(sf0, hp[r0]),
+      const float h0 = __fadd_rn(__fmul_rn(sf0, hv.x),
                                  __fmul_rn(__fsub_rn(1.0f, sf0), __fmul_rn(c0, sc0)));
-      const float h1 = __fadd_rn(__fmul_rn(sf1, hp[r1]),
+      const float h1 = __fadd_rn(__fmul_rn(sf1, hv.y),
                                  __fmul_rn(__fsub_rn(1.0f, sf1), __fmul_rn(c1, sc1)));
       float o0, o1;
       if (e.gate == TERN_GATE_SIGMOID_H) {
@@ -664,14 +680,18 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
         o0 = __fmul_rn(g0, h0);
         o1 = __fmul_rn(g1, h1);
       }
-      hp[r0] = h0;
+      *reinterpret_cast<float2*>(hp + r0) = make_float2(h0, h1);
       st_act<TY>(out + (int64_t)m * e.ldo + r0, o0);
-      if (c + 1 < e.n_out) {
-        hp[r1] = h1;
-        st_act<TY>(out + (int64_t)m * e.ldo + r1, o1);
-      }
+      st_act<TY>(out + (int64_t)m * e.ldo + r1, o1);
     }
     return;
+  }
+  // one segment or the interleaved f|c|g columns: columns c, c+1 (c even)
+  int2 a = make_int2(0, 0);
+  for (int k = 0; k < ksplit; ++k) {
+    const int2 v = __ldg(reinterpret_cast<const int2*>(prow + k * sl + c));
+    a.x += v.x;
+    a.y += v.y;
   }
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
@@ -683,7 +703,7 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
       r = (col / (kSegRows * e.n_seg)) * kSegRows + (col % kSegRows);
       if (r >= e.n_out) continue;
     }
-    float o = val(col, seg, r);
+    float o = dqv((j == 0 ? a.x : a.y) - qs, seg, r);
     if (e.kind == EPI_RESID)
       o = __fadd_rn(ld_act<TY>(static_cast<const TY*>(e.res) + (int64_t)m * e.ldr + r), o);
     st_act<TY>(out + (int64_t)m * e.ldo + (e.kind == EPI_FCG ? col : r), o);
@@ -754,8 +774,9 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   }
   const int tiles = a.n_tiles * a.m_tiles;
   const size_t slice = (size_t)M * w.n_rows * sizeof(int32_t);
+  // (the split-K epilogue reads column pairs: even n_rows, true for every fused group)
   const bool finalize = ks_out != nullptr || epi.kind == EPI_MLGRU ||
-                        (part && part_bytes >= slice && epi.kind != EPI_NONE &&
+                        (part && part_bytes >= slice && epi.kind != EPI_NONE && w.n_rows % 2 == 0 &&
                          epi.acc == nullptr && tiles * 2 <= num_sms && a.num_kb >= 2);
   if (finalize) {
     if (!part || part_bytes < slice) return cudaErrorInvalidValue;
