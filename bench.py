@@ -298,6 +298,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     from paper_2406_02528_b200 import model, synth
 
     L.load()
+    if os.environ.get("TERN_BENCH_FIN") is not None:   # debug: batched-decode finalize path
+        L.tern_set_batched_fin(int(os.environ["TERN_BENCH_FIN"]))
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     pk = peaks()

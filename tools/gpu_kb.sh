@@ -1,5 +1,5 @@
-timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_norm_centered_gpu.py tests/test_stack_decode_gpu.py tests/test_shard_gpu.py -x -q -k "bitlinear or batched or decode or shard or zero" > gpurun_out/pb.log 2>&1; echo tests=$?; tail -1 gpurun_out/pb.log
+for fin in 0 1; do
 for c in "c3" "c4 --decode-batch 128"; do
-timeout 600 python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --decode-steps 100 > /tmp/bb.log 2>&1; echo "$c: $(tail -1 /tmp/bb.log | python -c "import json,sys; D=json.loads(sys.stdin.read()); d=D['decode']; print(d['tokens_per_s'], d['ms_per_token_step'])")"
+TERN_BENCH_FIN=$fin timeout 600 python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --decode-steps 100 > /tmp/bb.log 2>&1; echo "fin=$fin $c: $(tail -1 /tmp/bb.log | python -c "import json,sys; D=json.loads(sys.stdin.read()); d=D['decode']; print(d['tokens_per_s'], d['ms_per_token_step'])")"
 done
-timeout 600 python tools/c1_sweep.py --ms 16,256 > gpurun_out/c1b.log 2>&1; tail -1 gpurun_out/c1b.log
+done
