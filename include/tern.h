@@ -368,7 +368,10 @@ int32_t tern_trace_collect(uint64_t* out, int32_t max_launches);
  * which = 1: sigmoid equals 1/(1+exp_c(-x)) with IEEE division at 2^24
  * points in [-96, 96);
  * which = 2: the paired vector sigmoid of the scan / SwiGLU epilogue equals
- * the same except that results below 2^-126 may be 0.
+ * the same except that results below 2^-126 may be 0;
+ * which = 3: the conversion-free round half away from zero used by every
+ * quantizer (and its integer extraction) equals the reference for every
+ * float with |v| < 2^22. 
  * Synchronous; writes the mismatch count to *mismatches (host).  ws: device
  * scratch of >= 64 bytes. */
 tern_status tern_selftest(int32_t which, void* ws, uint64_t* mismatches);

@@ -138,6 +138,19 @@ __device__ __forceinline__ float round_half_away(float v) {
   return t;
 }
 
+// The same for |v| < 2^22 without the conversion pipe (truncf is an FRND, and
+// the float->int that follows an F2I, both on the 16/clk/SM conversion unit):
+// v + 1.5*2^23 rounds to nearest even; a tie (|v - r| == 0.5, exact) is moved
+// away from zero.  Equal to round_half_away on that range (tern_selftest 3).
+__device__ __forceinline__ float round_half_away_small(float v) {
+  const float r = __fsub_rn(__fadd_rn(v, 12582912.0f), 12582912.0f);
+  return fabsf(__fsub_rn(v, r)) == 0.5f ? __fadd_rn(v, copysignf(0.5f, v)) : r;
+}
+// integral float |r| < 2^22 -> int, also on the FP32 pipe
+__device__ __forceinline__ int int_of_integral(float r) {
+  return __float_as_int(__fadd_rn(r, 12582912.0f)) - 0x4B400000;
+}
+
 // bf16 storage rounding (R0-R3): round to nearest even and widen back.
 __device__ __forceinline__ float bf16r(float v) {
   return __bfloat162float(__float2bfloat16_rn(v));

@@ -240,8 +240,8 @@ __global__ void __launch_bounds__(kFinThreads, 1) k_fin(const FinArgs a) {
         v1 = __fmul_rn(v1, g.y);
       }
       // |v*sc| <= 127(1+2^-23): the clamp to [-128,127] (C5) never acts
-      const int q0 = __float2int_rz(round_half_away(__fmul_rn(v0, sc)));
-      const int q1 = __float2int_rz(round_half_away(__fmul_rn(v1, sc)));
+      const int q0 = int_of_integral(round_half_away_small(__fmul_rn(v0, sc)));
+      const int q1 = int_of_integral(round_half_away_small(__fmul_rn(v1, sc)));
       qsum += q0 + q1;
       *reinterpret_cast<uint16_t*>(qr + 2 * p) = (uint16_t)((q0 & 0xff) | ((q1 & 0xff) << 8));
     }

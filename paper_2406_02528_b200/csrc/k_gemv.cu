@@ -354,7 +354,7 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
             float y = __fmul_rn(CENT ? __fsub_rn(xf[j], mu[m]) : xf[j], rinv[m]);
             if (a.gain) y = __fmul_rn(y, __ldg(a.gain + v * VE + j));
             // |y*sc| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
-            const int qi = (int)round_half_away(__fmul_rn(y, sc));
+            const int qi = int_of_integral(round_half_away_small(__fmul_rn(y, sc)));
             tq += qi;
             pk[j >> 2] |= ((uint32_t)qi & 0xffu) << (8 * (j & 3));
           }

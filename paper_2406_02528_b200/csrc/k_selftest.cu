@@ -5,6 +5,7 @@
 //   1: sigmoid_c(x) == 1/(1+exp_c(-x)) with IEEE division over a dense x sweep
 //   2: sigmoid2 (the paired vector sigmoid) == the same, except that results
 //      below 2^-126 may be 0, over the same sweep
+//   3: the conversion-free round half away from zero (and int extraction)
 #include "common.cuh"
 
 namespace tern {
@@ -44,6 +45,22 @@ __global__ void k_selftest_sigmoid(unsigned long long* bad) {
   if (__float_as_uint(a) != __float_as_uint(b) && !(a != a && b != b)) atomicAdd(bad, 1ull);
 }
 
+// 3: round_half_away_small == round_half_away and int_of_integral == (int)
+//    for every float with |v| < 2^22 (both signs, exponent fields 0..148)
+__global__ void k_selftest_rha(unsigned long long* bad) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;  // mantissa
+  if (m >= (1u << 23)) return;
+  unsigned long long nb = 0;
+  for (uint32_t ex = 0; ex <= 148; ++ex)
+    for (uint32_t sg = 0; sg < 2; ++sg) {
+      const float v = __uint_as_float((sg << 31) | (ex << 23) | m);
+      const float a = round_half_away_small(v), b = round_half_away(v);
+      nb += __float_as_uint(a) != __float_as_uint(b) && !(a == 0.0f && b == 0.0f);
+      nb += int_of_integral(b) != (int)b;
+    }
+  if (nb) atomicAdd(bad, nb);
+}
+
 cudaError_t launch_selftest(int which, unsigned long long* bad, int* exps, int n_exp,
                             cudaStream_t s) {
   (void)exps;
@@ -52,8 +69,10 @@ cudaError_t launch_selftest(int which, unsigned long long* bad, int* exps, int n
     k_selftest_rcp<<<(1 << 23) / 256, 256, 0, s>>>(bad);
   } else if (which == 1) {
     k_selftest_sigmoid<<<(1 << 24) / 256, 256, 0, s>>>(bad);
-  } else {
+  } else if (which == 2) {
     k_selftest_sigmoid2<<<(1 << 23) / 256, 256, 0, s>>>(bad);
+  } else {
+    k_selftest_rha<<<(1 << 23) / 256, 256, 0, s>>>(bad);
   }
   return cudaGetLastError();
 }

@@ -142,7 +142,7 @@ __global__ void k_slice_quant(const SliceNorm a, int rounds, int8_t* __restrict_
       const float x = ld_x<TX>(a.x, (int64_t)m * a.ldx + j);
       float y = __fmul_rn(a.cent ? __fsub_rn(x, rs.mu) : x, rs.r);
       if (a.gain) y = __fmul_rn(y, __ldg(a.gain + a.rank * a.cs + j));
-      qi = __float2int_rz(round_half_away(__fmul_rn(y, sc)));   // |y sc| <= 127 (C5)
+      qi = int_of_integral(round_half_away_small(__fmul_rn(y, sc)));   // |y sc| <= 127 (C5)
     }
     send[(int64_t)m * a.cs + j] = (int8_t)qi;
     qs += qi;

@@ -62,7 +62,7 @@ def acts(shape, seed, dtype="f32"):
 
 
 # ------------------------------------------------------------------------ numerics shortcuts
-@pytest.mark.parametrize("which", [0, 1, 2])
+@pytest.mark.parametrize("which", [0, 1, 2, 3])
 def test_device_selftest(L, which):
     """The FMA-corrected reciprocals equal IEEE division on [1, 2^126); the scalar sigmoid
     equals 1/(1+exp_c(-x)); the paired vector sigmoid equals it wherever the result is a

@@ -1,5 +1,4 @@
-for fin in 0 1; do
-for c in "c3" "c4 --decode-batch 128"; do
-TERN_BENCH_FIN=$fin timeout 600 python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --decode-steps 100 > /tmp/bb.log 2>&1; echo "fin=$fin $c: $(tail -1 /tmp/bb.log | python -c "import json,sys; D=json.loads(sys.stdin.read()); d=D['decode']; print(d['tokens_per_s'], d['ms_per_token_step'])")"
-done
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_gpu.log
+for c in c2 c4; do
+timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --decode-steps 100 > /tmp/bb.log 2>&1; echo "$c: $(tail -1 /tmp/bb.log | python -c "import json,sys; D=json.loads(sys.stdin.read()); k=D['kernels']; d=D['decode']; print(D['value'], D['roofline']['frac'], k['quant']['ms_per_launch'], k['quant']['frac'], d['tokens_per_s'])")"
 done
