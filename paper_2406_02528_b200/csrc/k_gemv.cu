@@ -424,49 +424,77 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
     }
   }
   TY* out = static_cast<TY*>(e.out);
+  // MM == 1 and a warp owning >= 2 channels: channels j and j+1 share the q
+  // loads and their dot chains interleave (the c3/c4 gate|up phases have up to
+  // 3 channels per warp); results parked in accn[] for the second channel
+  int accn[3] = {0, 0, 0};
+  bool have_next = false;
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
     const int i = warp + j * kGWarps;
     if (i >= a.ch) break;
     const int rr = unit * a.ch + i;
-    int part[3][MM];
+    int acc[3] = {0, 0, 0};
+    if (have_next) {
 #pragma unroll
-    for (int sgi = 0; sgi < 3; ++sgi)
-#pragma unroll
-      for (int m = 0; m < MM; ++m) part[sgi][m] = -lq[m];
-    for (int w = lane; w < W; w += 32) {
-      uint4 qv[MM];
-#pragma unroll
-      for (int m = 0; m < MM; ++m) qv[m] = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
+      for (int sgi = 0; sgi < 3; ++sgi) acc[sgi] = accn[sgi];
+      have_next = false;
+    } else {
+      const int i2 = i + kGWarps;
+      const bool two = MM == 1 && j < 3 && i2 < a.ch;
+      int part[3][MM], part2[3];
 #pragma unroll
       for (int sgi = 0; sgi < 3; ++sgi) {
-        if (sgi < a.n_seg) {
-          const uint32_t wd = swd[(sgi * nkb + (w >> 3)) * SW + i * 8 + (w & 7)];
+        part2[sgi] = -lq[0];
 #pragma unroll
-          for (int m = 0; m < MM; ++m) {
-            const int f0 = dp4a_us(wd & 0x03030303u, qv[m].x, 0);
-            const int f1 = dp4a_us(wd & 0x0C0C0C0Cu, qv[m].y, 0);
-            const int f2 = dp4a_us(wd & 0x30303030u, qv[m].z, 0);
-            const int f3 = dp4a_us(wd & 0xC0C0C0C0u, qv[m].w, 0);
-            part[sgi][m] += f0 + (f1 >> 2) + (f2 >> 4) + (f3 >> 6);   // exact multiples
+        for (int m = 0; m < MM; ++m) part[sgi][m] = -lq[m];
+      }
+      for (int w = lane; w < W; w += 32) {
+        uint4 qv[MM];
+#pragma unroll
+        for (int m = 0; m < MM; ++m) qv[m] = *reinterpret_cast<const uint4*>(qs + m * a.Kp + w * 16);
+#pragma unroll
+        for (int sgi = 0; sgi < 3; ++sgi) {
+          if (sgi < a.n_seg) {
+            const uint32_t* wrow = swd + (sgi * nkb + (w >> 3)) * SW + (w & 7);
+            const uint32_t wd = wrow[i * 8];
+#pragma unroll
+            for (int m = 0; m < MM; ++m) {
+              const int f0 = dp4a_us(wd & 0x03030303u, qv[m].x, 0);
+              const int f1 = dp4a_us(wd & 0x0C0C0C0Cu, qv[m].y, 0);
+              const int f2 = dp4a_us(wd & 0x30303030u, qv[m].z, 0);
+              const int f3 = dp4a_us(wd & 0xC0C0C0C0u, qv[m].w, 0);
+              part[sgi][m] += f0 + (f1 >> 2) + (f2 >> 4) + (f3 >> 6);   // exact multiples
+            }
+            if (two) {
+              const uint32_t wd2 = wrow[i2 * 8];
+              const int f0 = dp4a_us(wd2 & 0x03030303u, qv[0].x, 0);
+              const int f1 = dp4a_us(wd2 & 0x0C0C0C0Cu, qv[0].y, 0);
+              const int f2 = dp4a_us(wd2 & 0x30303030u, qv[0].z, 0);
+              const int f3 = dp4a_us(wd2 & 0xC0C0C0C0u, qv[0].w, 0);
+              part2[sgi] += f0 + (f1 >> 2) + (f2 >> 4) + (f3 >> 6);
+            }
           }
         }
       }
-    }
-    if (j == 0) { GPROF(7) }
-    // all-reduce, then lane m keeps token m's accumulators
-    int acc[3] = {0, 0, 0};
+      // all-reduce, then lane m keeps token m's accumulators
 #pragma unroll
-    for (int sgi = 0; sgi < 3; ++sgi) {
-      if (sgi < a.n_seg) {
+      for (int sgi = 0; sgi < 3; ++sgi) {
+        if (sgi < a.n_seg) {
 #pragma unroll
-        for (int m = 0; m < MM; ++m) {
-          const int v = warp_allsum_i32(part[sgi][m]);
-          if (lane == m) acc[sgi] = v;
+          for (int m = 0; m < MM; ++m) {
+            const int v = warp_allsum_i32(part[sgi][m]);
+            if (lane == m) acc[sgi] = v;
+          }
+          if (two) {
+            const int v = warp_allsum_i32(part2[sgi]);
+            if (lane == 0) accn[sgi] = v;
+          }
         }
       }
+      have_next = two;
     }
-    if (j == 0) { GPROF(8) }
+    if (j == 0) { GPROF(7) }
     if (rr >= a.n_out || lane >= a.M) continue;
     const int m = lane;
     float dq = deq[0];

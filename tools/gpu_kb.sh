@@ -1,4 +1,4 @@
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_stack_decode_gpu.py -x -q -k "bitlinear or decode or c0 or persistent" > gpurun_out/pb.log 2>&1; echo tests=$?; tail -1 gpurun_out/pb.log
 for c in c2 c4; do
-timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --decode-steps 100 > /tmp/bb.log 2>&1; echo "$c: $(tail -1 /tmp/bb.log | python -c "import json,sys; D=json.loads(sys.stdin.read()); k=D['kernels']; d=D['decode']; print(D['value'], D['roofline']['frac'], k['quant']['ms_per_launch'], k['quant']['frac'], d['tokens_per_s'])")"
+timeout 600 python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --decode-steps 200 > /tmp/bb.log 2>&1; echo "$c: $(tail -1 /tmp/bb.log | python -c "import json,sys; D=json.loads(sys.stdin.read()); d=D['decode']; print(d['tokens_per_s'], d['ms_per_token_step'])")"
 done
