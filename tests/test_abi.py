@@ -73,6 +73,34 @@ def test_validation_rejects_before_launch(lib):
     assert st == L.TERN_ERR_INVALID_ARG
 
 
+def test_validation_of_the_later_entry_points(lib):
+    """stack_decode, the knobs and the self-test reject bad arguments up front."""
+    from paper_2406_02528_b200 import _lib as L
+    fake = C.c_void_p(0x1000)
+    harr = (C.c_void_p * 1)(0x2000)
+    st = lib.stack_decode(None, 0, fake, fake, 0, 1, harr, fake, 1 << 20, None)
+    assert st == L.TERN_ERR_INVALID_ARG and b"stack_decode" in lib.tern_last_error()
+    ws = C.create_string_buffer(64)
+    bad = C.c_uint64(0)
+    assert lib.tern_selftest(9, ws, C.byref(bad)) == L.TERN_ERR_INVALID_ARG
+    assert lib.tern_stack_decode_workspace(None, 0, 1, 0) == 0
+    # a block whose norm mode is out of range is rejected by the block checks
+    w3 = L.tern_weight(0x1000, 0x2000, 256, 256, 16, 3, 768)
+    w1 = L.tern_weight(0x1000, 0x2000, 256, 256, 16, 1, 256)
+    wgu = L.tern_weight(0x1000, 0x2000, 688, 256, 16, 2, 2 * 704)
+    wdn = L.tern_weight(0x1000, 0x2000, 256, 688, 48, 1, 256)
+    mix = L.tern_mlgru(w3, w1, None, None, None, None, 0, 1e-6, 7)
+    ch = L.tern_glu(wgu, wdn, None, None, 1e-6, 0)
+    blk = L.tern_block(mix, ch, 256, 688)
+    st = lib.block_decode(C.byref(blk), fake, C.c_void_p(0x5000), 0, 1, fake, fake, 1 << 30, None)
+    assert st == L.TERN_ERR_INVALID_ARG and b"norm" in lib.tern_last_error()
+    # knobs are clamped, not trusted
+    old = lib.tern_get_norm_mode()
+    lib.tern_set_norm_mode(5)
+    assert lib.tern_get_norm_mode() == 0
+    lib.tern_set_norm_mode(old)
+
+
 def test_product_path_has_no_fallback(tmp_path, monkeypatch):
     """The binding raises when the CUDA library is missing (no CPU fallback)."""
     import importlib
