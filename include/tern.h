@@ -235,6 +235,10 @@ typedef struct {
  * Requires ds % 64 == 0 and ls % 16 == 0.  world <= 1: no sharding. */
 typedef int (*tern_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes_per_rank,
                                  tern_stream stream);
+/* Sum of `count` int32 over the ranks into recv (recv may equal send), on
+ * `stream`; 0 = ok (a torch.distributed / NCCL all_reduce).  Exact. */
+typedef int (*tern_allreduce_fn)(void* ctx, const int32_t* send, int32_t* recv, size_t count,
+                                 tern_stream stream);
 typedef struct {
   int32_t rank, world;
   tern_allgather_fn ag;
@@ -249,6 +253,18 @@ typedef struct {
    * except in the rare fp64-boundary cases of reading C4.  The block output y
    * is still gathered whole.  0 (default): gather activations. */
   int32_t gather_q;
+  /* SURVEY 8(f) f1(ii), Megatron pairing: 1 = f|c|g and gate|up stay
+   * column-parallel (output rows [r*ds..), [r*ls..) as above) but W_o and
+   * W_down are ROW-parallel: rank r holds their input columns [r*ds, (r+1)*ds)
+   * and [r*ls, (r+1)*ls) for all d outputs (tern_weight k = ds / ls, n_out =
+   * d, packed with the full matrix's scale).  Each of o' and p then stays a
+   * local slice: its row moments are exchanged (as with gather_q), every rank
+   * quantizes its slice, multiplies it by its weight columns into int32
+   * partials of all d outputs, and `ar` sums them exactly -- 2 collectives of
+   * activations per block instead of 4, and x1 / y come out whole on every
+   * rank.  Requires ar; always the tensor-core path. */
+  int32_t megatron;
+  tern_allreduce_fn ar;
 } tern_shard;
 
 typedef struct {

@@ -52,9 +52,14 @@ class tern_glu(C.Structure):
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 
+# int ar(void* ctx, const int32_t* send, int32_t* recv, size_t count, cudaStream_t stream)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
 class tern_shard(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("ag", ALLGATHER_FN),
-                ("ctx", C.c_void_p), ("gather_q", C.c_int32)]
+                ("ctx", C.c_void_p), ("gather_q", C.c_int32), ("megatron", C.c_int32),
+                ("ar", ALLREDUCE_FN)]
 
 
 class tern_block(C.Structure):

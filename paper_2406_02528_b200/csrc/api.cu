@@ -146,13 +146,13 @@ Epi make_epi(int kind, const tern_weight& w, const float* bias, void* out, int l
 }
 
 struct BlockWs {
-  size_t q, deq, qsum, fcg, oprime, x1, p, sout, gbuf, stl, stg, qsend, qgath, part, part_bytes,
-      total;
+  size_t q, deq, qsum, fcg, oprime, x1, p, sout, gbuf, stl, stg, qsend, qgath, accb, part,
+      part_bytes, total;
 };
 // world > 1 adds the rank's local outputs [M][max(ds,ls)] and the gather
 // target [world][M][max(ds,ls)] (M > 1 gathers are then unshuffled to [M][width])
 BlockWs block_ws(int32_t M, int32_t d, int32_t l, int32_t fcg_rows, tern_dtype dt,
-                 int32_t world = 1) {
+                 int32_t world = 1, bool mega = false) {
   BlockWs w{};
   size_t off = 0;
   const int kq = kpad(d > l ? d : l);
@@ -174,6 +174,10 @@ BlockWs block_ws(int32_t M, int32_t d, int32_t l, int32_t fcg_rows, tern_dtype d
     w.qsend = off; off += al256((size_t)M * cs + 4 * (size_t)M);
     w.qgath = off; off += al256((size_t)world * ((size_t)M * cs + 4 * (size_t)M));
   }
+  // Megatron pairing: int32 partials of all d outputs + the q-sum partials,
+  // all-reduced together
+  w.accb = off;
+  if (world > 1 && mega) off += al256(((size_t)M * d + (size_t)M) * 4);
   // split-K partial sums for small M (decode batches above the GEMV limit)
   w.part = off;
   w.part_bytes = 0;
@@ -231,11 +235,21 @@ tern_status check_block(const tern_block* b) {
   const int ds = d / world, ls = l / world;
   tern_status st;
   if ((st = check_weight(&b->mix.fcg, d, 3, "fcg")) != TERN_OK) return st;
-  if ((st = check_weight(&b->mix.o, d, 1, "o")) != TERN_OK) return st;
+  const bool mega_w = world > 1 && b->shard.megatron;
+  if ((st = check_weight(&b->mix.o, mega_w ? ds : d, 1, "o")) != TERN_OK) return st;
   if ((st = check_weight(&b->ch.gu, d, 2, "gate|up")) != TERN_OK) return st;
-  if ((st = check_weight(&b->ch.down, l, 1, "down")) != TERN_OK) return st;
-  CHECK(b->mix.fcg.n_out == ds && b->mix.o.n_out == ds, "MLGRU weights must be d x d/world");
-  CHECK(b->ch.gu.n_out == ls && b->ch.down.n_out == ds, "GLU weights must be d->l/world, l->d/world");
+  if ((st = check_weight(&b->ch.down, mega_w ? ls : l, 1, "down")) != TERN_OK) return st;
+  const bool mega = world > 1 && b->shard.megatron;
+  CHECK(!mega || b->shard.ar, "Megatron-paired block: null all-reduce callback");
+  CHECK(b->mix.fcg.n_out == ds, "MLGRU f|c|g weights must be d -> d/world");
+  CHECK(b->ch.gu.n_out == ls, "GLU gate|up weights must be d -> l/world");
+  if (mega) {   // row-parallel o and down: input columns of this rank, all d outputs
+    CHECK(b->mix.o.n_out == d && b->mix.o.k == ds, "Megatron o must be d/world -> d");
+    CHECK(b->ch.down.n_out == d && b->ch.down.k == ls, "Megatron down must be l/world -> d");
+  } else {
+    CHECK(b->mix.o.n_out == ds, "MLGRU o weights must be d -> d/world");
+    CHECK(b->ch.down.n_out == ds, "GLU down weights must be l -> d/world");
+  }
   CHECK(b->mix.gate == TERN_GATE_SIGMOID_H || b->mix.gate == TERN_GATE_LINEAR_H, "bad gate mode");
   CHECK(b->mix.eps > 0 && b->ch.eps > 0, "eps must be > 0");
   CHECK((b->mix.norm == TERN_NORM_RMS || b->mix.norm == TERN_NORM_CENTERED) &&
@@ -495,13 +509,15 @@ size_t tern_glu_workspace(const tern_glu* p, int32_t m, int32_t d, int32_t l, te
 }
 size_t tern_block_workspace(const tern_block* b, int32_t B, int32_t T, tern_dtype dt) {
   if (!b) return 0;
-  return block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt, block_world(b)).total;
+  return block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt, block_world(b),
+                   b->shard.megatron != 0).total;
 }
 
 tern_status tern_block_ws_layout(const tern_block* b, int32_t B, int32_t T, tern_dtype dt,
                                  tern_block_taps* out) {
   CHECK(b && out, "tern_block_ws_layout: null pointer");
-  BlockWs w = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt, block_world(b));
+  BlockWs w = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt, block_world(b),
+                   b->shard.megatron != 0);
   out->fcg = w.fcg;
   out->oprime = w.oprime;
   out->x1 = w.x1;
@@ -660,7 +676,8 @@ tern_status shard_gather_q(const tern_shard& sh, const void* x_r, int M, int cs,
     st[rnd] = g;
   }
   int8_t* send = at<int8_t>(ws, L.qsend);
-  TRY_CUDA(launch_slice_quant(x_r, cs, M, cs, world, sh.rank, dt, gain, eps, norm, st, send,
+  TRY_CUDA(launch_slice_quant(x_r, cs, M, cs, world, sh.rank, dt, gain, eps, norm, st, send, cs,
+                              reinterpret_cast<int32_t*>(send + (size_t)M * cs),
                               at<float>(ws, L.deq), s),
            "slice quant");
   const size_t per = (size_t)M * cs + 4 * (size_t)M;
@@ -679,6 +696,46 @@ tern_status gemm_q(int M, int K, const tern_weight& w, tern_dtype dt, const Epi&
   TRY_CUDA(launch_gemm(at<int8_t>(ws, L.q), M, kpad(K), at<float>(ws, L.deq),
                        at<int32_t>(ws, L.qsum), w, dt, e, s, at<int32_t>(ws, L.part), L.part_bytes),
            "gemm");
+  return TERN_OK;
+}
+
+// f1(ii): a row-parallel BitLinear: x_r [M][cs] this rank's slice of the input
+// -> moments exchanged, slice quantized, int32 partials of all n outputs
+// (minus nothing: the q-sum partials ride along) -> all-reduce -> epilogue e
+tern_status rowpar_bitlinear(const tern_shard& sh, const void* x_r, int M, int cs,
+                             const float* gain, float eps, int norm, const tern_weight& w,
+                             const Epi& e, tern_dtype dt, void* ws, const BlockWs& L,
+                             cudaStream_t s) {
+  const int world = sh.world, n = w.n_out;
+  double* stl = at<double>(ws, L.stl);
+  const double* st[3] = {nullptr, nullptr, nullptr};
+  const int rounds = slice_rounds(norm, gain != nullptr);
+  for (int rnd = 0; rnd < rounds; ++rnd) {
+    TRY_CUDA(launch_slice_stats(x_r, cs, M, cs, world, sh.rank, dt, gain, eps, norm, st, rnd, stl,
+                                s),
+             "slice stats");
+    double* g = at<double>(ws, L.stg + (size_t)rnd * al256((size_t)world * M * 16));
+    const int rc = sh.ag(sh.ctx, stl, g, (size_t)M * 16, (tern_stream)s);
+    if (rc != 0) return fail(TERN_ERR_CUDA, "all-gather callback failed (%d)", rc);
+    st[rnd] = g;
+  }
+  int32_t* acc = at<int32_t>(ws, L.accb);        // [M][n] partials, then [M] q sums
+  int32_t* qs_r = acc + (size_t)M * n;
+  int8_t* q = at<int8_t>(ws, L.q);
+  TRY_CUDA(launch_slice_quant(x_r, cs, M, cs, world, sh.rank, dt, gain, eps, norm, st, q, kpad(cs),
+                              qs_r, at<float>(ws, L.deq), s),
+           "slice quant");
+  int ks = 1;   // one K slice: the partials go straight to the all-reduce
+  {
+    Prof pr(TERN_K_GEMM, EPI_NONE, M, w.n_rows, cs, 1, dt, s);
+    Epi ge = make_epi(EPI_NONE, w, nullptr, nullptr, 0);
+    TRY_CUDA(launch_gemm(q, M, kpad(cs), at<float>(ws, L.deq), qs_r, w, dt, ge, s, acc,
+                         (size_t)M * n * 4, &ks),
+             "gemm (row-parallel partials)");
+  }
+  const int rc = sh.ar(sh.ctx, acc, acc, (size_t)M * n + (size_t)M, (tern_stream)s);
+  if (rc != 0) return fail(TERN_ERR_CUDA, "all-reduce callback failed (%d)", rc);
+  TRY_CUDA(launch_splitk_epi(acc, 1, M, n, at<float>(ws, L.deq), qs_r, e, dt, s), "epilogue");
   return TERN_OK;
 }
 
@@ -709,6 +766,26 @@ tern_status run_block_sharded(const tern_block& b, const void* x, void* y, tern_
     if ((st = bitlinear_any(false, x, dt, M, d, mx.gain_x, mx.eps, mx.fcg, e1, ws, L, s, mx.norm))) return st;
     Prof pr(TERN_K_SCAN, mx.gate, M, ds, ds, 3, dt, s);
     TRY_CUDA(launch_scan(fcg, dt, B, T, ds, mx.gate, h, sout, s), "scan");
+  }
+  if (sh.megatron) {
+    // f1(ii): o and down row-parallel; o' and p never leave the rank, x1 and y
+    // are produced whole on every rank by the all-reduced epilogues
+    if ((st = rowpar_bitlinear(sh, sout, M, ds, mx.gain_o, mx.eps, mx.norm, mx.o,
+                               [&] {
+                                 Epi e2 = make_epi(EPI_RESID, mx.o, mx.bias_o, x1, d);
+                                 e2.res = x;
+                                 e2.ldr = d;
+                                 return e2;
+                               }(),
+                               dt, ws, L, s)))
+      return st;
+    Epi e3 = make_epi(EPI_SWIGLU, gl.gu, nullptr, sout, ls);
+    if ((st = bitlinear_any(false, x1, dt, M, d, gl.gain_x, gl.eps, gl.gu, e3, ws, L, s, gl.norm)))
+      return st;
+    Epi e4 = make_epi(EPI_RESID, gl.down, nullptr, y, d);
+    e4.res = x1;
+    e4.ldr = d;
+    return rowpar_bitlinear(sh, sout, M, ls, gl.gain_p, gl.eps, gl.norm, gl.down, e4, dt, ws, L, s);
   }
   if (sh.gather_q && !gv) {
     // f1(i): o', x1 and p cross the ranks as int8 codes; x1 stays a local slice
@@ -866,7 +943,8 @@ static tern_status block_run(const tern_block* b, const void* x, void* y, tern_d
   CHECK(valid_dt(dt), "%s: bad dtype", name);
   if (B * T == 0) return TERN_OK;   // no tokens: a no-op (buffers may be empty / NULL)
   CHECK(h, "%s: null state", name);
-  BlockWs L = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt, block_world(b));
+  BlockWs L = block_ws(B * T, b->d, b->l, b->mix.fcg.n_rows, dt, block_world(b),
+                   b->shard.megatron != 0);
   if ((st = check_act(x, y, ws, ws_bytes, L.total, dt, name)) != TERN_OK) return st;
   if ((st = check_device()) != TERN_OK) return st;
   if (B * T == 0) return TERN_OK;

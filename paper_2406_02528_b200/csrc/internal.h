@@ -71,7 +71,7 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
 // a4 (tcgen05 int8 GEMM): q [M][ldq] -> epilogue
 // part: optional int32 scratch [M][n_rows] enabling split-K for small M (nullptr: never)
 // ks_out: partials only (part required): the K-slice count is returned and no
-// epilogue runs (launch_fin finalizes)
+// epilogue runs (launch_fin finalizes); *ks_out > 0 on entry caps the count
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
                         int32_t* part = nullptr, size_t part_bytes = 0, int* ks_out = nullptr);
@@ -123,7 +123,11 @@ cudaError_t launch_slice_stats(const void* x, int ldx, int M, int cs, int world,
                                int rnd, double* out, cudaStream_t s);
 cudaError_t launch_slice_quant(const void* x, int ldx, int M, int cs, int world, int rank, int dt,
                                const float* gain, float eps, int norm, const double* const* st,
-                               int8_t* send, float* deq, cudaStream_t s);
+                               int8_t* q, int ldq, int32_t* qs_out, float* deq, cudaStream_t s);
+// the split-K epilogue on its own: sums ks int32 slices part[ks][M][n_rows] and
+// applies e (f1(ii): after the all-reduce of a row-parallel GEMM's partials)
+cudaError_t launch_splitk_epi(const int32_t* part, int ks, int M, int n_rows, const float* deq,
+                              const int32_t* qsum, const Epi& e, int ydt, cudaStream_t s);
 cudaError_t launch_unshard_q(const int8_t* gathered, int world, int M, int cs, int8_t* q, int ldq,
                              int32_t* qsum, cudaStream_t s);
 // a4 + a6 fused (prefill): f|c|g GEMM with the MLGRU scan in its epilogue

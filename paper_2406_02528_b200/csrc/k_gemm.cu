@@ -781,6 +781,7 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   if (finalize) {
     if (!part || part_bytes < slice) return cudaErrorInvalidValue;
     int ks = num_sms / tiles;   // one round of work units over the SMs
+    if (ks_out && *ks_out > 0 && ks > *ks_out) ks = *ks_out;
     if (ks < 1) ks = 1;
     // the slices' int32 partials cost L2 traffic (ks * M * n * 4 bytes): few, long K
     // slices -- except for very small M, where that traffic is negligible
@@ -817,6 +818,21 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
               : gemm_dispatch_bn<true, float>(BN, ta, tb, to, tr, a, s);
   return yb ? gemm_dispatch_bn<false, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)
             : gemm_dispatch_bn<false, float>(BN, ta, tb, to, tr, a, s);
+}
+
+cudaError_t launch_splitk_epi(const int32_t* part, int ks, int M, int n_rows, const float* deq,
+                              const int32_t* qsum, const Epi& epi, int ydt, cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  const bool chan = epi.kind == EPI_SWIGLU || epi.kind == EPI_MLGRU;
+  const int ncol = chan ? epi.n_out : (epi.kind == EPI_FCG ? n_rows : epi.n_out);
+  const int64_t n = (int64_t)M * ((ncol + 1) / 2);
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  unsigned long long* tr = trace_slot(TERN_K_GEMM + 16, (int)grid);
+  if (ydt == TERN_BF16)
+    return launch_pdl(k_splitk_epi<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, part, ks, M,
+                      n_rows, deq, qsum, epi, tr);
+  return launch_pdl(k_splitk_epi<float>, dim3(grid), dim3(256), 0, s, part, ks, M, n_rows, deq,
+                    qsum, epi, tr);
 }
 
 // ----------------------------------------------------------------- u8 expansion (kPre B)

@@ -128,8 +128,9 @@ __global__ void k_slice_stats(const SliceNorm a, int rnd, double* __restrict__ o
 // quantize this rank's slice with the combined row scalars: codes [M][cs] then
 // the row q-sum partials [M] (int32) behind them (one send buffer); deq [M]
 template <typename TX>
-__global__ void k_slice_quant(const SliceNorm a, int rounds, int8_t* __restrict__ send,
-                              float* __restrict__ deq) {
+// codes to q [M][ldq] (zero padded from cs to ldq), q-sum partials to qs_out [M]
+__global__ void k_slice_quant(const SliceNorm a, int rounds, int8_t* __restrict__ q, int ldq,
+                              int32_t* __restrict__ qs_out, float* __restrict__ deq) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= a.M) return;
   const int m = warp;
@@ -144,12 +145,13 @@ __global__ void k_slice_quant(const SliceNorm a, int rounds, int8_t* __restrict_
       if (a.gain) y = __fmul_rn(y, __ldg(a.gain + a.rank * a.cs + j));
       qi = int_of_integral(round_half_away_small(__fmul_rn(y, sc)));   // |y sc| <= 127 (C5)
     }
-    send[(int64_t)m * a.cs + j] = (int8_t)qi;
+    q[(int64_t)m * ldq + j] = (int8_t)qi;
     qs += qi;
   }
+  for (int j = a.cs + lane; j < ldq; j += 32) q[(int64_t)m * ldq + j] = 0;
   qs = warp_sum_i32(qs);
   if (lane == 0) {
-    reinterpret_cast<int32_t*>(send + (int64_t)a.M * a.cs)[m] = qs;
+    qs_out[m] = qs;
     deq[m] = rs.amax > 0.0f ? __fdiv_rn(rs.amax, 127.0f) : 0.0f;   // identical on every rank
   }
 }
@@ -212,15 +214,15 @@ cudaError_t launch_slice_stats(const void* x, int ldx, int M, int cs, int world,
 
 cudaError_t launch_slice_quant(const void* x, int ldx, int M, int cs, int world, int rank, int dt,
                                const float* gain, float eps, int norm, const double* const* st,
-                               int8_t* send, float* deq, cudaStream_t s) {
+                               int8_t* q, int ldq, int32_t* qs_out, float* deq, cudaStream_t s) {
   SliceNorm a = slice_norm(x, ldx, M, cs, world, rank, dt, gain, eps, norm);
   a.st0 = st[0];
   a.st1 = st[1];
   a.st2 = st[2];
   const int rounds = slice_rounds(norm, gain != nullptr);
   const unsigned grid = (unsigned)((M * 32 + 255) / 256);
-  if (dt == TERN_BF16) k_slice_quant<__nv_bfloat16><<<grid, 256, 0, s>>>(a, rounds, send, deq);
-  else k_slice_quant<float><<<grid, 256, 0, s>>>(a, rounds, send, deq);
+  if (dt == TERN_BF16) k_slice_quant<__nv_bfloat16><<<grid, 256, 0, s>>>(a, rounds, q, ldq, qs_out, deq);
+  else k_slice_quant<float><<<grid, 256, 0, s>>>(a, rounds, q, ldq, qs_out, deq);
   return cudaGetLastError();
 }
 

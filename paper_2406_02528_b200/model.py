@@ -55,7 +55,7 @@ class Block:
     def __init__(self, latent: dict, d: int, l: int, gate=L.TERN_GATE_SIGMOID_H, eps=1e-6,
                  gains: dict | None = None, biases: dict | None = None, device="cuda",
                  shard=None, norm=L.TERN_NORM_RMS):
-        """shard = (rank, AllGather[, gather_q]) for an output-feature-sharded block (shard.py);
+        """shard = (rank, AllGather[, gather_q[, megatron]]) for a sharded block (shard.py);
         latent holds the FULL matrices, gains/biases this rank's slices.  norm: the
         norm in front of every BitLinear (TERN_NORM_RMS, or TERN_NORM_CENTERED =
         Alg. 1's centred form)."""
@@ -66,8 +66,9 @@ class Block:
         if shard is not None:
             from . import shard as S
             rank, gather = shard[0], shard[1]
+            mega = len(shard) > 3 and bool(shard[3])
             sc = S.full_scales(lat, dev)
-            lat = S.shard_latents(lat, d, l, gather.world, rank)
+            lat = S.shard_latents(lat, d, l, gather.world, rank, megatron=mega)
         # which groups keep only the 2-bit codes (the prefill GEMM then unpacks B
         # tiles in shared memory instead of loading the u8 copy): debug knob
         packed_only = set(os.environ.get("TERN_PACKED_B", "").split(","))
@@ -104,7 +105,7 @@ class Block:
         self.struct = L.tern_block(self.mix, self.ch, d, l)
         if shard is not None:
             from . import shard as S
-            self.struct.shard = S.make_shard(shard[1], shard[0], *shard[2:3])
+            self.struct.shard = S.make_shard(shard[1], shard[0], *shard[2:4])
 
     @property
     def weight_bytes(self) -> int:

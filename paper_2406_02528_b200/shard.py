@@ -38,13 +38,20 @@ def plan(d: int, l: int, world: int, rank: int) -> dict:
             "gl": (rank * ls, (rank + 1) * ls)}
 
 
-def shard_latents(latent: dict, d: int, l: int, world: int, rank: int) -> dict:
-    """Row slices of one block's latent matrices for `rank` (see plan())."""
+def shard_latents(latent: dict, d: int, l: int, world: int, rank: int,
+                  megatron: bool = False) -> dict:
+    """Slices of one block's latent matrices for `rank` (see plan()): output rows
+    of every matrix, or with megatron the input COLUMNS of W_o
+    and W_down (row-parallel: [r*ds, (r+1)*ds) of o's and [r*ls, (r+1)*ls) of
+    down's inputs, all d outputs)."""
     p = plan(d, l, world, rank)
     c0, c1 = p["ch"]
     g0, g1 = p["gl"]
     out = {k: latent[k][c0:c1] for k in ("f", "c", "g", "o", "down")}
     out.update({k: latent[k][g0:g1] for k in ("gate", "up")})
+    if megatron:
+        out["o"] = latent["o"][:, c0:c1].contiguous()
+        out["down"] = latent["down"][:, g0:g1].contiguous()
     return out
 
 
@@ -63,6 +70,7 @@ class AllGather:
         self.world = world
         self._tensors = []
         self.cb = L.ALLGATHER_FN(self._call)
+        self.cb_ar = L.ALLREDUCE_FN(self._call_ar)
         self.error = None
 
     def register(self, *tensors):
@@ -91,6 +99,17 @@ class AllGather:
     def gather(self, rank, send, recv, nbytes, stream):
         raise NotImplementedError
 
+    def _call_ar(self, ctx, send, recv, count, stream):
+        try:
+            self.all_reduce(int(ctx or 0), int(send), int(recv), int(count), int(stream or 0))
+            return 0
+        except Exception as e:
+            self.error = e
+            return 1
+
+    def all_reduce(self, rank, send, recv, count, stream):
+        raise NotImplementedError
+
 
 class NcclAllGather(AllGather):
     """torch.distributed all-gather (NCCL) on the library's stream."""
@@ -107,6 +126,14 @@ class NcclAllGather(AllGather):
             self.dist.all_gather_into_tensor(self.view(recv, nbytes * self.world),
                                              self.view(send, nbytes), group=self.group)
 
+    def all_reduce(self, rank, send, recv, count, stream):
+        s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            r = self.view(recv, count * 4).view(torch.int32)
+            if send != recv:
+                r.copy_(self.view(send, count * 4).view(torch.int32))
+            self.dist.all_reduce(r, group=self.group)
+
 
 class ThreadAllGather(AllGather):
     """`world` virtual ranks as host threads on one GPU (one stream each).  At a
@@ -122,6 +149,8 @@ class ThreadAllGather(AllGather):
         self.ev = [None] * world
         self.ev2 = [None] * world
         self.streams = {}
+        self.lock = threading.Lock()
+        self.slots = None   # all-reduce staging: [world][n] int32
 
     def gather(self, rank, send, recv, nbytes, stream):
         s = torch.cuda.ExternalStream(stream)
@@ -141,8 +170,42 @@ class ThreadAllGather(AllGather):
             s.wait_event(self.ev2[r])
         self.barrier.wait()   # all waits enqueued before the slots are reused
 
+    def all_reduce(self, rank, send, recv, count, stream):
+        """Each rank stages its int32 vector, then every rank sums all of them
+        (in rank order; integer sums are exact anyway) into its recv."""
+        s = torch.cuda.ExternalStream(stream)
+        with self.lock:
+            if self.slots is None or self.slots.shape[1] < count:
+                self.slots = torch.empty((self.world, count), dtype=torch.int32,
+                                         device=torch.device("cuda"))
+        self.barrier.wait()   # slots allocated before anyone stages
+        slots = self.slots
+        with torch.cuda.stream(s):
+            slots[rank, :count].copy_(self.view(send, count * 4).view(torch.int32))
+        e = torch.cuda.Event()
+        e.record(s)
+        self.ev[rank] = e
+        self.barrier.wait()
+        with torch.cuda.stream(s):
+            for r in range(self.world):
+                s.wait_event(self.ev[r])
+            acc = slots[0, :count].clone()
+            for r in range(1, self.world):
+                acc += slots[r, :count]
+            self.view(recv, count * 4).view(torch.int32).copy_(acc)
+        e2 = torch.cuda.Event()
+        e2.record(s)
+        self.ev2[rank] = e2
+        self.barrier.wait()
+        for r in range(self.world):
+            s.wait_event(self.ev2[r])
+        self.barrier.wait()
 
-def make_shard(gather: AllGather, rank: int, gather_q: bool = False) -> "L.tern_shard":
+
+def make_shard(gather: AllGather, rank: int, gather_q: bool = False,
+               megatron: bool = False) -> "L.tern_shard":
     """gather_q: move o', x1 and p between ranks as int8 codes + row-moment
-    partials instead of activations (tern.h tern_shard.gather_q)."""
-    return L.tern_shard(rank, gather.world, gather.cb, C.c_void_p(rank), int(bool(gather_q)))
+    partials instead of activations (tern.h tern_shard.gather_q).
+    megatron: row-parallel o and down with exact int32 all-reduces (f1(ii))."""
+    return L.tern_shard(rank, gather.world, gather.cb, C.c_void_p(rank), int(bool(gather_q)),
+                        int(bool(megatron)), gather.cb_ar)

@@ -62,6 +62,59 @@ def _sharded_block(lat, x, H_shard, rank, world, gate):
     return y.reshape(Bx, Tx, D), H_shard
 
 
+def _allreduce_i64(a):
+    t = torch.from_numpy(np.ascontiguousarray(a.astype(np.int64)))
+    dist.all_reduce(t)
+    return t.numpy()
+
+
+def _rowpar_bitlinear(x_r, t_cols, m_w, K, eps=1e-6):
+    """Row-parallel BitLinear on rank's input slice x_r: the row
+    moments are exchanged (binary64 partials summed in rank order), the slice is
+    quantized with the shared r / absmax and its int32 products with
+    the weight columns are all-reduced (exact) before the dequantization."""
+    x64 = x_r.astype(np.float64)
+    ss = _gather(np.sum(x64 * x64, axis=1, keepdims=True))    # [M][world] partials
+    mx = _gather(np.max(np.abs(x_r), axis=1, keepdims=True).astype(np.float32))
+    ss_tot = np.zeros(ss.shape[0])
+    for r in range(ss.shape[1]):
+        ss_tot = ss_tot + ss[:, r]
+    r32 = (1.0 / np.sqrt(ss_tot / K + eps)).astype(np.float32)
+    amax = (np.max(mx, axis=1) * r32).astype(np.float32)
+    y = (x_r * r32[:, None]).astype(np.float32)
+    sc = np.where(amax > 0, np.float32(127.0) / np.where(amax > 0, amax, 1), 0).astype(np.float32)
+    v = (y * sc[:, None]).astype(np.float32)
+    q = np.clip(np.sign(v) * np.floor(np.abs(v) + np.float32(0.5)), -128, 127).astype(np.int64)
+    acc = _allreduce_i64(q @ t_cols.astype(np.int64).T)
+    deq = np.where(amax > 0, (amax / np.float32(127.0)).astype(np.float32), 0).astype(np.float32)
+    return (acc.astype(np.float32) * (deq * np.float32(m_w))[:, None]).astype(np.float32)
+
+
+def _megatron_block(lat, x, H_shard, rank, world, gate):
+    """Megatron-paired block (tern_shard.megatron): f|c|g and gate|up column-parallel,
+    o and down row-parallel with int32 all-reduces; x1 and y come out whole."""
+    p = shard.plan(D, LW, world, rank)
+    c0, c1 = p["ch"]
+    g0, g1 = p["gl"]
+    t, m = {}, {}
+    for k in lat:
+        t[k], m[k] = O.ternarize(lat[k])
+    Bx, Tx, _ = x.shape
+    X = x.reshape(Bx * Tx, D)
+    fh = O.bitlinear(X, t["f"][c0:c1], m["f"]).reshape(Bx, Tx, -1)
+    ch = O.bitlinear(X, t["c"][c0:c1], m["c"]).reshape(Bx, Tx, -1)
+    gh = O.bitlinear(X, t["g"][c0:c1], m["g"]).reshape(Bx, Tx, -1)
+    op, H_shard = O.mlgru_scan(fh, ch, gh, H_shard, gate_mode=gate)
+    o = _rowpar_bitlinear(op.reshape(Bx * Tx, -1), t["o"][:, c0:c1], m["o"], D)
+    x1 = (X + o).astype(np.float32)
+    gg = O.bitlinear(x1, t["gate"][g0:g1], m["gate"])
+    uu = O.bitlinear(x1, t["up"][g0:g1], m["up"])
+    p_s = O.silu_mul(gg, uu)
+    dn = _rowpar_bitlinear(p_s, t["down"][:, g0:g1], m["down"], LW)
+    y = (x1 + dn).astype(np.float32)
+    return y.reshape(Bx, Tx, D), H_shard
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -78,6 +131,10 @@ def _worker(rank, world, port, q):
             y0, Hs = _sharded_block(lat, x[:, :T], Hs, rank, world, gate)   # prefill
             y1, Hs = _sharded_block(lat, x[:, T:], Hs, rank, world, gate)   # decode step
             res[gate] = (y0, y1, _gather(Hs))
+            Hm = np.zeros((B, ds), np.float32)
+            m0, Hm = _megatron_block(lat, x[:, :T], Hm, rank, world, gate)
+            m1, Hm = _megatron_block(lat, x[:, T:], Hm, rank, world, gate)
+            res[("mega", gate)] = (m0, m1, _gather(Hm))
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -138,3 +195,7 @@ def test_two_rank_gloo_sharded_block_equals_unsharded_oracle():
             assert np.array_equal(g0, y0), f"prefill rank {r} gate {gate}"
             assert np.array_equal(g1, y1), f"decode rank {r} gate {gate}"
             assert np.array_equal(Hg, H), f"state rank {r} gate {gate}"
+            m0, m1, Hm = out[r][("mega", gate)]   # Megatron pairing (f1(ii))
+            assert np.array_equal(m0, y0), f"megatron prefill rank {r} gate {gate}"
+            assert np.array_equal(m1, y1), f"megatron decode rank {r} gate {gate}"
+            assert np.array_equal(Hm, H), f"megatron state rank {r} gate {gate}"

@@ -16,7 +16,7 @@ from paper_2406_02528_b200 import synth
 pytestmark = pytest.mark.gpu
 
 
-def _run(world, cfg, T, n_dec, B, gather_q=False, norm=0):
+def _run(world, cfg, T, n_dec, B, gather_q=False, norm=0, megatron=False):
     from paper_2406_02528_b200 import _lib as L
     from paper_2406_02528_b200 import model, shard
     L.load()
@@ -30,7 +30,7 @@ def _run(world, cfg, T, n_dec, B, gather_q=False, norm=0):
     yref = torch.cat(ys, 1)
 
     gather = shard.ThreadAllGather(world)
-    stacks = [model.Stack.random(cfg, device="cuda", gen_device="cpu", shard=(r, gather, gather_q),
+    stacks = [model.Stack.random(cfg, device="cuda", gen_device="cpu", shard=(r, gather, gather_q, megatron),
                                  norm=norm)
               for r in range(world)]
     outs, errs = [None] * world, []
@@ -82,3 +82,15 @@ def test_sharded_int8_code_gathers(world, dtype, norm):
     sums differ only in order: reading C4)."""
     cfg = synth.Config("shard_q", 2, 512, 1024, dtype, 23, 8, 10, 8, 2)
     _run(world, cfg, T=10, n_dec=2, B=8, gather_q=True, norm=norm)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("dtype,norm", [("f32", 0), ("bf16", 1)])
+def test_megatron_paired_sharding(world, dtype, norm):
+    """tern_shard.megatron: f|c|g and gate|up column-parallel, o and
+    down row-parallel with the int32 partials of all outputs summed by the all-reduce
+    callback (exact); prefill and decode (B = 1 takes the GEMV for f|c|g and the
+    tensor-core path for the row-parallel BitLinears).  Equal to the unsharded path up to
+    the order of the row-moment sums (reading C4)."""
+    cfg = synth.Config("shard_mg", 2, 512, 1024, dtype, 29, 2, 40, 2, 3)
+    _run(world, cfg, T=40, n_dec=3, B=2, norm=norm, megatron=True)
