@@ -402,11 +402,14 @@ tern_norm_mode tern_get_norm_mode(void);
  * 0 forces the tensor-core path everywhere).  Not thread-safe to change
  * while calls are in flight. */
 void tern_set_gemv_max_m(int32_t m);
-/* Tuning knob (host): 1 (default) runs the prefill f|c|g BitLinear and the
- * MLGRU scan as one fused kernel (k_fcgscan; needs the e8 weight copy and
- * d % 64 == 0), 0 runs GEMM + tern_mlgru_scan (then the f^c^g^ tap of
- * tern_block_ws_layout is written).  Results are identical. */
-void tern_set_fused_scan(int32_t on);
+/* Tuning knob (host): how prefill runs the f|c|g BitLinear and the MLGRU scan.
+ * 2 always as one fused kernel (k_fcgscan; needs the e8 weight copy and
+ * d % 64 == 0); 0 never: GEMM + tern_mlgru_scan (then the f^c^g^ tap of
+ * tern_block_ws_layout is written); 1 (default) fused when its 64-channel
+ * chains fill at least two thirds of the SMs (3*B*d/64 >= 2*#SMs), else
+ * unfused, whose scan spreads 8 channels per CTA.  Results are identical.  Values outside
+ * 0..2 are clamped. */
+void tern_set_fused_scan(int32_t mode);
 int32_t tern_get_fused_scan(void);
 int32_t tern_get_gemv_max_m(void);
 /* Tuning knob (host): 1 runs decode steps with gemv_max_m < B <= 256 as, per

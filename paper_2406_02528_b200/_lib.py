@@ -288,8 +288,11 @@ def tern_set_gemv_max_m(m: int):
     load().tern_set_gemv_max_m(int(m))
 
 
-def tern_set_fused_scan(on: bool):
-    load().tern_set_fused_scan(1 if on else 0)
+def tern_set_fused_scan(mode):
+    """True / 2: always the fused f|c|g+scan kernel; False / 0: never; 1: by grid size (default)."""
+    if isinstance(mode, bool):
+        mode = 2 if mode else 0
+    load().tern_set_fused_scan(int(mode))
 
 
 def tern_set_norm_mode(mode: int):
@@ -309,8 +312,8 @@ def tern_get_batched_fin() -> bool:
     return bool(load().tern_get_batched_fin())
 
 
-def tern_get_fused_scan() -> bool:
-    return bool(load().tern_get_fused_scan())
+def tern_get_fused_scan() -> int:
+    return int(load().tern_get_fused_scan())
 
 
 def tern_get_gemv_max_m() -> int:

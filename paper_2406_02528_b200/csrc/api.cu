@@ -313,7 +313,7 @@ int32_t tern_profile_collect(tern_prof_rec* out, int32_t max) {
   return out ? (n < max ? n : max) : n;
 }
 const char* tern_last_error(void) { return g_err.c_str(); }
-void tern_set_fused_scan(int32_t on) { g_fused_scan = on != 0; }
+void tern_set_fused_scan(int32_t mode) { g_fused_scan = mode < 0 ? 0 : mode > 2 ? 2 : mode; }
 int32_t tern_get_fused_scan(void) { return g_fused_scan; }
 void tern_set_gemv_max_m(int32_t m) { g_gemv_max_m = m < 0 ? 0 : (m > kGemvMaxM ? kGemvMaxM : m); }
 int32_t tern_get_gemv_max_m(void) { return g_gemv_max_m; }
@@ -574,7 +574,8 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
     tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
                            nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
     if (st) return st;
-  } else if (g_fused_scan && T >= 64 && fcgscan_supported(p.fcg, d)) {
+  } else if (T >= 64 && fcgscan_supported(p.fcg, d) &&
+             (g_fused_scan == 2 || (g_fused_scan == 1 && fcgscan_preferred(B, d)))) {
     // a4 + a6 fused: f^c^g^ stay on chip (k_fcgscan.cu)
     {
       Prof pr(TERN_K_QUANT, 0, M, 0, d, 0, dt, s);

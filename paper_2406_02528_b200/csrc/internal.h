@@ -136,6 +136,7 @@ cudaError_t launch_fcgscan(const int8_t* q, int ldq, const float* deq, const int
                            const tern_weight& w, const float* bias, int dt, int B, int T, int d,
                            int gate, float* h, void* oprime, cudaStream_t s);
 // a6
+bool fcgscan_preferred(int B, int d);
 cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
                         void* oprime, cudaStream_t s);
 

@@ -376,6 +376,21 @@ static cudaError_t fcgscan_go(const CUtensorMap& ta, const CUtensorMap& tb, cons
   return cudaGetLastError();
 }
 
+// The fused kernel runs one CTA per 64-channel chain of one sequence; below two thirds of
+// the SMs in chains (B*d/64 < 2*#SMs/3 = 98.7: c2 at B <= 6, c3 at B <= 3, c4 at B <= 2)
+// the unfused path (GEMM over all SMs + the 8-channel-wide scan, 8x more CTAs) is
+// faster or equal (measured).
+bool fcgscan_preferred(int B, int d) {
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (num_sms <= 0) num_sms = 148;
+  }
+  return (int64_t)B * (d / kFCW) * 3 >= 2 * (int64_t)num_sms;
+}
+
 bool fcgscan_supported(const tern_weight& w, int d) {
   return w.e8 != nullptr && w.n_seg == 3 && w.n_out == d && d % kFCW == 0 &&
          sizeof(FcgScanSmem) + 1024 <= 227 * 1024;

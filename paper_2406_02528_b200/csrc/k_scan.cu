@@ -4,45 +4,78 @@
 // The recurrence h_t = f_t h_{t-1} + (1-f_t) c_t is evaluated exactly in the
 // sequential order of its definition (h and o' bit-identical to the oracle);
 // only its two dependent operations per step stay sequential, everything
-// transcendental runs parallel over time.  One CTA = 32 channels of one
-// sequence, warp-specialised and pipelined over time tiles of kTS steps:
-//   warp 0 lane 0   TMA producer: 3 boxes [kTS steps x 32 ch] (f^, c^, g^ of the
+// transcendental runs parallel over time.  One CTA = kC (32, 16 or 8) channels of
+// one sequence, warp-specialised and pipelined over time tiles of kTS = 1024/kC steps:
+//   warp 0 lane 0   TMA producer: 3 boxes [kTS steps x kC ch] (f^, c^, g^ of the
 //                   fused interleaved pre-activations) per tile into a kS-deep ring
 //   warps 2..9      gates, phase 1 of tile i: f = sigma(f^), b = (1-f) SiLU(c^)
-//                   (parallel over time, lane = channel); then phase 3 of tile
-//                   i-1: o' = g^ sigma(h) (or g^ h) -> global
-//   warp 1          the carry: h = f h + b over the tile's steps, in order
-// so the serial carry of tile i overlaps the gate work of tiles i+1 and i-1,
+//                   (parallel over time and channels); then phase 3 of tile
+//                   i-kLag: o' = g^ sigma(h) (or g^ h) -> global
+//   warp 1          the carry: h = f h + b over the tile's steps, in order (lane = channel)
+// so the serial carry of tile i overlaps the gate work of the tiles around it,
 // and loads run kS tiles ahead.
+#include <cstdio>
+
 #include "epilogue.cuh"
 
 namespace tern {
 
-constexpr int kSCh = 32;                    // channels per CTA (one per lane)
-constexpr int kTS = 32;                     // time steps per tile
-constexpr int kS = 4;                       // ring stages
+// A tile holds kTE = 1024 (step, channel) elements: kC channels x kTS = kTE / kC
+// steps.  kC = 32 (lane = channel) when the grid B*d/32 already fills the SMs; for
+// small B*d the CTA narrows to 16 or 8 channels so that the gate arithmetic, which is
+// what bounds a CTA here (3 exact sigmoids per element on the FP32 pipe, ~45 cycles
+// per step at kC = 32), spreads over up to 4x more SMs.  The carry keeps one lane per
+// channel and walks kTS steps per tile.
+constexpr int kTE = 1024;
+constexpr int kSShallow = 4;                // ring stages when >= 1 CTA per SM is busy
+constexpr int kSDeep = 8;                   // ring stages for small grids
 constexpr int kGateWarps = 8;
-constexpr int kScanThreads = (2 + kGateWarps) * 32;
-constexpr int kStepsPerGateWarp = kTS / kGateWarps;
+// 12 warps: 0 producer, 1 carry, 5 and 9 idle, the other 8 the gates.  Warp w issues
+// from sub-partition w % 4, so the carry's dependent chain owns sub-partition 1 instead
+// of sharing its issue slots with two busy gate warps.
+constexpr int kScanThreads = 12 * 32;
+__device__ __forceinline__ int gate_warp_index(int warp) {   // -1: not a gate warp
+  return (warp < 2 || warp == 5 || warp == 9) ? -1 : warp - 2 - (warp > 5) - (warp > 9);
+}
+constexpr int kElemsPerLane = kTE / (kGateWarps * 32);   // 4
 
-template <typename T>
+// The carry reads (f, b) of two steps as one 16-byte word and writes h of four steps as
+// one: fb[(t/2)*kC + c] = (f_t, b_t, f_t+1, b_t+1), hs[(t/4)*kC + c] = (h_t .. h_t+3).
+// This keeps the chain's loads and stores (1/2 + 1/2 + 1/4 per step) off its critical
+// path: the loop then runs at the FMUL->FADD latency (measured, tools/micro).
+template <int kC>
+__device__ __forceinline__ int fb_word(int e) {   // word index of f for element e = t*kC + c
+  const int t = e / kC, c = e % kC;
+  return ((t >> 1) * kC + c) * 4 + (t & 1) * 2;
+}
+template <int kC>
+__device__ __forceinline__ int h_word(int e) {
+  const int t = e / kC, c = e % kC;
+  return ((t >> 2) * kC + c) * 4 + (t & 3);
+}
+
+template <typename T, int kS>
 struct ScanSmem {
-  T in[kS][3][kTS][kSCh];       // TMA destination: f^, c^, g^
-  float fh[kS][kTS][kSCh];      // f, then h after the carry
-  float bv[kS][kTS][kSCh];      // (1-f) c
+  T in[kS][3][kTE];                         // TMA destination: f^, c^, g^ boxes [kTS][kC]
+  __align__(16) float fb[kS][2 * kTE];      // (f, (1-f) c) pairs, layout above
+  __align__(16) float hs[kS][kTE];          // h after the carry, layout above
   uint64_t full[kS], gated[kS], scanned[kS], empty[kS];
 };
 
-template <typename T>
+template <typename T, int kS, int kC>
 __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ CUtensorMap tmX, int B,
                                                        int T_, int d, int gate,
-                                                       float* __restrict__ h, T* __restrict__ oprime) {
+                                                       float* __restrict__ h, T* __restrict__ oprime,
+                                                       unsigned long long* prof) {
+  // prof (debug, TERN_SCAN_PROF): per CTA [8] cycles: producer empty-wait, carry
+  // gated-wait, carry total, gate0 full-wait, phase 1, scanned-wait, phase 3, gate0 total
+  constexpr int kTS = kTE / kC;
   extern __shared__ __align__(128) uint8_t scan_smem[];
-  ScanSmem<T>& sm = *reinterpret_cast<ScanSmem<T>*>(scan_smem);
+  ScanSmem<T, kS>& sm = *reinterpret_cast<ScanSmem<T, kS>*>(scan_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cpb = d / kSCh;                       // channel blocks per sequence
+  const int cpb = d / kC;                         // channel blocks per sequence
   const int b = blockIdx.x / cpb;
-  const int c0 = (blockIdx.x % cpb) * kSCh;
+  const int c0 = (blockIdx.x % cpb) * kC;
   // interleaved fused layout: per 64-channel group [64 f | 64 c | 64 g]
   const int colf = (c0 / kSegRows) * (3 * kSegRows) + (c0 % kSegRows);
   const int nt = (T_ + kTS - 1) / kTS;
@@ -65,76 +98,117 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
     // ---------------- producer
     if (lane == 0) {
       tma_prefetch_desc(&tmX);
-      const uint32_t bytes = 3u * kTS * kSCh * sizeof(T);
+      const uint32_t bytes = 3u * kTE * sizeof(T);
       for (int i = 0; i < nt; ++i) {
         const int s = i % kS;
-        if (i >= kS) mbar_wait(&sm.empty[s], ((i / kS) - 1) & 1);
+        if (i >= kS) {
+          const long long w0 = prof ? clock64() : 0;
+          mbar_wait(&sm.empty[s], ((i / kS) - 1) & 1);
+          if (prof) prof[blockIdx.x * 8 + 0] += clock64() - w0;
+        }
         mbar_arrive_expect_tx(&sm.full[s], bytes);
         const int row = b * T_ + i * kTS;
 #pragma unroll
         for (int g = 0; g < 3; ++g)
-          tma_load_2d(&sm.in[s][g][0][0], &tmX, &sm.full[s], colf + g * kSegRows, row);
+          tma_load_2d(&sm.in[s][g][0], &tmX, &sm.full[s], colf + g * kSegRows, row);
       }
     }
   } else if (warp == 1) {
     // ---------------- the carry (exact definition order: (f*h) + ((1-f)*c))
-    float hc = h[(int64_t)b * d + c0 + lane];
-    for (int i = 0; i < nt; ++i) {
-      const int s = i % kS;
-      mbar_wait(&sm.gated[s], (i / kS) & 1);
-      const int steps = min(kTS, T_ - i * kTS);
-      if (steps == kTS) {
-#pragma unroll 8
-        for (int t = 0; t < kTS; ++t) {
-          hc = __fadd_rn(__fmul_rn(sm.fh[s][t][lane], hc), sm.bv[s][t][lane]);
-          sm.fh[s][t][lane] = hc;
+    if (lane < kC) {
+      float hc = h[(int64_t)b * d + c0 + lane];
+      const long long c_t0 = clock64();
+      long long c_w = 0;
+      for (int i = 0; i < nt; ++i) {
+        const int s = i % kS;
+        const long long w0 = clock64();
+        mbar_wait(&sm.gated[s], (i / kS) & 1);
+        c_w += clock64() - w0;
+        const int steps = min(kTS, T_ - i * kTS);
+        const float4* __restrict__ fb4 = reinterpret_cast<const float4*>(sm.fb[s]) + lane;
+        float4* __restrict__ hs4 = reinterpret_cast<float4*>(sm.hs[s]) + lane;
+        if (steps == kTS) {
+          // (f, b) of group g + 2 are loaded (in program order) before group g's h is
+          // stored, so the shared-memory latency overlaps the dependent chain
+          constexpr int kG = kTS / 4;   // groups of 4 steps
+          float4 pf[kG], qf[kG];
+          pf[0] = fb4[0], qf[0] = fb4[kC];
+          if (kG > 1) pf[1] = fb4[2 * kC], qf[1] = fb4[3 * kC];
+#pragma unroll
+          for (int g = 0; g < kG; ++g) {
+            if (g + 2 < kG) pf[g + 2] = fb4[(2 * g + 4) * kC], qf[g + 2] = fb4[(2 * g + 5) * kC];
+            const float4 p = pf[g], q = qf[g];
+            float4 o;
+            o.x = __fadd_rn(__fmul_rn(p.x, hc), p.y);
+            o.y = __fadd_rn(__fmul_rn(p.z, o.x), p.w);
+            o.z = __fadd_rn(__fmul_rn(q.x, o.y), q.y);
+            o.w = __fadd_rn(__fmul_rn(q.z, o.z), q.w);
+            hs4[g * kC] = o;
+            hc = o.w;
+          }
+        } else {
+          for (int t = 0; t < steps; ++t) {
+            const int e = t * kC + lane;
+            const float* fbw = &sm.fb[s][fb_word<kC>(e)];
+            hc = __fadd_rn(__fmul_rn(fbw[0], hc), fbw[1]);
+            sm.hs[s][h_word<kC>(e)] = hc;
+          }
         }
-      } else {
-        for (int t = 0; t < steps; ++t) {
-          hc = __fadd_rn(__fmul_rn(sm.fh[s][t][lane], hc), sm.bv[s][t][lane]);
-          sm.fh[s][t][lane] = hc;
-        }
+        __syncwarp(kC == 32 ? 0xffffffffu : (1u << (kC & 31)) - 1u);
+        if (lane == 0) mbar_arrive(&sm.scanned[s]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.scanned[s]);
+      h[(int64_t)b * d + c0 + lane] = hc;
+      if (prof && lane == 0) {
+        prof[blockIdx.x * 8 + 1] = c_w;
+        prof[blockIdx.x * 8 + 2] = clock64() - c_t0;
+      }
     }
-    h[(int64_t)b * d + c0 + lane] = hc;
-  } else {
-    // ---------------- gate warps
-    const int gw = warp - 2;
-    T* obase = oprime + (int64_t)b * T_ * d + c0 + lane;
+  } else if (gate_warp_index(warp) >= 0) {
+    // ---------------- gate warps: element e = (gw*4 + j)*32 + lane <-> (t = e / kC, c = e % kC)
+    const int gw = gate_warp_index(warp);
+    const int c = lane % kC;
+    T* obase = oprime + (int64_t)b * T_ * d + c0 + c;
+    const bool pr = prof && gw == 0 && lane == 0;
+    long long acc[5] = {0, 0, 0, 0, 0};
+    const long long g_t0 = clock64();
     auto phase1 = [&](int i) {
       const int s = i % kS;
+      long long w0 = clock64();
       mbar_wait(&sm.full[s], (i / kS) & 1);
-      float fv[kStepsPerGateWarp], bvv[kStepsPerGateWarp];
+      long long w1 = clock64();
+      acc[0] += w1 - w0;
+      float fv[kElemsPerLane], bvv[kElemsPerLane];
 #pragma unroll
-      for (int j = 0; j < kStepsPerGateWarp; ++j) {
-        const int t = gw * kStepsPerGateWarp + j;
-        const float fx = ld_act<T>(&sm.in[s][0][t][lane]);
-        const float cx = ld_act<T>(&sm.in[s][1][t][lane]);
+      for (int j = 0; j < kElemsPerLane; ++j) {
+        const int e = (gw * kElemsPerLane + j) * 32 + lane;
+        const float fx = ld_act<T>(&sm.in[s][0][e]);
+        const float cx = ld_act<T>(&sm.in[s][1][e]);
         float f, sc;
         sigmoid2(fx, cx, f, sc);
         fv[j] = f;
         bvv[j] = __fmul_rn(__fsub_rn(1.0f, f), __fmul_rn(cx, sc));   // (1-f) SiLU(c)
       }
 #pragma unroll
-      for (int j = 0; j < kStepsPerGateWarp; ++j) {
-        const int t = gw * kStepsPerGateWarp + j;
-        sm.fh[s][t][lane] = fv[j];
-        sm.bv[s][t][lane] = bvv[j];
+      for (int j = 0; j < kElemsPerLane; ++j) {
+        const int e = (gw * kElemsPerLane + j) * 32 + lane;
+        *reinterpret_cast<float2*>(&sm.fb[s][fb_word<kC>(e)]) = make_float2(fv[j], bvv[j]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.gated[s]);
+      acc[1] += clock64() - w1;
     };
     auto phase3 = [&](int i) {
       const int s = i % kS;
+      long long w0 = clock64();
       mbar_wait(&sm.scanned[s], (i / kS) & 1);
-      float ov[kStepsPerGateWarp];
+      long long w1 = clock64();
+      acc[2] += w1 - w0;
+      float ov[kElemsPerLane];
 #pragma unroll
-      for (int j = 0; j < kStepsPerGateWarp; j += 2) {
-        const int t = gw * kStepsPerGateWarp + j;
-        const float g0 = ld_act<T>(&sm.in[s][2][t][lane]), g1 = ld_act<T>(&sm.in[s][2][t + 1][lane]);
-        const float h0 = sm.fh[s][t][lane], h1 = sm.fh[s][t + 1][lane];
+      for (int j = 0; j < kElemsPerLane; j += 2) {
+        const int e = (gw * kElemsPerLane + j) * 32 + lane;
+        const float g0 = ld_act<T>(&sm.in[s][2][e]), g1 = ld_act<T>(&sm.in[s][2][e + 32]);
+        const float h0 = sm.hs[s][h_word<kC>(e)], h1 = sm.hs[s][h_word<kC>(e + 32)];
         if (gate == TERN_GATE_SIGMOID_H) {
           float s0, s1;
           sigmoid2(h0, h1, s0, s1);
@@ -148,47 +222,115 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);   // stage free once read
 #pragma unroll
-      for (int j = 0; j < kStepsPerGateWarp; ++j) {
-        const int t = i * kTS + gw * kStepsPerGateWarp + j;
+      for (int j = 0; j < kElemsPerLane; ++j) {
+        const int t = i * kTS + ((gw * kElemsPerLane + j) * 32 + lane) / kC;
         if (t < T_) st_act<T>(obase + (int64_t)t * d, ov[j]);
       }
+      acc[3] += clock64() - w1;
     };
+    // phase 1 runs kLag tiles ahead of phase 3 so that the carry warp finds the next
+    // tiles gated while the gate warps wait for it (kLag <= kS - 1: the stage phase 1
+    // fills next was released by a phase 3 already issued)
+    constexpr int kLag = kS >= 8 ? 4 : 1;
     for (int i = 0; i < nt; ++i) {
       phase1(i);
-      if (i > 0) phase3(i - 1);
+      if (i >= kLag) phase3(i - kLag);
     }
-    phase3(nt - 1);
+    for (int i = max(nt - kLag, 0); i < nt; ++i) phase3(i);
+    if (pr) {
+      for (int k = 0; k < 4; ++k) prof[blockIdx.x * 8 + 3 + k] = acc[k];
+      prof[blockIdx.x * 8 + 7] = clock64() - g_t0;
+    }
   }
 }
 
-template <typename TE>
-static cudaError_t scan_go(const CUtensorMap& tm, int grid, int B, int T, int d, int gate,
-                           float* h, void* oprime, cudaStream_t s) {
+template <typename TE, int kS, int kC>
+static cudaError_t scan_go(const void* fcg, int B, int T, int d, int gate, float* h,
+                           void* oprime, cudaStream_t s) {
   static bool attr = false;
-  const size_t smem = sizeof(ScanSmem<TE>);
+  const size_t smem = sizeof(ScanSmem<TE, kS>);
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan<TE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_scan<TE, kS, kC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(k_scan<TE>, dim3(grid), dim3(kScanThreads), smem, s, tm, B, T, d, gate, h,
-                    static_cast<TE*>(oprime));
+  const bool bf = sizeof(TE) == 2;
+  CUtensorMap tm;
+  if (!make_map_2d(&tm, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, fcg,
+                   (uint64_t)3 * d, (uint64_t)B * T, (uint64_t)3 * d * sizeof(TE), kC, kTE / kC,
+                   CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  const int grid = B * (d / kC);
+  static unsigned long long* dprof = nullptr;
+  static const bool prof_on = getenv("TERN_SCAN_PROF") != nullptr;
+  if (prof_on) {   // debug only: printed after a synchronous run
+    if (!dprof) cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * 4096);
+    cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * 8 * 4096, s);
+  }
+  cudaError_t e = launch_pdl(k_scan<TE, kS, kC>, dim3(grid), dim3(kScanThreads), smem, s, tm, B,
+                             T, d, gate, h, static_cast<TE*>(oprime), prof_on ? dprof : nullptr);
+  if (e != cudaSuccess || !prof_on || grid > 4096) return e;
+  static unsigned long long hp[8 * 4096];
+  cudaMemcpyAsync(hp, dprof, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  double sum[8] = {0};
+  for (int b = 0; b < grid; ++b)
+    for (int i = 0; i < 8; ++i) sum[i] += (double)hp[b * 8 + i] / grid;
+  fprintf(stderr,
+          "[scan prof] B=%d T=%d d=%d kC=%d kS=%d grid=%d | per CTA cycles: prod.empty=%.0f "
+          "carry.wait=%.0f carry.total=%.0f gate.full=%.0f phase1=%.0f gate.scanned=%.0f "
+          "phase3=%.0f gate.total=%.0f\n",
+          B, T, d, kC, kS, grid, sum[0], sum[1], sum[2], sum[3], sum[4], sum[5], sum[6], sum[7]);
+  return cudaGetLastError();
+}
+
+static int scan_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static int env_knob(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// Channel width: 8 (measured best at every c2 batch: the gate arithmetic
+// of a CTA is latency-bound, so 4x more, narrower CTAs win even when 32-wide ones fill
+// the SMs); TERN_SCAN_KC overrides with 16 or 32.  Ring depth: deep when the grid leaves
+// SMs idle (one CTA per SM then streams alone).
+template <typename TE>
+static cudaError_t scan_pick(const void* fcg, int B, int T, int d, int gate, float* h,
+                            void* oprime, cudaStream_t s) {
+  static const int kc_env = env_knob("TERN_SCAN_KC", 8);
+  static const int deep_env = env_knob("TERN_SCAN_DEEP", 2);  // 0 never, 1 always, 2 auto
+  const int sms = scan_num_sms();
+  int kc = (kc_env == 16 || kc_env == 32) ? kc_env : 8;
+  if (d % kc) kc = 8;
+  const bool deep = deep_env == 1 || (deep_env == 2 && (int64_t)B * (d / kc) < sms);
+#define TERN_SCAN_GO(S, C) scan_go<TE, S, C>(fcg, B, T, d, gate, h, oprime, s)
+  if (deep) {
+    if (kc == 8) return TERN_SCAN_GO(kSDeep, 8);
+    if (kc == 16) return TERN_SCAN_GO(kSDeep, 16);
+    return TERN_SCAN_GO(kSDeep, 32);
+  }
+  if (kc == 8) return TERN_SCAN_GO(kSShallow, 8);
+  if (kc == 16) return TERN_SCAN_GO(kSShallow, 16);
+  return TERN_SCAN_GO(kSShallow, 32);
+#undef TERN_SCAN_GO
 }
 
 cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
                         void* oprime, cudaStream_t s) {
   if (B == 0 || T == 0) return cudaSuccess;
-  const int grid = B * (d / kSCh);
-  const bool bf = dt == TERN_BF16;
-  const size_t es = bf ? 2 : 4;
-  CUtensorMap tm;
-  if (!make_map_2d(&tm, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, fcg,
-                   (uint64_t)3 * d, (uint64_t)B * T, (uint64_t)3 * d * es, kSCh, kTS,
-                   CU_TENSOR_MAP_SWIZZLE_NONE))
-    return cudaErrorInvalidValue;
-  return bf ? scan_go<__nv_bfloat16>(tm, grid, B, T, d, gate, h, oprime, s)
-            : scan_go<float>(tm, grid, B, T, d, gate, h, oprime, s);
+  return dt == TERN_BF16 ? scan_pick<__nv_bfloat16>(fcg, B, T, d, gate, h, oprime, s)
+                         : scan_pick<float>(fcg, B, T, d, gate, h, oprime, s);
 }
 
 }  // namespace tern

@@ -342,6 +342,7 @@ def test_fused_fcg_scan_equals_unfused(L, M, dtype, B, T, d, gate):
     st = M.Stack.random(cfg, gate=gate, gen_device="cpu")
     x = synth.hidden((B, T, d), synth.generator(4), dtype).cuda()
     outs = []
+    old = L.tern_get_fused_scan()
     for fused in (True, False):
         L.tern_set_fused_scan(fused)
         try:
@@ -350,7 +351,7 @@ def test_fused_fcg_scan_equals_unfused(L, M, dtype, B, T, d, gate):
             torch.cuda.synchronize()
             outs.append((y.clone(), h[0].clone()))
         finally:
-            L.tern_set_fused_scan(True)
+            L.tern_set_fused_scan(old)
     assert torch.equal(outs[0][0], outs[1][0]), "y differs"
     assert torch.equal(outs[0][1], outs[1][1]), "h differs"
 

@@ -19,8 +19,11 @@ ap.add_argument("--T", type=int, default=None)
 ap.add_argument("--blocks", type=int, default=2)
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--prefill", action="store_true")
+ap.add_argument("--unfused", action="store_true", help="GEMM + scan instead of the fused f|c|g+scan")
 args = ap.parse_args()
 L.load()
+if args.unfused:
+    L.tern_set_fused_scan(False)
 cfg = synth.CONFIGS[args.config]
 st = model.Stack.random(cfg, device="cuda", gen_device="cuda", n_blocks=args.blocks)
 B = args.B or (cfg.prefill_B if args.prefill else cfg.decode_B)
