@@ -104,6 +104,16 @@ def lib():
                                     C.c_int, C.c_int, C.c_float, C.c_int, C.c_int, f32p, f32p,
                                     C.c_void_p]
             L.orc_swiglu_arr.argtypes = [f32p, f32p, C.c_int64, C.c_int, f32p]
+            i16p = np.ctypeslib.ndpointer(np.int16, flags="C_CONTIGUOUS")
+            u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+            L.orc_fxp_scales.argtypes = [f32p, C.c_int, C.c_int, i8p, C.POINTER(C.c_int)]
+            L.orc_fxp_quant_act.argtypes = [f32p, C.c_int64, i16p, C.POINTER(C.c_int)]
+            L.orc_fxp_sigmoid.restype = C.c_int32
+            L.orc_fxp_sigmoid.argtypes = [C.c_int32]
+            L.orc_fxp_sigmoid_arr.argtypes = [i32p, i32p, C.c_int64]
+            L.orc_fxp_inv_sqrt_arr.argtypes = [u64p, i32p, C.c_int64, u32p, i32p]
+            L.orc_fxp_rmsnorm.argtypes = [i16p, C.c_int, i8p, C.c_int, C.c_int, C.c_int,
+                                          C.c_double, i16p, i32p]
             L.orc_set_threads.argtypes = [C.c_int]
             L.orc_get_threads.restype = C.c_int
             _lib = L
@@ -389,3 +399,58 @@ def stack(blocks, X, Hs, **kw):
     for i, blk in enumerate(blocks):
         X, Hs[i] = block(blk, X, Hs[i], **kw)
     return X, Hs
+
+
+# ---------------------------------------------------------------- fixed-point W8A16 (f4(ii))
+# PAPER.md P:499-518; readings F1-F5 in DESIGN.md.  Integer in, integer out.
+FXP_XEXP, FXP_YEXP, FXP_NSIG = 6, 15, 8
+
+
+def fxp_scales(w, shift=6):
+    """F1: (w_q int8, e) with w ~ w_q 2^e, 2^e = 2^(round(log2 max|w|) - shift)."""
+    w = _f32(w)
+    wq = np.zeros(w.size, np.int8)
+    e = C.c_int(0)
+    _check(lib().orc_fxp_scales(w, w.size, int(shift), wq, C.byref(e)), "orc_fxp_scales")
+    return wq, e.value
+
+
+def fxp_quant_act(x):
+    """F2: (q int16, e) with x ~ q 2^e, e the smallest fitting power of two."""
+    x = _f32(x)
+    q = np.zeros(x.shape, np.int16)
+    e = C.c_int(0)
+    _check(lib().orc_fxp_quant_act(x.reshape(-1), x.size, q.reshape(-1), C.byref(e)),
+           "orc_fxp_quant_act")
+    return q, e.value
+
+
+def fxp_sigmoid(x):
+    """F3: Q6 int32 inputs -> Q15 int32 sigma."""
+    x = np.ascontiguousarray(x, dtype=np.int32)
+    y = np.zeros(x.shape, np.int32)
+    lib().orc_fxp_sigmoid_arr(x.reshape(-1), y.reshape(-1), x.size)
+    return y
+
+
+def fxp_inv_sqrt(v, e):
+    """F4: 1/sqrt(v 2^e) ~ y 2^ey; returns (y uint32, ey int32)."""
+    v = np.ascontiguousarray(v, dtype=np.uint64)
+    e = np.ascontiguousarray(np.broadcast_to(np.asarray(e, np.int32), v.shape), dtype=np.int32)
+    y = np.zeros(v.shape, np.uint32)
+    ey = np.zeros(v.shape, np.int32)
+    _check(lib().orc_fxp_inv_sqrt_arr(v.reshape(-1), e.reshape(-1), v.size, y.reshape(-1),
+                                      ey.reshape(-1)), "orc_fxp_inv_sqrt")
+    return y, ey
+
+
+def fxp_rmsnorm(xq, ex, wq, ew, eps=1e-3):
+    """F5 (Eq. 1, eps = 1e-3 P:510): int16 rows -> (int16 rows, per-row exponent)."""
+    xq = np.ascontiguousarray(xq, dtype=np.int16)
+    rows, d = xq.shape
+    wq = np.ascontiguousarray(wq, dtype=np.int8)
+    out = np.zeros((rows, d), np.int16)
+    eo = np.zeros(rows, np.int32)
+    _check(lib().orc_fxp_rmsnorm(xq, int(ex), wq, int(ew), rows, d, float(eps), out, eo),
+           "orc_fxp_rmsnorm")
+    return out, eo

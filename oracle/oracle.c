@@ -27,7 +27,8 @@
  * reduced sequentially, so results do not depend on the thread count.
  *
  * Parity status per function: all functions are pinned by tests in
- * tests/test_oracle_pins.py except the composed end-to-end block values,
+ * tests/test_oracle_pins.py (the fixed-point orc_fxp_* section by
+ * tests/test_fxp_oracle.py) except the composed end-to-end block values,
  * which the paper never prints ("parity unpinned" for orc_block values;
  * they are pinned only through their pinned parts and invariants).
  */
@@ -525,4 +526,187 @@ int orc_block(const orc_mlgru_w* mw, const orc_glu_w* gw, const float* X, int B,
   free(D);
   if (!x1_tap) free(X1);
   return rc;
+}
+
+/* ======================================================================== */
+/* Fixed-point W8A16 numerics of the Loihi 2 deployment (*/
+/* PAPER.md P:499-518 "Implementation Details on Intel Loihi 2"    */
+/* Appendix "Fixed-Point Implementation Details").  Readings F1-F5 in        */
+/* DESIGN.md.  Integer arithmetic only, except where a reading says a       */
+/* constant is formed in binary64.                                           */
+/* ======================================================================== */
+
+/* round half away from zero of an exact rational v / 2^s, s >= 0 (F2, F5) */
+static int64_t rha_shift(int64_t v, int s) {
+  if (s == 0) return v;
+  const uint64_t a = v < 0 ? (uint64_t)(-v) : (uint64_t)v;
+  const uint64_t r = (a + ((uint64_t)1 << (s - 1))) >> s;
+  return v < 0 ? -(int64_t)r : (int64_t)r;
+}
+
+/* F1 -- norm-scale quantization: w_q = round(w / s_w),
+ * s_w = 2^(round(log2(max|w|)) - shift).  The paper's literal form is shift = 0
+ * (then |w_q| <= 1); shift = 6 uses the int8 range (|w_q| <= 91).  round() is
+ * half away from zero (C3); log2 is evaluated in binary64. */
+int orc_fxp_scales(const float* w, int n, int shift, int8_t* wq, int* e_out) {
+  if (n <= 0 || shift < 0 || shift > 6) return ORC_ERR_ARG;
+  float mx = 0.0f;
+  for (int i = 0; i < n; ++i) {
+    const float a = fabsf(w[i]);
+    if (a > mx) mx = a;
+  }
+  if (!(mx > 0.0f) || !isfinite(mx)) return ORC_ERR_DEGENERATE;
+  const int e = (int)round(log2((double)mx)) - shift;
+  for (int i = 0; i < n; ++i) {
+    const double v = round(ldexp((double)w[i], -e));   /* w / 2^e is exact */
+    if (v > 127.0 || v < -127.0) return ORC_ERR_OVERFLOW;
+    wq[i] = (int8_t)v;
+  }
+  *e_out = e;
+  return ORC_OK;
+}
+
+/* F2 -- dynamic 16-bit activation quantization, P:508 ("quantization scales
+ * for the activations are computed for each batch individually"), with a
+ * power-of-two scale ("bit-shift operations"): e = the smallest integer
+ * with round(max|x| / 2^e) <= 32767; q = round(x / 2^e).  An all-zero tensor
+ * gets e = 0. */
+int orc_fxp_quant_act(const float* x, int64_t n, int16_t* q, int* e_out) {
+  if (n < 0) return ORC_ERR_ARG;
+  float mx = 0.0f;
+  for (int64_t i = 0; i < n; ++i) {
+    const float a = fabsf(x[i]);
+    if (!isfinite(a)) return ORC_ERR_ARG;
+    if (a > mx) mx = a;
+  }
+  int e = 0;
+  if (mx > 0.0f) {
+    int p;
+    frexp((double)mx, &p);            /* mx in [2^(p-1), 2^p) */
+    e = p - 16;                       /* mx / 2^e in [2^15, 2^16): too big ... */
+    while (round(ldexp((double)mx, -e)) > 32767.0) ++e;
+    while (round(ldexp((double)mx, -(e - 1))) <= 32767.0) --e;   /* ... smallest e */
+  }
+  for (int64_t i = 0; i < n; ++i) q[i] = (int16_t)round(ldexp((double)x[i], -e));
+  *e_out = e;
+  return ORC_OK;
+}
+
+/* F3 -- sigmoid LUT: x_fxp = round(x 2^x_exp), x_exp = 6; LUT of
+ * N_sigma + 1 = 9 points x_i = i 2^x_exp (i = 0..8, i.e. x = 0, 1, ..., 8),
+ * y_i = floor(sigma(i) 2^y_exp), y_exp = 15, sigma in binary64; piecewise
+ * linear interpolation between adjacent points with a floor; inputs beyond
+ * the last point take y_8; negative inputs via sigma(-x) = 1 - sigma(x), i.e.
+ * 2^y_exp - y(|x|). */
+#define ORC_FXP_XEXP 6
+#define ORC_FXP_YEXP 15
+#define ORC_FXP_NSIG 8
+int32_t orc_fxp_sigmoid(int32_t x) {
+  int32_t lut[ORC_FXP_NSIG + 1];
+  for (int i = 0; i <= ORC_FXP_NSIG; ++i)
+    lut[i] = (int32_t)floor(ldexp(1.0 / (1.0 + exp(-(double)i)), ORC_FXP_YEXP));
+  const int64_t a = x < 0 ? -(int64_t)x : (int64_t)x;
+  int32_t y;
+  if (a >= ((int64_t)ORC_FXP_NSIG << ORC_FXP_XEXP)) {
+    y = lut[ORC_FXP_NSIG];
+  } else {
+    const int i = (int)(a >> ORC_FXP_XEXP);
+    const int64_t fr = a - ((int64_t)i << ORC_FXP_XEXP);
+    y = lut[i] + (int32_t)(((int64_t)(lut[i + 1] - lut[i]) * fr) >> ORC_FXP_XEXP);
+  }
+  return x < 0 ? (1 << ORC_FXP_YEXP) - y : y;
+}
+void orc_fxp_sigmoid_arr(const int32_t* x, int32_t* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = orc_fxp_sigmoid(x[i]);
+}
+
+/* F4 -- inverse square root, P:722-723 ("treats the input as an integer
+ * paired with a fixed exponent, uses a LUT with 24 values to produce an
+ * initial guess ... refined using five iterations of the Newton-Raphson
+ * method, all in a fixed-point format").  Input v 2^e with v > 0.  Normalise
+ * to m 2^E, m in [1, 4) held as Q30 (m_q = m 2^30), E even; the 24 LUT values
+ * are 1/sqrt of the centres of the 24 intervals [1 + k/8, 1 + (k+1)/8) that
+ * tile [1, 4): g_k = round(2^30 / sqrt(1 + (k + 1/2)/8)) (binary64); then five
+ * Newton steps y <- y (3 - m y^2) / 2 in Q30 with truncating shifts:
+ *   y <- (y * (3*2^30 - ((m_q * ((y*y) >> 30)) >> 30))) >> 31.
+ * Result: 1/sqrt(v 2^e) = y 2^(ey), ey = -30 - E/2. */
+int orc_fxp_inv_sqrt(uint64_t v, int e, uint32_t* y_out, int* ey_out) {
+  if (v == 0) return ORC_ERR_ARG;
+  int p = 63;
+  while (!((v >> p) & 1)) --p;                     /* v in [2^p, 2^(p+1)) */
+  uint64_t m = p >= 30 ? v >> (p - 30) : v << (30 - p);   /* [2^30, 2^31); drops low bits */
+  int E = e + p;
+  if (E & 1) {                                     /* make the exponent even */
+    m <<= 1;
+    E -= 1;
+  }
+  const int k = (int)((m - ((uint64_t)1 << 30)) >> 27);   /* (m - 1) * 8 in [0, 24) */
+  uint64_t y = (uint64_t)llround(ldexp(1.0, 30) / sqrt(1.0 + (k + 0.5) / 8.0));
+  for (int it = 0; it < 5; ++it) {
+    const uint64_t y2 = (y * y) >> 30;
+    const uint64_t my2 = (m * y2) >> 30;
+    y = (y * ((uint64_t)3 * ((uint64_t)1 << 30) - my2)) >> 31;
+  }
+  *y_out = (uint32_t)y;
+  *ey_out = -30 - E / 2;
+  return ORC_OK;
+}
+int orc_fxp_inv_sqrt_arr(const uint64_t* v, const int32_t* e, int64_t n, uint32_t* y,
+                         int32_t* ey) {
+  for (int64_t i = 0; i < n; ++i) {
+    int t;
+    const int rc = orc_fxp_inv_sqrt(v[i], e[i], &y[i], &t);
+    if (rc) return rc;
+    ey[i] = t;
+  }
+  return ORC_OK;
+}
+
+/* F5 -- RMSNorm of Eq. 1 in fixed point with eps = 1e-3,
+ * read with the mean over the d channels (C1; the printed Eq. 1 omits 1/d):
+ *   y_i = x_i / sqrt(eps + (1/d) sum_j x_j^2) * w_i
+ * with x_i = xq_i 2^ex (int16, F2) and w_i = wq_i 2^ew (int8, F1).  Since
+ *   1/sqrt(eps + S 2^(2ex)/d) = sqrt(d) 2^(-ex) / sqrt(S + eps_q),
+ * S = sum xq_j^2 (int64, exact) and eps_q = round(d eps 2^(-2ex)) (binary64,
+ * half away; 0 when eps underflows -- the paper's reason for eps = 1e-3),
+ * the row computes (yq, ey) = inv_sqrt(S + eps_q, 0) (F4),
+ * rsd = (yq * sd) >> 16 with sd = round(sqrt(d) 2^16) (binary64), then
+ * t_i = xq_i * wq_i * rsd (int64, real value t_i 2^(ew + ey)), and stores
+ * out_i = round(t_i / 2^s) (half away) with the smallest s >= 0 for which
+ * every |out_i| <= 32767: output exponent eo = s + ew + ey per row.
+ * A row with S + eps_q = 0 (all zero, eps underflowed) outputs zeros, eo = 0. */
+int orc_fxp_rmsnorm(const int16_t* xq, int ex, const int8_t* wq, int ew, int rows, int d,
+                    double eps, int16_t* out, int32_t* eo) {
+  if (rows < 0 || d <= 0 || d > 65536 || !(eps >= 0.0)) return ORC_ERR_ARG;
+  const double eps_d = round(ldexp((double)d * eps, -2 * ex));
+  if (eps_d > 0x1p60) return ORC_ERR_OVERFLOW;
+  const int64_t eps_q = (int64_t)eps_d;
+  const int64_t sd = (int64_t)llround(ldexp(sqrt((double)d), 16));
+  for (int r = 0; r < rows; ++r) {
+    const int16_t* x = xq + (int64_t)r * d;
+    int16_t* o = out + (int64_t)r * d;
+    int64_t S = 0;
+    for (int j = 0; j < d; ++j) S += (int64_t)x[j] * x[j];
+    const uint64_t D = (uint64_t)S + (uint64_t)eps_q;
+    if (D == 0) {
+      for (int j = 0; j < d; ++j) o[j] = 0;
+      eo[r] = 0;
+      continue;
+    }
+    uint32_t yq;
+    int ey;
+    orc_fxp_inv_sqrt(D, 0, &yq, &ey);
+    const int64_t rsd = (int64_t)(((uint64_t)yq * (uint64_t)sd) >> 16);
+    int64_t tmax = 0;
+    for (int j = 0; j < d; ++j) {
+      int64_t t = (int64_t)x[j] * wq[j] * rsd;
+      if (t < 0) t = -t;
+      if (t > tmax) tmax = t;
+    }
+    int s = 0;
+    while (rha_shift(tmax, s) > 32767) ++s;
+    for (int j = 0; j < d; ++j) o[j] = (int16_t)rha_shift((int64_t)x[j] * wq[j] * rsd, s);
+    eo[r] = s + ew + ey;
+  }
+  return ORC_OK;
 }
