@@ -378,6 +378,49 @@ int32_t tern_profile_collect(tern_prof_rec* out, int32_t max);
 void tern_trace_enable(int32_t on);
 int32_t tern_trace_collect(uint64_t* out, int32_t max_launches);
 
+/* ------------------------------------------------------------------------
+ * Fixed-point W8A16 numerics of the paper's Loihi 2 deployment (SURVEY 8(f)
+ * f4(ii); readings F1-F5 in DESIGN.md §3b).
+ * Integers in, integers out, a value v with exponent e meaning v * 2^e.
+ * Asynchronous on `stream` unless stated; device pointers unless stated.
+ * ------------------------------------------------------------------------ */
+/* F1: norm gains w [n] (fp32) -> wq [n] (int8) and the exponent e
+ * (written to *e_host) with w ~ wq 2^e, 2^e = 2^(round(log2 max|w|) - shift),
+ * round half away; shift 0 is the printed formula (|wq| <= 1), shift 6 uses
+ * the int8 range (|wq| <= 91).  0 <= shift <= 6.  ws: device scratch >= 16
+ * bytes, 16-byte aligned.  Synchronous (an offline weight-preparation step);
+ * TERN_ERR_DEGENERATE if max|w| is 0 or not finite (wq then untouched). */
+tern_status tern_fxp_scales(const float* w, int32_t n, int32_t shift, int8_t* wq, int32_t* e_host,
+                            void* ws, tern_stream stream);
+/* F2: dynamic 16-bit activation quantization of x [n] (fp32 or bf16,
+ * finite) with ONE power-of-two exponent for the tensor: *e (device int32) =
+ * the smallest e with round(max|x| / 2^e) <= 32767, q = round(x / 2^e) (half
+ * away) int16 [n].  An all-zero x gives e = 0.  ws: device scratch >= 16
+ * bytes, 16-byte aligned (the max).  n == 0: no-op. */
+tern_status tern_fxp_quant_act(const void* x, tern_dtype dt, int64_t n, int16_t* q, int32_t* e,
+                               void* ws, tern_stream stream);
+/* F3: LUT sigmoid, x [n] int32 in Q6 (x_exp = 6) -> y [n] int32
+ * in Q15 (y_exp = 15): 9 points x = 0..8 holding floor(sigma(i) 2^15), linear
+ * interpolation with a floor, |x| >= 8 -> the last point, sigma(-x) = 2^15 -
+ * sigma(x).  x, y 16-byte aligned. */
+tern_status tern_fxp_sigmoid(const int32_t* x, int64_t n, int32_t* y, tern_stream stream);
+/* F4: 1/sqrt(v 2^e) ~ y 2^ey for v [n] (uint64, > 0) and e [n]
+ * (int32): 24-entry seed table over [1, 4) + five Newton steps in Q30.
+ * y [n] uint32 (Q30 mantissa in (2^29, 2^30]), ey [n] int32.  v == 0 is
+ * outside the domain and gives y = 0, ey = 0.  v 8-byte aligned. */
+tern_status tern_fxp_inv_sqrt(const uint64_t* v, const int32_t* e, int64_t n, uint32_t* y,
+                              int32_t* ey, tern_stream stream);
+/* F5 (Eq. 1; eps = 1e-3 P:510): RMSNorm of int16 rows xq
+ * [rows][d] with exponent *ex (device int32, e.g. from tern_fxp_quant_act)
+ * and int8 gains wq [d] with exponent ew (host, from tern_fxp_scales):
+ * out [rows][d] int16 and eo [rows] int32 (one exponent per row, the
+ * smallest that fits).  Integer sum of squares, eps on its grid
+ * (round(d eps 2^(-2 ex)), clamped to 2^60), F4 for the inverse square root,
+ * sqrt(d) in Q16.  1 <= d <= 65536; xq 16-byte aligned. */
+tern_status tern_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_t* wq, int32_t ew,
+                             double eps, int32_t rows, int32_t d, int16_t* out, int32_t* eo,
+                             tern_stream stream);
+
 /* Device self-check of the numerics shortcuts the kernels take (test use):
  * which = 0: the FMA-corrected reciprocals used by the sigmoids equal IEEE
  * 1/d for every mantissa of every exponent 0..125 (d in [1, 2^126));

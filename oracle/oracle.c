@@ -668,7 +668,8 @@ int orc_fxp_inv_sqrt_arr(const uint64_t* v, const int32_t* e, int64_t n, uint32_
  * with x_i = xq_i 2^ex (int16, F2) and w_i = wq_i 2^ew (int8, F1).  Since
  *   1/sqrt(eps + S 2^(2ex)/d) = sqrt(d) 2^(-ex) / sqrt(S + eps_q),
  * S = sum xq_j^2 (int64, exact) and eps_q = round(d eps 2^(-2ex)) (binary64,
- * half away; 0 when eps underflows -- the paper's reason for eps = 1e-3),
+ * half away; 0 when eps underflows -- the paper's reason for eps = 1e-3 --, and
+ * clamped to 2^60 so that S + eps_q stays in 64 bits for tiny activations),
  * the row computes (yq, ey) = inv_sqrt(S + eps_q, 0) (F4),
  * rsd = (yq * sd) >> 16 with sd = round(sqrt(d) 2^16) (binary64), then
  * t_i = xq_i * wq_i * rsd (int64, real value t_i 2^(ew + ey)), and stores
@@ -679,8 +680,7 @@ int orc_fxp_rmsnorm(const int16_t* xq, int ex, const int8_t* wq, int ew, int row
                     double eps, int16_t* out, int32_t* eo) {
   if (rows < 0 || d <= 0 || d > 65536 || !(eps >= 0.0)) return ORC_ERR_ARG;
   const double eps_d = round(ldexp((double)d * eps, -2 * ex));
-  if (eps_d > 0x1p60) return ORC_ERR_OVERFLOW;
-  const int64_t eps_q = (int64_t)eps_d;
+  const int64_t eps_q = eps_d > 0x1p60 ? ((int64_t)1 << 60) : (int64_t)eps_d;   /* F5 clamp */
   const int64_t sd = (int64_t)llround(ldexp(sqrt((double)d), 16));
   for (int r = 0; r < rows; ++r) {
     const int16_t* x = xq + (int64_t)r * d;

@@ -123,6 +123,11 @@ _SIGS = {
     "tern_set_norm_mode": (None, [C.c_int]),
     "tern_get_norm_mode": (C.c_int, []),
     "tern_get_batched_fin": (I32, []),
+    "tern_fxp_scales": (C.c_int, [P, I32, I32, P, C.POINTER(I32), P, P]),
+    "tern_fxp_quant_act": (C.c_int, [P, C.c_int, C.c_int64, P, P, P, P]),
+    "tern_fxp_sigmoid": (C.c_int, [P, C.c_int64, P, P]),
+    "tern_fxp_inv_sqrt": (C.c_int, [P, P, C.c_int64, P, P, P]),
+    "tern_fxp_rmsnorm": (C.c_int, [P, P, P, I32, C.c_double, I32, I32, P, P, P]),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -357,6 +362,46 @@ def tern_profile_collect() -> list:
         out.append({"kernel": KERNEL_NAMES.get(r.kernel, str(r.kernel)), "epi": r.epi, "m": r.m,
                     "n": r.n, "k": r.k, "n_seg": r.n_seg, "dtype": r.dtype, "ms": float(r.ms)})
     return out
+
+
+# ---------------------------------------------------------------- fixed point W8A16 (f4(ii))
+def tern_fxp_scales(w: torch.Tensor, shift: int = 6, stream=None):
+    """F1: fp32 gains [n] (device) -> (int8 wq [n] device tensor, exponent e)."""
+    wq = torch.empty(w.numel(), dtype=torch.int8, device=w.device)
+    ws = torch.zeros(16, dtype=torch.uint8, device=w.device)
+    e = I32(0)
+    _check(load().tern_fxp_scales(ptr(w), w.numel(), int(shift), ptr(wq), C.byref(e), ptr(ws),
+                                  stream_handle(stream)), "tern_fxp_scales")
+    return wq, int(e.value)
+
+
+def tern_fxp_quant_act(x: torch.Tensor, q: torch.Tensor, e: torch.Tensor, ws=None, stream=None):
+    """F2: x (fp32/bf16) -> q int16 (same numel), e int32 [1] (device)."""
+    if ws is None:
+        ws = torch.empty(16, dtype=torch.uint8, device=x.device)
+    _check(load().tern_fxp_quant_act(ptr(x), dtype_code(x.dtype), x.numel(), ptr(q), ptr(e),
+                                     ptr(ws), stream_handle(stream)), "tern_fxp_quant_act")
+
+
+def tern_fxp_sigmoid(x: torch.Tensor, y: torch.Tensor, stream=None):
+    """F3: int32 Q6 -> int32 Q15."""
+    _check(load().tern_fxp_sigmoid(ptr(x), x.numel(), ptr(y), stream_handle(stream)),
+           "tern_fxp_sigmoid")
+
+
+def tern_fxp_inv_sqrt(v: torch.Tensor, e: torch.Tensor, y: torch.Tensor, ey: torch.Tensor,
+                      stream=None):
+    """F4: v (uint64 as int64 storage) and e int32 -> y (uint32 as int32 storage), ey int32."""
+    _check(load().tern_fxp_inv_sqrt(ptr(v), ptr(e), v.numel(), ptr(y), ptr(ey),
+                                    stream_handle(stream)), "tern_fxp_inv_sqrt")
+
+
+def tern_fxp_rmsnorm(xq: torch.Tensor, ex: torch.Tensor, wq: torch.Tensor, ew: int,
+                     out: torch.Tensor, eo: torch.Tensor, eps: float = 1e-3, stream=None):
+    """F5: int16 rows [rows][d] (exponent ex: device int32 [1]) -> int16 rows, int32 [rows]."""
+    rows, d = xq.shape
+    _check(load().tern_fxp_rmsnorm(ptr(xq), ptr(ex), ptr(wq), int(ew), float(eps), rows, d,
+                                   ptr(out), ptr(eo), stream_handle(stream)), "tern_fxp_rmsnorm")
 
 
 def tern_selftest(which: int) -> int:

@@ -486,6 +486,76 @@ tern_status tern_contract(const int8_t* q, int32_t m, int32_t ldq, const int32_t
   return TERN_OK;
 }
 
+// ---------------------------------------------------------------- fixed point (f4(ii))
+tern_status tern_fxp_scales(const float* w, int32_t n, int32_t shift, int8_t* wq, int32_t* e_host,
+                            void* ws, tern_stream stream) {
+  CHECK(w && wq && e_host && ws, "tern_fxp_scales: null pointer");
+  CHECK(n > 0 && shift >= 0 && shift <= 6, "tern_fxp_scales: n=%d shift=%d", n, shift);
+  CHECK(aligned16(ws), "tern_fxp_scales: workspace not 16-byte aligned");
+  tern_status st = check_device();
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* dev = static_cast<int32_t*>(ws);   // [0] e, [1] status
+  TRY_CUDA(launch_fxp_scales(w, n, shift, wq, dev, dev + 1, s), "fxp_scales");
+  int32_t h[2] = {0, 0};
+  TRY_CUDA(cudaMemcpyAsync(h, dev, sizeof(h), cudaMemcpyDeviceToHost, s), "fxp_scales d2h");
+  TRY_CUDA(cudaStreamSynchronize(s), "fxp_scales sync");
+  if (h[1]) return fail(TERN_ERR_DEGENERATE, "tern_fxp_scales: max|w| is 0 or not finite");
+  *e_host = h[0];
+  return TERN_OK;
+}
+
+tern_status tern_fxp_quant_act(const void* x, tern_dtype dt, int64_t n, int16_t* q, int32_t* e,
+                               void* ws, tern_stream stream) {
+  CHECK(valid_dt(dt), "tern_fxp_quant_act: bad dtype");
+  CHECK(n >= 0, "tern_fxp_quant_act: n=%lld", (long long)n);
+  if (n == 0) return TERN_OK;
+  CHECK(x && q && e && ws, "tern_fxp_quant_act: null pointer");
+  CHECK(aligned16(ws), "tern_fxp_quant_act: workspace not 16-byte aligned");
+  tern_status st = check_device();
+  if (st) return st;
+  TRY_CUDA(launch_fxp_quant_act(x, dt, n, q, e, static_cast<uint32_t*>(ws), (cudaStream_t)stream),
+           "fxp_quant_act");
+  return TERN_OK;
+}
+
+tern_status tern_fxp_sigmoid(const int32_t* x, int64_t n, int32_t* y, tern_stream stream) {
+  CHECK(n >= 0, "tern_fxp_sigmoid: n=%lld", (long long)n);
+  if (n == 0) return TERN_OK;
+  CHECK(x && y && aligned16(x) && aligned16(y), "tern_fxp_sigmoid: null or unaligned pointer");
+  tern_status st = check_device();
+  if (st) return st;
+  TRY_CUDA(launch_fxp_sigmoid(x, n, y, (cudaStream_t)stream), "fxp_sigmoid");
+  return TERN_OK;
+}
+
+tern_status tern_fxp_inv_sqrt(const uint64_t* v, const int32_t* e, int64_t n, uint32_t* y,
+                              int32_t* ey, tern_stream stream) {
+  CHECK(n >= 0, "tern_fxp_inv_sqrt: n=%lld", (long long)n);
+  if (n == 0) return TERN_OK;
+  CHECK(v && e && y && ey, "tern_fxp_inv_sqrt: null pointer");
+  CHECK((reinterpret_cast<uintptr_t>(v) & 7u) == 0, "tern_fxp_inv_sqrt: v not 8-byte aligned");
+  tern_status st = check_device();
+  if (st) return st;
+  TRY_CUDA(launch_fxp_inv_sqrt(v, e, n, y, ey, (cudaStream_t)stream), "fxp_inv_sqrt");
+  return TERN_OK;
+}
+
+tern_status tern_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_t* wq, int32_t ew,
+                             double eps, int32_t rows, int32_t d, int16_t* out, int32_t* eo,
+                             tern_stream stream) {
+  CHECK(rows >= 0 && d >= 1 && d <= 65536, "tern_fxp_rmsnorm: rows=%d d=%d", rows, d);
+  CHECK(eps >= 0.0 && eps < 1e30, "tern_fxp_rmsnorm: eps=%g", eps);
+  if (rows == 0) return TERN_OK;
+  CHECK(xq && ex && wq && out && eo, "tern_fxp_rmsnorm: null pointer");
+  CHECK(aligned16(xq), "tern_fxp_rmsnorm: xq not 16-byte aligned");
+  tern_status st = check_device();
+  if (st) return st;
+  TRY_CUDA(launch_fxp_rmsnorm(xq, ex, wq, ew, eps, rows, d, out, eo, (cudaStream_t)stream),
+           "fxp_rmsnorm");
+  return TERN_OK;
+}
+
 tern_status tern_mlgru_scan(const void* fcg, tern_dtype dt, int32_t B, int32_t T, int32_t d,
                             tern_gate_mode gate, float* h, void* oprime, tern_stream stream) {
   CHECK(fcg && h && oprime, "tern_mlgru_scan: null pointer");

@@ -137,6 +137,17 @@ cudaError_t launch_fcgscan(const int8_t* q, int ldq, const float* deq, const int
                            int gate, float* h, void* oprime, cudaStream_t s);
 // a6
 bool fcgscan_preferred(int B, int d);
+// k_fxp.cu: fixed-point W8A16 numerics (f4(ii))
+cudaError_t launch_fxp_scales(const float* w, int n, int shift, int8_t* wq, int32_t* e,
+                              int32_t* status, cudaStream_t s);
+cudaError_t launch_fxp_quant_act(const void* x, int dt, int64_t n, int16_t* q, int32_t* e,
+                                 uint32_t* ws, cudaStream_t s);
+cudaError_t launch_fxp_sigmoid(const int32_t* x, int64_t n, int32_t* y, cudaStream_t s);
+cudaError_t launch_fxp_inv_sqrt(const uint64_t* v, const int32_t* e, int64_t n, uint32_t* y,
+                                int32_t* ey, cudaStream_t s);
+cudaError_t launch_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_t* wq, int ew,
+                               double eps, int rows, int d, int16_t* out, int32_t* eo,
+                               cudaStream_t s);
 cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
                         void* oprime, cudaStream_t s);
 

@@ -101,6 +101,39 @@ def test_validation_of_the_later_entry_points(lib):
     lib.tern_set_norm_mode(old)
 
 
+def test_validation_of_the_fixed_point_entry_points(lib):
+    """tern_fxp_* (f4(ii)) reject bad arguments before touching the device; empty calls are
+    no-ops; the fused-scan knob is clamped."""
+    from paper_2406_02528_b200 import _lib as L
+    fake = C.c_void_p(0x1000)
+    odd = C.c_void_p(0x1004)
+    e = C.c_int32(0)
+    assert lib.tern_fxp_scales(None, 4, 6, fake, C.byref(e), fake, None) == L.TERN_ERR_INVALID_ARG
+    assert lib.tern_fxp_scales(fake, 4, 7, fake, C.byref(e), fake, None) == L.TERN_ERR_INVALID_ARG
+    assert lib.tern_fxp_scales(fake, 4, 6, fake, C.byref(e), odd, None) == L.TERN_ERR_INVALID_ARG
+    assert lib.tern_fxp_quant_act(fake, 5, 4, fake, fake, fake, None) == L.TERN_ERR_INVALID_ARG
+    assert lib.tern_fxp_quant_act(None, 0, 0, None, None, None, None) == L.TERN_OK
+    assert lib.tern_fxp_sigmoid(odd, 8, fake, None) == L.TERN_ERR_INVALID_ARG
+    assert lib.tern_fxp_sigmoid(None, 0, None, None) == L.TERN_OK
+    assert lib.tern_fxp_inv_sqrt(odd, fake, 3, fake, fake, None) == L.TERN_ERR_INVALID_ARG
+    assert lib.tern_fxp_rmsnorm(fake, fake, fake, 0, 1e-3, 2, 0, fake, fake, None) == \
+        L.TERN_ERR_INVALID_ARG
+    assert lib.tern_fxp_rmsnorm(fake, fake, fake, 0, 1e-3, 2, 70000, fake, fake, None) == \
+        L.TERN_ERR_INVALID_ARG
+    assert lib.tern_fxp_rmsnorm(odd, fake, fake, 0, 1e-3, 2, 64, fake, fake, None) == \
+        L.TERN_ERR_INVALID_ARG
+    assert lib.tern_fxp_rmsnorm(fake, fake, fake, 0, -1.0, 2, 64, fake, fake, None) == \
+        L.TERN_ERR_INVALID_ARG
+    assert b"tern_fxp_rmsnorm" in lib.tern_last_error()
+    assert lib.tern_fxp_rmsnorm(None, None, None, 0, 1e-3, 0, 64, None, None, None) == L.TERN_OK
+    old = lib.tern_get_fused_scan()
+    lib.tern_set_fused_scan(9)
+    assert lib.tern_get_fused_scan() == 2
+    lib.tern_set_fused_scan(-3)
+    assert lib.tern_get_fused_scan() == 0
+    lib.tern_set_fused_scan(old)
+
+
 def test_product_path_has_no_fallback(tmp_path, monkeypatch):
     """The binding raises when the CUDA library is missing (no CPU fallback)."""
     import importlib
