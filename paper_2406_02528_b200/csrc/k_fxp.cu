@@ -50,23 +50,25 @@ __device__ __forceinline__ int64_t fx_rha_shift(int64_t v, int s) {   // round(v
 }
 
 // F3: Q6 -> Q15 sigma through the 9-point table, linear interpolation with a floor
-__device__ __forceinline__ int32_t fx_sigmoid(int32_t x, const SigLut& L) {
+// (the tables are read from shared memory: lanes index them divergently, which the
+// constant bank would serialise)
+__device__ __forceinline__ int32_t fx_sigmoid(int32_t x, const int32_t* __restrict__ L) {
   const uint32_t a = x < 0 ? 0u - (uint32_t)x : (uint32_t)x;
   int32_t y;
   if (a >= (uint32_t)(kFxNsig << kFxXexp)) {
-    y = L.y[kFxNsig];
+    y = L[kFxNsig];
   } else {
     const int i = (int)(a >> kFxXexp);
     const int32_t fr = (int32_t)(a & ((1u << kFxXexp) - 1));
-    const int32_t y0 = L.y[i], y1 = L.y[i + 1];
+    const int32_t y0 = L[i], y1 = L[i + 1];
     y = y0 + (((y1 - y0) * fr) >> kFxXexp);   // (y1 - y0) * fr < 2^15 * 2^6: no overflow
   }
   return x < 0 ? (1 << kFxYexp) - y : y;
 }
 
 // F4: 1/sqrt(v 2^e) = y 2^ey, v > 0
-__device__ __forceinline__ void fx_inv_sqrt(uint64_t v, int e, const RsqLut& L, uint32_t& y_out,
-                                            int& ey_out) {
+__device__ __forceinline__ void fx_inv_sqrt(uint64_t v, int e, const uint32_t* __restrict__ L,
+                                            uint32_t& y_out, int& ey_out) {
   const int p = 63 - __clzll((long long)v);
   uint64_t m = p >= 30 ? v >> (p - 30) : v << (30 - p);
   int E = e + p;
@@ -75,7 +77,7 @@ __device__ __forceinline__ void fx_inv_sqrt(uint64_t v, int e, const RsqLut& L, 
     E -= 1;
   }
   const int k = (int)((m - (1ull << 30)) >> 27);
-  uint64_t y = L.g[k];
+  uint64_t y = L[k];
 #pragma unroll
   for (int it = 0; it < 5; ++it) {
     const uint64_t y2 = (y * y) >> 30;
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(1024) k_fxp_scales(const float* __restrict__ w
 // ---------------------------------------------------------------- F2 activations
 template <typename T>
 __device__ __forceinline__ float fx_ld(const T* p, int64_t i) {
-  if constexpr (sizeof(T) == 4) return __ldg(reinterpret_cast<const float*>(p) + i);
+  if constexpr (sizeof(T) == 4) return reinterpret_cast<const float*>(p)[i];
   else return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
 }
 
@@ -147,7 +149,16 @@ __global__ void __launch_bounds__(kFxThreads) k_fxp_absmax(const T* __restrict__
   __shared__ uint32_t red[kFxThreads / 32];
   uint32_t mx = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int kV = 16 / sizeof(T);   // elements per 16-byte vector
+  const int64_t nv = (reinterpret_cast<uintptr_t>(x) & 15) ? 0 : n / kV;
+  for (int64_t i = tid; i < nv; i += stride) {
+    const int4 raw = __ldg(reinterpret_cast<const int4*>(x) + i);
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int k = 0; k < kV; ++k) mx = max(mx, __float_as_uint(fabsf(fx_ld<T>(e, k))));
+  }
+  for (int64_t i = nv * kV + tid; i < n; i += stride)
     mx = max(mx, __float_as_uint(fabsf(fx_ld<T>(x, i))));
   mx = fx_warp_max_u32(mx);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -179,14 +190,35 @@ __global__ void __launch_bounds__(kFxThreads) k_fxp_quant_act(const T* __restric
   const int e = fx_act_exponent(*mx);
   if (blockIdx.x == 0 && threadIdx.x == 0) *e_out = e;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const float sc = ldexpf(1.0f, -e);   // x 2^-e is exact as a product with 2^-e ...
+  constexpr int kV = 16 / sizeof(T);
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(q)) & 15) == 0 &&
+                   e > -126 && e < 126;   // ... while 2^-e is a normal float
+  const int64_t nv = vec ? n / kV : 0;
+  for (int64_t i = tid; i < nv; i += stride) {
+    const int4 raw = __ldg(reinterpret_cast<const int4*>(x) + i);
+    const T* el = reinterpret_cast<const T*>(&raw);
+    int16_t o[kV];
+#pragma unroll
+    for (int k = 0; k < kV; ++k) o[k] = (int16_t)roundf(__fmul_rn(fx_ld<T>(el, k), sc));
+    if constexpr (kV == 8) {
+      *reinterpret_cast<int4*>(q + i * kV) = *reinterpret_cast<const int4*>(o);
+    } else {
+      *reinterpret_cast<int2*>(q + i * kV) = *reinterpret_cast<const int2*>(o);
+    }
+  }
+  for (int64_t i = nv * kV + tid; i < n; i += stride)
     q[i] = (int16_t)roundf(ldexpf(fx_ld<T>(x, i), -e));
 }
 
 // ---------------------------------------------------------------- F3 / F4 elementwise
 __global__ void __launch_bounds__(kFxThreads) k_fxp_sigmoid(const int32_t* __restrict__ x, int64_t n,
                                                             int32_t* __restrict__ y,
-                                                            const SigLut L) {
+                                                            const SigLut Lp) {
+  __shared__ int32_t L[kFxNsig + 1];
+  if (threadIdx.x <= kFxNsig) L[threadIdx.x] = Lp.y[threadIdx.x];
+  __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n4 = n >> 2;
   const int4* x4 = reinterpret_cast<const int4*>(x);
@@ -204,7 +236,10 @@ __global__ void __launch_bounds__(kFxThreads) k_fxp_inv_sqrt(const uint64_t* __r
                                                              const int32_t* __restrict__ e,
                                                              int64_t n, uint32_t* __restrict__ y,
                                                              int32_t* __restrict__ ey,
-                                                             const RsqLut L) {
+                                                             const RsqLut Lp) {
+  __shared__ uint32_t L[24];
+  if (threadIdx.x < 24) L[threadIdx.x] = Lp.g[threadIdx.x];
+  __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint64_t vi = __ldg(reinterpret_cast<const unsigned long long*>(v) + i);
@@ -253,9 +288,12 @@ __global__ void __launch_bounds__(kFxThreads) k_fxp_rmsnorm(const int16_t* __res
                                                             double eps, int64_t sd, int rows, int d,
                                                             int16_t* __restrict__ out,
                                                             int32_t* __restrict__ eo,
-                                                            const RsqLut L) {
+                                                            const RsqLut Lp) {
   extern __shared__ __align__(16) int16_t row_s[];
   __shared__ int64_t red[kFxThreads / 32];
+  __shared__ uint32_t L[24];
+  if (threadIdx.x < 24) L[threadIdx.x] = Lp.g[threadIdx.x];
+  __syncthreads();
   const int ex = *ex_dev;
   // eps_q = round(d eps 2^(-2 ex)) in binary64 (F5): the same operations as the definition
   // (clamped to 2^60 so S + eps_q stays in 64 bits for tiny activations)
@@ -309,6 +347,95 @@ __global__ void __launch_bounds__(kFxThreads) k_fxp_rmsnorm(const int16_t* __res
       o[i] = (int16_t)fx_rha_shift((int64_t)(row_s[i] * (int32_t)__ldg(wq + i)) * rsd, s);
     if (threadIdx.x == 0) eo[r] = s + ew + ey;
     __syncthreads();   // row_s is rewritten by the next row
+  }
+}
+
+// Fast path for d = 256 NV (NV <= 12; c2-c4 widths 1024, 2048, 2560, 2816): one WARP per
+// row, the row in registers (NV 16-byte vectors per lane), reductions by shuffles only,
+// the gains staged once per CTA in shared memory.  Same arithmetic as k_fxp_rmsnorm.
+constexpr int kFxWarpRows = 8;   // warps (rows in flight) per CTA
+template <int NV>
+__global__ void __launch_bounds__(kFxWarpRows * 32) k_fxp_rmsnorm_warp(
+    const int16_t* __restrict__ xq, const int32_t* __restrict__ ex_dev,
+    const int8_t* __restrict__ wq, int ew, double eps, int64_t sd, int rows,
+    int16_t* __restrict__ out, int32_t* __restrict__ eo, const RsqLut Lp) {
+  constexpr int d = NV * 256;
+  __shared__ __align__(16) int8_t w_s[d];
+  __shared__ uint32_t L[24];
+  if (threadIdx.x < 24) L[threadIdx.x] = Lp.g[threadIdx.x];
+  for (int i = threadIdx.x; i < d / 16; i += blockDim.x)
+    reinterpret_cast<int4*>(w_s)[i] = __ldg(reinterpret_cast<const int4*>(wq) + i);
+  __syncthreads();
+  const int ex = *ex_dev;
+  const double eps_d = round(ldexp(__dmul_rn((double)d, eps), -2 * ex));
+  const int64_t eps_q = eps_d > 0x1p60 ? (1ll << 60) : (int64_t)eps_d;
+  const int lane = threadIdx.x & 31;
+  const int wid = blockIdx.x * kFxWarpRows + (threadIdx.x >> 5);
+  for (int r = wid; r < rows; r += gridDim.x * kFxWarpRows) {
+    const int4* x4 = reinterpret_cast<const int4*>(xq + (int64_t)r * d);
+    int4 v[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = __ldg(x4 + lane + 32 * j);
+    int64_t S = 0;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {   // two squares (each <= 2^30) per uint32, then widen
+        const int32_t lo = (int16_t)(w4[k] & 0xffff), hi = w4[k] >> 16;
+        S += (int64_t)((uint32_t)(lo * lo) + (uint32_t)(hi * hi));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+    const uint64_t D = (uint64_t)S + (uint64_t)eps_q;
+    int16_t* orow = out + (int64_t)r * d;
+    if (D == 0) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        reinterpret_cast<int4*>(orow)[lane + 32 * j] = make_int4(0, 0, 0, 0);
+      if (lane == 0) eo[r] = 0;
+      continue;
+    }
+    uint32_t yq;
+    int ey;
+    fx_inv_sqrt(D, 0, L, yq, ey);
+    const int64_t rsd = (int64_t)(((uint64_t)yq * (uint64_t)sd) >> 16);
+    // x * w per element (|.| < 2^22, int32), then the int64 product with rsd
+    int32_t xw[NV][8];
+    int64_t tmax = 0;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int2 wv = *reinterpret_cast<const int2*>(w_s + (lane + 32 * j) * 8);
+      const int32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int32_t xv = (int16_t)((w4[k >> 1] >> ((k & 1) * 16)) & 0xffff);
+        const int32_t wk = (int8_t)(((k < 4 ? wv.x : wv.y) >> ((k & 3) * 8)) & 0xff);
+        xw[j][k] = xv * wk;
+        const int32_t a = xw[j][k] < 0 ? -xw[j][k] : xw[j][k];
+        tmax = max(tmax, (int64_t)a);
+      }
+    }
+    // max |t| = max |x w| * rsd (rsd > 0): one int64 product instead of d
+    tmax *= rsd;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tmax = max(tmax, (int64_t)__shfl_xor_sync(0xffffffffu, tmax, o));
+    int s = 0;
+    while (fx_rha_shift(tmax, s) > 32767) ++s;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      int32_t o8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o8[k] = (int32_t)fx_rha_shift((int64_t)xw[j][k] * rsd, s);
+      int4 ov;
+      ov.x = (o8[0] & 0xffff) | (o8[1] << 16);
+      ov.y = (o8[2] & 0xffff) | (o8[3] << 16);
+      ov.z = (o8[4] & 0xffff) | (o8[5] << 16);
+      ov.w = (o8[6] & 0xffff) | (o8[7] << 16);
+      reinterpret_cast<int4*>(orow)[lane + 32 * j] = ov;
+    }
+    if (lane == 0) eo[r] = s + ew + ey;
   }
 }
 
@@ -375,6 +502,21 @@ cudaError_t launch_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_
     cudaError_t e = cudaFuncSetAttribute(k_fxp_rmsnorm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
+  }
+  if (d % 256 == 0 && d <= 12 * 256 && ((reinterpret_cast<uintptr_t>(wq) |
+                                           reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+    const int want = (rows + kFxWarpRows - 1) / kFxWarpRows;
+    const int grid = want < fx_sms() * 8 ? want : fx_sms() * 8;
+#define TERN_FXW(NV)                                                                         \
+  case NV:                                                                                   \
+    k_fxp_rmsnorm_warp<NV><<<grid, kFxWarpRows * 32, 0, s>>>(xq, ex, wq, ew, eps, sd, rows, \
+                                                              out, eo, L);                  \
+    return cudaGetLastError();
+    switch (d / 256) {
+      TERN_FXW(1) TERN_FXW(2) TERN_FXW(3) TERN_FXW(4) TERN_FXW(5) TERN_FXW(6)
+      TERN_FXW(7) TERN_FXW(8) TERN_FXW(9) TERN_FXW(10) TERN_FXW(11) TERN_FXW(12)
+    }
+#undef TERN_FXW
   }
   const int grid = rows < fx_sms() * 8 ? rows : fx_sms() * 8;
   k_fxp_rmsnorm<<<grid, kFxThreads, smem, s>>>(xq, ex, wq, ew, eps, sd, rows, d, out, eo, L);
