@@ -114,6 +114,8 @@ def lib():
             L.orc_fxp_inv_sqrt_arr.argtypes = [u64p, i32p, C.c_int64, u32p, i32p]
             L.orc_fxp_rmsnorm.argtypes = [i16p, C.c_int, i8p, C.c_int, C.c_int, C.c_int,
                                           C.c_double, i16p, i32p]
+            L.orc_fxp_bitlinear.argtypes = [i16p, C.c_int, i8p, C.c_int, C.c_double, i8p,
+                                             C.c_float, C.c_int, C.c_int, C.c_int, i16p, i32p]
             L.orc_set_threads.argtypes = [C.c_int]
             L.orc_get_threads.restype = C.c_int
             _lib = L
@@ -454,3 +456,17 @@ def fxp_rmsnorm(xq, ex, wq, ew, eps=1e-3):
     _check(lib().orc_fxp_rmsnorm(xq, int(ex), wq, int(ew), rows, d, float(eps), out, eo),
            "orc_fxp_rmsnorm")
     return out, eo
+
+
+def fxp_bitlinear(xq, ex, gq, eg, t, beta, eps=1e-3):
+    """F6: W8A16 BitLinear, int16 rows [M][K] -> (int16 [M][N], exponent per row)."""
+    xq = np.ascontiguousarray(xq, dtype=np.int16)
+    M, K = xq.shape
+    t = np.ascontiguousarray(t, dtype=np.int8)
+    N = t.shape[0]
+    y = np.zeros((M, N), np.int16)
+    ey = np.zeros(M, np.int32)
+    _check(lib().orc_fxp_bitlinear(xq, int(ex), np.ascontiguousarray(gq, dtype=np.int8), int(eg),
+                                   float(eps), t, C.c_float(beta), M, K, N, y, ey),
+           "orc_fxp_bitlinear")
+    return y, ey

@@ -710,3 +710,49 @@ int orc_fxp_rmsnorm(const int16_t* xq, int ex, const int8_t* wq, int ew, int row
   }
   return ORC_OK;
 }
+
+/* F6 -- a BitLinear in W8A16 ("8-bit weights and 16-bit activations"; the
+ * ternary weights need no further quantization): F5's RMSNorm of the int16 input,
+ * the ternary contraction of the int16 normalised activations (exact, int64 here; it
+ * fits int32 for K <= 65535), the matrix scale beta quantized like the norm scales (F1
+ * with shift 6 applied to the scalar beta), and the output requantized per row to int16
+ * with the smallest fitting exponent (as in F5):
+ *   (yn, en) = F5(xq, ex, gq, eg, eps);  acc[r][n] = sum_k t[n][k] yn[r][k];
+ *   (bq, eb) = F1([beta], 6);  p = acc bq;  y = round(p / 2^s) (half away),
+ *   ey[r] = s + en[r] + eb. */
+int orc_fxp_bitlinear(const int16_t* xq, int ex, const int8_t* gq, int eg, double eps,
+                      const int8_t* t, float beta, int M, int K, int N, int16_t* y, int32_t* ey) {
+  if (M < 0 || K <= 0 || K > 65535 || N <= 0) return ORC_ERR_ARG;
+  int8_t bq;
+  int eb;
+  int rc = orc_fxp_scales(&beta, 1, 6, &bq, &eb);
+  if (rc) return rc;
+  int16_t* yn = (int16_t*)malloc(sizeof(int16_t) * ((size_t)M * K + 1));
+  int32_t* en = (int32_t*)malloc(sizeof(int32_t) * ((size_t)M + 1));
+  int64_t* p = (int64_t*)malloc(sizeof(int64_t) * (size_t)N);
+  if (!yn || !en || !p) {
+    free(yn);
+    free(en);
+    free(p);
+    return ORC_ERR_ARG;
+  }
+  rc = orc_fxp_rmsnorm(xq, ex, gq, eg, M, K, eps, yn, en);
+  for (int r = 0; r < M && rc == ORC_OK; ++r) {
+    int64_t pmax = 0;
+    for (int n = 0; n < N; ++n) {
+      int64_t acc = 0;
+      for (int k = 0; k < K; ++k) acc += (int64_t)t[(int64_t)n * K + k] * yn[(int64_t)r * K + k];
+      p[n] = acc * bq;
+      const int64_t a = p[n] < 0 ? -p[n] : p[n];
+      if (a > pmax) pmax = a;
+    }
+    int s = 0;
+    while (rha_shift(pmax, s) > 32767) ++s;
+    for (int n = 0; n < N; ++n) y[(int64_t)r * N + n] = (int16_t)rha_shift(p[n], s);
+    ey[r] = s + en[r] + eb;
+  }
+  free(yn);
+  free(en);
+  free(p);
+  return rc;
+}

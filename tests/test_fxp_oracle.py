@@ -188,3 +188,60 @@ def test_rmsnorm_zero_gain_and_scale_covariance():
     b, eb = O.fxp_rmsnorm(x, -9, wq, -6)       # doubling x: output changes by < 0.1 %
     va, vb = a * 2.0 ** ea[:, None], b * 2.0 ** eb[:, None]
     assert np.abs(va - vb).max() <= 1e-3 * np.abs(va).max()
+
+
+# ------------------------------------------------------------------ F6 W8A16 BitLinear
+def _f6_case(M, K, N, seed):
+    rng = np.random.default_rng(seed)
+    x = (rng.standard_normal((M, K)) * 3.0).astype(np.float32)
+    g = (1.0 + 0.2 * rng.standard_normal(K)).astype(np.float32)
+    W = (0.02 * rng.standard_normal((N, K))).astype(np.float32)
+    t, beta = O.ternarize(W)
+    xq, ex = O.fxp_quant_act(x)
+    gq, eg = O.fxp_scales(g)
+    return x, g, t, beta, xq, ex, gq, eg
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 64, 16), (5, 1000, 300), (3, 1024, 1024)])
+def test_bitlinear_w8a16_vs_float(M, K, N):
+    """(a) Against the float BitLinear (Eq. 1 RMSNorm with eps = 1e-3, the ternary product,
+    the scale) of the QUANTIZED operands x_q 2^ex, g_q 2^eg, b_q 2^eb: within the int16
+    roundings, 1e-4 of the row's largest output plus one output step.  (b) Against the float
+    operands within the gains' and beta's int8 quantization errors, bounded term by term."""
+    x, g, t, beta, xq, ex, gq, eg = _f6_case(M, K, N, K + N)
+    y, ey = O.fxp_bitlinear(xq, ex, gq, eg, t, beta)
+    got = y * 2.0 ** ey[:, None].astype(np.float64)
+    step = 2.0 ** ey[:, None].astype(np.float64)
+    bq, eb = O.fxp_scales(np.array([beta], np.float32))
+    bqv = float(bq[0]) * 2.0 ** eb
+    gqv = gq * 2.0 ** eg
+    ref_q = _eq1(xq * 2.0 ** ex, gqv, 1e-3) @ t.T.astype(np.float64) * bqv
+    scale = np.abs(ref_q).max(1, keepdims=True)
+    assert np.all(np.abs(got - ref_q) <= 1e-4 * scale + step)
+    assert np.all(np.abs(y).max(1) > 16383)      # the smallest fitting output exponent
+    xn1 = _eq1(x, np.ones(K), 1e-3)              # x / rms(x)
+    ref = xn1 * g @ t.T.astype(np.float64) * beta
+    bound = (np.abs(xn1) * np.abs(g - gqv)) @ np.abs(t.T).astype(np.float64) * abs(bqv) \
+        + np.abs(ref) * abs(bqv / beta - 1.0) + 2e-3 * scale + step
+    assert np.all(np.abs(got - ref) <= bound)
+
+
+def test_bitlinear_w8a16_identity_and_zero():
+    """t = I: the output is F5's normalised row times beta's int8 value, exactly rescaled;
+    a zero row stays zero."""
+    K = 128
+    rng = np.random.default_rng(9)
+    xq = rng.integers(-20000, 20000, (2, K)).astype(np.int16)
+    xq[1] = 0
+    gq, eg = np.full(K, 64, np.int8), -6
+    t = np.eye(K, dtype=np.int8)
+    beta = 0.75                                  # log2 0.75 -> 0: e = -6, bq = 48 exactly
+    y, ey = O.fxp_bitlinear(xq, -4, gq, eg, t, beta)
+    yn, en = O.fxp_rmsnorm(xq, -4, gq, eg)
+    p = yn[0].astype(np.int64) * 48
+    s = 0
+    while np.abs(np.where(p < 0, -((-p + (1 << s >> 1)) >> s), (p + (1 << s >> 1)) >> s)).max() > 32767:
+        s += 1
+    assert ey[0] == s + en[0] - 6
+    assert np.allclose(y[0] * 2.0 ** ey[0], yn[0] * 2.0 ** en[0] * 0.75, atol=2.0 ** ey[0])
+    assert not y[1].any()
