@@ -421,6 +421,23 @@ tern_status tern_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_t*
                              double eps, int32_t rows, int32_t d, int16_t* out, int32_t* eo,
                              tern_stream stream);
 
+/* F6: a BitLinear in W8A16.  xq [m][k] int16 with exponent *ex
+ * (device int32), norm gains gq [k] int8 with exponent eg (host), eps (1e-3):
+ *   (yn, en) = tern_fxp_rmsnorm(xq)            (per-row exponents en)
+ *   acc[r][n] = sum_k t[n][k] yn[r][k]          (exact; on the int8 tensor
+ *     cores as 256 (W hi) + (W lo') + 128 sum_k t[n][k], hi = yn >> 8,
+ *     lo' = (yn & 255) - 128, both s8)
+ *   (bq, eb) = F1(w->scales[0], shift 6);  y = round(acc bq / 2^s) int16
+ *   with the smallest fitting s per row, ey[r] = s + en[r] + eb.
+ * w: n_seg == 1, w->k == k <= 65535.  y [m][ldy] int16, ldy >= n_out; ey [m].
+ * xq and ws 16-byte aligned; ws_bytes >= tern_fxp_bitlinear_workspace(m, k,
+ * w->n_rows).  m == 0: no-op. */
+size_t tern_fxp_bitlinear_workspace(int32_t m, int32_t k, int32_t n_rows);
+tern_status tern_fxp_bitlinear(const int16_t* xq, const int32_t* ex, int32_t m, int32_t k,
+                               const int8_t* gq, int32_t eg, double eps, const tern_weight* w,
+                               int16_t* y, int32_t ldy, int32_t* ey, void* ws, size_t ws_bytes,
+                               tern_stream stream);
+
 /* Device self-check of the numerics shortcuts the kernels take (test use):
  * which = 0: the FMA-corrected reciprocals used by the sigmoids equal IEEE
  * 1/d for every mantissa of every exponent 0..125 (d in [1, 2^126));

@@ -128,6 +128,9 @@ _SIGS = {
     "tern_fxp_sigmoid": (C.c_int, [P, C.c_int64, P, P]),
     "tern_fxp_inv_sqrt": (C.c_int, [P, P, C.c_int64, P, P, P]),
     "tern_fxp_rmsnorm": (C.c_int, [P, P, P, I32, C.c_double, I32, I32, P, P, P]),
+    "tern_fxp_bitlinear_workspace": (SZ, [I32, I32, I32]),
+    "tern_fxp_bitlinear": (C.c_int, [P, P, I32, I32, P, I32, C.c_double, C.POINTER(tern_weight),
+                                     P, I32, P, P, SZ, P]),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -402,6 +405,20 @@ def tern_fxp_rmsnorm(xq: torch.Tensor, ex: torch.Tensor, wq: torch.Tensor, ew: i
     rows, d = xq.shape
     _check(load().tern_fxp_rmsnorm(ptr(xq), ptr(ex), ptr(wq), int(ew), float(eps), rows, d,
                                    ptr(out), ptr(eo), stream_handle(stream)), "tern_fxp_rmsnorm")
+
+
+def tern_fxp_bitlinear(xq: torch.Tensor, ex: torch.Tensor, gq: torch.Tensor, eg: int,
+                       w: tern_weight, y: torch.Tensor, ey: torch.Tensor, eps: float = 1e-3,
+                       ws=None, stream=None):
+    """F6: W8A16 BitLinear, int16 [m][k] -> int16 [m][n_out] + int32 exponents [m]."""
+    m, k = xq.shape
+    L = load()
+    need = int(L.tern_fxp_bitlinear_workspace(m, k, w.n_rows))
+    if ws is None:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=xq.device)
+    _check(L.tern_fxp_bitlinear(ptr(xq), ptr(ex), m, k, ptr(gq), int(eg), float(eps), C.byref(w),
+                                ptr(y), y.stride(0), ptr(ey), ptr(ws), ws.numel(),
+                                stream_handle(stream)), "tern_fxp_bitlinear")
 
 
 def tern_selftest(which: int) -> int:

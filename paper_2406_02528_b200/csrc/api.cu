@@ -556,6 +556,86 @@ tern_status tern_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_t*
   return TERN_OK;
 }
 
+// W8A16 BitLinear (F6) workspace: the normalised rows, their exponents, two s8 digit planes
+// with q-sums, a ones row, the rows' ternary sums and two int32 accumulator planes
+struct FxpBlWs {
+  size_t yn, en, hi, lo, qh, ql, ones, qo, rsum, ah, al, total;
+};
+static FxpBlWs fxp_bl_ws(int m, int k, int n_rows) {
+  auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t ldq = (size_t)kpad(k);
+  FxpBlWs L;
+  size_t o = 0;
+  L.yn = o; o += up((size_t)m * k * 2 + 16);
+  L.en = o; o += up((size_t)m * 4 + 4);
+  L.hi = o; o += up((size_t)m * ldq + 16);
+  L.lo = o; o += up((size_t)m * ldq + 16);
+  L.qh = o; o += up((size_t)m * 4 + 4);
+  L.ql = o; o += up((size_t)m * 4 + 4);
+  L.ones = o; o += up(ldq);
+  L.qo = o; o += up(4);
+  L.rsum = o; o += up((size_t)n_rows * 4);
+  L.ah = o; o += up((size_t)m * n_rows * 4 + 4);
+  L.al = o; o += up((size_t)m * n_rows * 4 + 4);
+  L.total = o;
+  return L;
+}
+
+size_t tern_fxp_bitlinear_workspace(int32_t m, int32_t k, int32_t n_rows) {
+  if (m < 0 || k <= 0 || n_rows <= 0) return 0;
+  return fxp_bl_ws(m, k, n_rows).total;
+}
+
+tern_status tern_fxp_bitlinear(const int16_t* xq, const int32_t* ex, int32_t m, int32_t k,
+                               const int8_t* gq, int32_t eg, double eps, const tern_weight* w,
+                               int16_t* y, int32_t ldy, int32_t* ey, void* ws, size_t ws_bytes,
+                               tern_stream stream) {
+  CHECK(m >= 0 && k >= 1 && k <= 65535, "tern_fxp_bitlinear: m=%d k=%d", m, k);
+  CHECK(eps >= 0.0 && eps < 1e30, "tern_fxp_bitlinear: eps=%g", eps);
+  tern_status st = check_weight(w, k, 1, "tern_fxp_bitlinear");
+  if (st) return st;
+  if (m == 0) return TERN_OK;
+  CHECK(xq && ex && gq && y && ey && ws, "tern_fxp_bitlinear: null pointer");
+  CHECK(aligned16(xq) && aligned16(ws), "tern_fxp_bitlinear: xq / ws not 16-byte aligned");
+  CHECK(ldy >= w->n_out, "tern_fxp_bitlinear: ldy=%d < n_out=%d", ldy, w->n_out);
+  const FxpBlWs L = fxp_bl_ws(m, k, w->n_rows);
+  CHECK(ws_bytes >= L.total, "tern_fxp_bitlinear: workspace %zu < %zu", ws_bytes, L.total);
+  st = check_device();
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* b = static_cast<char*>(ws);
+  int16_t* yn = reinterpret_cast<int16_t*>(b + L.yn);
+  int32_t* en = reinterpret_cast<int32_t*>(b + L.en);
+  int8_t* hi = reinterpret_cast<int8_t*>(b + L.hi);
+  int8_t* lo = reinterpret_cast<int8_t*>(b + L.lo);
+  int32_t* qh = reinterpret_cast<int32_t*>(b + L.qh);
+  int32_t* ql = reinterpret_cast<int32_t*>(b + L.ql);
+  int8_t* ones = reinterpret_cast<int8_t*>(b + L.ones);
+  int32_t* qo = reinterpret_cast<int32_t*>(b + L.qo);
+  int32_t* rsum = reinterpret_cast<int32_t*>(b + L.rsum);
+  int32_t* ah = reinterpret_cast<int32_t*>(b + L.ah);
+  int32_t* al = reinterpret_cast<int32_t*>(b + L.al);
+  const int ldq = kpad(k);
+  TRY_CUDA(launch_fxp_rmsnorm(xq, ex, gq, eg, eps, m, k, yn, en, s), "fxp_bitlinear norm");
+  TRY_CUDA(launch_fxp_split(yn, m, k, ldq, hi, lo, qh, ql, ones, qo, s), "fxp_bitlinear split");
+  // three exact int8 x ternary contractions on the tcgen05 GEMM (EPI_NONE: int32 out)
+  const int8_t* qs[3] = {hi, lo, ones};
+  const int32_t* sums[3] = {qh, ql, qo};
+  int32_t* outs[3] = {ah, al, rsum};
+  const int rows[3] = {m, m, 1};
+  for (int i = 0; i < 3; ++i) {
+    Epi e = make_epi(EPI_NONE, *w, nullptr, nullptr, 0);
+    e.acc = outs[i];
+    e.ldacc = w->n_rows;
+    TRY_CUDA(launch_gemm(qs[i], rows[i], ldq, reinterpret_cast<const float*>(sums[i]), sums[i], *w,
+                         TERN_F32, e, s),
+             "fxp_bitlinear gemm");
+  }
+  TRY_CUDA(launch_fxp_combine(ah, al, w->n_rows, rsum, w->scales, w->n_out, m, en, y, ldy, ey, s),
+           "fxp_bitlinear combine");
+  return TERN_OK;
+}
+
 tern_status tern_mlgru_scan(const void* fcg, tern_dtype dt, int32_t B, int32_t T, int32_t d,
                             tern_gate_mode gate, float* h, void* oprime, tern_stream stream) {
   CHECK(fcg && h && oprime, "tern_mlgru_scan: null pointer");

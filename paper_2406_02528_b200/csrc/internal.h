@@ -145,6 +145,13 @@ cudaError_t launch_fxp_quant_act(const void* x, int dt, int64_t n, int16_t* q, i
 cudaError_t launch_fxp_sigmoid(const int32_t* x, int64_t n, int32_t* y, cudaStream_t s);
 cudaError_t launch_fxp_inv_sqrt(const uint64_t* v, const int32_t* e, int64_t n, uint32_t* y,
                                 int32_t* ey, cudaStream_t s);
+cudaError_t launch_fxp_split(const int16_t* a, int m, int k, int ldq, int8_t* hi, int8_t* lo,
+                             int32_t* qs_hi, int32_t* qs_lo, int8_t* ones, int32_t* qs_ones,
+                             cudaStream_t s);
+cudaError_t launch_fxp_combine(const int32_t* acc_hi, const int32_t* acc_lo, int ldacc,
+                               const int32_t* rowsum, const float* scale, int n, int m,
+                               const int32_t* en, int16_t* y, int ldy, int32_t* ey,
+                               cudaStream_t s);
 cudaError_t launch_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_t* wq, int ew,
                                double eps, int rows, int d, int16_t* out, int32_t* eo,
                                cudaStream_t s);

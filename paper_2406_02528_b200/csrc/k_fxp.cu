@@ -439,6 +439,97 @@ __global__ void __launch_bounds__(kFxWarpRows * 32) k_fxp_rmsnorm_warp(
   }
 }
 
+// ---------------------------------------------------------------- F6 W8A16 BitLinear
+// int16 rows -> two s8 digit planes for the int8 tensor cores: a = 256 hi + lo' + 128 with
+// hi = a >> 8 in [-128, 127] and lo' = (a & 255) - 128 in [-128, 127]; pads (k >= K) are
+// 0 in both planes (their ternary codes are 0, so nothing is lost); per-row digit sums are
+// the GEMM's q-sum corrections.  One warp per row.
+__global__ void __launch_bounds__(256) k_fxp_split(const int16_t* __restrict__ a, int m, int k,
+                                                    int ldq, int8_t* __restrict__ hi,
+                                                    int8_t* __restrict__ lo,
+                                                    int32_t* __restrict__ qs_hi,
+                                                    int32_t* __restrict__ qs_lo) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= m) return;
+  const int16_t* ar = a + (int64_t)r * k;
+  int8_t* hr = hi + (int64_t)r * ldq;
+  int8_t* lr = lo + (int64_t)r * ldq;
+  int32_t sh = 0, sl = 0;
+  for (int c = lane * 4; c < ldq; c += 128) {   // 4 columns per lane: one 32-bit store each
+    uint32_t ph = 0, pl = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int32_t h = 0, l = 0;
+      if (c + j < k) {
+        const int32_t v = ar[c + j];
+        h = v >> 8;                  // arithmetic: floor(v / 256)
+        l = (v & 255) - 128;
+      }
+      sh += h;
+      sl += l;
+      ph |= (uint32_t)(h & 255) << (8 * j);
+      pl |= (uint32_t)(l & 255) << (8 * j);
+    }
+    *reinterpret_cast<uint32_t*>(hr + c) = ph;
+    *reinterpret_cast<uint32_t*>(lr + c) = pl;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sh += __shfl_xor_sync(0xffffffffu, sh, o);
+    sl += __shfl_xor_sync(0xffffffffu, sl, o);
+  }
+  if (lane == 0) {
+    qs_hi[r] = sh;
+    qs_lo[r] = sl;
+  }
+}
+
+// a row of K ones (pads 0) and its sum: contracting it gives each output's sum_k t[n][k]
+__global__ void k_fxp_ones(int8_t* __restrict__ ones, int k, int ldq, int32_t* __restrict__ qs) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ldq; c += gridDim.x * blockDim.x)
+    ones[c] = c < k ? 1 : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *qs = k;
+}
+
+// (bq, eb) = F1([beta], shift 6) on the device: the same frexp rule as k_fxp_scales
+__device__ __forceinline__ void fx_beta(float beta, int& bq, int& eb) {
+  int p;
+  const float f = frexpf(fabsf(beta), &p);
+  eb = ((double)f >= 0.70710678118654752440 ? p : p - 1) - 6;
+  bq = (int)roundf(ldexpf(beta, -eb));
+}
+
+// acc = 256 acc_hi + acc_lo + 128 rowsum (exact), p = acc bq, per-row int16 requantization
+__global__ void __launch_bounds__(kFxThreads) k_fxp_combine(
+    const int32_t* __restrict__ acc_hi, const int32_t* __restrict__ acc_lo, int ldacc,
+    const int32_t* __restrict__ rowsum, const float* __restrict__ scale, int n, int m,
+    const int32_t* __restrict__ en, int16_t* __restrict__ y, int ldy, int32_t* __restrict__ ey) {
+  __shared__ int64_t red[kFxThreads / 32];
+  int bq, eb;
+  fx_beta(__ldg(scale), bq, eb);
+  for (int r = blockIdx.x; r < m; r += gridDim.x) {
+    const int32_t* h = acc_hi + (int64_t)r * ldacc;
+    const int32_t* l = acc_lo + (int64_t)r * ldacc;
+    int64_t pmax = 0;
+    for (int c = threadIdx.x; c < n; c += kFxThreads) {
+      const int64_t acc = 256 * (int64_t)h[c] + l[c] + 128 * (int64_t)__ldg(rowsum + c);
+      const int64_t pv = acc * bq;
+      pmax = max(pmax, pv < 0 ? -pv : pv);
+    }
+    pmax = fx_block_max_i64(pmax, red);
+    int s = 0;
+    while (fx_rha_shift(pmax, s) > 32767) ++s;
+    int16_t* yr = y + (int64_t)r * ldy;
+    for (int c = threadIdx.x; c < n; c += kFxThreads) {
+      const int64_t acc = 256 * (int64_t)h[c] + l[c] + 128 * (int64_t)__ldg(rowsum + c);
+      yr[c] = (int16_t)fx_rha_shift(acc * bq, s);
+    }
+    if (threadIdx.x == 0) ey[r] = s + en[r] + eb;
+    __syncthreads();   // red is reused by the next row
+  }
+}
+
 // ---------------------------------------------------------------- host side
 static SigLut sig_lut() {   // F3: y_i = floor(sigma(i) 2^15), sigma in binary64
   SigLut L;
@@ -523,4 +614,25 @@ cudaError_t launch_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_
   return cudaGetLastError();
 }
 
+}  // namespace tern
+
+namespace tern {
+cudaError_t launch_fxp_split(const int16_t* a, int m, int k, int ldq, int8_t* hi, int8_t* lo,
+                             int32_t* qs_hi, int32_t* qs_lo, int8_t* ones, int32_t* qs_ones,
+                             cudaStream_t s) {
+  k_fxp_ones<<<(ldq + 255) / 256, 256, 0, s>>>(ones, k, ldq, qs_ones);
+  if (m > 0) k_fxp_split<<<(m + 7) / 8, 256, 0, s>>>(a, m, k, ldq, hi, lo, qs_hi, qs_lo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fxp_combine(const int32_t* acc_hi, const int32_t* acc_lo, int ldacc,
+                               const int32_t* rowsum, const float* scale, int n, int m,
+                               const int32_t* en, int16_t* y, int ldy, int32_t* ey,
+                               cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  const int grid = m < fx_sms() * 4 ? m : fx_sms() * 4;
+  k_fxp_combine<<<grid, kFxThreads, 0, s>>>(acc_hi, acc_lo, ldacc, rowsum, scale, n, m, en, y,
+                                            ldy, ey);
+  return cudaGetLastError();
+}
 }  // namespace tern

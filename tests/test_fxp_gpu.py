@@ -139,3 +139,58 @@ def test_rmsnorm_eps_underflow(L, eps):
     out_o, eo_o = O.fxp_rmsnorm(xq.cpu().numpy(), 0, wq.cpu().numpy(), -6, eps=eps)
     assert np.array_equal(out.cpu().numpy(), out_o) and np.array_equal(eo.cpu().numpy(), eo_o)
     assert not out[0].any()
+
+
+@pytest.fixture(scope="module")
+def M():
+    from paper_2406_02528_b200 import model
+    return model
+
+
+@pytest.mark.parametrize("m,k,n", [(1, 64, 16), (1, 1024, 1024), (4, 1000, 300), (7, 688, 256),
+                                   (130, 1024, 640), (300, 2816, 1024), (2048, 1024, 3072)])
+def test_bitlinear_w8a16(L, M, m, k, n):
+    """F6 through the C ABI: F5 norm, the int16 x ternary contraction as two s8 digit planes on
+    the tcgen05 GEMM plus the ternary row sums, the pow2 int8 beta, per-row requantization --
+    bit-exact against the oracle over ragged m / k / n (k not a multiple of 128, n not a
+    multiple of the GEMM tile); rows span 1e-2..1e2 of the tensor scale, one zero row."""
+    g = synth.generator(m * 13 + k + n)
+    W = synth.latent_matrix(n, k, g)
+    pw = M.PackedWeight([W.cuda()])
+    t, beta = O.ternarize(W.numpy())
+    x = synth.hidden((m, k), g, "f32") * torch.logspace(-2, 2, m)[:, None]
+    if m > 2:
+        x[2] = 0.0
+    gain = 1.0 + 0.25 * torch.randn(k, generator=g)
+    xq = torch.empty((m, k), dtype=torch.int16, device="cuda")
+    ex = torch.empty(1, dtype=torch.int32, device="cuda")
+    L.tern_fxp_quant_act(x.cuda(), xq, ex)
+    gq, eg = L.tern_fxp_scales(gain.cuda())
+    y = torch.full((m, n), 321, dtype=torch.int16, device="cuda")
+    ey = torch.full((m,), 99, dtype=torch.int32, device="cuda")
+    L.tern_fxp_bitlinear(xq, ex, gq, eg, pw.struct, y, ey)
+    torch.cuda.synchronize()
+    y_o, ey_o = O.fxp_bitlinear(xq.cpu().numpy(), int(ex.item()), gq.cpu().numpy(), eg, t, beta)
+    assert np.array_equal(ey.cpu().numpy(), ey_o)
+    assert np.array_equal(y.cpu().numpy(), y_o)
+
+
+def test_bitlinear_w8a16_extreme_digits(L, M):
+    """Inputs at the int16 extremes (-32768, 32767, -1, 255, 256): the normalised rows reach
+    +-32767, exercising the digit split's ends (hi = -128 / 127, lo' = -128 / 127) and the
+    128 sum_k t correction."""
+    k, n, m = 256, 128, 3
+    W = synth.latent_matrix(n, k, synth.generator(77))
+    pw = M.PackedWeight([W.cuda()])
+    t, beta = O.ternarize(W.numpy())
+    vals = np.array([-32768, 32767, -1, 255, 256, -256, 0, 128], np.int16)
+    xq_np = np.resize(vals, (m, k)).astype(np.int16)
+    xq_np[1] = np.roll(xq_np[1], 3)
+    xq = torch.from_numpy(xq_np).cuda()
+    ex = torch.tensor([-12], dtype=torch.int32, device="cuda")
+    gq = torch.full((k,), 64, dtype=torch.int8, device="cuda")
+    y = torch.empty((m, n), dtype=torch.int16, device="cuda")
+    ey = torch.empty((m,), dtype=torch.int32, device="cuda")
+    L.tern_fxp_bitlinear(xq, ex, gq, -6, pw.struct, y, ey)
+    y_o, ey_o = O.fxp_bitlinear(xq_np, -12, np.full(k, 64, np.int8), -6, t, beta)
+    assert np.array_equal(y.cpu().numpy(), y_o) and np.array_equal(ey.cpu().numpy(), ey_o)

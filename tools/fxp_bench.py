@@ -100,6 +100,33 @@ eyv = torch.empty(n, dtype=torch.int32, device=dev)
 us = timed(lambda: L.tern_fxp_inv_sqrt(v, ev, yv, eyv), args.reps)
 report("fxp_inv_sqrt", us, n * (8 + 4 + 4 + 4), "u64 + i32 in, u32 + i32 out")
 
+# W8A16 BitLinear (F6) on the c2 o-projection shape: 16384 x 1024 -> 1024
+from paper_2406_02528_b200 import model  # noqa: E402
+
+i8 = json.load(open(os.path.join(ROOT, "profiles", "int8_peak.json")))["int8_tops_sustained"]
+Wl = synth.latent_matrix(1024, K, synth.generator(8, "cuda"), device="cuda")
+pw = model.PackedWeight([Wl])
+yb = [torch.empty((M, 1024), dtype=torch.int16, device=dev) for _ in range(NC)]
+eyb = torch.empty(M, dtype=torch.int32, device=dev)
+wsb = torch.empty(int(L.load().tern_fxp_bitlinear_workspace(M, K, 1024)), dtype=torch.uint8,
+                  device=dev)
+
+
+def bl():
+    i = it[0] % NC
+    it[0] += 1
+    L.tern_fxp_bitlinear(qs[i], e, wq, ew, pw.struct, yb[i], eyb, ws=wsb)
+
+
+us = timed(bl, args.reps)
+tops = 2.0 * M * K * 1024 / (us * 1e-6) / 1e12
+rows.append({"kernel": "fxp_bitlinear (norm + split + 3 tcgen05 GEMMs + combine)", "us": round(us, 2),
+             "dense_equiv_TOPS_int16xternary": round(tops, 1),
+             "int8_TOPS_issued": round(2 * tops, 1), "int8_peak_TOPS": i8,
+             "int8_frac_issued": round(2 * tops / i8, 4),
+             "note": "two s8 digit planes: 2 int8 GEMMs per int16 contraction"})
+print(json.dumps(rows[-1]), flush=True)
+
 res = {"hbm_peak_GBps": hbm, "device": torch.cuda.get_device_name(0), "points": rows,
        "method": "CUDA events around back-to-back calls; quant_act / rmsnorm cycle through 4 "
                  "copies (256 / 256 MB) so no call finds its data in L2; sigmoid / inv_sqrt "
