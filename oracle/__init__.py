@@ -116,6 +116,11 @@ def lib():
                                           C.c_double, i16p, i32p]
             L.orc_fxp_bitlinear.argtypes = [i16p, C.c_int, i8p, C.c_int, C.c_double, i8p,
                                              C.c_float, C.c_int, C.c_int, C.c_int, i16p, i32p]
+            L.orc_set_scan_slices.argtypes = [C.c_int]
+            L.orc_set_scan_slices.restype = None
+            L.orc_get_scan_slices.restype = C.c_int
+            L.orc_scan_seqpar.argtypes = [f32p, f32p, C.c_int, C.c_int, C.c_float, f32p,
+                                          C.POINTER(C.c_float)]
             L.orc_set_threads.argtypes = [C.c_int]
             L.orc_get_threads.restype = C.c_int
             _lib = L
@@ -470,3 +475,29 @@ def fxp_bitlinear(xq, ex, gq, eg, t, beta, eps=1e-3):
                                    float(eps), t, C.c_float(beta), M, K, N, y, ey),
            "orc_fxp_bitlinear")
     return y, ey
+
+
+# ---------------------------------------------------------------- sequence-parallel scan (f3)
+def scan_seqpar(f, c, W, h0=0.0):
+    """Reading C23: W contiguous slices, slice aggregates composed in order, each slice
+    scanned sequentially from its boundary state.  -> (h [T], final state)."""
+    f, c = _f32(f), _f32(c)
+    h = np.empty_like(f)
+    hf = C.c_float(0.0)
+    lib().orc_scan_seqpar(f, c, f.size, int(W), C.c_float(h0), h, C.byref(hf))
+    return h, np.float32(hf.value)
+
+
+class scan_slices:
+    """Context manager: orc_mlgru_scan (and so mlgru / block / stack) uses the W-slice
+    sequence-parallel scan of reading C23 while active."""
+
+    def __init__(self, w: int):
+        self.w = int(w)
+
+    def __enter__(self):
+        self.old = lib().orc_get_scan_slices()
+        lib().orc_set_scan_slices(self.w)
+
+    def __exit__(self, *exc):
+        lib().orc_set_scan_slices(self.old)

@@ -408,9 +408,70 @@ void orc_scan_chunked(const float* f, const float* c, int T, int chunk, float h0
   }
 }
 
+/* Sequence-parallel scan ("a multi-GPU sequence-parallel scan (carry
+ * exchange) is the long-context variant"; reading C23 in DESIGN.md).  The T steps are cut
+ * into W contiguous slices [j T / W, (j+1) T / W).  Each slice's aggregate is the
+ * left-to-right composition of its pairs (a, b) = (f, (1-f) c),
+ *   A = A a,  Bv = a Bv + b   (from A = 1, Bv = 0; i.e. the recurrence from h = 0),
+ * the boundary states compose in slice order, h_in(0) = H, h_in(j+1) = A_j h_in(j) + Bv_j,
+ * each slice is then scanned sequentially from its h_in, and the final state is the
+ * composition through every slice, h_in(W).  W = 1 is the sequential scan. */
+static int g_scan_slices = 1;
+void orc_set_scan_slices(int w) { g_scan_slices = w >= 1 ? w : 1; }
+int orc_get_scan_slices(void) { return g_scan_slices; }
+
+void orc_scan_seqpar(const float* f, const float* c, int T, int W, float h0, float* h_out,
+                     float* h_final) {
+  float hin = h0;
+  for (int j = 0; j < W; ++j) {
+    const int s0 = (int)((int64_t)j * T / W), s1 = (int)((int64_t)(j + 1) * T / W);
+    float A = 1.0f, Bv = 0.0f;
+    for (int t = s0; t < s1; ++t) {
+      A = A * f[t];
+      Bv = scan_step(f[t], Bv, c[t]);
+    }
+    float h = hin;
+    for (int t = s0; t < s1; ++t) {
+      h = scan_step(f[t], h, c[t]);
+      h_out[t] = h;
+    }
+    hin = A * hin + Bv;
+  }
+  *h_final = hin;
+}
+
+static int orc_mlgru_scan_sp(const float* fhat, const float* chat, const float* ghat, int B, int T,
+                             int d, int gate_mode, int bf16, float* H, float* oprime, int W) {
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int b = 0; b < B; ++b)
+    for (int ch = 0; ch < d; ++ch) {
+      float hin = H[(int64_t)b * d + ch];
+      for (int j = 0; j < W; ++j) {
+        const int s0 = (int)((int64_t)j * T / W), s1 = (int)((int64_t)(j + 1) * T / W);
+        float A = 1.0f, Bv = 0.0f, h = hin;
+        for (int t = s0; t < s1; ++t) {
+          int64_t i = ((int64_t)b * T + t) * d + ch;
+          float f = orc_sigmoid(fhat[i]);
+          float c = orc_silu(chat[i]);
+          A = A * f;
+          Bv = scan_step(f, Bv, c);
+          h = scan_step(f, h, c);
+          float o = gate_mode == 0 ? ghat[i] * orc_sigmoid(h) : ghat[i] * h;
+          if (bf16) o = orc_bf16(o);
+          oprime[i] = o;
+        }
+        hin = A * hin + Bv;
+      }
+      H[(int64_t)b * d + ch] = hin;
+    }
+  return ORC_OK;
+}
+
 int orc_mlgru_scan(const float* fhat, const float* chat, const float* ghat, int B, int T, int d,
                    int gate_mode, int bf16, float* H, float* oprime) {
   if (B < 0 || T < 0 || d <= 0) return ORC_ERR_ARG;
+  if (g_scan_slices > 1)
+    return orc_mlgru_scan_sp(fhat, chat, ghat, B, T, d, gate_mode, bf16, H, oprime, g_scan_slices);
 #pragma omp parallel for collapse(2) schedule(static)
   for (int b = 0; b < B; ++b)
     for (int ch = 0; ch < d; ++ch) {

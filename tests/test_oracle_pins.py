@@ -488,3 +488,51 @@ def test_state_is_constant_size():
     for _ in range(20):
         _, H = O.block(blk, rng.standard_normal((1, 1, d)).astype(np.float32), H)
         assert H.shape == (1, d) and H.nbytes == d * 4
+
+
+# ---------------------------------------------------------------- sequence-parallel scan (C23)
+def test_scan_seqpar_single_slice_is_sequential():
+    f = O.sigmoid_c(rng.standard_normal(300).astype(np.float32))
+    c = rng.standard_normal(300).astype(np.float32)
+    h, hf = O.scan_seqpar(f, c, 1, 0.3)
+    hs = O.scan_seq(f, c, 0.3)
+    assert np.array_equal(h, hs) and hf == hs[-1]
+
+
+def test_scan_seqpar_closed_form_exact():
+    # S2 (f = 1/2, c = 1): h_t = 1 - 2^-t is exact in fp32 under any association (t <= 24),
+    # so every slicing reproduces it bit for bit, final state included
+    T = 24
+    f, c = np.full(T, 0.5, np.float32), np.ones(T, np.float32)
+    ref = (1.0 - 0.5 ** np.arange(1, T + 1)).astype(np.float32)
+    for W in (1, 2, 3, 4, 8, 24):
+        h, hf = O.scan_seqpar(f, c, W)
+        assert np.array_equal(h, ref) and hf == ref[-1], W
+
+
+def test_scan_seqpar_vs_sequential():
+    # only the boundary states are reassociated: the first slice is bit-identical to the
+    # sequential scan, the rest agree within the chunked-scan tolerance (S4)
+    for T, W in ((17, 2), (256, 4), (1000, 8), (5, 8)):
+        f = O.sigmoid_c(rng.standard_normal(T).astype(np.float32) * 2)
+        c = rng.standard_normal(T).astype(np.float32)
+        h, hf = O.scan_seqpar(f, c, W, -0.7)
+        hs = O.scan_seq(f, c, -0.7)
+        s1 = T // W
+        assert np.array_equal(h[:s1], hs[:s1])
+        assert np.allclose(h, hs, rtol=1e-5, atol=1e-6)
+        assert abs(hf - hs[-1]) <= 1e-5 * max(1.0, abs(hs[-1]))
+
+
+def test_mlgru_scan_slices_mode():
+    B, T, d = 2, 40, 8
+    fh, ch, gh = (rng.standard_normal((B, T, d)).astype(np.float32) for _ in range(3))
+    H = rng.standard_normal((B, d)).astype(np.float32)
+    o1, H1 = O.mlgru_scan(fh, ch, gh, H)
+    with O.scan_slices(4):
+        o4, H4 = O.mlgru_scan(fh, ch, gh, H)
+    assert np.array_equal(o4[:, :10], o1[:, :10])          # slice 0 starts from the true state
+    assert np.allclose(o4, o1, rtol=1e-5, atol=1e-6)
+    assert np.allclose(H4, H1, rtol=1e-5, atol=1e-6)
+    with O.scan_slices(1):
+        assert np.array_equal(O.mlgru_scan(fh, ch, gh, H)[0], o1)
