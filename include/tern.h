@@ -379,6 +379,34 @@ void tern_trace_enable(int32_t on);
 int32_t tern_trace_collect(uint64_t* out, int32_t max_launches);
 
 /* ------------------------------------------------------------------------
+ * Sequence-parallel prefill (the long-context variant; reading
+ * C23 in DESIGN.md).  The T tokens of every sequence are cut into `world`
+ * contiguous slices [r T/world, (r+1) T/world); rank r runs
+ * block_prefill_sp on its slice x [B][T_local][d] with the state h [B][d]
+ * the whole sequence starts from (identical on every rank).  Per block, the
+ * MLGRU scan exchanges ONE all-gather of 2 B d floats per rank -- the slice
+ * aggregates (A = prod f, B = the recurrence from 0, composed left to right,
+ * S:197) -- each rank composes the earlier ranks' aggregates in rank order into
+ * its boundary state, scans its slice exactly from it, and h leaves holding
+ * the state after the WHOLE sequence (the composition through every slice,
+ * the same on all ranks).  Everything else in the block is token-local.  The
+ * result equals the oracle's W-slice scan (O.scan_slices) bit for bit; with
+ * world = 1 it equals block_prefill.  T_local may be 0 (a rank with no
+ * tokens still joins the exchange; x, y may then be NULL).  The block must
+ * not be output-sharded.  ag is called once per block on `stream`.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t rank, world;
+  tern_allgather_fn ag;
+  void* ctx;
+} tern_seqpar;
+size_t tern_block_prefill_sp_workspace(const tern_block* b, int32_t B, int32_t T_local,
+                                       tern_dtype dt, int32_t world);
+tern_status block_prefill_sp(const tern_block* b, const void* x, void* y, tern_dtype dt,
+                             int32_t B, int32_t T_local, float* h, const tern_seqpar* sp,
+                             void* ws, size_t ws_bytes, tern_stream stream);
+
+/* ------------------------------------------------------------------------
  * Fixed-point W8A16 numerics of the paper's Loihi 2 deployment (SURVEY 8(f)
  * f4(ii); readings F1-F5 in DESIGN.md §3b).
  * Integers in, integers out, a value v with exponent e meaning v * 2^e.

@@ -62,6 +62,11 @@ class tern_shard(C.Structure):
                 ("ar", ALLREDUCE_FN)]
 
 
+class tern_seqpar(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("ag", ALLGATHER_FN),
+                ("ctx", C.c_void_p)]
+
+
 class tern_block(C.Structure):
     _fields_ = [("mix", tern_mlgru), ("ch", tern_glu), ("d", C.c_int32), ("l", C.c_int32),
                 ("shard", tern_shard), ("next_block", C.c_void_p)]
@@ -123,6 +128,9 @@ _SIGS = {
     "tern_set_norm_mode": (None, [C.c_int]),
     "tern_get_norm_mode": (C.c_int, []),
     "tern_get_batched_fin": (I32, []),
+    "tern_block_prefill_sp_workspace": (SZ, [C.POINTER(tern_block), I32, I32, C.c_int, I32]),
+    "block_prefill_sp": (C.c_int, [C.POINTER(tern_block), P, P, C.c_int, I32, I32, P,
+                                   C.POINTER(tern_seqpar), P, SZ, P]),
     "tern_fxp_scales": (C.c_int, [P, I32, I32, P, C.POINTER(I32), P, P]),
     "tern_fxp_quant_act": (C.c_int, [P, C.c_int, C.c_int64, P, P, P, P]),
     "tern_fxp_sigmoid": (C.c_int, [P, C.c_int64, P, P]),
@@ -365,6 +373,15 @@ def tern_profile_collect() -> list:
         out.append({"kernel": KERNEL_NAMES.get(r.kernel, str(r.kernel)), "epi": r.epi, "m": r.m,
                     "n": r.n, "k": r.k, "n_seg": r.n_seg, "dtype": r.dtype, "ms": float(r.ms)})
     return out
+
+
+# ---------------------------------------------------------------- sequence-parallel prefill (f3)
+def block_prefill_sp(blk, x, y, h, sp: tern_seqpar, ws, B: int, T_local: int, dt,
+                     stream=None):
+    """One block over this rank's token slice x [B][T_local][d] (tern.h block_prefill_sp)."""
+    _check(load().block_prefill_sp(C.byref(blk), ptr(x), ptr(y), dtype_code(dt), B, T_local,
+                                   ptr(h), C.byref(sp), ptr(ws), ws.numel(),
+                                   stream_handle(stream)), "block_prefill_sp")
 
 
 # ---------------------------------------------------------------- fixed point W8A16 (f4(ii))

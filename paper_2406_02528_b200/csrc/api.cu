@@ -684,11 +684,54 @@ struct PfPlan {
   size_t n[2] = {0, 0};
 };
 
+// Sequence-parallel prefill (C23): this rank holds tokens [rank T/world, ...) of every
+// sequence; the scan's boundary state comes from the other ranks' slice aggregates.
+struct SeqPar {
+  int rank = 0, world = 1;
+  tern_allgather_fn ag = nullptr;
+  void* ctx = nullptr;
+  float *send = nullptr, *recv = nullptr, *hfin = nullptr;   // [2][B][d], [world][2][B][d], [B][d]
+};
+
 tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid, tern_dtype dt,
                       int B, int T, int d, float* h, void* ws, const BlockWs& L, cudaStream_t s,
-                      const PfPlan& pf = PfPlan()) {
+                      const PfPlan& pf = PfPlan(), const SeqPar* sp = nullptr) {
   const int M = B * T;
   void* op = at<char>(ws, L.oprime);
+  if (sp) {
+    // pass 1 on the f^c^g^ of this slice, exchange, compose, pass 2 = the exact scan of
+    // the slice from its boundary state; the state after the block is the composition
+    // through every slice (identical on all ranks)
+    int8_t* q = at<int8_t>(ws, L.q);
+    float* deq = at<float>(ws, L.deq);
+    int32_t* qsum = at<int32_t>(ws, L.qsum);
+    void* fcg = at<char>(ws, L.fcg);
+    const int ldq = kpad(d);
+    if (T > 0) {
+      Epi e1 = make_epi(EPI_FCG, p.fcg, p.bias_fcg, fcg, p.fcg.n_rows);
+      tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
+                             nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
+      if (st) return st;
+    }
+    TRY_CUDA(launch_scan_agg(fcg, dt, B, T, d, sp->send, s), "seqpar aggregates");
+    const size_t per = (size_t)2 * B * d * sizeof(float);
+    if (sp->ag(sp->ctx, sp->send, sp->recv, per, (tern_stream)s) != 0)
+      return fail(TERN_ERR_CUDA, "block_prefill_sp: all-gather callback failed");
+    TRY_CUDA(launch_sp_compose(sp->recv, sp->world, sp->rank, (int64_t)B * d, h, sp->hfin, s),
+             "seqpar compose");
+    if (T > 0) {
+      Prof pr(TERN_K_SCAN, p.gate, B * T, d, d, 3, dt, s);
+      TRY_CUDA(launch_scan(fcg, dt, B, T, d, p.gate, h, op, s), "scan");
+    }
+    TRY_CUDA(cudaMemcpyAsync(h, sp->hfin, sizeof(float) * B * d, cudaMemcpyDeviceToDevice, s),
+             "seqpar state");
+    if (T == 0) return TERN_OK;
+    Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.o, p.bias_o, out, d);
+    e2.res = x;
+    e2.ldr = d;
+    return bl_tc(op, dt, M, d, d, p.gain_o, p.eps, p.o, dt, e2, q, ldq, deq, qsum, nullptr,
+                 nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
+  }
   if (T == 1 && B <= g_gemv_max_m && gemv_supported(B, d, dt)) {
     Epi e1 = make_epi(EPI_MLGRU, p.fcg, p.bias_fcg, op, d);
     e1.h = h;
@@ -1121,6 +1164,58 @@ static tern_status block_run(const tern_block* b, const void* x, void* y, tern_d
   }
   if ((st = run_mlgru(b->mix, x, x1, true, dt, B, T, b->d, h, ws, L, s, pm)) != TERN_OK) return st;
   return run_glu(b->ch, x1, y, true, dt, B * T, b->d, b->l, ws, L, s, pg);
+}
+
+// ---------------------------------------------------------------- sequence-parallel prefill
+static size_t sp_extra(int B, int d, int world) {
+  return al256((size_t)2 * B * d * 4) + al256((size_t)world * 2 * B * d * 4) +
+         al256((size_t)B * d * 4);
+}
+
+size_t tern_block_prefill_sp_workspace(const tern_block* b, int32_t B, int32_t T_local,
+                                       tern_dtype dt, int32_t world) {
+  if (!b || B < 0 || T_local < 0 || world < 1) return 0;
+  return block_ws(B * (T_local > 0 ? T_local : 1), b->d, b->l, b->mix.fcg.n_rows, dt).total +
+         sp_extra(B, b->d, world);
+}
+
+tern_status block_prefill_sp(const tern_block* b, const void* x, void* y, tern_dtype dt,
+                             int32_t B, int32_t T_local, float* h, const tern_seqpar* sp,
+                             void* ws, size_t ws_bytes, tern_stream stream) {
+  tern_status st = check_block(b);
+  if (st) return st;
+  CHECK(sp && sp->ag, "block_prefill_sp: null seqpar / all-gather");
+  CHECK(sp->world >= 1 && sp->rank >= 0 && sp->rank < sp->world, "block_prefill_sp: rank %d of %d",
+        sp->rank, sp->world);
+  CHECK(block_world(b) == 1, "block_prefill_sp: the block must not be output-sharded");
+  CHECK(B >= 1 && T_local >= 0, "block_prefill_sp: B=%d T_local=%d", B, T_local);
+  CHECK(valid_dt(dt), "block_prefill_sp: bad dtype");
+  CHECK(h && ws && aligned16(ws), "block_prefill_sp: null state or unaligned workspace");
+  const int Tq = T_local > 0 ? T_local : 1;
+  BlockWs L = block_ws(B * Tq, b->d, b->l, b->mix.fcg.n_rows, dt);
+  const size_t need = L.total + sp_extra(B, b->d, sp->world);
+  CHECK(ws_bytes >= need, "block_prefill_sp: workspace %zu < %zu", ws_bytes, need);
+  if (T_local > 0) {
+    CHECK(x && y && aligned16(x) && aligned16(y), "block_prefill_sp: x / y null or unaligned");
+  }
+  if ((st = check_device()) != TERN_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  SeqPar P;
+  P.rank = sp->rank;
+  P.world = sp->world;
+  P.ag = sp->ag;
+  P.ctx = sp->ctx;
+  char* base = static_cast<char*>(ws) + L.total;
+  P.send = reinterpret_cast<float*>(base);
+  P.recv = reinterpret_cast<float*>(base + al256((size_t)2 * B * b->d * 4));
+  P.hfin = reinterpret_cast<float*>(base + al256((size_t)2 * B * b->d * 4) +
+                                    al256((size_t)sp->world * 2 * B * b->d * 4));
+  void* x1 = at<char>(ws, L.x1);
+  if ((st = run_mlgru(b->mix, x, x1, true, dt, B, T_local, b->d, h, ws, L, s, PfPlan(), &P)) !=
+      TERN_OK)
+    return st;
+  if (T_local == 0) return TERN_OK;
+  return run_glu(b->ch, x1, y, true, dt, B * T_local, b->d, b->l, ws, L, s);
 }
 
 tern_status block_prefill(const tern_block* b, const void* x, void* y, tern_dtype dt, int32_t B,

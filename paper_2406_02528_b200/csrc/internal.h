@@ -137,6 +137,12 @@ cudaError_t launch_fcgscan(const int8_t* q, int ldq, const float* deq, const int
                            int gate, float* h, void* oprime, cudaStream_t s);
 // a6
 bool fcgscan_preferred(int B, int d);
+// sequence-parallel scan (C23): slice aggregates, boundary-state composition
+cudaError_t launch_scan_agg(const void* fcg, int dt, int B, int T, int d, float* agg,
+                            cudaStream_t s);
+cudaError_t launch_sp_compose(const float* recv, int world, int rank, int64_t n, float* h,
+                              float* hfin, cudaStream_t s);
+cudaError_t launch_fill_f32(float* p, size_t n, float v, cudaStream_t s);
 // k_fxp.cu: fixed-point W8A16 numerics (f4(ii))
 cudaError_t launch_fxp_scales(const float* w, int n, int shift, int8_t* wq, int32_t* e,
                               int32_t* status, cudaStream_t s);

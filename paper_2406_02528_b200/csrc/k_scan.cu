@@ -62,11 +62,15 @@ struct ScanSmem {
   uint64_t full[kS], gated[kS], scanned[kS], empty[kS];
 };
 
-template <typename T, int kS, int kC>
+// AGG (sequence-parallel pass 1, reading C23): no outputs; the carry runs the recurrence
+// from h = 0 and the running product of f, and writes the slice aggregate (A, B) to
+// agg [2][B][d].
+template <typename T, int kS, int kC, bool AGG = false>
 __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ CUtensorMap tmX, int B,
                                                        int T_, int d, int gate,
                                                        float* __restrict__ h, T* __restrict__ oprime,
-                                                       unsigned long long* prof) {
+                                                       unsigned long long* prof,
+                                                       float* __restrict__ agg) {
   // prof (debug, TERN_SCAN_PROF): per CTA [8] cycles: producer empty-wait, carry
   // gated-wait, carry total, gate0 full-wait, phase 1, scanned-wait, phase 3, gate0 total
   constexpr int kTS = kTE / kC;
@@ -116,7 +120,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
   } else if (warp == 1) {
     // ---------------- the carry (exact definition order: (f*h) + ((1-f)*c))
     if (lane < kC) {
-      float hc = h[(int64_t)b * d + c0 + lane];
+      float hc = AGG ? 0.0f : h[(int64_t)b * d + c0 + lane];
+      float Ac = 1.0f;   // AGG: running product of f, left to right
       const long long c_t0 = clock64();
       long long c_w = 0;
       for (int i = 0; i < nt; ++i) {
@@ -143,7 +148,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
             o.y = __fadd_rn(__fmul_rn(p.z, o.x), p.w);
             o.z = __fadd_rn(__fmul_rn(q.x, o.y), q.y);
             o.w = __fadd_rn(__fmul_rn(q.z, o.z), q.w);
-            hs4[g * kC] = o;
+            if (AGG) {
+              Ac = __fmul_rn(__fmul_rn(__fmul_rn(__fmul_rn(Ac, p.x), p.z), q.x), q.z);
+            } else {
+              hs4[g * kC] = o;
+            }
             hc = o.w;
           }
         } else {
@@ -151,13 +160,19 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
             const int e = t * kC + lane;
             const float* fbw = &sm.fb[s][fb_word<kC>(e)];
             hc = __fadd_rn(__fmul_rn(fbw[0], hc), fbw[1]);
-            sm.hs[s][h_word<kC>(e)] = hc;
+            if (AGG) Ac = __fmul_rn(Ac, fbw[0]);
+            else sm.hs[s][h_word<kC>(e)] = hc;
           }
         }
         __syncwarp(kC == 32 ? 0xffffffffu : (1u << (kC & 31)) - 1u);
         if (lane == 0) mbar_arrive(&sm.scanned[s]);
       }
-      h[(int64_t)b * d + c0 + lane] = hc;
+      if (AGG) {
+        agg[(int64_t)b * d + c0 + lane] = Ac;
+        agg[(int64_t)(B + b) * d + c0 + lane] = hc;
+      } else {
+        h[(int64_t)b * d + c0 + lane] = hc;
+      }
       if (prof && lane == 0) {
         prof[blockIdx.x * 8 + 1] = c_w;
         prof[blockIdx.x * 8 + 2] = clock64() - c_t0;
@@ -203,6 +218,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
       mbar_wait(&sm.scanned[s], (i / kS) & 1);
       long long w1 = clock64();
       acc[2] += w1 - w0;
+      if (AGG) {   // nothing to output: release the stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        return;
+      }
       float ov[kElemsPerLane];
 #pragma unroll
       for (int j = 0; j < kElemsPerLane; j += 2) {
@@ -244,13 +264,13 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
   }
 }
 
-template <typename TE, int kS, int kC>
+template <typename TE, int kS, int kC, bool AGG = false>
 static cudaError_t scan_go(const void* fcg, int B, int T, int d, int gate, float* h,
-                           void* oprime, cudaStream_t s) {
+                           void* oprime, cudaStream_t s, float* agg = nullptr) {
   static bool attr = false;
   const size_t smem = sizeof(ScanSmem<TE, kS>);
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan<TE, kS, kC>,
+    cudaError_t e = cudaFuncSetAttribute(k_scan<TE, kS, kC, AGG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -268,8 +288,9 @@ static cudaError_t scan_go(const void* fcg, int B, int T, int d, int gate, float
     if (!dprof) cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * 4096);
     cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * 8 * 4096, s);
   }
-  cudaError_t e = launch_pdl(k_scan<TE, kS, kC>, dim3(grid), dim3(kScanThreads), smem, s, tm, B,
-                             T, d, gate, h, static_cast<TE*>(oprime), prof_on ? dprof : nullptr);
+  cudaError_t e = launch_pdl(k_scan<TE, kS, kC, AGG>, dim3(grid), dim3(kScanThreads), smem, s, tm,
+                             B, T, d, gate, h, static_cast<TE*>(oprime), prof_on ? dprof : nullptr,
+                             agg);
   if (e != cudaSuccess || !prof_on || grid > 4096) return e;
   static unsigned long long hp[8 * 4096];
   cudaMemcpyAsync(hp, dprof, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost, s);
@@ -331,6 +352,61 @@ cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, 
   if (B == 0 || T == 0) return cudaSuccess;
   return dt == TERN_BF16 ? scan_pick<__nv_bfloat16>(fcg, B, T, d, gate, h, oprime, s)
                          : scan_pick<float>(fcg, B, T, d, gate, h, oprime, s);
+}
+
+// Sequence-parallel pass 1 (C23): the slice aggregates (A, B) of every (sequence, channel)
+cudaError_t launch_scan_agg(const void* fcg, int dt, int B, int T, int d, float* agg,
+                            cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  if (T == 0) {   // empty slice: the identity (A, B) = (1, 0)
+    cudaError_t e = cudaMemsetAsync(agg + (size_t)B * d, 0, sizeof(float) * B * d, s);
+    if (e != cudaSuccess) return e;
+    return launch_fill_f32(agg, (size_t)B * d, 1.0f, s);
+  }
+  const bool deep = (int64_t)B * (d / 8) < scan_num_sms();
+  if (dt == TERN_BF16)
+    return deep ? scan_go<__nv_bfloat16, kSDeep, 8, true>(fcg, B, T, d, 0, nullptr, nullptr, s, agg)
+                : scan_go<__nv_bfloat16, kSShallow, 8, true>(fcg, B, T, d, 0, nullptr, nullptr, s,
+                                                             agg);
+  return deep ? scan_go<float, kSDeep, 8, true>(fcg, B, T, d, 0, nullptr, nullptr, s, agg)
+              : scan_go<float, kSShallow, 8, true>(fcg, B, T, d, 0, nullptr, nullptr, s, agg);
+}
+
+// Sequence-parallel composition (C23): recv [world][2][B][d] holds every rank's slice
+// aggregate in rank order; h (in: the state before the sequence) becomes this rank's
+// boundary state h_in(rank), hfin the state after the whole sequence h_in(world).
+__global__ void k_sp_compose(const float* __restrict__ recv, int world, int rank, int64_t n,
+                             float* __restrict__ h, float* __restrict__ hfin) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float hin = h[i], mine = hin;
+    for (int j = 0; j < world; ++j) {
+      if (j == rank) mine = hin;
+      const float A = recv[(int64_t)j * 2 * n + i], Bv = recv[(int64_t)j * 2 * n + n + i];
+      hin = __fadd_rn(__fmul_rn(A, hin), Bv);
+    }
+    h[i] = mine;
+    hfin[i] = hin;
+  }
+}
+
+cudaError_t launch_sp_compose(const float* recv, int world, int rank, int64_t n, float* h,
+                              float* hfin, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int grid = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
+  k_sp_compose<<<grid, 256, 0, s>>>(recv, world, rank, n, h, hfin);
+  return cudaGetLastError();
+}
+
+__global__ void k_fill_f32(float* p, size_t n, float v) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+cudaError_t launch_fill_f32(float* p, size_t n, float v, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_fill_f32<<<(unsigned)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184), 256, 0, s>>>(p, n, v);
+  return cudaGetLastError();
 }
 
 }  // namespace tern

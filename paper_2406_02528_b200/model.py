@@ -198,6 +198,29 @@ class Stack:
             cur = nxt
         return cur
 
+    def prefill_sp(self, x: torch.Tensor, states: list, gather, rank: int,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
+        """Sequence-parallel prefill (tern.h block_prefill_sp, reading C23): x is
+        this rank's token slice [B][T_local][d] (shard.seq_slice); states start as the state
+        of the whole sequence's start on every rank and end as the state after the whole
+        sequence (identical on all ranks).  One all-gather of 2 B d floats per block."""
+        B, T, d = x.shape
+        world = gather.world
+        dt = L.dtype_code(self.dtype)
+        need = max(int(L.load().tern_block_prefill_sp_workspace(C.byref(b.struct), B, T, dt,
+                                                                  world))
+                   for b in self.blocks)
+        ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+        bufs = (torch.empty_like(x), torch.empty_like(x))
+        gather.register(ws, x, *bufs, *([out] if out is not None else []))
+        sp = L.tern_seqpar(rank, world, gather.cb, C.c_void_p(rank))
+        cur = x
+        for i, blk in enumerate(self.blocks):
+            nxt = bufs[i % 2] if (i < len(self.blocks) - 1 or out is None) else out
+            L.block_prefill_sp(blk.struct, cur, nxt, states[i], sp, ws, B, T, self.dtype)
+            cur = nxt
+        return cur
+
     def _stack_struct(self):
         if getattr(self, "_blk_arr", None) is None:
             self._blk_arr = (L.tern_block * len(self.blocks))(*[b.struct for b in self.blocks])

@@ -38,6 +38,14 @@ def plan(d: int, l: int, world: int, rank: int) -> dict:
             "gl": (rank * ls, (rank + 1) * ls)}
 
 
+def seq_slice(T: int, world: int, rank: int) -> tuple[int, int]:
+    """Token range [t0, t1) of `rank` in the sequence-parallel prefill (reading C23:
+    contiguous slices [r T / world, (r+1) T / world)); pure host logic."""
+    if world < 1 or not 0 <= rank < world or T < 0:
+        raise ValueError(f"rank {rank} of world {world}, T={T}")
+    return rank * T // world, (rank + 1) * T // world
+
+
 def shard_latents(latent: dict, d: int, l: int, world: int, rank: int,
                   megatron: bool = False) -> dict:
     """Slices of one block's latent matrices for `rank` (see plan()): output rows
