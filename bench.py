@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c0", "c2", "c3", "c4"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--decode-steps", type=int, default=None)
+    ap.add_argument("--no-flatness", action="store_true",
+                    help="skip the decode flatness sweep (n = 500..4000 steps)")
     ap.add_argument("--decode-batch", type=int, default=None,
                     help="decode batch per GPU (default: the config's, e.g. c4 also runs 128)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -472,6 +474,36 @@ def run_ours(args, cfg, rank, world, local_rank):
                     if persistent else
                     "4 launches per block (decode GEMV for B<=4: norm+quant prologue, "
                     "MLGRU/SwiGLU/residual epilogues; quant + split-K tcgen05 GEMM above)")}
+    # flatness of decode throughput in the number of generated tokens (Table 2 P:237-244,
+    # constant time and memory per token): n in {500, 1000, 2000, 4000} steps from
+    # h = 0 at the config's decode batch, one graph replay per step
+    flat = None
+    if rank == 0 and world == 1 and not args.no_flatness:
+        st.persistent_decode = False
+        fstates = st.new_state(Bd)
+        gf, xin_f, _ = st.capture_decode(Bd, fstates)
+        nmax = 4000
+        xf = synth.hidden((64, Bd, d), synth.generator(cfg.seed + 47, dev), cfg.dtype, device=dev)
+        per_n = {}
+        for n_ in (500, 1000, 2000, nmax):
+            for h in fstates:
+                h.zero_()
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record()
+            for t_ in range(n_):
+                xin_f.copy_(xf[t_ % 64])
+                gf.replay()
+            f1.record()
+            torch.cuda.synchronize()
+            per_n[str(n_)] = round(n_ * Bd / (f0.elapsed_time(f1) / 1e3), 1)
+        del gf
+        vals = list(per_n.values())
+        flat = {"tokens_per_s": per_n, "batch": Bd, "max_over_min": round(max(vals) / min(vals), 4),
+                "within_10pct": max(vals) / min(vals) <= 1.10,
+                "note": "steps from h = 0; inputs cycle through 64 pre-drawn tokens; the state is "
+                        "[B][d] per block whatever n is (S:593)"}
+        dec["flatness"] = flat
     pms, ppath = time_decode(True)
     if ppath == "persistent":   # the one-launch alternative (stack_decode), for comparison
         dec["persistent_kernel"] = {"tokens_per_s": round(nd * Bd * world / (pms / 1e3), 1),
