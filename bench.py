@@ -113,6 +113,8 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ algorithmic work
+ZERO_FRAC = 0.310   # ternary zeros of the synthetic N(0, 0.02) weights
+
 def algo_work(rec: dict, elem: int) -> tuple[str, float]:
     """(unit, amount) of algorithmic work of one launch."""
     k, m, n = rec["k"], rec["m"], rec["n"]
@@ -145,7 +147,11 @@ def roofline(records, elem, pk, traffic_db):
             peak = pk["int8"]["int8_tops_sustained"] if "int8" in pk else \
                 2.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
             kernels[name] = {"bound": "tensor", "achieved": round(ach, 1), "peak": round(peak, 1),
-                             "unit": "TFLOP/s", "frac": round(ach / peak, 4)}
+                             "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                             # the adds the method needs, nnz * M with the zero
+                             # fraction of N(0, s) weights at the 1/2 mean|W| threshold:
+                             # P(|z| < sqrt(2/pi)/2) = 0.310 (31.0 % measured)
+                             "ternary_adds_T_per_s": round(ach / 2.0 * (1.0 - ZERO_FRAC), 1)}
         else:
             ach = e["work"] / s / 1e9
             peak = pk["hbm_gbs"]
