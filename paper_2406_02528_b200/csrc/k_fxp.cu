@@ -614,9 +614,6 @@ cudaError_t launch_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_
   return cudaGetLastError();
 }
 
-}  // namespace tern
-
-namespace tern {
 cudaError_t launch_fxp_split(const int16_t* a, int m, int k, int ldq, int8_t* hi, int8_t* lo,
                              int32_t* qs_hi, int32_t* qs_lo, int8_t* ones, int32_t* qs_ones,
                              cudaStream_t s) {
@@ -635,4 +632,5 @@ cudaError_t launch_fxp_combine(const int32_t* acc_hi, const int32_t* acc_lo, int
                                             ldy, ey);
   return cudaGetLastError();
 }
+
 }  // namespace tern
