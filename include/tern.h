@@ -454,7 +454,8 @@ tern_status tern_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_t*
  *   (yn, en) = tern_fxp_rmsnorm(xq)            (per-row exponents en)
  *   acc[r][n] = sum_k t[n][k] yn[r][k]          (exact; on the int8 tensor
  *     cores as 256 (W hi) + (W lo') + 128 sum_k t[n][k], hi = yn >> 8,
- *     lo' = (yn & 255) - 128, both s8)
+ *     lo' = (yn & 255) - 128, both s8: one GEMM over 2m + 1 operand rows,
+ *     the last a row of ones)
  *   (bq, eb) = F1(w->scales[0], shift 6);  y = round(acc bq / 2^s) int16
  *   with the smallest fitting s per row, ey[r] = s + en[r] + eb.
  * w: n_seg == 1, w->k == k <= 65535.  y [m][ldy] int16, ldy >= n_out; ey [m].

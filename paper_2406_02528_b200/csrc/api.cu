@@ -556,27 +556,23 @@ tern_status tern_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_t*
   return TERN_OK;
 }
 
-// W8A16 BitLinear (F6) workspace: the normalised rows, their exponents, two s8 digit planes
-// with q-sums, a ones row, the rows' ternary sums and two int32 accumulator planes
+// W8A16 BitLinear (F6) workspace: the normalised rows and their exponents, then ONE int8
+// operand of 2m + 1 rows for the tcgen05 GEMM -- the m high-digit rows, the m low-digit
+// rows and a row of ones (its product is sum_k t[n][k]) -- with their q-sums, and the
+// int32 accumulators of all 2m + 1 rows: one GEMM launch for the whole contraction
 struct FxpBlWs {
-  size_t yn, en, hi, lo, qh, ql, ones, qo, rsum, ah, al, total;
+  size_t yn, en, a, qs, acc, total;
 };
 static FxpBlWs fxp_bl_ws(int m, int k, int n_rows) {
   auto up = [](size_t b) { return (b + 255) / 256 * 256; };
-  const size_t ldq = (size_t)kpad(k);
+  const size_t ldq = (size_t)kpad(k), rows = 2 * (size_t)m + 1;
   FxpBlWs L;
   size_t o = 0;
   L.yn = o; o += up((size_t)m * k * 2 + 16);
   L.en = o; o += up((size_t)m * 4 + 4);
-  L.hi = o; o += up((size_t)m * ldq + 16);
-  L.lo = o; o += up((size_t)m * ldq + 16);
-  L.qh = o; o += up((size_t)m * 4 + 4);
-  L.ql = o; o += up((size_t)m * 4 + 4);
-  L.ones = o; o += up(ldq);
-  L.qo = o; o += up(4);
-  L.rsum = o; o += up((size_t)n_rows * 4);
-  L.ah = o; o += up((size_t)m * n_rows * 4 + 4);
-  L.al = o; o += up((size_t)m * n_rows * 4 + 4);
+  L.a = o; o += up(rows * ldq + 16);
+  L.qs = o; o += up(rows * 4);
+  L.acc = o; o += up(rows * n_rows * 4);
   L.total = o;
   return L;
 }
@@ -606,32 +602,24 @@ tern_status tern_fxp_bitlinear(const int16_t* xq, const int32_t* ex, int32_t m, 
   char* b = static_cast<char*>(ws);
   int16_t* yn = reinterpret_cast<int16_t*>(b + L.yn);
   int32_t* en = reinterpret_cast<int32_t*>(b + L.en);
-  int8_t* hi = reinterpret_cast<int8_t*>(b + L.hi);
-  int8_t* lo = reinterpret_cast<int8_t*>(b + L.lo);
-  int32_t* qh = reinterpret_cast<int32_t*>(b + L.qh);
-  int32_t* ql = reinterpret_cast<int32_t*>(b + L.ql);
-  int8_t* ones = reinterpret_cast<int8_t*>(b + L.ones);
-  int32_t* qo = reinterpret_cast<int32_t*>(b + L.qo);
-  int32_t* rsum = reinterpret_cast<int32_t*>(b + L.rsum);
-  int32_t* ah = reinterpret_cast<int32_t*>(b + L.ah);
-  int32_t* al = reinterpret_cast<int32_t*>(b + L.al);
+  int8_t* a = reinterpret_cast<int8_t*>(b + L.a);
+  int32_t* qs = reinterpret_cast<int32_t*>(b + L.qs);
+  int32_t* acc = reinterpret_cast<int32_t*>(b + L.acc);
   const int ldq = kpad(k);
+  const size_t nr = (size_t)w->n_rows;
   TRY_CUDA(launch_fxp_rmsnorm(xq, ex, gq, eg, eps, m, k, yn, en, s), "fxp_bitlinear norm");
-  TRY_CUDA(launch_fxp_split(yn, m, k, ldq, hi, lo, qh, ql, ones, qo, s), "fxp_bitlinear split");
-  // three exact int8 x ternary contractions on the tcgen05 GEMM (EPI_NONE: int32 out)
-  const int8_t* qs[3] = {hi, lo, ones};
-  const int32_t* sums[3] = {qh, ql, qo};
-  int32_t* outs[3] = {ah, al, rsum};
-  const int rows[3] = {m, m, 1};
-  for (int i = 0; i < 3; ++i) {
-    Epi e = make_epi(EPI_NONE, *w, nullptr, nullptr, 0);
-    e.acc = outs[i];
-    e.ldacc = w->n_rows;
-    TRY_CUDA(launch_gemm(qs[i], rows[i], ldq, reinterpret_cast<const float*>(sums[i]), sums[i], *w,
-                         TERN_F32, e, s),
-             "fxp_bitlinear gemm");
-  }
-  TRY_CUDA(launch_fxp_combine(ah, al, w->n_rows, rsum, w->scales, w->n_out, m, en, y, ldy, ey, s),
+  TRY_CUDA(launch_fxp_split(yn, m, k, ldq, a, a + (size_t)m * ldq, qs, qs + m,
+                            a + (size_t)2 * m * ldq, qs + 2 * m, s),
+           "fxp_bitlinear split");
+  // the exact int8 x ternary contraction of all 2m + 1 rows (EPI_NONE: int32 out)
+  Epi e = make_epi(EPI_NONE, *w, nullptr, nullptr, 0);
+  e.acc = acc;
+  e.ldacc = w->n_rows;
+  TRY_CUDA(launch_gemm(a, 2 * m + 1, ldq, reinterpret_cast<const float*>(qs), qs, *w, TERN_F32, e,
+                       s),
+           "fxp_bitlinear gemm");
+  TRY_CUDA(launch_fxp_combine(acc, acc + (size_t)m * nr, w->n_rows, acc + (size_t)2 * m * nr,
+                              w->scales, w->n_out, m, en, y, ldy, ey, s),
            "fxp_bitlinear combine");
   return TERN_OK;
 }

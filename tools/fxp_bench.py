@@ -120,7 +120,7 @@ def bl():
 
 us = timed(bl, args.reps)
 tops = 2.0 * M * K * 1024 / (us * 1e-6) / 1e12
-rows.append({"kernel": "fxp_bitlinear (norm + split + 3 tcgen05 GEMMs + combine)", "us": round(us, 2),
+rows.append({"kernel": "fxp_bitlinear (norm + split + one tcgen05 GEMM over 2m+1 rows + combine)", "us": round(us, 2),
              "dense_equiv_TOPS_int16xternary": round(tops, 1),
              "int8_TOPS_issued": round(2 * tops, 1), "int8_peak_TOPS": i8,
              "int8_frac_issued": round(2 * tops / i8, 4),
