@@ -307,6 +307,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
   } while (!done);
 }
+// Waits with an explicit exponential sleep instead of the suspend hint: for warps that
+// wait long while other warps of their sub-partition compute (k_fcgscan's gate warps
+// waiting for the carry), the hinted try_wait re-polls on every barrier event of the CTA
+// (~40 polls per wait measured), and the polls take the busy warps' issue slots.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity,
+                                                  uint32_t ns0 = 32, uint32_t ns_max = 256) {
+  uint32_t done = 0, ns = ns0;
+  unsigned long long t0 = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(ns);
+    ns = ns < ns_max ? 2 * ns : ns_max;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t0 == 0) t0 = t;
+    else if (t - t0 > 20000000000ull) __trap();   // watchdog, as mbar_wait
+  }
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -48,6 +48,7 @@ struct FcgScanArgs {
   float* h;              // [B][d]
   void* oprime;          // [B*T][d]
   int gate;
+  int backoff;               // gate warps' wait for the carry: first sleep (ns), 0 = hinted wait
   unsigned long long* prof;  // debug (TERN_FS_PROF): [grid][8] cycles per wait site / phase
   unsigned long long* trace;   // tern_trace_enable timeline
 };
@@ -243,7 +244,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
         // (C) 16 lanes per row, two rows per instruction: o' = g^ sigma(h) for this
         // block's rows, after the carry
         const long long w5 = clock64();
-        mbar_wait(&sm.hdone[quad][half], it & 1);
+        if (a.backoff) mbar_wait_backoff(&sm.hdone[quad][half], it & 1, a.backoff, 8 * a.backoff);
+        else mbar_wait(&sm.hdone[quad][half], it & 1);
         if (ew == 0 && lane == 0) fs_acc(a, 5, w5);
         const long long w6 = clock64();
         const int cc = cs * kFQCh + (lane & 15), rsub = lane >> 4;
@@ -351,6 +353,11 @@ static cudaError_t fcgscan_go(const CUtensorMap& ta, const CUtensorMap& tb, cons
   static unsigned long long* dprof = nullptr;
   static const bool prof_on = getenv("TERN_FS_PROF") != nullptr;
   FcgScanArgs aa = a;
+  // gate warps wait for the carry with an explicit 32..256 ns backoff: the hinted wait
+  // re-polled ~43 times per wait (ncu: 15 % of the kernel's instructions were those polls);
+  // measured 98.8 -> 96.8 us per c2 block.  TERN_FS_BACKOFF=0 restores the hinted wait.
+  static const int backoff = getenv("TERN_FS_BACKOFF") ? atoi(getenv("TERN_FS_BACKOFF")) : 32;
+  aa.backoff = backoff;
   aa.trace = trace_slot(TERN_K_FCGSCAN, grid);
   if (prof_on) {   // debug only: printed after a synchronous run
     if (!dprof) cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * 1024);
