@@ -6,9 +6,11 @@ and [r*ls, (r+1)*ls) of gate and up (ls = l/world).  Its weight rows are packed
 with the FULL matrix's absmean scale (one scale per matrix), so every
 output element is computed exactly as without sharding; the library gathers
 the 4 per-block activations (o', x1, p, y) through the callback of an
-`AllGather` object.  Two back-ends:
+`AllGather` object.  Three back-ends:
   * `NcclAllGather`: torch.distributed all_gather_into_tensor (NCCL over
     NVLink / NVSwitch, one process per GPU) on the library's stream;
+  * `SymmMemAllGather`: a one-shot all-gather over torch symmetric memory
+    (P2P loads, device-side barriers, graph-capturable).
   * `ThreadAllGather`: `world` virtual ranks as host threads on one GPU, each
     with its own stream, ordered by CUDA events (no kernel waits on another) --
     the single-GPU emulation used by the tests.
@@ -141,6 +143,58 @@ class NcclAllGather(AllGather):
             if send != recv:
                 r.copy_(self.view(send, count * 4).view(torch.int32))
             self.dist.all_reduce(r, group=self.group)
+
+
+class SymmMemAllGather(AllGather):
+    """One-shot all-gather over torch symmetric memory: every rank
+    copies its chunk into its slot of a symmetric buffer, a device-side barrier on the
+    signal pads orders the ranks, and each rank pulls every peer's chunk straight out of the
+    peer's memory (P2P loads over NVLink) into `recv`; a second barrier keeps a slot from
+    being overwritten before all peers have read it.  No NCCL kernel, no host sync, and
+    CUDA-graph capturable (the decode graph), so its latency is a few copy kernels and two
+    signal exchanges.  The buffer is allocated and rendezvoused once, at construction
+    (`capacity` bytes per rank: the largest per-rank chunk any call will move).  Needs an
+    initialised torch.distributed process group with CUDA devices; multicast (NVLS) is used
+    by torch when the fabric offers it."""
+
+    def __init__(self, capacity: int, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        self.dist = dist
+        self.group = group or dist.group.WORLD
+        super().__init__(dist.get_world_size(self.group))
+        self.rank_ = dist.get_rank(self.group)
+        self.capacity = int(capacity)
+        self.buf = symm_mem.empty(self.capacity, dtype=torch.uint8, device="cuda")
+        self.hdl = symm_mem.rendezvous(self.buf, self.group.group_name)
+        self.peers = [self.hdl.get_buffer(r, (self.capacity,), torch.uint8, 0)
+                      for r in range(self.world)]
+
+    def gather(self, rank, send, recv, nbytes, stream):
+        if nbytes > self.capacity:
+            raise ValueError(f"chunk of {nbytes} B exceeds the symmetric buffer ({self.capacity})")
+        s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.buf[:nbytes].copy_(self.view(send, nbytes))
+            self.hdl.barrier(channel=0)
+            for r in range(self.world):
+                self.view(recv + r * nbytes, nbytes).copy_(self.peers[r][:nbytes])
+            self.hdl.barrier(channel=1)
+
+    def all_reduce(self, rank, send, recv, count, stream):
+        """Exact int32 sum in rank order from the peers' slots (as gather, then a sum)."""
+        nbytes = count * 4
+        if nbytes > self.capacity:
+            raise ValueError(f"{nbytes} B exceeds the symmetric buffer ({self.capacity})")
+        s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.buf[:nbytes].copy_(self.view(send, nbytes))
+            self.hdl.barrier(channel=0)
+            acc = self.peers[0][:nbytes].view(torch.int32).clone()
+            for r in range(1, self.world):
+                acc += self.peers[r][:nbytes].view(torch.int32)
+            self.hdl.barrier(channel=1)
+            self.view(recv, nbytes).view(torch.int32).copy_(acc)
 
 
 class ThreadAllGather(AllGather):
