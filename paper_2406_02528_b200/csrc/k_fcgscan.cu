@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "epilogue.cuh"
 
@@ -250,23 +251,36 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const long long w6 = clock64();
         const int cc = cs * kFQCh + (lane & 15), rsub = lane >> 4;
         TY* obase = static_cast<TY*>(a.oprime) + (int64_t)(b * a.T + t0) * a.d + c0 + cc;
+        // full tiles and the gate mode are resolved outside the loop (no per-element
+        // branch reconvergence)
+        auto phase_c = [&](auto full_c, auto sig_c) {
+          constexpr bool kFull = decltype(full_c)::value, kSig = decltype(sig_c)::value;
 #pragma unroll 2
-        for (int rr = 0; rr < 32; rr += 4) {
-          const int t = quad * 32 + rr + rsub;   // rows t and t + 2
-          const float h0 = sm.F[t][cc], h1 = sm.F[t + 2][cc];
-          const float g0 = sm.G[t][cc], g1 = sm.G[t + 2][cc];
-          float o0, o1;
-          if (a.gate == TERN_GATE_SIGMOID_H) {
-            float q0, q1;
-            sigmoid2(h0, h1, q0, q1);
-            o0 = __fmul_rn(g0, q0);
-            o1 = __fmul_rn(g1, q1);
-          } else {
-            o0 = __fmul_rn(g0, h0);
-            o1 = __fmul_rn(g1, h1);
+          for (int rr = 0; rr < 32; rr += 4) {
+            const int t = quad * 32 + rr + rsub;   // rows t and t + 2
+            const float h0 = sm.F[t][cc], h1 = sm.F[t + 2][cc];
+            const float g0 = sm.G[t][cc], g1 = sm.G[t + 2][cc];
+            float o0, o1;
+            if constexpr (kSig) {
+              float q0, q1;
+              sigmoid2(h0, h1, q0, q1);
+              o0 = __fmul_rn(g0, q0);
+              o1 = __fmul_rn(g1, q1);
+            } else {
+              o0 = __fmul_rn(g0, h0);
+              o1 = __fmul_rn(g1, h1);
+            }
+            if (kFull || t < steps) st_act<TY>(obase + (int64_t)t * a.d, o0);
+            if (kFull || t + 2 < steps) st_act<TY>(obase + (int64_t)(t + 2) * a.d, o1);
           }
-          if (t < steps) st_act<TY>(obase + (int64_t)t * a.d, o0);
-          if (t + 2 < steps) st_act<TY>(obase + (int64_t)(t + 2) * a.d, o1);
+        };
+        const bool sig = a.gate == TERN_GATE_SIGMOID_H;
+        if (steps == kFBM) {
+          if (sig) phase_c(std::true_type{}, std::true_type{});
+          else phase_c(std::true_type{}, std::false_type{});
+        } else {
+          if (sig) phase_c(std::false_type{}, std::true_type{});
+          else phase_c(std::false_type{}, std::false_type{});
         }
         if (ew == 0 && lane == 0) fs_acc(a, 6, w6);
         // this block's smem rows are rewritten only by this warp's next phase A,
