@@ -208,6 +208,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const int qs = rv ? __ldg(a.qsum + row) : 0;
         const float sf = __fmul_rn(deq, msf), sc = __fmul_rn(deq, msc), sg = __fmul_rn(deq, msg);
         const int cb = c0 + cs * kFQCh;
+        // fp32: the bias test is resolved outside the unrolled channel loop (c2 block
+        // 374 -> 367 us); bf16 keeps it inside (hoisting measured 2.4 % slower on c3 / c4)
+        auto phase_a = [&](auto mode_c) {
+          constexpr int kMode = decltype(mode_c)::value;   // 0 none, 1 bias, 2 run-time test
 #pragma unroll
         for (int j = 0; j < kFQCh; j += 2) {
           float fh0 = __fmul_rn(i2f_small((int)vf[j] - qs), sf);
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           float ch1 = __fmul_rn(i2f_small((int)vc[j + 1] - qs), sc);
           float gh0 = __fmul_rn(i2f_small((int)vg[j] - qs), sg);
           float gh1 = __fmul_rn(i2f_small((int)vg[j + 1] - qs), sg);
-          if (a.bias) {
+          if (kMode == 1 || (kMode == 2 && a.bias)) {
             fh0 = __fadd_rn(fh0, __ldg(a.bias + cb + j));
             fh1 = __fadd_rn(fh1, __ldg(a.bias + cb + j + 1));
             ch0 = __fadd_rn(ch0, __ldg(a.bias + a.d + cb + j));
@@ -239,6 +243,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
           sm.G[r][cc] = gh0;
           sm.G[r][cc + 1] = gh1;
         }
+        };
+        if constexpr (!std::is_same<TY, float>::value) phase_a(std::integral_constant<int, 2>{});
+        else if (a.bias) phase_a(std::integral_constant<int, 1>{});
+        else phase_a(std::integral_constant<int, 0>{});
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.ready[quad][half]);   // carry may run these rows
         if (ew == 0 && lane == 0) fs_acc(a, 4, w4);
