@@ -15,6 +15,7 @@
 // so the serial carry of tile i overlaps the gate work of the tiles around it,
 // and loads run kS tiles ahead.
 #include <cstdio>
+#include <type_traits>
 
 #include "epilogue.cuh"
 
@@ -223,28 +224,40 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const __grid_constant__ C
         if (lane == 0) mbar_arrive(&sm.empty[s]);
         return;
       }
-      float ov[kElemsPerLane];
+      // the gate mode and full tiles are resolved per tile, not per element
+      auto out_tile = [&](auto full_c, auto sig_c) {
+        constexpr bool kFull = decltype(full_c)::value, kSig = decltype(sig_c)::value;
+        float ov[kElemsPerLane];
 #pragma unroll
-      for (int j = 0; j < kElemsPerLane; j += 2) {
-        const int e = (gw * kElemsPerLane + j) * 32 + lane;
-        const float g0 = ld_act<T>(&sm.in[s][2][e]), g1 = ld_act<T>(&sm.in[s][2][e + 32]);
-        const float h0 = sm.hs[s][h_word<kC>(e)], h1 = sm.hs[s][h_word<kC>(e + 32)];
-        if (gate == TERN_GATE_SIGMOID_H) {
-          float s0, s1;
-          sigmoid2(h0, h1, s0, s1);
-          ov[j] = __fmul_rn(g0, s0);
-          ov[j + 1] = __fmul_rn(g1, s1);
-        } else {
-          ov[j] = __fmul_rn(g0, h0);
-          ov[j + 1] = __fmul_rn(g1, h1);
+        for (int j = 0; j < kElemsPerLane; j += 2) {
+          const int e = (gw * kElemsPerLane + j) * 32 + lane;
+          const float g0 = ld_act<T>(&sm.in[s][2][e]), g1 = ld_act<T>(&sm.in[s][2][e + 32]);
+          const float h0 = sm.hs[s][h_word<kC>(e)], h1 = sm.hs[s][h_word<kC>(e + 32)];
+          if constexpr (kSig) {
+            float s0, s1;
+            sigmoid2(h0, h1, s0, s1);
+            ov[j] = __fmul_rn(g0, s0);
+            ov[j + 1] = __fmul_rn(g1, s1);
+          } else {
+            ov[j] = __fmul_rn(g0, h0);
+            ov[j + 1] = __fmul_rn(g1, h1);
+          }
         }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[s]);   // stage free once read
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);   // stage free once read
 #pragma unroll
-      for (int j = 0; j < kElemsPerLane; ++j) {
-        const int t = i * kTS + ((gw * kElemsPerLane + j) * 32 + lane) / kC;
-        if (t < T_) st_act<T>(obase + (int64_t)t * d, ov[j]);
+        for (int j = 0; j < kElemsPerLane; ++j) {
+          const int t = i * kTS + ((gw * kElemsPerLane + j) * 32 + lane) / kC;
+          if (kFull || t < T_) st_act<T>(obase + (int64_t)t * d, ov[j]);
+        }
+      };
+      const bool full = (i + 1) * kTS <= T_, sig = gate == TERN_GATE_SIGMOID_H;
+      if (full) {
+        if (sig) out_tile(std::true_type{}, std::true_type{});
+        else out_tile(std::true_type{}, std::false_type{});
+      } else {
+        if (sig) out_tile(std::false_type{}, std::true_type{});
+        else out_tile(std::false_type{}, std::false_type{});
       }
       acc[3] += clock64() - w1;
     };
