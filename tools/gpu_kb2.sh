@@ -1,3 +1,3 @@
-python tools/kernel_breakdown.py --config c2 --prefill --B 1 --T 2048 --blocks 2 2>&1 | grep -E "per block|scan"
-python tools/kernel_breakdown.py --config c2 --prefill --B 4 --T 2048 --blocks 2 2>&1 | grep -E "per block|scan"
-python -m pytest tests -q -x -m gpu -k "scan or prefill or seqpar or centered or block" 2>&1 | tail -1
+python -m pytest tests -q -m gpu 2>&1 | tail -2
+python tools/kernel_breakdown.py --config c3 --prefill --B 16 --T 2048 --blocks 2 2>&1 | grep -E "per block|fcgscan|swiglu"
+python tools/kernel_breakdown.py --config c4 --prefill --B 32 --T 4096 --blocks 1 2>&1 | grep -E "per block|fcgscan|swiglu"
