@@ -28,7 +28,8 @@
  *
  * Parity status per function: all functions are pinned by tests in
  * tests/test_oracle_pins.py (the fixed-point orc_fxp_* section by
- * tests/test_fxp_oracle.py) except the composed end-to-end block values,
+ * tests/test_fxp_oracle.py; the bf16 rounding points R1-R3 by its test_bf16_*
+ * pins against torch's RNE) except the composed end-to-end block values,
  * which the paper never prints ("parity unpinned" for orc_block values;
  * they are pinned only through their pinned parts and invariants).
  */
@@ -729,9 +730,13 @@ int orc_fxp_inv_sqrt_arr(const uint64_t* v, const int32_t* e, int64_t n, uint32_
  * with x_i = xq_i 2^ex (int16, F2) and w_i = wq_i 2^ew (int8, F1).  Since
  *   1/sqrt(eps + S 2^(2ex)/d) = sqrt(d) 2^(-ex) / sqrt(S + eps_q),
  * S = sum xq_j^2 (int64, exact) and eps_q = round(d eps 2^(-2ex)) (binary64,
- * half away; 0 when eps underflows -- the paper's reason for eps = 1e-3 --, and
- * clamped to 2^60 so that S + eps_q stays in 64 bits for tiny activations),
- * the row computes (yq, ey) = inv_sqrt(S + eps_q, 0) (F4),
+ * half away; 0 when eps underflows -- the paper's reason for eps = 1e-3),
+ * the row computes (yq, ey) = inv_sqrt(S + eps_q, 0) (F4).  For activations so
+ * small that round(d eps 2^(-2ex)) > 2^60 the sum is formed on a coarser even
+ * grid 2^(2k) instead, with the smallest k for which it fits (reading F5b):
+ *   D = rha(S / 2^(2k)) + round(d eps 2^(-2ex-2k)),  (yq, ey) = inv_sqrt(D, 2k),
+ * which is the same value to 2^-60 relative (F4 keeps 31 bits of it); k = 0 is
+ * the formula above.  Then
  * rsd = (yq * sd) >> 16 with sd = round(sqrt(d) 2^16) (binary64), then
  * t_i = xq_i * wq_i * rsd (int64, real value t_i 2^(ew + ey)), and stores
  * out_i = round(t_i / 2^s) (half away) with the smallest s >= 0 for which
@@ -740,15 +745,16 @@ int orc_fxp_inv_sqrt_arr(const uint64_t* v, const int32_t* e, int64_t n, uint32_
 int orc_fxp_rmsnorm(const int16_t* xq, int ex, const int8_t* wq, int ew, int rows, int d,
                     double eps, int16_t* out, int32_t* eo) {
   if (rows < 0 || d <= 0 || d > 65536 || !(eps >= 0.0)) return ORC_ERR_ARG;
-  const double eps_d = round(ldexp((double)d * eps, -2 * ex));
-  const int64_t eps_q = eps_d > 0x1p60 ? ((int64_t)1 << 60) : (int64_t)eps_d;   /* F5 clamp */
+  int k2 = 0;                                      /* the even grid 2^k2 of D (F5b) */
+  while (round(ldexp((double)d * eps, -2 * ex - k2)) > 0x1p60) k2 += 2;
+  const int64_t eps_q = (int64_t)round(ldexp((double)d * eps, -2 * ex - k2));
   const int64_t sd = (int64_t)llround(ldexp(sqrt((double)d), 16));
   for (int r = 0; r < rows; ++r) {
     const int16_t* x = xq + (int64_t)r * d;
     int16_t* o = out + (int64_t)r * d;
     int64_t S = 0;
     for (int j = 0; j < d; ++j) S += (int64_t)x[j] * x[j];
-    const uint64_t D = (uint64_t)S + (uint64_t)eps_q;
+    const uint64_t D = (uint64_t)rha_shift(S, k2) + (uint64_t)eps_q;
     if (D == 0) {
       for (int j = 0; j < d; ++j) o[j] = 0;
       eo[r] = 0;
@@ -756,7 +762,7 @@ int orc_fxp_rmsnorm(const int16_t* xq, int ex, const int8_t* wq, int ew, int row
     }
     uint32_t yq;
     int ey;
-    orc_fxp_inv_sqrt(D, 0, &yq, &ey);
+    orc_fxp_inv_sqrt(D, k2, &yq, &ey);
     const int64_t rsd = (int64_t)(((uint64_t)yq * (uint64_t)sd) >> 16);
     int64_t tmax = 0;
     for (int j = 0; j < d; ++j) {

@@ -295,10 +295,11 @@ __global__ void __launch_bounds__(kFxThreads) k_fxp_rmsnorm(const int16_t* __res
   if (threadIdx.x < 24) L[threadIdx.x] = Lp.g[threadIdx.x];
   __syncthreads();
   const int ex = *ex_dev;
-  // eps_q = round(d eps 2^(-2 ex)) in binary64 (F5): the same operations as the definition
-  // (clamped to 2^60 so S + eps_q stays in 64 bits for tiny activations)
-  const double eps_d = round(ldexp(__dmul_rn((double)d, eps), -2 * ex));
-  const int64_t eps_q = eps_d > 0x1p60 ? (1ll << 60) : (int64_t)eps_d;
+  // eps_q = round(d eps 2^(-2 ex - k2)) in binary64 (F5), on the even grid 2^k2 of the sum:
+  // k2 = 0 unless the activations are so small that eps_q would exceed 2^60 (reading F5b)
+  int k2 = 0;
+  while (round(ldexp(__dmul_rn((double)d, eps), -2 * ex - k2)) > 0x1p60) k2 += 2;
+  const int64_t eps_q = (int64_t)round(ldexp(__dmul_rn((double)d, eps), -2 * ex - k2));
   const bool vec = (d & 7) == 0;
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     const int16_t* x = xq + (int64_t)r * d;
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(kFxThreads) k_fxp_rmsnorm(const int16_t* __res
       }
     }
     S = fx_block_sum_i64(S, red);
-    const uint64_t D = (uint64_t)S + (uint64_t)eps_q;
+    const uint64_t D = (uint64_t)fx_rha_shift(S, k2) + (uint64_t)eps_q;
     int16_t* o = out + (int64_t)r * d;
     if (D == 0) {
       for (int i = threadIdx.x; i < d; i += kFxThreads) o[i] = 0;
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(kFxThreads) k_fxp_rmsnorm(const int16_t* __res
     }
     uint32_t yq;
     int ey;
-    fx_inv_sqrt(D, 0, L, yq, ey);
+    fx_inv_sqrt(D, k2, L, yq, ey);
     const int64_t rsd = (int64_t)(((uint64_t)yq * (uint64_t)sd) >> 16);
     int64_t tmax = 0;
     for (int i = threadIdx.x; i < d; i += kFxThreads) {
@@ -367,8 +368,9 @@ __global__ void __launch_bounds__(kFxWarpRows * 32) k_fxp_rmsnorm_warp(
     reinterpret_cast<int4*>(w_s)[i] = __ldg(reinterpret_cast<const int4*>(wq) + i);
   __syncthreads();
   const int ex = *ex_dev;
-  const double eps_d = round(ldexp(__dmul_rn((double)d, eps), -2 * ex));
-  const int64_t eps_q = eps_d > 0x1p60 ? (1ll << 60) : (int64_t)eps_d;
+  int k2 = 0;   // F5b (as k_fxp_rmsnorm)
+  while (round(ldexp(__dmul_rn((double)d, eps), -2 * ex - k2)) > 0x1p60) k2 += 2;
+  const int64_t eps_q = (int64_t)round(ldexp(__dmul_rn((double)d, eps), -2 * ex - k2));
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * kFxWarpRows + (threadIdx.x >> 5);
   for (int r = wid; r < rows; r += gridDim.x * kFxWarpRows) {
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(kFxWarpRows * 32) k_fxp_rmsnorm_warp(
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
-    const uint64_t D = (uint64_t)S + (uint64_t)eps_q;
+    const uint64_t D = (uint64_t)fx_rha_shift(S, k2) + (uint64_t)eps_q;
     int16_t* orow = out + (int64_t)r * d;
     if (D == 0) {
 #pragma unroll
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(kFxWarpRows * 32) k_fxp_rmsnorm_warp(
     }
     uint32_t yq;
     int ey;
-    fx_inv_sqrt(D, 0, L, yq, ey);
+    fx_inv_sqrt(D, k2, L, yq, ey);
     const int64_t rsd = (int64_t)(((uint64_t)yq * (uint64_t)sd) >> 16);
     // x * w per element (|.| < 2^22, int32), then the int64 product with rsd
     int32_t xw[NV][8];

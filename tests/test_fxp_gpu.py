@@ -141,6 +141,28 @@ def test_rmsnorm_eps_underflow(L, eps):
     assert not out[0].any()
 
 
+@pytest.mark.parametrize("scale,d", [(1e-9, 1024), (1e-12, 2560), (1e-12, 64)])
+def test_rmsnorm_tiny_activations(L, scale, d):
+    """Reading F5b: tiny activations put eps_q above 2^60, so both sides form the sum on the
+    coarser even grid; both warp-per-row (d <= 3072, multiple of 256) and CTA-per-row kernels."""
+    g = synth.generator(d + 5)
+    x = synth.hidden((6, d), g, "f32") * scale
+    w = 1.0 + 0.25 * torch.randn(d, generator=g)
+    xq = torch.empty((6, d), dtype=torch.int16, device="cuda")
+    ex = torch.empty(1, dtype=torch.int32, device="cuda")
+    L.tern_fxp_quant_act(x.cuda(), xq, ex)
+    wq, ew = L.tern_fxp_scales(w.cuda())
+    out = torch.empty((6, d), dtype=torch.int16, device="cuda")
+    eo = torch.empty(6, dtype=torch.int32, device="cuda")
+    L.tern_fxp_rmsnorm(xq, ex, wq, ew, out, eo)
+    xq_o, ex_o = O.fxp_quant_act(x.numpy())
+    wq_o, ew_o = O.fxp_scales(w.numpy())
+    assert round(d * 1e-3 * 2.0 ** (-2 * ex_o)) > 2.0 ** 60
+    out_o, eo_o = O.fxp_rmsnorm(xq_o, ex_o, wq_o, ew_o)
+    assert np.array_equal(eo.cpu().numpy(), eo_o)
+    assert np.array_equal(out.cpu().numpy(), out_o)
+
+
 @pytest.fixture(scope="module")
 def M():
     from paper_2406_02528_b200 import model

@@ -158,6 +158,29 @@ def test_rmsnorm_matches_eq1(d):
     assert np.abs(got - fl)[4:].max() <= 0.02 * np.abs(fl[4:]).max()
 
 
+@pytest.mark.parametrize("scale", [1e-3, 1e-6, 1e-9, 1e-12])
+def test_rmsnorm_tiny_activations_keep_eq1(scale):
+    """Reading F5b: when round(d eps 2^(-2 ex)) would exceed 2^60 (tiny activations) the sum
+    S + eps_q is formed on a coarser even grid 2^(2k) and handed to F4 with that exponent, so
+    the output is still Eq. 1 with eps = 1e-3 -- pinned here against the
+    float definition.  (A clamp of eps_q at 2^60 would make the norm too large by
+    sqrt(eps_q / 2^60): 2^25 at scale 1e-12.)"""
+    rng = np.random.default_rng(11)
+    d = 1024
+    x = (rng.standard_normal((4, d)) * scale).astype(np.float32)
+    w = (1.0 + 0.25 * rng.standard_normal(d)).astype(np.float32)
+    xq, ex = O.fxp_quant_act(x)
+    wq, ew = O.fxp_scales(w)
+    if scale < 1e-5:
+        assert round(d * 1e-3 * 2.0 ** (-2 * ex)) > 2.0 ** 60   # the coarse-grid regime
+    out, eo = O.fxp_rmsnorm(xq, ex, wq, ew)
+    got = out * 2.0 ** eo[:, None].astype(np.float64)
+    ref = _eq1(xq * 2.0 ** ex, wq * 2.0 ** ew, 1e-3)
+    tol = 0.5 * 2.0 ** eo[:, None].astype(np.float64) + 5e-7 * np.abs(ref).max(1, keepdims=True)
+    assert np.all(np.abs(got - ref) <= tol)
+    assert np.abs(out).max() > 16383          # the output still uses the int16 range
+
+
 def test_rmsnorm_one_hot_and_zero():
     d = 256
     x = np.zeros((3, d), np.int16)

@@ -536,3 +536,98 @@ def test_mlgru_scan_slices_mode():
     assert np.allclose(H4, H1, rtol=1e-5, atol=1e-6)
     with O.scan_slices(1):
         assert np.array_equal(O.mlgru_scan(fh, ch, gh, H)[0], o1)
+
+
+# ------------------------------------------------------------------ bf16 rounding points (C13)
+# Reading C13: in bf16 mode values are rounded to bf16 (RNE) at R0 (block inputs /
+# outputs), R1 (every BitLinear output), R2 (o' and p before their quantizer) and R3 (the
+# residual stream), and NOWHERE else: h and every scale stay fp32.  These pins check the bf16
+# mode of each oracle function against its fp32 mode plus a bf16 rounding done by torch (an
+# independent implementation of RNE to bf16), so a missing, misplaced or extra rounding fails.
+def _bf(x):
+    torch = pytest.importorskip("torch")
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(torch.bfloat16).float().numpy()
+
+
+def _is_bf16(x):
+    return np.array_equal(_bf(x), x)
+
+
+def test_bf16_R1_bitlinear_output_only():
+    # R1: the BitLinear output is rounded; its norm, quantizer and accumulator are not touched
+    d, n = 48, 40
+    r = np.random.default_rng(21)
+    t, m = O.ternarize((r.standard_normal((n, d)) * 0.02).astype(np.float32))
+    X = _bf(r.standard_normal((7, d)))                          # R0: bf16 input
+    bias = r.standard_normal(n).astype(np.float32) * 0.1
+    y32, tp32 = O.bitlinear(X, t, m, bias=bias, taps=True)
+    y16, tp16 = O.bitlinear(X, t, m, bias=bias, bf16=True, taps=True)
+    assert not _is_bf16(y32)                                    # the pin is not vacuous
+    assert np.array_equal(y16, _bf(y32))
+    for k in ("q", "acc", "deq"):
+        assert np.array_equal(tp16[k], tp32[k])
+
+
+def test_bf16_R2_scan_rounds_oprime_not_h():
+    # R2 on o' only; the state h is fp32 (C13), identical in both modes
+    B, T, d = 2, 33, 24
+    r = np.random.default_rng(22)
+    fh, ch, gh = (_bf(r.standard_normal((B, T, d)) * 2) for _ in range(3))
+    H0 = r.standard_normal((B, d)).astype(np.float32)
+    for gate in (0, 1):
+        o32, H32 = O.mlgru_scan(fh, ch, gh, H0, gate_mode=gate)
+        o16, H16 = O.mlgru_scan(fh, ch, gh, H0, gate_mode=gate, bf16=True)
+        assert np.array_equal(H16, H32)
+        assert not _is_bf16(H32)                                # h really is not rounded
+        assert np.array_equal(o16, _bf(o32)) and not _is_bf16(o32)
+
+
+def test_bf16_mlgru_rounding_points():
+    # f̂ĉĝ (R1) are the rounded fp32-mode BitLinear outputs; the scan sees the rounded values;
+    # o' (R2) and o (R1) are rounded; H is the fp32 recurrence of the rounded gates
+    d = 32
+    blk, _ = _blk(d, 48, 23)
+    r = np.random.default_rng(23)
+    X = _bf(r.standard_normal((2, 5, d)))
+    H0 = np.zeros((2, d), np.float32)
+    out, H, tp = O.mlgru(blk, X, H0, bf16=True, taps=True)
+    Xf = X.reshape(-1, d)
+    taps = {}
+    for name, key in (("f", "fhat"), ("c", "chat"), ("g", "ghat")):
+        taps[key] = _bf(O.bitlinear(Xf, blk.t[name], blk.m[name])).reshape(X.shape)
+        assert np.array_equal(tp[key], taps[key])
+    o32, Hs = O.mlgru_scan(taps["fhat"], taps["chat"], taps["ghat"], H0)
+    assert np.array_equal(H, Hs) and not _is_bf16(H)
+    assert np.array_equal(tp["oprime"], _bf(o32))
+    assert np.array_equal(out.reshape(-1, d),
+                          _bf(O.bitlinear(_bf(o32).reshape(-1, d), blk.t["o"], blk.m["o"])))
+
+
+def test_bf16_glu_rounding_points():
+    d, l = 24, 64
+    blk, _ = _blk(d, l, 24)
+    X = _bf(np.random.default_rng(24).standard_normal((5, d)))
+    out, tp = O.glu(blk, X, bf16=True, taps=True)
+    g = _bf(O.bitlinear(X, blk.t["gate"], blk.m["gate"]))      # R1
+    u = _bf(O.bitlinear(X, blk.t["up"], blk.m["up"]))          # R1
+    assert np.array_equal(tp["ghat"], g) and np.array_equal(tp["uhat"], u)
+    p32 = (g * O.sigmoid_c(g)) * u
+    assert not _is_bf16(p32)
+    assert np.array_equal(tp["p"], _bf(p32))                    # R2
+    assert np.array_equal(out, _bf(O.bitlinear(_bf(p32), blk.t["down"], blk.m["down"])))
+
+
+def test_bf16_R3_block_residuals():
+    # x1 = bf16(x + o), y = bf16(x1 + dn) (R3), o and dn themselves bf16 (R1); H unrounded
+    d, l = 32, 64
+    blk, _ = _blk(d, l, 25)
+    X = _bf(np.random.default_rng(25).standard_normal((2, 6, d)))
+    H0 = np.zeros((2, d), np.float32)
+    Y, H, x1 = O.block(blk, X, H0, bf16=True, taps=True)
+    o, Hm = O.mlgru(blk, X, H0, bf16=True)
+    assert np.array_equal(H, Hm)
+    assert not _is_bf16(X + o)
+    assert np.array_equal(x1, _bf(X + o))
+    dn = O.glu(blk, x1.reshape(-1, d), bf16=True)
+    assert np.array_equal(Y.reshape(-1, d), _bf(x1.reshape(-1, d) + dn))
+    assert _is_bf16(Y) and _is_bf16(x1)
