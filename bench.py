@@ -42,20 +42,58 @@ def parse():
                     help="decode batch per GPU (default: the config's, e.g. c4 also runs 128)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=None, help="oracle sample tokens")
+    ap.add_argument("--shard", default="dp", choices=list(SHARD_MODES),
+                    help="partition over the N ranks (DESIGN.md §10): dp = sequences split, "
+                         "weights replicated (weak scaling, no collective); out = BitLinear "
+                         "output features sharded + NCCL all-gathers; gather_q = out with int8 "
+                         "code gathers; megatron = column/row-parallel pairs + exact int32 "
+                         "all-reduce; seq = sequence-parallel prefill (token slices + one "
+                         "aggregate all-gather per block); all but dp: strong scaling")
     return ap.parse_args()
 
 
+SHARD_MODES = {
+    "dp": "dp{w} (sequences split, weights replicated)",
+    "out": "tp{w} output-feature sharding, activation all-gathers (NCCL)",
+    "gather_q": "tp{w} output-feature sharding, int8-code all-gathers (NCCL)",
+    "megatron": "tp{w} column|row-parallel pairs, exact int32 all-reduce (NCCL)",
+    "seq": "sp{w} sequence-parallel prefill (token slices, aggregate all-gather, NCCL)",
+}
+
+
 def peaks():
+    """Roofline denominators (B200_PROFILING.md): MEASURED_PEAKS.json, else the guide's
+    fallback.  The dense INT8 peak is the measured bf16 GEMM peak x 2 (the nominal
+    int8:bf16 ratio of B200, 4.5 / 2.25 PFLOP/s dense): burst for an unthrottled run,
+    sustained when the run's clocks show sw_power_cap (int8_peak_for)."""
     try:
         pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pk = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
               "_fallback": True}
-    try:   # dense INT8 peak measured on this pool by tools/int8_peak.py (cuBLASLt IMMA)
-        pk["int8"] = json.load(open(os.path.join(ROOT, "profiles", "int8_peak.json")))
+    try:   # side note only: cuBLASLt IMMA measured on this pool by tools/int8_peak.py
+        pk["int8_cublaslt"] = json.load(open(os.path.join(ROOT, "profiles", "int8_peak.json")))
     except Exception:
         pass
     return pk
+
+
+def int8_peak_for(pk: dict, clocks: dict | None) -> tuple[float, str]:
+    """(dense INT8 TOPS, label): 2 x MEASURED_PEAKS bf16 burst, or 2 x sustained when
+    the timed region ran under the power cap / well below max clocks."""
+    capped = False
+    if clocks:
+        sm, mx = clocks.get("sm_mhz"), clocks.get("sm_max_mhz")
+        capped = "sw_power_cap" in (clocks.get("reasons") or []) or \
+            (sm is not None and mx is not None and sm < 0.95 * mx)
+    src = "of fallback" if pk.get("_fallback") else "of measured"
+    if capped:
+        return 2.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"]), \
+            f"MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal int8:bf16), {src}; " \
+            "sustained because the timed region saw sw_power_cap / reduced clocks"
+    return 2.0 * pk["bf16_tflops"], \
+        f"MEASURED_PEAKS.json bf16_tflops x 2 (nominal int8:bf16), burst, {src}; " \
+        "clocks at max with no power cap during the timed region"
 
 
 # ------------------------------------------------------------------ clocks
@@ -130,7 +168,7 @@ def algo_work(rec: dict, elem: int) -> tuple[str, float]:
     return "byte", 0.0
 
 
-def roofline(records, elem, pk, traffic_db):
+def roofline(records, elem, pk, traffic_db, clocks=None):
     by = {}
     for r in records:
         u, w = algo_work(r, elem)
@@ -140,14 +178,17 @@ def roofline(records, elem, pk, traffic_db):
         e["launches"] += 1
     tot = sum(e["ms"] for e in by.values()) or 1.0
     kernels = {}
+    i8peak, i8src = int8_peak_for(pk, clocks)
     for name, e in by.items():
         s = e["ms"] / 1e3
         if e["unit"] == "flop":
             ach = e["work"] / s / 1e12
-            peak = pk["int8"]["int8_tops_sustained"] if "int8" in pk else \
-                2.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+            peak = i8peak
             kernels[name] = {"bound": "tensor", "achieved": round(ach, 1), "peak": round(peak, 1),
                              "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                             "frac_of_burst": round(ach / (2.0 * pk["bf16_tflops"]), 4),
+                             "frac_of_sustained": round(
+                                 ach / (2.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])), 4),
                              # the adds the method needs, nnz * M with the zero
                              # fraction of N(0, s) weights at the 1/2 mean|W| threshold:
                              # P(|z| < sqrt(2/pi)/2) = 0.310 (31.0 % measured)
@@ -186,11 +227,17 @@ def roofline(records, elem, pk, traffic_db):
         tr = tr.get("bytes_per_launch") if isinstance(tr, dict) else tr
         rl = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
               "unit": d["unit"], "frac": d["frac"], "traffic": tr,
-              "peak_source": (("profiles/int8_peak.json int8_tops_sustained (cuBLASLt s8 GEMM "
-                               "8192^3 measured on this pool, back to back)" if "int8" in pk else
-                               "MEASURED_PEAKS.json bf16_tflops_sustained x 2 (int8:bf16 nominal "
-                               "ratio)") if d["bound"] == "tensor" else "MEASURED_PEAKS.json hbm_gbs")
-              + (" [fallback]" if pk.get("_fallback") else "")}
+              "peak_source": i8src if d["bound"] == "tensor" else
+              "MEASURED_PEAKS.json hbm_gbs" + (" (of fallback)" if pk.get("_fallback")
+                                                 else " (of measured)")}
+        if d["bound"] == "tensor":
+            rl["frac_of_burst"] = d["frac_of_burst"]
+            rl["frac_of_sustained"] = d["frac_of_sustained"]
+            if "int8_cublaslt" in pk:   # side note: cuBLASLt s8 GEMM on this pool
+                rl["note_cublaslt_int8_tops"] = {
+                    k: pk["int8_cublaslt"].get(k) for k in ("int8_tops_burst", "int8_tops_sustained")}
+        if tr is None:
+            rl["traffic_note"] = "no ncu --set full capture of this config in profiles/traffic.json"
     return rl, kernels
 
 
@@ -269,7 +316,7 @@ def run_reference(args, cfg, rank, world):
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": config_dict(cfg, world),
+           "config": config_dict(cfg, world, args.shard),
            "cpu_baseline": {"value": round(val, 3), "unit": "tokens/s", "cores": O.get_threads(),
                             "kind": "oracle", "sample": sample, "cpu": cpu_model()},
            "e2e": {"value": round(val, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -287,16 +334,88 @@ def cpu_model():
     return None
 
 
-def config_dict(cfg, world):
+def config_dict(cfg, world, mode="dp"):
+    per = "per GPU" if mode == "dp" else f"global (the same batch on all {world} ranks)"
     return {"workload": f"{cfg.name}: {cfg.L}-block stack d={cfg.d} l={cfg.l} "
-                        f"{cfg.dtype} activations, prefill {cfg.prefill_B}x{cfg.prefill_T} per GPU",
-            "L": cfg.L, "d": cfg.d, "l": cfg.l, "batch_per_gpu": cfg.prefill_B,
+                        f"{cfg.dtype} activations, prefill {cfg.prefill_B}x{cfg.prefill_T} {per}",
+            "L": cfg.L, "d": cfg.d, "l": cfg.l,
+            ("batch_per_gpu" if mode == "dp" else "global_batch"): cfg.prefill_B,
             "seq_len": cfg.prefill_T, "activations": cfg.dtype,
-            "parallelism": f"dp{world} (sequences split, weights replicated)",
+            "parallelism": SHARD_MODES[mode].format(w=world),
             "l2": "flushed between timed steps (256 MiB write); activations > L2"}
 
 
 # ------------------------------------------------------------------ our arm
+def finish_sharded(args, cfg, rank, world, mode, st, value, ms_max, rl, kernels, recs, ck, e2e,
+                   pk):
+    """The JSON line of a sharded run (--shard out|gather_q|megatron|seq): prefill of one
+    global batch over the N ranks (strong scaling), plus -- for the output-feature modes --
+    the config's decode batch through the sharded stack (one CUDA-graph replay per step,
+    4 collectives per block issued by the library through the all-gather callback)."""
+    import torch
+
+    from paper_2406_02528_b200 import synth
+    dev = st.device
+    dec = None
+    if mode != "seq":
+        nd = args.decode_steps if args.decode_steps is not None else min(cfg.decode_steps, 200)
+        Bd = args.decode_batch or cfg.decode_B
+        xs = synth.hidden((nd, Bd, cfg.d), synth.generator(cfg.seed + 31, dev), cfg.dtype,
+                          device=dev)
+        dstates = st.new_state(Bd)
+        g, xin_d, _ = st.capture_decode(Bd, dstates)
+        for t_ in range(3):
+            xin_d.copy_(xs[t_])
+            g.replay()
+        for h in dstates:
+            h.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record()
+        for t_ in range(nd):
+            xin_d.copy_(xs[t_])
+            g.replay()
+        d1.record()
+        torch.cuda.synchronize()
+        dms = max_over_ranks(d0.elapsed_time(d1), world, dev)
+        wbytes = st.weight_bytes
+        dec = {"tokens_per_s": round(nd * Bd / (dms / 1e3), 1), "global_batch": Bd,
+               "steps": nd, "ms_per_token_step": round(dms / nd, 4),
+               "weight_bytes_per_step_per_gpu": wbytes,
+               "hbm_frac_of_weights_stream": round(wbytes / (dms / nd / 1e3) / 1e9 / pk["hbm_gbs"],
+                                                   4),
+               "path": "per_block, sharded", "graph": True,
+               "collectives_per_step": (2 if mode == "megatron" else 4) * cfg.L}
+        del g
+    out = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "shard": mode,
+           "data": "synthetic (seeded N(0,0.02) latent weights, N(0,1) hidden states; no "
+                   "embedding/LM head)",
+           "config": config_dict(cfg, world, mode), "roofline": rl, "kernels": kernels,
+           "gpu_launches": len(recs), "clocks": ck, "e2e": e2e, "decode": dec,
+           "comm": comm_info(world)}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def comm_info(world: int) -> dict:
+    import torch
+    info = {"world": world}
+    if world > 1:
+        import torch.distributed as dist
+        info["backend"] = dist.get_backend()
+        try:
+            v = torch.cuda.nccl.version()
+            info["nccl_version"] = ".".join(map(str, v)) if isinstance(v, tuple) else v
+        except Exception:
+            pass
+    return info
+
+
 def run_ours(args, cfg, rank, world, local_rank):
     import numpy as np
     import torch
@@ -311,8 +430,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     pk = peaks()
-    try:
+    try:   # ncu --set full dram bytes per launch, keyed by config (tools/ncu_traffic.py)
         traffic_db = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic_db = traffic_db.get(cfg.name + ("" if args.shard == "dp" or world == 1
+                                                else f":{args.shard}{world}"), {})
     except Exception:
         traffic_db = {}
 
@@ -321,12 +442,29 @@ def run_ours(args, cfg, rank, world, local_rank):
     nb_cpu, cpu_tokens = cpu_sample_plan(cfg, args)
     if do_cpu:
         keep = nb_cpu
-    st = model.Stack.random(cfg, device=dev, gen_device=dev, keep_latents=keep)
+    mode = args.shard
+    sharded = mode in ("out", "gather_q", "megatron")
+    gather = None
+    if sharded:
+        from paper_2406_02528_b200 import shard as S
+        gather = S.NcclAllGather()
+        shard_spec = (rank, gather, mode == "gather_q", mode == "megatron")
+    st = model.Stack.random(cfg, device=dev, gen_device=dev, keep_latents=keep,
+                            shard=shard_spec if sharded else None)
     dt = synth.torch_dtype(cfg.dtype)
     elem = 2 if cfg.dtype == "bf16" else 4
     B, T, d = cfg.prefill_B, cfg.prefill_T, cfg.d
-    gx = synth.generator(cfg.seed + 7919 * (rank + 1), dev)
-    x = synth.hidden((B, T, d), gx, cfg.dtype, device=dev)
+    if mode == "dp":   # every rank its own B sequences (weak scaling)
+        gx = synth.generator(cfg.seed + 7919 * (rank + 1), dev)
+        x = synth.hidden((B, T, d), gx, cfg.dtype, device=dev)
+    else:              # one global batch, the same on every rank (strong scaling)
+        gx = synth.generator(cfg.seed + 7919, dev)
+        x = synth.hidden((B, T, d), gx, cfg.dtype, device=dev)
+        if mode == "seq":   # this rank's contiguous token slice of every sequence (C23)
+            from paper_2406_02528_b200 import shard as S
+            t0, t1 = S.seq_slice(T, world, rank)
+            x = x[:, t0:t1].contiguous()
+            gather = S.NcclAllGather()
     y = torch.empty_like(x)
     bufs = (torch.empty_like(x), torch.empty_like(x))
     states = st.new_state(B)
@@ -337,7 +475,10 @@ def run_ours(args, cfg, rank, world, local_rank):
             dist.barrier()
 
     def step():
-        st.prefill(x, states, out=y, bufs=bufs)
+        if mode == "seq":
+            st.prefill_sp(x, states, gather, rank, out=y)
+        else:
+            st.prefill(x, states, out=y, bufs=bufs)
 
     def reset():
         for h in states:
@@ -376,14 +517,16 @@ def run_ours(args, cfg, rank, world, local_rank):
     recs = L.tern_profile_collect()
     ms = sum(a.elapsed_time(b) for a, b in ev)
     ms_max = max_over_ranks(ms, world, dev)
-    tokens = B * T * args.steps * world
+    tokens = B * T * args.steps * (world if mode == "dp" else 1)
     value = tokens / (ms_max / 1e3)
-    rl, kernels = roofline(recs, elem, pk, traffic_db)
+    rl, kernels = roofline(recs, elem, pk, traffic_db, ck)
 
     # ---------------- e2e: pinned host input -> device, prefill, device -> pinned host result,
     # every step (Stack.prefill_host: uploads / downloads on copy streams, double-buffered)
     xh = [x.cpu().pin_memory() for _ in range(args.steps)]
     yh = [torch.empty_like(xh[0]).pin_memory() for _ in range(args.steps)]
+    if mode == "seq":
+        st.prefill_host_fn = lambda xi, hs, yo: st.prefill_sp(xi, hs, gather, rank, out=yo)
     st.prefill_host(xh[:1], yh[:1])
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -404,6 +547,9 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     # ---------------- one long sequence (B = 1 x T): the workload of P:198 (batch 1, seq 2048,
     # "one MMF layer"); prefill picks GEMM + the 8-channel scan here
+    if mode != "dp":
+        return finish_sharded(args, cfg, rank, world, mode, st, value, ms_max, rl, kernels, recs,
+                              ck, e2e, pk)
     x1 = x[:1].contiguous()
     y1 = torch.empty_like(x1)
     s1 = st.new_state(1)
@@ -526,7 +672,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "embedding/LM head)",
            "config": config_dict(cfg, world), "roofline": rl, "kernels": kernels,
            "gpu_launches": len(recs), "clocks": ck, "e2e": e2e, "decode": dec,
-           "prefill_b1": prefill_b1}
+           "prefill_b1": prefill_b1, "comm": comm_info(world)}
 
     if do_cpu:
         try:
@@ -551,25 +697,58 @@ def run_ours(args, cfg, rank, world, local_rank):
         print(json.dumps(out), flush=True)
 
 
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a torchrun environment: re-run this command as N
+    ranks under torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(launch_ranks(args.gpus))
     from paper_2406_02528_b200 import synth
     cfg = synth.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
-    if world > 1:
+    if world > 1 or args.shard != "dp":
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if not dist.is_initialized():
+            if "MASTER_ADDR" not in os.environ:   # 1-rank group for --shard at N = 1
+                os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()),
+                                  RANK="0", WORLD_SIZE="1")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        t = torch.ones(1, device="cuda")   # force communicator creation before timing
+        dist.all_reduce(t)
+        torch.cuda.synchronize()
+        print(f"[bench] rank {dist.get_rank()}/{dist.get_world_size()}: NCCL communicator up on "
+              f"cuda:{local_rank} (all_reduce check = {int(t.item())})", file=sys.stderr,
+              flush=True)
     try:
         run_ours(args, cfg, rank, world, local_rank)
     finally:
-        if world > 1:
-            import torch.distributed as dist
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
             dist.destroy_process_group()
 
 

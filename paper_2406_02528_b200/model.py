@@ -207,11 +207,15 @@ class Stack:
         B, T, d = x.shape
         world = gather.world
         dt = L.dtype_code(self.dtype)
-        need = max(int(L.load().tern_block_prefill_sp_workspace(C.byref(b.struct), B, T, dt,
-                                                                  world))
-                   for b in self.blocks)
-        ws = torch.empty(need, dtype=torch.uint8, device=x.device)
-        bufs = (torch.empty_like(x), torch.empty_like(x))
+        key = (B, T, world)
+        if getattr(self, "_sp_key", None) != key:   # workspace + ping-pong buffers, kept
+            need = max(int(L.load().tern_block_prefill_sp_workspace(C.byref(b.struct), B, T, dt,
+                                                                      world))
+                       for b in self.blocks)
+            self._sp_ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+            self._sp_bufs = (torch.empty_like(x), torch.empty_like(x))
+            self._sp_key = key
+        ws, bufs = self._sp_ws, self._sp_bufs
         gather.register(ws, x, *bufs, *([out] if out is not None else []))
         sp = L.tern_seqpar(rank, world, gather.cb, C.c_void_p(rank))
         cur = x
@@ -263,7 +267,11 @@ class Stack:
                 h.zero_()
             if before_step is not None:
                 before_step(i)
-            self.prefill(xin[k], states, out=yout[k], bufs=bufs)
+            fn = getattr(self, "prefill_host_fn", None)   # e.g. the sequence-parallel prefill
+            if fn is not None:
+                fn(xin[k], states, yout[k])
+            else:
+                self.prefill(xin[k], states, out=yout[k], bufs=bufs)
             ev_free[k].record(main)
             ev_out[k].record(main)
             with torch.cuda.stream(down):

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
+import weakref
 
 import torch
 
@@ -78,19 +79,27 @@ class AllGather:
 
     def __init__(self, world: int):
         self.world = world
-        self._tensors = []
+        self._tensors = {}   # (data_ptr, nbytes) -> weakref to the tensor
+        self._lock = threading.Lock()
         self.cb = L.ALLGATHER_FN(self._call)
         self.cb_ar = L.ALLREDUCE_FN(self._call_ar)
         self.error = None
 
     def register(self, *tensors):
-        have = {(t.data_ptr(), t.numel() * t.element_size()) for t in self._tensors}
-        for t in tensors:
-            if (t.data_ptr(), t.numel() * t.element_size()) not in have:
-                self._tensors.append(t)
+        """Make the tensors' memory resolvable by view().  Only weak references are kept:
+        a tensor the caller drops leaves the registry (no memory is held alive by it)."""
+        with self._lock:
+            for k in [k for k, r in self._tensors.items() if r() is None]:
+                del self._tensors[k]
+            for t in tensors:
+                self._tensors[(t.data_ptr(), t.numel() * t.element_size())] = weakref.ref(t)
 
     def view(self, p: int, nbytes: int) -> torch.Tensor:
-        for t in self._tensors:
+        with self._lock:
+            live = [r() for r in self._tensors.values()]
+        for t in live:
+            if t is None:
+                continue
             base = t.data_ptr()
             size = t.numel() * t.element_size()
             if base <= p and p + nbytes <= base + size:

@@ -48,3 +48,55 @@ def test_split_sequences_covers_batch():
             f, n = bench.split_sequences(B, world, r)
             seen += list(range(f, f + n))
         assert seen == list(range(B))
+
+
+def _bench(args, env_extra=None, timeout=300):
+    import json
+    import subprocess
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env.update(env_extra or {})
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT,
+                       env=env, capture_output=True, text=True, timeout=timeout)
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    return r, lines
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` without torchrun re-launches itself as 2 ranks (ADVICE r1:
+    --gpus was ignored); the reference arm prints one line, from rank 0, with n_gpus 2."""
+    r, lines = _bench(["--impl", "reference", "--gpus", "2", "--config", "c0", "--steps", "1",
+                       "--warmup", "0", "--cpu-tokens", "2"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+    assert "launching 2 ranks" in r.stderr
+
+
+def test_bench_gpus_mismatch_fails():
+    r, lines = _bench(["--impl", "reference", "--gpus", "2", "--config", "c0"],
+                      {"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode != 0 and not lines and "WORLD_SIZE=1" in r.stderr
+
+
+def test_bench_shard_modes_parse():
+    sys.path.insert(0, ROOT)
+    import bench
+    assert set(bench.SHARD_MODES) == {"dp", "out", "gather_q", "megatron", "seq"}
+    assert bench.config_dict(type("C", (), dict(name="c3", L=24, d=2048, l=5632, dtype="bf16",
+                                                prefill_B=16, prefill_T=2048))(), 8,
+                             "out")["parallelism"].startswith("tp8")
+
+
+def test_int8_peak_from_measured_peaks():
+    """The INT8 roofline peak is reproducible from MEASURED_PEAKS.json: 2 x bf16 burst for an
+    unthrottled run, 2 x sustained under sw_power_cap."""
+    sys.path.insert(0, ROOT)
+    import json
+    import bench
+    mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    pk = bench.peaks()
+    p, src = bench.int8_peak_for(pk, {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0, "reasons": []})
+    assert p == 2 * mp["bf16_tflops"] and "burst" in src
+    p, src = bench.int8_peak_for(pk, {"sm_mhz": 1700.0, "sm_max_mhz": 1965.0,
+                                      "reasons": ["sw_power_cap"]})
+    assert p == 2 * mp["bf16_tflops_sustained"] and "sustained" in src

@@ -314,10 +314,10 @@ def test_stack_truncated_parity(L, M, cfg_name, n_blocks, T, n_dec):
     assert np.array_equal(yg, yo)
 
 
-def test_sampled_full_size_bitlinear_c1(L, M):
-    """configs[1] at a full-size point (M=4096, K=2048, N=5632, bf16) checked on
-    sampled rows the oracle computes one by one."""
-    m, k, n = 4096, 2048, 5632
+@pytest.mark.parametrize("m,k,n", [(4096, 2048, 5632), (4096, 5632, 2048), (16384, 1024, 1024)])
+def test_sampled_full_size_bitlinear_c1(L, M, m, k, n):
+    """configs[1] at full-size points (bf16) checked on sampled rows the oracle computes one
+    by one: both GLU-shaped matrices at M = 4096 and the (1024,1024) one at M = 16384."""
     W = latents(n, k, 1)
     pw = M.PackedWeight([W.cuda()])
     t, mw = O.ternarize(W.numpy())
@@ -395,7 +395,7 @@ def test_batched_decode_split_k_parity(L, M, cfg_name, B, T, n_dec, fin):
 
 
 # ------------------------------------------------------------------------ full size, bench launch config
-@pytest.mark.parametrize("cfg_name,n_tok", [("c2", 24), ("c4", 8)])
+@pytest.mark.parametrize("cfg_name,n_tok", [("c2", 24), ("c3", 8), ("c4", 8)])
 def test_full_size_prefill_sampled_prefixes(L, M, cfg_name, n_tok):
     """The bench workload at full size and in bench.py's launch configuration (all blocks,
     B x T prefill, fused f|c|g+scan, tcgen05 GEMMs): the MLGRU is causal, so the first
@@ -450,3 +450,68 @@ def test_zero_rows_and_empty_calls(L, M):
     h0 = st.new_state(0)
     y0 = st.prefill(x0, h0)
     assert y0.shape == (0, 4, 128)
+
+
+@pytest.mark.parametrize("cfg_name,n_tok", [("c2", 300), ("c3", 260)])
+def test_full_size_fused_scan_crosses_time_tiles(L, M, cfg_name, n_tok):
+    """k_fcgscan at the bench's launch configuration (full B x T prefill, full width d, the
+    fused f|c|g GEMM + scan path, asserted from the launch records) through 2 blocks,
+    against the oracle on the first n_tok > 256 tokens of sampled sequences: the prefix
+    crosses two 128-token time tiles, so the carry hand-off between tiles (mbarriers, the
+    h carried in registers) is checked against the definition, not against CUDA."""
+    cfg = synth.CONFIGS[cfg_name]
+    st = M.Stack.random(cfg, device="cuda", gen_device="cuda", keep_latents=2, n_blocks=2)
+    B, T = cfg.prefill_B, cfg.prefill_T
+    x = synth.hidden((B, T, cfg.d), synth.generator(cfg.seed + 7919), cfg.dtype).cuda()
+    states = st.new_state(B)
+    L.tern_profile_enable(True)
+    try:
+        y = st.prefill(x, states)
+        torch.cuda.synchronize()
+    finally:
+        L.tern_profile_enable(False)
+    kernels = {r["kernel"] for r in L.tern_profile_collect()}
+    assert "fcgscan" in kernels, f"fused scan not launched: {kernels}"
+    ob = [O.OracleBlock({k: v.numpy() for k, v in lat.items()}, cfg.d, cfg.l) for lat in st.latents]
+    bf = cfg.dtype == "bf16"
+    for b in (0, B - 1):
+        xo = f32np(x[b:b + 1, :n_tok])
+        Hs = [np.zeros((1, cfg.d), np.float32) for _ in ob]
+        yo, Hs = O.stack(ob, xo, Hs, bf16=bf)
+        yg = f32np(y[b:b + 1, :n_tok])
+        close(yg, yo, 2e-2 if bf else 1e-4, f"{cfg_name} seq {b}")
+        assert np.array_equal(yg, yo), f"{cfg_name} sequence {b}"
+
+
+def test_c2_decode_through_all_blocks(L, M):
+    """8 decode steps of the c2 stack (all 24 blocks, B = 1, the GEMV path in the
+    bench's CUDA graph) after a short prefill, free-running against the oracle; the
+    per-block states after the last step too."""
+    cfg = synth.CONFIGS["c2"]
+    st = M.Stack.random(cfg, device="cuda", gen_device="cuda", keep_latents=cfg.L)
+    T, n_dec = 4, 8
+    x = synth.hidden((1, T + n_dec, cfg.d), synth.generator(cfg.seed + 31), cfg.dtype)
+    xd = x.cuda()
+    states = st.new_state(1)
+    st.prefill(xd[:, :T].contiguous(), states)
+    g, xin, yout = st.capture_decode(1, states)
+    ys = []
+    for t in range(T, T + n_dec):
+        xin.copy_(xd[:, t])
+        g.replay()
+        ys.append(yout.clone().unsqueeze(1))
+    torch.cuda.synchronize()
+    yg = f32np(torch.cat(ys, 1))
+    ob = [O.OracleBlock({k: v.numpy() for k, v in lat.items()}, cfg.d, cfg.l) for lat in st.latents]
+    Hs = [np.zeros((1, cfg.d), np.float32) for _ in ob]
+    xo = f32np(x)
+    _, Hs = O.stack(ob, xo[:, :T], Hs)
+    outs = []
+    for t in range(T, T + n_dec):
+        yt, Hs = O.stack(ob, xo[:, t:t + 1], Hs)
+        outs.append(yt)
+    yo = np.concatenate(outs, 1)
+    close(yg, yo, 1e-4, "c2 decode")
+    assert np.array_equal(yg, yo)
+    for i in range(cfg.L):
+        assert np.array_equal(states[i].cpu().numpy(), Hs[i]), f"block {i} state"

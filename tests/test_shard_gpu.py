@@ -3,14 +3,17 @@
 shard of every weight, exchanging o', x1, p and y through the library's
 all-gather callback (shard.ThreadAllGather: CUDA events + copies, no kernel
 waits on another).  Every rank's output must be bit-identical to the unsharded
-library path (and that one to the oracle, tests/test_parity_gpu.py): gathers
+library path, and that one must match the oracle's unsharded stack (O.stack,
+prefill then decode, north_star tolerances; in practice bit-exact): gathers
 move values unchanged, int32 sums are exact and every norm sees the full row.
 """
 import threading
 
+import numpy as np
 import pytest
 import torch
 
+import oracle as O
 from paper_2406_02528_b200 import synth
 
 pytestmark = pytest.mark.gpu
@@ -20,7 +23,8 @@ def _run(world, cfg, T, n_dec, B, gather_q=False, norm=0, megatron=False):
     from paper_2406_02528_b200 import _lib as L
     from paper_2406_02528_b200 import model, shard
     L.load()
-    ref = model.Stack.random(cfg, device="cuda", gen_device="cpu", norm=norm)
+    ref = model.Stack.random(cfg, device="cuda", gen_device="cpu", norm=norm,
+                             keep_latents=cfg.L)
     x = synth.hidden((B, T + n_dec, cfg.d), synth.generator(3), cfg.dtype).cuda()
     hs = ref.new_state(B)
     ys = [ref.prefill(x[:, :T].contiguous(), hs)]
@@ -28,6 +32,24 @@ def _run(world, cfg, T, n_dec, B, gather_q=False, norm=0, megatron=False):
         ys.append(ref.decode(x[:, t].contiguous(), hs).unsqueeze(1))
     torch.cuda.synchronize()
     yref = torch.cat(ys, 1)
+    # the unsharded result against the oracle's unsharded stack (prefill, then decode steps)
+    ob = [O.OracleBlock({k: v.numpy() for k, v in lat.items()}, cfg.d, cfg.l)
+          for lat in ref.latents]
+    xo = x.float().cpu().numpy()
+    bf = cfg.dtype == "bf16"
+    with O.norm_mode(norm):
+        Hs = [np.zeros((B, cfg.d), np.float32) for _ in ob]
+        yo, Hs = O.stack(ob, xo[:, :T], Hs, bf16=bf, eps=cfg.eps)
+        outs = [yo]
+        for t in range(T, T + n_dec):
+            yt, Hs = O.stack(ob, xo[:, t:t + 1], Hs, bf16=bf, eps=cfg.eps)
+            outs.append(yt)
+    yo = np.concatenate(outs, 1)
+    g = yref.float().cpu().numpy()
+    tol = 2e-2 if bf else 1e-4
+    rms = np.sqrt((yo.astype(np.float64) ** 2).mean(-1, keepdims=True))
+    assert np.all(np.abs(g - yo) <= tol * np.maximum(np.abs(yo), 1e-2 * rms)), \
+        f"unsharded CUDA vs oracle: max abs err {np.abs(g - yo).max()}"
 
     gather = shard.ThreadAllGather(world)
     stacks = [model.Stack.random(cfg, device="cuda", gen_device="cpu", shard=(r, gather, gather_q, megatron),
@@ -58,7 +80,7 @@ def _run(world, cfg, T, n_dec, B, gather_q=False, norm=0, megatron=False):
     for t in th:
         t.join(timeout=600)
     assert not errs, errs
-    for r in range(world):
+    for r in range(world):   # sharded == unsharded (bit for bit) == oracle (tolerance above)
         assert torch.equal(outs[r], yref), f"rank {r} differs from the unsharded path"
 
 
