@@ -97,6 +97,71 @@ def int8_peak_for(pk: dict, clocks: dict | None) -> tuple[float, str]:
 
 
 # ------------------------------------------------------------------ clocks
+class NvmlClocks:
+    """NVML sampler (every ~2 ms) running during the timed region: SM clock and the
+    clock-event (throttle) reasons, as nvidia-smi reports them (B200_PROFILING.md).
+    Short timed regions (tens of ms) get samples too, unlike `nvidia-smi -lms`."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown", 0x8),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap", 0x4))
+
+    def __init__(self, gpu_index: int):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        self.rows = []
+        self.stop_ev = threading.Event()
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        return sm, mx, int(get(self.h))
+
+    def start(self):
+        self._sample()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.rows.append(self._sample())
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def stop(self):
+        self.stop_ev.set()
+        self.t.join(timeout=2)
+        try:
+            self.rows.append(self._sample())
+        except Exception:
+            pass
+        reasons = set()
+        for _, _, bits in self.rows:
+            for name, const, default in self.REASONS:
+                if bits & getattr(self.nv, const, default):
+                    reasons.add(name)
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(r[1] for r in self.rows) if self.rows else None,
+                "reasons": sorted(reasons), "samples": len(sm), "sampler": "nvml"}
+
+
+def clock_sampler(gpu_index: int):
+    try:
+        return NvmlClocks(gpu_index).start()
+    except Exception:
+        return Clocks(gpu_index).start()
+
+
 class Clocks:
     """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
 
@@ -489,7 +554,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
 
-    clocks = Clocks(local_rank).start()
+    clocks = clock_sampler(local_rank)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     for i in range(args.steps):

@@ -207,15 +207,17 @@ class Stack:
         B, T, d = x.shape
         world = gather.world
         dt = L.dtype_code(self.dtype)
-        key = (B, T, world)
-        if getattr(self, "_sp_key", None) != key:   # workspace + ping-pong buffers, kept
+        # workspace + ping-pong buffers, kept per (shape, rank): virtual ranks (threads)
+        # may share one Stack, so each rank owns its own set
+        key = (B, T, world, rank, x.dtype)
+        cache = self.__dict__.setdefault("_sp_cache", {})
+        if key not in cache:
             need = max(int(L.load().tern_block_prefill_sp_workspace(C.byref(b.struct), B, T, dt,
                                                                       world))
                        for b in self.blocks)
-            self._sp_ws = torch.empty(need, dtype=torch.uint8, device=x.device)
-            self._sp_bufs = (torch.empty_like(x), torch.empty_like(x))
-            self._sp_key = key
-        ws, bufs = self._sp_ws, self._sp_bufs
+            cache[key] = (torch.empty(need, dtype=torch.uint8, device=x.device),
+                          (torch.empty_like(x), torch.empty_like(x)))
+        ws, bufs = cache[key]
         gather.register(ws, x, *bufs, *([out] if out is not None else []))
         sp = L.tern_seqpar(rank, world, gather.cb, C.c_void_p(rank))
         cur = x
