@@ -49,6 +49,8 @@ struct GemvArgs {
   int sw_stride;  // words between consecutive K-blocks of a segment in smem
   double inv_k;  // 1/K (binary64)
   int norm;      // tern_norm_mode of the input row
+  int ld_at;     // debug knob TERN_GEMV_LD_AT: where launch_dependents fires (0: after the
+                 // wait, 1: after the quant, 2: at the end)
   Epi epi;
   QuantTaps taps;
   const uint8_t* pf;         // L2 prefetch hint: a later launch's packed weights
@@ -388,6 +390,7 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
       }
   }
   __syncthreads();            // q rows visible
+  if (a.ld_at == 1) pdl_launch_dependents();
   mbar_wait(wbar, parity);    // weights landed (long since, in a PDL chain)
   GPROF(6)
   if (unit == 0 && a.taps.q) {
@@ -535,6 +538,224 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
   GPROF(9)
 }
 
+// ---------------------------------------------------------------- lean batch-1 kernel
+// The batch-1 decode phase (c2 / c4 B = 1, the paper's generate workload P:241): one token,
+// RMSNorm without a gain, no taps.  The arithmetic is gemv_run's bit for bit (binary64
+// sum of squares rounded once to r, C4; round half away, C3; Σ e q − Σ q).  A
+// phase is a few microseconds of latency-bound work on every SM, and with 16 warps per CTA
+// the SM sub-partitions' issue slots are the binding resource, so the kernel spends as few
+// warp-instructions as it can after the dependency wait (measured):
+//   * only the warps that hold part of the x row take part in the norm and the quant;
+//   * warp reductions of the max and of the integer sums are single REDUX instructions
+//     (max |x| compares float bits: order-preserving for non-negative floats);
+//   * the dot keeps one accumulator per 2-bit field (sum_f dp4a(w & mask_f, q_f)): the
+//     field scales 4^f are divided out once per channel instead of once per word (exact:
+//     every term of field f is a multiple of 4^f) -- 2 instructions per 4 trits;
+//   * the epilogue runs lane-parallel: lane j finishes the warp's j-th channel;
+//   * compact code (no per-M unrolling, no gain / centred / tap / profiling paths).
+template <typename TX, typename TY>
+__global__ void __launch_bounds__(kGThreads) k_gemv1(const GemvArgs a) {
+  extern __shared__ __align__(128) uint8_t g_smem[];
+  int8_t* qs = reinterpret_cast<int8_t*>(g_smem + (size_t)a.n_seg * (a.Kp >> 7) * a.sw_stride * 4);
+  __shared__ double red_d[kGWarps];
+  __shared__ unsigned red_m[kGWarps];
+  __shared__ int red_q[kGWarps];
+  __shared__ float sh_amax;
+  __shared__ __align__(8) uint64_t wbar;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int unit = blockIdx.x;
+  if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 0] = gtimer();
+  if (warp == 0) {   // this CTA's packed weights -> smem (bulk copies; independent of the chain)
+    if (lane == 0) {
+      mbar_init(&wbar, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    gemv_issue(a, unit, sw_words(g_smem), &wbar, lane, false);
+  }
+  if (a.pf && tid == 32) {   // L2 prefetch of this CTA's share of a later launch's weights
+    const size_t chunk = ((a.pf_bytes + gridDim.x - 1) / gridDim.x + 15) & ~size_t(15);
+    const size_t off = chunk * blockIdx.x;
+    if (off < a.pf_bytes) {
+      const size_t n = a.pf_bytes - off < chunk ? a.pf_bytes - off : chunk;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf + off), "r"((uint32_t)n)
+                   : "memory");
+    }
+  }
+  const Epi& e = a.epi;
+  // epilogue operands of this warp's channels: lane j <-> channel warp + 16 j (j < 4)
+  const int ich = warp + lane * kGWarps, rch = unit * a.ch + ich;
+  const bool own = lane < 4 && ich < a.ch && rch < a.n_out;
+  float msc[3];
+#pragma unroll
+  for (int sg = 0; sg < 3; ++sg) msc[sg] = sg < a.n_seg ? __ldg(e.scales + sg) : 0.0f;
+  pdl_wait();
+  if (a.ld_at == 0) pdl_launch_dependents();
+  if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 1] = gtimer();
+  float pre = 0.0f;
+  // (trace marks, tid 0: 9 x loaded, 10 norm done, 5 q row ready, 6 first dot loop,
+  //  7 its sums, 8 all dots, 2 epilogue done)
+  if (own && e.kind == EPI_MLGRU) pre = __ldcg(e.h + rch);
+  if (own && e.kind == EPI_RESID) pre = ld_act_cg<TY>(static_cast<const TY*>(e.res) + rch);
+  // ---- x -> registers, binary64 sum of squares and max |x| (a2, C4): warps holding data
+  constexpr int VE = XVec<TX>::N;
+  const int nvec = a.K / VE, nvecp = a.Kp / VE;
+  const int nwx = (nvecp + 31) >> 5 < kGWarps ? (nvecp + 31) >> 5 : kGWarps;   // data warps
+  const bool xw = warp < nwx;
+  uint4 xv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+  if (xw) {
+    const uint4* src = static_cast<const uint4*>(a.x);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int v = tid + i * kGThreads;
+      if (v < nvec) xv[i] = __ldcg(src + v);
+    }
+    double s0 = 0.0, s1 = 0.0;
+    float xm = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      float v[VE];
+      XVec<TX>::unpack(xv[i], v);
+#pragma unroll
+      for (int j = 0; j < VE; j += 2) {
+        s0 = fma((double)v[j], (double)v[j], s0);
+        s1 = fma((double)v[j + 1], (double)v[j + 1], s1);
+        xm = fmaxf(xm, fmaxf(fabsf(v[j]), fabsf(v[j + 1])));
+      }
+    }
+    double sd = s0 + s1;
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 9] = gtimer();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+    const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(xm));
+    if (lane == 0) {
+      red_d[warp] = sd;
+      red_m[warp] = mb;
+    }
+  }
+  __syncthreads();
+  int tq = 0;
+  if (xw) {
+    double sd = lane < nwx ? red_d[lane] : 0.0;
+#pragma unroll
+    for (int o = kGWarps / 2; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+    sd = __shfl_sync(0xffffffffu, sd, 0);
+    const unsigned mb = __reduce_max_sync(0xffffffffu, lane < nwx ? red_m[lane] : 0u);
+    const float rinv = (float)rsqrt(fma(sd, a.inv_k, (double)a.eps));
+    // max|fl(x r)| = fl(max|x| r): rounding is monotone and r > 0
+    const float amax = __fmul_rn(__uint_as_float(mb), rinv);
+    if (tid == 0) sh_amax = amax;
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 10] = gtimer();
+    // quantize own elements: q = round(x r * 127/amax), half away from zero (C3, C5)
+    const float sc = amax > 0.0f ? __fdiv_rn(127.0f, amax) : 0.0f;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int v = tid + i * kGThreads;
+      if (v < nvecp) {
+        uint32_t pk[VE / 4];
+#pragma unroll
+        for (int j4 = 0; j4 < VE / 4; ++j4) pk[j4] = 0;
+        if (v < nvec && amax > 0.0f) {
+          float xf[VE];
+          XVec<TX>::unpack(xv[i], xf);
+#pragma unroll
+          for (int j = 0; j < VE; ++j) {
+            // |y*sc| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
+            const int qi =
+                int_of_integral(round_half_away_small(__fmul_rn(__fmul_rn(xf[j], rinv), sc)));
+            tq += qi;
+            pk[j >> 2] |= ((uint32_t)qi & 0xffu) << (8 * (j & 3));
+          }
+        }
+        if (VE == 4)
+          *reinterpret_cast<uint32_t*>(qs + v * 4) = pk[0];
+        else
+          *reinterpret_cast<uint2*>(qs + v * 8) = make_uint2(pk[0], pk[VE / 4 - 1]);
+      }
+    }
+    tq = __reduce_add_sync(0xffffffffu, tq);
+    if (lane == 0) red_q[warp] = tq;
+  }
+  __syncthreads();            // q row, q-sum partials and amax visible
+  if (a.ld_at == 1) pdl_launch_dependents();
+  if (warp >= a.ch) return;   // no channel for this warp (nothing else to do)
+  mbar_wait(&wbar, 0);        // weights landed (long since, in a PDL chain)
+  if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 5] = gtimer();
+  const int qsum = __reduce_add_sync(0xffffffffu, lane < nwx ? red_q[lane] : 0);
+  // ---- dot (a3): warp w owns channels w, w+16, ... with all their segments; lanes split
+  // the row's 32-bit words (16 trits x 16 q bytes each)
+  const int W = a.Kp >> 4, nkb = a.Kp >> 7, SW = a.sw_stride;
+  const uint32_t* swd = sw_words(g_smem);
+  int accl[3] = {0, 0, 0};   // lane j: channel warp + 16 j
+#pragma unroll 1
+  for (int j = 0; j < 4; ++j) {
+    const int i = warp + j * kGWarps;
+    if (i >= a.ch) break;
+    int pf[3][4];
+#pragma unroll
+    for (int sg = 0; sg < 3; ++sg)
+#pragma unroll
+      for (int f = 0; f < 4; ++f) pf[sg][f] = 0;
+#pragma unroll 2
+    for (int w = lane; w < W; w += 32) {
+      const uint4 qv = *reinterpret_cast<const uint4*>(qs + w * 16);
+      const uint32_t* wrow = swd + (w >> 3) * SW + (w & 7) + i * 8;
+#pragma unroll
+      for (int sg = 0; sg < 3; ++sg) {
+        if (sg < a.n_seg) {
+          const uint32_t wd = wrow[sg * nkb * SW];
+          // field f of the word holds trits 4f..4f+3, i.e. q bytes [4f, 4f+4), times 4^f
+          pf[sg][0] = dp4a_us(wd & 0x03030303u, qv.x, pf[sg][0]);
+          pf[sg][1] = dp4a_us(wd & 0x0C0C0C0Cu, qv.y, pf[sg][1]);
+          pf[sg][2] = dp4a_us(wd & 0x30303030u, qv.z, pf[sg][2]);
+          pf[sg][3] = dp4a_us(wd & 0xC0C0C0C0u, qv.w, pf[sg][3]);
+        }
+      }
+    }
+    if (a.trace && tid == 0 && j == 0) a.trace[blockIdx.x * 16 + 6] = gtimer();
+#pragma unroll
+    for (int sg = 0; sg < 3; ++sg) {
+      if (sg < a.n_seg) {
+        // sum e q over the row (each field's sum is an exact multiple of its 4^f)
+        const int t = __reduce_add_sync(0xffffffffu, pf[sg][0]) +
+                      (__reduce_add_sync(0xffffffffu, pf[sg][1]) >> 2) +
+                      (__reduce_add_sync(0xffffffffu, pf[sg][2]) >> 4) +
+                      (__reduce_add_sync(0xffffffffu, pf[sg][3]) >> 6);
+        if (lane == j) accl[sg] = t - qsum;   // sum e q - sum q = sum t q
+      }
+    }
+    if (a.trace && tid == 0 && j == 0) a.trace[blockIdx.x * 16 + 7] = gtimer();
+  }
+  if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 8] = gtimer();
+  if (!own) return;
+  // ---- epilogue (a5-a8), lane-parallel over the warp's channels
+  const float amax = sh_amax;
+  const float deq = amax > 0.0f ? __fdiv_rn(amax, 127.0f) : 0.0f;
+  TY* out = static_cast<TY*>(e.out);
+  const int rr = rch;
+  if (e.kind == EPI_MLGRU) {
+    const float fh = bl_val<TY>(e, accl[0], deq, msc[0], 0, rr);
+    const float chh = bl_val<TY>(e, accl[1], deq, msc[1], 1, rr);
+    const float gh = bl_val<TY>(e, accl[2], deq, msc[2], 2, rr);
+    const float h = mlgru_step(sigmoid_c(fh), pre, silu_c(chh));
+    e.h[rr] = h;
+    st_act<TY>(out + rr, mlgru_out(gh, h, e.gate));
+  } else if (e.kind == EPI_SWIGLU) {
+    const float gh = bl_val<TY>(e, accl[0], deq, msc[0], 0, rr);
+    const float uh = bl_val<TY>(e, accl[1], deq, msc[1], 1, rr);
+    st_act<TY>(out + rr, swiglu(gh, uh));
+  } else if (e.kind == EPI_RESID) {
+    st_act<TY>(out + rr, __fadd_rn(pre, bl_val<TY>(e, accl[0], deq, msc[0], 0, rr)));
+  } else {   // EPI_STORE / EPI_FCG
+    for (int sg = 0; sg < a.n_seg; ++sg) {
+      const float o = bl_val<TY>(e, sg == 0 ? accl[0] : (sg == 1 ? accl[1] : accl[2]), deq,
+                                 sg == 0 ? msc[0] : (sg == 1 ? msc[1] : msc[2]), sg, rr);
+      st_act<TY>(out + (e.kind == EPI_FCG ? packed_row(sg, rr, a.n_seg) : rr), o);
+    }
+  }
+  if (a.trace && lane == 0 && warp == 0) a.trace[blockIdx.x * 16 + 2] = gtimer();
+}
+
 // One BitLinear per launch (PDL chain of launches).
 template <int MM, typename TX, typename TY, bool CENT>
 __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
@@ -581,7 +802,7 @@ __global__ void __launch_bounds__(kGThreads) k_gemv(const GemvArgs a) {
   pdl_wait();
   // let the next kernel start its weight prefetch only now: earlier triggers
   // let grids two launches ahead occupy SM slots and delay this grid's CTAs
-  pdl_launch_dependents();
+  if (a.ld_at == 0) pdl_launch_dependents();
   GPROF(1)
   if (a.trace && tid == 0) a.trace[blockIdx.x * 16 + 1] = gtimer();
   float pre[4];
@@ -797,6 +1018,8 @@ void gemv_trace_enable(int on) {
   }
   g_trace_on = on && g_trace;
   g_trace_seq = 0;
+  if (g_trace_on)   // unwritten marks read as 0 (tools/decode_trace.py prints them as '-')
+    cudaMemset(g_trace, 0, sizeof(unsigned long long) * kTraceLaunches * kTraceCtas * 16);
 }
 
 unsigned long long* trace_slot(int kind, int ctas) {
@@ -883,8 +1106,47 @@ static cudaError_t gemv_launch(const GemvArgs& a, int units, cudaStream_t s) {
   return err;
 }
 
+// the lean batch-1 kernel: M = 1, RMSNorm without a gain, no taps (TERN_GEMV_LEAN=0: off)
+static bool gemv_lean_ok(const GemvArgs& a) {
+  static const bool on = !getenv("TERN_GEMV_LEAN") || atoi(getenv("TERN_GEMV_LEAN")) != 0;
+  return on && a.M == 1 && a.gain == nullptr && a.norm == TERN_NORM_RMS && a.prof == nullptr &&
+         a.taps.q == nullptr && a.taps.deq == nullptr && a.taps.inv_rms == nullptr &&
+         a.taps.absmax == nullptr && a.epi.acc == nullptr && a.epi.kind != EPI_NONE;
+}
+
+template <typename TX, typename TY>
+static cudaError_t gemv1_launch(const GemvArgs& a, int units, cudaStream_t s) {
+  const size_t smem = gemv_smem(1, a.n_seg, a.ch, a.Kp);
+  auto kern = k_gemv1<TX, TY>;
+  static size_t smem_set = 48 * 1024;
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    smem_set = 200 * 1024;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(units);
+  cfg.blockDim = dim3(kGThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GemvArgs aa = a;
+  if (g_trace_on && units <= kTraceCtas) {
+    const int slot = g_trace_seq % kTraceLaunches;
+    aa.trace = g_trace + (size_t)slot * kTraceCtas * 16;
+    g_trace_units[slot] = units | (TERN_K_GEMV << 20);
+    ++g_trace_seq;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, aa);
+}
+
 template <typename TX, typename TY>
 static cudaError_t gemv_dispatch_m(const GemvArgs& a, int units, cudaStream_t s) {
+  if (gemv_lean_ok(a)) return gemv1_launch<TX, TY>(a, units, s);
   if (a.M <= 1) return gemv_launch<1, TX, TY>(a, units, s);
   if (a.M <= 2) return gemv_launch<2, TX, TY>(a, units, s);
   return gemv_launch<4, TX, TY>(a, units, s);
@@ -919,6 +1181,8 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
   a.K = K;
   a.inv_k = 1.0 / (double)K;
   a.norm = norm;
+  static const int ld_at = getenv("TERN_GEMV_LD_AT") ? atoi(getenv("TERN_GEMV_LD_AT")) : 0;
+  a.ld_at = ld_at;
   a.Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
   a.M = M;
   a.gain = gain;

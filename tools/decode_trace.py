@@ -16,6 +16,8 @@ from paper_2406_02528_b200 import model, synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--blocks", type=int, default=4)
+ap.add_argument("--lean-marks", action="store_true",
+                help="label the marks of the batch-1 kernel k_gemv1 (x, norm, q, dot0, sums0, dots)")
 ap.add_argument("--per-block", action="store_true",
                 help="trace the per-block launch chain instead of the persistent kernel")
 args = ap.parse_args()
@@ -46,15 +48,21 @@ names = ["fcg", "o", "gu", "down"]
 prev_end = None
 t0 = min(int(r[:, 0].min()) for _, r in recs)
 print(f"{'launch':>8} {'ctas':>5} {'start_min':>9} {'start_max':>9} {'rel_min':>8} {'rel_max':>8} "
-      f"{'end_max':>8} {'post_wait':>9} {'gap_after_prev':>14} | mean ns after release: x warpred bar r quant dot0 red0 end")
+      f"{'end_max':>8} {'post_wait':>9} {'gap_after_prev':>14} | mean ns after release: "
+      f"sq warpred bar r quant dot0 epi end  ('-': mark not recorded by this kernel)")
 for i, (u, r) in enumerate(recs):
     u &= 0xFFFFF
     s0, s1 = int(r[:, 0].min()) - t0, int(r[:, 0].max()) - t0
     w0, w1 = int(r[:, 1].min()) - t0, int(r[:, 1].max()) - t0
     e = int(r[:, 2].max()) - t0
     gap = (w0 - prev_end) if prev_end is not None else 0
-    ph = [int((r[:, 5 + k] - r[:, 1]).mean()) for k in range(7)] + [int((r[:, 2] - r[:, 1]).mean())]
+    # marks: slots 5..10 = GPROF(2..7), slot 12 = GPROF(9) (slot 11 is never written)
+    ph = []
+    for k in ((9, 10, 5, 6, 7, 8) if args.lean_marks else (5, 6, 7, 8, 9, 10, 12)):
+        col = r[:, k]
+        ph.append(int((col - r[:, 1]).mean()) if np.all(col > 0) else None)
+    ph.append(int((r[:, 2] - r[:, 1]).mean()))
     ghz = float(np.median((r[:, 4] - r[:, 3]) / np.maximum(r[:, 2] - r[:, 0], 1)))
     print(f"{names[i % 4] + str(i // 4):>8} {u:5d} {s0:9d} {s1:9d} {w0:8d} {w1:8d} {e:8d} {e - w0:9d} {gap:14d} | "
-          + " ".join(f"{v:5d}" for v in ph) + f"  clk {ghz:.2f} GHz")
+          + " ".join(f"{v:5d}" if v is not None else "    -" for v in ph) + f"  clk {ghz:.2f} GHz")
     prev_end = e
