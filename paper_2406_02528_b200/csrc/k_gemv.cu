@@ -51,6 +51,8 @@ struct GemvArgs {
   int norm;      // tern_norm_mode of the input row
   int ld_at;     // debug knob TERN_GEMV_LD_AT: where launch_dependents fires (0: after the
                  // wait, 1: after the quant, 2: at the end)
+  int strip;     // debug knob TERN_GEMV_STRIP (timing experiments only, wrong results):
+                 // 1 skip the dot, 2 skip the epilogue math, 4 skip the quant
   Epi epi;
   QuantTaps taps;
   const uint8_t* pf;         // L2 prefetch hint: a later launch's packed weights
@@ -549,7 +551,7 @@ __device__ __forceinline__ void gemv_run(const GemvArgs& a, int unit, const uint
 //   * warp reductions of the max and of the integer sums are single REDUX instructions
 //     (max |x| compares float bits: order-preserving for non-negative floats);
 //   * the dot keeps one accumulator per 2-bit field (sum_f dp4a(w & mask_f, q_f)): the
-//     field scales 4^f are divided out once per channel instead of once per word (exact:
+//     field scales 4^f are divided out once per lane and channel instead of once per word (exact:
 //     every term of field f is a multiple of 4^f) -- 2 instructions per 4 trits;
 //   * the epilogue runs lane-parallel: lane j finishes the warp's j-th channel;
 //   * compact code (no per-M unrolling, no gain / centred / tap / profiling paths).
@@ -651,7 +653,7 @@ __global__ void __launch_bounds__(kGThreads) k_gemv1(const GemvArgs a) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int v = tid + i * kGThreads;
-      if (v < nvecp) {
+      if (v < nvecp && !(a.strip & 4)) {
         uint32_t pk[VE / 4];
 #pragma unroll
         for (int j4 = 0; j4 < VE / 4; ++j4) pk[j4] = 0;
@@ -697,7 +699,7 @@ __global__ void __launch_bounds__(kGThreads) k_gemv1(const GemvArgs a) {
 #pragma unroll
       for (int f = 0; f < 4; ++f) pf[sg][f] = 0;
 #pragma unroll 2
-    for (int w = lane; w < W; w += 32) {
+    for (int w = lane; w < ((a.strip & 1) ? 0 : W); w += 32) {
       const uint4 qv = *reinterpret_cast<const uint4*>(qs + w * 16);
       const uint32_t* wrow = swd + (w >> 3) * SW + (w & 7) + i * 8;
 #pragma unroll
@@ -716,11 +718,10 @@ __global__ void __launch_bounds__(kGThreads) k_gemv1(const GemvArgs a) {
 #pragma unroll
     for (int sg = 0; sg < 3; ++sg) {
       if (sg < a.n_seg) {
-        // sum e q over the row (each field's sum is an exact multiple of its 4^f)
-        const int t = __reduce_add_sync(0xffffffffu, pf[sg][0]) +
-                      (__reduce_add_sync(0xffffffffu, pf[sg][1]) >> 2) +
-                      (__reduce_add_sync(0xffffffffu, pf[sg][2]) >> 4) +
-                      (__reduce_add_sync(0xffffffffu, pf[sg][3]) >> 6);
+        // sum e q over the row: every term of the lane's field-f sum is a multiple of 4^f,
+        // so the shifts are exact per lane; one REDUX per segment
+        const int t = __reduce_add_sync(0xffffffffu, pf[sg][0] + (pf[sg][1] >> 2) +
+                                                         (pf[sg][2] >> 4) + (pf[sg][3] >> 6));
         if (lane == j) accl[sg] = t - qsum;   // sum e q - sum q = sum t q
       }
     }
@@ -733,7 +734,9 @@ __global__ void __launch_bounds__(kGThreads) k_gemv1(const GemvArgs a) {
   const float deq = amax > 0.0f ? __fdiv_rn(amax, 127.0f) : 0.0f;
   TY* out = static_cast<TY*>(e.out);
   const int rr = rch;
-  if (e.kind == EPI_MLGRU) {
+  if (a.strip & 2) {
+    st_act<TY>(out + rr, (float)accl[0]);
+  } else if (e.kind == EPI_MLGRU) {
     const float fh = bl_val<TY>(e, accl[0], deq, msc[0], 0, rr);
     const float chh = bl_val<TY>(e, accl[1], deq, msc[1], 1, rr);
     const float gh = bl_val<TY>(e, accl[2], deq, msc[2], 2, rr);
@@ -1182,7 +1185,9 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
   a.inv_k = 1.0 / (double)K;
   a.norm = norm;
   static const int ld_at = getenv("TERN_GEMV_LD_AT") ? atoi(getenv("TERN_GEMV_LD_AT")) : 0;
+  static const int strip = getenv("TERN_GEMV_STRIP") ? atoi(getenv("TERN_GEMV_STRIP")) : 0;
   a.ld_at = ld_at;
+  a.strip = strip;
   a.Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
   a.M = M;
   a.gain = gain;

@@ -59,6 +59,22 @@ __global__ void lat_shfl(float* out, float a, int n, long long* cyc) {
   out[threadIdx.x] = x;
   if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
+__global__ void lat_redux(int* out, int n, long long* cyc) {
+  int x = threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) x = __reduce_add_sync(0xffffffffu, x) + threadIdx.x;
+  long long t1 = clock64();
+  out[threadIdx.x] = x;
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+__global__ void thr_redux(int* out, int n) {
+  int x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+  for (int i = 0; i < n; ++i) {
+    x0 = __reduce_add_sync(0xffffffffu, x0) ^ i; x1 = __reduce_add_sync(0xffffffffu, x1) ^ i;
+    x2 = __reduce_add_sync(0xffffffffu, x2) ^ i; x3 = __reduce_add_sync(0xffffffffu, x3) ^ i;
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3;
+}
 __global__ void lat_bar(float* out, int n, long long* cyc) {
   __shared__ float s[256];
   float x = threadIdx.x;
@@ -85,7 +101,16 @@ int main() {
   printf("SHFL+FADD chain: %.2f cyc\n", (double)h / n);
   lat_bar<<<1, 256>>>(f, 1024, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
   printf("STS+BAR+LDS+BAR (256 thr): %.2f cyc\n", (double)h / 1024);
+  lat_redux<<<1, 32>>>((int*)f, n, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("REDUX.SUM dependent chain: %.2f cyc\n", (double)h / n);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  {
+    float ms2;
+    thr_redux<<<148, 512>>>((int*)d, 1024);
+    cudaEventRecord(e0); thr_redux<<<148, 512>>>((int*)d, 1024); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms2, e0, e1);
+    printf("REDUX throughput: %.2f warp-REDUX per clk per SM at 1.9GHz\n", 4.0 * 1024 * 148 * 16 / (ms2 * 1e-3) / 148 / 1.9e9);
+  }
   int blocks = 148 * 8, thr = 256, it = 2048;
   thr_dfma<<<blocks, thr>>>(d, 1.0, it);
   cudaEventRecord(e0); thr_dfma<<<blocks, thr>>>(d, 1.0, it); cudaEventRecord(e1); cudaEventSynchronize(e1);
