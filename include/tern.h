@@ -508,6 +508,13 @@ int32_t tern_get_gemv_max_m(void);
  * GEMM + epilogue per BitLinear.  Results are identical. */
 void tern_set_batched_fin(int32_t on);
 int32_t tern_get_batched_fin(void);
+/* Tuning knob (host): 1 runs the contraction of 4 < M <= 256 token calls that have a
+ * split-K workspace (decode batches) with the swap-AB kernel (weights as the MMA's
+ * 128-row operand, streamed as 2-bit codes and unpacked in shared memory; tokens as N);
+ * 0 (default, measured faster on c3 B = 64 and c4 B = 128) with the u8-tile GEMM.
+ * Results are identical (integer sums).  Initial value: env TERN_GEMM_SAB, else 0. */
+void tern_set_gemm_sab(int32_t on);
+int32_t tern_get_gemm_sab(void);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -125,6 +125,8 @@ _SIGS = {
     "tern_set_fused_scan": (None, [I32]),
     "tern_get_fused_scan": (I32, []),
     "tern_set_batched_fin": (None, [I32]),
+    "tern_set_gemm_sab": (None, [I32]),
+    "tern_get_gemm_sab": (I32, []),
     "tern_set_norm_mode": (None, [C.c_int]),
     "tern_get_norm_mode": (C.c_int, []),
     "tern_get_batched_fin": (I32, []),
@@ -322,6 +324,14 @@ def tern_get_norm_mode() -> int:
 
 def tern_set_batched_fin(on: bool):
     load().tern_set_batched_fin(1 if on else 0)
+
+
+def tern_set_gemm_sab(on: bool):
+    load().tern_set_gemm_sab(1 if on else 0)
+
+
+def tern_get_gemm_sab() -> bool:
+    return bool(load().tern_get_gemm_sab())
 
 
 def tern_get_batched_fin() -> bool:

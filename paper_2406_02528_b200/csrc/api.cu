@@ -318,6 +318,8 @@ int32_t tern_get_fused_scan(void) { return g_fused_scan; }
 void tern_set_gemv_max_m(int32_t m) { g_gemv_max_m = m < 0 ? 0 : (m > kGemvMaxM ? kGemvMaxM : m); }
 int32_t tern_get_gemv_max_m(void) { return g_gemv_max_m; }
 void tern_set_batched_fin(int32_t on) { g_batched_fin = on ? 1 : 0; }
+void tern_set_gemm_sab(int32_t on) { g_gemm_sab = on ? 1 : 0; }
+int32_t tern_get_gemm_sab(void) { return g_gemm_sab; }
 void tern_set_norm_mode(tern_norm_mode mode) {
   g_norm_mode = mode == TERN_NORM_CENTERED ? TERN_NORM_CENTERED : TERN_NORM_RMS;
 }

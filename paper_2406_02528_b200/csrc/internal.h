@@ -68,8 +68,17 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
                         float eps, const tern_weight& w, const Epi& epi, const QuantTaps* taps,
                         cudaStream_t s, const void* pf = nullptr, size_t pf_bytes = 0,
                         int norm = TERN_NORM_RMS);
+// swap-AB tcgen05 contraction for decode batches (k_gemm_sab.cu): int32 partials
+// part[ks][M][n_rows] from the 2-bit codes; *ks_out = slices used
+bool gemm_sab_supported(int M);
+extern int g_gemm_sab;   // tern_set_gemm_sab
+cudaError_t launch_gemm_sab(const int8_t* q, int M, int ldq, const tern_weight& w, int32_t* part,
+                            size_t part_bytes, int ks_max, int* ks_out, cudaStream_t s);
+cudaError_t launch_splitk_epi(const int32_t* part, int ks, int M, int n_rows, const float* deq,
+                              const int32_t* qsum, const Epi& e, int ydt, cudaStream_t s);
 // a4 (tcgen05 int8 GEMM): q [M][ldq] -> epilogue
-// part: optional int32 scratch [M][n_rows] enabling split-K for small M (nullptr: never)
+// part: optional int32 scratch [M][n_rows] enabling split-K for small M (nullptr: never);
+// with part, decode batches (M <= 256) take the swap-AB kernel above
 // ks_out: partials only (part required): the K-slice count is returned and no
 // epilogue runs (launch_fin finalizes); *ks_out > 0 on entry caps the count
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
@@ -124,10 +133,9 @@ cudaError_t launch_slice_stats(const void* x, int ldx, int M, int cs, int world,
 cudaError_t launch_slice_quant(const void* x, int ldx, int M, int cs, int world, int rank, int dt,
                                const float* gain, float eps, int norm, const double* const* st,
                                int8_t* q, int ldq, int32_t* qs_out, float* deq, cudaStream_t s);
-// the split-K epilogue on its own: sums ks int32 slices part[ks][M][n_rows] and
-// applies e (f1(ii): after the all-reduce of a row-parallel GEMM's partials)
-cudaError_t launch_splitk_epi(const int32_t* part, int ks, int M, int n_rows, const float* deq,
-                              const int32_t* qsum, const Epi& e, int ydt, cudaStream_t s);
+// (launch_splitk_epi, above: the split-K epilogue on its own -- sums ks int32 slices
+// part[ks][M][n_rows] and applies e; also f1(ii), after the all-reduce of a row-parallel
+// GEMM's partials)
 cudaError_t launch_unshard_q(const int8_t* gathered, int world, int M, int cs, int8_t* q, int ldq,
                              int32_t* qsum, cudaStream_t s);
 // a4 + a6 fused (prefill): f|c|g GEMM with the MLGRU scan in its epilogue

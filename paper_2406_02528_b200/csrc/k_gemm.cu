@@ -710,6 +710,8 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
   }
 }
 
+int g_gemm_sab = getenv("TERN_GEMM_SAB") ? (atoi(getenv("TERN_GEMM_SAB")) != 0) : 0;
+
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
                         int32_t* part, size_t part_bytes, int* ks_out) {
@@ -778,6 +780,21 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   const bool finalize = ks_out != nullptr || epi.kind == EPI_MLGRU ||
                         (part && part_bytes >= slice && epi.kind != EPI_NONE && w.n_rows % 2 == 0 &&
                          epi.acc == nullptr && tiles * 2 <= num_sms && a.num_kb >= 2);
+  // decode batches, opt-in (TERN_GEMM_SAB=1; measured slower, k_gemm_sab.cu): the swap-AB
+  // kernel streams the 2-bit codes (weights as the MMA's M operand, tokens as N) into int32
+  // K-slice partials
+  if (g_gemm_sab && M <= kSmallM && gemm_sab_supported(M) && part && part_bytes >= slice &&
+      epi.acc == nullptr && (epi.kind != EPI_NONE || ks_out) && w.n_rows % 2 == 0) {
+    int ks = 0;
+    const int ks_max = (ks_out && *ks_out > 0) ? *ks_out : 0;
+    cudaError_t err = launch_gemm_sab(q, M, ldq, w, part, part_bytes, ks_max, &ks, s);
+    if (err != cudaSuccess) return err;
+    if (ks_out) {   // partials only: the caller finalizes (k_fin.cu)
+      *ks_out = ks;
+      return cudaSuccess;
+    }
+    return launch_splitk_epi(part, ks, M, w.n_rows, deq, qsum, epi, ydt, s);
+  }
   if (finalize) {
     if (!part || part_bytes < slice) return cudaErrorInvalidValue;
     int ks = num_sms / tiles;   // one round of work units over the SMs

@@ -359,8 +359,8 @@ def test_fused_fcg_scan_equals_unfused(L, M, dtype, B, T, d, gate):
 # ------------------------------------------------------------------------ batched decode (split-K)
 @pytest.mark.parametrize("cfg_name,B,T,n_dec", [("c2", 32, 3, 2), ("c4", 16, 2, 2), ("c3", 64, 1, 2),
                                                ("c4", 128, 1, 2)])
-@pytest.mark.parametrize("fin", [False, True])
-def test_batched_decode_split_k_parity(L, M, cfg_name, B, T, n_dec, fin):
+@pytest.mark.parametrize("fin,sab", [(False, False), (True, False), (False, True), (True, True)])
+def test_batched_decode_split_k_parity(L, M, cfg_name, B, T, n_dec, fin, sab):
     """Decode batches above the GEMV limit: per BitLinear a split-K tcgen05 GEMM (int32
     slices) and a row-wise finalize that applies the epilogue and quantizes the row for the
     next BitLinear (k_fin.cu); short prefills take quant + GEMM + split-K epilogue.
@@ -370,15 +370,17 @@ def test_batched_decode_split_k_parity(L, M, cfg_name, B, T, n_dec, fin):
     x = synth.hidden((B, T + n_dec, cfg.d), synth.generator(cfg.seed + 77), cfg.dtype)
     xd = x.cuda()
     states = st.new_state(B)
-    old = L.tern_get_batched_fin()
+    old, old_sab = L.tern_get_batched_fin(), L.tern_get_gemm_sab()
     try:
         L.tern_set_batched_fin(fin)
+        L.tern_set_gemm_sab(sab)   # swap-AB small-M kernel (k_gemm_sab.cu, opt-in)
         ys = [st.prefill(xd[:, :T].contiguous(), states)]
         for t in range(T, T + n_dec):
             ys.append(st.decode(xd[:, t].contiguous(), states).unsqueeze(1))
         torch.cuda.synchronize()
     finally:
         L.tern_set_batched_fin(old)
+        L.tern_set_gemm_sab(old_sab)
     yg = f32np(torch.cat(ys, 1))
     bf = cfg.dtype == "bf16"
     H = [np.zeros((B, cfg.d), np.float32)]

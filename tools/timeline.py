@@ -16,7 +16,7 @@ import torch  # noqa: E402
 from paper_2406_02528_b200 import _lib as L  # noqa: E402
 from paper_2406_02528_b200 import model, synth  # noqa: E402
 
-NAMES = {0: "quant", 1: "gemv", 2: "gemm", 18: "splitk_epi", 3: "scan", 4: "fcgscan",
+NAMES = {0: "quant", 1: "gemv", 2: "gemm", 18: "splitk_epi", 34: "gemm_sab", 3: "scan", 4: "fcgscan",
          5: "stack", 6: "fin"}
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
