@@ -32,16 +32,19 @@ constexpr int kEpiWarps = 8;
 constexpr int kEpiBuf = 4096;  // bytes of one 32x32 staging tile (fp32)
 constexpr int kSmallM = 256;   // M at or below: packed B tiles (+ split-K when tiles are few)
 
-template <int BN, bool kPre> struct GemmCfg {
+template <int BN, bool kPre, bool RES = false> struct GemmCfg {
   static constexpr int A_BYTES = kBM * kBK;        // 16 KB
   static constexpr int B_BYTES = BN * kBK;         // u8 B tile
   static constexpr int BP_BYTES = BN * (kBK / 4);  // packed B: BN rows x 8 words
   // TMA ring depth S, unpacked ring depth U (packed path only), epilogue
   // staging tiles per warp NB: the u8 256-wide ring takes a 4th stage (deeper
-  // load pipeline) at the price of single-buffered epilogue stores
-  static constexpr int S = kPre ? 4 : (BN == 256 ? 4 : 5);
+  // load pipeline) at the price of single-buffered epilogue stores -- except for the
+  // residual epilogue (RES), where two staging tiles per warp let each chunk's residual
+  // load be issued one chunk ahead (its HBM latency otherwise serialises the drain and
+  // the MMA waits on the accumulators: TERN_GEMM_PROF mma.tempty)
+  static constexpr int S = kPre ? ((RES && BN == 256) ? 3 : 4) : (BN == 256 ? 4 : 5);
   static constexpr int U = kPre ? 0 : 2;
-  static constexpr int NB = (kPre && BN == 256) ? 1 : 2;
+  static constexpr int NB = (kPre && BN == 256 && !RES) ? 1 : 2;
   static constexpr int RING = kPre ? S * (A_BYTES + B_BYTES) : S * (A_BYTES + BP_BYTES) + U * B_BYTES;
   static constexpr int EPI_BYTES = kEpiWarps * NB * kEpiBuf;
   static constexpr int SMEM = RING + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
@@ -164,12 +167,12 @@ __device__ void acc_tap_chunk(const Epi& e, const GemmArgs& a, int* si, int lane
   __syncwarp();
 }
 
-template <int BN, bool kPre, typename TY>
+template <int BN, bool kPre, typename TY, bool RES = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
               const GemmArgs a) {
-  using Cfg = GemmCfg<BN, kPre>;
+  using Cfg = GemmCfg<BN, kPre, RES>;
   constexpr int S = Cfg::S;
   constexpr int U = Cfg::U;
   extern __shared__ __align__(1024) uint8_t gsm_raw[];
@@ -366,7 +369,88 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const float msc2 = nseg > 2 ? __ldg(e.scales + 2) : 0.0f;
     uint32_t it = 0, nchunk = 0;
     uint32_t rphase[2] = {0, 0};
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+    if (RES) {
+      // residual epilogue (EPI_RESID, no taps, no split-K): chunk k of this warp (over its
+      // tiles in order) reads its residual into staging buffer k & 1; the load of chunk k+1
+      // is issued before chunk k is computed, so its latency hides behind one chunk
+      auto chunk_at = [&](int t_, int c_, int& row0_, int& col0_) -> bool {
+        // the first chunk of this warp at or after (t_, c_): its tile row / column
+        for (; t_ < total; t_ += gridDim.x, c_ = half) {
+          const int tile_ = t_ / a.ksplit;
+          const int m0_ = (tile_ / a.n_tiles) * kBM, n0_ = (tile_ % a.n_tiles) * BN;
+          if (c_ < BN / 32 && n0_ + c_ * 32 < a.n_rows) {
+            row0_ = m0_ + quad * 32;
+            col0_ = n0_ + c_ * 32;
+            return true;
+          }
+        }
+        return false;
+      };
+      int nr0 = 0, nc0 = 0;
+      if (lead && chunk_at(blockIdx.x, half, nr0, nc0)) {
+        mbar_arrive_expect_tx(&rb[0], 32 * 32 * sizeof(TY));
+        tma_load_2d(bufs, &tmR, &rb[0], nc0, nr0);
+      }
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        const uint32_t acc = it & 1;
+        const int tile = t / a.ksplit;
+        const int m0 = (tile / a.n_tiles) * kBM, n0 = (tile % a.n_tiles) * BN;
+        pwait(&tfull[acc], (it >> 1) & 1, (ew == 0 && lead) ? a.prof : nullptr, 5);
+        tc_fence_after();
+        const int row0 = m0 + quad * 32;
+        const int row = row0 + lane;
+        const bool rv = row < a.M;
+        const float deq = rv ? __ldg(a.deq + row) : 0.0f;
+        const int qsum = rv ? __ldg(a.qsum + row) : 0;
+        const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+        for (int c = half; c < BN / 32; c += 2) {
+          const int col0 = n0 + c * 32;
+          if (col0 >= a.n_rows) continue;
+          uint32_t v[32];
+          tmem_ld32(trow + c * 32, v);
+          const int buf = nchunk & 1;
+          uint8_t* sb = bufs + buf * kEpiBuf;
+          // next chunk's residual into the other buffer, once its last store has read it
+          if (lead) {
+            bulk_wait_read<0>();
+            if (chunk_at(c + 2 < BN / 32 ? t : t + gridDim.x, c + 2 < BN / 32 ? c + 2 : half, nr0,
+                         nc0)) {
+              mbar_arrive_expect_tx(&rb[buf ^ 1], 32 * 32 * sizeof(TY));
+              tma_load_2d(bufs + (buf ^ 1) * kEpiBuf, &tmR, &rb[buf ^ 1], nc0, nr0);
+            }
+          }
+          tmem_ld_wait();
+          const float sc = __fmul_rn(deq, msc0);
+          float o[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float x = __fmul_rn(i2f_small((int)v[j] - qsum), sc);
+            if (e.bias) x = __fadd_rn(x, __ldg(e.bias + col0 + j));
+            o[j] = storage_round<TY>(x);
+          }
+          mbar_wait(&rb[buf], rphase[buf]);
+          rphase[buf] ^= 1;
+          float xr[32];
+          stg_read_row<TY>(sb, lane, xr);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __fadd_rn(xr[j], o[j]);
+          __syncwarp();   // all lanes read their residual rows before they are overwritten
+          stg_write_row<TY>(sb, lane, o);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lead) {
+            tma_store_2d(&tmO, sb, col0, row0);   // rows >= M / cols >= n clipped by TMA
+            bulk_commit();
+          }
+          ++nchunk;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lead) mbar_arrive(&tempty[acc]);
+      }
+    }
+    for (int t = blockIdx.x; t < (RES ? 0 : total); t += gridDim.x, ++it) {
       const uint32_t acc = it & 1;
       const int tile = t / a.ksplit;
       const int m0 = (tile / a.n_tiles) * kBM, n0 = (tile % a.n_tiles) * BN;
@@ -544,11 +628,11 @@ bool make_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uin
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool kPre, typename TY>
+template <int BN, bool kPre, typename TY, bool RES = false>
 static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
                                const CUtensorMap& tr, const GemmArgs& a, cudaStream_t s) {
-  using Cfg = GemmCfg<BN, kPre>;
-  auto kern = k_gemm_tc<BN, kPre, TY>;
+  using Cfg = GemmCfg<BN, kPre, RES>;
+  auto kern = k_gemm_tc<BN, kPre, TY, RES>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -596,6 +680,13 @@ template <bool kPre, typename TY>
 static cudaError_t gemm_dispatch_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb,
                                     const CUtensorMap& to, const CUtensorMap& tr,
                                     const GemmArgs& a, cudaStream_t s) {
+  // the residual-prefetch epilogue (GemmCfg RES) for the u8 256-wide residual GEMMs
+  static const int res_on = getenv("TERN_GEMM_RES") ? atoi(getenv("TERN_GEMM_RES")) : 1;   // debug
+  // (short K only: with K >= 2816 the 4th ring stage matters more -- measured c2 o 49.0 ->
+  // 37.7 us, c3 o 141 -> 124 us; c2 down 57.7 -> 61.9 us with it, so down keeps S = 4)
+  if (BN == 256 && kPre && res_on && a.epi.kind == EPI_RESID && a.epi.acc == nullptr &&
+      a.part == nullptr && a.ksplit == 1 && a.num_kb <= 16)
+    return gemm_launch<256, kPre, TY, true>(ta, tb, to, tr, a, s);
   return BN == 256 ? gemm_launch<256, kPre, TY>(ta, tb, to, tr, a, s)
                    : gemm_launch<128, kPre, TY>(ta, tb, to, tr, a, s);
 }
