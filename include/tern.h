@@ -210,7 +210,21 @@ typedef struct {
   tern_gate_mode gate;
   float eps;
   tern_norm_mode norm;              /* of both BitLinears' inputs (0: RMSNorm) */
+  /* Prefill scan over time ("parallel scan"; reading C23): 1 = the exact sequential
+   * recurrence (bit-identical to the definition); 4 = the chunked scan: each channel's
+   * sequence is cut into 4 contiguous chunks [j T/4, (j+1) T/4) scanned concurrently
+   * from their composed boundary states (chunk aggregates A = prod f, B = the recurrence
+   * from 0, composed in order) -- equal to the oracle's 4-slice composition
+   * (O.scan_slices(4)) and within reading S4's tolerance of the sequential scan; 0 = auto,
+   * currently 1: the chunked kernel measured slower than the sequential one at every
+   * few-sequence config.  Other values: TERN_ERR_UNSUPPORTED.
+   * tern_mlgru_chunks() reports the resolved value. */
+  int32_t num_chunks;
 } tern_mlgru;
+
+/* The scan chunk count mlgru_fwd / block_prefill will use for B sequences of T tokens
+ * (host helper; resolves num_chunks = 0). */
+int32_t tern_mlgru_chunks(const tern_mlgru* p, int32_t B, int32_t T, int32_t d);
 
 typedef struct {
   tern_weight gu, down;

@@ -40,7 +40,8 @@ class tern_bl_taps(C.Structure):
 class tern_mlgru(C.Structure):
     _fields_ = [("fcg", tern_weight), ("o", tern_weight), ("gain_x", C.c_void_p),
                 ("gain_o", C.c_void_p), ("bias_fcg", C.c_void_p), ("bias_o", C.c_void_p),
-                ("gate", C.c_int), ("eps", C.c_float), ("norm", C.c_int)]
+                ("gate", C.c_int), ("eps", C.c_float), ("norm", C.c_int),
+                ("num_chunks", C.c_int32)]
 
 
 class tern_glu(C.Structure):
@@ -104,6 +105,7 @@ _SIGS = {
     "tern_contract": (C.c_int, [P, I32, I32, P, C.POINTER(tern_weight), P, I32, P]),
     "tern_mlgru_scan": (C.c_int, [P, C.c_int, I32, I32, I32, C.c_int, P, P, P]),
     "tern_mlgru_workspace": (SZ, [C.POINTER(tern_mlgru), I32, I32, I32, C.c_int]),
+    "tern_mlgru_chunks": (I32, [C.POINTER(tern_mlgru), I32, I32, I32]),
     "tern_glu_workspace": (SZ, [C.POINTER(tern_glu), I32, I32, I32, C.c_int]),
     "tern_block_workspace": (SZ, [C.POINTER(tern_block), I32, I32, C.c_int]),
     "tern_block_ws_layout": (C.c_int, [C.POINTER(tern_block), I32, I32, C.c_int,

@@ -169,6 +169,10 @@ cudaError_t launch_fxp_combine(const int32_t* acc_hi, const int32_t* acc_lo, int
 cudaError_t launch_fxp_rmsnorm(const int16_t* xq, const int32_t* ex, const int8_t* wq, int ew,
                                double eps, int rows, int d, int16_t* out, int32_t* eo,
                                cudaStream_t s);
+// chunked prefill scan (tern_mlgru.num_chunks, reading C23): resolve 0 = auto to 1 or 4
+int scan_chunks_resolve(int num_chunks, int B, int T, int d);
+cudaError_t launch_scan_chunks(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
+                               void* oprime, int chunks, cudaStream_t s);
 cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
                         void* oprime, cudaStream_t s);
 

@@ -319,6 +319,244 @@ static cudaError_t scan_go(const void* fcg, int B, int T, int d, int gate, float
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- chunked scan (num_chunks > 1)
+// Few long sequences (B * d / 8 CTAs do not fill the SMs, e.g. B = 1): the recurrence of
+// every channel is cut into NCH = 4 contiguous time chunks [j T / 4, (j+1) T / 4) that run
+// CONCURRENTLY on the 32 lanes of the carry warp (lane = chunk * 8 + channel), so each lane
+// walks a quarter of the sequence ("the linear recurrence ... allows a parallel
+// scan"; reading C23 fixes the composition):
+//   pass A  the carry runs each chunk from h = 0 and the running product of f: the chunk
+//           aggregate (A_j, B_j) with A = A f, B = f B + b (left to right);
+//   compose h_in(0) = h, h_in(j+1) = A_j h_in(j) + B_j over the chunks in order (shuffles
+//           within the carry warp); the state after the sequence is h_in(4);
+//   pass B  the exact sequential scan of each chunk from h_in(j), with the gates' output
+//           o' = g sigma(h) (or g h) -- bit-identical to the oracle's O.scan_slices(4).
+// A pipeline stage holds one round: time tile r (128 steps x 8 channels) of all 4 chunks;
+// the gates compute (f, (1-f) SiLU(c)) of a round in both passes (5 sigmoids per element
+// in total instead of 3: the carry chain, not the gate arithmetic, bounds a CTA here).
+constexpr int kChN = 4;            // chunks
+constexpr int kChC = 8;            // channels per CTA
+constexpr int kChTS = kTE / kChC;  // 128 steps per tile
+constexpr int kChS = 2;            // ring stages (rounds)
+
+template <typename T>
+struct ChunkSmem {
+  T in[kChS][kChN][3][kTE];                 // f^, c^, g^ boxes [kChTS][kChC] per chunk
+  __align__(16) float fb[kChS][kChN][2 * kTE];
+  __align__(16) float hs[kChS][kChN][kTE];
+  uint64_t full[kChS], gated[kChS], scanned[kChS], empty[kChS];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kScanThreads) k_scan_chunked(const __grid_constant__ CUtensorMap tmX,
+                                                               int B, int T_, int d, int gate,
+                                                               float* __restrict__ h,
+                                                               T* __restrict__ oprime) {
+  extern __shared__ __align__(128) uint8_t scan_smem[];
+  ChunkSmem<T>& sm = *reinterpret_cast<ChunkSmem<T>*>(scan_smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cpb = d / kChC;
+  const int b = blockIdx.x / cpb;
+  const int c0 = (blockIdx.x % cpb) * kChC;
+  const int colf = (c0 / kSegRows) * (3 * kSegRows) + (c0 % kSegRows);
+  // chunk j = steps [t0(j), t0(j+1)); rounds per pass = tiles of the longest chunk
+  auto t0 = [&](int j) { return (int)((int64_t)j * T_ / kChN); };
+  const int R = (t0(1) - t0(0) > t0(kChN) - t0(kChN - 1) ? t0(1) - t0(0) : t0(kChN) - t0(kChN - 1)) +
+                kChTS - 1;
+  const int nr = R / kChTS;          // rounds per pass
+  const int n_seq = 2 * nr;          // pass A rounds, then pass B rounds
+  auto steps_of = [&](int j, int r) {   // valid steps of chunk j's tile r
+    const int left = t0(j + 1) - t0(j) - r * kChTS;
+    return left < 0 ? 0 : (left > kChTS ? kChTS : left);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kChS; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.gated[s], kGateWarps);
+      mbar_init(&sm.scanned[s], 1);
+      mbar_init(&sm.empty[s], kGateWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    // ---------------- producer: one round = the r-th tile of every chunk (pass A: f^, c^;
+    // pass B: f^, c^, g^); tiles past a chunk's end are not loaded
+    if (lane == 0) {
+      tma_prefetch_desc(&tmX);
+      for (int i = 0; i < n_seq; ++i) {
+        const int s = i % kChS, r = i % nr;
+        const bool passB = i >= nr;
+        if (i >= kChS) mbar_wait(&sm.empty[s], ((i / kChS) - 1) & 1);
+        const int nbox = passB ? 3 : 2;
+        int ntile = 0;
+        for (int j = 0; j < kChN; ++j) ntile += steps_of(j, r) > 0;
+        mbar_arrive_expect_tx(&sm.full[s], (uint32_t)(ntile * nbox * kTE * sizeof(T)));
+        for (int j = 0; j < kChN; ++j) {
+          if (steps_of(j, r) == 0) continue;
+          const int row = b * T_ + t0(j) + r * kChTS;
+          for (int g = 0; g < nbox; ++g)
+            tma_load_2d(&sm.in[s][j][g][0], &tmX, &sm.full[s], colf + g * kSegRows, row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- the carry: lane = chunk j * 8 + channel c
+    const int j = lane / kChC, c = lane % kChC;
+    float hc = 0.0f, Ac = 1.0f;
+    for (int i = 0; i < n_seq; ++i) {
+      const int s = i % kChS, r = i % nr;
+      const bool passB = i >= nr;
+      if (i == nr) {
+        // compose the chunk aggregates in chunk order (reading C23): h_in(j) for this lane,
+        // and the state after the whole sequence
+        float hin = h[(int64_t)b * d + c0 + c], mine = hin;
+#pragma unroll
+        for (int k = 0; k < kChN; ++k) {
+          const float A = __shfl_sync(0xffffffffu, Ac, k * kChC + c);
+          const float Bv = __shfl_sync(0xffffffffu, hc, k * kChC + c);
+          if (k == j) mine = hin;
+          hin = __fadd_rn(__fmul_rn(A, hin), Bv);
+        }
+        if (j == 0) h[(int64_t)b * d + c0 + c] = hin;
+        hc = mine;
+      }
+      mbar_wait(&sm.gated[s], (i / kChS) & 1);
+      const int steps = steps_of(j, r);
+      const float4* __restrict__ fb4 = reinterpret_cast<const float4*>(sm.fb[s][j]) + c;
+      float4* __restrict__ hs4 = reinterpret_cast<float4*>(sm.hs[s][j]) + c;
+      if (__all_sync(0xffffffffu, steps == kChTS)) {
+        constexpr int kG = kChTS / 4;   // groups of 4 steps; (f, b) loaded 2 groups ahead
+        float4 pf[kG], qf[kG];
+        pf[0] = fb4[0], qf[0] = fb4[kChC];
+        pf[1] = fb4[2 * kChC], qf[1] = fb4[3 * kChC];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          if (g + 2 < kG) pf[g + 2] = fb4[(2 * g + 4) * kChC], qf[g + 2] = fb4[(2 * g + 5) * kChC];
+          const float4 p = pf[g], q = qf[g];
+          float4 o;
+          o.x = __fadd_rn(__fmul_rn(p.x, hc), p.y);
+          o.y = __fadd_rn(__fmul_rn(p.z, o.x), p.w);
+          o.z = __fadd_rn(__fmul_rn(q.x, o.y), q.y);
+          o.w = __fadd_rn(__fmul_rn(q.z, o.z), q.w);
+          if (passB) hs4[g * kChC] = o;
+          else Ac = __fmul_rn(__fmul_rn(__fmul_rn(__fmul_rn(Ac, p.x), p.z), q.x), q.z);
+          hc = o.w;
+        }
+      } else {
+        for (int t = 0; t < steps; ++t) {
+          const int e = t * kChC + c;
+          const float* fbw = &sm.fb[s][j][fb_word<kChC>(e)];
+          hc = __fadd_rn(__fmul_rn(fbw[0], hc), fbw[1]);
+          if (passB) sm.hs[s][j][h_word<kChC>(e)] = hc;
+          else Ac = __fmul_rn(Ac, fbw[0]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.scanned[s]);
+    }
+  } else if (gate_warp_index(warp) >= 0) {
+    // ---------------- gate warps: element e = (gw*4 + k)*32 + lane of each chunk's tile
+    const int gw = gate_warp_index(warp);
+    const int cl = lane % kChC;
+    T* obase = oprime + (int64_t)b * T_ * d + c0 + cl;
+    auto phase1 = [&](int i) {   // (f, (1-f) SiLU(c)) of round i
+      const int s = i % kChS, r = i % nr;
+      mbar_wait(&sm.full[s], (i / kChS) & 1);
+#pragma unroll 1
+      for (int j = 0; j < kChN; ++j) {
+        if (steps_of(j, r) == 0) continue;
+        float fv[kElemsPerLane], bvv[kElemsPerLane];
+#pragma unroll
+        for (int k = 0; k < kElemsPerLane; ++k) {
+          const int e = (gw * kElemsPerLane + k) * 32 + lane;
+          const float fx = ld_act<T>(&sm.in[s][j][0][e]);
+          const float cx = ld_act<T>(&sm.in[s][j][1][e]);
+          float f, sc;
+          sigmoid2(fx, cx, f, sc);
+          fv[k] = f;
+          bvv[k] = __fmul_rn(__fsub_rn(1.0f, f), __fmul_rn(cx, sc));   // (1-f) SiLU(c)
+        }
+#pragma unroll
+        for (int k = 0; k < kElemsPerLane; ++k) {
+          const int e = (gw * kElemsPerLane + k) * 32 + lane;
+          *reinterpret_cast<float2*>(&sm.fb[s][j][fb_word<kChC>(e)]) = make_float2(fv[k], bvv[k]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.gated[s]);
+    };
+    auto phase3 = [&](int i) {   // pass B: o' = g sigma(h) or g h, valid steps only
+      const int s = i % kChS, r = i % nr;
+      mbar_wait(&sm.scanned[s], (i / kChS) & 1);
+      if (i >= nr) {
+        const bool sig = gate == TERN_GATE_SIGMOID_H;
+#pragma unroll 1
+        for (int j = 0; j < kChN; ++j) {
+          const int steps = steps_of(j, r);
+          if (steps == 0) continue;
+          float ov[kElemsPerLane];
+#pragma unroll
+          for (int k = 0; k < kElemsPerLane; k += 2) {
+            const int e = (gw * kElemsPerLane + k) * 32 + lane;
+            const float g0 = ld_act<T>(&sm.in[s][j][2][e]), g1 = ld_act<T>(&sm.in[s][j][2][e + 32]);
+            const float h0 = sm.hs[s][j][h_word<kChC>(e)], h1 = sm.hs[s][j][h_word<kChC>(e + 32)];
+            if (sig) {
+              float s0, s1;
+              sigmoid2(h0, h1, s0, s1);
+              ov[k] = __fmul_rn(g0, s0);
+              ov[k + 1] = __fmul_rn(g1, s1);
+            } else {
+              ov[k] = __fmul_rn(g0, h0);
+              ov[k + 1] = __fmul_rn(g1, h1);
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < kElemsPerLane; ++k) {
+            const int tl = ((gw * kElemsPerLane + k) * 32 + lane) / kChC;
+            if (tl < steps) st_act<T>(obase + (int64_t)(t0(j) + r * kChTS + tl) * d, ov[k]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+    };
+    // phase 1 of round i runs before phase 3 of round i-1, so the carry finds a gated round
+    // while the gates wait for its previous one (2 stages: round i+1 refills the stage that
+    // phase 3 of round i-1 released)
+    for (int i = 0; i < n_seq; ++i) {
+      phase1(i);
+      if (i >= 1) phase3(i - 1);
+    }
+    if (n_seq > 0) phase3(n_seq - 1);
+  }
+}
+
+template <typename TE>
+static cudaError_t scan_chunked_go(const void* fcg, int B, int T, int d, int gate, float* h,
+                                   void* oprime, cudaStream_t s) {
+  static bool attr = false;
+  const size_t smem = sizeof(ChunkSmem<TE>);
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan_chunked<TE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const bool bf = sizeof(TE) == 2;
+  CUtensorMap tm;
+  if (!make_map_2d(&tm, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, fcg,
+                   (uint64_t)3 * d, (uint64_t)B * T, (uint64_t)3 * d * sizeof(TE), kChC, kChTS,
+                   CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  return launch_pdl(k_scan_chunked<TE>, dim3(B * (d / kChC)), dim3(kScanThreads), smem, s, tm, B, T, d,
+                    gate, h, static_cast<TE*>(oprime));
+}
+
 static int scan_num_sms() {
   static int n = 0;
   if (!n) {
@@ -358,6 +596,28 @@ static cudaError_t scan_pick(const void* fcg, int B, int T, int d, int gate, flo
   if (kc == 16) return TERN_SCAN_GO(kSShallow, 16);
   return TERN_SCAN_GO(kSShallow, 32);
 #undef TERN_SCAN_GO
+}
+
+// num_chunks (tern_mlgru.num_chunks): 1 = the exact sequential scan; 4 = the chunked scan
+// (reading C23); 0 = auto = 1: the chunked kernel measured SLOWER than the sequential one at
+// every few-sequence shape (c2 B = 1 x 2048: 33.3 vs 21.2 us; c3 61.9 vs 31.2; c4 B = 1 x 4096:
+// 180.7 vs 75.8 us, tools/scan_chunk_bench.py) -- the sequential kernel is bound by its gate
+// arithmetic and pipeline, not by the carry chain, and the chunked one computes the gates of
+// f and c twice (5 sigmoids per element instead of 3)
+int scan_chunks_resolve(int num_chunks, int B, int T, int d) {
+  (void)B;
+  (void)T;
+  if (num_chunks == kChN && d % kChC == 0) return kChN;
+  return 1;
+}
+
+cudaError_t launch_scan_chunks(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
+                               void* oprime, int chunks, cudaStream_t s) {
+  if (B == 0 || T == 0) return cudaSuccess;
+  if (chunks == kChN)
+    return dt == TERN_BF16 ? scan_chunked_go<__nv_bfloat16>(fcg, B, T, d, gate, h, oprime, s)
+                           : scan_chunked_go<float>(fcg, B, T, d, gate, h, oprime, s);
+  return launch_scan(fcg, dt, B, T, d, gate, h, oprime, s);
 }
 
 cudaError_t launch_scan(const void* fcg, int dt, int B, int T, int d, int gate, float* h,

@@ -54,11 +54,12 @@ class Block:
 
     def __init__(self, latent: dict, d: int, l: int, gate=L.TERN_GATE_SIGMOID_H, eps=1e-6,
                  gains: dict | None = None, biases: dict | None = None, device="cuda",
-                 shard=None, norm=L.TERN_NORM_RMS):
+                 shard=None, norm=L.TERN_NORM_RMS, num_chunks: int = 0):
         """shard = (rank, AllGather[, gather_q[, megatron]]) for a sharded block (shard.py);
         latent holds the FULL matrices, gains/biases this rank's slices.  norm: the
         norm in front of every BitLinear (TERN_NORM_RMS, or TERN_NORM_CENTERED =
-        Alg. 1's centred form)."""
+        Alg. 1's centred form).  num_chunks: the prefill scan over time (tern.h
+        tern_mlgru.num_chunks: 0 auto, 1 exact sequential, 4 chunked, reading C23)."""
         self.d, self.l = d, l
         dev = torch.device(device)
         lat = {k: v.to(dev) for k, v in latent.items()}
@@ -99,7 +100,7 @@ class Block:
             bias_fcg = torch.cat([biases.get(k, z).float().cpu() for k in ("f", "c", "g")])
         self.mix = L.tern_mlgru(self.fcg.struct, self.o.struct, dp(gains.get("x")),
                                 dp(gains.get("o")), dp(bias_fcg), dp(biases.get("o")), int(gate),
-                                float(eps), int(norm))
+                                float(eps), int(norm), int(num_chunks))
         self.ch = L.tern_glu(self.gu.struct, self.down.struct, dp(gains.get("x1")),
                              dp(gains.get("p")), float(eps), int(norm))
         self.struct = L.tern_block(self.mix, self.ch, d, l)
@@ -110,6 +111,10 @@ class Block:
     @property
     def weight_bytes(self) -> int:
         return sum(w.nbytes for w in (self.fcg, self.o, self.gu, self.down))
+
+    def scan_chunks(self, B: int, T: int) -> int:
+        """The prefill scan's chunk count for B x T (1 = exact sequential; tern_mlgru_chunks)."""
+        return int(L.load().tern_mlgru_chunks(C.byref(self.mix), B, T, self.d))
 
     def workspace_bytes(self, B: int, T: int, dtype: torch.dtype) -> int:
         return int(L.load().tern_block_workspace(C.byref(self.struct), B, T, L.dtype_code(dtype)))
@@ -144,7 +149,7 @@ class Stack:
 
     @classmethod
     def random(cls, cfg: synth.Config, device="cuda", gate=L.TERN_GATE_SIGMOID_H, n_blocks=None,
-               gen_device=None, keep_latents=0, shard=None, norm=L.TERN_NORM_RMS):
+               gen_device=None, keep_latents=0, shard=None, norm=L.TERN_NORM_RMS, num_chunks=0):
         """Build cfg's stack from seeded N(0, 0.02) latents (drawn per block on
         gen_device, packed on the GPU and dropped).  keep_latents=n keeps the
         first n blocks' latents on the host (for oracle parity)."""
@@ -156,7 +161,7 @@ class Stack:
             if i < keep_latents:
                 kept.append({k: v.cpu() for k, v in lat.items()})
             blocks.append(Block(lat, cfg.d, cfg.l, gate=gate, eps=cfg.eps, device=device,
-                                shard=shard, norm=norm))
+                                shard=shard, norm=norm, num_chunks=num_chunks))
             del lat
         st = cls(blocks, cfg.d, cfg.l, synth.torch_dtype(cfg.dtype), device)
         st.gather = None if shard is None else shard[1]
