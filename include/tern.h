@@ -529,6 +529,11 @@ int32_t tern_get_batched_fin(void);
  * Results are identical (integer sums).  Initial value: env TERN_GEMM_SAB, else 0. */
 void tern_set_gemm_sab(int32_t on);
 int32_t tern_get_gemm_sab(void);
+/* Tuning knob (host): 1 (default) runs large-M GEMMs with the u8 weight copy and K >= 2048
+ * on CTA pairs (tcgen05.mma.cta_group::2, 256 x 256 tiles, k_gemm_2sm); 0 always on single
+ * CTAs (128 x 256 tiles).  Results are identical.  Initial value: env TERN_GEMM_2SM, else 1. */
+void tern_set_gemm_2sm(int32_t on);
+int32_t tern_get_gemm_2sm(void);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -128,6 +128,8 @@ _SIGS = {
     "tern_get_fused_scan": (I32, []),
     "tern_set_batched_fin": (None, [I32]),
     "tern_set_gemm_sab": (None, [I32]),
+    "tern_set_gemm_2sm": (None, [I32]),
+    "tern_get_gemm_2sm": (I32, []),
     "tern_get_gemm_sab": (I32, []),
     "tern_set_norm_mode": (None, [C.c_int]),
     "tern_get_norm_mode": (C.c_int, []),
@@ -330,6 +332,14 @@ def tern_set_batched_fin(on: bool):
 
 def tern_set_gemm_sab(on: bool):
     load().tern_set_gemm_sab(1 if on else 0)
+
+
+def tern_set_gemm_2sm(on: bool):
+    load().tern_set_gemm_2sm(1 if on else 0)
+
+
+def tern_get_gemm_2sm() -> bool:
+    return bool(load().tern_get_gemm_2sm())
 
 
 def tern_get_gemm_sab() -> bool:

@@ -321,6 +321,8 @@ void tern_set_gemv_max_m(int32_t m) { g_gemv_max_m = m < 0 ? 0 : (m > kGemvMaxM 
 int32_t tern_get_gemv_max_m(void) { return g_gemv_max_m; }
 void tern_set_batched_fin(int32_t on) { g_batched_fin = on ? 1 : 0; }
 void tern_set_gemm_sab(int32_t on) { g_gemm_sab = on ? 1 : 0; }
+void tern_set_gemm_2sm(int32_t on) { g_gemm_2sm = on ? 1 : 0; }
+int32_t tern_get_gemm_2sm(void) { return g_gemm_2sm; }
 int32_t tern_get_gemm_sab(void) { return g_gemm_sab; }
 void tern_set_norm_mode(tern_norm_mode mode) {
   g_norm_mode = mode == TERN_NORM_CENTERED ? TERN_NORM_CENTERED : TERN_NORM_RMS;

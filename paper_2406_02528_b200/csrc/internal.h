@@ -72,6 +72,7 @@ cudaError_t launch_gemv(const void* x, int xdt, int ydt, int M, int K, int ldx, 
 // part[ks][M][n_rows] from the 2-bit codes; *ks_out = slices used
 bool gemm_sab_supported(int M);
 extern int g_gemm_sab;   // tern_set_gemm_sab
+extern int g_gemm_2sm;   // tern_set_gemm_2sm
 cudaError_t launch_gemm_sab(const int8_t* q, int M, int ldq, const tern_weight& w, int32_t* part,
                             size_t part_bytes, int ks_max, int* ks_out, cudaStream_t s);
 cudaError_t launch_splitk_epi(const int32_t* part, int ks, int M, int n_rows, const float* deq,

@@ -594,6 +594,293 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 8 + 7] = clock64() - t_start;
 }
 
+// ----------------------------------------------------------------- 2-SM tiles (cta_group::2)
+// A CTA pair (a cluster of 2 on one TPC) computes a 256 x 256 output tile: each CTA loads
+// its own 128 rows of A (q) and its 128-row half of B (the u8 weights) per k-block, the
+// leader issues tcgen05.mma.cta_group::2 (M = 256, N = 256) reading both CTAs' shared
+// memory, and the accumulator rows land in each CTA's own TMEM.  Per CTA and k-block that
+// is 32 KB of TMA writes and 32 KB of MMA operand reads instead of 48 + 48 KB for a 1-CTA
+// 128 x 256 tile -- shared-memory bandwidth is the binding resource of these GEMMs
+// (TERN_GEMM_PROF: the MMA of a 1-CTA c2 tile takes ~3x its issue time) -- and the freed
+// space buys a 6-stage ring.  Barriers: the k-block "full" barrier lives in the leader and
+// counts one arrival (with its transaction bytes) per CTA, both CTAs' TMA loads complete on
+// it; "empty" and "accumulator full" are signalled to both CTAs by multicast commits;
+// "accumulator empty" lives in the leader and counts the 8 drain warps of both CTAs.
+constexpr int kS2 = 6;
+constexpr int k2Tile = 128 * kBK;   // A or B half-tile bytes per CTA per stage
+constexpr int k2Smem = kS2 * 2 * k2Tile + kEpiWarps * kEpiBuf + 1024 + 512;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void cl_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cl_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cl_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// TMA load into this CTA's shared memory completing on an mbarrier of the pair (the leader's)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, uint32_t bar, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit of the pair's MMAs, arriving on the barrier at this offset in BOTH CTAs
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <typename TY>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
+               const GemmArgs a) {
+  extern __shared__ __align__(1024) uint8_t gsm_raw[];
+  uint8_t* sm = gsm_raw + ((1024u - (smem_u32(gsm_raw) & 1023u)) & 1023u);
+  uint8_t* sA = sm;                          // [kS2][16 KB] this CTA's 128 rows of A (SW128)
+  uint8_t* sB = sA + kS2 * k2Tile;           // [kS2][16 KB] this CTA's half of B (SW128)
+  uint8_t* sEpi = sB + kS2 * k2Tile;         // [8 warps][4 KB] staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kEpiWarps * kEpiBuf);
+  uint64_t* full = bars;          // [kS2] (the leader's is the one used)
+  uint64_t* empty = bars + 8;     // [kS2]
+  uint64_t* tfull = bars + 16;    // [2]
+  uint64_t* tempty = bars + 18;   // [2] (the leader's)
+  uint64_t* rbar = bars + 20;     // [8 warps] residual tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int total = a.n_tiles * a.m_tiles;   // 256 x 256 tiles
+  const int nk = a.num_kb;
+  const Epi& e = a.epi;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmO);
+    for (int s = 0; s < kS2; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kEpiWarps);
+    }
+    for (int i = 0; i < kEpiWarps; ++i) mbar_init(&rbar[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();   // both CTAs' barriers initialised before any remote arrival
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (warp != 0) pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs): own A rows, own half of B
+    if (lane == 0) {
+      auto fullL = [&](int s) { return mapa_rank(&full[s], 0); };
+      uint32_t npre = 0;
+      if (cid < total) {   // weights of the first stages before the dependency wait
+        const int n0 = (cid % a.n_tiles) * 256 + (int)rank * 128;
+        for (int kb = 0; kb < nk && npre < (uint32_t)kS2; ++kb, ++npre) {
+          cl_expect_tx(fullL((int)npre), k2Tile);
+          tma_load_2d_pair(sB + npre * k2Tile, &tmB, fullL((int)npre), kb * kBK, n0);
+        }
+      }
+      pdl_wait();
+      uint32_t g = 0;
+      for (int t = cid; t < total; t += ncl) {
+        const int m0 = (t / a.n_tiles) * 256 + (int)rank * 128;
+        const int n0 = (t % a.n_tiles) * 256 + (int)rank * 128;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % kS2;
+          if (g >= (uint32_t)kS2) mbar_wait(&empty[s], ((g / kS2) - 1) & 1);
+          if (g < npre) {
+            cl_arrive_expect_tx(fullL(s), k2Tile);
+            tma_load_2d_pair(sA + s * k2Tile, &tmA, fullL(s), kb * kBK, m0);
+          } else {
+            cl_arrive_expect_tx(fullL(s), 2 * k2Tile);
+            tma_load_2d_pair(sA + s * k2Tile, &tmA, fullL(s), kb * kBK, m0);
+            tma_load_2d_pair(sB + s * k2Tile, &tmB, fullL(s), kb * kBK, n0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (the leader's lane 0)
+    if (leader && lane == 0) {
+      // kind::i8: D s32, A s8, B u8, both K-major, M = 256 (the pair), N = 256
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (0u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+      uint32_t g = 0, it = 0;
+      for (int t = cid; t < total; t += ncl, ++it) {
+        const uint32_t acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_addr = tmem_base + acc * 256;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % kS2;
+          mbar_wait(&full[s], (g / kS2) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + s * k2Tile), b_addr = smem_u32(sB + s * k2Tile);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 32; ++kk)
+            mma_i8_pair(d_addr, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                        idesc, (kb | kk) != 0);
+          mma_commit_pair(&empty[s]);
+        }
+        mma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ---------------- epilogue (warps 6-13 of both CTAs): this CTA's 128 rows x 256 columns
+    const int ew = warp - kEpiWarp0;
+    const int quad = warp & 3;
+    const int half = ew >> 2;
+    uint8_t* sb = sEpi + ew * kEpiBuf;
+    uint64_t* rb = rbar + ew;
+    const bool lead = lane == 0;
+    const int nseg = e.n_seg;
+    const float msc0 = __ldg(e.scales), msc1 = nseg > 1 ? __ldg(e.scales + 1) : 0.0f;
+    const float msc2 = nseg > 2 ? __ldg(e.scales + 2) : 0.0f;
+    const uint32_t temptyL = mapa_rank(&tempty[0], 0);
+    uint32_t it = 0, rphase = 0;
+    for (int t = cid; t < total; t += ncl, ++it) {
+      const uint32_t acc = it & 1;
+      const int m0 = (t / a.n_tiles) * 256 + (int)rank * 128, n0 = (t % a.n_tiles) * 256;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row0 = m0 + quad * 32;
+      const int row = row0 + lane;
+      const bool rv = row < a.M;
+      const float deq = rv ? __ldg(a.deq + row) : 0.0f;
+      const int qsum = rv ? __ldg(a.qsum + row) : 0;
+      const uint32_t trow = tmem_base + acc * 256 + ((uint32_t)(quad * 32) << 16);
+      const bool swig = e.kind == EPI_SWIGLU;
+      const int nch = swig ? 256 / 64 : 256 / 32;
+#pragma unroll 1
+      for (int c = half; c < nch; c += 2) {
+        int col0, out_col0;
+        if (swig) {
+          col0 = n0 + (c >> 1) * 128 + (c & 1) * 32;
+          out_col0 = (col0 / 128) * 64 + (c & 1) * 32;
+        } else {
+          col0 = n0 + c * 32;
+          out_col0 = e.kind == EPI_FCG ? col0 : (col0 / (kSegRows * nseg)) * kSegRows + (col0 % kSegRows);
+        }
+        if (col0 >= a.n_rows || (swig && out_col0 >= e.n_out)) continue;
+        uint32_t v[32], vu[32];
+        tmem_ld32(trow + (col0 - n0), v);
+        if (swig) tmem_ld32(trow + (col0 - n0) + 64, vu);
+        if (lead) bulk_wait_read<0>();   // the staging tile's last store has read it
+        __syncwarp();
+        const bool resid = e.kind == EPI_RESID;
+        if (resid && lead) {
+          mbar_arrive_expect_tx(rb, 32 * 32 * sizeof(TY));
+          tma_load_2d(sb, &tmR, rb, out_col0, row0);
+        }
+        tmem_ld_wait();
+        const int seg = (col0 / kSegRows) % nseg;
+        const int rr0 = (col0 / (kSegRows * nseg)) * kSegRows + (col0 % kSegRows);
+        const float msc = seg == 0 ? msc0 : (seg == 1 ? msc1 : msc2);
+        const float sc = __fmul_rn(deq, msc);
+        float o[32];
+        if (swig) {
+          const float scu = __fmul_rn(deq, msc1);
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float g0 = storage_round<TY>(__fmul_rn(i2f_small((int)v[j] - qsum), sc));
+            const float g1 = storage_round<TY>(__fmul_rn(i2f_small((int)v[j + 1] - qsum), sc));
+            const float u0 = storage_round<TY>(__fmul_rn(i2f_small((int)vu[j] - qsum), scu));
+            const float u1 = storage_round<TY>(__fmul_rn(i2f_small((int)vu[j + 1] - qsum), scu));
+            float s0, s1;
+            sigmoid2(g0, g1, s0, s1);
+            o[j] = __fmul_rn(__fmul_rn(g0, s0), u0);   // SwiGLU p = SiLU(g) u
+            o[j + 1] = __fmul_rn(__fmul_rn(g1, s1), u1);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float x = __fmul_rn(i2f_small((int)v[j] - qsum), sc);
+            if (e.bias) x = __fadd_rn(x, __ldg(e.bias + seg * e.n_out + rr0 + j));
+            o[j] = storage_round<TY>(x);
+          }
+        }
+        if (resid) {
+          mbar_wait(rb, rphase);
+          rphase ^= 1;
+          float xr[32];
+          stg_read_row<TY>(sb, lane, xr);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __fadd_rn(xr[j], o[j]);
+          __syncwarp();
+        }
+        stg_write_row<TY>(sb, lane, o);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lead) {
+          tma_store_2d(&tmO, sb, out_col0, row0);   // rows >= M / cols >= n clipped by TMA
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lead) cl_arrive(temptyL + acc * 8);   // the leader's tempty[acc]
+    }
+    if (lead) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();   // the pair is done with TMEM and with each other's barriers
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
+                 : "memory");
+  }
+}
+
 // ----------------------------------------------------------------- host side
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -674,6 +961,42 @@ static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, con
             sum[1], sum[2], sum[3], sum[4], sum[5]);
   }
   return cudaGetLastError();
+}
+
+template <typename TY>
+static cudaError_t gemm2_launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
+                                const CUtensorMap& tr, const GemmArgs& a, cudaStream_t s) {
+  auto kern = k_gemm_2sm<TY>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k2Smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int total = a.n_tiles * a.m_tiles;
+  int grid = 2 * total < num_sms ? 2 * total : num_sms;
+  grid &= ~1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = k2Smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;   // the CTA pair
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, to, tr, a);
 }
 
 template <bool kPre, typename TY>
@@ -802,6 +1125,7 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
 }
 
 int g_gemm_sab = getenv("TERN_GEMM_SAB") ? (atoi(getenv("TERN_GEMM_SAB")) != 0) : 0;
+int g_gemm_2sm = getenv("TERN_GEMM_2SM") ? (atoi(getenv("TERN_GEMM_2SM")) != 0) : 1;
 
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
@@ -920,6 +1244,22 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
                         w.n_rows, deq, qsum, epi, tr);
     return launch_pdl(k_splitk_epi<float>, dim3(grid), dim3(256), 0, s, pc, a.ksplit, M, w.n_rows,
                       deq, qsum, epi, tr);
+  }
+  // large M with the u8 weight copy and a long K loop: 256 x 256 tiles on CTA pairs
+  // (k_gemm_2sm; measured: c2 down 57.5 -> 55.5 us, c3 gate|up 538 -> 508, c3 down 253 -> 220;
+  // short-K GEMMs stay on single CTAs: c2 gate|up (K = 1024) 96 -> 108 us on pairs, and the
+  // short residual GEMMs take the residual-prefetch variant)
+  const bool res_short = epi.kind == EPI_RESID && a.num_kb <= 16;
+  if (pre && BN == 256 && g_gemm_2sm && epi.acc == nullptr && epi.kind != EPI_NONE &&
+      a.num_kb >= 16 && !res_short && M > kSmallM) {
+    CUtensorMap tb2;
+    if (!make_map_2d(&tb2, CU_TENSOR_MAP_DATA_TYPE_UINT8, w.e8, (uint64_t)kp, (uint64_t)w.n_rows,
+                     (uint64_t)kp, kBK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+    GemmArgs a2 = a;
+    a2.m_tiles = (M + 255) / 256;
+    return yb ? gemm2_launch<__nv_bfloat16>(ta, tb2, to, tr, a2, s)
+              : gemm2_launch<float>(ta, tb2, to, tr, a2, s);
   }
   if (pre)
     return yb ? gemm_dispatch_bn<true, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)

@@ -517,3 +517,46 @@ def test_c2_decode_through_all_blocks(L, M):
     assert np.array_equal(yg, yo)
     for i in range(cfg.L):
         assert np.array_equal(states[i].cpu().numpy(), Hs[i]), f"block {i} state"
+
+
+@pytest.mark.parametrize("m,k,n,dtype", [(300, 2048, 192, "f32"), (1000, 2304, 1088, "bf16"),
+                                         (257, 4096, 256, "f32")])
+def test_two_sm_gemm_parity(L, M, m, k, n, dtype):
+    """The CTA-pair GEMM (k_gemm_2sm: tcgen05.mma.cta_group::2, 256 x 256 tiles, both CTAs'
+    TMA loads completing on the leader's barrier, multicast commits) against the oracle,
+    with ragged M (not a multiple of 256), N below / not a multiple of 256 (the second CTA's
+    B half partly or wholly beyond the matrix) and K of 16..32 k-blocks."""
+    old = L.tern_get_gemm_2sm()
+    L.tern_set_gemm_2sm(True)
+    try:
+        W = latents(n, k, m)
+        pw = M.PackedWeight([W.cuda()])
+        t, mw = O.ternarize(W.numpy())
+        x = acts((m, k), m + 1, dtype)
+        y = torch.empty((m, n), dtype=synth.torch_dtype(dtype), device="cuda")
+        L.bitlinear_fwd(x.cuda(), pw.struct, y)
+        torch.cuda.synchronize()
+        assert np.array_equal(f32np(y), O.bitlinear(f32np(x), t, mw, bf16=dtype == "bf16"))
+    finally:
+        L.tern_set_gemm_2sm(old)
+
+
+@pytest.mark.parametrize("dtype,B,T,d,l", [("f32", 3, 200, 512, 2176), ("bf16", 2, 300, 2048, 704)])
+def test_two_sm_gemm_block_epilogues(L, M, dtype, B, T, d, l):
+    """The CTA-pair GEMM's residual (down, K = l > 2048) and SwiGLU (gate|up, K = d = 2048)
+    epilogues inside a block prefill, free-running against the oracle block."""
+    old = L.tern_get_gemm_2sm()
+    L.tern_set_gemm_2sm(True)
+    try:
+        cfg = synth.Config("p2", 1, d, l, dtype, 19, B, T, B, 0)
+        st = M.Stack.random(cfg, gen_device="cpu", keep_latents=1)
+        x = synth.hidden((B, T, d), synth.generator(d + l), dtype)
+        h = st.new_state(B)
+        y = st.prefill(x.cuda(), h)
+        torch.cuda.synchronize()
+        ob = O.OracleBlock({kk: v.numpy() for kk, v in st.latents[0].items()}, d, l)
+        yo, ho = O.block(ob, f32np(x), np.zeros((B, d), np.float32), bf16=dtype == "bf16")
+        assert np.array_equal(f32np(y), yo)
+        assert np.array_equal(h[0].cpu().numpy(), ho)
+    finally:
+        L.tern_set_gemm_2sm(old)
