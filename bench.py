@@ -470,8 +470,8 @@ def finish_sharded(args, cfg, rank, world, mode, st, value, ms_max, rl, kernels,
 def comm_info(world: int) -> dict:
     import torch
     info = {"world": world}
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
         info["backend"] = dist.get_backend()
         try:
             v = torch.cuda.nccl.version()

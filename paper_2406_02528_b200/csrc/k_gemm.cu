@@ -32,7 +32,7 @@ constexpr int kEpiWarps = 8;
 constexpr int kEpiBuf = 4096;  // bytes of one 32x32 staging tile (fp32)
 constexpr int kSmallM = 256;   // M at or below: packed B tiles (+ split-K when tiles are few)
 
-template <int BN, bool kPre, bool RES = false> struct GemmCfg {
+template <int BN, bool kPre, bool RES = false, int EW = kEpiWarps> struct GemmCfg {
   static constexpr int A_BYTES = kBM * kBK;        // 16 KB
   static constexpr int B_BYTES = BN * kBK;         // u8 B tile
   static constexpr int BP_BYTES = BN * (kBK / 4);  // packed B: BN rows x 8 words
@@ -42,11 +42,16 @@ template <int BN, bool kPre, bool RES = false> struct GemmCfg {
   // residual epilogue (RES), where two staging tiles per warp let each chunk's residual
   // load be issued one chunk ahead (its HBM latency otherwise serialises the drain and
   // the MMA waits on the accumulators: TERN_GEMM_PROF mma.tempty)
-  static constexpr int S = kPre ? ((RES && BN == 256) ? 3 : 4) : (BN == 256 ? 4 : 5);
+  // EW = 12 drain warps (the u8 path's idle unpack warps 2-5 join the 8 drain warps) for
+  // the SwiGLU epilogue, whose arithmetic (2 exact sigmoids per p) outlasts a K = 1024 tile's
+  // MMAs; its staging takes the 4th ring stage
+  static constexpr int S = kPre ? (((RES || EW == 12) && BN == 256) ? 3 : 4) : (BN == 256 ? 4 : 5);
   static constexpr int U = kPre ? 0 : 2;
   static constexpr int NB = (kPre && BN == 256 && !RES) ? 1 : 2;
+  static constexpr int EW0 = EW == 12 ? 2 : kEpiWarp0;   // first drain warp
+  static constexpr int NG = EW / 4;                      // drain warps per TMEM lane quadrant
   static constexpr int RING = kPre ? S * (A_BYTES + B_BYTES) : S * (A_BYTES + BP_BYTES) + U * B_BYTES;
-  static constexpr int EPI_BYTES = kEpiWarps * NB * kEpiBuf;
+  static constexpr int EPI_BYTES = EW * NB * kEpiBuf;
   static constexpr int SMEM = RING + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int TMEM_COLS = 2 * BN;
 };
@@ -167,14 +172,16 @@ __device__ void acc_tap_chunk(const Epi& e, const GemmArgs& a, int* si, int lane
   __syncwarp();
 }
 
-template <int BN, bool kPre, typename TY, bool RES = false>
+template <int BN, bool kPre, typename TY, bool RES = false, int EW = kEpiWarps>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
               const GemmArgs a) {
-  using Cfg = GemmCfg<BN, kPre, RES>;
+  using Cfg = GemmCfg<BN, kPre, RES, EW>;
+  static_assert(EW == 8 || (EW == 12 && kPre), "12 drain warps only on the u8 path");
   constexpr int S = Cfg::S;
   constexpr int U = Cfg::U;
+  constexpr int NG = Cfg::NG;
   extern __shared__ __align__(1024) uint8_t gsm_raw[];
   // 1024-byte alignment for the swizzle atoms; offset arithmetic keeps the
   // pointer in the shared address space (no generic loads/stores)
@@ -190,8 +197,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* ufree = bars + 20;           // [U] MMA finished with the unpacked B
   uint64_t* tfull = bars + 24;           // [2] accumulator ready
   uint64_t* tempty = bars + 26;          // [2] accumulator drained
-  uint64_t* rbar = bars + 28;            // [8 warps][2] residual tile landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 44);
+  uint64_t* rbar = bars + 28;            // [EW warps][2] residual tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 56);
 
   const long long t_start = clock64();
 #ifdef TERN_TRACE
@@ -216,9 +223,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
+      mbar_init(&tempty[i], EW);
     }
-    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&rbar[i], 1);
+    for (int i = 0; i < 2 * EW; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
@@ -320,7 +327,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mma_commit(&tfull[acc]);
       }
     }
-  } else if (warp < kEpiWarp0) {
+  } else if (warp < Cfg::EW0) {
     // ---------------- unpack (warps 2-5, packed path): 2-bit fields -> u8 e, SW128 K-major
     if (!kPre) {
       const int tid = threadIdx.x - 64;
@@ -357,9 +364,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // ---------------- epilogue (warps 6-13): two warps per TMEM lane quadrant
-    const int ew = warp - kEpiWarp0;
+    const int ew = warp - Cfg::EW0;
     const int quad = warp & 3;          // TMEM lanes [32*quad, 32*quad+32)
-    const int half = ew >> 2;           // which half of the chunks this warp takes
+    const int half = ew >> 2;           // which of the quadrant's NG chunk streams this warp takes
     uint8_t* bufs = sEpi + ew * Cfg::NB * kEpiBuf;
     uint64_t* rb = rbar + ew * 2;
     const bool lead = lane == 0;
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int qsum = rv ? __ldg(a.qsum + row) : 0;
         const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
-        for (int c = half; c < BN / 32; c += 2) {
+        for (int c = half; c < BN / 32; c += NG) {
           const int col0 = n0 + c * 32;
           if (col0 >= a.n_rows) continue;
           uint32_t v[32];
@@ -414,7 +421,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // next chunk's residual into the other buffer, once its last store has read it
           if (lead) {
             bulk_wait_read<0>();
-            if (chunk_at(c + 2 < BN / 32 ? t : t + gridDim.x, c + 2 < BN / 32 ? c + 2 : half, nr0,
+            if (chunk_at(c + NG < BN / 32 ? t : t + gridDim.x, c + NG < BN / 32 ? c + NG : half, nr0,
                          nc0)) {
               mbar_arrive_expect_tx(&rb[buf ^ 1], 32 * 32 * sizeof(TY));
               tma_load_2d(bufs + (buf ^ 1) * kEpiBuf, &tmR, &rb[buf ^ 1], nc0, nr0);
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // fixed order (exact int32) and applies the epilogue
         int32_t* slice = a.part + (int64_t)(t % a.ksplit) * a.M * a.n_rows;
         int* si = reinterpret_cast<int*>(bufs);
-        for (int c = half; c < BN / 32; c += 2) {
+        for (int c = half; c < BN / 32; c += NG) {
           const int col0 = n0 + c * 32;
           if (col0 >= a.n_rows) continue;
           uint32_t v[32];
@@ -492,7 +499,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const bool swig = e.kind == EPI_SWIGLU;
       const int nch = swig ? BN / 64 : BN / 32;   // chunks (or gate/up pairs) per tile
 #pragma unroll 1
-      for (int c = half; c < nch; c += 2) {
+      for (int c = half; c < nch; c += NG) {
         // column bookkeeping of this chunk
         int col0, out_col0;
         if (swig) {
@@ -606,9 +613,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // counts one arrival (with its transaction bytes) per CTA, both CTAs' TMA loads complete on
 // it; "empty" and "accumulator full" are signalled to both CTAs by multicast commits;
 // "accumulator empty" lives in the leader and counts the 8 drain warps of both CTAs.
-constexpr int kS2 = 6;
 constexpr int k2Tile = 128 * kBK;   // A or B half-tile bytes per CTA per stage
-constexpr int k2Smem = kS2 * 2 * k2Tile + kEpiWarps * kEpiBuf + 1024 + 512;
+// NB staging tiles per drain warp: 1 with a 6-stage ring, or 2 (stores overlap the next
+// chunk, the residual of chunk k+1 loads during chunk k) with a 5-stage ring
+template <int NB> struct Cfg2 {
+  static constexpr int S = NB == 2 ? 5 : 6;
+  static constexpr int SMEM = S * 2 * k2Tile + kEpiWarps * NB * kEpiBuf + 1024 + 512;
+};
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -664,23 +675,24 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <typename TY>
+template <typename TY, int NB>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
                const GemmArgs a) {
+  constexpr int kS2 = Cfg2<NB>::S;
   extern __shared__ __align__(1024) uint8_t gsm_raw[];
   uint8_t* sm = gsm_raw + ((1024u - (smem_u32(gsm_raw) & 1023u)) & 1023u);
   uint8_t* sA = sm;                          // [kS2][16 KB] this CTA's 128 rows of A (SW128)
   uint8_t* sB = sA + kS2 * k2Tile;           // [kS2][16 KB] this CTA's half of B (SW128)
-  uint8_t* sEpi = sB + kS2 * k2Tile;         // [8 warps][4 KB] staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kEpiWarps * kEpiBuf);
+  uint8_t* sEpi = sB + kS2 * k2Tile;         // [8 warps][NB][4 KB] staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kEpiWarps * NB * kEpiBuf);
   uint64_t* full = bars;          // [kS2] (the leader's is the one used)
   uint64_t* empty = bars + 8;     // [kS2]
   uint64_t* tfull = bars + 16;    // [2]
   uint64_t* tempty = bars + 18;   // [2] (the leader's)
-  uint64_t* rbar = bars + 20;     // [8 warps] residual tile landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+  uint64_t* rbar = bars + 20;     // [8 warps][2] residual tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 40);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -701,7 +713,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * kEpiWarps);
     }
-    for (int i = 0; i < kEpiWarps; ++i) mbar_init(&rbar[i], 1);
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -779,14 +791,49 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int ew = warp - kEpiWarp0;
     const int quad = warp & 3;
     const int half = ew >> 2;
-    uint8_t* sb = sEpi + ew * kEpiBuf;
-    uint64_t* rb = rbar + ew;
+    uint8_t* bufs = sEpi + ew * NB * kEpiBuf;
+    uint64_t* rb = rbar + ew * 2;
     const bool lead = lane == 0;
     const int nseg = e.n_seg;
+    const bool swig = e.kind == EPI_SWIGLU, resid = e.kind == EPI_RESID;
+    const int nch = swig ? 256 / 64 : 256 / 32;
     const float msc0 = __ldg(e.scales), msc1 = nseg > 1 ? __ldg(e.scales + 1) : 0.0f;
     const float msc2 = nseg > 2 ? __ldg(e.scales + 2) : 0.0f;
     const uint32_t temptyL = mapa_rank(&tempty[0], 0);
-    uint32_t it = 0, rphase = 0;
+    // column bookkeeping of chunk c of a tile at column n0
+    auto cols = [&](int n0, int c, int& col0, int& out_col0) -> bool {
+      if (swig) {
+        col0 = n0 + (c >> 1) * 128 + (c & 1) * 32;
+        out_col0 = (col0 / 128) * 64 + (c & 1) * 32;
+      } else {
+        col0 = n0 + c * 32;
+        out_col0 = e.kind == EPI_FCG ? col0 : (col0 / (kSegRows * nseg)) * kSegRows + (col0 % kSegRows);
+      }
+      return col0 < a.n_rows && !(swig && out_col0 >= e.n_out);
+    };
+    // the first valid chunk of this warp at or after (tile t_, chunk c_): residual coordinates
+    auto next_chunk = [&](int t_, int c_, int& r0_, int& oc0_) -> bool {
+      for (; t_ < total; t_ += ncl, c_ = half) {
+        const int m0_ = (t_ / a.n_tiles) * 256 + (int)rank * 128, n0_ = (t_ % a.n_tiles) * 256;
+        for (; c_ < nch; c_ += 2) {
+          int col0_;
+          if (cols(n0_, c_, col0_, oc0_)) {
+            r0_ = m0_ + quad * 32;
+            return true;
+          }
+        }
+      }
+      return false;
+    };
+    uint32_t it = 0, nchunk = 0;
+    uint32_t rphase[2] = {0, 0};
+    if (NB == 2 && resid && lead) {   // chunk 0's residual
+      int r0_, oc0_;
+      if (next_chunk(cid, half, r0_, oc0_)) {
+        mbar_arrive_expect_tx(&rb[0], 32 * 32 * sizeof(TY));
+        tma_load_2d(bufs, &tmR, &rb[0], oc0_, r0_);
+      }
+    }
     for (int t = cid; t < total; t += ncl, ++it) {
       const uint32_t acc = it & 1;
       const int m0 = (t / a.n_tiles) * 256 + (int)rank * 128, n0 = (t % a.n_tiles) * 256;
@@ -798,28 +845,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const float deq = rv ? __ldg(a.deq + row) : 0.0f;
       const int qsum = rv ? __ldg(a.qsum + row) : 0;
       const uint32_t trow = tmem_base + acc * 256 + ((uint32_t)(quad * 32) << 16);
-      const bool swig = e.kind == EPI_SWIGLU;
-      const int nch = swig ? 256 / 64 : 256 / 32;
 #pragma unroll 1
       for (int c = half; c < nch; c += 2) {
         int col0, out_col0;
-        if (swig) {
-          col0 = n0 + (c >> 1) * 128 + (c & 1) * 32;
-          out_col0 = (col0 / 128) * 64 + (c & 1) * 32;
-        } else {
-          col0 = n0 + c * 32;
-          out_col0 = e.kind == EPI_FCG ? col0 : (col0 / (kSegRows * nseg)) * kSegRows + (col0 % kSegRows);
-        }
-        if (col0 >= a.n_rows || (swig && out_col0 >= e.n_out)) continue;
+        if (!cols(n0, c, col0, out_col0)) continue;
         uint32_t v[32], vu[32];
         tmem_ld32(trow + (col0 - n0), v);
         if (swig) tmem_ld32(trow + (col0 - n0) + 64, vu);
-        if (lead) bulk_wait_read<0>();   // the staging tile's last store has read it
-        __syncwarp();
-        const bool resid = e.kind == EPI_RESID;
-        if (resid && lead) {
-          mbar_arrive_expect_tx(rb, 32 * 32 * sizeof(TY));
-          tma_load_2d(sb, &tmR, rb, out_col0, row0);
+        const int buf = NB == 2 ? (nchunk & 1) : 0;
+        uint8_t* sb = bufs + buf * kEpiBuf;
+        if (NB == 2 && resid) {
+          // the next chunk's residual into the other buffer once its last store read it
+          if (lead) {
+            bulk_wait_read<0>();
+            int r0_, oc0_;
+            if (next_chunk(c + 2 < nch ? t : t + ncl, c + 2 < nch ? c + 2 : half, r0_, oc0_)) {
+              mbar_arrive_expect_tx(&rb[buf ^ 1], 32 * 32 * sizeof(TY));
+              tma_load_2d(bufs + (buf ^ 1) * kEpiBuf, &tmR, &rb[buf ^ 1], oc0_, r0_);
+            }
+          }
+        } else {
+          if (lead) {   // the store that last read this buffer (NB chunks ago) is done
+            if (NB == 2) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
+          __syncwarp();
+          if (resid && lead) {
+            mbar_arrive_expect_tx(&rb[buf], 32 * 32 * sizeof(TY));
+            tma_load_2d(sb, &tmR, &rb[buf], out_col0, row0);
+          }
         }
         tmem_ld_wait();
         const int seg = (col0 / kSegRows) % nseg;
@@ -849,8 +903,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
         if (resid) {
-          mbar_wait(rb, rphase);
-          rphase ^= 1;
+          mbar_wait(&rb[buf], rphase[buf]);
+          rphase[buf] ^= 1;
           float xr[32];
           stg_read_row<TY>(sb, lane, xr);
 #pragma unroll
@@ -864,6 +918,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tma_store_2d(&tmO, sb, out_col0, row0);   // rows >= M / cols >= n clipped by TMA
           bulk_commit();
         }
+        ++nchunk;
       }
       tc_fence_before();
       __syncwarp();
@@ -915,11 +970,11 @@ bool make_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uin
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool kPre, typename TY, bool RES = false>
+template <int BN, bool kPre, typename TY, bool RES = false, int EW = kEpiWarps>
 static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
                                const CUtensorMap& tr, const GemmArgs& a, cudaStream_t s) {
-  using Cfg = GemmCfg<BN, kPre, RES>;
-  auto kern = k_gemm_tc<BN, kPre, TY, RES>;
+  using Cfg = GemmCfg<BN, kPre, RES, EW>;
+  auto kern = k_gemm_tc<BN, kPre, TY, RES, EW>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -963,10 +1018,11 @@ static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, con
   return cudaGetLastError();
 }
 
-template <typename TY>
+template <typename TY, int NB>
 static cudaError_t gemm2_launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
                                 const CUtensorMap& tr, const GemmArgs& a, cudaStream_t s) {
-  auto kern = k_gemm_2sm<TY>;
+  auto kern = k_gemm_2sm<TY, NB>;
+  constexpr int k2Smem = Cfg2<NB>::SMEM;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k2Smem);
@@ -1010,6 +1066,13 @@ static cudaError_t gemm_dispatch_bn(int BN, const CUtensorMap& ta, const CUtenso
   if (BN == 256 && kPre && res_on && a.epi.kind == EPI_RESID && a.epi.acc == nullptr &&
       a.part == nullptr && a.ksplit == 1 && a.num_kb <= 16)
     return gemm_launch<256, kPre, TY, true>(ta, tb, to, tr, a, s);
+  // (12 drain warps measured slower on c2 gate|up: 96 -> 103 us; TERN_GEMM_EW12=1 turns it on)
+  static const int ew12 = getenv("TERN_GEMM_EW12") ? atoi(getenv("TERN_GEMM_EW12")) : 0;   // debug
+  if constexpr (kPre) {
+    if (BN == 256 && ew12 && a.epi.kind == EPI_SWIGLU && a.epi.acc == nullptr &&
+        a.part == nullptr && a.ksplit == 1)
+      return gemm_launch<256, true, TY, false, 12>(ta, tb, to, tr, a, s);
+  }
   return BN == 256 ? gemm_launch<256, kPre, TY>(ta, tb, to, tr, a, s)
                    : gemm_launch<128, kPre, TY>(ta, tb, to, tr, a, s);
 }
@@ -1249,17 +1312,22 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   // (k_gemm_2sm; measured: c2 down 57.5 -> 55.5 us, c3 gate|up 538 -> 508, c3 down 253 -> 220;
   // short-K GEMMs stay on single CTAs: c2 gate|up (K = 1024) 96 -> 108 us on pairs, and the
   // short residual GEMMs take the residual-prefetch variant)
+  static const int kb2 = getenv("TERN_GEMM_2SM_KB") ? atoi(getenv("TERN_GEMM_2SM_KB")) : 16;  // debug
   const bool res_short = epi.kind == EPI_RESID && a.num_kb <= 16;
   if (pre && BN == 256 && g_gemm_2sm && epi.acc == nullptr && epi.kind != EPI_NONE &&
-      a.num_kb >= 16 && !res_short && M > kSmallM) {
+      a.num_kb >= kb2 && !res_short && M > kSmallM) {
     CUtensorMap tb2;
     if (!make_map_2d(&tb2, CU_TENSOR_MAP_DATA_TYPE_UINT8, w.e8, (uint64_t)kp, (uint64_t)w.n_rows,
                      (uint64_t)kp, kBK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
     GemmArgs a2 = a;
     a2.m_tiles = (M + 255) / 256;
-    return yb ? gemm2_launch<__nv_bfloat16>(ta, tb2, to, tr, a2, s)
-              : gemm2_launch<float>(ta, tb2, to, tr, a2, s);
+    static const int nb2 = getenv("TERN_GEMM_2SM_NB") ? atoi(getenv("TERN_GEMM_2SM_NB")) : 2;  // debug
+    if (nb2 == 1)
+      return yb ? gemm2_launch<__nv_bfloat16, 1>(ta, tb2, to, tr, a2, s)
+                : gemm2_launch<float, 1>(ta, tb2, to, tr, a2, s);
+    return yb ? gemm2_launch<__nv_bfloat16, 2>(ta, tb2, to, tr, a2, s)
+              : gemm2_launch<float, 2>(ta, tb2, to, tr, a2, s);
   }
   if (pre)
     return yb ? gemm_dispatch_bn<true, __nv_bfloat16>(BN, ta, tb, to, tr, a, s)
