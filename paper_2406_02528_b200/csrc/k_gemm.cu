@@ -1313,7 +1313,8 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   // short-K GEMMs stay on single CTAs: c2 gate|up (K = 1024) 96 -> 108 us on pairs, and the
   // short residual GEMMs take the residual-prefetch variant)
   static const int kb2 = getenv("TERN_GEMM_2SM_KB") ? atoi(getenv("TERN_GEMM_2SM_KB")) : 16;  // debug
-  const bool res_short = epi.kind == EPI_RESID && a.num_kb <= 16;
+  static const int res2 = getenv("TERN_GEMM_2SM_RESID") ? atoi(getenv("TERN_GEMM_2SM_RESID")) : 0;  // debug
+  const bool res_short = epi.kind == EPI_RESID && a.num_kb <= 16 && !res2;
   if (pre && BN == 256 && g_gemm_2sm && epi.acc == nullptr && epi.kind != EPI_NONE &&
       a.num_kb >= kb2 && !res_short && M > kSmallM) {
     CUtensorMap tb2;

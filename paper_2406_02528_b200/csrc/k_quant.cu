@@ -9,6 +9,8 @@
 // Element loops are branch-free (out-of-row vectors are predicated to zero,
 // which also produces the zero padding up to Kp); sum(x^2) accumulates in
 // binary64 with explicit fma (C4), partials combined in a fixed order.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -385,12 +387,14 @@ static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const floa
     quant_nv<TX, 256>((nvp + 255) / 256, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
     return cudaGetLastError();
   }
-  // smallest threads-per-row with <= 8 vectors per thread
-  if (nvp <= 32 * 8)
+  // smallest threads-per-row with <= NVMAX vectors per thread (8; debug knob TERN_QUANT_NVMAX)
+  static const int nvmax_env = getenv("TERN_QUANT_NVMAX") ? atoi(getenv("TERN_QUANT_NVMAX")) : 8;
+  const int nvmax = (nvmax_env >= 2 && nvmax_env <= 8) ? nvmax_env : 8;
+  if (nvp <= 32 * nvmax)
     quant_nv<TX, 32>((nvp + 31) / 32, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
-  else if (nvp <= 64 * 8)
+  else if (nvp <= 64 * nvmax)
     quant_nv<TX, 64>((nvp + 63) / 64, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
-  else if (nvp <= 128 * 8)
+  else if (nvp <= 128 * nvmax)
     quant_nv<TX, 128>((nvp + 127) / 128, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
   else if (nvp <= 256 * 8)
     quant_nv<TX, 256>((nvp + 255) / 256, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
