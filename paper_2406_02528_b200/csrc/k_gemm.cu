@@ -1199,6 +1199,20 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   int BN = (w.n_rows >= 1024 || w.n_rows % 256 == 0) ? 256 : 128;
   // small M (decode batches): narrower tiles so the weight rows spread over more SMs
   if (M <= kSmallM) BN = 128;
+  // few 256-wide tiles (a short prefill, e.g. one 2048-token sequence: the N = 1024 GEMMs
+  // have 64 tiles for 148 SMs): 128-wide tiles double the CTAs that work while still one
+  // wave (measured c2 B = 1 x 2048: 103.5 -> 98.5 us per block; the same switch where it
+  // makes two waves -- c3's 128-tile GEMMs -- cost c3 B = 1 170 -> 188 us)
+  {
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int t256 = ((M + kBM - 1) / kBM) * ((w.n_rows + 255) / 256);
+    if (BN == 256 && 2 * t256 <= nsm) BN = 128;
+  }
   if (bn_force == 128 || bn_force == 256) BN = bn_force;
   // the u8 copy halves shared-memory traffic when the tensor cores are the limit
   // (large M); for decode batches the weight bytes are, and the 2-bit codes are 4x fewer
