@@ -52,7 +52,14 @@ struct FcgScanArgs {
   int backoff;               // gate warps' wait for the carry: first sleep (ns), 0 = hinted wait
   unsigned long long* prof;  // debug (TERN_FS_PROF): [grid][8] cycles per wait site / phase
   unsigned long long* trace;   // tern_trace_enable timeline
+  int nogate;                  // debug (TERN_FS_NOGATE=1): skip the gate / carry arithmetic
+  unsigned long long* tl;      // debug (TERN_FS_TL=file): CTA 0 per-warp phase clocks [20][nt][8]
 };
+
+__device__ __forceinline__ void fs_tl(const FcgScanArgs& a, int warp, int i, int k) {
+  if (a.tl && blockIdx.x == 0 && (threadIdx.x & 31) == 0)
+    a.tl[((size_t)warp * ((a.T + 127) / 128) + i) * 8 + k] = clock64();
+}
 
 // debug: add the cycles since t0 to counter `site` of this CTA
 __device__ __forceinline__ void fs_acc(const FcgScanArgs& a, int site, long long t0) {
@@ -152,6 +159,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           const long long w1 = clock64();
           mbar_wait(&sm.tempty[acc], ((it >> 1) & 1) ^ 1);
           fs_acc(a, 1, w1);
+          fs_tl(a, 1, i, 0);
           tc_fence_after();
           const uint32_t d_addr = tmem_base + acc * 256;
           for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
@@ -168,6 +176,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             mma_commit(&sm.empty[s]);
           }
           mma_commit(&sm.tfull[acc]);
+          fs_tl(a, 1, i, 1);
         }
       }
     }
@@ -189,7 +198,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const int steps = min(kFBM, a.T - t0);
         // (A) thread = token row: dequant, gates -> smem
         const long long w3 = clock64();
+        fs_tl(a, warp, i, 0);
         mbar_wait(&sm.tfull[acc], (it >> 1) & 1);
+        fs_tl(a, warp, i, 1);
         if (ew == 0 && lane == 0) fs_acc(a, 3, w3);
         const long long w4 = clock64();
         tc_fence_after();
@@ -244,18 +255,22 @@ __global__ void __launch_bounds__(kFThreads, 1)
           sm.G[r][cc + 1] = gh1;
         }
         };
-        if constexpr (!std::is_same<TY, float>::value) phase_a(std::integral_constant<int, 2>{});
+        if (a.nogate) {
+        } else if constexpr (!std::is_same<TY, float>::value) phase_a(std::integral_constant<int, 2>{});
         else if (a.bias) phase_a(std::integral_constant<int, 1>{});
         else phase_a(std::integral_constant<int, 0>{});
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.ready[quad][half]);   // carry may run these rows
+        fs_tl(a, warp, i, 2);
         if (ew == 0 && lane == 0) fs_acc(a, 4, w4);
-        // (C) 16 lanes per row, two rows per instruction: o' = g^ sigma(h) for this
+        // (C) 16 lanes per row, two rows 16 apart per instruction (their kFPad = 65 float
+        // rows start 16 banks apart: conflict-free loads): o' = g^ sigma(h) for this
         // block's rows, after the carry
         const long long w5 = clock64();
         if (a.backoff) mbar_wait_backoff(&sm.hdone[quad][half], it & 1, a.backoff, 8 * a.backoff);
         else mbar_wait(&sm.hdone[quad][half], it & 1);
         if (ew == 0 && lane == 0) fs_acc(a, 5, w5);
+        fs_tl(a, warp, i, 3);
         const long long w6 = clock64();
         const int cc = cs * kFQCh + (lane & 15), rsub = lane >> 4;
         TY* obase = static_cast<TY*>(a.oprime) + (int64_t)(b * a.T + t0) * a.d + c0 + cc;
@@ -264,10 +279,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
         auto phase_c = [&](auto full_c, auto sig_c) {
           constexpr bool kFull = decltype(full_c)::value, kSig = decltype(sig_c)::value;
 #pragma unroll 2
-          for (int rr = 0; rr < 32; rr += 4) {
-            const int t = quad * 32 + rr + rsub;   // rows t and t + 2
-            const float h0 = sm.F[t][cc], h1 = sm.F[t + 2][cc];
-            const float g0 = sm.G[t][cc], g1 = sm.G[t + 2][cc];
+          for (int rr = 0; rr < 16; rr += 2) {
+            const int t = quad * 32 + rr + 16 * rsub;   // rows t and t + 1
+            const float h0 = sm.F[t][cc], h1 = sm.F[t + 1][cc];
+            const float g0 = sm.G[t][cc], g1 = sm.G[t + 1][cc];
             float o0, o1;
             if constexpr (kSig) {
               float q0, q1;
@@ -279,11 +294,12 @@ __global__ void __launch_bounds__(kFThreads, 1)
               o1 = __fmul_rn(g1, h1);
             }
             if (kFull || t < steps) st_act<TY>(obase + (int64_t)t * a.d, o0);
-            if (kFull || t + 2 < steps) st_act<TY>(obase + (int64_t)(t + 2) * a.d, o1);
+            if (kFull || t + 1 < steps) st_act<TY>(obase + (int64_t)(t + 1) * a.d, o1);
           }
         };
         const bool sig = a.gate == TERN_GATE_SIGMOID_H;
-        if (steps == kFBM) {
+        if (a.nogate) {
+        } else if (steps == kFBM) {
           if (sig) phase_c(std::true_type{}, std::true_type{});
           else phase_c(std::true_type{}, std::false_type{});
         } else {
@@ -291,6 +307,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           else phase_c(std::false_type{}, std::false_type{});
         }
         if (ew == 0 && lane == 0) fs_acc(a, 6, w6);
+        fs_tl(a, warp, i, 4);
         // this block's smem rows are rewritten only by this warp's next phase A,
         // after the carry has finished with them (hdone above)
       }
@@ -308,8 +325,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const int steps = min(kFBM, a.T - i * kFBM);
         for (int q = 0; q < 4; ++q) {
           mbar_wait(&sm.ready[q][half], it & 1);
+          fs_tl(a, warp, i, 2 * q);
           const int tb = q * 32, te = min(tb + 32, steps);
-          if (te - tb == 32) {
+          if (a.nogate) {
+          } else if (te - tb == 32) {
 #pragma unroll
             for (int t8 = 0; t8 < 32; t8 += 8) {
               float fv[8], bv[8];
@@ -332,6 +351,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.hdone[q][half]);
+          fs_tl(a, warp, i, 2 * q + 1);
         }
       }
       a.h[(int64_t)b * a.d + c0 + cc] = hc;
@@ -381,6 +401,17 @@ static cudaError_t fcgscan_go(const CUtensorMap& ta, const CUtensorMap& tb, cons
   static const int backoff = getenv("TERN_FS_BACKOFF") ? atoi(getenv("TERN_FS_BACKOFF")) : 32;
   aa.backoff = backoff;
   aa.trace = trace_slot(TERN_K_FCGSCAN, grid);
+  aa.nogate = getenv("TERN_FS_NOGATE") != nullptr;
+  static const char* tl_path = getenv("TERN_FS_TL");   // debug: CTA 0 phase timeline
+  static unsigned long long* dtl = nullptr;
+  const int ntl = (a.T + kFBM - 1) / kFBM;
+  const size_t tl_n = (size_t)(2 + kFEpiWarps + 2) * ntl * 8;
+  if (tl_path) {
+    if (dtl) cudaFree(dtl);
+    cudaMalloc(&dtl, tl_n * sizeof(unsigned long long));
+    cudaMemsetAsync(dtl, 0, tl_n * sizeof(unsigned long long), s);
+    aa.tl = dtl;
+  }
   if (prof_on) {   // debug only: printed after a synchronous run
     if (!dprof) cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * 1024);
     cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * 8 * 1024, s);
@@ -390,6 +421,18 @@ static cudaError_t fcgscan_go(const CUtensorMap& ta, const CUtensorMap& tb, cons
   (void)t0;
   cudaError_t lerr = launch_pdl(kern, dim3(grid), dim3(kFThreads), smem, s, ta, tb, aa);
   if (lerr != cudaSuccess) return lerr;
+  if (tl_path) {
+    unsigned long long* h = (unsigned long long*)malloc(tl_n * sizeof(unsigned long long));
+    cudaMemcpyAsync(h, dtl, tl_n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    FILE* f = fopen(tl_path, "a");
+    if (f) {
+      fprintf(f, "launch B=%d T=%d d=%d nt=%d\n", a.B, a.T, a.d, ntl);
+      for (size_t j = 0; j < tl_n; ++j) fprintf(f, "%llu%c", h[j], (j % 8 == 7) ? '\n' : ' ');
+      fclose(f);
+    }
+    free(h);
+  }
   if (prof_on) {
     static unsigned long long h[8 * 1024];
     cudaMemcpyAsync(h, dprof, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost, s);
