@@ -32,6 +32,15 @@ constexpr int kEpiWarps = 8;
 constexpr int kEpiBuf = 4096;  // bytes of one 32x32 staging tile (fp32)
 constexpr int kSmallM = 256;   // M at or below: packed B tiles (+ split-K when tiles are few)
 
+// residual-epilogue variant (RES): ring stages and staging tiles per drain warp (the
+// residual loads run kResNB - 1 chunks ahead)
+#ifndef TERN_RES_S
+#define TERN_RES_S 3
+#endif
+#ifndef TERN_RES_NB
+#define TERN_RES_NB 2
+#endif
+constexpr int kResS = TERN_RES_S, kResNB = TERN_RES_NB;
 template <int BN, bool kPre, bool RES = false, int EW = kEpiWarps> struct GemmCfg {
   static constexpr int A_BYTES = kBM * kBK;        // 16 KB
   static constexpr int B_BYTES = BN * kBK;         // u8 B tile
@@ -45,9 +54,10 @@ template <int BN, bool kPre, bool RES = false, int EW = kEpiWarps> struct GemmCf
   // EW = 12 drain warps (the u8 path's idle unpack warps 2-5 join the 8 drain warps) for
   // the SwiGLU epilogue, whose arithmetic (2 exact sigmoids per p) outlasts a K = 1024 tile's
   // MMAs; its staging takes the 4th ring stage
-  static constexpr int S = kPre ? (((RES || EW == 12) && BN == 256) ? 3 : 4) : (BN == 256 ? 4 : 5);
+  static constexpr int S = kPre ? ((RES && BN == 256) ? kResS : (EW == 12 && BN == 256) ? 3 : 4)
+                               : (BN == 256 ? 4 : 5);
   static constexpr int U = kPre ? 0 : 2;
-  static constexpr int NB = (kPre && BN == 256 && !RES) ? 1 : 2;
+  static constexpr int NB = (kPre && BN == 256 && RES) ? kResNB : (kPre && BN == 256) ? 1 : 2;
   static constexpr int EW0 = EW == 12 ? 2 : kEpiWarp0;   // first drain warp
   static constexpr int NG = EW / 4;                      // drain warps per TMEM lane quadrant
   static constexpr int RING = kPre ? S * (A_BYTES + B_BYTES) : S * (A_BYTES + BP_BYTES) + U * B_BYTES;
@@ -197,8 +207,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* ufree = bars + 20;           // [U] MMA finished with the unpacked B
   uint64_t* tfull = bars + 24;           // [2] accumulator ready
   uint64_t* tempty = bars + 26;          // [2] accumulator drained
-  uint64_t* rbar = bars + 28;            // [EW warps][2] residual tile landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 56);
+  constexpr int RBW = Cfg::NB > 2 ? Cfg::NB : 2;   // residual barriers per drain warp
+  static_assert(28 + RBW * EW + 1 <= 64, "barrier area");
+  uint64_t* rbar = bars + 28;            // [EW warps][RBW] residual tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28 + RBW * EW);
 
   const long long t_start = clock64();
 #ifdef TERN_TRACE
@@ -225,7 +237,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], EW);
     }
-    for (int i = 0; i < 2 * EW; ++i) mbar_init(&rbar[i], 1);
+    for (int i = 0; i < RBW * EW; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int quad = warp & 3;          // TMEM lanes [32*quad, 32*quad+32)
     const int half = ew >> 2;           // which of the quadrant's NG chunk streams this warp takes
     uint8_t* bufs = sEpi + ew * Cfg::NB * kEpiBuf;
-    uint64_t* rb = rbar + ew * 2;
+    uint64_t* rb = rbar + ew * RBW;
     const bool lead = lane == 0;
     const bool legacy = e.acc != nullptr || e.kind == EPI_NONE;   // tap / parity path
     const int nseg = e.n_seg;
@@ -378,26 +390,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t rphase[2] = {0, 0};
     if (RES) {
       // residual epilogue (EPI_RESID, no taps, no split-K): chunk k of this warp (over its
-      // tiles in order) reads its residual into staging buffer k & 1; the load of chunk k+1
-      // is issued before chunk k is computed, so its latency hides behind one chunk
-      auto chunk_at = [&](int t_, int c_, int& row0_, int& col0_) -> bool {
-        // the first chunk of this warp at or after (t_, c_): its tile row / column
+      // tiles in order) reads its residual into staging buffer k % NB; the loads run NB - 1
+      // chunks ahead of the compute, so their HBM latency hides behind NB - 1 chunks
+      constexpr int NBR = Cfg::NB;
+      // the first chunk of this warp at or after (t_, c_) (both updated to it): its tile
+      // row / column
+      auto chunk_at = [&](int& t_, int& c_, int& row0_, int& col0_) -> bool {
         for (; t_ < total; t_ += gridDim.x, c_ = half) {
           const int tile_ = t_ / a.ksplit;
           const int m0_ = (tile_ / a.n_tiles) * kBM, n0_ = (tile_ % a.n_tiles) * BN;
-          if (c_ < BN / 32 && n0_ + c_ * 32 < a.n_rows) {
-            row0_ = m0_ + quad * 32;
-            col0_ = n0_ + c_ * 32;
-            return true;
-          }
+          for (; c_ < BN / 32; c_ += NG)
+            if (n0_ + c_ * 32 < a.n_rows) {
+              row0_ = m0_ + quad * 32;
+              col0_ = n0_ + c_ * 32;
+              return true;
+            }
         }
         return false;
       };
-      int nr0 = 0, nc0 = 0;
-      if (lead && chunk_at(blockIdx.x, half, nr0, nc0)) {
-        mbar_arrive_expect_tx(&rb[0], 32 * 32 * sizeof(TY));
-        tma_load_2d(bufs, &tmR, &rb[0], nc0, nr0);
-      }
+      int ti = blockIdx.x, ci = half;   // issue cursor: the next chunk whose residual to load
+      uint32_t nissued = 0;
+      auto issue_next = [&]() {
+        int nr0, nc0;
+        if (chunk_at(ti, ci, nr0, nc0)) {
+          const int bi = nissued % NBR;
+          mbar_arrive_expect_tx(&rb[bi], 32 * 32 * sizeof(TY));
+          tma_load_2d(bufs + bi * kEpiBuf, &tmR, &rb[bi], nc0, nr0);
+          ++nissued;
+          ci += NG;
+        }
+      };
+      if (lead)
+        for (int j = 0; j < NBR - 1; ++j) issue_next();
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
         const uint32_t acc = it & 1;
         const int tile = t / a.ksplit;
@@ -416,16 +440,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (col0 >= a.n_rows) continue;
           uint32_t v[32];
           tmem_ld32(trow + c * 32, v);
-          const int buf = nchunk & 1;
+          const int buf = nchunk % NBR;
           uint8_t* sb = bufs + buf * kEpiBuf;
-          // next chunk's residual into the other buffer, once its last store has read it
+          // the residual NB - 1 chunks ahead, into the buffer of the previous chunk once
+          // its store has read it
           if (lead) {
             bulk_wait_read<0>();
-            if (chunk_at(c + NG < BN / 32 ? t : t + gridDim.x, c + NG < BN / 32 ? c + NG : half, nr0,
-                         nc0)) {
-              mbar_arrive_expect_tx(&rb[buf ^ 1], 32 * 32 * sizeof(TY));
-              tma_load_2d(bufs + (buf ^ 1) * kEpiBuf, &tmR, &rb[buf ^ 1], nc0, nr0);
-            }
+            issue_next();
           }
           tmem_ld_wait();
           const float sc = __fmul_rn(deq, msc0);
@@ -436,8 +457,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (e.bias) x = __fadd_rn(x, __ldg(e.bias + col0 + j));
             o[j] = storage_round<TY>(x);
           }
-          mbar_wait(&rb[buf], rphase[buf]);
-          rphase[buf] ^= 1;
+          mbar_wait(&rb[buf], (nchunk / NBR) & 1);
           float xr[32];
           stg_read_row<TY>(sb, lane, xr);
 #pragma unroll
