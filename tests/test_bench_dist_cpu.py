@@ -100,3 +100,8 @@ def test_int8_peak_from_measured_peaks():
     p, src = bench.int8_peak_for(pk, {"sm_mhz": 1700.0, "sm_max_mhz": 1965.0,
                                       "reasons": ["sw_power_cap"]})
     assert p == 2 * mp["bf16_tflops_sustained"] and "sustained" in src
+    # power-cap events with the clock held at max: the burst figure (a tensor peak follows
+    # the clock)
+    p, src = bench.int8_peak_for(pk, {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0,
+                                      "reasons": ["sw_power_cap"]})
+    assert p == 2 * mp["bf16_tflops"] and "burst" in src and "held" in src
