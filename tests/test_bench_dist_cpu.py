@@ -105,3 +105,12 @@ def test_int8_peak_from_measured_peaks():
     p, src = bench.int8_peak_for(pk, {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0,
                                       "reasons": ["sw_power_cap"]})
     assert p == 2 * mp["bf16_tflops"] and "burst" in src and "held" in src
+    # a GEMM above the sustained-derived figure under a reduced clock is measured against
+    # the burst figure (no fraction > 1)
+    m, n, k = 131072, 2560, 6912
+    ach = 1.05 * 2 * mp["bf16_tflops_sustained"]
+    rec = {"kernel": "gemm_tc", "ms": 2 * m * n * k / (ach * 1e12) * 1e3, "m": m, "n": n, "k": k,
+           "n_seg": 1, "epi": "resid"}
+    rl, _ = bench.roofline([rec], 2, pk, {}, {"sm_mhz": 1725.0, "sm_max_mhz": 1965.0,
+                                              "reasons": ["sw_power_cap"]})
+    assert rl["peak"] == round(2 * mp["bf16_tflops"], 1) and rl["frac"] < 1.0
