@@ -215,9 +215,12 @@ typedef struct {
    * sequence is cut into 4 contiguous chunks [j T/4, (j+1) T/4) scanned concurrently
    * from their composed boundary states (chunk aggregates A = prod f, B = the recurrence
    * from 0, composed in order) -- equal to the oracle's 4-slice composition
-   * (O.scan_slices(4)) and within reading S4's tolerance of the sequential scan; 0 = auto,
-   * currently 1: the chunked kernel measured slower than the sequential one at every
-   * few-sequence config.  Other values: TERN_ERR_UNSUPPORTED.
+   * (O.scan_slices(4)) and within reading S4's tolerance of the sequential scan; 8 = the
+   * same with 8 chunks (O.scan_slices(8)).  With d % 32 == 0 and ceil(T / chunks) <= 512
+   * the chunks of a 32-channel group run on the CTAs of one thread-block cluster, handing
+   * the boundary state on through distributed shared memory; otherwise 4 runs on one CTA
+   * per 8 channels (d % 8 == 0) and 8 falls back to the exact scan.  0 = auto, currently 1
+   * (DESIGN.md §6 has the measured comparison).  Other values: TERN_ERR_UNSUPPORTED.
    * tern_mlgru_chunks() reports the resolved value. */
   int32_t num_chunks;
 } tern_mlgru;

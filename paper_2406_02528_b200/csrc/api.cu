@@ -251,8 +251,9 @@ tern_status check_block(const tern_block* b) {
     CHECK(b->ch.down.n_out == ds, "GLU down weights must be l -> d/world");
   }
   CHECK(b->mix.gate == TERN_GATE_SIGMOID_H || b->mix.gate == TERN_GATE_LINEAR_H, "bad gate mode");
-  if (b->mix.num_chunks != 0 && b->mix.num_chunks != 1 && b->mix.num_chunks != 4)
-    return fail(TERN_ERR_UNSUPPORTED, "num_chunks=%d (0, 1 or 4)", b->mix.num_chunks);
+  if (b->mix.num_chunks != 0 && b->mix.num_chunks != 1 && b->mix.num_chunks != 4 &&
+      b->mix.num_chunks != 8)
+    return fail(TERN_ERR_UNSUPPORTED, "num_chunks=%d (0, 1, 4 or 8)", b->mix.num_chunks);
   CHECK(b->mix.eps > 0 && b->ch.eps > 0, "eps must be > 0");
   CHECK((b->mix.norm == TERN_NORM_RMS || b->mix.norm == TERN_NORM_CENTERED) &&
             (b->ch.norm == TERN_NORM_RMS || b->ch.norm == TERN_NORM_CENTERED),
@@ -750,7 +751,7 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   int32_t* qsum = at<int32_t>(ws, L.qsum);
   void* fcg = at<char>(ws, L.fcg);
   const int ldq = kpad(d);
-  // the prefill scan: sequential (1) or chunked over time (4; tern_mlgru.num_chunks)
+  // the prefill scan: sequential (1) or chunked over time (4, 8; tern_mlgru.num_chunks)
   const int chunks = T > 1 ? scan_chunks_resolve(p.num_chunks, B, T, d) : 1;
   // the fused kernel walks each sequence's 128-token tiles; short sequences (decode
   // steps with B > gemv_max_m) take GEMM + scan instead
@@ -1088,7 +1089,8 @@ tern_status check_act(const void* x, const void* y, const void* ws, size_t ws_by
 
 int32_t tern_mlgru_chunks(const tern_mlgru* p, int32_t B, int32_t T, int32_t d) {
   if (!p || B < 1 || T < 2 || d < 1) return 1;
-  if (p->num_chunks != 0 && p->num_chunks != 1 && p->num_chunks != 4) return 0;
+  if (p->num_chunks != 0 && p->num_chunks != 1 && p->num_chunks != 4 && p->num_chunks != 8)
+    return 0;
   return tern::scan_chunks_resolve(p->num_chunks, B, T, d);
 }
 
@@ -1105,8 +1107,8 @@ tern_status mlgru_fwd(const tern_mlgru* p, const void* x, void* out, tern_dtype 
   CHECK(p->fcg.n_out == d && p->o.n_out == d, "mlgru_fwd: weights must be d x d");
   CHECK(p->eps > 0, "mlgru_fwd: eps");
   CHECK(p->norm == TERN_NORM_RMS || p->norm == TERN_NORM_CENTERED, "mlgru_fwd: bad norm mode");
-  if (p->num_chunks != 0 && p->num_chunks != 1 && p->num_chunks != 4)
-    return fail(TERN_ERR_UNSUPPORTED, "mlgru_fwd: num_chunks=%d (0, 1 or 4)", p->num_chunks);
+  if (p->num_chunks != 0 && p->num_chunks != 1 && p->num_chunks != 4 && p->num_chunks != 8)
+    return fail(TERN_ERR_UNSUPPORTED, "mlgru_fwd: num_chunks=%d (0, 1, 4 or 8)", p->num_chunks);
   BlockWs L = block_ws(B * T, d, 0, p->fcg.n_rows, dt);
   if ((st = check_act(x, out, ws, ws_bytes, L.total, dt, "mlgru_fwd")) != TERN_OK) return st;
   if ((st = check_device()) != TERN_OK) return st;

@@ -604,16 +604,330 @@ static cudaError_t scan_pick(const void* fcg, int B, int T, int d, int gate, flo
 // 180.7 vs 75.8 us, tools/scan_chunk_bench.py) -- the sequential kernel is bound by its gate
 // arithmetic and pipeline, not by the carry chain, and the chunked one computes the gates of
 // f and c twice (5 sigmoids per element instead of 3)
+// ---------------------------------------------------------------- cross-CTA chunked scan
+// num_chunks = 4 for few long sequences: the 4 slices [j T / 4, (j+1) T / 4) of a 32-channel
+// group run on the 4 CTAs of one thread-block cluster (rank = slice j), so every slice has
+// an SM of its own (4x the SMs of the in-CTA layout below; one CTA per SM keeps each carry
+// warp's sub-partition free of other carries), and the boundary state crosses the
+// cluster through distributed shared memory (reading C23):
+//   pass A  gates f = sigma(f^), b = (1-f) SiLU(c^) for the whole slice into shared memory
+//           (16 warps; g^ staged too), then the carry warp (lane = channel) runs the slice
+//           aggregate A = A f, B = f B + b from (1, 0), left to right;
+//   hop     slice j waits for h_in(j) from rank j-1 (slice 0: the state h) and sends
+//           h_in(j+1) = A h_in(j) + B to rank j+1 (st.async into its shared memory,
+//           completing on its mbarrier); the last slice writes the final state to h;
+//   pass B  the carry scans the slice from h_in(j) over the stored (f, b), then all warps
+//           form o' = g^ sigma(h) (or g^ h).
+// Every operation and its order is O.scan_slices(4)'s, so the result is bit-identical to it.
+constexpr int kLBC = 32;           // channels per CTA (lane = channel in the carry)
+constexpr int kLBThreads = 512;    // warp 0 the carry; gates / output on the warps of
+                                   // sub-partitions 1-3 (warp % 4 != 0: 12 warps), so the
+                                   // carry's dependent chain has sub-partition 0 to itself
+constexpr int kLBTS = 64;          // steps per pipeline tile
+constexpr int kLBMaxT = 8;         // tiles per slice held in shared memory
+constexpr int kLBMaxL = kLBTS * kLBMaxT;
+constexpr int kLBGate = 12 * 32;   // gate / output threads
+
+__device__ __forceinline__ uint32_t lb_mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void lb_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+// shared memory (rows = steps of the slice, 32 channels each): raw f^ c^ g^ TA [3][512][32]
+// (TMA, every tile issued up front), then f, b fp32 [2][512][32] (the raw f^ c^ arrays
+// themselves when TA is fp32: converted in place, each element by the thread that reads it)
+// (rows = the longest slice rounded up to whole tiles)
+template <typename TA>
+__host__ __device__ constexpr size_t lb_smem_bytes(int rows) {
+  return (size_t)3 * rows * kLBC * sizeof(TA) +
+         (sizeof(TA) == 4 ? 0 : (size_t)2 * rows * kLBC * sizeof(float)) + 128;
+}
+
+template <typename TA>
+__global__ void __launch_bounds__(kLBThreads, 1) k_scan_lb(const __grid_constant__ CUtensorMap tmX,
+                                                           int B, int T, int d, int nch, int rows,
+                                                           int gate, float* h, TA* oprime,
+                                                           unsigned long long* tl) {
+  extern __shared__ __align__(128) float lbs[];
+  __shared__ __align__(8) uint64_t full[kLBMaxT], gated[kLBMaxT], hdone[kLBMaxT], gbar, hbar;
+  __shared__ __align__(16) float hin_s[kLBC];
+  const int G = d / kLBC;
+  const int j = blockIdx.x % nch, rem = blockIdx.x / nch, b = rem / G, cg = rem % G;
+  const int s0 = (int)((int64_t)j * T / nch), s1 = (int)((int64_t)(j + 1) * T / nch);
+  const int L = s1 - s0, nt = (L + kLBTS - 1) / kLBTS;
+  const int kArr = rows * kLBC;
+  TA* rf = reinterpret_cast<TA*>(lbs);            // raw f^, c^, g^
+  TA* rc = rf + kArr;
+  TA* rg = rc + kArr;
+  float* F = sizeof(TA) == 4 ? reinterpret_cast<float*>(rf) : reinterpret_cast<float*>(rg + kArr);
+  float* Bv = sizeof(TA) == 4 ? reinterpret_cast<float*>(rc) : F + kArr;   // f -> h, b
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c0 = cg * kLBC;
+  const int row0 = b * T + s0;                    // first row of the slice in [B*T][3d]
+  const int colf = packed_row(0, c0, 3), colc = packed_row(1, c0, 3), colg = packed_row(2, c0, 3);
+  constexpr uint32_t kTileBytes = kLBTS * kLBC * sizeof(TA);
+  auto mark = [&](int k) {   // debug timeline (TERN_LB_TL): globaltimer per CTA and phase
+    if (tl && threadIdx.x == 0) tl[(size_t)blockIdx.x * 8 + k] = gtimer();
+  };
+  mark(6);
+  if (tid == 0) {
+    tma_prefetch_desc(&tmX);
+    for (int i = 0; i < kLBMaxT; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&gated[i], kLBGate / 32);
+      mbar_init(&hdone[i], 1);
+    }
+    mbar_init(&gbar, 1);
+    mbar_init(&hbar, 1);
+    fence_barrier_init();
+    if (j > 0) mbar_arrive_expect_tx(&hbar, kLBC * sizeof(float));
+  }
+  lb_cluster_sync();          // every rank's barriers armed before any st.async
+  pdl_wait();                 // f^c^g^ and h come from earlier kernels
+  pdl_launch_dependents();
+  mark(0);
+  if (tid == 32) {            // the whole slice in flight at once: f^ c^ per tile, then g^
+    for (int k = 0; k < nt; ++k) {
+      mbar_arrive_expect_tx(&full[k], 2 * kTileBytes);
+      tma_load_2d(rf + k * kLBTS * kLBC, &tmX, &full[k], colf, row0 + k * kLBTS);
+      tma_load_2d(rc + k * kLBTS * kLBC, &tmX, &full[k], colc, row0 + k * kLBTS);
+    }
+    if (nt > 0) {
+      mbar_arrive_expect_tx(&gbar, nt * kTileBytes);
+      for (int k = 0; k < nt; ++k)
+        tma_load_2d(rg + k * kLBTS * kLBC, &tmX, &gbar, colg, row0 + k * kLBTS);
+    }
+  }
+  if (warp == 0) {
+    // ---- pass A carry, tile by tile behind the gates: the aggregate from (A, B) = (1, 0)
+    float A = 1.0f, Bs = 0.0f;
+    for (int k = 0; k < nt; ++k) {
+      mbar_wait(&gated[k], 0);
+      const int st1 = min(L, (k + 1) * kLBTS);
+      int st = k * kLBTS;
+      // groups of 8 steps, the next group's loads issued before this group's chain
+      float fv[8], bv[8];
+      if (st + 8 <= st1) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          fv[u] = F[(st + u) * kLBC + lane];
+          bv[u] = Bv[(st + u) * kLBC + lane];
+        }
+      }
+      for (; st + 8 <= st1; st += 8) {
+        float fn[8], bn[8];
+        const bool more = st + 16 <= st1;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          fn[u] = more ? F[(st + 8 + u) * kLBC + lane] : 0.0f;
+          bn[u] = more ? Bv[(st + 8 + u) * kLBC + lane] : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          A = __fmul_rn(A, fv[u]);
+          Bs = __fadd_rn(__fmul_rn(fv[u], Bs), bv[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          fv[u] = fn[u];
+          bv[u] = bn[u];
+        }
+      }
+      for (; st < st1; ++st) {
+        const float fv = F[st * kLBC + lane];
+        A = __fmul_rn(A, fv);
+        Bs = __fadd_rn(__fmul_rn(fv, Bs), Bv[st * kLBC + lane]);
+      }
+    }
+    mark(1);
+    // ---- hop: h_in(j) from rank j-1 (or the state), h_in(j+1) to rank j+1 (or the state)
+    const int64_t hi = (int64_t)b * d + c0 + lane;
+    float hin;
+    if (j == 0) {
+      hin = __ldcg(h + hi);
+    } else {
+      mbar_wait(&hbar, 0);
+      hin = hin_s[lane];
+    }
+    const float hout = __fadd_rn(__fmul_rn(A, hin), Bs);
+    if (j + 1 < nch) {
+      const uint32_t dst = lb_mapa(&hin_s[lane], (uint32_t)(j + 1));
+      const uint32_t bar = lb_mapa(&hbar, (uint32_t)(j + 1));
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst),
+                   "r"(__float_as_uint(hout)), "r"(bar)
+                   : "memory");
+    } else {
+      h[hi] = hout;   // the state after the sequence: the composition through every slice
+    }
+    mark(2);
+    // ---- pass B carry: the exact scan of the slice from h_in(j), h over f in place, the
+    // output gate following tile by tile
+    float hh = hin;
+    for (int k = 0; k < nt; ++k) {
+      const int st1 = min(L, (k + 1) * kLBTS);
+      int st = k * kLBTS;
+      float fv[8], bv[8];
+      if (st + 8 <= st1) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          fv[u] = F[(st + u) * kLBC + lane];
+          bv[u] = Bv[(st + u) * kLBC + lane];
+        }
+      }
+      for (; st + 8 <= st1; st += 8) {
+        float fn[8], bn[8], hv[8];
+        const bool more = st + 16 <= st1;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          fn[u] = more ? F[(st + 8 + u) * kLBC + lane] : 0.0f;
+          bn[u] = more ? Bv[(st + 8 + u) * kLBC + lane] : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          hh = __fadd_rn(__fmul_rn(fv[u], hh), bv[u]);
+          hv[u] = hh;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          F[(st + u) * kLBC + lane] = hv[u];
+          fv[u] = fn[u];
+          bv[u] = bn[u];
+        }
+      }
+      for (; st < st1; ++st) {
+        hh = __fadd_rn(__fmul_rn(F[st * kLBC + lane], hh), Bv[st * kLBC + lane]);
+        F[st * kLBC + lane] = hh;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hdone[k]);
+    }
+    mark(3);
+  } else if (warp & 3) {
+    // ---- gates (12 warps): tile k's f = sigma(f^), b = (1-f) SiLU(c^), in place
+    const int gt = (warp - 1 - (warp >> 2)) * 32 + lane;   // 0 .. 383
+    for (int k = 0; k < nt; ++k) {
+      mbar_wait(&full[k], 0);
+      const int e0 = k * kLBTS * kLBC, e1 = min(L, (k + 1) * kLBTS) * kLBC;
+      for (int e = e0 + gt; e < e1; e += kLBGate) {
+        const float fh = ld_act<TA>(rf + e), ch = ld_act<TA>(rc + e);
+        float f, sc;
+        sigmoid2(fh, ch, f, sc);
+        F[e] = f;
+        Bv[e] = __fmul_rn(__fsub_rn(1.0f, f), __fmul_rn(ch, sc));   // (1-f) SiLU(c)
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&gated[k]);
+    }
+    // ---- output gate, tile by tile behind the carry (a warp stores one step's 32 channels)
+    if (nt > 0) mbar_wait(&gbar, 0);
+    TA* obase = oprime + (int64_t)row0 * d + c0 + lane;
+    const bool sig = gate == TERN_GATE_SIGMOID_H;
+    for (int k = 0; k < nt; ++k) {
+      mbar_wait(&hdone[k], 0);
+      const int e0 = k * kLBTS * kLBC, e1 = min(L, (k + 1) * kLBTS) * kLBC;
+      int e = e0 + gt;
+      if (sig) {
+        for (; e + kLBGate < e1; e += 2 * kLBGate) {
+          float q0, q1;
+          sigmoid2(F[e], F[e + kLBGate], q0, q1);
+          st_act<TA>(obase + (int64_t)(e >> 5) * d, __fmul_rn(ld_act<TA>(rg + e), q0));
+          st_act<TA>(obase + (int64_t)((e + kLBGate) >> 5) * d,
+                     __fmul_rn(ld_act<TA>(rg + e + kLBGate), q1));
+        }
+        if (e < e1) {
+          float q0, q1;
+          sigmoid2(F[e], F[e], q0, q1);
+          st_act<TA>(obase + (int64_t)(e >> 5) * d, __fmul_rn(ld_act<TA>(rg + e), q0));
+        }
+      } else {
+        for (; e < e1; e += kLBGate)
+          st_act<TA>(obase + (int64_t)(e >> 5) * d, __fmul_rn(ld_act<TA>(rg + e), F[e]));
+      }
+    }
+  }
+  mark(5);
+  lb_cluster_sync();          // no rank leaves while a peer's st.async may target it
+}
+
+static bool lb_ok(int nch, int T, int d) {
+  return d % kLBC == 0 && (T + nch - 1) / nch <= kLBMaxL;
+}
+
+template <typename TA>
+static cudaError_t scan_lb_go(const void* fcg, int B, int T, int d, int nch, int gate, float* h,
+                              void* oprime, cudaStream_t s) {
+  const int rows = ((T + nch - 1) / nch + kLBTS - 1) / kLBTS * kLBTS;
+  const size_t smem = lb_smem_bytes<TA>(rows);
+  static bool attr = false;
+  cudaError_t e;
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_scan_lb<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lb_smem_bytes<TA>(kLBMaxL));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const bool bf = std::is_same<TA, __nv_bfloat16>::value;
+  CUtensorMap tm;
+  if (!make_map_2d(&tm, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, fcg,
+                   (uint64_t)3 * d, (uint64_t)B * T, (uint64_t)3 * d * sizeof(TA), kLBC, kLBTS,
+                   CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  const int grid = nch * B * (d / kLBC);
+  static const char* tl_path = getenv("TERN_LB_TL");   // debug: per-CTA phase timeline
+  static unsigned long long* dtl = nullptr;
+  if (tl_path && !dtl) cudaMalloc(&dtl, sizeof(unsigned long long) * 8 * 65536);
+  unsigned long long* tl = (tl_path && grid <= 65536) ? dtl : nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kLBThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;   // the slices of one channel group
+  at[0].val.clusterDim.x = nch;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  e = cudaLaunchKernelEx(&cfg, k_scan_lb<TA>, tm, B, T, d, nch, rows, gate, h,
+                         static_cast<TA*>(oprime), tl);
+  if (e == cudaSuccess && tl) {
+    static unsigned long long hbuf[8 * 65536];
+    cudaMemcpyAsync(hbuf, tl, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    FILE* f = fopen(tl_path, "a");
+    if (f) {
+      fprintf(f, "launch B=%d T=%d d=%d nch=%d grid=%d\n", B, T, d, nch, grid);
+      for (int i = 0; i < grid; ++i)
+        fprintf(f, "%llu %llu %llu %llu %llu %llu %llu\n", hbuf[i * 8], hbuf[i * 8 + 1],
+                hbuf[i * 8 + 2], hbuf[i * 8 + 3], hbuf[i * 8 + 4], hbuf[i * 8 + 5], hbuf[i * 8 + 6]);
+      fclose(f);
+    }
+  }
+  return e;
+}
+
 int scan_chunks_resolve(int num_chunks, int B, int T, int d) {
   (void)B;
-  (void)T;
-  if (num_chunks == kChN && d % kChC == 0) return kChN;
+  if (num_chunks == kChN && d % kChC == 0) return kChN;   // cluster kernel or the in-CTA one
+  if (num_chunks == 8 && lb_ok(8, T, d)) return 8;       // cluster kernel only
   return 1;
 }
 
 cudaError_t launch_scan_chunks(const void* fcg, int dt, int B, int T, int d, int gate, float* h,
                                void* oprime, int chunks, cudaStream_t s) {
   if (B == 0 || T == 0) return cudaSuccess;
+  static const int lb_on = getenv("TERN_SCAN_LB") ? atoi(getenv("TERN_SCAN_LB")) : 1;   // debug
+  if ((chunks == kChN && lb_on && lb_ok(chunks, T, d)) || chunks == 8)
+    return dt == TERN_BF16 ? scan_lb_go<__nv_bfloat16>(fcg, B, T, d, chunks, gate, h, oprime, s)
+                           : scan_lb_go<float>(fcg, B, T, d, chunks, gate, h, oprime, s);
   if (chunks == kChN)
     return dt == TERN_BF16 ? scan_chunked_go<__nv_bfloat16>(fcg, B, T, d, gate, h, oprime, s)
                            : scan_chunked_go<float>(fcg, B, T, d, gate, h, oprime, s);

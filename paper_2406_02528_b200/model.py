@@ -59,7 +59,7 @@ class Block:
         latent holds the FULL matrices, gains/biases this rank's slices.  norm: the
         norm in front of every BitLinear (TERN_NORM_RMS, or TERN_NORM_CENTERED =
         Alg. 1's centred form).  num_chunks: the prefill scan over time (tern.h
-        tern_mlgru.num_chunks: 0 auto, 1 exact sequential, 4 chunked, reading C23)."""
+        tern_mlgru.num_chunks: 0 auto, 1 exact sequential, 4 or 8 chunked, reading C23)."""
         self.d, self.l = d, l
         dev = torch.device(device)
         lat = {k: v.to(dev) for k, v in latent.items()}

@@ -31,17 +31,19 @@ def _run(cfg, B, T, num_chunks, gate=0, n_blocks=1):
     return st, x, y, hs, ob
 
 
+@pytest.mark.parametrize("nch", [4, 8])
 @pytest.mark.parametrize("dtype,B,T,gate", [("f32", 1, 2048, 0), ("bf16", 1, 2048, 1),
                                             ("f32", 2, 1030, 1), ("bf16", 3, 517, 0),
                                             ("f32", 1, 9, 0), ("f32", 1, 4, 0)])
-def test_chunked_scan_equals_oracle_composition(dtype, B, T, gate):
-    """num_chunks = 4 through block_prefill (ragged chunks: T = 1030, 517, 9 are not
-    multiples of 4 x 128; T = 4: one step per chunk), both gate modes, fp32 and bf16: y and
-    the per-block state equal O.stack under O.scan_slices(4) bit for bit."""
+def test_chunked_scan_equals_oracle_composition(dtype, B, T, gate, nch):
+    """num_chunks = 4 and 8 through block_prefill (ragged chunks: T = 1030, 517, 9 are not
+    multiples of nch x 64; T = 4: one step per chunk, or none for half of the 8), both gate
+    modes, fp32 and bf16: y and the per-block state equal O.stack under O.scan_slices(nch)
+    bit for bit.  (d = 256: the cluster kernel, 8 groups of 32 channels.)"""
     cfg = synth.Config("chk", 1, 256, 688, dtype, 61, B, T, B, 0)
-    st, x, y, hs, ob = _run(cfg, B, T, 4, gate)
-    assert st.blocks[0].scan_chunks(B, T) == 4
-    with O.scan_slices(4):
+    st, x, y, hs, ob = _run(cfg, B, T, nch, gate)
+    assert st.blocks[0].scan_chunks(B, T) == nch
+    with O.scan_slices(nch):
         yo, Ho = O.stack(ob, x.float().numpy(), [np.zeros((B, cfg.d), np.float32)],
                          bf16=(dtype == "bf16"), gate_mode=gate)
     assert np.array_equal(y.float().cpu().numpy(), yo)
@@ -68,6 +70,26 @@ def test_chunked_scan_at_c2_batch1():
     assert np.all(np.abs(H4[0] - Hseq[0]) <= 1e-5 * np.maximum(np.abs(Hseq[0]), 1e-2))
     st0, *_ = _run(synth.Config("auto", 1, 256, 688, "f32", 63, 1, 8, 1, 0), 1, 8, 0)
     assert st0.blocks[0].scan_chunks(1, 4096) == 1
+
+
+def test_eight_chunks_at_c2_batch1_and_fallbacks():
+    """num_chunks = 8 at the c2 width, batch 1 x 2048 through 2 blocks: bit for bit the
+    oracle's 8-slice composition; beyond 8 x 512 steps (T = 4104) it resolves to the exact
+    sequential scan and then equals the sequential oracle."""
+    cfg = synth.CONFIGS["c2"]
+    st, x, y, hs, ob = _run(cfg, 1, 2048, 8, n_blocks=2)
+    assert st.blocks[0].scan_chunks(1, 2048) == 8
+    with O.scan_slices(8):
+        yo, Ho = O.stack(ob, x.float().numpy(), [np.zeros((1, cfg.d), np.float32)] * 2)
+    assert np.array_equal(y.float().cpu().numpy(), yo)
+    for i in range(2):
+        assert np.array_equal(hs[i].cpu().numpy(), Ho[i])
+    cfg2 = synth.Config("chk8", 1, 256, 688, "f32", 64, 1, 4104, 1, 0)
+    st2, x2, y2, hs2, ob2 = _run(cfg2, 1, 4104, 8)
+    assert st2.blocks[0].scan_chunks(1, 4104) == 1
+    yo2, Ho2 = O.stack(ob2, x2.float().numpy(), [np.zeros((1, cfg2.d), np.float32)])
+    assert np.array_equal(y2.float().cpu().numpy(), yo2)
+    assert np.array_equal(hs2[0].cpu().numpy(), Ho2[0])
 
 
 def test_num_chunks_one_stays_exact():

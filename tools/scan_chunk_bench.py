@@ -1,5 +1,5 @@
 """Time the prefill scan at few sequences with the sequential (num_chunks = 1) and the chunked
-(num_chunks = 4) scan: per-launch scan time from the library's event records, and one block's
+(num_chunks = 4, 8) scan: per-launch scan time from the library's event records, and one block's
 prefill.  python tools/scan_chunk_bench.py [--config c2] [--B 1] [--T 2048]"""
 import argparse
 import os
@@ -20,7 +20,7 @@ L.load()
 cfg = synth.CONFIGS[args.config]
 T = args.T or cfg.prefill_T
 x = synth.hidden((args.B, T, cfg.d), synth.generator(3, "cuda"), cfg.dtype, device="cuda")
-for nc in (1, 4):
+for nc in (1, 4, 8):
     st = model.Stack.random(cfg, device="cuda", gen_device="cuda", n_blocks=1, num_chunks=nc)
     hs = st.new_state(args.B)
     for _ in range(3):
