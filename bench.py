@@ -474,7 +474,11 @@ def other_config_prefill(name: str, steps: int, warmup: int, pk: dict, dev) -> d
     torch.cuda.synchronize()
     L.tern_profile_enable(False)
     recs = L.tern_profile_collect()
-    rl, kernels = roofline(recs, 2 if cfg.dtype == "bf16" else 4, pk, {}, ck)
+    try:   # this config's ncu --set full capture (profiles/traffic.json), if any
+        tdb = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(cfg.name, {})
+    except Exception:
+        tdb = {}
+    rl, kernels = roofline(recs, 2 if cfg.dtype == "bf16" else 4, pk, tdb, ck)
     out = {"workload": f"{name}: {cfg.L}-block stack d={cfg.d} l={cfg.l} {cfg.dtype}, prefill "
                        f"{B}x{T}", "tokens_per_s": round(B * T * steps / (ms / 1e3), 1),
            "ms_per_step": round(ms / steps, 3), "steps": steps, "warmup": warmup,
