@@ -534,6 +534,11 @@ def test_mlgru_scan_slices_mode():
     assert np.array_equal(o4[:, :10], o1[:, :10])          # slice 0 starts from the true state
     assert np.allclose(o4, o1, rtol=1e-5, atol=1e-6)
     assert np.allclose(H4, H1, rtol=1e-5, atol=1e-6)
+    with O.scan_slices(8):                                  # tern_mlgru.num_chunks = 8
+        o8, H8 = O.mlgru_scan(fh, ch, gh, H)
+    assert np.array_equal(o8[:, :5], o1[:, :5])
+    assert np.allclose(o8, o1, rtol=1e-5, atol=1e-6)
+    assert np.allclose(H8, H1, rtol=1e-5, atol=1e-6)
     with O.scan_slices(1):
         assert np.array_equal(O.mlgru_scan(fh, ch, gh, H)[0], o1)
 
