@@ -493,7 +493,8 @@ tern_status tern_fxp_bitlinear(const int16_t* xq, const int32_t* ex, int32_t m, 
  * the same except that results below 2^-126 may be 0;
  * which = 3: the conversion-free round half away from zero used by every
  * quantizer (and its integer extraction) equals the reference for every
- * float with |v| < 2^22. 
+ * float with |v| < 2^22;
+ * which = 4: the round-toward-zero form of it (k_quant's) equals the same. 
  * Synchronous; writes the mismatch count to *mismatches (host).  ws: device
  * scratch of >= 64 bytes. */
 tern_status tern_selftest(int32_t which, void* ws, uint64_t* mismatches);

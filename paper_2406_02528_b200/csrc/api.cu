@@ -268,7 +268,7 @@ extern "C" {
 int tern_abi_version(void) { return TERN_ABI_VERSION; }
 
 tern_status tern_selftest(int32_t which, void* ws, uint64_t* mismatches) {
-  CHECK(ws && mismatches && aligned16(ws) && which >= 0 && which <= 3, "tern_selftest: args");
+  CHECK(ws && mismatches && aligned16(ws) && which >= 0 && which <= 4, "tern_selftest: args");
   tern_status st = check_device();
   if (st) return st;
   static const int exps[11] = {0, 1, 2, 5, 10, 20, 40, 60, 80, 100, 119};

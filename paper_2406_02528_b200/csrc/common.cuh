@@ -150,6 +150,17 @@ __device__ __forceinline__ float round_half_away_small(float v) {
 __device__ __forceinline__ int int_of_integral(float r) {
   return __float_as_int(__fadd_rn(r, 12582912.0f)) - 0x4B400000;
 }
+// int_of_integral(round_half_away_small(v)) in fewer instructions, for |v| < 2^22:
+// w = v + copysign(1/2, v) rounded toward zero, then w's integer part (toward zero) from the
+// bits of w + copysign(1.5 * 2^23, v), also rounded toward zero.  Exact: rounding toward zero
+// never steps over an integer (integers are floats), so trunc(fl_rz(v +- 1/2)) ==
+// trunc(v +- 1/2) == round half away from zero (checked for every such float: tern_selftest 4)
+__device__ __forceinline__ int rha_int_small(float v) {
+  const uint32_t sg = __float_as_uint(v) & 0x80000000u;
+  const float w = __fadd_rz(v, __uint_as_float(sg | 0x3f000000u));
+  const uint32_t b = __float_as_uint(__fadd_rz(w, __uint_as_float(sg | 0x4B400000u)));
+  return sg ? (int)(0xCB400000u - b) : (int)(b - 0x4B400000u);
+}
 
 // bf16 storage rounding (R0-R3): round to nearest even and widen back.
 __device__ __forceinline__ float bf16r(float v) {

@@ -155,7 +155,7 @@ __device__ __forceinline__ void centred_row(const uint4 (&xv)[NV], bool rv, int 
         if (v < nvec) {
           float y = __fmul_rn(__fsub_rn(xf[4 * j4 + j], mu), r);
           if (gain) y = __fmul_rn(y, __ldg(gain + v * VE + 4 * j4 + j));
-          qi[j] = int_of_integral(round_half_away_small(__fmul_rn(y, sc)));
+          qi[j] = rha_int_small(__fmul_rn(y, sc));
         }
         qs += qi[j];
       }
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
         float y = __fmul_rn(xf[4 * j4 + j], r);
         if (GAIN) y = __fmul_rn(y, g[j]);
         // |y*sc| <= 127(1+2^-23), so the clamp to [-128,127] (C5) never acts
-        qi[j] = int_of_integral(round_half_away_small(__fmul_rn(y, sc)));
+        qi[j] = rha_int_small(__fmul_rn(y, sc));
         qs += qi[j];
       }
       // low bytes of the four ints -> one word (two byte permutes)

@@ -61,6 +61,19 @@ __global__ void k_selftest_rha(unsigned long long* bad) {
   if (nb) atomicAdd(bad, nb);
 }
 
+// 4: rha_int_small == int_of_integral(round_half_away(v)) for every float with |v| < 2^22
+__global__ void k_selftest_rha_int(unsigned long long* bad) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;  // mantissa
+  if (m >= (1u << 23)) return;
+  unsigned long long nb = 0;
+  for (uint32_t ex = 0; ex <= 148; ++ex)
+    for (uint32_t sg = 0; sg < 2; ++sg) {
+      const float v = __uint_as_float((sg << 31) | (ex << 23) | m);
+      nb += rha_int_small(v) != int_of_integral(round_half_away(v));
+    }
+  if (nb) atomicAdd(bad, nb);
+}
+
 cudaError_t launch_selftest(int which, unsigned long long* bad, int* exps, int n_exp,
                             cudaStream_t s) {
   (void)exps;
@@ -71,8 +84,10 @@ cudaError_t launch_selftest(int which, unsigned long long* bad, int* exps, int n
     k_selftest_sigmoid<<<(1 << 24) / 256, 256, 0, s>>>(bad);
   } else if (which == 2) {
     k_selftest_sigmoid2<<<(1 << 23) / 256, 256, 0, s>>>(bad);
-  } else {
+  } else if (which == 3) {
     k_selftest_rha<<<(1 << 23) / 256, 256, 0, s>>>(bad);
+  } else {
+    k_selftest_rha_int<<<(1 << 23) / 256, 256, 0, s>>>(bad);
   }
   return cudaGetLastError();
 }
