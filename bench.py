@@ -243,7 +243,7 @@ def algo_work(rec: dict, elem: int) -> tuple[str, float]:
     """(unit, amount) of algorithmic work of one launch."""
     k, m, n = rec["k"], rec["m"], rec["n"]
     kp = (k + 127) // 128 * 128
-    if rec["kernel"] in ("gemm_tc", "fcgscan"):
+    if rec["kernel"] in ("gemm_tc", "fcgscan", "gemm_qf"):
         return "flop", 2.0 * m * n * k                       # dense-equivalent int8 ops
     if rec["kernel"] == "quant":
         return "byte", m * k * elem + m * kp + 12.0 * m      # read x, write q + stats
@@ -254,14 +254,25 @@ def algo_work(rec: dict, elem: int) -> tuple[str, float]:
     return "byte", 0.0
 
 
+def qf_bytes(rec: dict, elem: int) -> float:
+    """HBM bytes of the fused quantization inside a gemm_qf launch: the a2 pass it replaces
+    (read x, write q + stats) and the GEMM's own A read of q."""
+    k, m = rec["k"], rec["m"]
+    kp = (k + 127) // 128 * 128
+    return m * k * elem + 2.0 * m * kp + 12.0 * m
+
+
 def roofline(records, elem, pk, traffic_db, clocks=None):
     by = {}
     for r in records:
         u, w = algo_work(r, elem)
-        e = by.setdefault(r["kernel"], {"ms": 0.0, "work": 0.0, "unit": u, "launches": 0})
+        e = by.setdefault(r["kernel"], {"ms": 0.0, "work": 0.0, "unit": u, "launches": 0,
+                                        "bytes": 0.0})
         e["ms"] += r["ms"]
         e["work"] += w
         e["launches"] += 1
+        if r["kernel"] == "gemm_qf":
+            e["bytes"] += qf_bytes(r, elem)
     tot = sum(e["ms"] for e in by.values()) or 1.0
     kernels = {}
     i8peak, i8src = int8_peak_for(pk, clocks)
@@ -283,6 +294,13 @@ def roofline(records, elem, pk, traffic_db, clocks=None):
                              # fraction of N(0, s) weights at the 1/2 mean|W| threshold:
                              # P(|z| < sqrt(2/pi)/2) = 0.310 (31.0 % measured)
                              "ternary_adds_T_per_s": round(ach / 2.0 * (1.0 - ZERO_FRAC), 1)}
+            if e["bytes"] > 0:   # gemm_qf: the fused quantization's HBM stream beside the MMAs
+                hb = e["bytes"] / s / 1e9
+                kernels[name]["fused_quant_hbm"] = {
+                    "achieved": round(hb, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": round(hb / pk["hbm_gbs"], 4),
+                    "note": "bytes of the a2 quantization fused into this GEMM (read x, write "
+                            "q + stats, the GEMM's A read), over the same launch time"}
         else:
             ach = e["work"] / s / 1e9
             peak = pk["hbm_gbs"]
@@ -294,7 +312,7 @@ def roofline(records, elem, pk, traffic_db, clocks=None):
     epi_names = {0: "store", 1: "resid", 2: "fcg", 3: "mlgru", 4: "swiglu", 5: "acc"}
     sub = {}
     for r in records:
-        if r["kernel"] not in ("gemm_tc", "gemv", "fcgscan"):
+        if r["kernel"] not in ("gemm_tc", "gemm_qf", "gemv", "fcgscan"):
             continue
         key = f'{r["kernel"]}:{epi_names.get(r["epi"], r["epi"])}:n{r["n"]}k{r["k"]}'
         u, w = algo_work(r, elem)

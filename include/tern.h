@@ -363,7 +363,9 @@ tern_status stack_decode(const tern_block* blocks, int32_t L, const void* x, voi
  * kept until the next tern_profile_enable(1).  Not for use in production.
  * ------------------------------------------------------------------------ */
 typedef enum { TERN_K_QUANT = 0, TERN_K_GEMV = 1, TERN_K_GEMM = 2, TERN_K_SCAN = 3,
-               TERN_K_FCGSCAN = 4, TERN_K_STACK = 5, TERN_K_FIN = 6 } tern_kernel_id;
+               TERN_K_FCGSCAN = 4, TERN_K_STACK = 5, TERN_K_FIN = 6,
+               TERN_K_GEMM_QF = 7 /* GEMM with the a2 quantization of its A fused in */
+             } tern_kernel_id;
 typedef struct {
   int32_t kernel;   /* tern_kernel_id                                        */
   int32_t epi;      /* epilogue kind (GEMV/GEMM) or gate mode (scan)         */
@@ -538,6 +540,14 @@ int32_t tern_get_gemm_sab(void);
  * CTAs (128 x 256 tiles).  Results are identical.  Initial value: env TERN_GEMM_2SM, else 1. */
 void tern_set_gemm_2sm(int32_t on);
 int32_t tern_get_gemm_2sm(void);
+/* Tuning knob (host): 1 fuses the RMSNorm + int8 quantization (a2) of the
+ * o, gate|up and down BitLinears' inputs into their prefill GEMMs (block_prefill, mlgru_fwd,
+ * glu_fwd with M > 256 tokens): the GEMM's warps 2-5 quantize rows in order and publish
+ * 128-row blocks through counters in the block workspace, the TMA producer waits for a
+ * block before loading it; no standalone quant launch.  Bit-identical results; default 0
+ * (measured slower than quant + GEMM on B200: DESIGN.md section 6). */
+void tern_set_qfuse(int32_t on);
+int32_t tern_get_qfuse(void);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -83,7 +83,7 @@ class tern_prof_rec(C.Structure):
                 ("k", C.c_int32), ("n_seg", C.c_int32), ("dtype", C.c_int32), ("ms", C.c_float)]
 
 
-KERNEL_NAMES = {0: "quant", 1: "gemv", 2: "gemm_tc", 3: "scan", 4: "fcgscan", 5: "stack", 6: "fin"}
+KERNEL_NAMES = {0: "quant", 1: "gemv", 2: "gemm_tc", 3: "scan", 4: "fcgscan", 5: "stack", 6: "fin", 7: "gemm_qf"}
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -129,6 +129,8 @@ _SIGS = {
     "tern_set_batched_fin": (None, [I32]),
     "tern_set_gemm_sab": (None, [I32]),
     "tern_set_gemm_2sm": (None, [I32]),
+    "tern_set_qfuse": (None, [I32]),
+    "tern_get_qfuse": (I32, []),
     "tern_get_gemm_2sm": (I32, []),
     "tern_get_gemm_sab": (I32, []),
     "tern_set_norm_mode": (None, [C.c_int]),
@@ -336,6 +338,15 @@ def tern_set_gemm_sab(on: bool):
 
 def tern_set_gemm_2sm(on: bool):
     load().tern_set_gemm_2sm(1 if on else 0)
+
+
+def tern_set_qfuse(on: bool):
+    """f3: the a2 quantization fused into the prefill GEMMs (opt-in, include/tern.h)."""
+    load().tern_set_qfuse(1 if on else 0)
+
+
+def tern_get_qfuse() -> bool:
+    return bool(load().tern_get_qfuse())
 
 
 def tern_get_gemm_2sm() -> bool:

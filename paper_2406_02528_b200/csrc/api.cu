@@ -146,7 +146,7 @@ Epi make_epi(int kind, const tern_weight& w, const float* bias, void* out, int l
 }
 
 struct BlockWs {
-  size_t q, deq, qsum, fcg, oprime, x1, p, sout, gbuf, stl, stg, qsend, qgath, accb, part,
+  size_t q, deq, qsum, qf, fcg, oprime, x1, p, sout, gbuf, stl, stg, qsend, qgath, accb, part,
       part_bytes, total;
 };
 // world > 1 adds the rank's local outputs [M][max(ds,ls)] and the gather
@@ -159,6 +159,9 @@ BlockWs block_ws(int32_t M, int32_t d, int32_t l, int32_t fcg_rows, tern_dtype d
   w.q = off; off += al256((size_t)M * kq);
   w.deq = off; off += al256((size_t)M * 4);
   w.qsum = off; off += al256((size_t)M * 4);
+  // fused-quantization counters (QFuse): one area per fused GEMM of the block (o, gate|up,
+  // down), zeroed by the block's first quant launch
+  w.qf = off; off += al256((size_t)kQfAreas * qf_words(M) * 4);
   w.fcg = off; off += al256((size_t)M * fcg_rows * dsize(dt));
   w.oprime = off; off += al256((size_t)M * d * dsize(dt));
   w.x1 = off; off += al256((size_t)M * d * dsize(dt));
@@ -206,14 +209,32 @@ tern_status bl_tc(const void* x, tern_dtype xdt, int M, int K, int ldx, const fl
                   float eps, const tern_weight& w, tern_dtype ydt, const Epi& epi, int8_t* q,
                   int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
                   cudaStream_t s, int32_t* part = nullptr, size_t part_bytes = 0,
-                  int norm = TERN_NORM_RMS) {
+                  int norm = TERN_NORM_RMS, uint32_t* zero = nullptr, int nzero = 0) {
   {
     Prof p(TERN_K_QUANT, 0, M, 0, K, 0, xdt, s);
-    TRY_CUDA(launch_quant(x, xdt, M, K, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm),
+    TRY_CUDA(launch_quant(x, xdt, M, K, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm,
+                          zero, nzero),
              "quant");
   }
   Prof p(TERN_K_GEMM, epi.kind, M, w.n_rows, w.k, w.n_seg, ydt, s);
   TRY_CUDA(launch_gemm(q, M, ldq, deq, qsum, w, ydt, epi, s, part, part_bytes), "gemm");
+  return TERN_OK;
+}
+
+// The same BitLinear with the a2 quantization fused into the GEMM (f3, k_gemm.cu "fused
+// quantization") when the shape takes the large-M tensor-core path and the norm is the
+// RMSNorm; ctr = a zeroed QFuse counter area.  Otherwise quant + GEMM as bl_tc.
+tern_status bl_tc_qf(const void* x, tern_dtype dt, int M, int K, const float* gain, float eps,
+                     const tern_weight& w, const Epi& epi, int8_t* q, int ldq, float* deq,
+                     int32_t* qsum, uint32_t* ctr, cudaStream_t s, int32_t* part,
+                     size_t part_bytes, int norm) {
+  if (ctr == nullptr || norm != TERN_NORM_RMS || !gemm_qfuse_ok(M, w, epi, part, part_bytes))
+    return bl_tc(x, dt, M, K, K, gain, eps, w, dt, epi, q, ldq, deq, qsum, nullptr, nullptr, s,
+                 part, part_bytes, norm);
+  QFuse qf{x, K, gain, eps, ctr};
+  Prof p(TERN_K_GEMM_QF, epi.kind, M, w.n_rows, w.k, w.n_seg, dt, s);
+  TRY_CUDA(launch_gemm(q, M, ldq, deq, qsum, w, dt, epi, s, part, part_bytes, nullptr, &qf),
+           "gemm + fused quant");
   return TERN_OK;
 }
 
@@ -323,6 +344,8 @@ int32_t tern_get_gemv_max_m(void) { return g_gemv_max_m; }
 void tern_set_batched_fin(int32_t on) { g_batched_fin = on ? 1 : 0; }
 void tern_set_gemm_sab(int32_t on) { g_gemm_sab = on ? 1 : 0; }
 void tern_set_gemm_2sm(int32_t on) { g_gemm_2sm = on ? 1 : 0; }
+void tern_set_qfuse(int32_t on) { g_qfuse_on = on ? 1 : 0; }
+int32_t tern_get_qfuse(void) { return g_qfuse_on; }
 int32_t tern_get_gemm_2sm(void) { return g_gemm_2sm; }
 int32_t tern_get_gemm_sab(void) { return g_gemm_sab; }
 void tern_set_norm_mode(tern_norm_mode mode) {
@@ -751,6 +774,10 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   int32_t* qsum = at<int32_t>(ws, L.qsum);
   void* fcg = at<char>(ws, L.fcg);
   const int ldq = kpad(d);
+  // QFuse counter areas of this block's fused GEMMs (o, gate|up, down): the first quant
+  // launch below zeroes them
+  uint32_t* qf0 = at<uint32_t>(ws, L.qf);
+  const int nqf = kQfAreas * qf_words(M);
   // the prefill scan: sequential (1) or chunked over time (4, 8; tern_mlgru.num_chunks)
   const int chunks = T > 1 ? scan_chunks_resolve(p.num_chunks, B, T, d) : 1;
   // the fused kernel walks each sequence's 128-token tiles; short sequences (decode
@@ -770,7 +797,7 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
     {
       Prof pr(TERN_K_QUANT, 0, M, 0, d, 0, dt, s);
       TRY_CUDA(launch_quant(x, dt, M, d, d, p.gain_x, p.eps, q, ldq, deq, qsum, nullptr, nullptr, s,
-                            p.norm),
+                            p.norm, qf0, nqf),
                "quant");
     }
     Prof pr(TERN_K_FCGSCAN, p.gate, M, p.fcg.n_rows, d, 3, dt, s);
@@ -779,7 +806,8 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   } else {
     Epi e1 = make_epi(EPI_FCG, p.fcg, p.bias_fcg, fcg, p.fcg.n_rows);
     tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.fcg, dt, e1, q, ldq, deq, qsum,
-                           nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
+                           nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm,
+                           qf0, nqf);
     if (st) return st;
     Prof pr(TERN_K_SCAN, p.gate, B * T, d, d, 3, dt, s);
     TRY_CUDA(launch_scan_chunks(fcg, dt, B, T, d, p.gate, h, op, chunks, s), "scan");
@@ -787,14 +815,15 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.o, p.bias_o, out, d);
   e2.res = x;
   e2.ldr = d;
-  return bl_tc(op, dt, M, d, d, p.gain_o, p.eps, p.o, dt, e2, q, ldq, deq, qsum, nullptr, nullptr,
-               s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
+  // o' is quantized inside the o GEMM (counter area 0, zeroed by the quant of x above)
+  return bl_tc_qf(op, dt, M, d, p.gain_o, p.eps, p.o, e2, q, ldq, deq, qsum, qf0, s,
+                  at<int32_t>(ws, L.part), L.part_bytes, p.norm);
 }
 
 // channel mixer: x [M][d] -> out (d, or y = x + d when resid)
 tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, tern_dtype dt, int M,
                     int d, int l, void* ws, const BlockWs& L, cudaStream_t s,
-                    const PfPlan& pf = PfPlan()) {
+                    const PfPlan& pf = PfPlan(), bool qf_ready = false) {
   void* pp = at<char>(ws, L.p);
   Epi e1 = make_epi(EPI_SWIGLU, p.gu, nullptr, pp, l);
   Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.down, nullptr, out, d);
@@ -816,11 +845,18 @@ tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, ter
   int8_t* q = at<int8_t>(ws, L.q);
   float* deq = at<float>(ws, L.deq);
   int32_t* qsum = at<int32_t>(ws, L.qsum);
-  tern_status st = bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.gu, dt, e1, q, kpad(d), deq, qsum,
-                         nullptr, nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
+  // QFuse counter areas 1 (gate|up) and 2 (down); qf_ready: zeroed by the token mixer's
+  // first quant launch (block prefill), else by the quant of x here
+  uint32_t* qf0 = at<uint32_t>(ws, L.qf);
+  const int qw = qf_words(M);
+  tern_status st = qf_ready
+      ? bl_tc_qf(x, dt, M, d, p.gain_x, p.eps, p.gu, e1, q, kpad(d), deq, qsum, qf0 + qw, s,
+                 at<int32_t>(ws, L.part), L.part_bytes, p.norm)
+      : bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.gu, dt, e1, q, kpad(d), deq, qsum, nullptr,
+              nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm, qf0, kQfAreas * qw);
   if (st) return st;
-  return bl_tc(pp, dt, M, l, l, p.gain_p, p.eps, p.down, dt, e2, q, kpad(l), deq, qsum, nullptr,
-               nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
+  return bl_tc_qf(pp, dt, M, l, p.gain_p, p.eps, p.down, e2, q, kpad(l), deq, qsum, qf0 + 2 * qw,
+                  s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);
 }
 
 // one BitLinear on either path (decode GEMV with its fused prologue, or quant + GEMM)
@@ -1169,7 +1205,8 @@ static tern_status block_run(const tern_block* b, const void* x, void* y, tern_d
     }
   }
   if ((st = run_mlgru(b->mix, x, x1, true, dt, B, T, b->d, h, ws, L, s, pm)) != TERN_OK) return st;
-  return run_glu(b->ch, x1, y, true, dt, B * T, b->d, b->l, ws, L, s, pg);
+  // prefill: the token mixer's quant of x zeroed the gate|up counters (QFuse)
+  return run_glu(b->ch, x1, y, true, dt, B * T, b->d, b->l, ws, L, s, pg, T > 1);
 }
 
 // ---------------------------------------------------------------- sequence-parallel prefill

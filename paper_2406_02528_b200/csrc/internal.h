@@ -59,7 +59,23 @@ size_t pack_workspace_bytes();
 // a2
 cudaError_t launch_quant(const void* x, int xdt, int m, int k, int ldx, const float* gain,
                          float eps, int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
-                         float* absmax, cudaStream_t s, int norm = TERN_NORM_RMS);
+                         float* absmax, cudaStream_t s, int norm = TERN_NORM_RMS,
+                         uint32_t* zero = nullptr, int nzero = 0);
+// a2 fused into the consuming GEMM (f3; k_gemm.cu "fused quantization"): the GEMM's idle
+// warps 2-5 run the RMSNorm + absmax quantization of x row by row (rows taken
+// in a static order), publishing each finished 128-row block in ctr[1 + block]; the TMA
+// producer waits for a block before loading its A tiles.  ctr must be zero at launch
+// ([1 + ceil(M/128)] words; block_ws region qf, zeroed by the block's first quant launch).
+struct QFuse {
+  const void* x;
+  int ldx;
+  const float* gain;   // NULL = ones
+  float eps;
+  uint32_t* ctr;
+};
+extern int g_qfuse_on;   // tern_set_qfuse
+constexpr int kQfAreas = 3;   // o, gate|up, down (one counter area per fused GEMM of a block)
+inline int qf_words(int M) { return 1 + (M + 127) / 128; }
 // a3 (decode GEMV, norm+quant prologue fused): x [M][ldx] -> epilogue
 constexpr int kGemvMaxM = 4;
 bool gemv_supported(int M, int K, int xdt);   // M <= kGemvMaxM and K within the register tile
@@ -84,7 +100,10 @@ cudaError_t launch_splitk_epi(const int32_t* part, int ks, int M, int n_rows, co
 // epilogue runs (launch_fin finalizes); *ks_out > 0 on entry caps the count
 cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
-                        int32_t* part = nullptr, size_t part_bytes = 0, int* ks_out = nullptr);
+                        int32_t* part = nullptr, size_t part_bytes = 0, int* ks_out = nullptr,
+                        const QFuse* qf = nullptr);
+// whether launch_gemm runs a QFuse request inside the GEMM (else it launches k_quant first)
+bool gemm_qfuse_ok(int M, const tern_weight& w, const Epi& epi, int32_t* part, size_t part_bytes);
 // batched decode: one CTA per row sums the ks partial slices [ks][M][n_rows],
 // applies e (MLGRU / SWIGLU / RESID / STORE) and, when nq is set, the next
 // BitLinear's RMSNorm + int8 quant of the stored output row (gain ngain, eps

@@ -75,6 +75,19 @@ struct GemmArgs {
   const int32_t* qsum;
   Epi epi;
   unsigned long long* prof;  // debug (TERN_GEMM_PROF): [grid][8] wait cycles per site
+  // fused quantization of A (QFuse, qctr != NULL): warps 2-5 quantize rows of qx into
+  // q = the A operand (qq, ldq), deq and qsum; qctr[0] reserved, qctr[1 + b] publishes
+  // 128-row block b (complete at 128)
+  const void* qx;
+  int qldx, qK, qmb;         // qmb = ceil(M / 128) blocks
+  const float* qgain;
+  float qeps;
+  double qinv_k;
+  int8_t* qq;
+  int qldq;
+  float* qdeq;
+  int32_t* qqsum;
+  uint32_t* qctr;
 #ifdef TERN_TRACE
   unsigned long long* trace; // tern_trace_enable timeline (trace build only)
 #endif
@@ -180,6 +193,244 @@ __device__ void acc_tap_chunk(const Epi& e, const GemmArgs& a, int* si, int lane
     if (row0 + r < a.M && col0 + lane < a.n_rows)
       e.acc[(int64_t)(row0 + r) * e.ldacc + col0 + lane] = si[r * 32 + (lane ^ r)];
   __syncwarp();
+}
+
+// ----------------------------------------------------------------- fused quantization (f3)
+// a2 (RMSNorm + per-token absmax int8, readings C1-C5; DESIGN.md "Canonical
+// numerics") run by the GEMM's otherwise idle warps 2-5 while the tensor cores work on
+// blocks already quantized: the A operand of 128-row block b is published in qctr[1 + b]
+// (a release add per finished row; the producer waits for 128 with acquire loads, then a
+// generic -> async proxy fence before its TMA reads), so no standalone quant launch, no
+// launch gap, and the quantization's HBM traffic overlaps the MMAs.  The arithmetic is
+// k_quant's (binary64 fma sum of squares in a fixed per-warp tree order, C4; the 1-ulp
+// binary64 rsqrt; fl(max|x| r) when there is no gain; IEEE divisions; round half away).
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// block until 128-row block mb of the fused quantization is published
+__device__ __forceinline__ void qf_wait_block(const uint32_t* ctr, int mb) {
+  const uint32_t* f = ctr + 1 + mb;
+  if (ld_acquire_u32(f) >= 128u) return;
+  const unsigned long long t0 = gtimer();
+  while (ld_acquire_u32(f) < 128u) {
+    __nanosleep(40);
+    if (gtimer() - t0 > 4000000000ull) __trap();   // watchdog (4 s), as mbar_wait
+  }
+}
+template <typename TY> __device__ __forceinline__ void qf_unpack(const uint4& u, float* v);
+template <> __device__ __forceinline__ void qf_unpack<float>(const uint4& u, float* v) {
+  v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y);
+  v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
+}
+template <> __device__ __forceinline__ void qf_unpack<__nv_bfloat16>(const uint4& u, float* v) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+constexpr int kQfCh = 8;   // 16-byte vectors per lane per chunk of a row
+
+// one chunk of the row (kQfCh vectors per lane, vector v = c*256 + i*32 + lane)
+template <typename TY>
+__device__ __forceinline__ void qf_load_chunk(const uint4* xr, bool rv, int c, int nvec, int lane,
+                                              uint4 (&xv)[kQfCh]) {
+#pragma unroll
+  for (int i = 0; i < kQfCh; ++i) {
+    const int v = c * 32 * kQfCh + i * 32 + lane;
+    xv[i] = (rv && v < nvec) ? __ldg(xr + v) : make_uint4(0, 0, 0, 0);
+  }
+}
+// quantize one loaded chunk: q bytes of vectors < nvecp (zeros beyond K = the padding)
+template <typename TY>
+__device__ __forceinline__ int qf_quant_chunk(const uint4 (&xv)[kQfCh], int c, int nvec, int nvecp,
+                                              int lane, float r, float sc, const float* gain,
+                                              int8_t* qr, bool rv) {
+  constexpr int VE = 16 / sizeof(TY);
+  int qs = 0;
+#pragma unroll
+  for (int i = 0; i < kQfCh; ++i) {
+    const int v = c * 32 * kQfCh + i * 32 + lane;
+    float xf[VE];
+    qf_unpack<TY>(xv[i], xf);
+    uint32_t pk[VE / 4];
+#pragma unroll
+    for (int j4 = 0; j4 < VE / 4; ++j4) {
+      int qi[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float y = __fmul_rn(xf[4 * j4 + j], r);
+        if (gain != nullptr && v < nvec) y = __fmul_rn(y, __ldg(gain + v * VE + 4 * j4 + j));
+        qi[j] = rha_int_small(__fmul_rn(y, sc));
+        qs += qi[j];
+      }
+      pk[j4] = __byte_perm(__byte_perm(qi[0], qi[1], 0x0040), __byte_perm(qi[2], qi[3], 0x0040),
+                           0x5410);
+    }
+    if (rv && v < nvecp) {
+      if (VE == 4)
+        reinterpret_cast<uint32_t*>(qr)[v] = pk[0];
+      else
+        reinterpret_cast<uint2*>(qr)[v] = make_uint2(pk[0], pk[VE / 4 - 1]);
+    }
+  }
+  return qs;
+}
+template <typename TY>
+__device__ __forceinline__ void qf_stats_chunk(const uint4 (&xv)[kQfCh], double& s0, double& s1,
+                                               float& xm) {
+  constexpr int VE = 16 / sizeof(TY);
+#pragma unroll
+  for (int i = 0; i < kQfCh; ++i) {
+    float v[VE];
+    qf_unpack<TY>(xv[i], v);
+#pragma unroll
+    for (int j = 0; j < VE; j += 2) {
+      const double d0 = (double)v[j], d1 = (double)v[j + 1];
+      s0 = fma(d0, d0, s0);
+      s1 = fma(d1, d1, s1);
+      xm = fmaxf(xm, fmaxf(fabsf(v[j]), fabsf(v[j + 1])));
+    }
+  }
+}
+template <typename TY>
+__device__ __forceinline__ float qf_gain_max_chunk(const uint4 (&xv)[kQfCh], int c, int nvec, int lane,
+                                                   float r, const float* gain) {
+  constexpr int VE = 16 / sizeof(TY);
+  float am = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kQfCh; ++i) {
+    const int v = c * 32 * kQfCh + i * 32 + lane;
+    if (v >= nvec) continue;
+    float xf[VE];
+    qf_unpack<TY>(xv[i], xf);
+#pragma unroll
+    for (int j = 0; j < VE; ++j)
+      am = fmaxf(am, fabsf(__fmul_rn(__fmul_rn(xf[j], r), __ldg(gain + v * VE + j))));
+  }
+  return am;
+}
+
+// one row by one warp, NCH chunks of kQfCh 16-byte vectors per lane (NCH == 1: the row
+// stays in registers between the two passes; else the second pass reloads it, from L1/L2)
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+// make this warp's stores of a finished row visible, then count the row in its block
+__device__ __forceinline__ void qf_publish(uint32_t* ctr, int row, int lane) {
+  fence_proxy_async_global();   // generic -> async proxy (the consumers read q by TMA)
+  fence_acq_rel_gpu();
+  __syncwarp();
+  if (lane == 0) red_release_add(ctr + 1 + (row >> 7), 1u);
+}
+
+// One row by one warp, NCH chunks of kQfCh 16-byte vectors per lane (NCH == 1: the row
+// stays in registers between the two passes; else the second pass reloads it, from L1/L2).
+// The previous row of this warp is published between the passes, when its stores have
+// long been issued (the fence then rarely waits).
+template <typename TY, int NCH>
+__device__ __forceinline__ void qf_row(const GemmArgs& a, int cur, int prev, int lane) {
+  constexpr int VE = 16 / sizeof(TY);
+  const int K = a.qK, nvec = K / VE, nvecp = a.num_kb * kBK / VE;
+  const TY* x = static_cast<const TY*>(a.qx);
+  const bool rv = cur < a.M;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)(rv ? cur : 0) * a.qldx);
+  int8_t* qr = a.qq + (int64_t)(rv ? cur : 0) * a.qldq;
+  double s0 = 0.0, s1 = 0.0;
+  float xm = 0.0f;
+  uint4 xv[kQfCh];
+  qf_load_chunk<TY>(xr, rv, 0, nvec, lane, xv);
+  qf_stats_chunk<TY>(xv, s0, s1, xm);
+#pragma unroll 1
+  for (int c = 1; c < NCH; ++c) {
+    uint4 xc[kQfCh];
+    qf_load_chunk<TY>(xr, rv, c, nvec, lane, xc);
+    qf_stats_chunk<TY>(xc, s0, s1, xm);
+  }
+  double ss = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    xm = fmaxf(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+  }
+  if (prev >= 0) qf_publish(a.qctr, prev, lane);
+  const float r = (float)rsqrt(fma(ss, a.qinv_k, (double)a.qeps));
+  float amax;
+  if (a.qgain == nullptr) {
+    amax = __fmul_rn(xm, r);   // max|fl(x r)| = fl(max|x| r): rounding is monotone, r > 0
+  } else {
+    float am = qf_gain_max_chunk<TY>(xv, 0, nvec, lane, r, a.qgain);
+#pragma unroll 1
+    for (int c = 1; c < NCH; ++c) {
+      uint4 xc[kQfCh];
+      qf_load_chunk<TY>(xr, rv, c, nvec, lane, xc);
+      am = fmaxf(am, qf_gain_max_chunk<TY>(xc, c, nvec, lane, r, a.qgain));
+    }
+    amax = warp_max_f32(am);
+  }
+  const float sc = amax > 0.0f ? __fdiv_rn(127.0f, amax) : 0.0f;
+  int qs = 0;
+  if (NCH == 1) {
+    qs = qf_quant_chunk<TY>(xv, 0, nvec, nvecp, lane, r, sc, a.qgain, qr, rv);
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < NCH; ++c) {
+      uint4 xc[kQfCh];
+      qf_load_chunk<TY>(xr, rv, c, nvec, lane, xc);
+      qs += qf_quant_chunk<TY>(xc, c, nvec, nvecp, lane, r, sc, a.qgain, qr, rv);
+    }
+  }
+  qs = warp_sum_i32(qs);
+  if (lane == 0 && rv) {
+    a.qdeq[cur] = amax > 0.0f ? __fdiv_rn(amax, 127.0f) : 0.0f;
+    a.qqsum[cur] = qs;
+  }
+}
+
+// warps 2-5: static row assignment, row = gw + i * GW over the grid's quant warps (in row
+// order, so blocks complete in the order the tile schedule needs them; every CTA of the
+// persistent grid is resident, so no warp waits on a row that cannot progress); the
+// rows two ahead are prefetched into L2
+template <typename TY, int NCH>
+__device__ void qf_quant_loop(const GemmArgs& a, int qw, int lane) {
+  const int mpad = a.qmb * 128;
+  const int GW = gridDim.x * 4, gw = blockIdx.x * 4 + qw;
+  const TY* x = static_cast<const TY*>(a.qx);
+  const uint32_t row_bytes = (uint32_t)a.qK * sizeof(TY);
+  if (lane == 0)
+    for (int j = 0; j < 2; ++j)
+      if (gw + j * GW < a.M) prefetch_l2_bulk(x + (int64_t)(gw + j * GW) * a.qldx, row_bytes);
+  int prev = -1;
+  for (int cur = gw; cur < mpad; cur += GW) {
+    if (lane == 0 && cur + 2 * GW < a.M)
+      prefetch_l2_bulk(x + (int64_t)(cur + 2 * GW) * a.qldx, row_bytes);
+    qf_row<TY, NCH>(a, cur, prev, lane);
+    prev = cur;
+  }
+  if (prev >= 0) qf_publish(a.qctr, prev, lane);
+}
+template <typename TY>
+__device__ void qf_quant_warps(const GemmArgs& a, int qw, int lane) {
+  constexpr int VE = 16 / sizeof(TY);
+  const int nch = (a.num_kb * kBK / VE + 32 * kQfCh - 1) / (32 * kQfCh);
+  switch (nch) {
+    case 1: qf_quant_loop<TY, 1>(a, qw, lane); break;
+    case 2: qf_quant_loop<TY, 2>(a, qw, lane); break;
+    case 3: qf_quant_loop<TY, 3>(a, qw, lane); break;
+    default: qf_quant_loop<TY, 4>(a, qw, lane); break;
+  }
 }
 
 template <int BN, bool kPre, typename TY, bool RES = false, int EW = kEpiWarps>
@@ -288,6 +539,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int tile = t / a.ksplit, sp = t % a.ksplit;
         const int m0 = (tile / a.n_tiles) * kBM, n0 = (tile % a.n_tiles) * BN;
         const int kb1 = min(nk, (sp + 1) * a.kb_per);
+        if (a.qctr) {   // fused quantization: this tile's A rows must be published
+          qf_wait_block(a.qctr, m0 >> 7);
+          fence_proxy_async_global();
+        }
         for (int kb = sp * a.kb_per; kb < kb1; ++kb, ++g) {
           const int s = g % S;
           if (g >= (uint32_t)S) pwait(&empty[s], ((g / S) - 1) & 1, a.prof, 0);
@@ -341,7 +596,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp < Cfg::EW0) {
     // ---------------- unpack (warps 2-5, packed path): 2-bit fields -> u8 e, SW128 K-major
-    if (!kPre) {
+    // (u8 path: the fused quantization of A when requested)
+    if (kPre && EW == kEpiWarps) {
+      if (a.qctr) qf_quant_warps<TY>(a, warp - 2, lane);
+    } else if (!kPre) {
       const int tid = threadIdx.x - 64;
       const bool pt = tid == 0;
       uint32_t g = 0;
@@ -431,8 +689,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int row0 = m0 + quad * 32;
         const int row = row0 + lane;
         const bool rv = row < a.M;
-        const float deq = rv ? __ldg(a.deq + row) : 0.0f;
-        const int qsum = rv ? __ldg(a.qsum + row) : 0;
+        if (a.qctr) qf_wait_block(a.qctr, m0 >> 7);   // deq / qsum written in this kernel
+        const float deq = rv ? __ldcg(a.deq + row) : 0.0f;
+        const int qsum = rv ? __ldcg(a.qsum + row) : 0;
         const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
         for (int c = half; c < BN / 32; c += NG) {
@@ -513,8 +772,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       const int row = row0 + lane;
       const bool rv = row < a.M;
-      const float deq = rv ? __ldg(a.deq + row) : 0.0f;
-      const int qsum = rv ? __ldg(a.qsum + row) : 0;
+      if (a.qctr) qf_wait_block(a.qctr, m0 >> 7);   // deq / qsum written in this kernel
+      const float deq = rv ? __ldcg(a.deq + row) : 0.0f;
+      const int qsum = rv ? __ldcg(a.qsum + row) : 0;
       const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
       const bool swig = e.kind == EPI_SWIGLU;
       const int nch = swig ? BN / 64 : BN / 32;   // chunks (or gate/up pairs) per tile
@@ -766,6 +1026,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int t = cid; t < total; t += ncl) {
         const int m0 = (t / a.n_tiles) * 256 + (int)rank * 128;
         const int n0 = (t % a.n_tiles) * 256 + (int)rank * 128;
+        if (a.qctr) {   // fused quantization: this CTA's 128 A rows must be published
+          qf_wait_block(a.qctr, m0 >> 7);
+          fence_proxy_async_global();
+        }
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % kS2;
           if (g >= (uint32_t)kS2) mbar_wait(&empty[s], ((g / kS2) - 1) & 1);
@@ -862,8 +1126,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row0 = m0 + quad * 32;
       const int row = row0 + lane;
       const bool rv = row < a.M;
-      const float deq = rv ? __ldg(a.deq + row) : 0.0f;
-      const int qsum = rv ? __ldg(a.qsum + row) : 0;
+      if (a.qctr) qf_wait_block(a.qctr, m0 >> 7);   // deq / qsum written in this kernel
+      const float deq = rv ? __ldcg(a.deq + row) : 0.0f;
+      const int qsum = rv ? __ldcg(a.qsum + row) : 0;
       const uint32_t trow = tmem_base + acc * 256 + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
       for (int c = half; c < nch; c += 2) {
@@ -945,6 +1210,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lead) cl_arrive(temptyL + acc * 8);   // the leader's tempty[acc]
     }
     if (lead) bulk_wait<0>();
+  } else if (warp >= 2 && a.qctr) {
+    // ---------------- fused quantization of A (warps 2-5 of both CTAs)
+    qf_quant_warps<TY>(a, warp - 2, lane);
   }
   tc_fence_before();
   __syncthreads();
@@ -1090,7 +1358,7 @@ static cudaError_t gemm_dispatch_bn(int BN, const CUtensorMap& ta, const CUtenso
   static const int ew12 = getenv("TERN_GEMM_EW12") ? atoi(getenv("TERN_GEMM_EW12")) : 0;   // debug
   if constexpr (kPre) {
     if (BN == 256 && ew12 && a.epi.kind == EPI_SWIGLU && a.epi.acc == nullptr &&
-        a.part == nullptr && a.ksplit == 1)
+        a.part == nullptr && a.ksplit == 1 && a.qctr == nullptr)
       return gemm_launch<256, true, TY, false, 12>(ta, tb, to, tr, a, s);
   }
   return BN == 256 ? gemm_launch<256, kPre, TY>(ta, tb, to, tr, a, s)
@@ -1210,11 +1478,16 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
 int g_gemm_sab = getenv("TERN_GEMM_SAB") ? (atoi(getenv("TERN_GEMM_SAB")) != 0) : 0;
 int g_gemm_2sm = getenv("TERN_GEMM_2SM") ? (atoi(getenv("TERN_GEMM_2SM")) != 0) : 1;
 
-cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
-                        const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
-                        int32_t* part, size_t part_bytes, int* ks_out) {
-  if (M <= 0) return cudaSuccess;
-  const int kp = (w.k + kKAlign - 1) / kKAlign * kKAlign;
+// the split-K / finalize decision of launch_gemm (small M, few tiles)
+static bool gemm_finalize(int M, const tern_weight& w, const Epi& epi, int32_t* part,
+                          size_t part_bytes, int tiles, int num_kb, int num_sms, bool ks_req) {
+  const size_t slice = (size_t)M * w.n_rows * sizeof(int32_t);
+  return ks_req || epi.kind == EPI_MLGRU ||
+         (part && part_bytes >= slice && epi.kind != EPI_NONE && w.n_rows % 2 == 0 &&
+          epi.acc == nullptr && tiles * 2 <= num_sms && num_kb >= 2);
+}
+
+static int gemm_bn(int M, const tern_weight& w, int nsm) {
   static const int bn_force = getenv("TERN_GEMM_BN") ? atoi(getenv("TERN_GEMM_BN")) : 0;   // debug
   int BN = (w.n_rows >= 1024 || w.n_rows % 256 == 0) ? 256 : 128;
   // small M (decode batches): narrower tiles so the weight rows spread over more SMs
@@ -1223,17 +1496,49 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   // have 64 tiles for 148 SMs): 128-wide tiles double the CTAs that work while still one
   // wave (measured c2 B = 1 x 2048: 103.5 -> 98.5 us per block; the same switch where it
   // makes two waves -- c3's 128-tile GEMMs -- cost c3 B = 1 170 -> 188 us)
-  {
-    static int nsm = 0;
-    if (!nsm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int t256 = ((M + kBM - 1) / kBM) * ((w.n_rows + 255) / 256);
-    if (BN == 256 && 2 * t256 <= nsm) BN = 128;
-  }
+  const int t256 = ((M + kBM - 1) / kBM) * ((w.n_rows + 255) / 256);
+  if (BN == 256 && 2 * t256 <= nsm) BN = 128;
   if (bn_force == 128 || bn_force == 256) BN = bn_force;
+  return BN;
+}
+
+static int sm_count() {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm;
+}
+
+// fused quantization: opt-in (tern_set_qfuse; measured slower than quant + GEMM)
+int g_qfuse_on = getenv("TERN_QFUSE") ? (atoi(getenv("TERN_QFUSE")) != 0) : 0;
+
+bool gemm_qfuse_ok(int M, const tern_weight& w, const Epi& epi, int32_t* part, size_t part_bytes) {
+  if (!g_qfuse_on || M <= kSmallM || w.e8 == nullptr || epi.acc != nullptr) return false;
+  if (epi.kind == EPI_NONE || epi.kind == EPI_MLGRU) return false;
+  const int nsm = sm_count();
+  const int BN = gemm_bn(M, w, nsm);
+  const int kp = (w.k + kKAlign - 1) / kKAlign * kKAlign;
+  const int tiles = ((w.n_rows + BN - 1) / BN) * ((M + kBM - 1) / kBM);
+  return !gemm_finalize(M, w, epi, part, part_bytes, tiles, kp / kBK, nsm, false);
+}
+
+cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const int32_t* qsum,
+                        const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
+                        int32_t* part, size_t part_bytes, int* ks_out, const QFuse* qf) {
+  if (M <= 0) return cudaSuccess;
+  if (qf && (ks_out || !gemm_qfuse_ok(M, w, epi, part, part_bytes))) {
+    // not a fusable shape: the standalone quantization first
+    cudaError_t qe = launch_quant(qf->x, ydt, M, w.k, qf->ldx, qf->gain, qf->eps,
+                                  const_cast<int8_t*>(q), ldq, const_cast<float*>(deq),
+                                  const_cast<int32_t*>(qsum), nullptr, nullptr, s);
+    if (qe != cudaSuccess) return qe;
+    qf = nullptr;
+  }
+  const int kp = (w.k + kKAlign - 1) / kKAlign * kKAlign;
+  const int BN = gemm_bn(M, w, sm_count());
   // the u8 copy halves shared-memory traffic when the tensor cores are the limit
   // (large M); for decode batches the weight bytes are, and the 2-bit codes are 4x fewer
   // small M: the u8 copy too (TMA only, no smem unpack on the critical path:
@@ -1276,6 +1581,20 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   a.epi = epi;
   a.ksplit = 1;
   a.kb_per = a.num_kb;
+  if (qf) {   // fused quantization of A (only on the paths below that take it)
+    a.qx = qf->x;
+    a.qldx = qf->ldx;
+    a.qK = w.k;
+    a.qmb = (M + 127) / 128;
+    a.qgain = qf->gain;
+    a.qeps = qf->eps;
+    a.qinv_k = 1.0 / (double)w.k;
+    a.qq = const_cast<int8_t*>(q);
+    a.qldq = ldq;
+    a.qdeq = const_cast<float*>(deq);
+    a.qqsum = const_cast<int32_t*>(qsum);
+    a.qctr = qf->ctr;
+  }
   // split-K / finalize mode when the tiles cannot fill the SMs (decode batches,
   // small M) or the epilogue is the MLGRU step (decode T = 1 above the GEMV
   // limit): K slices write int32 partials, k_splitk_epi sums them exactly and
@@ -1289,9 +1608,8 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
   const int tiles = a.n_tiles * a.m_tiles;
   const size_t slice = (size_t)M * w.n_rows * sizeof(int32_t);
   // (the split-K epilogue reads column pairs: even n_rows, true for every fused group)
-  const bool finalize = ks_out != nullptr || epi.kind == EPI_MLGRU ||
-                        (part && part_bytes >= slice && epi.kind != EPI_NONE && w.n_rows % 2 == 0 &&
-                         epi.acc == nullptr && tiles * 2 <= num_sms && a.num_kb >= 2);
+  const bool finalize = gemm_finalize(M, w, epi, part, part_bytes, tiles, a.num_kb, num_sms,
+                                      ks_out != nullptr);
   // decode batches, opt-in (TERN_GEMM_SAB=1; measured slower, k_gemm_sab.cu): the swap-AB
   // kernel streams the 2-bit codes (weights as the MMA's M operand, tokens as N) into int32
   // K-slice partials

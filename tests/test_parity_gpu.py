@@ -561,3 +561,56 @@ def test_two_sm_gemm_block_epilogues(L, M, dtype, B, T, d, l):
         assert np.array_equal(h[0].cpu().numpy(), ho)
     finally:
         L.tern_set_gemm_2sm(old)
+
+
+# ------------------------------------------------------------------------ f3: fused quantization
+@pytest.mark.parametrize("dtype,B,T,d,l", [("f32", 3, 200, 512, 2176), ("bf16", 2, 300, 2048, 704),
+                                           ("f32", 1, 1000, 1024, 2816)])
+def test_qfuse_block_prefill(L, M, dtype, B, T, d, l):
+    """SURVEY 8(f) f3, the a2 RMSNorm + quantization fused into the o, gate|up and down GEMMs
+    (tern_set_qfuse; k_gemm.cu "fused quantization"): a block prefill with ragged M (not a
+    multiple of 128), 1-CTA and CTA-pair GEMMs, fp32 and bf16, free-running against the oracle
+    block, bit for bit."""
+    old = L.tern_get_qfuse()
+    L.tern_set_qfuse(True)
+    try:
+        cfg = synth.Config("qf", 1, d, l, dtype, 23, B, T, B, 0)
+        st = M.Stack.random(cfg, gen_device="cpu", keep_latents=1)
+        x = synth.hidden((B, T, d), synth.generator(d + l + 1), dtype)
+        h = st.new_state(B)
+        y = st.prefill(x.cuda(), h)
+        torch.cuda.synchronize()
+        ob = O.OracleBlock({kk: v.numpy() for kk, v in st.latents[0].items()}, d, l)
+        yo, ho = O.block(ob, f32np(x), np.zeros((B, d), np.float32), bf16=dtype == "bf16")
+        close(f32np(y), yo, 2e-2 if dtype == "bf16" else 1e-4, "qfuse block")
+        assert np.array_equal(f32np(y), yo)
+        assert np.array_equal(h[0].cpu().numpy(), ho)
+    finally:
+        L.tern_set_qfuse(old)
+
+
+@pytest.mark.parametrize("cfg_name,n_tok", [("c2", 24), ("c3", 8)])
+def test_qfuse_full_size_prefixes(L, M, cfg_name, n_tok):
+    """The fused quantization at the bench workload's full size (all blocks, B x T), sampled
+    sequence prefixes through the whole stack against the oracle."""
+    old = L.tern_get_qfuse()
+    L.tern_set_qfuse(True)
+    try:
+        cfg = synth.CONFIGS[cfg_name]
+        st = M.Stack.random(cfg, device="cuda", gen_device="cuda", keep_latents=cfg.L)
+        B, T = cfg.prefill_B, cfg.prefill_T
+        x = synth.hidden((B, T, cfg.d), synth.generator(cfg.seed + 7919), cfg.dtype).cuda()
+        states = st.new_state(B)
+        y = st.prefill(x, states)
+        torch.cuda.synchronize()
+        ob = [O.OracleBlock({k: v.numpy() for k, v in lat.items()}, cfg.d, cfg.l)
+              for lat in st.latents]
+        bf = cfg.dtype == "bf16"
+        for b in (0, B - 1):
+            xo = f32np(x[b:b + 1, :n_tok])
+            Hs = [np.zeros((1, cfg.d), np.float32) for _ in ob]
+            yo, _ = O.stack(ob, xo, Hs, bf16=bf)
+            yg = f32np(y[b:b + 1, :n_tok])
+            assert np.array_equal(yg, yo), f"{cfg_name} sequence {b}"
+    finally:
+        L.tern_set_qfuse(old)
