@@ -121,6 +121,9 @@ def lib():
             L.orc_get_scan_slices.restype = C.c_int
             L.orc_scan_seqpar.argtypes = [f32p, f32p, C.c_int, C.c_int, C.c_float, f32p,
                                           C.POINTER(C.c_float)]
+            f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+            L.orc_bitlinear_bwd.argtypes = [f32p, C.c_int, C.c_int, i8p, C.c_int, C.c_float,
+                                            C.c_float, C.c_int, f32p, f64p, f64p, C.c_void_p]
             L.orc_set_threads.argtypes = [C.c_int]
             L.orc_get_threads.restype = C.c_int
             _lib = L
@@ -295,6 +298,23 @@ def bitlinear(X, t, m, gain=None, bias=None, eps=1e-6, bf16=False, taps=False):
     if taps:
         return O, dict(q=q, acc=acc, deq=deq)
     return O
+
+
+def bitlinear_bwd(X, t, m, dO, eps=1e-6, norm=0):
+    """Alg. 1 BackwardPass with the straight-through estimator (readings
+    B1-B6): returns dX [M][K], dW [N][K], db [N] in float64.
+    norm: 0 = RMSNorm (C1), 1 = Alg. 1's centred norm (C22)."""
+    X = _f32(X)
+    t = np.ascontiguousarray(t, np.int8)
+    dO = _f32(dO)
+    M, K = X.shape
+    N = t.shape[0]
+    dX = np.empty((M, K), np.float64)
+    dW = np.empty((N, K), np.float64)
+    db = np.empty(N, np.float64)
+    _check(lib().orc_bitlinear_bwd(X, M, K, t, N, C.c_float(m), C.c_float(eps), int(norm), dO,
+                                   dX, dW, _ptr(db)), "bitlinear_bwd")
+    return dX, dW, db
 
 
 # ---------------------------------------------------------------- a6

@@ -823,3 +823,100 @@ int orc_fxp_bitlinear(const int16_t* xq, int ex, const int8_t* gq, int eg, doubl
   free(p);
   return rc;
 }
+
+/* ------------------------------------------------------------------------ */
+/* f4(iii): Alg. 1 BackwardPass of one BitLinear, straight-       */
+/* through estimator.  Readings:                       */
+/*   B1  "dY = dO x W^T": W is the ternarized weight the forward      */
+/*       multiplied by, W~ = t m (the straight-through estimator passes the   */
+/*       gradient of the quantizers through unchanged);                       */
+/*   B2  "dW = dO^T x Y~" is [n_out][k_in], the latent weight's       */
+/*       layout; Y~ = q deq (the forward's dequantized activation, a5);       */
+/*   B3  mu, sigma^2, r "loaded" are the forward's own values,        */
+/*       recomputed here with the forward's arithmetic (orc_rmsnorm);         */
+/*   B4  rms_norm_bwd literally for the centred norm (norm = 1,   */
+/*       reading C22); for the default RMSNorm (norm = 0, C1) mu is the       */
+/*       constant 0, so the d mu term is absent: dX = r dY + 2 dsigma^2 X/N;  */
+/*   B5  mean(X - mu) in d mu is as printed (the textbook factor -2   */
+/*       multiplies the same mean, which is 0 up to rounding);                */
+/*   B6  no gain (Alg. 1 has none); every sum in binary64, index order; the  */
+/*       outputs are binary64 (the oracle's precision).                       */
+/* Inputs: X [M][K] fp32, t [N][K] int8 trits with scale m_w (the forward's   */
+/* W~ = t m_w), dO [M][N] fp32.  Outputs: dX [M][K], dW [N][K], db [N]        */
+/* (db may be NULL), all double.                                              */
+/* ------------------------------------------------------------------------ */
+int orc_bitlinear_bwd(const float* X, int M, int K, const int8_t* t, int N, float m_w, float eps,
+                      int norm, const float* dO, double* dX, double* dW, double* db) {
+  if (M < 0 || K <= 0 || N <= 0 || (norm != 0 && norm != 1)) return ORC_ERR_ARG;
+  const int saved = g_norm_mode;
+  g_norm_mode = norm;
+  double* Yt = (double*)malloc(sizeof(double) * ((size_t)M * K + 1));   /* Y~ = q deq, exact */
+  if (!Yt) { g_norm_mode = saved; return ORC_ERR_ARG; }
+  int bad = 0;
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < M; ++i) {
+    const float* x = X + (int64_t)i * K;
+    float* y = (float*)malloc(sizeof(float) * (size_t)K);
+    int8_t* q = (int8_t*)malloc((size_t)K);
+    double* dY = (double*)malloc(sizeof(double) * (size_t)K);
+    if (!y || !q || !dY) { bad = 1; free(y); free(q); free(dY); continue; }
+    /* forward recompute (B3): r from rms_norm_fwd, Y~ from activation_quant */
+    const float r = orc_rmsnorm(x, K, NULL, eps, y);
+    float deq;
+    orc_act_quant(y, K, q, &deq);
+    for (int j = 0; j < K; ++j) Yt[(int64_t)i * K + j] = (double)q[j] * (double)deq;
+    float mu = 0.0f;
+    if (norm == 1) {
+      double sx = 0.0;
+      for (int j = 0; j < K; ++j) sx += (double)x[j];
+      mu = (float)(sx / (double)K);
+    }
+    /* dY = dO x W~^T (B1) */
+    for (int j = 0; j < K; ++j) {
+      double s = 0.0;
+      for (int n = 0; n < N; ++n)
+        s += (double)dO[(int64_t)i * N + n] * ((double)t[(int64_t)n * K + j] * (double)m_w);
+      dY[j] = s;
+    }
+    /* rms_norm_bwd (B4/B5) */
+    const double rd = (double)r;
+    double dsig = 0.0;
+    for (int j = 0; j < K; ++j) dsig += dY[j] * ((double)x[j] - (double)mu) * -0.5 * rd * rd * rd;
+    double dmu = 0.0;
+    if (norm == 1) {
+      double s1 = 0.0, s2 = 0.0;
+      for (int j = 0; j < K; ++j) {
+        s1 += -rd * dY[j];
+        s2 += (double)x[j] - (double)mu;
+      }
+      dmu = s1 + dsig * (s2 / (double)K);
+    }
+    for (int j = 0; j < K; ++j)
+      dX[(int64_t)i * K + j] = rd * dY[j] + 2.0 * dsig * ((double)x[j] - (double)mu) / (double)K +
+                               dmu / (double)K;
+    free(y);
+    free(q);
+    free(dY);
+  }
+  g_norm_mode = saved;
+  if (!bad) {
+    /* dW = dO^T x Y~ (B2): dW[n][j] = sum_m dO[m][n] Y~[m][j] */
+#pragma omp parallel for schedule(static)
+    for (int n = 0; n < N; ++n)
+      for (int j = 0; j < K; ++j) {
+        double s = 0.0;
+        for (int i = 0; i < M; ++i)
+          s += (double)dO[(int64_t)i * N + n] * Yt[(int64_t)i * K + j];
+        dW[(int64_t)n * K + j] = s;
+      }
+    /* db = sum(dO) over tokens */
+    if (db)
+      for (int n = 0; n < N; ++n) {
+        double s = 0.0;
+        for (int i = 0; i < M; ++i) s += (double)dO[(int64_t)i * N + n];
+        db[n] = s;
+      }
+  }
+  free(Yt);
+  return bad ? ORC_ERR_ARG : ORC_OK;
+}
