@@ -355,6 +355,31 @@ tern_status stack_decode(const tern_block* blocks, int32_t L, const void* x, voi
                          tern_stream stream);
 
 /* ------------------------------------------------------------------------
+ * Alg. 1 BackwardPass of one BitLinear
+ * with the straight-through estimator; readings B1-B6:
+ *   dY = dO x W~^T        W~ = t * scale, the ternary weight the forward used (B1)
+ *   dX = rms_norm_bwd(dY, X, mu, sigma^2, r)                      (B4, B5)
+ *        dsig = sum_j dY_j (x_j - mu) (-1/2) r^3
+ *        dmu  = sum_j (-r dY_j) + dsig * mean(x - mu)   (norm = TERN_NORM_CENTERED only;
+ *               TERN_NORM_RMS has mu = 0 and no dmu term)
+ *        dX_j = r dY_j + 2 dsig (x_j - mu) / k + dmu / k
+ *   dW = dO^T x Y~        Y~ = q * deq, the forward's quantized activation (B2)
+ *   db = sum over the m tokens of dO
+ * mu, r, q, deq are the forward's (recomputed from x with the forward's own quantizer,
+ * B3); no gain (Alg. 1 has none).  Arguments (device pointers, caller-owned):
+ *   x  [m][k] fp32, row-major, the forward input;  w: one segment (n_seg = 1) with its
+ *   u8 copy e8 (tern_expand);  dO [m][n_out] fp32;  outputs dX [m][k], dW [n_out][k] (the
+ *   latent weight's layout), db [n_out] (NULL = skip), all fp32;  ws >=
+ *   bitlinear_bwd_workspace(m, k, n_out) bytes, 16-byte aligned.  m == 0 writes dW = 0
+ *   and db = 0.  The contractions run on CUDA cores in fp32 with deterministic sums.
+ * Errors: TERN_ERR_INVALID_ARG (null pointers, k % 16 != 0, n_seg != 1, no e8, small
+ * ws, bad norm), all checked before any launch; asynchronous faults as elsewhere. */
+size_t bitlinear_bwd_workspace(int32_t m, int32_t k, int32_t n_out);
+tern_status bitlinear_bwd(const float* x, int32_t m, int32_t k, const tern_weight* w, float eps,
+                          int32_t norm, const float* dO, float* dX, float* dW, float* db,
+                          void* ws, size_t ws_bytes, tern_stream stream);
+
+/* ------------------------------------------------------------------------
  * Measurement hooks (bench.py roofline): while enabled, every kernel launch
  * made by this library on a non-capturing stream is bracketed by two CUDA
  * events recorded on that same stream, with its shape.  tern_profile_collect

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libtern.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["api.cu", "k_pack.cu", "k_quant.cu", "k_gemv.cu", "k_gemm.cu", "k_scan.cu", "k_selftest.cu", "k_shard.cu", "k_fcgscan.cu", "k_fin.cu", "k_fxp.cu", "k_gemm_sab.cu"]
+SOURCES = ["api.cu", "k_pack.cu", "k_quant.cu", "k_gemv.cu", "k_gemm.cu", "k_scan.cu", "k_selftest.cu", "k_shard.cu", "k_fcgscan.cu", "k_fin.cu", "k_fxp.cu", "k_gemm_sab.cu", "k_bwd.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}"]

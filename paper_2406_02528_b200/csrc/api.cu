@@ -496,6 +496,38 @@ tern_status bitlinear_fwd(const void* x, tern_dtype xdt, int32_t m, int32_t k, i
                g_norm_mode);
 }
 
+size_t bitlinear_bwd_workspace(int32_t m, int32_t k, int32_t n) {
+  if (m <= 0 || k <= 0 || n <= 0) return 0;
+  return bwd_workspace(m, k, n);
+}
+
+tern_status bitlinear_bwd(const float* x, int32_t m, int32_t k, const tern_weight* w, float eps,
+                          int32_t norm, const float* dO, float* dX, float* dW, float* db, void* ws,
+                          size_t ws_bytes, tern_stream stream) {
+  CHECK(m >= 0 && k > 0 && k % 16 == 0, "bitlinear_bwd: m=%d k=%d", m, k);
+  CHECK(norm == TERN_NORM_RMS || norm == TERN_NORM_CENTERED, "bitlinear_bwd: norm=%d", norm);
+  tern_status st = check_weight(w, k, 1, "bitlinear_bwd");
+  if (st) return st;
+  CHECK(w->e8 != nullptr, "bitlinear_bwd: the weight's u8 copy e8 is required (tern_expand)");
+  CHECK(eps > 0, "bitlinear_bwd: eps must be > 0");
+  CHECK(dW, "bitlinear_bwd: null dW");
+  if (m == 0) {   // no tokens: dW = 0, db = 0
+    TRY_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)w->n_out * k, (cudaStream_t)stream),
+             "bwd zero dW");
+    if (db) TRY_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * w->n_out, (cudaStream_t)stream), "bwd zero db");
+    return TERN_OK;
+  }
+  CHECK(x && dO && dX, "bitlinear_bwd: null pointer");
+  CHECK(k <= 32 * 128 * 4, "bitlinear_bwd: k=%d too large", k);
+  CHECK(ws && aligned16(ws) && ws_bytes >= bwd_workspace(m, k, w->n_out),
+        "bitlinear_bwd: workspace too small (%zu < %zu)", ws_bytes, bwd_workspace(m, k, w->n_out));
+  st = check_device();
+  if (st) return st;
+  TRY_CUDA(launch_bitlinear_bwd(x, m, k, *w, eps, norm, dO, dX, dW, db, ws, (cudaStream_t)stream),
+           "bitlinear_bwd");
+  return TERN_OK;
+}
+
 tern_status tern_contract(const int8_t* q, int32_t m, int32_t ldq, const int32_t* qsum,
                           const tern_weight* w, int32_t* acc, int32_t ldacc, tern_stream stream) {
   CHECK(q && qsum && acc && w, "tern_contract: null pointer");

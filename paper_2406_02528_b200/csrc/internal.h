@@ -102,6 +102,11 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
                         int32_t* part = nullptr, size_t part_bytes = 0, int* ks_out = nullptr,
                         const QFuse* qf = nullptr);
+// f4(iii) Alg. 1 backward (k_bwd.cu)
+size_t bwd_workspace(int m, int k, int n);
+cudaError_t launch_bitlinear_bwd(const float* x, int m, int k, const tern_weight& w, float eps,
+                                 int norm, const float* dO, float* dX, float* dW, float* db,
+                                 void* ws, cudaStream_t s);
 // whether launch_gemm runs a QFuse request inside the GEMM (else it launches k_quant first)
 bool gemm_qfuse_ok(int M, const tern_weight& w, const Epi& epi, int32_t* part, size_t part_bytes);
 // batched decode: one CTA per row sums the ks partial slices [ks][M][n_rows],
