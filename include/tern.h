@@ -371,10 +371,14 @@ tern_status stack_decode(const tern_block* blocks, int32_t L, const void* x, voi
  *   u8 copy e8 (tern_expand);  dO [m][n_out] fp32;  outputs dX [m][k], dW [n_out][k] (the
  *   latent weight's layout), db [n_out] (NULL = skip), all fp32;  ws >=
  *   bitlinear_bwd_workspace(m, k, n_out) bytes, 16-byte aligned.  m == 0 writes dW = 0
- *   and db = 0.  The contractions run on CUDA cores in fp32 with deterministic sums.
+ *   and db = 0.  Deterministic sums (no atomics).
  * Errors: TERN_ERR_INVALID_ARG (null pointers, k % 16 != 0, n_seg != 1, no e8, small
  * ws, bad norm), all checked before any launch; asynchronous faults as elsewhere. */
 size_t bitlinear_bwd_workspace(int32_t m, int32_t k, int32_t n_out);
+/* 1 (default): the backward's two contractions on the tensor cores (bf16 hi + lo split of
+ * the fp32 operand, reading B7); 0: fp32 CUDA-core GEMMs (the reference path). */
+void tern_set_bwd_tc(int32_t on);
+int32_t tern_get_bwd_tc(void);
 tern_status bitlinear_bwd(const float* x, int32_t m, int32_t k, const tern_weight* w, float eps,
                           int32_t norm, const float* dO, float* dX, float* dW, float* db,
                           void* ws, size_t ws_bytes, tern_stream stream);

@@ -133,6 +133,8 @@ _SIGS = {
     "tern_set_gemm_sab": (None, [I32]),
     "tern_set_gemm_2sm": (None, [I32]),
     "tern_set_qfuse": (None, [I32]),
+    "tern_set_bwd_tc": (None, [I32]),
+    "tern_get_bwd_tc": (I32, []),
     "tern_get_qfuse": (I32, []),
     "tern_get_gemm_2sm": (I32, []),
     "tern_get_gemm_sab": (I32, []),
@@ -362,6 +364,15 @@ def tern_set_qfuse(on: bool):
 
 def tern_get_qfuse() -> bool:
     return bool(load().tern_get_qfuse())
+
+
+def tern_set_bwd_tc(on: bool):
+    """Backward contractions on the tensor cores (default) or fp32 CUDA cores."""
+    load().tern_set_bwd_tc(1 if on else 0)
+
+
+def tern_get_bwd_tc() -> bool:
+    return bool(load().tern_get_bwd_tc())
 
 
 def tern_get_gemm_2sm() -> bool:

@@ -345,6 +345,8 @@ void tern_set_batched_fin(int32_t on) { g_batched_fin = on ? 1 : 0; }
 void tern_set_gemm_sab(int32_t on) { g_gemm_sab = on ? 1 : 0; }
 void tern_set_gemm_2sm(int32_t on) { g_gemm_2sm = on ? 1 : 0; }
 void tern_set_qfuse(int32_t on) { g_qfuse_on = on ? 1 : 0; }
+void tern_set_bwd_tc(int32_t on) { g_bwd_tc = on ? 1 : 0; }
+int32_t tern_get_bwd_tc(void) { return g_bwd_tc; }
 int32_t tern_get_qfuse(void) { return g_qfuse_on; }
 int32_t tern_get_gemm_2sm(void) { return g_gemm_2sm; }
 int32_t tern_get_gemm_sab(void) { return g_gemm_sab; }
@@ -518,6 +520,7 @@ tern_status bitlinear_bwd(const float* x, int32_t m, int32_t k, const tern_weigh
     return TERN_OK;
   }
   CHECK(x && dO && dX, "bitlinear_bwd: null pointer");
+  CHECK(aligned16(x) && aligned16(dX) && aligned16(dO), "bitlinear_bwd: x, dO, dX must be 16-byte aligned");
   CHECK(k <= 32 * 128 * 4, "bitlinear_bwd: k=%d too large", k);
   CHECK(ws && aligned16(ws) && ws_bytes >= bwd_workspace(m, k, w->n_out),
         "bitlinear_bwd: workspace too small (%zu < %zu)", ws_bytes, bwd_workspace(m, k, w->n_out));

@@ -102,7 +102,8 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
                         const tern_weight& w, int ydt, const Epi& epi, cudaStream_t s,
                         int32_t* part = nullptr, size_t part_bytes = 0, int* ks_out = nullptr,
                         const QFuse* qf = nullptr);
-// f4(iii) Alg. 1 backward (k_bwd.cu)
+// f4(iii) Alg. 1 backward (k_bwd.cu); g_bwd_tc: tensor-core contractions (tern_set_bwd_tc)
+extern int g_bwd_tc;
 size_t bwd_workspace(int m, int k, int n);
 cudaError_t launch_bitlinear_bwd(const float* x, int m, int k, const tern_weight& w, float eps,
                                  int norm, const float* dO, float* dX, float* dW, float* db,

@@ -40,11 +40,23 @@ def close(g, o, tol, what):
                           f"max abs err {np.max(np.abs(g - o)):.3e}"
 
 
+@pytest.mark.parametrize("tc", [True, False])
 @pytest.mark.parametrize("m,k,n,norm", [(37, 64, 48, 0), (37, 64, 48, 1), (300, 1024, 1000, 0),
-                                        (513, 2816, 1024, 1), (2048, 1024, 1024, 0)])
-def test_bwd_parity(L, M, m, k, n, norm):
+                                        (513, 2816, 1024, 1), (2048, 1024, 1024, 0),
+                                        (1000, 2048, 200, 0)])
+def test_bwd_parity(L, M, m, k, n, norm, tc):
     """dX, dW and db against the oracle: ragged m and n (not tile multiples), both norms,
-    contractions spanning several 128-wide tiles and 16-deep steps."""
+    contractions spanning several 128-wide tiles and k-blocks; the tensor-core path (bf16
+    hi + lo split, B7, with split-K slices for dW) and the fp32 CUDA-core path."""
+    old = L.tern_get_bwd_tc()
+    L.tern_set_bwd_tc(tc)
+    try:
+        _bwd_case(L, M, m, k, n, norm)
+    finally:
+        L.tern_set_bwd_tc(old)
+
+
+def _bwd_case(L, M, m, k, n, norm):
     g = synth.generator(m + k + n + norm)
     W = synth.latent_matrix(n, k, g)
     x = synth.hidden((m, k), g, "f32") * 1.3 + 0.2
