@@ -507,6 +507,55 @@ def other_config_prefill(name: str, steps: int, warmup: int, pk: dict, dev) -> d
 
 
 # ------------------------------------------------------------------ our arm
+def backward_line(pk: dict, dev) -> dict:
+    """Alg. 1 BackwardPass of one c2-sized BitLinear
+    (tokens of one c2 prefill step, d -> d and l -> d), bitlinear_bwd on the tensor cores
+    (bf16 hi + lo split, reading B7) and on the fp32 CUDA cores; side measurement, not part
+    of `value` (the north_star path is the forward).  Rates count the dense products the
+    backward computes, 2 m n k each for dY and dW (fp32-equivalent); the tensor cores execute
+    twice that in bf16 (the split), which `mma_bf16_tflops_equiv` reports against the bf16
+    peak."""
+    import torch
+    from paper_2406_02528_b200 import _lib as Lb
+    from paper_2406_02528_b200 import model, synth
+    res = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for (m, k, n) in [(16384, 1024, 1024), (16384, 2816, 1024)]:
+        W = synth.latent_matrix(n, k, synth.generator(101, dev), device=dev)
+        pw = model.PackedWeight([W])
+        x = torch.randn(m, k, device=dev)
+        dO = torch.randn(m, n, device=dev)
+        dX, dW, db = torch.empty_like(x), torch.empty(n, k, device=dev), torch.empty(n, device=dev)
+        ws = torch.empty(int(Lb.load().bitlinear_bwd_workspace(m, k, n)), dtype=torch.uint8,
+                         device=dev)
+        row = {}
+        for tc in (True, False):
+            Lb.tern_set_bwd_tc(tc)
+            Lb.bitlinear_bwd(x, pw.struct, dO, dX, dW, db, ws=ws)
+            ts = []
+            for _ in range(3):
+                flush.fill_(1.0)
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record()
+                Lb.bitlinear_bwd(x, pw.struct, dO, dX, dW, db, ws=ws)
+                b_.record()
+                torch.cuda.synchronize()
+                ts.append(a_.elapsed_time(b_))
+            ms = min(ts)
+            fl = 4.0 * m * n * k
+            r = {"ms": round(ms, 4), "tflops_fp32_equiv": round(fl / ms / 1e9, 1)}
+            if tc:
+                r["mma_bf16_tflops_equiv"] = round(2 * fl / ms / 1e9, 1)
+                r["frac_of_bf16_peak_whole_call"] = round(2 * fl / ms / 1e9 / pk["bf16_tflops"], 4)
+            row["tensor_core" if tc else "cuda_core_fp32"] = r
+        res[f"m{m}_k{k}_n{n}"] = row
+    Lb.tern_set_bwd_tc(True)
+    res["note"] = ("whole bitlinear_bwd call (forward quant recompute, operand prep, dY GEMM, "
+                   "norm backward, dW GEMM + slice reduce, db), min of 3, L2 flushed; "
+                   "per-kernel split in profiles/r02_bwd_launches.txt")
+    return res
+
+
 def finish_sharded(args, cfg, rank, world, mode, st, value, ms_max, rl, kernels, recs, ck, e2e,
                    pk):
     """The JSON line of a sharded run (--shard out|gather_q|megatron|seq): prefill of one
@@ -834,6 +883,11 @@ def run_ours(args, cfg, rank, world, local_rank):
            "config": config_dict(cfg, world), "roofline": rl, "kernels": kernels,
            "gpu_launches": len(recs), "clocks": ck, "e2e": e2e, "decode": dec,
            "prefill_b1": prefill_b1, "comm": comm_info(world), "paper_context": PAPER_CONTEXT}
+    if rank == 0 and world == 1 and cfg.name == "c2" and not args.no_other_configs:
+        try:
+            out["backward"] = backward_line(pk, dev)
+        except Exception as e:   # reported, never required
+            out["backward"] = {"error": repr(e)}
     if rank == 0 and world == 1 and cfg.name == "c2" and not args.no_other_configs:
         # the metric spans 370M-2.7B: the 1.3B (c3) and 2.7B (c4) prefill lines, each its own
         # stack at full size (BASELINE.json configs[3], configs[4]); not part of `value`
