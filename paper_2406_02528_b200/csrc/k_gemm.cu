@@ -433,7 +433,9 @@ __device__ void qf_quant_warps(const GemmArgs& a, int qw, int lane) {
   }
 }
 
-template <int BN, bool kPre, typename TY, bool RES = false, int EW = kEpiWarps>
+// QF: the fused-quantization variant (a separate instantiation, so the default kernels'
+// register allocation is not shaped by the quant warps' code)
+template <int BN, bool kPre, typename TY, bool RES = false, int EW = kEpiWarps, bool QF = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
@@ -539,7 +541,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int tile = t / a.ksplit, sp = t % a.ksplit;
         const int m0 = (tile / a.n_tiles) * kBM, n0 = (tile % a.n_tiles) * BN;
         const int kb1 = min(nk, (sp + 1) * a.kb_per);
-        if (a.qctr) {   // fused quantization: this tile's A rows must be published
+        if constexpr (QF) {   // fused quantization: this tile's A rows must be published
           qf_wait_block(a.qctr, m0 >> 7);
           fence_proxy_async_global();
         }
@@ -598,7 +600,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ---------------- unpack (warps 2-5, packed path): 2-bit fields -> u8 e, SW128 K-major
     // (u8 path: the fused quantization of A when requested)
     if (kPre && EW == kEpiWarps) {
-      if (a.qctr) qf_quant_warps<TY>(a, warp - 2, lane);
+      if constexpr (QF) qf_quant_warps<TY>(a, warp - 2, lane);
     } else if (!kPre) {
       const int tid = threadIdx.x - 64;
       const bool pt = tid == 0;
@@ -689,9 +691,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int row0 = m0 + quad * 32;
         const int row = row0 + lane;
         const bool rv = row < a.M;
-        if (a.qctr) qf_wait_block(a.qctr, m0 >> 7);   // deq / qsum written in this kernel
-        const float deq = rv ? __ldcg(a.deq + row) : 0.0f;
-        const int qsum = rv ? __ldcg(a.qsum + row) : 0;
+        float deq;
+        int qsum;
+        if constexpr (QF) {   // deq / qsum written in this kernel: acquire, then L2 loads
+          qf_wait_block(a.qctr, m0 >> 7);
+          deq = rv ? __ldcg(a.deq + row) : 0.0f;
+          qsum = rv ? __ldcg(a.qsum + row) : 0;
+        } else {
+          deq = rv ? __ldg(a.deq + row) : 0.0f;
+          qsum = rv ? __ldg(a.qsum + row) : 0;
+        }
         const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
         for (int c = half; c < BN / 32; c += NG) {
@@ -772,9 +781,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       const int row = row0 + lane;
       const bool rv = row < a.M;
-      if (a.qctr) qf_wait_block(a.qctr, m0 >> 7);   // deq / qsum written in this kernel
-      const float deq = rv ? __ldcg(a.deq + row) : 0.0f;
-      const int qsum = rv ? __ldcg(a.qsum + row) : 0;
+      float deq;
+      int qsum;
+      if constexpr (QF) {   // deq / qsum written in this kernel: acquire, then L2 loads
+        qf_wait_block(a.qctr, m0 >> 7);
+        deq = rv ? __ldcg(a.deq + row) : 0.0f;
+        qsum = rv ? __ldcg(a.qsum + row) : 0;
+      } else {
+        deq = rv ? __ldg(a.deq + row) : 0.0f;
+        qsum = rv ? __ldg(a.qsum + row) : 0;
+      }
       const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
       const bool swig = e.kind == EPI_SWIGLU;
       const int nch = swig ? BN / 64 : BN / 32;   // chunks (or gate/up pairs) per tile
@@ -955,7 +971,7 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <typename TY, int NB>
+template <typename TY, int NB, bool QF = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
@@ -1026,7 +1042,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int t = cid; t < total; t += ncl) {
         const int m0 = (t / a.n_tiles) * 256 + (int)rank * 128;
         const int n0 = (t % a.n_tiles) * 256 + (int)rank * 128;
-        if (a.qctr) {   // fused quantization: this CTA's 128 A rows must be published
+        if constexpr (QF) {   // fused quantization: this CTA's 128 A rows must be published
           qf_wait_block(a.qctr, m0 >> 7);
           fence_proxy_async_global();
         }
@@ -1126,9 +1142,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row0 = m0 + quad * 32;
       const int row = row0 + lane;
       const bool rv = row < a.M;
-      if (a.qctr) qf_wait_block(a.qctr, m0 >> 7);   // deq / qsum written in this kernel
-      const float deq = rv ? __ldcg(a.deq + row) : 0.0f;
-      const int qsum = rv ? __ldcg(a.qsum + row) : 0;
+      float deq;
+      int qsum;
+      if constexpr (QF) {   // deq / qsum written in this kernel: acquire, then L2 loads
+        qf_wait_block(a.qctr, m0 >> 7);
+        deq = rv ? __ldcg(a.deq + row) : 0.0f;
+        qsum = rv ? __ldcg(a.qsum + row) : 0;
+      } else {
+        deq = rv ? __ldg(a.deq + row) : 0.0f;
+        qsum = rv ? __ldg(a.qsum + row) : 0;
+      }
       const uint32_t trow = tmem_base + acc * 256 + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
       for (int c = half; c < nch; c += 2) {
@@ -1210,7 +1233,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lead) cl_arrive(temptyL + acc * 8);   // the leader's tempty[acc]
     }
     if (lead) bulk_wait<0>();
-  } else if (warp >= 2 && a.qctr) {
+  } else if (QF && warp >= 2) {
     // ---------------- fused quantization of A (warps 2-5 of both CTAs)
     qf_quant_warps<TY>(a, warp - 2, lane);
   }
@@ -1258,11 +1281,11 @@ bool make_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uin
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool kPre, typename TY, bool RES = false, int EW = kEpiWarps>
+template <int BN, bool kPre, typename TY, bool RES = false, int EW = kEpiWarps, bool QF = false>
 static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
                                const CUtensorMap& tr, const GemmArgs& a, cudaStream_t s) {
   using Cfg = GemmCfg<BN, kPre, RES, EW>;
-  auto kern = k_gemm_tc<BN, kPre, TY, RES, EW>;
+  auto kern = k_gemm_tc<BN, kPre, TY, RES, EW, QF>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -1306,10 +1329,10 @@ static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, con
   return cudaGetLastError();
 }
 
-template <typename TY, int NB>
+template <typename TY, int NB, bool QF = false>
 static cudaError_t gemm2_launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
                                 const CUtensorMap& tr, const GemmArgs& a, cudaStream_t s) {
-  auto kern = k_gemm_2sm<TY, NB>;
+  auto kern = k_gemm_2sm<TY, NB, QF>;
   constexpr int k2Smem = Cfg2<NB>::SMEM;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1353,7 +1376,8 @@ static cudaError_t gemm_dispatch_bn(int BN, const CUtensorMap& ta, const CUtenso
   // 37.7 us, c3 o 141 -> 124 us; c2 down 57.7 -> 61.9 us with it, so down keeps S = 4)
   if (BN == 256 && kPre && res_on && a.epi.kind == EPI_RESID && a.epi.acc == nullptr &&
       a.part == nullptr && a.ksplit == 1 && a.num_kb <= 16)
-    return gemm_launch<256, kPre, TY, true>(ta, tb, to, tr, a, s);
+    return a.qctr ? gemm_launch<256, kPre, TY, true, kEpiWarps, kPre>(ta, tb, to, tr, a, s)
+                  : gemm_launch<256, kPre, TY, true>(ta, tb, to, tr, a, s);
   // (12 drain warps measured slower on c2 gate|up: 96 -> 103 us; TERN_GEMM_EW12=1 turns it on)
   static const int ew12 = getenv("TERN_GEMM_EW12") ? atoi(getenv("TERN_GEMM_EW12")) : 0;   // debug
   if constexpr (kPre) {
@@ -1361,6 +1385,9 @@ static cudaError_t gemm_dispatch_bn(int BN, const CUtensorMap& ta, const CUtenso
         a.part == nullptr && a.ksplit == 1 && a.qctr == nullptr)
       return gemm_launch<256, true, TY, false, 12>(ta, tb, to, tr, a, s);
   }
+  if (a.qctr)   // (only on the u8 path: launch_gemm's gemm_qfuse_ok requires e8)
+    return BN == 256 ? gemm_launch<256, kPre, TY, false, kEpiWarps, kPre>(ta, tb, to, tr, a, s)
+                     : gemm_launch<128, kPre, TY, false, kEpiWarps, kPre>(ta, tb, to, tr, a, s);
   return BN == 256 ? gemm_launch<256, kPre, TY>(ta, tb, to, tr, a, s)
                    : gemm_launch<128, kPre, TY>(ta, tb, to, tr, a, s);
 }
@@ -1676,6 +1703,9 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
     GemmArgs a2 = a;
     a2.m_tiles = (M + 255) / 256;
     static const int nb2 = getenv("TERN_GEMM_2SM_NB") ? atoi(getenv("TERN_GEMM_2SM_NB")) : 2;  // debug
+    if (a2.qctr)
+      return yb ? gemm2_launch<__nv_bfloat16, 2, true>(ta, tb2, to, tr, a2, s)
+                : gemm2_launch<float, 2, true>(ta, tb2, to, tr, a2, s);
     if (nb2 == 1)
       return yb ? gemm2_launch<__nv_bfloat16, 1>(ta, tb2, to, tr, a2, s)
                 : gemm2_launch<float, 1>(ta, tb2, to, tr, a2, s);
