@@ -134,6 +134,42 @@ def test_validation_of_the_fixed_point_entry_points(lib):
     lib.tern_set_fused_scan(old)
 
 
+def test_validation_of_the_backward_and_qfuse_knobs(lib):
+    """bitlinear_bwd (f4(iii)) rejects bad arguments before any launch: k % 16, a fused
+    group (n_seg != 1), a weight without its u8 copy, a bad norm, a short workspace;
+    the workspace query; the f3 / backward knobs read back what was set."""
+    from paper_2406_02528_b200 import _lib as L
+    fake = C.c_void_p(0x1000)
+    w1 = L.tern_weight(0x1000, 0x2000, 64, 128, 8, 1, 64)
+    w1.e8 = 0x4000
+    ws = 1 << 30
+    bw = lib.bitlinear_bwd
+    assert bw(fake, 4, 120, C.byref(w1), 1e-6, 0, fake, fake, fake, None, fake, ws, None) == \
+        L.TERN_ERR_INVALID_ARG
+    w3 = L.tern_weight(0x1000, 0x2000, 64, 128, 8, 3, 192)
+    w3.e8 = 0x4000
+    assert bw(fake, 4, 128, C.byref(w3), 1e-6, 0, fake, fake, fake, None, fake, ws, None) == \
+        L.TERN_ERR_INVALID_ARG
+    w0 = L.tern_weight(0x1000, 0x2000, 64, 128, 8, 1, 64)   # no e8
+    assert bw(fake, 4, 128, C.byref(w0), 1e-6, 0, fake, fake, fake, None, fake, ws, None) == \
+        L.TERN_ERR_INVALID_ARG and b"e8" in lib.tern_last_error()
+    assert bw(fake, 4, 128, C.byref(w1), 1e-6, 3, fake, fake, fake, None, fake, ws, None) == \
+        L.TERN_ERR_INVALID_ARG and b"norm" in lib.tern_last_error()
+    need = lib.bitlinear_bwd_workspace(4, 128, 64)
+    assert need > 4 * 128 * 4
+    assert bw(fake, 4, 128, C.byref(w1), 1e-6, 0, fake, fake, fake, None, fake, need - 16, None) \
+        == L.TERN_ERR_INVALID_ARG and b"workspace" in lib.tern_last_error()
+    assert lib.bitlinear_bwd_workspace(0, 128, 64) == 0
+    for get, put in ((lib.tern_get_qfuse, lib.tern_set_qfuse),
+                     (lib.tern_get_bwd_tc, lib.tern_set_bwd_tc)):
+        old = get()
+        put(7)
+        assert get() == 1
+        put(0)
+        assert get() == 0
+        put(old)
+
+
 def test_product_path_has_no_fallback(tmp_path, monkeypatch):
     """The binding raises when the CUDA library is missing (no CPU fallback)."""
     import importlib
