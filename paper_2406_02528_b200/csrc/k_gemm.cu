@@ -1426,15 +1426,25 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
   if (chan) {   // n_out even: channels c, c+1 share a 64-row group (c even)
     const int nseg = e.kind == EPI_SWIGLU ? 2 : 3;
     int2 a[3] = {make_int2(0, 0), make_int2(0, 0), make_int2(0, 0)};
-    for (int k = 0; k < ksplit; ++k) {
+    // four slices' loads issued together per round (a runtime trip count would otherwise
+    // serialise one L2 round trip per slice); the sums stay in slice order (exact anyway)
+    for (int k0 = 0; k0 < ksplit; k0 += 4) {
+      int2 v[4][3];
 #pragma unroll
-      for (int sg = 0; sg < 3; ++sg) {
-        if (sg < nseg) {
-          const int2 v = __ldg(reinterpret_cast<const int2*>(prow + k * sl + packed_row(sg, c, nseg)));
-          a[sg].x += v.x;
-          a[sg].y += v.y;
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int sg = 0; sg < 3; ++sg)
+          v[u][sg] = (k0 + u < ksplit && sg < nseg)
+                         ? __ldg(reinterpret_cast<const int2*>(prow + (k0 + u) * sl +
+                                                               packed_row(sg, c, nseg)))
+                         : make_int2(0, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int sg = 0; sg < 3; ++sg) {
+          a[sg].x += v[u][sg].x;
+          a[sg].y += v[u][sg].y;
         }
-      }
     }
 #pragma unroll
     for (int sg = 0; sg < 3; ++sg) {
@@ -1480,10 +1490,17 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
   }
   // one segment or the interleaved f|c|g columns: columns c, c+1 (c even)
   int2 a = make_int2(0, 0);
-  for (int k = 0; k < ksplit; ++k) {
-    const int2 v = __ldg(reinterpret_cast<const int2*>(prow + k * sl + c));
-    a.x += v.x;
-    a.y += v.y;
+  for (int k0 = 0; k0 < ksplit; k0 += 4) {   // four slices' loads in flight per round
+    int2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = k0 + u < ksplit ? __ldg(reinterpret_cast<const int2*>(prow + (k0 + u) * sl + c))
+                             : make_int2(0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a.x += v[u].x;
+      a.y += v[u].y;
+    }
   }
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
