@@ -262,17 +262,41 @@ def qf_bytes(rec: dict, elem: int) -> float:
     return m * k * elem + 2.0 * m * kp + 12.0 * m
 
 
+def gemm_bytes(rec: dict, elem: int) -> float:
+    """Algorithmic HBM bytes of one tensor-core GEMM launch: the int8 activations
+    (M x Kp), the 2-bit packed weights (N x Kp / 4), the outputs and, for the residual
+    epilogue, the residual input (SwiGLU writes N/2 outputs; the fused scan writes d = N/3)."""
+    k, m, n, epi = rec["k"], rec["m"], rec["n"], rec["epi"]
+    kp = (k + 127) // 128 * 128
+    if rec["kernel"] == "fcgscan":
+        n_out = n // 3
+    else:
+        n_out = n // 2 if epi == 4 else n
+    b = m * kp + n * kp / 4.0 + m * n_out * elem
+    if rec["kernel"] != "fcgscan" and epi == 1:   # residual epilogue reads x
+        b += m * n_out * elem
+    if rec["kernel"] == "gemm_qf":
+        b += qf_bytes(rec, elem) - m * kp   # (the A read is in both)
+    return b
+
+
 def roofline(records, elem, pk, traffic_db, clocks=None):
     by = {}
+    i8peak0, _ = int8_peak_for(pk, clocks)
     for r in records:
         u, w = algo_work(r, elem)
         e = by.setdefault(r["kernel"], {"ms": 0.0, "work": 0.0, "unit": u, "launches": 0,
-                                        "bytes": 0.0})
+                                        "bytes": 0.0, "attainable_ms": 0.0})
         e["ms"] += r["ms"]
         e["work"] += w
         e["launches"] += 1
         if r["kernel"] == "gemm_qf":
             e["bytes"] += qf_bytes(r, elem)
+        if u == "flop":
+            # SURVEY 8(d): the attainable roofline of each launch, max(ops / tensor peak,
+            # algorithmic bytes / HBM peak) -- the N = 1024 GEMMs sit below the ridge
+            e["attainable_ms"] += 1e3 * max(w / (i8peak0 * 1e12),
+                                            gemm_bytes(r, elem) / (pk["hbm_gbs"] * 1e9))
     tot = sum(e["ms"] for e in by.values()) or 1.0
     kernels = {}
     i8peak, i8src = int8_peak_for(pk, clocks)
@@ -293,7 +317,8 @@ def roofline(records, elem, pk, traffic_db, clocks=None):
                              # the adds the method needs, nnz * M with the zero
                              # fraction of N(0, s) weights at the 1/2 mean|W| threshold:
                              # P(|z| < sqrt(2/pi)/2) = 0.310 (31.0 % measured)
-                             "ternary_adds_T_per_s": round(ach / 2.0 * (1.0 - ZERO_FRAC), 1)}
+                             "ternary_adds_T_per_s": round(ach / 2.0 * (1.0 - ZERO_FRAC), 1),
+                             "frac_of_attainable": round(e["attainable_ms"] / e["ms"], 4)}
             if e["bytes"] > 0:   # gemm_qf: the fused quantization's HBM stream beside the MMAs
                 hb = e["bytes"] / s / 1e9
                 kernels[name]["fused_quant_hbm"] = {
@@ -341,6 +366,11 @@ def roofline(records, elem, pk, traffic_db, clocks=None):
         if d["bound"] == "tensor":
             rl["frac_of_burst"] = d["frac_of_burst"]
             rl["frac_of_sustained"] = d["frac_of_sustained"]
+            rl["frac_of_attainable"] = d["frac_of_attainable"]
+            rl["attainable_note"] = ("sum over launches of max(dense-equivalent ops / the tensor "
+                                     "peak, algorithmic bytes / HBM peak) over the measured time "
+                                     "(SURVEY 8(d): GEMMs below the ridge, e.g. the N = 1024 "
+                                     "projections, are HBM-bound)")
             if "int8_cublaslt" in pk:   # side note: cuBLASLt s8 GEMM on this pool
                 rl["note_cublaslt_int8_tops"] = {
                     k: pk["int8_cublaslt"].get(k) for k in ("int8_tops_burst", "int8_tops_sustained")}
