@@ -41,6 +41,10 @@ constexpr int kSmallM = 256;   // M at or below: packed B tiles (+ split-K when 
 #define TERN_RES_NB 2
 #endif
 constexpr int kResS = TERN_RES_S, kResNB = TERN_RES_NB;
+// ring stages of the 128-wide u8 tiles (decode batches, short prefills)
+#ifndef TERN_S128
+#define TERN_S128 4
+#endif
 template <int BN, bool kPre, bool RES = false, int EW = kEpiWarps> struct GemmCfg {
   static constexpr int A_BYTES = kBM * kBK;        // 16 KB
   static constexpr int B_BYTES = BN * kBK;         // u8 B tile
@@ -54,7 +58,8 @@ template <int BN, bool kPre, bool RES = false, int EW = kEpiWarps> struct GemmCf
   // EW = 12 drain warps (the u8 path's idle unpack warps 2-5 join the 8 drain warps) for
   // the SwiGLU epilogue, whose arithmetic (2 exact sigmoids per p) outlasts a K = 1024 tile's
   // MMAs; its staging takes the 4th ring stage
-  static constexpr int S = kPre ? ((RES && BN == 256) ? kResS : (EW == 12 && BN == 256) ? 3 : 4)
+  static constexpr int S = kPre ? ((RES && BN == 256) ? kResS : (EW == 12 && BN == 256) ? 3
+                                   : (BN == 128 ? TERN_S128 : 4))
                                : (BN == 256 ? 4 : 5);
   static constexpr int U = kPre ? 0 : 2;
   static constexpr int NB = (kPre && BN == 256 && RES) ? kResNB : (kPre && BN == 256) ? 1 : 2;
