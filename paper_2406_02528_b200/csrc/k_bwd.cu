@@ -215,8 +215,80 @@ __global__ void __launch_bounds__(kBwdThreads)
   }
 }
 
+// the same with one warp per row (K <= 128 NV: 32 lanes x NV float4 each of x and dY): shuffle
+// reductions only, no block barriers, 8 rows per CTA
+template <int NV>
+__global__ void __launch_bounds__(256)
+    k_bwd_norm_w(const float* __restrict__ x, const float* __restrict__ dY, const float* __restrict__ r,
+                 int M, int K, int centred, float* __restrict__ dX) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  pdl_wait();
+  pdl_launch_dependents();
+  if (row >= M) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)row * K);
+  const float4* dyr = reinterpret_cast<const float4*>(dY + (int64_t)row * K);
+  const int nv = K / 4;
+  float4 xv[NV], gv[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int v = lane + i * 32;
+    xv[i] = v < nv ? __ldg(xr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+    gv[i] = v < nv ? __ldg(dyr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float mu = 0.0f;
+  if (centred) {
+    double sx = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      sx += ((double)xv[i].x + (double)xv[i].y) + ((double)xv[i].z + (double)xv[i].w);
+    mu = (float)(warp_sum_f64(sx) / (double)K);
+  }
+  double sdx = 0.0, sdy = 0.0, sxc = 0.0;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    if (lane + i * 32 >= nv) continue;
+    const float xs[4] = {xv[i].x, xv[i].y, xv[i].z, xv[i].w};
+    const float gs[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double xc = (double)xs[j] - (double)mu, g = (double)gs[j];
+      sdx = fma(g, xc, sdx);
+      sdy += g;
+      sxc += xc;
+    }
+  }
+  sdx = warp_sum_f64(sdx);
+  const double rd = (double)__ldg(r + row);
+  const double dsig = sdx * -0.5 * rd * rd * rd;
+  double dmu = 0.0;
+  if (centred) {
+    sdy = warp_sum_f64(sdy);
+    sxc = warp_sum_f64(sxc);
+    dmu = -rd * sdy + dsig * (sxc / (double)K);
+  }
+  const double c1 = 2.0 * dsig / (double)K, c0 = dmu / (double)K;
+  float4* dxr = reinterpret_cast<float4*>(dX + (int64_t)row * K);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int v = lane + i * 32;
+    if (v >= nv) continue;
+    const float xs[4] = {xv[i].x, xv[i].y, xv[i].z, xv[i].w};
+    const float gs[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      o[j] = (float)(rd * (double)gs[j] + c1 * ((double)xs[j] - (double)mu) + c0);
+    dxr[v] = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 static cudaError_t launch_bwd_norm(const float* x, const float* dY, const float* r, int m, int k,
                                    int centred, float* dX, cudaStream_t s) {
+  // rows up to 1024 elements: a warp per row (registers, shuffles); longer rows: a CTA per row
+  const unsigned gw = (unsigned)((m + 7) / 8);
+  if (k <= 512) return launch_pdl(k_bwd_norm_w<4>, dim3(gw), dim3(256), 0, s, x, dY, r, m, k, centred, dX);
+  if (k <= 1024) return launch_pdl(k_bwd_norm_w<8>, dim3(gw), dim3(256), 0, s, x, dY, r, m, k, centred, dX);
   const int nv = (k / 4 + kBwdThreads - 1) / kBwdThreads;   // float4 vectors per thread
   if (nv <= 1) return launch_pdl(k_bwd_norm<1>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
   if (nv <= 2) return launch_pdl(k_bwd_norm<2>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
