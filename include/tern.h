@@ -367,8 +367,9 @@ tern_status stack_decode(const tern_block* blocks, int32_t L, const void* x, voi
  *   db = sum over the m tokens of dO
  * mu, r, q, deq are the forward's (recomputed from x with the forward's own quantizer,
  * B3); no gain (Alg. 1 has none).  Arguments (device pointers, caller-owned):
- *   x  [m][k] fp32, row-major, the forward input;  w: one segment (n_seg = 1) with its
- *   u8 copy e8 (tern_expand);  dO [m][n_out] fp32;  outputs dX [m][k], dW [n_out][k] (the
+ *   x  [m][k] of dt (fp32, or bf16 widened exactly -- the bf16 configs; bf16 needs the
+ *   tensor-core path), row-major, the forward input;  w: one segment (n_seg = 1) with its
+ *   u8 copy e8 (tern_expand);  dO [m][n_out] of dt;  outputs fp32 dX [m][k], dW [n_out][k] (the
  *   latent weight's layout), db [n_out] (NULL = skip), all fp32;  ws >=
  *   bitlinear_bwd_workspace(m, k, n_out) bytes, 16-byte aligned.  m == 0 writes dW = 0
  *   and db = 0.  Deterministic sums (no atomics).
@@ -379,8 +380,8 @@ size_t bitlinear_bwd_workspace(int32_t m, int32_t k, int32_t n_out);
  * the fp32 operand, reading B7); 0: fp32 CUDA-core GEMMs (the reference path). */
 void tern_set_bwd_tc(int32_t on);
 int32_t tern_get_bwd_tc(void);
-tern_status bitlinear_bwd(const float* x, int32_t m, int32_t k, const tern_weight* w, float eps,
-                          int32_t norm, const float* dO, float* dX, float* dW, float* db,
+tern_status bitlinear_bwd(const void* x, tern_dtype dt, int32_t m, int32_t k, const tern_weight* w,
+                          float eps, int32_t norm, const void* dO, float* dX, float* dW, float* db,
                           void* ws, size_t ws_bytes, tern_stream stream);
 
 /* ------------------------------------------------------------------------

@@ -104,8 +104,8 @@ _SIGS = {
                                 C.c_int, I32, C.POINTER(tern_bl_taps), P, SZ, P]),
     "tern_contract": (C.c_int, [P, I32, I32, P, C.POINTER(tern_weight), P, I32, P]),
     "bitlinear_bwd_workspace": (SZ, [I32, I32, I32]),
-    "bitlinear_bwd": (C.c_int, [P, I32, I32, C.POINTER(tern_weight), F, I32, P, P, P, P, P, SZ,
-                                P]),
+    "bitlinear_bwd": (C.c_int, [P, C.c_int, I32, I32, C.POINTER(tern_weight), F, I32, P, P, P, P,
+                                P, SZ, P]),
     "tern_mlgru_scan": (C.c_int, [P, C.c_int, I32, I32, I32, C.c_int, P, P, P]),
     "tern_mlgru_workspace": (SZ, [C.POINTER(tern_mlgru), I32, I32, I32, C.c_int]),
     "tern_mlgru_chunks": (I32, [C.POINTER(tern_mlgru), I32, I32, I32]),
@@ -260,14 +260,16 @@ def bitlinear_fwd(x, w: tern_weight, y, gain=None, bias=None, eps=1e-6, taps=Non
 
 def bitlinear_bwd(x, w: tern_weight, dO, dX, dW, db=None, eps=1e-6, norm=TERN_NORM_RMS,
                   ws=None, stream=None):
-    """Alg. 1 BackwardPass of one BitLinear (include/tern.h); fp32 tensors."""
+    """Alg. 1 BackwardPass of one BitLinear (include/tern.h): x and dO fp32 or
+    bf16 (same dtype), fp32 dX, dW, db."""
     m, k = x.shape
     L = load()
     need = int(L.bitlinear_bwd_workspace(m, k, w.n_out))
     if ws is None:
         ws = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
-    _check(L.bitlinear_bwd(ptr(x), m, k, C.byref(w), eps, int(norm), ptr(dO), ptr(dX), ptr(dW),
-                           ptr(db), ptr(ws), ws.numel(), stream_handle(stream)), "bitlinear_bwd")
+    _check(L.bitlinear_bwd(ptr(x), dtype_code(x.dtype), m, k, C.byref(w), eps, int(norm), ptr(dO),
+                           ptr(dX), ptr(dW), ptr(db), ptr(ws), ws.numel(), stream_handle(stream)),
+           "bitlinear_bwd")
 
 
 def tern_contract(q, qsum, w: tern_weight, acc, stream=None):

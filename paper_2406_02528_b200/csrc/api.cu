@@ -503,9 +503,11 @@ size_t bitlinear_bwd_workspace(int32_t m, int32_t k, int32_t n) {
   return bwd_workspace(m, k, n);
 }
 
-tern_status bitlinear_bwd(const float* x, int32_t m, int32_t k, const tern_weight* w, float eps,
-                          int32_t norm, const float* dO, float* dX, float* dW, float* db, void* ws,
-                          size_t ws_bytes, tern_stream stream) {
+tern_status bitlinear_bwd(const void* x, tern_dtype dt, int32_t m, int32_t k, const tern_weight* w,
+                          float eps, int32_t norm, const void* dO, float* dX, float* dW, float* db,
+                          void* ws, size_t ws_bytes, tern_stream stream) {
+  CHECK(valid_dt(dt), "bitlinear_bwd: bad dtype");
+  CHECK(dt == TERN_F32 || g_bwd_tc, "bitlinear_bwd: bf16 inputs need the tensor-core path");
   CHECK(m >= 0 && k > 0 && k % 16 == 0, "bitlinear_bwd: m=%d k=%d", m, k);
   CHECK(norm == TERN_NORM_RMS || norm == TERN_NORM_CENTERED, "bitlinear_bwd: norm=%d", norm);
   tern_status st = check_weight(w, k, 1, "bitlinear_bwd");
@@ -526,7 +528,8 @@ tern_status bitlinear_bwd(const float* x, int32_t m, int32_t k, const tern_weigh
         "bitlinear_bwd: workspace too small (%zu < %zu)", ws_bytes, bwd_workspace(m, k, w->n_out));
   st = check_device();
   if (st) return st;
-  TRY_CUDA(launch_bitlinear_bwd(x, m, k, *w, eps, norm, dO, dX, dW, db, ws, (cudaStream_t)stream),
+  TRY_CUDA(launch_bitlinear_bwd(x, dt, m, k, *w, eps, norm, dO, dX, dW, db, ws,
+                                (cudaStream_t)stream),
            "bitlinear_bwd");
   return TERN_OK;
 }

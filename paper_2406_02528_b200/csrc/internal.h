@@ -105,9 +105,9 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
 // f4(iii) Alg. 1 backward (k_bwd.cu); g_bwd_tc: tensor-core contractions (tern_set_bwd_tc)
 extern int g_bwd_tc;
 size_t bwd_workspace(int m, int k, int n);
-cudaError_t launch_bitlinear_bwd(const float* x, int m, int k, const tern_weight& w, float eps,
-                                 int norm, const float* dO, float* dX, float* dW, float* db,
-                                 void* ws, cudaStream_t s);
+cudaError_t launch_bitlinear_bwd(const void* x, int dt, int m, int k, const tern_weight& w,
+                                 float eps, int norm, const void* dO, float* dX, float* dW,
+                                 float* db, void* ws, cudaStream_t s);
 // whether launch_gemm runs a QFuse request inside the GEMM (else it launches k_quant first)
 bool gemm_qfuse_ok(int M, const tern_weight& w, const Epi& epi, int32_t* part, size_t part_bytes);
 // batched decode: one CTA per row sums the ks partial slices [ks][M][n_rows],

@@ -148,14 +148,25 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
   for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
   return s;
 }
+// 4 consecutive activation values (vector v of the row) as floats: fp32 or bf16 storage
+template <typename TX> __device__ __forceinline__ float4 ld4(const TX* row, int v);
+template <> __device__ __forceinline__ float4 ld4<float>(const float* row, int v) {
+  return __ldg(reinterpret_cast<const float4*>(row) + v);
+}
+template <> __device__ __forceinline__ float4 ld4<__nv_bfloat16>(const __nv_bfloat16* row, int v) {
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(row) + v);
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                     __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+}
+
 // NV float4 vectors of x and dY per thread held in registers (K <= 1024 NV), one read of each
-template <int NV>
+template <int NV, typename TX>
 __global__ void __launch_bounds__(kBwdThreads)
-    k_bwd_norm(const float* __restrict__ x, const float* __restrict__ dY, const float* __restrict__ r,
+    k_bwd_norm(const TX* __restrict__ x, const float* __restrict__ dY, const float* __restrict__ r,
                int K, int centred, float* __restrict__ dX) {
   __shared__ double red[kBwdThreads / 32];
   const int row = blockIdx.x;
-  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)row * K);
+  const TX* xr = x + (int64_t)row * K;
   const float4* dyr = reinterpret_cast<const float4*>(dY + (int64_t)row * K);
   const int nv = K / 4;
   pdl_wait();
@@ -164,7 +175,7 @@ __global__ void __launch_bounds__(kBwdThreads)
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int v = threadIdx.x + i * kBwdThreads;
-    xv[i] = v < nv ? __ldg(xr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+    xv[i] = v < nv ? ld4<TX>(xr, v) : make_float4(0.f, 0.f, 0.f, 0.f);
     gv[i] = v < nv ? __ldg(dyr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   float mu = 0.0f;
@@ -217,23 +228,23 @@ __global__ void __launch_bounds__(kBwdThreads)
 
 // the same with one warp per row (K <= 128 NV: 32 lanes x NV float4 each of x and dY): shuffle
 // reductions only, no block barriers, 8 rows per CTA
-template <int NV>
+template <int NV, typename TX>
 __global__ void __launch_bounds__(256)
-    k_bwd_norm_w(const float* __restrict__ x, const float* __restrict__ dY, const float* __restrict__ r,
+    k_bwd_norm_w(const TX* __restrict__ x, const float* __restrict__ dY, const float* __restrict__ r,
                  int M, int K, int centred, float* __restrict__ dX) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   pdl_wait();
   pdl_launch_dependents();
   if (row >= M) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)row * K);
+  const TX* xr = x + (int64_t)row * K;
   const float4* dyr = reinterpret_cast<const float4*>(dY + (int64_t)row * K);
   const int nv = K / 4;
   float4 xv[NV], gv[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int v = lane + i * 32;
-    xv[i] = v < nv ? __ldg(xr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+    xv[i] = v < nv ? ld4<TX>(xr, v) : make_float4(0.f, 0.f, 0.f, 0.f);
     gv[i] = v < nv ? __ldg(dyr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   float mu = 0.0f;
@@ -283,18 +294,19 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-static cudaError_t launch_bwd_norm(const float* x, const float* dY, const float* r, int m, int k,
+template <typename TX>
+static cudaError_t launch_bwd_norm(const TX* x, const float* dY, const float* r, int m, int k,
                                    int centred, float* dX, cudaStream_t s) {
   // rows up to 1024 elements: a warp per row (registers, shuffles); longer rows: a CTA per row
   const unsigned gw = (unsigned)((m + 7) / 8);
-  if (k <= 512) return launch_pdl(k_bwd_norm_w<4>, dim3(gw), dim3(256), 0, s, x, dY, r, m, k, centred, dX);
-  if (k <= 1024) return launch_pdl(k_bwd_norm_w<8>, dim3(gw), dim3(256), 0, s, x, dY, r, m, k, centred, dX);
+  if (k <= 512) return launch_pdl(k_bwd_norm_w<4, TX>, dim3(gw), dim3(256), 0, s, x, dY, r, m, k, centred, dX);
+  if (k <= 1024) return launch_pdl(k_bwd_norm_w<8, TX>, dim3(gw), dim3(256), 0, s, x, dY, r, m, k, centred, dX);
   const int nv = (k / 4 + kBwdThreads - 1) / kBwdThreads;   // float4 vectors per thread
-  if (nv <= 1) return launch_pdl(k_bwd_norm<1>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
-  if (nv <= 2) return launch_pdl(k_bwd_norm<2>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
-  if (nv <= 4) return launch_pdl(k_bwd_norm<4>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
-  if (nv <= 8) return launch_pdl(k_bwd_norm<8>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
-  return launch_pdl(k_bwd_norm<16>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
+  if (nv <= 1) return launch_pdl(k_bwd_norm<1, TX>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
+  if (nv <= 2) return launch_pdl(k_bwd_norm<2, TX>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
+  if (nv <= 4) return launch_pdl(k_bwd_norm<4, TX>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
+  if (nv <= 8) return launch_pdl(k_bwd_norm<8, TX>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
+  return launch_pdl(k_bwd_norm<16, TX>, dim3(m), dim3(kBwdThreads), 0, s, x, dY, r, k, centred, dX);
 }
 
 // db[n] = sum over the M tokens of dO[m][n]: 32 columns per CTA, 8 warps over the rows, the
@@ -470,8 +482,9 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
 // Adw [n][2 mp] = [hi | lo] of the transposed dO' = dO deq[m] (mp = roundup(m, 64)), and
 // the column sums of this CTA's 64 rows, dbp[blockIdx.y][n] (rows in order); 64 x 64 tiles
 // through shared memory, column pairs per thread (bf16x2 stores)
+template <typename TD>
 __global__ void __launch_bounds__(256)
-    k_bwd_prep_do(const float* __restrict__ dO, const float* __restrict__ deq, int m, int n,
+    k_bwd_prep_do(const TD* __restrict__ dO, const float* __restrict__ deq, int m, int n,
                   int np, int mp, uint32_t* __restrict__ Ady, uint32_t* __restrict__ Adw,
                   float* __restrict__ dbp) {
   __shared__ float t[64][65];
@@ -488,12 +501,17 @@ __global__ void __launch_bounds__(256)
       const int r = grp * 8 + i, mm = m0 + r;
       float2 v = make_float2(0.0f, 0.0f);
       if (mm < m) {
-        const float* src = dO + (int64_t)mm * n + c;
+        const TD* src = dO + (int64_t)mm * n + c;
         if (c + 1 < n && (n & 1) == 0) {
-          v = __ldg(reinterpret_cast<const float2*>(src));
+          if constexpr (sizeof(TD) == 4) {
+            v = __ldg(reinterpret_cast<const float2*>(src));
+          } else {
+            const uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(src));
+            v = make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+          }
         } else {
-          if (c < n) v.x = __ldg(src);
-          if (c + 1 < n) v.y = __ldg(src + 1);
+          if (c < n) v.x = ld_act<TD>(src);
+          if (c + 1 < n) v.y = ld_act<TD>(src + 1);
         }
       }
       if (mm < m && c < np) {
@@ -676,9 +694,14 @@ static BwdWs bwd_ws(int m, int k, int n) {
 
 size_t bwd_workspace(int m, int k, int n) { return bwd_ws(m, k, n).total; }
 
-cudaError_t launch_bitlinear_bwd(const float* x, int m, int k, const tern_weight& w, float eps,
-                                 int norm, const float* dO, float* dX, float* dW, float* db,
-                                 void* ws, cudaStream_t s) {
+cudaError_t launch_bitlinear_bwd(const void* xv, int dt, int m, int k, const tern_weight& w,
+                                 float eps, int norm, const void* dOv, float* dX, float* dW,
+                                 float* db, void* ws, cudaStream_t s) {
+  const bool bf = dt == TERN_BF16;   // (bf16 x and dO: the tensor-core path only, checked by the API)
+  const float* x = static_cast<const float*>(xv);
+  const float* dO = static_cast<const float*>(dOv);
+  const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(xv);
+  const __nv_bfloat16* dOb = static_cast<const __nv_bfloat16*>(dOv);
   if (m == 0) return cudaSuccess;
   const int kp = (k + kKAlign - 1) / kKAlign * kKAlign;
   const int n = w.n_out;
@@ -690,7 +713,7 @@ cudaError_t launch_bitlinear_bwd(const float* x, int m, int k, const tern_weight
   float* r = reinterpret_cast<float*>(base + L.r);
   float* dY = reinterpret_cast<float*>(base + L.dy);
   // the forward's r, q, deq (B3)
-  cudaError_t e = launch_quant(x, TERN_F32, m, k, k, nullptr, eps, q, kp, deq, qsum, r, nullptr, s,
+  cudaError_t e = launch_quant(xv, dt, m, k, k, nullptr, eps, q, kp, deq, qsum, r, nullptr, s,
                                norm);
   if (e != cudaSuccess) return e;
   if (g_bwd_tc) {
@@ -701,9 +724,13 @@ cudaError_t launch_bitlinear_bwd(const float* x, int m, int k, const tern_weight
     auto* Qt = reinterpret_cast<__nv_bfloat16*>(base + L.qt);
     float* part = reinterpret_cast<float*>(base + L.part);
     float* dbp = reinterpret_cast<float*>(base + L.dbp);
-    e = launch_pdl(k_bwd_prep_do, dim3((np + 63) / 64, (mp + 63) / 64), dim3(256), 0, s, dO,
-                   (const float*)deq, m, n, np, mp, reinterpret_cast<uint32_t*>(Ady),
-                   reinterpret_cast<uint32_t*>(Adw), dbp);
+    const dim3 gp((np + 63) / 64, (mp + 63) / 64);
+    e = bf ? launch_pdl(k_bwd_prep_do<__nv_bfloat16>, gp, dim3(256), 0, s, dOb, (const float*)deq,
+                        m, n, np, mp, reinterpret_cast<uint32_t*>(Ady),
+                        reinterpret_cast<uint32_t*>(Adw), dbp)
+           : launch_pdl(k_bwd_prep_do<float>, gp, dim3(256), 0, s, dO, (const float*)deq, m, n,
+                        np, mp, reinterpret_cast<uint32_t*>(Ady), reinterpret_cast<uint32_t*>(Adw),
+                        dbp);
     if (e != cudaSuccess) return e;
     if (db) {
       e = launch_pdl(k_bwd_dbsum, dim3((n + 31) / 32), dim3(256), 0, s, (const float*)dbp,
@@ -720,7 +747,8 @@ cudaError_t launch_bitlinear_bwd(const float* x, int m, int k, const tern_weight
     // dY [m][k] = (dO_hi | dO_lo) x (T | T)^T * m_w
     e = bwd_mma(Ady, Tt, m, k, np, w.scales, dY, k, part, L.part_floats, s);
     if (e != cudaSuccess) return e;
-    e = launch_bwd_norm(x, dY, r, m, k, norm == TERN_NORM_CENTERED ? 1 : 0, dX, s);
+    e = bf ? launch_bwd_norm(xb, dY, r, m, k, norm == TERN_NORM_CENTERED ? 1 : 0, dX, s)
+           : launch_bwd_norm(x, dY, r, m, k, norm == TERN_NORM_CENTERED ? 1 : 0, dX, s);
     if (e != cudaSuccess) return e;
     // dW [n][k] = (dO'^T_hi | dO'^T_lo) x (q^T | q^T)^T
     e = bwd_mma(Adw, Qt, n, k, mp, nullptr, dW, k, part, L.part_floats, s);

@@ -144,20 +144,20 @@ def test_validation_of_the_backward_and_qfuse_knobs(lib):
     w1.e8 = 0x4000
     ws = 1 << 30
     bw = lib.bitlinear_bwd
-    assert bw(fake, 4, 120, C.byref(w1), 1e-6, 0, fake, fake, fake, None, fake, ws, None) == \
+    assert bw(fake, 0, 4, 120, C.byref(w1), 1e-6, 0, fake, fake, fake, None, fake, ws, None) == \
         L.TERN_ERR_INVALID_ARG
     w3 = L.tern_weight(0x1000, 0x2000, 64, 128, 8, 3, 192)
     w3.e8 = 0x4000
-    assert bw(fake, 4, 128, C.byref(w3), 1e-6, 0, fake, fake, fake, None, fake, ws, None) == \
+    assert bw(fake, 0, 4, 128, C.byref(w3), 1e-6, 0, fake, fake, fake, None, fake, ws, None) == \
         L.TERN_ERR_INVALID_ARG
     w0 = L.tern_weight(0x1000, 0x2000, 64, 128, 8, 1, 64)   # no e8
-    assert bw(fake, 4, 128, C.byref(w0), 1e-6, 0, fake, fake, fake, None, fake, ws, None) == \
+    assert bw(fake, 0, 4, 128, C.byref(w0), 1e-6, 0, fake, fake, fake, None, fake, ws, None) == \
         L.TERN_ERR_INVALID_ARG and b"e8" in lib.tern_last_error()
-    assert bw(fake, 4, 128, C.byref(w1), 1e-6, 3, fake, fake, fake, None, fake, ws, None) == \
+    assert bw(fake, 0, 4, 128, C.byref(w1), 1e-6, 3, fake, fake, fake, None, fake, ws, None) == \
         L.TERN_ERR_INVALID_ARG and b"norm" in lib.tern_last_error()
     need = lib.bitlinear_bwd_workspace(4, 128, 64)
     assert need > 4 * 128 * 4
-    assert bw(fake, 4, 128, C.byref(w1), 1e-6, 0, fake, fake, fake, None, fake, need - 16, None) \
+    assert bw(fake, 0, 4, 128, C.byref(w1), 1e-6, 0, fake, fake, fake, None, fake, need - 16, None) \
         == L.TERN_ERR_INVALID_ARG and b"workspace" in lib.tern_last_error()
     assert lib.bitlinear_bwd_workspace(0, 128, 64) == 0
     for get, put in ((lib.tern_get_qfuse, lib.tern_set_qfuse),

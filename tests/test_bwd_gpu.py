@@ -56,14 +56,26 @@ def test_bwd_parity(L, M, m, k, n, norm, tc):
         L.tern_set_bwd_tc(old)
 
 
-def _bwd_case(L, M, m, k, n, norm):
+@pytest.mark.parametrize("m,k,n,norm", [(300, 2048, 1000, 0), (513, 5632, 2048, 1)])
+def test_bwd_parity_bf16(L, M, m, k, n, norm):
+    """bf16 inputs (the c3 / c4 activation dtype, widened exactly for the oracle) on the
+    tensor-core path; the CUDA-core path rejects them."""
+    _bwd_case(L, M, m, k, n, norm, "bf16")
+
+
+def _bwd_case(L, M, m, k, n, norm, dtype="f32"):
     g = synth.generator(m + k + n + norm)
     W = synth.latent_matrix(n, k, g)
     x = synth.hidden((m, k), g, "f32") * 1.3 + 0.2
     dO = synth.hidden((m, n), g, "f32")
+    if dtype == "bf16":
+        x = x.to(torch.bfloat16).float()   # values exactly representable in both
+        dO = dO.to(torch.bfloat16).float()
     pw = M.PackedWeight([W.cuda()])
     t, mw = O.ternarize(W.numpy())
     xd, dOd = x.cuda(), dO.cuda()
+    if dtype == "bf16":
+        xd, dOd = xd.to(torch.bfloat16), dOd.to(torch.bfloat16)
     dX = torch.empty((m, k), device="cuda")
     dW = torch.empty((n, k), device="cuda")
     db = torch.empty(n, device="cuda")
@@ -96,3 +108,12 @@ def test_bwd_edge_cases(L, M):
     with pytest.raises(L.TernError):
         L.bitlinear_bwd(x, pw.struct, torch.randn(4, n, device="cuda"),
                         torch.empty_like(x), dW, db, norm=5)
+    old = L.tern_get_bwd_tc()
+    L.tern_set_bwd_tc(False)
+    try:
+        with pytest.raises(L.TernError):   # bf16 only on the tensor-core path
+            L.bitlinear_bwd(x.to(torch.bfloat16), pw.struct,
+                            torch.randn(4, n, device="cuda").to(torch.bfloat16),
+                            torch.empty_like(x), dW, db)
+    finally:
+        L.tern_set_bwd_tc(old)
