@@ -623,9 +623,10 @@ static int bwd_sms() {
 }
 
 // C[I][J] = alpha * sum_{k < 2 kp_half} A[i][k] B[j][k mod kp_half], A [I][2 kp_half], B [J][kp_half]
+// hi_only: the fp32 operand is exactly bf16 (lo = 0), so only the hi half is contracted
 static cudaError_t bwd_mma(const __nv_bfloat16* A, const __nv_bfloat16* B, int I, int J,
                            int kp_half, const float* alpha, float* out, int ldo, float* part,
-                           size_t part_floats, cudaStream_t s) {
+                           size_t part_floats, cudaStream_t s, bool hi_only = false) {
   constexpr int BN = 256;
   CUtensorMap ta, tb;
   if (!make_map_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, A, (uint64_t)2 * kp_half, (uint64_t)I,
@@ -633,7 +634,7 @@ static cudaError_t bwd_mma(const __nv_bfloat16* A, const __nv_bfloat16* B, int I
       !make_map_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, B, (uint64_t)kp_half, (uint64_t)J,
                    (uint64_t)kp_half * 2, kBwdKB, BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  const int nkb = 2 * kp_half / kBwdKB, nkb_b = kp_half / kBwdKB;
+  const int nkb_b = kp_half / kBwdKB, nkb = hi_only ? nkb_b : 2 * nkb_b;
   const int tiles = ((I + 127) / 128) * ((J + BN - 1) / BN);
   // split the contraction when the tiles cannot fill the SMs (dW: few tiles, long K)
   int ks = 1;
@@ -745,7 +746,7 @@ cudaError_t launch_bitlinear_bwd(const void* xv, int dt, int m, int k, const ter
                    reinterpret_cast<uint32_t*>(Qt));
     if (e != cudaSuccess) return e;
     // dY [m][k] = (dO_hi | dO_lo) x (T | T)^T * m_w
-    e = bwd_mma(Ady, Tt, m, k, np, w.scales, dY, k, part, L.part_floats, s);
+    e = bwd_mma(Ady, Tt, m, k, np, w.scales, dY, k, part, L.part_floats, s, bf);
     if (e != cudaSuccess) return e;
     e = bf ? launch_bwd_norm(xb, dY, r, m, k, norm == TERN_NORM_CENTERED ? 1 : 0, dX, s)
            : launch_bwd_norm(x, dY, r, m, k, norm == TERN_NORM_CENTERED ? 1 : 0, dX, s);
