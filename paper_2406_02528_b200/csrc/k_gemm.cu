@@ -1414,7 +1414,10 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
   const bool chan = e.kind == EPI_SWIGLU || e.kind == EPI_MLGRU;   // per logical channel
   const int ncol = chan ? e.n_out : (e.kind == EPI_FCG ? n_rows : e.n_out);
   const int npair = (ncol + 1) / 2;
-  if (idx >= (int64_t)M * npair) return;
+  if (idx >= (int64_t)M * npair) {
+    trace_mark(trace, 2);   // (thread 0 of the last CTA may have no pair)
+    return;
+  }
   const int m = (int)(idx / npair), c = (int)(idx % npair) * 2;
   const float dq = __ldg(deq + m);
   const int qs = __ldg(qsum + m);
@@ -1491,6 +1494,7 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
       st_act<TY>(out + (int64_t)m * e.ldo + r0, o0);
       st_act<TY>(out + (int64_t)m * e.ldo + r1, o1);
     }
+    trace_mark(trace, 2);
     return;
   }
   // one segment or the interleaved f|c|g columns: columns c, c+1 (c even)
@@ -1522,6 +1526,7 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
       o = __fadd_rn(ld_act<TY>(static_cast<const TY*>(e.res) + (int64_t)m * e.ldr + r), o);
     st_act<TY>(out + (int64_t)m * e.ldo + (e.kind == EPI_FCG ? col : r), o);
   }
+  trace_mark(trace, 2);
 }
 
 int g_gemm_sab = getenv("TERN_GEMM_SAB") ? (atoi(getenv("TERN_GEMM_SAB")) != 0) : 0;
