@@ -273,7 +273,7 @@ def gemm_bytes(rec: dict, elem: int) -> float:
     else:
         n_out = n // 2 if epi == 4 else n
     b = m * kp + n * kp / 4.0 + m * n_out * elem
-    if rec["kernel"] != "fcgscan" and epi == 1:   # residual epilogue reads x
+    if rec["kernel"] != "fcgscan" and epi in (1, 6):   # residual epilogue reads x (6: in place)
         b += m * n_out * elem
     if rec["kernel"] == "gemm_qf":
         b += qf_bytes(rec, elem) - m * kp   # (the A read is in both)
@@ -335,7 +335,7 @@ def roofline(records, elem, pk, traffic_db, clocks=None):
         kernels[name].update({"share": round(e["ms"] / tot, 4), "launches": e["launches"],
                               "ms_total": round(e["ms"], 3),
                               "ms_per_launch": round(e["ms"] / e["launches"], 5)})
-    epi_names = {0: "store", 1: "resid", 2: "fcg", 3: "mlgru", 4: "swiglu", 5: "acc"}
+    epi_names = {0: "store", 1: "resid", 2: "fcg", 3: "mlgru", 4: "swiglu", 5: "acc", 6: "resid_red"}
     sub = {}
     for r in records:
         if r["kernel"] not in ("gemm_tc", "gemm_qf", "gemv", "fcgscan"):

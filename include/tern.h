@@ -305,7 +305,9 @@ size_t tern_block_workspace(const tern_block* b, int32_t B, int32_t T, tern_dtyp
 /* Byte offsets of the block's intermediates inside its workspace, valid after
  * block_prefill / block_decode returns on the stream (parity taps):
  *   fcg [B*T][3d], oprime [B*T][d], x1 [B*T][d], p [B*T][l], all dtype dt
- *   (sharded blocks: fcg of the rank's channels; oprime, x1, p gathered whole). */
+ *   (sharded blocks: fcg of the rank's channels; oprime, x1, p gathered whole).
+ *   fp32 prefill with more than 256 tokens writes x1 into y instead and adds the channel
+ *   mixer onto it in place (TMA reduce-add), so the x1 tap is not written there. */
 typedef struct {
   size_t fcg, oprime, x1, p;
 } tern_block_taps;

@@ -20,6 +20,9 @@ thread_local std::string g_err;
 int g_gemv_max_m = kGemvMaxM;
 int g_fused_scan = 1;
 int g_batched_fin = 0;   // tern_set_batched_fin
+// fp32 block prefill: x1 is written into y and the channel mixer's down projection is added
+// onto it in place (EPI_RESID_RED, TMA reduce-add) -- no residual tile loads in its drain
+int g_resid_red = getenv("TERN_RESID_RED") ? (atoi(getenv("TERN_RESID_RED")) != 0) : 1;
 int g_norm_mode = TERN_NORM_RMS;   // tern_set_norm_mode (tern_quant, bitlinear_fwd)
 constexpr int kSplitKMaxM = 256;
 
@@ -859,13 +862,15 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
 }
 
 // channel mixer: x [M][d] -> out (d, or y = x + d when resid)
+// in_place: x is `out` (the block's x1 written into y), the residual added in place
 tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, tern_dtype dt, int M,
                     int d, int l, void* ws, const BlockWs& L, cudaStream_t s,
-                    const PfPlan& pf = PfPlan(), bool qf_ready = false) {
+                    const PfPlan& pf = PfPlan(), bool qf_ready = false, bool in_place = false) {
   void* pp = at<char>(ws, L.p);
   Epi e1 = make_epi(EPI_SWIGLU, p.gu, nullptr, pp, l);
-  Epi e2 = make_epi(resid ? EPI_RESID : EPI_STORE, p.down, nullptr, out, d);
-  e2.res = x;
+  Epi e2 = make_epi(in_place ? EPI_RESID_RED : (resid ? EPI_RESID : EPI_STORE), p.down, nullptr,
+                    out, d);
+  e2.res = in_place ? nullptr : x;
   e2.ldr = d;
   if (M <= g_gemv_max_m && gemv_supported(M, d, dt) && gemv_supported(M, l, dt)) {
     {
@@ -1242,9 +1247,14 @@ static tern_status block_run(const tern_block* b, const void* x, void* y, tern_d
       pg.n[1] = codes_bytes(nb->mix.o);
     }
   }
+  // fp32 prefill on the tensor-core path: x1 goes into y and the down projection is added
+  // onto it in place (EPI_RESID_RED)
+  const bool red = g_resid_red && dt == TERN_F32 && T > 1 && B * T > kSplitKMaxM &&
+                   b->mix.norm == TERN_NORM_RMS;
+  if (red) x1 = y;
   if ((st = run_mlgru(b->mix, x, x1, true, dt, B, T, b->d, h, ws, L, s, pm)) != TERN_OK) return st;
   // prefill: the token mixer's quant of x zeroed the gate|up counters (QFuse)
-  return run_glu(b->ch, x1, y, true, dt, B * T, b->d, b->l, ws, L, s, pg, T > 1);
+  return run_glu(b->ch, x1, y, true, dt, B * T, b->d, b->l, ws, L, s, pg, T > 1, red);
 }
 
 // ---------------------------------------------------------------- sequence-parallel prefill

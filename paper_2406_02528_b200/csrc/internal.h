@@ -18,7 +18,9 @@ enum EpiKind : int {
   EPI_FCG = 2,     // y[m][packed row] = R1(dequant + bias)  (interleaved pre-activations)
   EPI_MLGRU = 3,   // decode: f,c,g -> h update -> o'[m][r]              (n_seg == 3, GEMV)
   EPI_SWIGLU = 4,  // p[m][r] = R2(SiLU(R1 g) * R1 u)                    (n_seg == 2)
-  EPI_NONE = 5     // accumulators only (tap)
+  EPI_NONE = 5,    // accumulators only (tap)
+  EPI_RESID_RED = 6  // fp32: y[m][r] += R1(dequant + bias) in place (y holds the residual;
+                     // TMA reduce-add in the tensor-core GEMMs, one IEEE fp32 add = EPI_RESID's)
 };
 
 struct Epi {

@@ -117,6 +117,14 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, 
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
+// the staging tile added element-wise onto the global tensor (fp32 add at L2, one IEEE
+// rounding per element: the residual add of EPI_RESID_RED)
+__device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, const void* src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N> __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
@@ -879,7 +887,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lead) {
-          tma_store_2d(&tmO, sb, out_col0, row0);   // rows >= M / cols >= n clipped by TMA
+          // rows >= M / cols >= n clipped by TMA
+          if (e.kind == EPI_RESID_RED) tma_reduce_add_2d(&tmO, sb, out_col0, row0);
+          else tma_store_2d(&tmO, sb, out_col0, row0);
           bulk_commit();
         }
         ++nchunk;
@@ -1228,7 +1238,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lead) {
-          tma_store_2d(&tmO, sb, out_col0, row0);   // rows >= M / cols >= n clipped by TMA
+          // rows >= M / cols >= n clipped by TMA
+          if (e.kind == EPI_RESID_RED) tma_reduce_add_2d(&tmO, sb, out_col0, row0);
+          else tma_store_2d(&tmO, sb, out_col0, row0);
           bulk_commit();
         }
         ++nchunk;
@@ -1524,6 +1536,8 @@ __global__ void k_splitk_epi(const int32_t* __restrict__ part, int ksplit, int M
     float o = dqv((j == 0 ? a.x : a.y) - qs, seg, r);
     if (e.kind == EPI_RESID)
       o = __fadd_rn(ld_act<TY>(static_cast<const TY*>(e.res) + (int64_t)m * e.ldr + r), o);
+    else if (e.kind == EPI_RESID_RED)   // the residual is already in place
+      o = __fadd_rn(ld_act<TY>(out + (int64_t)m * e.ldo + r), o);
     st_act<TY>(out + (int64_t)m * e.ldo + (e.kind == EPI_FCG ? col : r), o);
   }
   trace_mark(trace, 2);

@@ -56,7 +56,7 @@ for _ in range(args.steps):
 torch.cuda.synchronize()
 L.tern_profile_enable(False)
 recs = L.tern_profile_collect()
-epi = {0: "store", 1: "resid", 2: "fcg", 3: "mlgru", 4: "swiglu", 5: "acc"}
+epi = {0: "store", 1: "resid", 2: "fcg", 3: "mlgru", 4: "swiglu", 5: "acc", 6: "resid_red"}
 agg = collections.OrderedDict()
 for r in recs:
     key = f'{r["kernel"]}:{epi.get(r["epi"], r["epi"]) if r["kernel"] != "quant" else ""}:n{r["n"]}k{r["k"]}'
