@@ -614,3 +614,33 @@ def test_qfuse_full_size_prefixes(L, M, cfg_name, n_tok):
             assert np.array_equal(yg, yo), f"{cfg_name} sequence {b}"
     finally:
         L.tern_set_qfuse(old)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_qfuse_with_gains_and_biases(L, M, dtype):
+    """QFuse with per-feature norm gains (the fused quantizer's max|x r w| pass) and biases,
+    1 block of 2 x 300 tokens, against the oracle block."""
+    d, l, B, T = 512, 1408, 2, 300
+    g = synth.generator(77)
+    lat = synth.latent_block(d, l, g)
+    gg = synth.generator(78)
+    gains = {k: (1.0 + 0.25 * torch.randn(n, generator=gg)).cuda()
+             for k, n in (("x", d), ("o", d), ("x1", d), ("p", l))}
+    biases = {k: (0.05 * torch.randn(d, generator=gg)).cuda() for k in ("f", "c", "g", "o")}
+    blk = M.Block(lat, d, l, gains=gains, biases=biases)
+    st = M.Stack([blk], d, l, synth.torch_dtype(dtype))
+    ob = O.OracleBlock({k: v.numpy() for k, v in lat.items()}, d, l,
+                       gains={k: v.cpu().numpy() for k, v in gains.items()},
+                       biases={k: v.cpu().numpy() for k, v in biases.items()})
+    x = synth.hidden((B, T, d), synth.generator(79), dtype)
+    old = L.tern_get_qfuse()
+    L.tern_set_qfuse(True)
+    try:
+        h = st.new_state(B)
+        y = st.prefill(x.cuda(), h)
+        torch.cuda.synchronize()
+    finally:
+        L.tern_set_qfuse(old)
+    yo, ho = O.block(ob, f32np(x), np.zeros((B, d), np.float32), bf16=dtype == "bf16")
+    close(f32np(y), yo, 2e-2 if dtype == "bf16" else 1e-4, "qfuse gains")
+    assert np.array_equal(f32np(y), yo)
