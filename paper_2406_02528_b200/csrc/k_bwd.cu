@@ -687,7 +687,14 @@ static BwdWs bwd_ws(int m, int k, int n) {
   w.tt = o; o += al256((size_t)k * np * 2);
   w.qt = o; o += al256((size_t)k * mp * 2);
   w.dbp = o; o += al256((size_t)(mp / 64) * n * 4);
-  w.part_floats = (size_t)8 * n * k;
+  // split-K slices exist only while tiles * ks <= the SM count, and I x J <= tiles x 128 x 256,
+  // so SMs x 128 x 256 floats always hold them (19 MB on 148 SMs, whatever the shape)
+  int nsm = 0;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess || nsm < 148) {
+    cudaGetLastError();   // no device (CPU host query): the B200 count
+    nsm = 148;
+  }
+  w.part_floats = (size_t)nsm * 128 * 256;
   w.part = o; o += al256(w.part_floats * 4);
   w.total = o;
   return w;
