@@ -163,7 +163,7 @@ BlockWs block_ws(int32_t M, int32_t d, int32_t l, int32_t fcg_rows, tern_dtype d
   w.deq = off; off += al256((size_t)M * 4);
   w.qsum = off; off += al256((size_t)M * 4);
   // fused-quantization counters (QFuse): one area per fused GEMM of the block (o, gate|up,
-  // down), zeroed by the block's first quant launch
+  // down), zeroed ahead of the block's first quant launch (QFuse mode only)
   w.qf = off; off += al256((size_t)kQfAreas * qf_words(M) * 4);
   w.fcg = off; off += al256((size_t)M * fcg_rows * dsize(dt));
   w.oprime = off; off += al256((size_t)M * d * dsize(dt));
@@ -818,7 +818,7 @@ tern_status run_mlgru(const tern_mlgru& p, const void* x, void* out, bool resid,
   // QFuse counter areas of this block's fused GEMMs (o, gate|up, down): the first quant
   // launch below zeroes them
   uint32_t* qf0 = at<uint32_t>(ws, L.qf);
-  const int nqf = kQfAreas * qf_words(M);
+  const int nqf = g_qfuse_on ? kQfAreas * qf_words(M) : 0;
   // the prefill scan: sequential (1) or chunked over time (4, 8; tern_mlgru.num_chunks)
   const int chunks = T > 1 ? scan_chunks_resolve(p.num_chunks, B, T, d) : 1;
   // the fused kernel walks each sequence's 128-token tiles; short sequences (decode
@@ -896,7 +896,8 @@ tern_status run_glu(const tern_glu& p, const void* x, void* out, bool resid, ter
       ? bl_tc_qf(x, dt, M, d, p.gain_x, p.eps, p.gu, e1, q, kpad(d), deq, qsum, qf0 + qw, s,
                  at<int32_t>(ws, L.part), L.part_bytes, p.norm)
       : bl_tc(x, dt, M, d, d, p.gain_x, p.eps, p.gu, dt, e1, q, kpad(d), deq, qsum, nullptr,
-              nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm, qf0, kQfAreas * qw);
+              nullptr, s, at<int32_t>(ws, L.part), L.part_bytes, p.norm, qf0,
+              g_qfuse_on ? kQfAreas * qw : 0);
   if (st) return st;
   return bl_tc_qf(pp, dt, M, l, p.gain_p, p.eps, p.down, e2, q, kpad(l), deq, qsum, qf0 + 2 * qw,
                   s, at<int32_t>(ws, L.part), L.part_bytes, p.norm);

@@ -67,7 +67,7 @@ cudaError_t launch_quant(const void* x, int xdt, int m, int k, int ldx, const fl
 // warps 2-5 run the RMSNorm + absmax quantization of x row by row (rows taken
 // in a static order), publishing each finished 128-row block in ctr[1 + block]; the TMA
 // producer waits for a block before loading its A tiles.  ctr must be zero at launch
-// ([1 + ceil(M/128)] words; block_ws region qf, zeroed by the block's first quant launch).
+// ([1 + ceil(M/128)] words; block_ws region qf, zeroed ahead of the block's first quant launch).
 struct QFuse {
   const void* x;
   int ldx;

@@ -197,7 +197,6 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
                                                      int32_t* __restrict__ qsum,
                                                      float* __restrict__ inv_rms,
                                                      float* __restrict__ absmax,
-                                                     uint32_t* __restrict__ zero, int nzero,
                                                      unsigned long long* trace) {
   trace_mark(trace, 0);
   constexpr int VE = QVec<TX>::N;
@@ -215,9 +214,6 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
   pdl_wait();                 // x is the previous kernel's output
   pdl_launch_dependents();
   trace_mark(trace, 1);
-  // side job: zero the fused-quantization counters of the block's later GEMMs (QFuse)
-  if (blockIdx.x == 0)
-    for (int i = threadIdx.x; i < nzero; i += kQThreads) zero[i] = 0u;
 
   uint4 xv[NV];
 #pragma unroll
@@ -349,7 +345,7 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
 template <typename TX, int TPR, int NV>
 static void quant_go(const TX* x, int m, int k, int ldx, const float* gain, float eps, int8_t* q,
                      int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
-                     cudaStream_t s, int norm, uint32_t* zero, int nzero) {
+                     cudaStream_t s, int norm) {
   constexpr int RPC = kQThreads / TPR;
   const int grid = (m + RPC - 1) / RPC;
   const double inv_k = 1.0 / (double)k;
@@ -359,50 +355,49 @@ static void quant_go(const TX* x, int m, int k, int ldx, const float* gain, floa
                   : (gain ? k_quant<TX, TPR, NV, true, false>
                           : (full ? k_quant<TX, TPR, NV, false, true> : k_quant<TX, TPR, NV, false, false>));
   launch_pdl(kern, dim3(grid), dim3(kQThreads), 0, s, x, m, k, ldx, gain, eps, inv_k, q, ldq, deq,
-             qsum, inv_rms, absmax, zero, nzero, trace_slot(TERN_K_QUANT, grid));
+             qsum, inv_rms, absmax, trace_slot(TERN_K_QUANT, grid));
 }
 
 template <typename TX, int TPR>
 static void quant_nv(int nv, const TX* x, int m, int k, int ldx, const float* gain, float eps,
                      int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms, float* absmax,
-                     cudaStream_t s, int norm, uint32_t* zero, int nzero) {
+                     cudaStream_t s, int norm) {
   // exactly as many register vectors as the row needs: predicated-off slots of
   // the fully unrolled loops still cost issue slots, and this kernel is issue-bound
   switch (nv) {
-    case 1: case 2: quant_go<TX, TPR, 2>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero); break;
-    case 3: quant_go<TX, TPR, 3>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero); break;
-    case 4: quant_go<TX, TPR, 4>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero); break;
-    case 5: quant_go<TX, TPR, 5>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero); break;
-    case 6: quant_go<TX, TPR, 6>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero); break;
-    case 7: quant_go<TX, TPR, 7>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero); break;
-    default: quant_go<TX, TPR, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero); break;
+    case 1: case 2: quant_go<TX, TPR, 2>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    case 3: quant_go<TX, TPR, 3>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    case 4: quant_go<TX, TPR, 4>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    case 5: quant_go<TX, TPR, 5>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    case 6: quant_go<TX, TPR, 6>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    case 7: quant_go<TX, TPR, 7>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
+    default: quant_go<TX, TPR, 8>(x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm); break;
   }
 }
 
 template <typename TX>
 static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const float* gain, float eps,
                                   int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
-                                  float* absmax, cudaStream_t s, int norm, uint32_t* zero,
-                                  int nzero) {
+                                  float* absmax, cudaStream_t s, int norm) {
   const int kp = (k + kKAlign - 1) / kKAlign * kKAlign;
   const int nvp = kp / QVec<TX>::N;   // vectors per (padded) row
   // few rows (decode batches): latency-bound, so spread each row over 256
   // threads (<= 4 vectors each) instead of maximising per-thread work
   if (m <= 256 && nvp > 64 && nvp <= 256 * 4) {
-    quant_nv<TX, 256>((nvp + 255) / 256, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero);
+    quant_nv<TX, 256>((nvp + 255) / 256, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
     return cudaGetLastError();
   }
   // smallest threads-per-row with <= NVMAX vectors per thread (8; debug knob TERN_QUANT_NVMAX)
   static const int nvmax_env = getenv("TERN_QUANT_NVMAX") ? atoi(getenv("TERN_QUANT_NVMAX")) : 8;
   const int nvmax = (nvmax_env >= 2 && nvmax_env <= 8) ? nvmax_env : 8;
   if (nvp <= 32 * nvmax)
-    quant_nv<TX, 32>((nvp + 31) / 32, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero);
+    quant_nv<TX, 32>((nvp + 31) / 32, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
   else if (nvp <= 64 * nvmax)
-    quant_nv<TX, 64>((nvp + 63) / 64, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero);
+    quant_nv<TX, 64>((nvp + 63) / 64, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
   else if (nvp <= 128 * nvmax)
-    quant_nv<TX, 128>((nvp + 127) / 128, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero);
+    quant_nv<TX, 128>((nvp + 127) / 128, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
   else if (nvp <= 256 * 8)
-    quant_nv<TX, 256>((nvp + 255) / 256, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm, zero, nzero);
+    quant_nv<TX, 256>((nvp + 255) / 256, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();
@@ -411,12 +406,18 @@ static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const floa
 cudaError_t launch_quant(const void* x, int xdt, int m, int k, int ldx, const float* gain,
                          float eps, int8_t* q, int ldq, float* deq, int32_t* qsum, float* inv_rms,
                          float* absmax, cudaStream_t s, int norm, uint32_t* zero, int nzero) {
+  // (QFuse, opt-in: the block's fused-quantization counters zeroed ahead of its GEMMs -- a
+  // memset node, not a side job of the kernel, which would cost it registers)
+  if (zero != nullptr && nzero > 0) {
+    const cudaError_t ze = cudaMemsetAsync(zero, 0, sizeof(uint32_t) * (size_t)nzero, s);
+    if (ze != cudaSuccess) return ze;
+  }
   if (m == 0) return cudaSuccess;
   if (xdt == TERN_BF16)
     return quant_dispatch(static_cast<const __nv_bfloat16*>(x), m, k, ldx, gain, eps, q, ldq, deq,
-                          qsum, inv_rms, absmax, s, norm, zero, nzero);
+                          qsum, inv_rms, absmax, s, norm);
   return quant_dispatch(static_cast<const float*>(x), m, k, ldx, gain, eps, q, ldq, deq, qsum,
-                        inv_rms, absmax, s, norm, zero, nzero);
+                        inv_rms, absmax, s, norm);
 }
 
 }  // namespace tern
