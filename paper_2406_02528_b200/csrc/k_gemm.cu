@@ -1700,7 +1700,8 @@ cudaError_t launch_gemm(const int8_t* q, int M, int ldq, const float* deq, const
     if (ks < 1) ks = 1;
     // the slices' int32 partials cost L2 traffic (ks * M * n * 4 bytes): few, long K
     // slices -- except for very small M, where that traffic is negligible
-    const int ks_cap = M <= 64 ? 16 : 4;
+    static const int ks_env = getenv("TERN_KS_CAP") ? atoi(getenv("TERN_KS_CAP")) : 0;   // debug
+    const int ks_cap = ks_env > 0 ? ks_env : (M <= 64 ? 16 : 4);
     if (ks > ks_cap) ks = ks_cap;
     if (ks > a.num_kb) ks = a.num_kb;
     if ((size_t)ks * slice > part_bytes) ks = (int)(part_bytes / slice);
