@@ -644,3 +644,21 @@ def test_qfuse_with_gains_and_biases(L, M, dtype):
     yo, ho = O.block(ob, f32np(x), np.zeros((B, d), np.float32), bf16=dtype == "bf16")
     close(f32np(y), yo, 2e-2 if dtype == "bf16" else 1e-4, "qfuse gains")
     assert np.array_equal(f32np(y), yo)
+
+
+@pytest.mark.parametrize("l", [1408, 2176])
+def test_inplace_channel_residual(L, M, l):
+    """fp32 block prefill with more than 256 tokens writes x1 into y and adds the down
+    projection onto it in place (EPI_RESID_RED, TMA reduce-add): the 1-CTA GEMM (l = 1408 <
+    2048) and the CTA-pair GEMM (l = 2176), ragged M = 3 x 230, against the oracle block."""
+    d, B, T = 512, 3, 230
+    cfg = synth.Config("red", 1, d, l, "f32", 29, B, T, B, 0)
+    st = M.Stack.random(cfg, gen_device="cpu", keep_latents=1)
+    x = synth.hidden((B, T, d), synth.generator(d + l + 7), "f32")
+    h = st.new_state(B)
+    y = st.prefill(x.cuda(), h)
+    torch.cuda.synchronize()
+    ob = O.OracleBlock({kk: v.numpy() for kk, v in st.latents[0].items()}, d, l)
+    yo, ho = O.block(ob, f32np(x), np.zeros((B, d), np.float32))
+    assert np.array_equal(f32np(y), yo)
+    assert np.array_equal(h[0].cpu().numpy(), ho)
