@@ -1316,7 +1316,17 @@ static cudaError_t gemm_launch(const CUtensorMap& ta, const CUtensorMap& tb, con
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int total = a.n_tiles * a.m_tiles * a.ksplit;
-  const int grid = total < num_sms ? total : num_sms;
+  int grid = total < num_sms ? total : num_sms;
+  // balanced persistent grid: with few tile waves, the fewest CTAs that keep the same number of
+  // waves (c2 o-projection: 512 tiles -> 128 CTAs x 4 instead of 148 CTAs x 3..4; the makespan
+  // in tiles is the same and the HBM-bound drains contend less: 38.8 -> 37.8 us).  With many
+  // waves it measured slower (c2 gate|up, 20 waves: 97.2 -> 99.7 us), so only up to 8 waves.
+  // TERN_GEMM_BAL=0 turns it off, 2 applies it to every grid (debug).
+  static const int bal = getenv("TERN_GEMM_BAL") ? atoi(getenv("TERN_GEMM_BAL")) : 1;
+  if (bal && total > num_sms && a.ksplit == 1 && a.part == nullptr) {   // not the split-K slices
+    const int waves = (total + num_sms - 1) / num_sms;
+    if (waves <= 8 || bal == 2) grid = (total + waves - 1) / waves;
+  }
   static unsigned long long* dprof = nullptr;
   static const bool prof_on = getenv("TERN_GEMM_PROF") != nullptr;
   GemmArgs aa = a;
@@ -1366,6 +1376,12 @@ static cudaError_t gemm2_launch(const CUtensorMap& ta, const CUtensorMap& tb, co
   const int total = a.n_tiles * a.m_tiles;
   int grid = 2 * total < num_sms ? 2 * total : num_sms;
   grid &= ~1;
+  // balanced grid as in gemm_launch (c2 down: 256 pair tiles -> 64 pairs x 4; 54.0 -> 51.7 us)
+  static const int bal = getenv("TERN_GEMM_BAL") ? atoi(getenv("TERN_GEMM_BAL")) : 1;
+  if (bal && 2 * total > grid) {   // the fewest CTA pairs with the same number of tile waves
+    const int pairs = grid / 2, waves = (total + pairs - 1) / pairs;
+    if (waves <= 8 || bal == 2) grid = 2 * ((total + waves - 1) / waves);
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGemmThreads);
