@@ -390,7 +390,11 @@ static cudaError_t quant_dispatch(const TX* x, int m, int k, int ldx, const floa
   // smallest threads-per-row with <= NVMAX vectors per thread (8; debug knob TERN_QUANT_NVMAX)
   static const int nvmax_env = getenv("TERN_QUANT_NVMAX") ? atoi(getenv("TERN_QUANT_NVMAX")) : 8;
   const int nvmax = (nvmax_env >= 2 && nvmax_env <= 8) ? nvmax_env : 8;
-  if (nvp <= 32 * nvmax)
+  // bf16 rows of 2048 (c3's d): two warps per row, 4 vectors each, measured faster than one warp
+  // with 8 (57.3 -> 54.0 us per launch at 32768 rows); fp32 rows and K = 5632 measured slower so
+  if (sizeof(TX) == 2 && nvp == 256 && nvmax == 8)
+    quant_nv<TX, 64>(4, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
+  else if (nvp <= 32 * nvmax)
     quant_nv<TX, 32>((nvp + 31) / 32, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);
   else if (nvp <= 64 * nvmax)
     quant_nv<TX, 64>((nvp + 63) / 64, x, m, k, ldx, gain, eps, q, ldq, deq, qsum, inv_rms, absmax, s, norm);

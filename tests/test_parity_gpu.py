@@ -103,7 +103,7 @@ def test_pack_degenerate(L, M):
 
 # ------------------------------------------------------------------------ a2 quant
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-@pytest.mark.parametrize("m,k", [(1, 256), (7, 688), (33, 1024), (5, 2816), (3, 6912), (300, 256)])
+@pytest.mark.parametrize("m,k", [(1, 256), (7, 688), (33, 1024), (5, 2816), (3, 6912), (300, 256), (300, 2048), (260, 2560)])
 def test_quant_parity(L, m, k, dtype):
     x = acts((m, k), 7 + k, dtype)
     x[0, :] = 0                       # all-zero row (C7)
