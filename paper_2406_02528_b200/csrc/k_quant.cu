@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
                                                      int32_t* __restrict__ qsum,
                                                      float* __restrict__ inv_rms,
                                                      float* __restrict__ absmax,
-                                                     unsigned long long* trace) {
+                                                     unsigned long long* trace, int rev) {
   trace_mark(trace, 0);
   constexpr int VE = QVec<TX>::N;
   constexpr int WPR = TPR / 32;                 // warps per row
@@ -207,8 +207,12 @@ __global__ void __launch_bounds__(kQThreads) k_quant(const TX* __restrict__ x, i
   __shared__ int red_i[RPC][WPR];
   const int lane = threadIdx.x & 31;
   const int rloc = threadIdx.x / TPR, t = threadIdx.x % TPR, wr = t >> 5;
-  const int row = blockIdx.x * RPC + rloc;
-  const bool rv = row < M;
+  // rev: the CTAs walk the rows from the last to the first.  The producing kernel wrote the rows
+  // in ascending order and x is larger than what L2 keeps, so the LAST rows are the ones still
+  // resident; reading in the producer's order would evict them just before they are needed.
+  const int row_f = blockIdx.x * RPC + rloc;
+  const bool rv = row_f < M;
+  const int row = rev ? M - 1 - row_f : row_f;
   const int nvec = K / VE, nvecp = ((K + kKAlign - 1) / kKAlign * kKAlign) / VE;
   const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)(rv ? row : 0) * ldx);
   pdl_wait();                 // x is the previous kernel's output
@@ -350,12 +354,14 @@ static void quant_go(const TX* x, int m, int k, int ldx, const float* gain, floa
   const int grid = (m + RPC - 1) / RPC;
   const double inv_k = 1.0 / (double)k;
   const bool full = k == TPR * NV * QVec<TX>::N;   // then also k == Kp
+  static const int rev_env = getenv("TERN_QUANT_REV") ? atoi(getenv("TERN_QUANT_REV")) : 1;   // debug
+  const int rev = rev_env && m > 256;   // prefill-sized inputs only
   auto kern = norm == TERN_NORM_CENTERED
                   ? k_quant<TX, TPR, NV, false, false, true>
                   : (gain ? k_quant<TX, TPR, NV, true, false>
                           : (full ? k_quant<TX, TPR, NV, false, true> : k_quant<TX, TPR, NV, false, false>));
   launch_pdl(kern, dim3(grid), dim3(kQThreads), 0, s, x, m, k, ldx, gain, eps, inv_k, q, ldq, deq,
-             qsum, inv_rms, absmax, trace_slot(TERN_K_QUANT, grid));
+             qsum, inv_rms, absmax, trace_slot(TERN_K_QUANT, grid), rev);
 }
 
 template <typename TX, int TPR>
